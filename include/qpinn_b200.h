@@ -1,0 +1,164 @@
+/*
+ * qpinn_b200.h -- C ABI of the B200-native QPINN hot path.
+ *
+ * Plain pointers, sizes and enums only: no torch types.  Every device
+ * pointer is a CUDA global-memory address on the current device; every
+ * `stream` argument is a cudaStream_t passed as void* (NULL = legacy default
+ * stream).  Launch functions are asynchronous: they validate arguments on the
+ * host, enqueue kernels on `stream` and return; device-side conditions
+ * (domain excursions, non-finite gradients) are reported through the
+ * status functions below.
+ *
+ * Reference interfaces replaced (paths relative to /root/reference/pkg/src/qpinn):
+ *   qpinn_circuit_*        <- ansatz.build_circuit / CircuitSpec (ansatz.py:70-207)
+ *   qpinn_pqc_forward      <- ansatz.quantum_layer_forward       (ansatz.py:341-400)
+ *   qpinn_pqc_backward     <- the taped backward of the same call
+ *                             (tape.py:118-148 through ansatz.py:378-400, qsim.py:122-209)
+ *   qpinn_loss_*           <- physics.LossEvaluator.evaluate      (physics.py:334-460)
+ *   qpinn_adam_step        <- training.adam_step                  (training.py:101-111)
+ *   qpinn_time_bin_weights <- physics.time_bin_weights            (physics.py:172-180)
+ */
+#ifndef QPINN_B200_H
+#define QPINN_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Status codes; the Python host maps them onto the reference exception
+ * classes of errors.py:4-37. */
+#define QPINN_OK 0
+#define QPINN_ERR_CONFIG 1        /* ConfigError        */
+#define QPINN_ERR_DOMAIN 2        /* DomainError        */
+#define QPINN_ERR_CAPACITY 3      /* CapacityError      */
+#define QPINN_ERR_INVALID_GATE 4  /* InvalidGateError   */
+#define QPINN_ERR_INVALID_BATCH 5 /* InvalidBatchError  */
+#define QPINN_ERR_NONFINITE 6     /* RunAborted         */
+#define QPINN_ERR_CUDA 7          /* CUDA runtime failure */
+
+#define QPINN_F32 0
+#define QPINN_F64 1
+
+/* AnsatzKind (ansatz.py:27-33), in declaration order */
+#define QPINN_ANSATZ_BASIC 0
+#define QPINN_ANSATZ_STRONGLY 1
+#define QPINN_ANSATZ_CROSS_MESH 2
+#define QPINN_ANSATZ_CROSS_MESH_2ROT 3
+#define QPINN_ANSATZ_CROSS_MESH_CNOT 4
+#define QPINN_ANSATZ_NO_ENTANGLEMENT 5
+
+/* ScaleKind (ansatz.py:36-41) */
+#define QPINN_SCALE_NONE 0
+#define QPINN_SCALE_PI 1
+#define QPINN_SCALE_BIAS 2
+#define QPINN_SCALE_ASIN 3
+#define QPINN_SCALE_ACOS 4
+
+/* Last error message of the calling thread (static storage). */
+const char* qpinn_last_error(void);
+/* Library version string. */
+const char* qpinn_version(void);
+
+/* ---- circuit (ansatz.py:159-207, fused plan ansatz.py:117-156) ---------- */
+typedef struct qpinn_circuit qpinn_circuit;
+
+/* Builds the gate list and fused plan and uploads the plan to the current
+ * device.  QPINN_ERR_CONFIG for n_qubits/n_layers < 1 or an entangling
+ * ansatz with n_qubits < 2 (ansatz.py:163-166). */
+int qpinn_circuit_create(int kind, int n_qubits, int n_layers, qpinn_circuit** out);
+void qpinn_circuit_destroy(qpinn_circuit* c);
+int qpinn_circuit_param_count(const qpinn_circuit* c);
+int qpinn_circuit_n_qubits(const qpinn_circuit* c);
+/* CircuitSpec.dump() text (ansatz.py:98-109); returns the required size
+ * including the NUL, writes at most `len` bytes. */
+size_t qpinn_circuit_dump(const qpinn_circuit* c, char* buf, size_t len);
+/* One line per fused step: "u1 <kind> <wire> <slots>" | "perm <p0,p1,...>" |
+ * "phases <c:t:slot ...>". */
+size_t qpinn_circuit_plan_dump(const qpinn_circuit* c, char* buf, size_t len);
+/* Largest n_qubits the register-resident kernels accept for `dtype`. */
+int qpinn_pqc_max_qubits(int dtype);
+
+/* ---- PQC forward + tangents (K1) and adjoint backward (K2) -------------- */
+/* Device scratch needed by forward/backward for `rows` points. */
+size_t qpinn_pqc_workspace_bytes(const qpinn_circuit* c, int dtype, int64_t rows);
+
+/* z[R,n] = <Z_q>, dz[3,R,n] = d<Z_q>/d(x,y,t) of the scaled-angle-embedded
+ * circuit; act_val [R,n], act_tan [3,R,n] row-major (act_tan/dz may be NULL
+ * for value-only evaluation), qparams [P].  Records max|act_val| in the
+ * workspace for qpinn_pqc_domain_check. */
+int qpinn_pqc_forward(const qpinn_circuit* c, int dtype, int scale, int64_t rows,
+                      const void* act_val, const void* act_tan, const void* qparams,
+                      void* z, void* dz, void* workspace, size_t workspace_bytes,
+                      void* stream);
+
+/* Gradients of L(z, dz) given g_z = dL/dz [R,n] and g_dz = dL/d(dz) [3,R,n]:
+ * g_act_val [R,n], g_act_tan [3,R,n] and g_qparams [P] (summed over all rows
+ * in a fixed, run-to-run deterministic order). */
+int qpinn_pqc_backward(const qpinn_circuit* c, int dtype, int scale, int64_t rows,
+                       const void* act_val, const void* act_tan, const void* qparams,
+                       const void* g_z, const void* g_dz, void* g_act_val,
+                       void* g_act_tan, void* g_qparams, void* workspace,
+                       size_t workspace_bytes, void* stream);
+
+/* Synchronises `stream`, reads max|act_val| of the last forward on this
+ * workspace: QPINN_ERR_DOMAIN if it exceeds 1 by more than 1e-12
+ * (ansatz.py:51-58); *clamped = 1 when 0 < excess <= 1e-12 (the kernels
+ * clamp those values, as the reference does with a warning). */
+int qpinn_pqc_domain_check(const void* workspace, void* stream, double* max_abs,
+                           int* clamped);
+
+/* ---- fused Maxwell loss (K4), physics.py:123-187, :334-460 -------------- */
+typedef struct qpinn_loss_spec {
+  int32_t nx, ny, nt;          /* CollocationGrid (physics.py:74-117)           */
+  double t_end;
+  int32_t case_id;             /* 0 vacuum, 1 dielectric, 2 asymmetric           */
+  int32_t balanced;            /* phys_mode == diel_balanced                     */
+  int32_t energy;              /* energy_enabled                                 */
+  double eps_r, slab_x0;       /* MaterialMap (physics.py:30-49)                 */
+  int32_t n_local_slices;      /* time slices this call covers                   */
+  const int32_t* slices;       /* device [n_local_slices] global slice indices   */
+  int32_t width;               /* head input width (n_qubits for hybrids)        */
+} qpinn_loss_spec;
+
+/* Number of doubles in the loss-sum vector: 5 bins x 4 keys
+ * (res1|res1_vac, res1_diel, res2, res3) + energy + sym + ic. */
+#define QPINN_LOSS_NSUMS 23
+size_t qpinn_loss_workspace_bytes(const qpinn_loss_spec* s, int dtype, int64_t rows);
+
+/* Head (out = h Wo + bo, network.py:302) + residuals + every loss term for
+ * the points of `slices` (row r = local slice r / (nx*ny), slice-major),
+ * with the adaptive weights `weights_dev` [5] (double, device; NULL = the
+ * pooled formula).  Writes dL/dh [R,W], dL/d(dh) [3,R,W], dL/dWo [W,3],
+ * dL/dbo [3] (dtype) and the raw per-term sums `sums_dev`
+ * [QPINN_LOSS_NSUMS] (double; deterministic fixed-order reduction). */
+int qpinn_loss_forward_backward(const qpinn_loss_spec* s, int dtype, int64_t rows,
+                                const void* h, const void* dh, const void* w_out,
+                                const void* b_out, const double* weights_dev,
+                                void* g_h, void* g_dh, void* g_w_out, void* g_b_out,
+                                double* sums_dev, void* workspace,
+                                size_t workspace_bytes, void* stream);
+
+/* From (globally reduced) sums: breakdown_dev[10] = phys, ic, sym, energy,
+ * total, bin_phys[5] (physics.py:416-426); when `weights_next_dev` is not
+ * NULL also time_bin_weights(bin_phys, kappa) into it (physics.py:172-180).
+ * `weights_dev` are the weights the sums were computed with (NULL = pooled). */
+int qpinn_loss_finalize(const qpinn_loss_spec* s, const double* sums_dev,
+                        const double* weights_dev, double kappa,
+                        double* breakdown_dev, double* weights_next_dev, void* stream);
+
+/* ---- Adam (training.py:87-111) ------------------------------------------ */
+/* If any grad entry is non-finite nothing is updated and *flag_dev is set to
+ * 1 (the reference raises RunAborted before touching its state); otherwise
+ * m, v, params are updated in place with bias correction for step t (1-based,
+ * i.e. the value of AdamState.t after its increment). */
+int qpinn_adam_step(int dtype, int64_t n, void* params, const void* grad, void* m,
+                    void* v, int64_t t, double lr, double beta1, double beta2,
+                    double eps, int32_t* flag_dev, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* QPINN_B200_H */
