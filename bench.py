@@ -1,0 +1,392 @@
+#!/usr/bin/env python
+"""QPINN train-step collocation points/sec on B200 (BASELINE.json metric).
+
+One "step" = one full training epoch of the reference trainer
+(training.py:359-407 without probes): forward with d/dx,y,t tangents
+(trunk + K1), the fused Maxwell loss (K4), the full gradient (trunk backward
++ K2 adjoint), [NCCL all-reduce], loss finalisation and Adam.
+
+Workloads: N=1 -> config 2 (vacuum, strongly/acos 7q x 4L, hidden
+128, RFF 128, energy + adaptive weighting, 64x64x16 = 2^16 points); N>1 ->
+config 3 (128x128x64 = 2^20 points sharded by whole time slices, strong
+scaling).  Synthetic = the reference's own seeded init and grid.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "QPINN train-step collocation points/sec"
+UNIT = "points/s"
+WORKLOADS = {
+    "config2": dict(grid=(64, 64, 16), name="config2: vacuum 7q x 4L strongly/acos, hidden 128, "
+                    "RFF 128, energy + adaptive time weighting, 64x64x16 = 2^16 points"),
+    "config3": dict(grid=(128, 128, 64), name="config3: vacuum 7q x 4L strongly/acos, hidden 128, "
+                    "RFF 128, energy + adaptive time weighting, 128x128x64 = 2^20 points, "
+                    "sharded by time slices"),
+}
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=20)
+    p.add_argument("--warmup", type=int, default=5)
+    p.add_argument("--impl", default="ours", choices=("ours", "reference"))
+    p.add_argument("--dtype", default="f32", choices=("f32", "f64"))
+    p.add_argument("--workload", default="auto", choices=("auto", "config2", "config3"))
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--cpu-seconds", type=float, default=15.0)
+    return p.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local = int(os.environ.get("LOCAL_RANK", 0))
+    return rank, world, local
+
+
+def train_config(grid):
+    from paper_2506_23246_b200.network import ModelConfig
+    from paper_2506_23246_b200.training import TrainConfig
+    return TrainConfig(case="vacuum", model=ModelConfig(variant="hybrid", ansatz="strongly",
+                       scale="acos", seed=0), epochs=1, grid=grid, energy_loss_enabled=True,
+                       adaptive_weighting=True, eval_cadence=0, probe_cadence=0)
+
+
+# -- clocks during the timed region ---------------------------------------------------
+
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_id: str):
+        self.gpu_id = gpu_id
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", self.gpu_id, f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+        return False
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def gpu_id_for(dev):
+    import torch
+    try:
+        p = torch.cuda.get_device_properties(dev)
+        return f"{p.pci_domain_id:08x}:{p.pci_bus_id:02x}:{p.pci_device_id:02x}.0"
+    except Exception:
+        return str(dev)
+
+
+# -- measured FP32 peak ----------------------------------------------------------------
+
+def fp32_peak():
+    import ctypes as C
+    from paper_2506_23246_b200 import build as B
+    path = B.TOOLS_LIB
+    if not os.path.exists(path):
+        return None, "unavailable"
+    lib = C.CDLL(path)
+    a, b, n = C.c_double(), C.c_double(), C.c_int()
+    if lib.qpinn_tool_fp32_peak(C.byref(a), C.byref(b), C.byref(n)) != 0:
+        return None, "unavailable"
+    return max(a.value, b.value), (f"measured in-run: FFMA microbenchmark on {n.value} SMs "
+                                   f"(imm {a.value:.1f}, reg {b.value:.1f} TFLOP/s)")
+
+
+# -- CPU reference (baseline/_ref qpinn, else the oracle port) --------------------------
+
+def _import_reference():
+    ref = os.path.join(ROOT, "baseline", "_ref")
+    if os.path.isdir(os.path.join(ref, "qpinn")):
+        sys.path.insert(0, ref)
+        import qpinn  # noqa: F401
+        return "reference"
+    return "port"
+
+
+def cpu_reference_rate(grid, seconds, steps=None, warmup=1, sample_slices=1):
+    """Time evaluate(tape=True) + adam_step of the reference on a bounded sample
+    (the first ``sample_slices`` whole time slices of the workload grid; the
+    per-point work equals the full step's)."""
+    import numpy as np
+    kind = _import_reference()
+    cores = os.cpu_count() or 1
+    try:
+        from threadpoolctl import threadpool_limits
+        limiter = threadpool_limits(cores)
+    except Exception:  # pragma: no cover
+        limiter = None
+    rates = []
+    if kind == "reference":
+        from qpinn.network import ModelConfig, build_model
+        from qpinn.physics import (CollocationGrid, LossEvaluator, MaterialMap,
+                                   time_bin_weights)
+        from qpinn.training import AdamState, adam_step, init_quantum_params
+        model = build_model(ModelConfig(variant="hybrid", ansatz="strongly", scale="acos",
+                                        seed=0, t_domain=1.5))
+        params = model.init_params()
+        params.quantum[:] = init_quantum_params("reg", model.n_quantum, 0)
+        g = CollocationGrid(*grid, 1.5)
+        ev = LossEvaluator(model, g, MaterialMap("vacuum"), case="vacuum", energy_enabled=True,
+                           chunk_slices=sample_slices)
+        ev.chunks = ev.chunks[:1]
+        npts = (ev.chunks[0].s1 - ev.chunks[0].s0) * g.slice_size
+        w = np.array([1.0, 0.9, 0.8, 0.7, 0.6])
+        adam = AdamState.zeros(model.total_parameter_count)
+
+        def one():
+            r = ev.evaluate(params, weights=w, tape=True)
+            adam_step(params, r.grad, adam, 1e-3)
+    else:
+        import oracle as O
+        om = O.OracleModel(seed=0)
+        flat = om.init_params()
+        flat[om.n_classical:] = O.init_quantum_params("reg", om.n_quantum, 0)
+        ev = O.Evaluator(om, O.Grid(*grid, 1.5), chunk_slices=sample_slices,
+                         slices=list(range(sample_slices)))
+        npts = sample_slices * grid[0] * grid[1]
+        w = np.array([1.0, 0.9, 0.8, 0.7, 0.6])
+        m = np.zeros(om.n_total)
+        v = np.zeros(om.n_total)
+        st = {"t": 0}
+
+        def one():
+            _, grad, _ = ev.evaluate(flat, w, tape=True)
+            st["t"] = O.adam_update(flat, grad, m, v, st["t"], 1e-3)
+    for _ in range(warmup):
+        one()
+    t_start = time.perf_counter()
+    while True:
+        t0 = time.perf_counter()
+        one()
+        rates.append(npts / (time.perf_counter() - t0))
+        done = len(rates) >= steps if steps else (time.perf_counter() - t_start >= seconds and len(rates) >= 2)
+        if done:
+            break
+    if limiter is not None:
+        limiter.unregister() if hasattr(limiter, "unregister") else None
+    sample = (f"{sample_slices} whole time slice(s) = {npts} points of the {grid[0]}x{grid[1]}x"
+              f"{grid[2]} grid per step, evaluate(tape=True)+adam_step, {len(rates)} timed steps")
+    return statistics.mean(rates), kind, cores, sample, rates
+
+
+# -- our arm --------------------------------------------------------------------------------
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+    from paper_2506_23246_b200 import _native as N
+    from paper_2506_23246_b200.roofline import pqc_flops
+    from paper_2506_23246_b200.training import Trainer, allreduce_fn
+
+    rank, world, local = dist_env()
+    if world != args.gpus:
+        args.gpus = world if world > 1 else args.gpus
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    wl = args.workload if args.workload != "auto" else ("config2" if world == 1 else "config3")
+    grid = WORKLOADS[wl]["grid"]
+    dtype = torch.float32 if args.dtype == "f32" else torch.float64
+    cfg = train_config(grid)
+    tr = Trainer(cfg, device=dev, dtype=dtype, rank=rank, world_size=world,
+                 reduce_fn=allreduce_fn() if world > 1 else None)
+    n_total = tr.grid.n_points
+
+    def barrier():
+        if world > 1:
+            dist.barrier(device_ids=[local])
+
+    def timed_steps(k):
+        barrier()
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(k):
+            tr.step()
+        e1.record()
+        torch.cuda.synchronize()
+        barrier()
+        ms = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+        return float(ms.item())
+
+    for _ in range(max(args.warmup, 3)):
+        tr.step()
+    launches0 = N.LAUNCHES["count"]
+    with ClockSampler(gpu_id_for(local)) as clk:
+        ms = timed_steps(args.steps)
+    launches = (N.LAUNCHES["count"] - launches0)
+    value = n_total * args.steps / (ms / 1e3)
+
+    # per-kernel CUDA-event timing over a second timed pass (own stream = current)
+    N.timing(True)
+    ms_prof = timed_steps(args.steps)
+    kern = N.timer_report()
+    N.timing(False)
+
+    # end to end: inputs copied from pinned host memory every step (+ loss D2H)
+    tr.set_host_inputs(True)
+    for _ in range(2):
+        tr.step()
+    ms_e2e = timed_steps(args.steps)
+    e2e_value = n_total * args.steps / (ms_e2e / 1e3)
+    h2d = tr.host_input_bytes()
+    d2h = tr.readback_bytes()
+
+    line = None
+    if rank == 0:
+        peak, peak_src = fp32_peak()
+        circuit = tr.model.circuit
+        R_local = tr.evaluator.n_local_points
+        f_fwd, f_adj = pqc_flops(circuit)
+        rl = {}
+        for name, per_pt in (("pqc_forward", f_fwd), ("pqc_backward", f_adj)):
+            if name in kern:
+                nl, mean_ms = kern[name]
+                launches_per_step = nl / args.steps
+                pts_per_launch = R_local / launches_per_step
+                achieved = per_pt * pts_per_launch / (mean_ms * 1e-3) / 1e12
+                rl[name] = {"bound": "fp32", "achieved": round(achieved, 3),
+                            "peak": round(peak, 3) if peak else None, "unit": "TFLOP/s",
+                            "frac": round(achieved / peak, 4) if peak else None,
+                            "traffic": traffic_for(name, pts_per_launch),
+                            "flop_per_point": per_pt, "points_per_launch": pts_per_launch,
+                            "ms_per_launch": round(mean_ms, 4),
+                            "share_of_step": round(mean_ms * launches_per_step / (ms_prof / args.steps), 4),
+                            "peak_source": peak_src}
+        dom = max(rl, key=lambda k: rl[k]["share_of_step"]) if rl else None
+        cpu = None
+        if world == 1 and not args.no_cpu_baseline:
+            v, kind, cores, sample, _ = cpu_reference_rate(grid, args.cpu_seconds)
+            cpu = {"value": round(v, 2), "unit": UNIT, "cores": cores, "kind": kind,
+                   "sample": sample}
+        line = {
+            "metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": max(args.warmup, 3),
+            "ms_per_step": round(ms / args.steps, 4), "higher_is_better": True,
+            "scaling": "strong" if world > 1 else "weak", "vs_baseline": None,
+            "dtype": "f32" if dtype == torch.float32 else "f64",
+            "data": "synthetic (reference seeded init: Model.init_params + init_quantum_params('reg', 84, 0); reference collocation grid)",
+            "config": {"workload": WORKLOADS[wl]["name"], "points_per_step": n_total,
+                       "points_per_gpu": R_local, "grid": list(grid),
+                       "parallelism": f"dp{world} (whole time slices per rank)",
+                       "l2": "inputs larger than L2 (per-step activations > 126 MB)"},
+            "e2e": {"value": round(e2e_value, 1), "unit": UNIT, "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": d2h},
+            "gpu_launches": int(launches),
+            "roofline": rl.get(dom) if dom else None,
+            "roofline_kernels": rl,
+            "cpu_baseline": cpu,
+            "clocks": clk.summary(),
+        }
+    if world > 1:
+        dist.barrier(device_ids=[local])
+        dist.destroy_process_group()
+    if line is not None:
+        print(json.dumps(line), flush=True)
+
+
+def traffic_for(name, pts):
+    """DRAM bytes per launch from the committed ncu capture (profiles/), else None."""
+    path = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        per_pt = d[name]["bytes_per_point"]
+        return round(per_pt * pts)
+    except Exception:
+        return None
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    wl = args.workload if args.workload != "auto" else ("config2" if world == 1 else "config3")
+    grid = WORKLOADS[wl]["grid"]
+    v, kind, cores, sample, rates = cpu_reference_rate(grid, 0, steps=args.steps,
+                                                       warmup=args.warmup)
+    ms = 1e3 * statistics.mean([grid[0] * grid[1] / r for r in rates])
+    line = {
+        "metric": METRIC, "value": round(v, 2), "unit": UNIT, "n_gpus": 0, "impl": "reference",
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (reference seeded init and grid)",
+        "config": {"workload": WORKLOADS[wl]["name"], "parallelism": "host CPU, numpy/OpenBLAS"},
+        "cpu_baseline": {"value": round(v, 2), "unit": UNIT, "cores": cores, "kind": kind,
+                         "sample": sample},
+        "e2e": {"value": round(v, 2), "unit": UNIT, "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

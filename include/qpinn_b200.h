@@ -15,8 +15,8 @@
  *   qpinn_pqc_backward     <- the taped backward of the same call
  *                             (tape.py:118-148 through ansatz.py:378-400, qsim.py:122-209)
  *   qpinn_loss_*           <- physics.LossEvaluator.evaluate      (physics.py:334-460)
+ *                             and physics.time_bin_weights     (physics.py:172-180)
  *   qpinn_adam_step        <- training.adam_step                  (training.py:101-111)
- *   qpinn_time_bin_weights <- physics.time_bin_weights            (physics.py:172-180)
  */
 #ifndef QPINN_B200_H
 #define QPINN_B200_H
@@ -87,8 +87,8 @@ size_t qpinn_pqc_workspace_bytes(const qpinn_circuit* c, int dtype, int64_t rows
 
 /* z[R,n] = <Z_q>, dz[3,R,n] = d<Z_q>/d(x,y,t) of the scaled-angle-embedded
  * circuit; act_val [R,n], act_tan [3,R,n] row-major (act_tan/dz may be NULL
- * for value-only evaluation), qparams [P].  Records max|act_val| in the
- * workspace for qpinn_pqc_domain_check. */
+ * for value-only evaluation), qparams [P].  Folds max|act_val| into the
+ * workspace's running maximum for qpinn_pqc_domain_check. */
 int qpinn_pqc_forward(const qpinn_circuit* c, int dtype, int scale, int64_t rows,
                       const void* act_val, const void* act_tan, const void* qparams,
                       void* z, void* dz, void* workspace, size_t workspace_bytes,
@@ -103,60 +103,77 @@ int qpinn_pqc_backward(const qpinn_circuit* c, int dtype, int scale, int64_t row
                        void* g_act_tan, void* g_qparams, void* workspace,
                        size_t workspace_bytes, void* stream);
 
-/* Synchronises `stream`, reads max|act_val| of the last forward on this
- * workspace: QPINN_ERR_DOMAIN if it exceeds 1 by more than 1e-12
+/* Synchronises `stream`, reads (and resets to 0) the running max|act_val| of
+ * the forwards launched on this workspace since the last check (a fresh
+ * workspace must be zero-filled): QPINN_ERR_DOMAIN if it exceeds 1 by more than 1e-12
  * (ansatz.py:51-58); *clamped = 1 when 0 < excess <= 1e-12 (the kernels
  * clamp those values, as the reference does with a warning). */
 int qpinn_pqc_domain_check(const void* workspace, void* stream, double* max_abs,
                            int* clamped);
 
 /* ---- fused Maxwell loss (K4), physics.py:123-187, :334-460 -------------- */
+/* Static per-grid description.  The host derives every table with the same
+ * numpy expressions as the reference (grid coordinates, permittivity, pulse,
+ * time bins, region counts) so the device never re-derives a floating-point
+ * bin edge. */
 typedef struct qpinn_loss_spec {
-  int32_t nx, ny, nt;          /* CollocationGrid (physics.py:74-117)           */
-  double t_end;
-  int32_t case_id;             /* 0 vacuum, 1 dielectric, 2 asymmetric           */
-  int32_t balanced;            /* phys_mode == diel_balanced                     */
-  int32_t energy;              /* energy_enabled                                 */
-  double eps_r, slab_x0;       /* MaterialMap (physics.py:30-49)                 */
-  int32_t n_local_slices;      /* time slices this call covers                   */
-  const int32_t* slices;       /* device [n_local_slices] global slice indices   */
-  int32_t width;               /* head input width (n_qubits for hybrids)        */
+  int32_t nx, ny;                /* slice geometry (physics.py:89-98)               */
+  int32_t n_local_slices;        /* time slices covered by this call                */
+  const int32_t* slice_bin;      /* device [n_local_slices] time bin (physics.py:115-117) */
+  const int32_t* slice_is_ic;    /* device [n_local_slices] 1 for the t = 0 slice   */
+  const double* eps;             /* device [nx*ny] permittivity (physics.py:45-49)   */
+  const double* ic_target;       /* device [nx*ny] E_z(t=0) pulse (physics.py:64-67) */
+  int32_t balanced;              /* diel_balanced: res1 split by region (physics.py:144-151) */
+  int32_t energy;                /* energy term enabled                             */
+  int32_t n_sym;                 /* parity terms (physics.py:194-205)               */
+  int32_t sym_field[6];          /* 0 ez, 1 hx, 2 hy                                */
+  int32_t sym_axis[6];           /* 0 x-mirror, 1 y-mirror                          */
+  double sym_sign[6];            /* +1 penalises f - f_mirror, -1 f + f_mirror      */
+  /* 1/count(key, slices of bin m) (0 when the key is unused or the bin empty),
+   * keys: 0 res1 | res1_vac, 1 res1_diel, 2 res2, 3 res3 (physics.py:432-450) */
+  double inv_count_bin[5][4];
+  double inv_count_all[4];       /* 1/count(key, all nt slices) (pooled formula)   */
+  double n_total;                /* grid points N (energy/sym normaliser)          */
+  double slice_size;             /* nx*ny (IC normaliser)                          */
 } qpinn_loss_spec;
 
-/* Number of doubles in the loss-sum vector: 5 bins x 4 keys
- * (res1|res1_vac, res1_diel, res2, res3) + energy + sym + ic. */
+/* Loss-sum vector: [bin m][key k] at 4*m + k (20), energy 20, sym 21, ic 22. */
 #define QPINN_LOSS_NSUMS 23
 size_t qpinn_loss_workspace_bytes(const qpinn_loss_spec* s, int dtype, int64_t rows);
 
-/* Head (out = h Wo + bo, network.py:302) + residuals + every loss term for
- * the points of `slices` (row r = local slice r / (nx*ny), slice-major),
- * with the adaptive weights `weights_dev` [5] (double, device; NULL = the
- * pooled formula).  Writes dL/dh [R,W], dL/d(dh) [3,R,W], dL/dWo [W,3],
- * dL/dbo [3] (dtype) and the raw per-term sums `sums_dev`
- * [QPINN_LOSS_NSUMS] (double; deterministic fixed-order reduction). */
+/* Residuals (physics.py:123-128) and every loss term of the fused evaluator
+ * (physics.py:352-414) for the rows of `slices` (row r = local slice
+ * r / (nx*ny), slice-major), given the head outputs out [R,3] = (E_z, H_x,
+ * H_y) and their input jacobians dout [3,R,3] (d/dx, d/dy, d/dt).  With the
+ * adaptive weights `weights_dev` [5] (double, device; NULL = the pooled
+ * formula) it writes the loss gradient g_out [R,3], g_dout [3,R,3] (dtype) and
+ * the raw per-term sums `sums_dev` [QPINN_LOSS_NSUMS] (double; deterministic
+ * fixed-order reduction). */
 int qpinn_loss_forward_backward(const qpinn_loss_spec* s, int dtype, int64_t rows,
-                                const void* h, const void* dh, const void* w_out,
-                                const void* b_out, const double* weights_dev,
-                                void* g_h, void* g_dh, void* g_w_out, void* g_b_out,
-                                double* sums_dev, void* workspace,
-                                size_t workspace_bytes, void* stream);
+                                const void* out, const void* dout,
+                                const double* weights_dev, void* g_out, void* g_dout,
+                                double* sums_dev, void* workspace, size_t workspace_bytes,
+                                void* stream);
 
 /* From (globally reduced) sums: breakdown_dev[10] = phys, ic, sym, energy,
  * total, bin_phys[5] (physics.py:416-426); when `weights_next_dev` is not
  * NULL also time_bin_weights(bin_phys, kappa) into it (physics.py:172-180).
- * `weights_dev` are the weights the sums were computed with (NULL = pooled). */
+ * `weighted` says whether the sums were taken with adaptive weights
+ * `weights_dev` (else the pooled formula). */
 int qpinn_loss_finalize(const qpinn_loss_spec* s, const double* sums_dev,
-                        const double* weights_dev, double kappa,
+                        const double* weights_dev, int weighted, double kappa,
                         double* breakdown_dev, double* weights_next_dev, void* stream);
 
 /* ---- Adam (training.py:87-111) ------------------------------------------ */
-/* If any grad entry is non-finite nothing is updated and *flag_dev is set to
- * 1 (the reference raises RunAborted before touching its state); otherwise
- * m, v, params are updated in place with bias correction for step t (1-based,
- * i.e. the value of AdamState.t after its increment). */
+/* If the loss *loss_dev (optional, device double) is non-finite, *flag_dev
+ * gets bit 2; if any grad entry is non-finite it gets bit 1; in either case
+ * nothing is updated (the reference raises RunAborted before touching its
+ * state, training.py:104-105, :363-364).  Otherwise m, v, params are updated
+ * in place with bias correction for step t (1-based, i.e. the value of
+ * AdamState.t after its increment). */
 int qpinn_adam_step(int dtype, int64_t n, void* params, const void* grad, void* m,
                     void* v, int64_t t, double lr, double beta1, double beta2,
-                    double eps, int32_t* flag_dev, void* stream);
+                    double eps, const double* loss_dev, int32_t* flag_dev, void* stream);
 
 #ifdef __cplusplus
 }

@@ -1,0 +1,369 @@
+"""Training orchestration on the device: one fused step per epoch.
+
+Mirrors ``qpinn.training`` (training.py): ``TrainConfig`` (:30-66),
+``init_quantum_params`` (:69-79), ``lr_at`` (:82-84), ``AdamState`` /
+``adam_step`` (:87-111), ``RunLog`` (:220-265) and ``train`` (:309-414).
+
+The epoch step is device-resident: K1/K4/K2 plus the torch trunk produce the
+gradient into the flat parameter tensor, the loss breakdown and the next
+adaptive weights are finalised on the device, Adam runs in place with its
+non-finite guard, and the host reads one small pinned record per step.
+With ``world_size > 1`` every rank owns a contiguous block of whole time
+slices; the packed [gradient | 23 loss sums] vector is all-reduced once
+(NCCL over NVLink) before finalisation, which is exact.
+Probes (Meyer-Wallach, energy history, L2 vs FDTD) are diagnostics off the
+step path and are not part of this engine.
+"""
+from __future__ import annotations
+
+import time
+from dataclasses import dataclass, field, replace
+from typing import Callable, List, Optional, Sequence
+
+import numpy as np
+import torch
+
+from . import _native as N
+from .errors import ConfigError, RunAborted
+from .network import Model, ModelConfig, ParameterStore, build_model, save_checkpoint
+from .physics import (CollocationGrid, LossBreakdown, LossEvaluator, MaterialMap, default_t_end,
+                      time_bin_weights)
+
+INIT_STRATEGIES = ("reg", "zeros", "pi", "pi_half")
+
+
+@dataclass
+class TrainConfig:
+    case: str = "vacuum"
+    model: ModelConfig = field(default_factory=lambda: ModelConfig(
+        variant="hybrid", ansatz="strongly", scale="acos"))
+    energy_loss_enabled: bool = True
+    phys_loss_mode: Optional[str] = None
+    epochs: int = 1000
+    lr0: float = 1e-3
+    lr_decay: float = 0.85
+    lr_decay_every: int = 2000
+    seed: int = 0
+    init_strategy: str = "reg"
+    grid: tuple = (64, 64, 64)
+    t_end: Optional[float] = None
+    eps_r: float = 4.0
+    slab_x0: float = 0.3
+    eval_cadence: int = 250
+    probe_cadence: int = 25
+    probe_grid: tuple = (64, 64, 32)
+    mw_probe_points: int = 32
+    adaptive_weighting: bool = True
+    kappa: float = 1.0
+    chunk_slices: int = 4
+
+    def __post_init__(self):
+        if self.lr0 <= 0:
+            raise ConfigError("lr0 must be positive")
+        if self.epochs < 1:
+            raise ConfigError("epochs must be >= 1")
+        if self.init_strategy not in INIT_STRATEGIES:
+            raise ConfigError(f"unknown init strategy {self.init_strategy!r}")
+        if self.case not in ("vacuum", "dielectric", "asymmetric"):
+            raise ConfigError(f"unknown case {self.case!r}")
+
+    def resolved_t_end(self) -> float:
+        return self.t_end if self.t_end is not None else default_t_end(self.case)
+
+
+def init_quantum_params(strategy: str, count: int, seed: int = 0) -> np.ndarray:
+    """training.py:69-79 (same numpy stream, float64)."""
+    if strategy == "reg":
+        return np.random.default_rng(seed).uniform(0.0, 2.0 * np.pi, count)
+    if strategy == "zeros":
+        return np.zeros(count)
+    if strategy == "pi":
+        return np.full(count, np.pi)
+    if strategy == "pi_half":
+        return np.full(count, np.pi / 2.0)
+    raise ConfigError(f"unknown init strategy {strategy!r}")
+
+
+def lr_at(epoch: int, lr0: float = 1e-3, decay: float = 0.85, every: int = 2000) -> float:
+    return lr0 * decay ** (epoch // every)
+
+
+@dataclass
+class AdamState:
+    """Device-resident Adam moments (training.py:87-98)."""
+    m: torch.Tensor
+    v: torch.Tensor
+    t: int = 0
+    beta1: float = 0.9
+    beta2: float = 0.999
+    eps: float = 1e-8
+
+    @classmethod
+    def zeros_like(cls, flat: torch.Tensor) -> "AdamState":
+        return cls(m=torch.zeros_like(flat), v=torch.zeros_like(flat))
+
+
+def adam_step(params: ParameterStore, grad: torch.Tensor, state: AdamState, lr: float,
+              loss_dev: Optional[torch.Tensor] = None, flag: Optional[torch.Tensor] = None,
+              sync: bool = True) -> None:
+    """Bias-corrected Adam in place (training.py:101-111); RunAborted on a
+    non-finite gradient (or loss) with params and state untouched."""
+    flat = params.flat if isinstance(params, ParameterStore) else params
+    if flag is None:
+        flag = torch.zeros(1, dtype=torch.int32, device=flat.device)
+    N.check(N.lib().qpinn_adam_step(
+        N.dtype_code(flat.dtype), flat.numel(), N.ptr(flat), N.ptr(grad.contiguous()),
+        N.ptr(state.m), N.ptr(state.v), state.t + 1, lr, state.beta1, state.beta2, state.eps,
+        N.ptr(loss_dev), N.ptr(flag), N.stream_ptr()), "qpinn_adam_step")
+    N.count_launches(2)
+    if sync:
+        f = int(flag.item())
+        if f:
+            raise RunAborted("non-finite gradient" if f & 1 else "non-finite loss")
+        state.t += 1
+
+
+# -- data parallelism over whole time slices ------------------------------------
+
+def shard_slices(nt: int, rank: int, world: int) -> List[int]:
+    """Contiguous, balanced block of whole time slices for ``rank``."""
+    if world < 1 or not 0 <= rank < world:
+        raise ConfigError("bad rank/world")
+    base, extra = divmod(nt, world)
+    lo = rank * base + min(rank, extra)
+    hi = lo + base + (1 if rank < extra else 0)
+    return list(range(lo, hi))
+
+
+def allreduce_fn(group=None) -> Callable[[torch.Tensor], None]:
+    """In-place sum all-reduce of the packed [grad | sums] vector."""
+    import torch.distributed as dist
+
+    def fn(t: torch.Tensor) -> None:
+        dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
+    return fn
+
+
+def reduce_packed(grad: torch.Tensor, sums: torch.Tensor, reduce_fn, packed: Optional[torch.Tensor] = None):
+    """Pack (grad as float64, sums), reduce once, unpack in place."""
+    n = grad.numel()
+    if packed is None:
+        packed = torch.empty(n + sums.numel(), dtype=torch.float64, device=grad.device)
+    packed[:n].copy_(grad.reshape(-1))
+    packed[n:].copy_(sums)
+    reduce_fn(packed)
+    grad.reshape(-1).copy_(packed[:n])
+    sums.copy_(packed[n:])
+    return packed
+
+
+# -- run log -------------------------------------------------------------------------
+
+CSV_COLUMNS = ("epoch", "lr", "phys", "ic", "sym", "energy", "total",
+               "grad_norm_all", "grad_var_all", "grad_norm_q", "grad_var_q",
+               "mw_q", "i_bh", "l2_err")
+
+
+@dataclass
+class RunRow:
+    epoch: int
+    lr: float
+    phys: float
+    ic: float
+    sym: float
+    energy: float
+    total: float
+    grad_norm_all: Optional[float] = None
+    grad_var_all: Optional[float] = None
+    grad_norm_q: Optional[float] = None
+    grad_var_q: Optional[float] = None
+    mw_q: Optional[float] = None
+    i_bh: Optional[float] = None
+    l2_err: Optional[float] = None
+    bin_phys: tuple = ()
+
+    def csv_cells(self):
+        def fmt(v):
+            return "" if v is None else repr(v)
+        return [str(self.epoch)] + [fmt(v) for v in
+                (self.lr, self.phys, self.ic, self.sym, self.energy, self.total,
+                 self.grad_norm_all, self.grad_var_all, self.grad_norm_q,
+                 self.grad_var_q, self.mw_q, self.i_bh, self.l2_err)]
+
+
+@dataclass
+class RunLog:
+    rows: List[RunRow] = field(default_factory=list)
+    wall_s: float = 0.0
+
+    def to_csv(self, path) -> None:
+        with open(path, "w") as f:
+            f.write(",".join(CSV_COLUMNS) + "\n")
+            for row in self.rows:
+                f.write(",".join(row.csv_cells()) + "\n")
+
+
+@dataclass
+class TrainResult:
+    log: RunLog
+    model: Model
+    params: ParameterStore
+
+
+# -- the step engine ---------------------------------------------------------------------
+
+class Trainer:
+    """Device-resident QPINN epoch step (training.py:359-407 without probes)."""
+
+    def __init__(self, config: TrainConfig, device="cuda", dtype=torch.float32,
+                 rank: int = 0, world_size: int = 1, reduce_fn=None, log_grad: bool = False,
+                 max_points: int = 1 << 21):
+        self.config = config
+        self.device = torch.device(device)
+        t_end = config.resolved_t_end()
+        self.model = build_model(replace(config.model, t_domain=t_end), device=device, dtype=dtype)
+        flat = self.model.init_params_np()
+        if self.model.n_quantum:
+            flat[self.model.n_classical:] = init_quantum_params(
+                config.init_strategy, self.model.n_quantum, config.seed)
+        self.params = self.model.params_from(flat)
+        self.flat = self.params.flat.requires_grad_(True)
+        nx, ny, nt = config.grid
+        self.grid = CollocationGrid(nx, ny, nt, t_end)
+        self.material = MaterialMap(case=config.case, eps_r=config.eps_r, slab_x0=config.slab_x0)
+        self.world_size, self.rank = world_size, rank
+        self.slices = shard_slices(nt, rank, world_size)
+        self.reduce_fn = reduce_fn if world_size > 1 else None
+        self.evaluator = LossEvaluator(
+            self.model, self.grid, self.material, case=config.case,
+            phys_mode=config.phys_loss_mode, energy_enabled=config.energy_loss_enabled,
+            chunk_slices=config.chunk_slices, slices=self.slices, max_points=max_points)
+        self.adam = AdamState.zeros_like(self.flat.detach())
+        dev = self.device
+        self.sums = torch.zeros(N.LOSS_NSUMS, dtype=torch.float64, device=dev)
+        self.bd = torch.zeros(10, dtype=torch.float64, device=dev)
+        self.flag = torch.zeros(1, dtype=torch.int32, device=dev)
+        self.weights = None
+        self.weights_next = None
+        self._packed = None
+        self.log_grad = log_grad
+        self._host = torch.zeros(16, dtype=torch.float64, pin_memory=True)
+        if config.adaptive_weighting:
+            # untaped initial pass (training.py:336-339)
+            bins = self._evaluate_untaped()
+            self.weights = torch.as_tensor(time_bin_weights(bins, config.kappa),
+                                           dtype=torch.float64, device=dev)
+            self.weights_next = torch.empty_like(self.weights)
+        self.epoch = 0
+        self._host_inputs = None
+
+    # -- end-to-end mode: collocation inputs come from pinned host memory ------
+    def set_host_inputs(self, on: bool) -> None:
+        if not on:
+            self._host_inputs = None
+            return
+        self._host_inputs = [tuple(v.detach().cpu().pin_memory() for v in (ch.x, ch.y, ch.t))
+                             for ch in self.evaluator.chunks]
+
+    def host_input_bytes(self) -> int:
+        if not self._host_inputs:
+            return 0
+        return sum(v.numel() * v.element_size() for hs in self._host_inputs for v in hs)
+
+    def readback_bytes(self) -> int:
+        return 11 * 8 + (32 if self.log_grad else 0)
+
+    def _evaluate_untaped(self):
+        sums = torch.zeros(N.LOSS_NSUMS, dtype=torch.float64, device=self.device)
+        with torch.no_grad():
+            self.evaluator.sweep(self.flat.detach(), None, False, sums)
+        if self.reduce_fn is not None:
+            self.reduce_fn(sums)
+        bd = self.evaluator.finalize(sums, None)
+        self._check_domain()
+        return bd[5:10].cpu().numpy()
+
+    def _check_domain(self):
+        if self.model.circuit is not None:
+            from .ansatz import check_domain
+            check_domain(self.model.circuit, self.model.dtype, self.device)
+
+    def step(self) -> RunRow:
+        """One epoch: evaluate(tape=True) -> (all-reduce) -> finalize -> Adam."""
+        cfg = self.config
+        epoch = self.epoch
+        lr = lr_at(epoch, cfg.lr0, cfg.lr_decay, cfg.lr_decay_every)
+        if self._host_inputs is not None:
+            for ch, (hx, hy, ht) in zip(self.evaluator.chunks, self._host_inputs):
+                ch.x.copy_(hx, non_blocking=True)
+                ch.y.copy_(hy, non_blocking=True)
+                ch.t.copy_(ht, non_blocking=True)
+        self.sums.zero_()
+        self.flat.grad = None
+        self.evaluator.sweep(self.flat, self.weights, True, self.sums)
+        grad = self.flat.grad
+        if self.reduce_fn is not None:
+            self._packed = reduce_packed(grad, self.sums, self.reduce_fn, self._packed)
+        self.evaluator.finalize(self.sums, self.weights, cfg.kappa, self.bd,
+                                self.weights_next if self.weights is not None else None)
+        adam_step(self.flat.detach(), grad, self.adam, lr, loss_dev=self.bd[4:5],
+                  flag=self.flag, sync=False)
+        host = self._host
+        host[:10].copy_(self.bd, non_blocking=True)
+        host[10:11].copy_(self.flag, non_blocking=True)
+        if self.log_grad:
+            g = grad.double()
+            host[11] = 0.0
+            host[11:12].copy_(torch.linalg.vector_norm(g).reshape(1), non_blocking=True)
+            host[12:13].copy_(torch.var(g, unbiased=False).reshape(1), non_blocking=True)
+            q = g[self.model.n_classical:]
+            if q.numel():
+                host[13:14].copy_(torch.linalg.vector_norm(q).reshape(1), non_blocking=True)
+                host[14:15].copy_(torch.var(q, unbiased=False).reshape(1), non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        self._check_domain()
+        v = host.numpy()
+        f = int(v[10])
+        if f:
+            raise RunAborted(("non-finite loss" if f & 2 else "non-finite gradient")
+                             + f" at epoch {epoch}; last good parameters preserved")
+        self.adam.t += 1
+        if self.weights is not None:
+            self.weights, self.weights_next = self.weights_next, self.weights
+        self.epoch += 1
+        bd = LossEvaluator.breakdown_from(v[:10])
+        row = RunRow(epoch=epoch, lr=lr, phys=bd.phys, ic=bd.ic, sym=bd.sym, energy=bd.energy,
+                     total=bd.total, bin_phys=bd.bin_phys)
+        if self.log_grad:
+            row.grad_norm_all, row.grad_var_all = float(v[11]), float(v[12])
+            if self.model.n_quantum:
+                row.grad_norm_q, row.grad_var_q = float(v[13]), float(v[14])
+        return row
+
+
+def train(config: TrainConfig, outdir=None, on_epoch=None, device="cuda",
+          dtype=torch.float32, rank: int = 0, world_size: int = 1, reduce_fn=None) -> TrainResult:
+    """Full-batch Adam training (training.py:309-414), probes excluded."""
+    t0 = time.perf_counter()
+    tr = Trainer(config, device=device, dtype=dtype, rank=rank, world_size=world_size,
+                 reduce_fn=reduce_fn, log_grad=True)
+    log = RunLog()
+    try:
+        for _ in range(config.epochs):
+            row = tr.step()
+            log.rows.append(row)
+            if on_epoch is not None:
+                on_epoch(row)
+    except RunAborted:
+        log.wall_s = time.perf_counter() - t0
+        if outdir is not None:
+            import os
+            save_checkpoint(os.path.join(str(outdir), "last_good.ckpt"), tr.model, tr.params)
+            log.to_csv(os.path.join(str(outdir), "metrics.csv"))
+        raise
+    log.wall_s = time.perf_counter() - t0
+    if outdir is not None:
+        import os
+        save_checkpoint(os.path.join(str(outdir), "final.ckpt"), tr.model, tr.params)
+        log.to_csv(os.path.join(str(outdir), "metrics.csv"))
+    return TrainResult(log=log, model=tr.model, params=tr.params)

@@ -1,0 +1,51 @@
+"""Host-side logic that needs no GPU: grid/bin/normaliser tables, parameter
+layout + RNG streams, data-parallel sharding arithmetic."""
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+from conftest import load_golden
+
+
+def test_model_layout_and_init_match_reference_golden():
+    from paper_2506_23246_b200.network import Model, ModelConfig
+    g = load_golden("eval_vacuum7.npz")
+    m = Model(ModelConfig(variant="hybrid", ansatz="strongly", scale="acos", seed=0),
+              device="cpu", dtype=torch.float64)
+    assert m.total_parameter_count == 66932
+    names = [(n, o) for n, o, _ in m.layout]
+    assert names[-1] == ("quantum", 66848)
+    assert dict(names)["tau_raw"] == 66847
+    assert np.array_equal(m.init_params_np(), g["flat"])
+
+
+def test_shard_slices_partition():
+    from paper_2506_23246_b200.training import shard_slices
+    for nt in (1, 5, 16, 64, 67):
+        for world in (1, 2, 3, 4, 8):
+            parts = [shard_slices(nt, r, world) for r in range(world)]
+            flat = [s for p in parts for s in p]
+            assert flat == list(range(nt))
+            sizes = [len(p) for p in parts]
+            assert max(sizes) - min(sizes) <= 1
+
+
+def test_time_bin_weights_matches_oracle(rng):
+    from paper_2506_23246_b200.physics import time_bin_weights
+    for _ in range(20):
+        b = rng.uniform(0, 3, 5)
+        assert np.allclose(time_bin_weights(b, 1.3), O.time_bin_weights(b, 1.3), rtol=0, atol=0)
+
+
+def test_grid_bins_and_mirrors_match_oracle():
+    from paper_2506_23246_b200.physics import CollocationGrid
+    for dims in ((64, 64, 16), (128, 128, 64), (6, 4, 5)):
+        g = CollocationGrid(*dims, 1.5)
+        o = O.Grid(*dims, 1.5)
+        assert [g.bin_of_slice(i) for i in range(g.nt)] == [o.bin_of_slice(i) for i in range(o.nt)]
+        assert np.array_equal(g.mirror_x_local, o.mirror_x)
+        assert np.array_equal(g.mirror_y_local, o.mirror_y)
+    g = CollocationGrid(64, 64, 16, 1.5)
+    pops = [sum(1 for i in range(16) if g.bin_of_slice(i) == m) for m in range(5)]
+    assert pops == [3, 3, 3, 3, 4]

@@ -1,0 +1,140 @@
+"""K1/K2 parity on the GPU through the C ABI, against reference golden vectors
+and the numpy oracle."""
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+from conftest import golden_cases
+from gpu_util import assert_close, cuda
+
+pytestmark = pytest.mark.gpu
+DTYPES = [torch.float64, torch.float32]
+
+
+def _run(d, kind, scale, L, dtype):
+    from paper_2506_23246_b200.ansatz import build_circuit, pqc_backward_raw, pqc_forward_raw
+    n = d["a"].shape[1]
+    c = build_circuit(kind, n, L)
+    a, da, qp = cuda(d["a"], dtype), cuda(d["da"], dtype), cuda(d["qp"], dtype)
+    z, dz = pqc_forward_raw(c, scale, a, da, qp)
+    zp, _ = pqc_forward_raw(c, scale, a, None, qp)
+    ga, gda, gq = pqc_backward_raw(c, scale, a, da, qp, cuda(d["gz"], dtype), cuda(d["gdz"], dtype))
+    return z, dz, zp, ga, gda, gq
+
+
+def _check_fixture(name, L_of, dtype):
+    for key, d in golden_cases(name).items():
+        parts = key.split("/")
+        kind = parts[0]
+        scale, L = L_of(parts)
+        z, dz, zp, ga, gda, gq = _run(d, kind, scale, L, dtype)
+        # the edge cases (|a| -> 0.995) amplify S'' ~ (1-a^2)^-1.5 ~ 1e3
+        s = 30.0 if "edge" in key and dtype == torch.float32 else 1.0
+        assert_close(z, d["z"], dtype, f"{key} z", s)
+        assert_close(dz, d["dz"], dtype, f"{key} dz", s)
+        assert_close(zp, d["zplain"], dtype, f"{key} z(value-only)", s)
+        assert_close(ga, d["ga"], dtype, f"{key} g_a", s)
+        assert_close(gda, d["gda"], dtype, f"{key} g_da", s)
+        assert_close(gq, d["gq"], dtype, f"{key} g_qparams", s)
+
+
+@pytest.mark.parametrize("dtype", DTYPES)
+def test_pqc_all_ansatz_scale_small(dtype):
+    _check_fixture("pqc_small.npz", lambda p: (p[1], 2), dtype)
+
+
+@pytest.mark.parametrize("dtype", DTYPES)
+def test_pqc_default_7q_4l(dtype):
+    _check_fixture("pqc_n7.npz", lambda p: (p[1], 4), dtype)
+
+
+@pytest.mark.parametrize("dtype", DTYPES)
+def test_pqc_mid_sizes(dtype):
+    _check_fixture("pqc_mid.npz", lambda p: ("bias", int(p[2])), dtype)
+
+
+@pytest.mark.parametrize("dtype", DTYPES)
+@pytest.mark.parametrize("n,L", [(1, 3), (2, 2), (8, 2)])
+def test_pqc_vs_oracle_other_sizes(dtype, n, L):
+    from paper_2506_23246_b200 import _native as N
+    if n > N.lib().qpinn_pqc_max_qubits(0 if dtype == torch.float32 else 1):
+        pytest.skip("beyond the register regime for this dtype")
+    rng = np.random.default_rng(n * 100 + L)
+    for kind in (("no_entanglement",) if n == 1 else ("strongly", "cross_mesh_2rot", "cross_mesh_cnot")):
+        P = O.build_circuit(kind, n, L)[1]
+        R = 37
+        d = dict(a=rng.uniform(-0.9, 0.9, (R, n)), da=rng.normal(size=(3, R, n)),
+                 qp=rng.uniform(0, 2 * np.pi, P), gz=rng.normal(size=(R, n)),
+                 gdz=rng.normal(size=(3, R, n)))
+        z, dz, zp, ga, gda, gq = _run(d, kind, "acos", L, dtype)
+        wz, wdz = O.pqc_forward(d["a"], d["da"], d["qp"], kind, "acos", L)
+        wga, wgda, wgq = O.pqc_backward(d["a"], d["da"], d["qp"], kind, "acos", L, d["gz"], d["gdz"])
+        assert_close(z, wz, dtype, "z")
+        assert_close(dz, wdz, dtype, "dz")
+        assert_close(zp, wz, dtype, "zp")
+        assert_close(ga, wga, dtype, "ga")
+        assert_close(gda, wgda, dtype, "gda")
+        assert_close(gq, wgq, dtype, "gq")
+
+
+@pytest.mark.parametrize("dtype", DTYPES)
+def test_pqc_large_batch_sampled_rows_and_properties(dtype):
+    """R = 2^16 (config-2 size): sampled rows vs oracle, |<Z>| <= 1, and the
+    no_entanglement/acos identity z == a at zero parameters (ansatz tests)."""
+    from paper_2506_23246_b200.ansatz import build_circuit, pqc_forward_raw
+    rng = np.random.default_rng(5)
+    R, n, L = 1 << 16, 7, 4
+    c = build_circuit("strongly", n, L)
+    a = rng.uniform(-0.95, 0.95, (R, n))
+    da = rng.normal(size=(3, R, n))
+    qp = rng.uniform(0, 2 * np.pi, c.param_count)
+    z, dz = pqc_forward_raw(c, "acos", cuda(a, dtype), cuda(da, dtype), cuda(qp, dtype))
+    zc = z.double().cpu().numpy()
+    assert np.all(np.abs(zc) <= 1 + 1e-5)
+    idx = rng.choice(R, 64, replace=False)
+    wz, wdz = O.pqc_forward(a[idx], da[:, idx], qp, "strongly", "acos", L)
+    assert_close(z[idx], wz, dtype, "z sampled")
+    assert_close(dz[:, idx], wdz, dtype, "dz sampled")
+    c0 = build_circuit("no_entanglement", n, L)
+    z0, _ = pqc_forward_raw(c0, "acos", cuda(a, dtype), None, cuda(np.zeros(c0.param_count), dtype))
+    assert np.max(np.abs(z0.double().cpu().numpy() - a)) <= (1e-10 if dtype == torch.float64 else 2e-6)
+    z1, _ = pqc_forward_raw(c0, "asin", cuda(a, dtype), None, cuda(np.zeros(c0.param_count), dtype))
+    assert np.max(np.abs(z1.double().cpu().numpy() + a)) <= (1e-10 if dtype == torch.float64 else 2e-6)
+
+
+def test_pqc_backward_is_bitwise_deterministic():
+    from paper_2506_23246_b200.ansatz import build_circuit, pqc_backward_raw
+    rng = np.random.default_rng(9)
+    R, n = 20000, 7
+    c = build_circuit("cross_mesh", n, 4)
+    args = [cuda(x, torch.float32) for x in (rng.uniform(-0.9, 0.9, (R, n)), rng.normal(size=(3, R, n)),
+                                              rng.uniform(0, 6, c.param_count), rng.normal(size=(R, n)),
+                                              rng.normal(size=(3, R, n)))]
+    r1 = pqc_backward_raw(c, "asin", *args)
+    r2 = pqc_backward_raw(c, "asin", *args)
+    for x, y in zip(r1, r2):
+        assert torch.equal(x, y)
+
+
+def test_quantum_layer_forward_autograd_and_domain():
+    from paper_2506_23246_b200 import BatchedDual, DomainError, build_circuit, quantum_layer_forward
+    rng = np.random.default_rng(2)
+    c = build_circuit("strongly", 3, 2)
+    d = golden_cases("pqc_small.npz")["strongly/acos"]
+    a = cuda(d["a"], torch.float64).requires_grad_(True)
+    da = cuda(d["da"], torch.float64).requires_grad_(True)
+    qp = cuda(d["qp"], torch.float64).requires_grad_(True)
+    out = quantum_layer_forward(BatchedDual(a, da), qp, c, "acos")
+    loss = (out.val * cuda(d["gz"], torch.float64)).sum() + (out.tan * cuda(d["gdz"], torch.float64)).sum()
+    loss.backward()
+    assert_close(a.grad, d["ga"], torch.float64, "autograd g_a")
+    assert_close(da.grad, d["gda"], torch.float64, "autograd g_da")
+    assert_close(qp.grad, d["gq"], torch.float64, "autograd g_qp")
+    bad = cuda(np.full((4, 3), 1.0 + 1e-9), torch.float64)
+    with pytest.raises(DomainError):
+        quantum_layer_forward(bad, qp.detach(), c, "acos")
+    edge = cuda(np.full((4, 3), 1.0 + 5e-13), torch.float64)
+    with pytest.warns(UserWarning):
+        z = quantum_layer_forward(edge, qp.detach(), c, "acos")
+    assert torch.isfinite(z).all()

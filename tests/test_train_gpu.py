@@ -1,0 +1,88 @@
+"""Full train-step parity on the GPU: LossEvaluator.evaluate(tape=True)
+gradients/breakdowns vs reference golden vectors, and loss curves vs the
+reference trainer."""
+import numpy as np
+import pytest
+import torch
+
+from conftest import load_golden
+from gpu_util import assert_close
+
+pytestmark = pytest.mark.gpu
+
+
+def _build(g, dtype):
+    from paper_2506_23246_b200.network import Model, ModelConfig
+    from paper_2506_23246_b200.physics import CollocationGrid, LossEvaluator, MaterialMap
+    h, F, n, L, seed = (int(v) for v in g["config"])
+    cfg = ModelConfig(variant="hybrid", hidden_width=h, rff_features=F, n_qubits=n,
+                      n_layers_pqc=L, ansatz=str(g["ansatz"]), scale=str(g["scale"]), seed=seed,
+                      t_domain=float(g["t_domain"]))
+    model = Model(cfg, device="cuda", dtype=dtype)
+    grid = CollocationGrid(*(int(v) for v in g["grid"]), float(g["t_end"]))
+    case = str(g["case"])
+    ev = LossEvaluator(model, grid, MaterialMap(case), case=case, phys_mode=str(g["phys_mode"]),
+                       energy_enabled=bool(g["energy"]), chunk_slices=int(g["chunk_slices"]))
+    return model, ev
+
+
+EVALS = ["eval_micro_vacuum.npz", "eval_micro_diel.npz", "eval_micro_asym.npz", "eval_desk.npz",
+         "eval_vacuum7.npz", "eval_diel7.npz"]
+
+
+@pytest.mark.parametrize("dtype", [torch.float64, torch.float32])
+@pytest.mark.parametrize("name", EVALS)
+def test_evaluate_tape_matches_reference(name, dtype):
+    g = load_golden(name)
+    model, ev = _build(g, dtype)
+    params = model.params_from(g["flat"])
+    assert np.array_equal(model.init_params_np(), g["flat"])
+    w = g["weights"] if g["weights"].size else None
+    res = ev.evaluate(params, weights=w, tape=True)
+    bd = res.breakdown
+    got = np.array([bd.phys, bd.ic, bd.sym, bd.energy, bd.total])
+    # scalar losses are sums of many squares: FP32 carries ~1e-6 relative
+    s = 1.0 if dtype == torch.float64 else 10.0
+    assert_close(got, g["breakdown"], dtype, "breakdown", s)
+    assert_close(np.array(bd.bin_phys), g["bin_phys"], dtype, "bin_phys", s)
+    assert_close(res.grad, g["grad"], dtype, "flat gradient", 1.0 if dtype == torch.float64 else 3.0)
+    from paper_2506_23246_b200.network import FieldBatch
+    x, y, t = ev.grid.flat_points()
+    fields, derivs = model.forward(params, x, y, t, derivs=True)
+    assert_close(torch.stack([fields.ez, fields.hx, fields.hy]), g["fields"], dtype, "fields")
+    assert_close(torch.stack([derivs.ez, derivs.hx, derivs.hy]), g["derivs"], dtype, "derivs")
+    plain = ev.evaluate(params, weights=w, tape=False)
+    assert abs(plain.breakdown.total - float(g["plain_total"])) <= (1e-10 if dtype == torch.float64 else 1e-4) * abs(float(g["plain_total"]))
+
+
+@pytest.mark.parametrize("dtype,epochs,rtol", [(torch.float64, 1000, 1e-9), (torch.float32, 1000, 1e-4)])
+def test_train_curve_matches_reference_desk(dtype, epochs, rtol):
+    """1k Adam steps of the desk_smoke model (4q x 2L, 8x8x10 grid)."""
+    from paper_2506_23246_b200.network import ModelConfig
+    from paper_2506_23246_b200.training import TrainConfig, train
+    g = load_golden("train_desk.npz")
+    h, F, n, L, seed = (int(v) for v in g["config"])
+    cfg = TrainConfig(case="vacuum", model=ModelConfig(variant="hybrid", hidden_width=h,
+                      rff_features=F, n_qubits=n, n_layers_pqc=L, ansatz=str(g["ansatz"]),
+                      scale=str(g["scale"]), seed=seed), epochs=epochs,
+                      grid=tuple(int(v) for v in g["grid"]), eval_cadence=0, probe_cadence=0)
+    res = train(cfg, dtype=dtype)
+    tot = np.array([r.total for r in res.log.rows])
+    want = g["total"][:epochs]
+    rel = np.max(np.abs(tot - want) / np.abs(want))
+    assert rel <= rtol, rel
+
+
+def test_train_curve_matches_reference_vacuum7_fp64():
+    """Full-width 7q x 4L model (66,932 params), 200 epochs on a 4x4x6 grid."""
+    from paper_2506_23246_b200.network import ModelConfig
+    from paper_2506_23246_b200.training import TrainConfig, train
+    g = load_golden("train_vacuum7.npz")
+    cfg = TrainConfig(case="vacuum", model=ModelConfig(variant="hybrid", ansatz="strongly",
+                      scale="acos", seed=0), epochs=200, grid=(4, 4, 6), eval_cadence=0,
+                      probe_cadence=0)
+    res = train(cfg, dtype=torch.float64)
+    tot = np.array([r.total for r in res.log.rows])
+    rel = np.max(np.abs(tot - g["total"]) / np.abs(g["total"]))
+    assert rel <= 1e-8, rel
+    assert np.allclose(res.params.flat.cpu().numpy(), g["final_flat"], rtol=1e-7, atol=1e-9)
