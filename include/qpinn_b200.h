@@ -85,23 +85,30 @@ int qpinn_pqc_max_qubits(int dtype);
 /* Device scratch needed by forward/backward for `rows` points. */
 size_t qpinn_pqc_workspace_bytes(const qpinn_circuit* c, int dtype, int64_t rows);
 
+/* Bytes of the optional final-state hand-off buffer (4 states x 2^n
+ * amplitudes per row) that lets the backward skip re-running the circuit. */
+size_t qpinn_pqc_state_bytes(const qpinn_circuit* c, int dtype, int64_t rows);
+
 /* z[R,n] = <Z_q>, dz[3,R,n] = d<Z_q>/d(x,y,t) of the scaled-angle-embedded
  * circuit; act_val [R,n], act_tan [3,R,n] row-major (act_tan/dz may be NULL
- * for value-only evaluation), qparams [P].  Folds max|act_val| into the
- * workspace's running maximum for qpinn_pqc_domain_check. */
+ * for value-only evaluation), qparams [P].  When `states` is not NULL (and
+ * tangents are on) the final psi, d psi/dx,y,t are stored there for
+ * qpinn_pqc_backward.  Folds max|act_val| into the workspace's running
+ * maximum for qpinn_pqc_domain_check. */
 int qpinn_pqc_forward(const qpinn_circuit* c, int dtype, int scale, int64_t rows,
                       const void* act_val, const void* act_tan, const void* qparams,
-                      void* z, void* dz, void* workspace, size_t workspace_bytes,
-                      void* stream);
+                      void* z, void* dz, void* states, void* workspace,
+                      size_t workspace_bytes, void* stream);
 
 /* Gradients of L(z, dz) given g_z = dL/dz [R,n] and g_dz = dL/d(dz) [3,R,n]:
  * g_act_val [R,n], g_act_tan [3,R,n] and g_qparams [P] (summed over all rows
- * in a fixed, run-to-run deterministic order). */
+ * in a fixed, run-to-run deterministic order).  `states` is the buffer a
+ * forward on the same inputs filled, or NULL to recompute the circuit. */
 int qpinn_pqc_backward(const qpinn_circuit* c, int dtype, int scale, int64_t rows,
                        const void* act_val, const void* act_tan, const void* qparams,
-                       const void* g_z, const void* g_dz, void* g_act_val,
-                       void* g_act_tan, void* g_qparams, void* workspace,
-                       size_t workspace_bytes, void* stream);
+                       const void* states, const void* g_z, const void* g_dz,
+                       void* g_act_val, void* g_act_tan, void* g_qparams,
+                       void* workspace, size_t workspace_bytes, void* stream);
 
 /* Synchronises `stream`, reads (and resets to 0) the running max|act_val| of
  * the forwards launched on this workspace since the last check (a fresh

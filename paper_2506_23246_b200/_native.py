@@ -54,9 +54,10 @@ SIGNATURES = [
     ("qpinn_circuit_plan_dump", _SZ, [_VP, C.c_char_p, _SZ]),
     ("qpinn_pqc_max_qubits", _I, [_I]),
     ("qpinn_pqc_workspace_bytes", _SZ, [_VP, _I, _I64]),
-    ("qpinn_pqc_forward", _I, [_VP, _I, _I, _I64, _VP, _VP, _VP, _VP, _VP, _VP, _SZ, _VP]),
+    ("qpinn_pqc_state_bytes", _SZ, [_VP, _I, _I64]),
+    ("qpinn_pqc_forward", _I, [_VP, _I, _I, _I64, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _SZ, _VP]),
     ("qpinn_pqc_backward", _I, [_VP, _I, _I, _I64, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP,
-                                _VP, _SZ, _VP]),
+                                _VP, _VP, _SZ, _VP]),
     ("qpinn_pqc_domain_check", _I, [_VP, _VP, C.POINTER(_D), C.POINTER(_I)]),
     ("qpinn_loss_workspace_bytes", _SZ, [C.POINTER(LossSpec), _I, _I64]),
     ("qpinn_loss_forward_backward", _I, [C.POINTER(LossSpec), _I, _I64, _VP, _VP, _VP, _VP,

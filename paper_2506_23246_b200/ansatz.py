@@ -245,8 +245,15 @@ def check_domain(circuit: CircuitSpec, dtype, device, stream=None) -> float:
     return m.value
 
 
-def pqc_forward_raw(circuit: CircuitSpec, scale_kind, a, da, qp):
-    """K1 launch: z [R,n] and dz [3,R,n] (dz None when da is None)."""
+def state_buffer(circuit: CircuitSpec, a) -> torch.Tensor:
+    """Final-state hand-off buffer K1 -> K2 (4 states x 2^n complex per row)."""
+    nbytes = N.lib().qpinn_pqc_state_bytes(circuit.handle, N.dtype_code(a.dtype), a.shape[0])
+    return torch.empty(nbytes // a.element_size(), dtype=a.dtype, device=a.device)
+
+
+def pqc_forward_raw(circuit: CircuitSpec, scale_kind, a, da, qp, states=None):
+    """K1 launch: z [R,n] and dz [3,R,n] (dz None when da is None); fills
+    ``states`` (see ``state_buffer``) for the backward when given."""
     R, n = a.shape
     z = torch.empty_like(a)
     dz = torch.empty((3, R, n), dtype=a.dtype, device=a.device) if da is not None else None
@@ -254,15 +261,16 @@ def pqc_forward_raw(circuit: CircuitSpec, scale_kind, a, da, qp):
     with N.timed("pqc_forward"):
         rc = N.lib().qpinn_pqc_forward(
             circuit.handle, N.dtype_code(a.dtype), _SCALE_CODE[ScaleKind(scale_kind)], R,
-            N.ptr(a), N.ptr(da), N.ptr(qp), N.ptr(z), N.ptr(dz), ws.data_ptr(), ws.numel(),
-            N.stream_ptr())
+            N.ptr(a), N.ptr(da), N.ptr(qp), N.ptr(z), N.ptr(dz), N.ptr(states), ws.data_ptr(),
+            ws.numel(), N.stream_ptr())
     N.check(rc, "qpinn_pqc_forward")
     N.count_launches(1 if R else 0)
     return z, dz
 
 
-def pqc_backward_raw(circuit: CircuitSpec, scale_kind, a, da, qp, gz, gdz):
-    """K2 launch: (g_a [R,n], g_da [3,R,n], g_qp [P])."""
+def pqc_backward_raw(circuit: CircuitSpec, scale_kind, a, da, qp, gz, gdz, states=None):
+    """K2 launch: (g_a [R,n], g_da [3,R,n], g_qp [P]); ``states`` from the
+    matching forward skips the circuit replay."""
     R, n = a.shape
     ga = torch.empty_like(a)
     gda = torch.empty_like(da)
@@ -271,8 +279,8 @@ def pqc_backward_raw(circuit: CircuitSpec, scale_kind, a, da, qp, gz, gdz):
     with N.timed("pqc_backward"):
         rc = N.lib().qpinn_pqc_backward(
             circuit.handle, N.dtype_code(a.dtype), _SCALE_CODE[ScaleKind(scale_kind)], R,
-            N.ptr(a), N.ptr(da), N.ptr(qp), N.ptr(gz), N.ptr(gdz), N.ptr(ga), N.ptr(gda),
-            N.ptr(gq), ws.data_ptr(), ws.numel(), N.stream_ptr())
+            N.ptr(a), N.ptr(da), N.ptr(qp), N.ptr(states), N.ptr(gz), N.ptr(gdz), N.ptr(ga),
+            N.ptr(gda), N.ptr(gq), ws.data_ptr(), ws.numel(), N.stream_ptr())
     N.check(rc, "qpinn_pqc_backward")
     N.count_launches(3 if R else 0)
     return ga, gda, gq
@@ -283,7 +291,10 @@ class _PQC(torch.autograd.Function):
 
     @staticmethod
     def forward(ctx, a, da, qp, circuit, scale_kind):
-        z, dz = pqc_forward_raw(circuit, scale_kind, a, da, qp)
+        need_grad = any(ctx.needs_input_grad[:3])
+        states = state_buffer(circuit, a) if need_grad else None
+        z, dz = pqc_forward_raw(circuit, scale_kind, a, da, qp, states)
+        ctx.states = states
         ctx.save_for_backward(a, da, qp)
         ctx.circuit = circuit
         ctx.scale_kind = scale_kind
@@ -294,7 +305,9 @@ class _PQC(torch.autograd.Function):
         a, da, qp = ctx.saved_tensors
         gz = torch.zeros_like(a) if gz is None else gz.contiguous()
         gdz = torch.zeros_like(da) if gdz is None else gdz.contiguous()
-        ga, gda, gq = pqc_backward_raw(ctx.circuit, ctx.scale_kind, a, da, qp, gz, gdz)
+        ga, gda, gq = pqc_backward_raw(ctx.circuit, ctx.scale_kind, a, da, qp, gz, gdz,
+                                       ctx.states)
+        ctx.states = None
         return ga, gda, gq, None, None
 
 

@@ -366,4 +366,6 @@ def train(config: TrainConfig, outdir=None, on_epoch=None, device="cuda",
         import os
         save_checkpoint(os.path.join(str(outdir), "final.ckpt"), tr.model, tr.params)
         log.to_csv(os.path.join(str(outdir), "metrics.csv"))
-    return TrainResult(log=log, model=tr.model, params=tr.params)
+    params = ParameterStore(tr.flat.detach(), tr.params.n_classical, tr.params.n_quantum,
+                            tr.params.t_domain)
+    return TrainResult(log=log, model=tr.model, params=params)
