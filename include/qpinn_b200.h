@@ -78,6 +78,14 @@ size_t qpinn_circuit_dump(const qpinn_circuit* c, char* buf, size_t len);
 /* One line per fused step: "u1 <kind> <wire> <slots>" | "perm <p0,p1,...>" |
  * "phases <c:t:slot ...>". */
 size_t qpinn_circuit_plan_dump(const qpinn_circuit* c, char* buf, size_t len);
+/* Kernel choice for this circuit: 0 (default) uses the layer-loop K1/K2
+ * (wires unrolled at compile time) when the fused plan has the uniform layer
+ * shape every build_circuit ansatz has, 1 forces the generic runtime-plan
+ * kernels.  Set it before the forward whose states feed a backward (the two
+ * must use the same variant). */
+int qpinn_circuit_set_kernel_variant(qpinn_circuit* c, int variant);
+/* 1 if the layer-loop kernels apply to this circuit. */
+int qpinn_circuit_specialized(const qpinn_circuit* c);
 /* Largest n_qubits the register-resident kernels accept for `dtype`. */
 int qpinn_pqc_max_qubits(int dtype);
 

@@ -163,6 +163,16 @@ class CircuitSpec:
             self._workspaces[key] = ws
         return ws
 
+    @property
+    def specialized(self) -> bool:
+        """Compile-time specialised K1/K2 exist for this (ansatz, n, L)."""
+        return bool(N.lib().qpinn_circuit_specialized(self._h))
+
+    def set_kernel_variant(self, variant: str) -> None:
+        """"auto" (specialised kernels when available) or "generic"."""
+        code = {"auto": 0, "generic": 1}[variant]
+        N.check(N.lib().qpinn_circuit_set_kernel_variant(self._h, code), "set_kernel_variant")
+
     def __repr__(self):
         return (f"CircuitSpec(kind={self.kind.value}, n_qubits={self.n_qubits}, "
                 f"n_layers={self.n_layers}, param_count={self.param_count})")

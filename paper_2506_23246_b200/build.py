@@ -15,7 +15,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libqpinn_b200.so")
-SOURCES = ["circuit.cu", "pqc.cu", "loss.cu", "adam.cu"]
+SOURCES = ["circuit.cu", "pqc.cu", "pqc_layer.cu", "loss.cu", "adam.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
          "-Xptxas", "-v"]

@@ -80,6 +80,7 @@ struct qpinn_circuit {
   std::vector<int> steps, u1, pairs, phase_off;
   std::vector<uint16_t> perm, iperm;
   int n_u1 = 0, n_perm = 0, n_phase = 0;
+  int variant = 0;  // 0: specialised kernels when available, 1: generic only
   int device = -1;
   void* dev_block = nullptr;
   qpinn::PlanDev dev{};

@@ -34,251 +34,9 @@
 #include <cstring>
 #include <mutex>
 
-#include "gates.cuh"
+#include "pqc_layer.h"
 
 namespace qpinn {
-
-// ---- lane geometry -----------------------------------------------------------------
-// AB register bits per lane: n <= 4 -> all in registers; else max(4, n - 3),
-// so that one state of a point spans at most 8 lanes.
-template <typename T, int N, int NSL>
-struct Geo {
-  static constexpr int AB = N <= 4 ? N : (N - 3 > 4 ? N - 3 : 4);
-  static constexpr int A = 1 << AB;
-  static constexpr int LB = N - AB;
-  static constexpr int G = 1 << LB;
-  static constexpr int LPP = NSL * G;  // lanes per point
-  static constexpr int SPW = 32 / LPP;  // points per warp
-  static constexpr int D = 1 << N;
-  static_assert(LPP <= 32, "one point must fit in a warp");
-};
-
-template <typename T>
-constexpr int max_qubits() { return sizeof(T) == 8 ? 7 : 8; }
-
-constexpr int kThreads = 128;  // 4 warps per block
-
-// shared-memory / hand-off layout index of basis state b within one state
-template <int AB, int G>
-__host__ __device__ __forceinline__ int lay(int b) {
-  return (b & ((1 << AB) - 1)) * G + (b >> AB);
-}
-
-// ---- fused step list as a by-value kernel parameter --------------------------------
-// Step descriptors live in the constant bank, so the per-step dispatch is
-// provably warp-uniform: no divergence barriers around the shuffles.
-constexpr int kMaxKSteps = 256;
-struct StepTable {
-  int n;
-  int2 s[kMaxKSteps];  // {type | (wire + 1) << 2, table index}
-};
-
-// ---- block prologue: gate matrices, phase tables, permutation tables --------
-template <typename T>
-struct Smem {
-  cplx<T>* U;     // [n_u1][4]
-  cplx<T>* ph;    // [n_phase][D] at lay(b)
-  uint16_t* pt;   // [n_perm][D]  lay(perm[b]) at lay(b)
-  uint16_t* pti;  // [n_perm][D]  lay(iperm[b]) at lay(b)
-  cplx<T>* buf;   // per-warp permutation buffer [warps][2][32 * A]
-  T* acc;         // K2: per-warp gradient accumulators [warps][n_acc]
-};
-
-__host__ __device__ inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
-
-template <typename T, int N, int AB>
-__host__ __device__ inline size_t smem_layout(const PlanDev& p, int warps, bool bwd, Smem<T>* out,
-                                              unsigned char* base) {
-  constexpr int D = 1 << N;
-  constexpr int A = 1 << AB;
-  size_t o = 0;
-  size_t oU = o; o = align_up(o + sizeof(cplx<T>) * 4 * p.n_u1, 16);
-  size_t oPh = o; o = align_up(o + sizeof(cplx<T>) * (size_t)D * p.n_phase, 16);
-  size_t oPt = o; o = align_up(o + 2 * (size_t)D * p.n_perm, 16);
-  size_t oPti = o; o = align_up(o + (bwd ? 2 * (size_t)D * p.n_perm : 0), 16);
-  size_t oBuf = o; o = align_up(o + sizeof(cplx<T>) * 32 * A * (bwd ? 2 : 1) * (size_t)warps, 16);
-  size_t oAcc = o;
-  if (bwd) o = align_up(o + sizeof(T) * (size_t)warps * (8 * p.n_u1 + (size_t)D * p.n_phase), 16);
-  if (out) {
-    out->U = (cplx<T>*)(base + oU);
-    out->ph = (cplx<T>*)(base + oPh);
-    out->pt = (uint16_t*)(base + oPt);
-    out->pti = (uint16_t*)(base + oPti);
-    out->buf = (cplx<T>*)(base + oBuf);
-    out->acc = (T*)(base + oAcc);
-  }
-  return o;
-}
-
-template <typename T, int N, int AB, int G>
-__device__ void prologue(const PlanDev& p, const T* __restrict__ qp, const Smem<T>& sm, bool bwd,
-                         int warps) {
-  constexpr int D = 1 << N;
-  const int tid = threadIdx.x, nt = blockDim.x;
-  for (int i = tid; i < p.n_u1; i += nt) {
-    const int kind = p.u1[i * 4];
-    double th[3] = {0, 0, 0};
-    for (int j = 0; j < u1_nslots(kind); ++j) th[j] = (double)qp[p.u1[i * 4 + 1 + j]];
-    double U[8];
-    u1_matrix_d(kind, th, U);
-    for (int e = 0; e < 4; ++e) sm.U[i * 4 + e] = {T(U[2 * e]), T(U[2 * e + 1])};
-  }
-  for (int i = tid; i < p.n_phase * D; i += nt) {
-    const int st = i / D, b = i % D;
-    double phi = 0.0;
-    for (int k = p.phase_off[st]; k < p.phase_off[st + 1]; ++k) {
-      const int c = p.pairs[3 * k], t = p.pairs[3 * k + 1], s = p.pairs[3 * k + 2];
-      const int on = (b >> (N - 1 - c)) & 1, tb = (b >> (N - 1 - t)) & 1;
-      phi += on * (tb - 0.5) * (double)qp[s];  // qsim.py:212-225, ansatz.py:259-265
-    }
-    sm.ph[st * D + lay<AB, G>(b)] = {T(cos(phi)), T(sin(phi))};
-  }
-  for (int i = tid; i < p.n_perm * D; i += nt) {
-    const int st = i / D, b = i % D;
-    sm.pt[st * D + lay<AB, G>(b)] = (uint16_t)lay<AB, G>(p.perm[i]);
-    if (bwd) sm.pti[st * D + lay<AB, G>(b)] = (uint16_t)lay<AB, G>(p.iperm[i]);
-  }
-  if (bwd) {
-    const size_t nacc = (size_t)warps * (8 * p.n_u1 + (size_t)D * p.n_phase);
-    for (size_t i = tid; i < nacc; i += nt) sm.acc[i] = T(0);
-  }
-}
-
-// ---- per-point embedding (ansatz.py:233-243, :380-390) in closed form --------
-// State s of the point: s = 0 -> phi = prod_q RX(theta_q)|0>; s = k+1 ->
-// d phi/dx_k = sum_q dtheta_kq d phi/dtheta_q.  Every amplitude is a real
-// magnitude times (-i)^popcount(b); the tangent replaces one factor by its
-// derivative (forward-mode product rule), which leaves the phase unchanged.
-template <typename T, int N, int AB>
-__device__ __forceinline__ void embed(const T (&c)[N], const T (&sn)[N], const T (&dth)[N],
-                                      bool tangent, int gl, cplx<T> (&st)[1 << AB]) {
-  constexpr int A = 1 << AB, LB = N - AB;
-  T mL = T(1), dL = T(0);
-#pragma unroll
-  for (int q = 0; q < LB; ++q) {
-    const int bit = (gl >> (LB - 1 - q)) & 1;
-    const T f = bit ? sn[q] : c[q];
-    const T df = bit ? T(0.5) * c[q] : T(-0.5) * sn[q];
-    dL = dL * f + mL * dth[q] * df;
-    mL *= f;
-  }
-  // register wires by doubling (wire LB is the most significant register bit);
-  // magnitudes in .re, their tangent in .im
-  st[0].re = T(1);
-  st[0].im = T(0);
-#pragma unroll
-  for (int qi = 0; qi < AB; ++qi) {
-    const int q = LB + qi;
-#pragma unroll
-    for (int i = (1 << qi) - 1; i >= 0; --i) {
-      const T m = st[i].re, d = st[i].im;
-      st[2 * i + 1].im = d * sn[q] + m * dth[LB + qi] * (T(0.5) * c[q]);
-      st[2 * i].im = d * c[q] + m * dth[LB + qi] * (T(-0.5) * sn[q]);
-      st[2 * i + 1].re = m * sn[q];
-      st[2 * i].re = m * c[q];
-    }
-  }
-  const int popL = __popc(gl);
-#pragma unroll
-  for (int r = 0; r < A; ++r) {
-    const int ph = (popL + __popc(r)) & 3;  // (-i)^popcount
-    const T m = tangent ? dL * st[r].re + mL * st[r].im : mL * st[r].re;
-    st[r].re = (ph == 0) ? m : (ph == 2) ? -m : T(0);
-    st[r].im = (ph == 1) ? -m : (ph == 3) ? m : T(0);
-  }
-}
-
-// ---- gate application (NR register-resident arrays sharing one gate) ----------
-template <int RB, typename T, int A, int NR>
-__device__ __forceinline__ void gate_reg(cplx<T> (&st)[NR][A], cplx<T> u00, cplx<T> u01,
-                                         cplx<T> u10, cplx<T> u11) {
-#pragma unroll
-  for (int r = 0; r < A; ++r) {
-    if (r & (1 << RB)) continue;
-    const int r1 = r | (1 << RB);
-#pragma unroll
-    for (int j = 0; j < NR; ++j) {
-      const cplx<T> a0 = st[j][r], a1 = st[j][r1];
-      st[j][r] = cmul2(u00, a0, u01, a1);
-      st[j][r1] = cmul2(u10, a0, u11, a1);
-    }
-  }
-}
-
-template <typename T, int A, int NR>
-__device__ __forceinline__ void gate_lane(cplx<T> (&st)[NR][A], int lm, bool beta, cplx<T> u00,
-                                          cplx<T> u01, cplx<T> u10, cplx<T> u11) {
-  const cplx<T> cs = beta ? u11 : u00, cp = beta ? u10 : u01;
-#pragma unroll
-  for (int r = 0; r < A; ++r)
-#pragma unroll
-    for (int j = 0; j < NR; ++j) {
-      const cplx<T> p = shfl_xor_c(st[j][r], lm);
-      st[j][r] = cmul2(cs, st[j][r], cp, p);
-    }
-}
-
-template <typename T, int N, int AB, int NR>
-__device__ __forceinline__ void apply_u1(cplx<T> (&st)[NR][1 << AB], int wire, int gl, cplx<T> u00,
-                                         cplx<T> u01, cplx<T> u10, cplx<T> u11) {
-  constexpr int LB = N - AB, A = 1 << AB;
-  if (wire < LB) {
-    const int lb = LB - 1 - wire;
-    gate_lane<T, A, NR>(st, 1 << lb, (gl >> lb) & 1, u00, u01, u10, u11);
-  } else {
-    const int rb = N - 1 - wire;
-    if (rb == 0) gate_reg<0, T, A, NR>(st, u00, u01, u10, u11);
-    if constexpr (AB > 1) if (rb == 1) gate_reg<1, T, A, NR>(st, u00, u01, u10, u11);
-    if constexpr (AB > 2) if (rb == 2) gate_reg<2, T, A, NR>(st, u00, u01, u10, u11);
-    if constexpr (AB > 3) if (rb == 3) gate_reg<3, T, A, NR>(st, u00, u01, u10, u11);
-    if constexpr (AB > 4) if (rb == 4) gate_reg<4, T, A, NR>(st, u00, u01, u10, u11);
-  }
-}
-
-// new[b] = old[table[b]] through the warp's shared buffer; every lane moves
-// its own state's A amplitudes (lane-fastest layout: conflict-free writes)
-template <typename T, int A, int G, int NR>
-__device__ __forceinline__ void permute(cplx<T> (&st)[NR][A], const uint16_t* tab, cplx<T>* buf,
-                                        int gl, int lane_hi) {
-  constexpr int W = 32 / G;  // lanes sharing one gl
-#pragma unroll
-  for (int j = 0; j < NR; ++j) {
-    cplx<T>* bj = buf + j * 32 * A;
-#pragma unroll
-    for (int r = 0; r < A; ++r) bj[(r * G + gl) * W + lane_hi] = st[j][r];
-  }
-  __syncwarp();
-#pragma unroll
-  for (int r = 0; r < A; ++r) {
-    const int src = tab[r * G + gl] * W + lane_hi;
-#pragma unroll
-    for (int j = 0; j < NR; ++j) st[j][r] = buf[j * 32 * A + src];
-  }
-  __syncwarp();
-}
-
-template <typename T>
-__device__ __forceinline__ void atomic_max_abs(unsigned long long* dst, T v) {
-  atomicMax(dst, (unsigned long long)__double_as_longlong((double)v));
-}
-
-// loads a, theta, cos/sin(theta/2), S', S'' and the lane's own tangent row
-template <typename T, int N>
-__device__ __forceinline__ void load_point(int scale, const T* __restrict__ act,
-                                           const T* __restrict__ act_tan, int64_t R, int64_t s,
-                                           bool valid, int k_own, T (&c)[N], T (&sn)[N],
-                                           T (&dth)[N], T (&s1)[N], T (&s2)[N], T& amax) {
-#pragma unroll
-  for (int q = 0; q < N; ++q) {
-    T a = valid ? act[s * N + q] : T(0);
-    amax = fmax(amax, fabs(a));
-    a = fmin(fmax(a, T(-1)), T(1));
-    T th;
-    scale_fn<T>(scale, a, th, s1[q], s2[q]);
-    sincos_(th * T(0.5), &sn[q], &c[q]);
-    dth[q] = (valid && k_own >= 0) ? s1[q] * act_tan[((int64_t)k_own * R + s) * N + q] : T(0);
-  }
-}
 
 // ---- K1: forward + tangents ---------------------------------------------------------
 template <typename T, int N, int NSL>
@@ -378,12 +136,6 @@ pqc_forward_kernel(PlanDev plan, const __grid_constant__ StepTable steps, int sc
 }
 
 // ---- K2: adjoint backward -------------------------------------------------------------
-template <typename T>
-__device__ __forceinline__ T warp_sum(T v) {
-#pragma unroll
-  for (int m = 16; m >= 1; m >>= 1) v += __shfl_xor_sync(0xffffffffu, v, m);
-  return v;
-}
 
 template <typename T, int N>
 __global__ void __launch_bounds__(kThreads)
@@ -647,13 +399,11 @@ __global__ void pqc_reduce_partials(const double* __restrict__ partial, int bloc
   tot[i] = v;
 }
 
-// gate-space gradients -> parameter slots
-template <typename T, int AB, int G>
-__global__ void pqc_param_grads(PlanDev p, const T* __restrict__ qp, const double* __restrict__ tot,
-                                T* __restrict__ g_qp) {
-  const int D = 1 << p.n;
-  const double* accP = tot + 8 * p.n_u1;
-  for (int i = threadIdx.x; i < p.n_u1; i += blockDim.x) {
+// gate-space gradients -> parameter slots of the u1 steps
+template <typename T>
+__global__ void pqc_u1_grads(PlanDev p, const T* __restrict__ qp, const double* __restrict__ tot,
+                             T* __restrict__ g_qp) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < p.n_u1; i += gridDim.x * blockDim.x) {
     const int kind = p.u1[i * 4];
     double th[3] = {0, 0, 0};
     const int ns = u1_nslots(kind);
@@ -683,13 +433,22 @@ __global__ void pqc_param_grads(PlanDev p, const T* __restrict__ qp, const doubl
       g_qp[p.u1[i * 4 + 1 + j]] = T(g);
     }
   }
+}
+
+// ... and of the CRZ-mesh phase steps (accumulators stored at lay(b))
+template <typename T>
+__global__ void pqc_phase_grads(PlanDev p, int ab, const double* __restrict__ tot,
+                                T* __restrict__ g_qp) {
+  const int D = 1 << p.n;
+  const int G = 1 << (p.n - ab);
+  const double* accP = tot + 8 * p.n_u1;
   for (int st = 0; st < p.n_phase; ++st) {
     for (int k = p.phase_off[st] + threadIdx.x; k < p.phase_off[st + 1]; k += blockDim.x) {
       const int c = p.pairs[3 * k], t = p.pairs[3 * k + 1], s = p.pairs[3 * k + 2];
       double g = 0.0;
       for (int b = 0; b < D; ++b) {
         const int on = (b >> (p.n - 1 - c)) & 1, tb = (b >> (p.n - 1 - t)) & 1;
-        if (on) g += (tb - 0.5) * accP[st * D + lay<AB, G>(b)];
+        if (on) g += (tb - 0.5) * accP[st * D + (b & ((1 << ab) - 1)) * G + (b >> ab)];
       }
       g_qp[s] = T(g);
     }
@@ -722,7 +481,6 @@ static int step_table(const qpinn_circuit* c, StepTable* t) {
     t->s[i] = make_int2(c->steps[3 * i] | ((c->steps[3 * i + 1] + 1) << 2), c->steps[3 * i + 2]);
   return QPINN_OK;
 }
-constexpr int kMaxBlocksPerSm = 16;  // 128-thread blocks: 2048 / 128
 
 template <typename T, int N>
 static int launch_forward(qpinn_circuit* c, int scale, int64_t R, const T* act, const T* tan,
@@ -770,18 +528,36 @@ static int launch_backward(qpinn_circuit* c, int scale, int64_t R, const T* act,
   int occ = occupancy_blocks(kern, smem);
   if (occ > kMaxBlocksPerSm) occ = kMaxBlocksPerSm;
   const int grid = grid_for(R, Gm::SPW, occ);
-  const int n_acc = 8 * p.n_u1 + Gm::D * p.n_phase;
   kern<<<grid, kThreads, smem, stream>>>(p, steps, scale, R, act, tan, qp, (const cplx<T>*)states,
                                          gz, gdz, g_act, g_tan, partial);
   QPINN_CUDA_CHECK(cudaGetLastError());
+  KArgs<T> a{scale, R, act, tan, qp, nullptr, nullptr, nullptr, nullptr, gz, gdz, g_act, g_tan,
+             g_qp, partial, tot, stream, nullptr};
+  return pqc_finish_grads<T>(c, grid, &a);
+}
+
+int pqc_grid(int64_t R, int spw, int occ) { return grid_for(R, spw, occ); }
+
+// fixed-order grid reduction of the block partials, then gate-space -> slots
+template <typename T>
+int pqc_finish_grads(const qpinn_circuit* c, int grid, const KArgs<T>* a) {
+  const PlanDev& p = c->dev;
+  const int n_acc = 8 * p.n_u1 + (1 << p.n) * p.n_phase;
   if (n_acc > 0) {
-    pqc_reduce_partials<<<(n_acc + 255) / 256, 256, 0, stream>>>(partial, grid, n_acc, tot);
+    pqc_reduce_partials<<<(n_acc + 255) / 256, 256, 0, a->stream>>>(a->partial, grid, n_acc, a->tot);
     QPINN_CUDA_CHECK(cudaGetLastError());
   }
-  pqc_param_grads<T, Gm::AB, Gm::G><<<1, 256, 0, stream>>>(p, qp, tot, g_qp);
+  pqc_u1_grads<T><<<1, 256, 0, a->stream>>>(p, a->qp, a->tot, a->g_qp);
   QPINN_CUDA_CHECK(cudaGetLastError());
+  if (p.n_phase) {
+    const int ab = c->n <= 4 ? c->n : (c->n - 3 > 4 ? c->n - 3 : 4);  // Geo::AB
+    pqc_phase_grads<T><<<1, 256, 0, a->stream>>>(p, ab, a->tot, a->g_qp);
+    QPINN_CUDA_CHECK(cudaGetLastError());
+  }
   return QPINN_OK;
 }
+template int pqc_finish_grads<float>(const qpinn_circuit*, int, const KArgs<float>*);
+template int pqc_finish_grads<double>(const qpinn_circuit*, int, const KArgs<double>*);
 
 // runtime n -> template instantiation
 #define QPINN_DISPATCH_N(MAXN, N_RT, CALL)                                         \
@@ -804,12 +580,26 @@ static size_t n_acc_of(const qpinn_circuit* c) {
 static size_t partial_bytes(const qpinn_circuit* c) {
   return align_up(sizeof(double) * n_acc_of(c) * (size_t)num_sms() * kMaxBlocksPerSm, 256);
 }
+static size_t tables_bytes_bound(const qpinn_circuit* c) {  // any dtype
+  const size_t D = (size_t)1 << c->n;
+  return align_up(16 * (4 * (size_t)c->n_u1 + D * c->n_phase) + 4 * D * c->n_perm + 1024, 256);
+}
 
 }  // namespace qpinn
 
 using namespace qpinn;
 
 extern "C" {
+
+int qpinn_circuit_set_kernel_variant(qpinn_circuit* c, int variant) {
+  if (!c || variant < 0 || variant > 1) return fail(QPINN_ERR_CONFIG, "bad kernel variant");
+  c->variant = variant;
+  return QPINN_OK;
+}
+
+int qpinn_circuit_specialized(const qpinn_circuit* c) {
+  return c && layer_entangler(c) >= 0 ? 1 : 0;
+}
 
 int qpinn_pqc_max_qubits(int dtype) {
   return dtype == QPINN_F64 ? max_qubits<double>() : max_qubits<float>();
@@ -819,7 +609,8 @@ size_t qpinn_pqc_workspace_bytes(const qpinn_circuit* c, int dtype, int64_t rows
   (void)rows;
   if (!c) return 0;
   if (c->n > qpinn_pqc_max_qubits(dtype)) return 256;
-  return 256 + partial_bytes(c) + align_up(sizeof(double) * n_acc_of(c), 256);
+  return 256 + partial_bytes(c) + align_up(sizeof(double) * n_acc_of(c), 256) +
+         tables_bytes_bound(c);
 }
 
 size_t qpinn_pqc_state_bytes(const qpinn_circuit* c, int dtype, int64_t rows) {
@@ -842,7 +633,8 @@ int qpinn_pqc_forward(const qpinn_circuit* cc, int dtype, int scale, int64_t row
                       void* dz, void* states, void* workspace, size_t workspace_bytes,
                       void* stream) {
   qpinn_circuit* c = const_cast<qpinn_circuit*>(cc);
-  int rc = check_common(c, dtype, scale, rows, workspace_bytes, 256);
+  int rc = check_common(c, dtype, scale, rows, workspace_bytes,
+                        qpinn_pqc_workspace_bytes(c, dtype, rows));
   if (rc) return rc;
   if ((act_tan == nullptr) != (dz == nullptr))
     return fail(QPINN_ERR_CONFIG, "act_tan and dz must both be given or both be NULL");
@@ -853,7 +645,23 @@ int qpinn_pqc_forward(const qpinn_circuit* cc, int dtype, int scale, int64_t row
   if (rc) return rc;
   cudaStream_t st = (cudaStream_t)stream;
   auto* maxabs = (unsigned long long*)workspace;  // running max, reset by domain_check
+  unsigned char* tables = (unsigned char*)workspace + 256 + partial_bytes(c) +
+                          align_up(sizeof(double) * n_acc_of(c), 256);
   if (rows == 0) return QPINN_OK;
+  if (c->variant == 0) {  // layer-loop kernels for every standard plan
+    if (dtype == QPINN_F32) {
+      KArgs<float> a{scale, rows, (const float*)act_val, (const float*)act_tan,
+                        (const float*)qparams, (float*)z, (float*)dz, states, maxabs,
+                        nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, st, tables};
+      rc = layer_dispatch<float>(true, c, &a);
+    } else {
+      KArgs<double> a{scale, rows, (const double*)act_val, (const double*)act_tan,
+                         (const double*)qparams, (double*)z, (double*)dz, states, maxabs,
+                         nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, st, tables};
+      rc = layer_dispatch<double>(true, c, &a);
+    }
+    if (rc != KERNEL_NONE) return rc;
+  }
   if (dtype == QPINN_F32) {
     QPINN_DISPATCH_N(8, n, (launch_forward<float, NN>(c, scale, rows, (const float*)act_val,
                                                       (const float*)act_tan, (const float*)qparams,
@@ -886,10 +694,28 @@ int qpinn_pqc_backward(const qpinn_circuit* cc, int dtype, int scale, int64_t ro
   cudaStream_t st = (cudaStream_t)stream;
   double* partial = (double*)((char*)workspace + 256);
   double* tot = (double*)((char*)workspace + 256 + partial_bytes(c));
+  unsigned char* tables = (unsigned char*)workspace + 256 + partial_bytes(c) +
+                          align_up(sizeof(double) * n_acc_of(c), 256);
   if (rows == 0) {
     QPINN_CUDA_CHECK(cudaMemsetAsync(g_qparams, 0,
                                      (dtype == QPINN_F64 ? 8 : 4) * (size_t)c->n_params, st));
     return QPINN_OK;
+  }
+  if (c->variant == 0) {
+    if (dtype == QPINN_F32) {
+      KArgs<float> a{scale, rows, (const float*)act_val, (const float*)act_tan,
+                        (const float*)qparams, nullptr, nullptr, const_cast<void*>(states),
+                        nullptr, (const float*)g_z, (const float*)g_dz, (float*)g_act_val,
+                        (float*)g_act_tan, (float*)g_qparams, partial, tot, st, tables};
+      rc = layer_dispatch<float>(false, c, &a);
+    } else {
+      KArgs<double> a{scale, rows, (const double*)act_val, (const double*)act_tan,
+                         (const double*)qparams, nullptr, nullptr, const_cast<void*>(states),
+                         nullptr, (const double*)g_z, (const double*)g_dz, (double*)g_act_val,
+                         (double*)g_act_tan, (double*)g_qparams, partial, tot, st, tables};
+      rc = layer_dispatch<double>(false, c, &a);
+    }
+    if (rc != KERNEL_NONE) return rc;
   }
   if (dtype == QPINN_F32) {
     QPINN_DISPATCH_N(8, n, (launch_backward<float, NN>(

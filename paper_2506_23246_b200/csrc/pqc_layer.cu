@@ -1,0 +1,541 @@
+// Layer-loop K1 / K2: the production PQC kernels for every ansatz.
+//
+// All six ansatze of build_circuit (ansatz.py:178-204) have the same layer
+// shape after fusion (ansatz.py:117-156): one single-qubit step (Rot, RX or
+// the fused RX.RZ) on each wire 0..n-1 in order, then at most one entangler
+// step, a CNOT-run permutation (basic, strongly, cross_mesh_cnot) or a CRZ-mesh
+// phase diagonal (cross_mesh, cross_mesh_2rot).  These kernels loop over the
+// layers at run time and unroll the wires at compile time: the wire ->
+// lane/register mapping, shuffle masks and register pairings are constants,
+// there is no per-gate dispatch and the loop-carried state only has to be
+// re-homed once per layer.  The body stays ~20 KB of SASS, inside the L1.5
+// instruction cache (a fully unrolled circuit does not: warps then stall on
+// instruction fetch).  Numerics, lane geometry, the K1 -> K2 state hand-off
+// layout and the deterministic reductions are those of the generic kernels
+// in pqc.cu, which remain the cross-check (kernel variant 1).
+#include "pqc_layer.h"
+
+namespace qpinn {
+
+// ---- single-qubit step on compile-time wire Q ---------------------------------------
+template <typename T, int N, int Q, int NR>
+__device__ __forceinline__ void gate_fwd(cplx<T> (&st)[NR][Geo<T, N, 4>::A], const cplx<T>* U,
+                                         int gl) {
+  using Gm = Geo<T, N, 4>;
+  constexpr int AB = Gm::AB, A = Gm::A, LB = Gm::LB;
+  const cplx<T> u00 = U[0], u01 = U[1], u10 = U[2], u11 = U[3];
+  if constexpr (Q < LB) {
+    constexpr int lb = LB - 1 - Q;
+    gate_lane<T, A, NR>(st, 1 << lb, (gl >> lb) & 1, u00, u01, u10, u11);
+  } else {
+    gate_reg<N - 1 - Q, T, A, NR>(st, u00, u01, u10, u11);
+  }
+  (void)AB;
+}
+
+// reverse step on wire Q: un-compute x, propagate the adjoint a (both by U^dagger)
+// and accumulate the post-gate outer product M'_ij = sum conj(a_i) x_j
+template <typename T, int N, int Q>
+__device__ __forceinline__ void gate_bwd(cplx<T> (&x)[Geo<T, N, 4>::A],
+                                         cplx<T> (&a)[Geo<T, N, 4>::A], const cplx<T>* U,
+                                         T* __restrict__ acc, int gl, int lane) {
+  using Gm = Geo<T, N, 4>;
+  constexpr int A = Gm::A, LB = Gm::LB;
+  const cplx<T> h00 = {U[0].re, -U[0].im}, h01 = {U[2].re, -U[2].im};
+  const cplx<T> h10 = {U[1].re, -U[1].im}, h11 = {U[3].re, -U[3].im};
+  T m[8] = {T(0), T(0), T(0), T(0), T(0), T(0), T(0), T(0)};
+  if constexpr (Q < LB) {
+    constexpr int lm = 1 << (LB - 1 - Q);
+    const bool beta = gl & lm;
+    const cplx<T> cs = beta ? h11 : h00, cp = beta ? h10 : h01;
+    T ms_re = 0, ms_im = 0, mc_re = 0, mc_im = 0;
+#pragma unroll
+    for (int r = 0; r < A; ++r) {
+      const cplx<T> xs = x[r], as = a[r];
+      const cplx<T> xp = shfl_xor_c(xs, lm), ap = shfl_xor_c(as, lm);
+      const cplx<T> t1 = cmulc(as, xs), t2 = cmulc(as, xp);
+      ms_re += t1.re; ms_im += t1.im; mc_re += t2.re; mc_im += t2.im;
+      x[r] = cmul2(cs, xs, cp, xp);
+      a[r] = cmul2(cs, as, cp, ap);
+    }
+    // own row i: beta = 0 -> M'(0,0), M'(0,1); beta = 1 -> M'(1,1), M'(1,0)
+    m[0] = beta ? T(0) : ms_re; m[1] = beta ? T(0) : ms_im;
+    m[2] = beta ? T(0) : mc_re; m[3] = beta ? T(0) : mc_im;
+    m[6] = beta ? ms_re : T(0); m[7] = beta ? ms_im : T(0);
+    m[4] = beta ? mc_re : T(0); m[5] = beta ? mc_im : T(0);
+  } else {
+    constexpr int S = 1 << (N - 1 - Q);
+#pragma unroll
+    for (int r = 0; r < A; ++r) {
+      if (r & S) continue;
+      const int r1 = r | S;
+      const cplx<T> x0 = x[r], x1 = x[r1], a0 = a[r], a1 = a[r1];
+      cplx<T> t;
+      t = cmulc(a0, x0); m[0] += t.re; m[1] += t.im;
+      t = cmulc(a0, x1); m[2] += t.re; m[3] += t.im;
+      t = cmulc(a1, x0); m[4] += t.re; m[5] += t.im;
+      t = cmulc(a1, x1); m[6] += t.re; m[7] += t.im;
+      x[r] = cmul2(h00, x0, h01, x1);
+      x[r1] = cmul2(h10, x0, h11, x1);
+      a[r] = cmul2(h00, a0, h01, a1);
+      a[r1] = cmul2(h10, a0, h11, a1);
+    }
+  }
+  const T v = warp_reduce8(m, lane);
+  if ((lane & 3) == 0) acc[lane >> 2] += v;
+}
+
+// lane-wire reverse step with a run-time lane mask: one code copy serves all
+// lane wires, which keeps K2's hot loop inside the instruction cache
+template <typename T, int N>
+__device__ __forceinline__ void gate_bwd_lane(cplx<T> (&x)[Geo<T, N, 4>::A],
+                                              cplx<T> (&a)[Geo<T, N, 4>::A], const cplx<T>* U,
+                                              T* __restrict__ acc, int lm, int gl, int lane) {
+  constexpr int A = Geo<T, N, 4>::A;
+  const cplx<T> h00 = {U[0].re, -U[0].im}, h01 = {U[2].re, -U[2].im};
+  const cplx<T> h10 = {U[1].re, -U[1].im}, h11 = {U[3].re, -U[3].im};
+  const bool beta = gl & lm;
+  const cplx<T> cs = beta ? h11 : h00, cp = beta ? h10 : h01;
+  T ms_re = 0, ms_im = 0, mc_re = 0, mc_im = 0;
+#pragma unroll
+  for (int r = 0; r < A; ++r) {
+    const cplx<T> xs = x[r], as = a[r];
+    const cplx<T> xp = shfl_xor_c(xs, lm), ap = shfl_xor_c(as, lm);
+    const cplx<T> t1 = cmulc(as, xs), t2 = cmulc(as, xp);
+    ms_re += t1.re; ms_im += t1.im; mc_re += t2.re; mc_im += t2.im;
+    x[r] = cmul2(cs, xs, cp, xp);
+    a[r] = cmul2(cs, as, cp, ap);
+  }
+  T m[8];
+  m[0] = beta ? T(0) : ms_re; m[1] = beta ? T(0) : ms_im;
+  m[2] = beta ? T(0) : mc_re; m[3] = beta ? T(0) : mc_im;
+  m[6] = beta ? ms_re : T(0); m[7] = beta ? ms_im : T(0);
+  m[4] = beta ? mc_re : T(0); m[5] = beta ? mc_im : T(0);
+  const T v = warp_reduce8(m, lane);
+  if ((lane & 3) == 0) acc[lane >> 2] += v;
+}
+
+// rotate the register index right by one bit: new[r] = old[rotl(r)]; after
+// AB rotations the layout is back to the original
+template <typename T, int AB>
+__device__ __forceinline__ void rotate_regs(cplx<T> (&v)[1 << AB]) {
+  constexpr int A = 1 << AB;
+  cplx<T> t[A];
+#pragma unroll
+  for (int r = 0; r < A; ++r) t[r] = v[((r << 1) | (r >> (AB - 1))) & (A - 1)];
+#pragma unroll
+  for (int r = 0; r < A; ++r) v[r] = t[r];
+}
+
+// new[r] = old[rotr(r)] (inverse of rotate_regs)
+template <typename T, int AB>
+__device__ __forceinline__ void rotate_regs_left(cplx<T> (&v)[1 << AB]) {
+  constexpr int A = 1 << AB;
+  cplx<T> t[A];
+#pragma unroll
+  for (int r = 0; r < A; ++r) t[r] = v[((r >> 1) | ((r & 1) << (AB - 1))) & (A - 1)];
+#pragma unroll
+  for (int r = 0; r < A; ++r) v[r] = t[r];
+}
+
+template <int I, typename F>  // I, I-1, ..., 0
+__device__ __forceinline__ void static_for_rev(F&& f) {
+  if constexpr (I >= 0) {
+    f(std::integral_constant<int, I>{});
+    static_for_rev<I - 1>(f);
+  }
+}
+
+// ---- K1 -----------------------------------------------------------------------------------
+template <typename T, int N, int NSL, int ENT>
+__global__ void __launch_bounds__(kThreads)
+pqc_forward_layer(PlanDev plan, const unsigned char* __restrict__ tables, int n_layers, int scale,
+                  int64_t R, const T* __restrict__ act, const T* __restrict__ act_tan,
+                  const T* __restrict__ qp, T* __restrict__ z,
+                  T* __restrict__ dz, cplx<T>* __restrict__ states,
+                  unsigned long long* __restrict__ maxabs) {
+  using Gm = Geo<T, N, NSL>;
+  constexpr int AB = Gm::AB, A = Gm::A, LB = Gm::LB, G = Gm::G, LPP = Gm::LPP, SPW = Gm::SPW,
+                D = Gm::D;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int warps = blockDim.x >> 5;
+  Smem<T> sm;
+  smem_layout<T, N, AB>(plan, warps, false, &sm, smem_raw);
+  copy_tables<T>(tables, table_bytes<T, N>(plan, false), smem_raw, sm.acc, 0);
+  __syncthreads();
+
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int pw = lane / LPP, sidx = (lane / G) % NSL, gl = lane & (G - 1);
+  const int lane_hi = lane >> LB;
+  const int psi_lane = pw * LPP + gl;
+  cplx<T>* buf = sm.buf + warp * 32 * A;
+  T amax = T(0);
+  const int64_t per_block = (int64_t)warps * SPW;
+  const int64_t stride = (int64_t)gridDim.x * per_block;
+  for (int64_t base = (int64_t)blockIdx.x * per_block; base < R; base += stride) {
+    const int64_t s = base + warp * SPW + pw;
+    const bool valid = s < R;
+    T c[N], sn[N], dth[N], s1[N], s2[N];
+    load_point_fast<T, N>(scale, act, act_tan, R, s, valid, sidx - 1, c, sn, dth, s1, s2, amax);
+    cplx<T> st[1][A];
+    embed<T, N, AB>(c, sn, dth, sidx > 0, gl, st[0]);
+    for (int l = 0; l < n_layers; ++l) {
+      const cplx<T>* Ul = sm.U + 4 * N * l;
+      for (int q = 0; q < LB; ++q) {  // lane wires, one shared copy
+        const int lb = LB - 1 - q;
+        const cplx<T>* U = Ul + 4 * q;
+        gate_lane<T, A, 1>(st, 1 << lb, (gl >> lb) & 1, U[0], U[1], U[2], U[3]);
+      }
+      // register wires LB .. N-1: bit (AB-1) .. 0; rotate left so each wire's
+      // bit arrives at position AB-1 of one shared gate copy
+      for (int i = 0; i < AB; ++i) {
+        const cplx<T>* U = Ul + 4 * (LB + i);
+        gate_reg<AB - 1, T, A, 1>(st, U[0], U[1], U[2], U[3]);
+        if constexpr (AB > 1) rotate_regs_left<T, AB>(st[0]);
+      }
+      if constexpr (ENT == ENT_PERM) {
+        permute<T, A, G, 1>(st, sm.pt + l * D, buf, gl, lane_hi);
+      } else if constexpr (ENT == ENT_PHASE) {
+        const cplx<T>* ph = sm.ph + l * D;
+#pragma unroll
+        for (int r = 0; r < A; ++r) st[0][r] = cmul(st[0][r], ph[r * G + gl]);
+      }
+    }
+    if (NSL == 4 && states != nullptr && valid) {  // hand-off for K2
+      cplx<T>* sp = states + s * (4 * D) + sidx * D;
+#pragma unroll
+      for (int r = 0; r < A; ++r) sp[r * G + gl] = st[0][r];
+    }
+    T out[N], tot = T(0);
+#pragma unroll
+    for (int q = 0; q < N; ++q) out[q] = T(0);
+#pragma unroll
+    for (int r = 0; r < A; ++r) {
+      T v;
+      if constexpr (NSL == 4) {
+        const cplx<T> p = {__shfl_sync(0xffffffffu, st[0][r].re, psi_lane),
+                           __shfl_sync(0xffffffffu, st[0][r].im, psi_lane)};
+        v = sidx == 0 ? p.re * p.re + p.im * p.im
+                      : T(2) * (p.re * st[0][r].re + p.im * st[0][r].im);
+      } else {
+        v = st[0][r].re * st[0][r].re + st[0][r].im * st[0][r].im;
+      }
+      tot += v;
+#pragma unroll
+      for (int qi = 0; qi < AB; ++qi) {
+        if ((r >> (AB - 1 - qi)) & 1) out[LB + qi] -= v;
+        else out[LB + qi] += v;
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < LB; ++q) out[q] = ((gl >> (LB - 1 - q)) & 1) ? -tot : tot;
+#pragma unroll
+    for (int m = 1; m < G; m <<= 1)
+#pragma unroll
+      for (int q = 0; q < N; ++q) out[q] += __shfl_xor_sync(0xffffffffu, out[q], m);
+    if (valid) {
+#pragma unroll
+      for (int q = 0; q < N; ++q) {
+        if ((q % G) != gl) continue;
+        if (sidx == 0) z[s * N + q] = out[q];
+        else dz[((int64_t)(sidx - 1) * R + s) * N + q] = out[q];
+      }
+    }
+  }
+#pragma unroll
+  for (int m = 16; m >= 1; m >>= 1) amax = fmax(amax, __shfl_xor_sync(0xffffffffu, amax, m));
+  if (lane == 0 && maxabs) atomic_max_abs(maxabs, amax);
+}
+
+// ---- K2 -----------------------------------------------------------------------------------
+template <typename T, int N, int ENT>
+__global__ void __launch_bounds__(kThreads)
+pqc_backward_layer(PlanDev plan, const unsigned char* __restrict__ tables, int n_layers,
+                   int scale, int64_t R, const T* __restrict__ act,
+                   const T* __restrict__ act_tan, const T* __restrict__ qp,
+                   const cplx<T>* __restrict__ states, const T* __restrict__ gz,
+                   const T* __restrict__ gdz, T* __restrict__ g_act, T* __restrict__ g_act_tan,
+                   double* __restrict__ partial) {
+  using Gm = Geo<T, N, 4>;
+  constexpr int AB = Gm::AB, A = Gm::A, LB = Gm::LB, G = Gm::G, LPP = Gm::LPP, SPW = Gm::SPW,
+                D = Gm::D;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int warps = blockDim.x >> 5;
+  Smem<T> sm;
+  smem_layout<T, N, AB>(plan, warps, true, &sm, smem_raw);
+  copy_tables<T>(tables, table_bytes<T, N>(plan, true), smem_raw, sm.acc,
+                 (size_t)warps * (8 * plan.n_u1 + (size_t)D * plan.n_phase));
+  __syncthreads();
+
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int pw = lane / LPP, sidx = (lane / G) % 4, gl = lane & (G - 1);
+  const int lane_hi = lane >> LB;
+  const int psi_lane = pw * LPP + gl;
+  cplx<T>* buf = sm.buf + warp * 2 * 32 * A;
+  const int n_acc = 8 * plan.n_u1 + D * plan.n_phase;
+  T* accU = sm.acc + (size_t)warp * n_acc;
+  T* accP = accU + 8 * plan.n_u1;
+  const int64_t per_block = (int64_t)warps * SPW;
+  const int64_t stride = (int64_t)gridDim.x * per_block;
+  for (int64_t base = (int64_t)blockIdx.x * per_block; base < R; base += stride) {
+    const int64_t s = base + warp * SPW + pw;
+    const bool valid = s < R;
+    T c[N], sn[N], dth[N], s1v[N], s2v[N], amax_unused = T(0);
+    load_point_fast<T, N>(scale, act, act_tan, R, s, valid, sidx - 1, c, sn, dth, s1v, s2v,
+                          amax_unused);
+    cplx<T> xa[2][A];  // [0] this lane's state, [1] its adjoint
+    {
+      const cplx<T>* sp = states + (valid ? s : 0) * (4 * D) + sidx * D;
+#pragma unroll
+      for (int r = 0; r < A; ++r) xa[0][r] = valid ? sp[r * G + gl] : cplx<T>{T(0), T(0)};
+    }
+    // adjoint seeds: lambda = 2 w psi + 2 sum_k v_k dpsi_k, mu_k = 2 v_k psi
+    T gsel[N];
+#pragma unroll
+    for (int q = 0; q < N; ++q)
+      gsel[q] = !valid ? T(0) : sidx == 0 ? gz[s * N + q]
+                                          : gdz[((int64_t)(sidx - 1) * R + s) * N + q];
+    T wl = T(0);
+#pragma unroll
+    for (int q = 0; q < LB; ++q) wl += ((gl >> (LB - 1 - q)) & 1) ? -gsel[q] : gsel[q];
+#pragma unroll
+    for (int r = 0; r < A; ++r) {
+      T w = wl;
+#pragma unroll
+      for (int qi = 0; qi < AB; ++qi)
+        w += ((r >> (AB - 1 - qi)) & 1) ? -gsel[LB + qi] : gsel[LB + qi];
+      w *= T(2);
+      const cplx<T> p = {__shfl_sync(0xffffffffu, xa[0][r].re, psi_lane),
+                         __shfl_sync(0xffffffffu, xa[0][r].im, psi_lane)};
+      cplx<T> t = {w * xa[0][r].re, w * xa[0][r].im};
+#pragma unroll
+      for (int m = G; m < 4 * G; m <<= 1) {
+        t.re += __shfl_xor_sync(0xffffffffu, t.re, m);
+        t.im += __shfl_xor_sync(0xffffffffu, t.im, m);
+      }
+      xa[1][r] = sidx == 0 ? t : cplx<T>{w * p.re, w * p.im};
+    }
+    // reverse sweep over layers
+    for (int l = n_layers - 1; l >= 0; --l) {
+      if constexpr (ENT == ENT_PERM) {
+        permute<T, A, G, 2>(xa, sm.pti + l * D, buf, gl, lane_hi);
+      } else if constexpr (ENT == ENT_PHASE) {
+        const cplx<T>* ph = sm.ph + l * D;
+        T* acc = accP + l * D;
+#pragma unroll
+        for (int r = 0; r < A; ++r) {
+          T pv = xa[1][r].im * xa[0][r].re - xa[1][r].re * xa[0][r].im;
+#pragma unroll
+          for (int mk = G; mk < 32; mk <<= 1) pv += __shfl_xor_sync(0xffffffffu, pv, mk);
+          if (lane_hi == 0) acc[r * G + gl] += pv;
+          const cplx<T> e = {ph[r * G + gl].re, -ph[r * G + gl].im};
+          xa[0][r] = cmul(xa[0][r], e);
+          xa[1][r] = cmul(xa[1][r], e);
+        }
+      }
+      const cplx<T>* Ul = sm.U + 4 * N * l;
+      T* accl = accU + 8 * N * l;
+      // register wires N-1 .. LB: one register-bit-0 gate copy, rotating the
+      // register index so the next wire's bit comes to position 0
+      for (int i = 0; i < AB; ++i) {
+        const int q = N - 1 - i;
+        gate_bwd<T, N, N - 1>(xa[0], xa[1], Ul + 4 * q, accl + 8 * q, gl, lane);
+        if constexpr (AB > 1) {
+          rotate_regs<T, AB>(xa[0]);
+          rotate_regs<T, AB>(xa[1]);
+        }
+      }
+      for (int q = LB - 1; q >= 0; --q)  // lane wires, one shared copy
+        gate_bwd_lane<T, N>(xa[0], xa[1], Ul + 4 * q, accl + 8 * q, 1 << (LB - 1 - q), gl, lane);
+    }
+    // embedding gradient: xa[1] = phibar (s = 0) or mu_k (s = k+1)
+    embed<T, N, AB>(c, sn, dth, false, gl, xa[0]);
+    cplx<T> rho[A];
+#pragma unroll
+    for (int r = 0; r < A; ++r) rho[r] = {T(0), T(0)};
+#pragma unroll
+    for (int q = 0; q < LB; ++q) {
+      const int lm = 1 << (LB - 1 - q);
+#pragma unroll
+      for (int r = 0; r < A; ++r) {
+        const cplx<T> p = shfl_xor_c(xa[1][r], lm);
+        rho[r].re += dth[q] * p.re;
+        rho[r].im += dth[q] * p.im;
+      }
+    }
+#pragma unroll
+    for (int qi = 0; qi < AB; ++qi) {
+      const int Sm = 1 << (AB - 1 - qi);
+#pragma unroll
+      for (int r = 0; r < A; ++r) {
+        rho[r].re += dth[LB + qi] * xa[1][r ^ Sm].re;
+        rho[r].im += dth[LB + qi] * xa[1][r ^ Sm].im;
+      }
+    }
+    T gt[N], gd[N];
+#pragma unroll
+    for (int q = 0; q < N; ++q) {
+      gt[q] = T(0);
+      gd[q] = T(0);
+#pragma unroll
+      for (int r = 0; r < A; ++r) {
+        cplx<T> y;
+        if (q < LB) y = shfl_xor_c(xa[0][r], 1 << (LB - 1 - q));
+        else y = xa[0][r ^ (1 << (N - 1 - q))];
+        const T half = T(0.5) * (xa[1][r].re * y.im - xa[1][r].im * y.re);
+        if (sidx == 0) gt[q] += half;
+        else {
+          gt[q] -= T(0.25) * (rho[r].re * y.re + rho[r].im * y.im);
+          gd[q] += half;
+        }
+      }
+    }
+#pragma unroll
+    for (int m = 1; m < G; m <<= 1)
+#pragma unroll
+      for (int q = 0; q < N; ++q) {
+        gt[q] += __shfl_xor_sync(0xffffffffu, gt[q], m);
+        gd[q] += __shfl_xor_sync(0xffffffffu, gd[q], m);
+      }
+#pragma unroll
+    for (int m = G; m < 4 * G; m <<= 1)
+#pragma unroll
+      for (int q = 0; q < N; ++q) gt[q] += __shfl_xor_sync(0xffffffffu, gt[q], m);
+    T gk[3][N];
+#pragma unroll
+    for (int k = 0; k < 3; ++k)
+#pragma unroll
+      for (int q = 0; q < N; ++q)
+        gk[k][q] = __shfl_sync(0xffffffffu, gd[q], pw * LPP + (k + 1) * G + gl);
+    if (valid) {
+#pragma unroll
+      for (int q = 0; q < N; ++q) {
+        if ((q % G) != gl) continue;
+        if (sidx == 0) {
+          T ga = gt[q] * s1v[q];
+#pragma unroll
+          for (int k = 0; k < 3; ++k)
+            ga += gk[k][q] * s2v[q] * act_tan[((int64_t)k * R + s) * N + q];
+          g_act[s * N + q] = ga;
+        } else {
+          g_act_tan[((int64_t)(sidx - 1) * R + s) * N + q] = gd[q] * s1v[q];
+        }
+      }
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < n_acc; i += blockDim.x) {
+    double v = 0.0;
+    for (int w = 0; w < warps; ++w) v += (double)sm.acc[(size_t)w * n_acc + i];
+    partial[(size_t)blockIdx.x * n_acc + i] = v;
+  }
+}
+
+// ---- launch ---------------------------------------------------------------------------------
+int layer_entangler(const qpinn_circuit* c) {
+  // the plan must be [n u1 on wires 0..n-1, entangler?] x L (ansatz.py:178-204)
+  const int n = c->n, L = c->L;
+  const int n_steps = (int)c->steps.size() / 3;
+  int ent = ENT_NONE;
+  if (c->n_perm) ent = ENT_PERM;
+  if (c->n_phase) ent = ENT_PHASE;
+  if (c->n_perm && c->n_phase) return -1;
+  const int per = n + (ent == ENT_NONE ? 0 : 1);
+  if (c->n_u1 != n * L || n_steps != per * L) return -1;
+  for (int l = 0; l < L; ++l) {
+    for (int q = 0; q < n; ++q) {
+      const int* s = &c->steps[3 * (l * per + q)];
+      if (s[0] != STEP_U1 || s[1] != q || s[2] != l * n + q) return -1;
+    }
+    if (ent != ENT_NONE) {
+      const int* s = &c->steps[3 * (l * per + n)];
+      if (s[0] != (ent == ENT_PERM ? STEP_PERM : STEP_PHASE) || s[2] != l) return -1;
+    }
+  }
+  return ent;
+}
+
+template <typename T, int N>
+static int prepare(const qpinn_circuit* c, const KArgs<T>* a) {
+  pqc_prepare_tables<T, N><<<4, 128, 0, a->stream>>>(c->dev, a->qp, a->tables);
+  QPINN_CUDA_CHECK(cudaGetLastError());
+  return QPINN_OK;
+}
+
+template <typename T, int N, int ENT>
+static int layer_fwd(const qpinn_circuit* c, const KArgs<T>* a) {
+  const PlanDev& p = c->dev;
+  if (int rc = prepare<T, N>(c, a)) return rc;
+  const size_t smem = smem_layout<T, N, Geo<T, N, 4>::AB>(p, kThreads / 32, false, nullptr, nullptr);
+  if (smem > 227 * 1024) return fail(QPINN_ERR_CAPACITY, "PQC plan tables exceed shared memory");
+  auto go = [&](auto kern, int spw) -> int {
+    QPINN_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)smem));
+    int occ = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kThreads, smem);
+    const int grid = pqc_grid(a->R, spw, occ > 0 ? occ : 1);
+    kern<<<grid, kThreads, smem, a->stream>>>(p, a->tables, c->L, a->scale, a->R, a->act, a->tan,
+                                              a->qp, a->z, a->dz, (cplx<T>*)a->states, a->maxabs);
+    QPINN_CUDA_CHECK(cudaGetLastError());
+    return QPINN_OK;
+  };
+  if (a->tan) return go(pqc_forward_layer<T, N, 4, ENT>, Geo<T, N, 4>::SPW);
+  return go(pqc_forward_layer<T, N, 1, ENT>, Geo<T, N, 1>::SPW);
+}
+
+template <typename T, int N, int ENT>
+static int layer_bwd(const qpinn_circuit* c, const KArgs<T>* a) {
+  using Gm = Geo<T, N, 4>;
+  const PlanDev& p = c->dev;
+  const size_t smem = smem_layout<T, N, Gm::AB>(p, kThreads / 32, true, nullptr, nullptr);
+  if (smem > 227 * 1024) return fail(QPINN_ERR_CAPACITY, "PQC plan tables exceed shared memory");
+  if (int rc = prepare<T, N>(c, a)) return rc;
+  auto kern = pqc_backward_layer<T, N, ENT>;
+  QPINN_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int occ = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kThreads, smem);
+  if (occ > kMaxBlocksPerSm) occ = kMaxBlocksPerSm;
+  const int grid = pqc_grid(a->R, Gm::SPW, occ > 0 ? occ : 1);
+  kern<<<grid, kThreads, smem, a->stream>>>(p, a->tables, c->L, a->scale, a->R, a->act, a->tan, a->qp,
+                                            (const cplx<T>*)a->states, a->gz, a->gdz, a->g_act,
+                                            a->g_tan, a->partial);
+  QPINN_CUDA_CHECK(cudaGetLastError());
+  return pqc_finish_grads<T>(c, grid, a);
+}
+
+template <typename T, int N>
+static int layer_n(bool fwd, int ent, const qpinn_circuit* c, const KArgs<T>* a) {
+  if (fwd) {
+    if (ent == ENT_PERM) return layer_fwd<T, N, ENT_PERM>(c, a);
+    if (ent == ENT_PHASE) return layer_fwd<T, N, ENT_PHASE>(c, a);
+    return layer_fwd<T, N, ENT_NONE>(c, a);
+  }
+  if (!a->states) return KERNEL_NONE;  // no hand-off: the generic kernel replays the circuit
+  if (ent == ENT_PERM) return layer_bwd<T, N, ENT_PERM>(c, a);
+  if (ent == ENT_PHASE) return layer_bwd<T, N, ENT_PHASE>(c, a);
+  return layer_bwd<T, N, ENT_NONE>(c, a);
+}
+
+template <typename T>
+int layer_dispatch(bool fwd, const qpinn_circuit* c, const KArgs<T>* a) {
+  const int ent = layer_entangler(c);
+  if (ent < 0) return KERNEL_NONE;
+  switch (c->n) {
+    case 1: return layer_n<T, 1>(fwd, ent, c, a);
+    case 2: return layer_n<T, 2>(fwd, ent, c, a);
+    case 3: return layer_n<T, 3>(fwd, ent, c, a);
+    case 4: return layer_n<T, 4>(fwd, ent, c, a);
+    case 5: return layer_n<T, 5>(fwd, ent, c, a);
+    case 6: return layer_n<T, 6>(fwd, ent, c, a);
+    case 7: return layer_n<T, 7>(fwd, ent, c, a);
+    case 8:
+      if constexpr (sizeof(T) == 4) return layer_n<T, 8>(fwd, ent, c, a);
+      return KERNEL_NONE;
+    default: return KERNEL_NONE;
+  }
+}
+
+template int layer_dispatch<float>(bool, const qpinn_circuit*, const KArgs<float>*);
+template int layer_dispatch<double>(bool, const qpinn_circuit*, const KArgs<double>*);
+
+}  // namespace qpinn

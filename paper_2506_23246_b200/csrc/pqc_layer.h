@@ -1,0 +1,45 @@
+// Interface between the PQC launcher (pqc.cu) and the layer-loop kernels
+// (pqc_layer.cu).
+#pragma once
+#include "pqc_common.cuh"
+
+namespace qpinn {
+
+constexpr int KERNEL_NONE = -1;
+constexpr int ENT_NONE = 0, ENT_PERM = 1, ENT_PHASE = 2;
+constexpr int kMaxBlocksPerSm = 16;  // 128-thread blocks: 2048 / 128
+
+template <typename T>
+struct KArgs {
+  int scale;
+  int64_t R;
+  const T* act;
+  const T* tan;
+  const T* qp;
+  T* z;
+  T* dz;
+  void* states;
+  unsigned long long* maxabs;
+  const T* gz;
+  const T* gdz;
+  T* g_act;
+  T* g_tan;
+  T* g_qp;
+  double* partial;
+  double* tot;
+  cudaStream_t stream;
+  unsigned char* tables;  // workspace region for pqc_prepare_tables
+};
+
+// QPINN_OK / error code, or KERNEL_NONE when the circuit's plan does not have
+// the uniform layer shape (the generic kernels then run).
+template <typename T>
+int layer_dispatch(bool fwd, const qpinn_circuit* c, const KArgs<T>* a);
+int layer_entangler(const qpinn_circuit* c);
+
+// provided by pqc.cu
+int pqc_grid(int64_t R, int spw, int occ);
+template <typename T>
+int pqc_finish_grads(const qpinn_circuit* c, int grid, const KArgs<T>* a);
+
+}  // namespace qpinn

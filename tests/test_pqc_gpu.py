@@ -138,3 +138,35 @@ def test_quantum_layer_forward_autograd_and_domain():
     with pytest.warns(UserWarning):
         z = quantum_layer_forward(edge, qp.detach(), c, "acos")
     assert torch.isfinite(z).all()
+
+
+@pytest.mark.parametrize("dtype", DTYPES)
+@pytest.mark.parametrize("kind", O.KINDS)
+def test_specialized_kernels_match_generic_and_oracle(kind, dtype):
+    """Compile-time specialised K1/K2 (GF(2) frame relabeling) vs the generic
+    runtime-plan kernels and the oracle, with the state hand-off."""
+    from paper_2506_23246_b200.ansatz import (build_circuit, pqc_backward_raw, pqc_forward_raw,
+                                              state_buffer)
+    rng = np.random.default_rng(11)
+    n, L, R = 7, 4, 301
+    res = {}
+    for variant in ("auto", "generic"):
+        c = build_circuit(kind, n, L)
+        assert c.specialized
+        c.set_kernel_variant(variant)
+        d = dict(a=rng.uniform(-0.9, 0.9, (R, n)), da=rng.normal(size=(3, R, n)),
+                 qp=rng.uniform(0, 2 * np.pi, c.param_count), gz=rng.normal(size=(R, n)),
+                 gdz=rng.normal(size=(3, R, n))) if not res else res["d"]
+        res["d"] = d
+        a, da, qp = cuda(d["a"], dtype), cuda(d["da"], dtype), cuda(d["qp"], dtype)
+        st = state_buffer(c, a)
+        z, dz = pqc_forward_raw(c, "acos", a, da, qp, st)
+        g = pqc_backward_raw(c, "acos", a, da, qp, cuda(d["gz"], dtype), cuda(d["gdz"], dtype), st)
+        res[variant] = (z, dz) + g
+    d = res["d"]
+    wz, wdz = O.pqc_forward(d["a"], d["da"], d["qp"], kind, "acos", L)
+    wg = O.pqc_backward(d["a"], d["da"], d["qp"], kind, "acos", L, d["gz"], d["gdz"])
+    for variant in ("auto", "generic"):
+        got = res[variant]
+        for name, x, w in zip(("z", "dz", "ga", "gda", "gq"), got, (wz, wdz) + tuple(wg)):
+            assert_close(x, w, dtype, f"{variant} {name}")
