@@ -126,6 +126,39 @@ int qpinn_pqc_backward(const qpinn_circuit* c, int dtype, int scale, int64_t row
 int qpinn_pqc_domain_check(const void* workspace, void* stream, double* max_abs,
                            int* clamped);
 
+/* ---- classical trunk with forward-mode tangents (network.py:133-147, :284-298)
+ * periodic map -> frozen RFF -> tanh hidden layers -> tanh adapter, carried as
+ * value + d/dx, d/dy, d/dt channels stacked along rows ([4, R, width]) so each
+ * layer is ONE GEMM on [4R, in] x [in, out] (tensor cores, FP32-accurate
+ * BF16x9 emulation for float32; DGEMM for float64).  Weights are read from
+ * and gradients written to the flat parameter vector at the given offsets. */
+typedef struct qpinn_trunk_desc {
+  int32_t n_hidden;      /* hidden tanh layers (3 for the hybrid, network.py:188-189) */
+  int32_t rff;           /* RFF features F; the first layer reads 2F                 */
+  int32_t hidden;        /* hidden width                                             */
+  int32_t n_out;         /* adapter width (= n_qubits)                               */
+  int64_t off_w[8];      /* flat offset of hidden layer i weights [in, out]          */
+  int64_t off_b[8];      /* flat offset of hidden layer i bias [out]                 */
+  int64_t off_adapter_w, off_adapter_b, off_tau_raw;
+  double t_domain;       /* tau = t_domain * (1 + softplus(tau_raw)) (network.py:292) */
+  const void* omega;     /* device [F, 6] frozen RFF projection (dtype)              */
+} qpinn_trunk_desc;
+
+size_t qpinn_trunk_workspace_bytes(const qpinn_trunk_desc* d, int dtype, int64_t rows);
+/* act [4, R, n_out]: a = tanh(h Wa + ba) and its x/y/t tangents (the PQC
+ * input: act_val = act, act_tan = act + R*n_out).  Saves what the backward
+ * needs in the workspace. */
+int qpinn_trunk_forward(const qpinn_trunk_desc* d, int dtype, int64_t rows, const void* x,
+                        const void* y, const void* t, const void* params, void* act,
+                        void* workspace, size_t workspace_bytes, void* stream);
+/* Given g_act = dL/d(act) [4, R, n_out] (from qpinn_pqc_backward), writes the
+ * gradients of every trunk weight, bias and tau_raw into `grad` (flat layout;
+ * overwrites those entries). */
+int qpinn_trunk_backward(const qpinn_trunk_desc* d, int dtype, int64_t rows, const void* x,
+                         const void* y, const void* t, const void* params, const void* act,
+                         const void* g_act, void* grad, void* workspace, size_t workspace_bytes,
+                         void* stream);
+
 /* ---- fused Maxwell loss (K4), physics.py:123-187, :334-460 -------------- */
 /* Static per-grid description.  The host derives every table with the same
  * numpy expressions as the reference (grid coordinates, permittivity, pulse,
@@ -163,12 +196,23 @@ size_t qpinn_loss_workspace_bytes(const qpinn_loss_spec* s, int dtype, int64_t r
  * adaptive weights `weights_dev` [5] (double, device; NULL = the pooled
  * formula) it writes the loss gradient g_out [R,3], g_dout [3,R,3] (dtype) and
  * the raw per-term sums `sums_dev` [QPINN_LOSS_NSUMS] (double; deterministic
- * fixed-order reduction). */
+ * fixed-order reduction).  See qpinn_loss_head_forward_backward for the
+ * variant with the linear head (network.py:302) fused in. */
 int qpinn_loss_forward_backward(const qpinn_loss_spec* s, int dtype, int64_t rows,
                                 const void* out, const void* dout,
                                 const double* weights_dev, void* g_out, void* g_dout,
                                 double* sums_dev, void* workspace, size_t workspace_bytes,
                                 void* stream);
+
+/* Same loss with the linear head fused in: reads the PQC output z [4, R, W]
+ * (value and x/y/t tangents, W <= 16) and the head weights w_out [W, 3],
+ * b_out [3] (dtype), and writes dL/dz [4, R, W] plus dL/dw_out, dL/db_out
+ * (into g_w_out [3W], g_b_out [3], dtype, deterministic reduction). */
+int qpinn_loss_head_forward_backward(const qpinn_loss_spec* s, int dtype, int64_t rows, int width,
+                                     const void* z, const void* w_out, const void* b_out,
+                                     const double* weights_dev, void* g_z, void* g_w_out,
+                                     void* g_b_out, double* sums_dev, void* workspace,
+                                     size_t workspace_bytes, void* stream);
 
 /* From (globally reduced) sums: breakdown_dev[10] = phys, ic, sym, energy,
  * total, bin_phys[5] (physics.py:416-426); when `weights_next_dev` is not

@@ -41,6 +41,16 @@ class LossSpec(C.Structure):
     ]
 
 
+class TrunkDesc(C.Structure):
+    """Mirror of ``qpinn_trunk_desc``."""
+    _fields_ = [
+        ("n_hidden", C.c_int32), ("rff", C.c_int32), ("hidden", C.c_int32), ("n_out", C.c_int32),
+        ("off_w", C.c_int64 * 8), ("off_b", C.c_int64 * 8),
+        ("off_adapter_w", C.c_int64), ("off_adapter_b", C.c_int64), ("off_tau_raw", C.c_int64),
+        ("t_domain", C.c_double), ("omega", C.c_void_p),
+    ]
+
+
 # (name, restype, argtypes) -- exactly the symbols of include/qpinn_b200.h
 _VP, _SZ, _I, _I64, _D = C.c_void_p, C.c_size_t, C.c_int, C.c_int64, C.c_double
 SIGNATURES = [
@@ -64,7 +74,14 @@ SIGNATURES = [
     ("qpinn_loss_workspace_bytes", _SZ, [C.POINTER(LossSpec), _I, _I64]),
     ("qpinn_loss_forward_backward", _I, [C.POINTER(LossSpec), _I, _I64, _VP, _VP, _VP, _VP,
                                          _VP, _VP, _VP, _SZ, _VP]),
+    ("qpinn_loss_head_forward_backward", _I, [C.POINTER(LossSpec), _I, _I64, _I, _VP, _VP, _VP,
+                                              _VP, _VP, _VP, _VP, _VP, _VP, _SZ, _VP]),
     ("qpinn_loss_finalize", _I, [C.POINTER(LossSpec), _VP, _VP, _I, _D, _VP, _VP, _VP]),
+    ("qpinn_trunk_workspace_bytes", _SZ, [C.POINTER(TrunkDesc), _I, _I64]),
+    ("qpinn_trunk_forward", _I, [C.POINTER(TrunkDesc), _I, _I64, _VP, _VP, _VP, _VP, _VP, _VP,
+                                 _SZ, _VP]),
+    ("qpinn_trunk_backward", _I, [C.POINTER(TrunkDesc), _I, _I64, _VP, _VP, _VP, _VP, _VP, _VP,
+                                  _VP, _VP, _SZ, _VP]),
     ("qpinn_adam_step", _I, [_I, _I64, _VP, _VP, _VP, _VP, _I64, _D, _D, _D, _D, _VP, _VP, _VP]),
 ]
 

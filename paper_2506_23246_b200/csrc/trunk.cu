@@ -1,0 +1,433 @@
+// Classical trunk with forward-mode x/y/t tangents: forward and reverse pass.
+//
+// Reference: network.py:133-147 (periodic map, frozen RFF), :284-298 (tanh
+// layers + tanh adapter on BatchedDuals, tangents riding as one stacked GEMM,
+// ops.py:282-298) and the tape's reverse pass through them.
+//
+// Activations are channel-major [4, R, width] (value, d/dx, d/dy, d/dt), so
+// every dense layer is ONE GEMM [4R, in] x [in, out] on the tensor cores.
+// float32 uses cuBLAS's FP32 emulation (BF16x9, FP32-accurate) -- a plain
+// library GEMM; float64 uses DGEMM.  Everything around the GEMMs is fused
+// here: the feature map + RFF with tangents, the dual tanh epilogue
+// (y = tanh(u0 + b), dy_k = (1 - y^2) du_k), its reverse
+// (g_u0 = g_y s - 2 y s sum_k g_dy_k du_k, g_du_k = g_dy_k s), deterministic
+// bias column sums, and the tau gradient through the learned time period.
+#include <cublas_v2.h>
+
+#include <cstdio>
+#include <cstdlib>
+#include <mutex>
+
+#include "gates.cuh"
+
+namespace qpinn {
+
+// ---- cuBLAS handle per device ---------------------------------------------------------
+struct BlasSlot {
+  cublasHandle_t h = nullptr;
+  void* ws = nullptr;
+};
+static BlasSlot g_blas[64];
+static std::mutex g_blas_mu;
+constexpr size_t kBlasWorkspace = 64ull << 20;
+
+static int blas_handle(cudaStream_t st, cublasHandle_t* out) {
+  int dev = 0;
+  QPINN_CUDA_CHECK(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(g_blas_mu);
+  BlasSlot& b = g_blas[dev & 63];
+  if (!b.h) {
+    if (cublasCreate(&b.h) != CUBLAS_STATUS_SUCCESS) return fail(QPINN_ERR_CUDA, "cublasCreate");
+    QPINN_CUDA_CHECK(cudaMalloc(&b.ws, kBlasWorkspace));
+    cublasSetWorkspace(b.h, b.ws, kBlasWorkspace);
+    cublasSetAtomicsMode(b.h, CUBLAS_ATOMICS_NOT_ALLOWED);  // deterministic reductions
+  }
+  if (cublasSetStream(b.h, st) != CUBLAS_STATUS_SUCCESS) return fail(QPINN_ERR_CUDA, "cublasSetStream");
+  *out = b.h;
+  return QPINN_OK;
+}
+
+// row-major C[M,N] = op(A) op(B) (+ beta C); op(A) is [M,K], op(B) is [K,N]
+template <typename T>
+static int gemm_rm(cublasHandle_t h, bool ta, bool tb, int64_t M, int64_t N, int64_t K, const T* A,
+                   int64_t lda, const T* B, int64_t ldb, T* C, int64_t ldc, T beta) {
+  const T alpha = T(1);
+  const cudaDataType dt = sizeof(T) == 8 ? CUDA_R_64F : CUDA_R_32F;
+  const cublasComputeType_t ct =
+      sizeof(T) == 8 ? CUBLAS_COMPUTE_64F : CUBLAS_COMPUTE_32F_EMULATED_16BFX9;
+  // column-major view: C^T[N,M] = op(B)^T op(A)^T
+  auto call = [&](cublasComputeType_t c) {
+    return cublasGemmEx(h, tb ? CUBLAS_OP_T : CUBLAS_OP_N, ta ? CUBLAS_OP_T : CUBLAS_OP_N, (int)N,
+                        (int)M, (int)K, &alpha, B, dt, (int)ldb, A, dt, (int)lda, &beta, C, dt,
+                        (int)ldc, c, CUBLAS_GEMM_DEFAULT);
+  };
+  cublasStatus_t s = call(ct);
+  if (s == CUBLAS_STATUS_NOT_SUPPORTED && sizeof(T) == 4) {
+    // shapes the BF16x9 emulation does not cover run as plain FP32 (same accuracy class)
+    static int logged = 0;
+    if (getenv("QPINN_VERBOSE") && logged++ < 16)
+      fprintf(stderr, "[qpinn] BF16x9 emulation unsupported for M=%ld N=%ld K=%ld ta=%d tb=%d: FP32\n",
+              (long)M, (long)N, (long)K, (int)ta, (int)tb);
+    s = call(CUBLAS_COMPUTE_32F_PEDANTIC);
+  }
+  if (s != CUBLAS_STATUS_SUCCESS)
+    return fail(QPINN_ERR_CUDA, std::string("cublasGemmEx: ") + cublasGetStatusString(s));
+  return QPINN_OK;
+}
+
+__device__ __forceinline__ void sincos_t(float x, float* s, float* c) { sincosf(x, s, c); }
+__device__ __forceinline__ void sincos_t(double x, double* s, double* c) { sincos(x, s, c); }
+__device__ __forceinline__ void sincospi_t(float x, float* s, float* c) { sincospif(x, s, c); }
+__device__ __forceinline__ void sincospi_t(double x, double* s, double* c) { sincospi(x, s, c); }
+
+template <typename T>
+__device__ __forceinline__ T tau_of(const T* params, int64_t off_tau, T t_dom) {
+  const T raw = params[off_tau];
+  const T sp = raw > T(20) ? raw : log1p(exp(raw));  // softplus (network.py:292-293)
+  return (T(1) + sp) * t_dom;
+}
+
+// periodic map (network.py:133-141) + RFF (network.py:144-147) with tangents
+template <typename T>
+__global__ void features_fwd(int64_t R, int F, const T* __restrict__ x, const T* __restrict__ y,
+                             const T* __restrict__ t, const T* __restrict__ omega,
+                             const T* __restrict__ params, int64_t off_tau, T t_dom,
+                             T* __restrict__ H0) {
+  const T tau = tau_of(params, off_tau, t_dom);
+  const int64_t n = R * F;
+  const int64_t W = 2 * (int64_t)F;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t p = i / F;
+    const int f = (int)(i % F);
+    T sx, cx, sy, cy, st, ct;
+    sincospi_t(x[p], &sx, &cx);  // x * 2 pi / lx, lx = 2
+    sincospi_t(y[p], &sy, &cy);
+    const T at = (t[p] * T(2.0 * kPi)) / tau;
+    sincos_t(at, &st, &ct);
+    const T w = T(2.0 * kPi) / tau;
+    const T* om = omega + 6 * f;
+    const T proj = sx * om[0] + cx * om[1] + sy * om[2] + cy * om[3] + st * om[4] + ct * om[5];
+    const T dpx = T(kPi) * cx * om[0] - T(kPi) * sx * om[1];
+    const T dpy = T(kPi) * cy * om[2] - T(kPi) * sy * om[3];
+    const T dpt = w * ct * om[4] - w * st * om[5];
+    T sp, cp;
+    sincos_t(proj, &sp, &cp);
+    H0[p * W + f] = cp;
+    H0[p * W + F + f] = sp;
+    const T dps[3] = {dpx, dpy, dpt};
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      T* Hk = H0 + (int64_t)(k + 1) * R * W + p * W;
+      Hk[f] = -sp * dps[k];
+      Hk[F + f] = cp * dps[k];
+    }
+  }
+}
+
+// dual tanh epilogue: H[0] = tanh(U[0] + b), H[k] = (1 - H[0]^2) U[k]
+template <typename T>
+__global__ void tanh_fwd(int64_t R, int N, const T* __restrict__ U, const T* __restrict__ b,
+                         T* __restrict__ H) {
+  const int64_t n = R * N;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int j = (int)(i % N);
+    const T yv = tanh(U[i] + b[j]);
+    const T s = T(1) - yv * yv;
+    H[i] = yv;
+    H[n + i] = s * U[n + i];
+    H[2 * n + i] = s * U[2 * n + i];
+    H[3 * n + i] = s * U[3 * n + i];
+  }
+}
+
+// reverse of the dual tanh: g_u0 = g_y s + sum_k g_dy_k du_k (-2 y s), g_du_k = g_dy_k s
+template <typename T>
+__global__ void tanh_bwd(int64_t R, int N, const T* __restrict__ GY, const T* __restrict__ Y,
+                         const T* __restrict__ U, T* __restrict__ GU) {
+  const int64_t n = R * N;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const T yv = Y[i];
+    const T s = T(1) - yv * yv;
+    const T g1 = GY[n + i], g2 = GY[2 * n + i], g3 = GY[3 * n + i];
+    GU[i] = GY[i] * s + (g1 * U[n + i] + g2 * U[2 * n + i] + g3 * U[3 * n + i]) * (T(-2) * yv * s);
+    GU[n + i] = g1 * s;
+    GU[2 * n + i] = g2 * s;
+    GU[3 * n + i] = g3 * s;
+  }
+}
+
+// deterministic column sums of X [R, N]: block b sums rows [b*rows_per, ...)
+template <typename T>
+__global__ void colsum_partial(int64_t R, int N, int64_t rows_per, const T* __restrict__ X,
+                               double* __restrict__ partial) {
+  const int64_t r0 = (int64_t)blockIdx.x * rows_per;
+  const int64_t r1 = r0 + rows_per < R ? r0 + rows_per : R;
+  for (int j = threadIdx.x; j < N; j += blockDim.x) {
+    double acc = 0.0;
+    for (int64_t r = r0; r < r1; ++r) acc += (double)X[r * N + j];
+    partial[(int64_t)blockIdx.x * N + j] = acc;
+  }
+}
+
+template <typename T>
+__global__ void colsum_reduce(int nb, int N, const double* __restrict__ partial, T* __restrict__ out) {
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < N; j += gridDim.x * blockDim.x) {
+    double acc = 0.0;
+    for (int b = 0; b < nb; ++b) acc += partial[(int64_t)b * N + j];
+    out[j] = T(acc);
+  }
+}
+
+// dL/dtau_raw through at = 2 pi t / tau and the t-tangent features (one warp per point)
+template <typename T>
+__global__ void features_bwd(int64_t R, int F, const T* __restrict__ x, const T* __restrict__ y,
+                             const T* __restrict__ t, const T* __restrict__ omega,
+                             const T* __restrict__ params, int64_t off_tau, T t_dom,
+                             const T* __restrict__ G0, double* __restrict__ partial) {
+  const T tau = tau_of(params, off_tau, t_dom);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, warps = blockDim.x >> 5;
+  const int64_t W = 2 * (int64_t)F;
+  double acc = 0.0;
+  for (int64_t p = (int64_t)blockIdx.x * warps + warp; p < R; p += (int64_t)gridDim.x * warps) {
+    T sx, cx, sy, cy, st, ct;
+    sincospi_t(x[p], &sx, &cx);
+    sincospi_t(y[p], &sy, &cy);
+    const T at = (t[p] * T(2.0 * kPi)) / tau;
+    sincos_t(at, &st, &ct);
+    const T w = T(2.0 * kPi) / tau;
+    T G4 = 0, G5 = 0, D4 = 0, D5 = 0;
+    for (int f = lane; f < F; f += 32) {
+      const T* om = omega + 6 * f;
+      const T proj = sx * om[0] + cx * om[1] + sy * om[2] + cy * om[3] + st * om[4] + ct * om[5];
+      const T dps[3] = {T(kPi) * cx * om[0] - T(kPi) * sx * om[1],
+                        T(kPi) * cy * om[2] - T(kPi) * sy * om[3], w * ct * om[4] - w * st * om[5]};
+      T sp, cp;
+      sincos_t(proj, &sp, &cp);
+      const T gc = G0[p * W + f], gs = G0[p * W + F + f];
+      T gproj = -sp * gc + cp * gs, gdp2 = 0;
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        const T* Gk = G0 + (int64_t)(k + 1) * R * W + p * W;
+        const T gdc = Gk[f], gds = Gk[F + f];
+        gproj += -cp * dps[k] * gdc - sp * dps[k] * gds;
+        if (k == 2) gdp2 = -sp * gdc + cp * gds;
+      }
+      G4 += gproj * om[4];
+      G5 += gproj * om[5];
+      D4 += gdp2 * om[4];
+      D5 += gdp2 * om[5];
+    }
+#pragma unroll
+    for (int m = 16; m >= 1; m >>= 1) {
+      G4 += __shfl_xor_sync(0xffffffffu, G4, m);
+      G5 += __shfl_xor_sync(0xffffffffu, G5, m);
+      D4 += __shfl_xor_sync(0xffffffffu, D4, m);
+      D5 += __shfl_xor_sync(0xffffffffu, D5, m);
+    }
+    const T dat = -at / tau;
+    const T w2 = T(2.0 * kPi) / (tau * tau);
+    const T gt = G4 * ct * dat + G5 * (-st) * dat + D4 * (-w2 * ct + w2 * at * st) +
+                 D5 * (w2 * st + w2 * at * ct);
+    acc += (double)gt;
+  }
+  __shared__ double red[32];
+  if (lane == 0) red[warp] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double v = 0.0;
+    for (int w2 = 0; w2 < warps; ++w2) v += red[w2];
+    partial[blockIdx.x] = v;
+  }
+}
+
+template <typename T>
+__global__ void tau_grad_reduce(int nb, const double* __restrict__ partial, const T* __restrict__ params,
+                                int64_t off_tau, T t_dom, T* __restrict__ grad) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  double v = 0.0;
+  for (int b = 0; b < nb; ++b) v += partial[b];
+  const double raw = (double)params[off_tau];
+  const double sig = 0.5 * (1.0 + tanh(0.5 * raw));  // d softplus / d raw
+  grad[off_tau] = T(v * (double)t_dom * sig);
+}
+
+// ---- workspace plan ----------------------------------------------------------------------------
+struct TrunkWS {
+  size_t h0, u[8], h[8], ua, g0, g1, part, tau_part, total;
+};
+
+constexpr int kColBlocks = 256;
+constexpr int kTauBlocks = 296;
+
+static TrunkWS trunk_ws(const qpinn_trunk_desc* d, size_t es, int64_t R) {
+  TrunkWS w{};
+  size_t o = 0;
+  auto take = [&](size_t n) {
+    size_t at = o;
+    o += (n * es + 255) / 256 * 256;
+    return at;
+  };
+  const size_t F2 = 2 * (size_t)d->rff, H = d->hidden;
+  w.h0 = take(4 * R * F2);
+  for (int i = 0; i < d->n_hidden; ++i) {
+    w.u[i] = take(4 * R * H);
+    w.h[i] = take(4 * R * H);
+  }
+  w.ua = take(4 * R * (size_t)d->n_out);
+  const size_t gmax = 4 * R * (F2 > H ? F2 : H);
+  w.g0 = take(gmax);
+  w.g1 = take(gmax);
+  w.part = o;
+  o += ((size_t)kColBlocks * (H > (size_t)d->n_out ? H : d->n_out) * 8 + 255) / 256 * 256;
+  w.tau_part = o;
+  o += (kTauBlocks * 8 + 255) / 256 * 256;
+  w.total = o;
+  return w;
+}
+
+static int grid_1d(int64_t n) {
+  int64_t g = (n + 255) / 256;
+  const int64_t cap = (int64_t)num_sms() * 16;
+  return (int)(g < 1 ? 1 : g > cap ? cap : g);
+}
+
+template <typename T>
+static int bias_grad(int64_t R, int N, const T* GU0, double* part, T* out, cudaStream_t st) {
+  const int64_t rows_per = (R + kColBlocks - 1) / kColBlocks;
+  const int nb = (int)((R + rows_per - 1) / rows_per);
+  colsum_partial<T><<<nb, N < 128 ? 32 * ((N + 31) / 32) : 128, 0, st>>>(R, N, rows_per, GU0, part);
+  colsum_reduce<T><<<(N + 127) / 128, 128, 0, st>>>(nb, N, part, out);
+  QPINN_CUDA_CHECK(cudaGetLastError());
+  return QPINN_OK;
+}
+
+template <typename T>
+static int forward_impl(const qpinn_trunk_desc* d, int64_t R, const T* x, const T* y, const T* t,
+                        const T* params, T* act, unsigned char* ws, cudaStream_t st) {
+  const TrunkWS w = trunk_ws(d, sizeof(T), R);
+  cublasHandle_t h;
+  if (int rc = blas_handle(st, &h)) return rc;
+  const int F = d->rff, H = d->hidden, n = d->n_out;
+  T* H0 = (T*)(ws + w.h0);
+  features_fwd<T><<<grid_1d(R * F), 256, 0, st>>>(R, F, x, y, t, (const T*)d->omega, params,
+                                                  d->off_tau_raw, (T)d->t_domain, H0);
+  QPINN_CUDA_CHECK(cudaGetLastError());
+  const T* in = H0;
+  int K = 2 * F;
+  for (int i = 0; i < d->n_hidden; ++i) {
+    T* U = (T*)(ws + w.u[i]);
+    T* Hn = (T*)(ws + w.h[i]);
+    if (int rc = gemm_rm<T>(h, false, false, 4 * R, H, K, in, K, params + d->off_w[i], H, U, H, T(0)))
+      return rc;
+    tanh_fwd<T><<<grid_1d(R * H), 256, 0, st>>>(R, H, U, params + d->off_b[i], Hn);
+    QPINN_CUDA_CHECK(cudaGetLastError());
+    in = Hn;
+    K = H;
+  }
+  T* Ua = (T*)(ws + w.ua);
+  if (int rc = gemm_rm<T>(h, false, false, 4 * R, n, K, in, K, params + d->off_adapter_w, n, Ua, n, T(0)))
+    return rc;
+  tanh_fwd<T><<<grid_1d(R * n), 256, 0, st>>>(R, n, Ua, params + d->off_adapter_b, act);
+  QPINN_CUDA_CHECK(cudaGetLastError());
+  return QPINN_OK;
+}
+
+template <typename T>
+static int backward_impl(const qpinn_trunk_desc* d, int64_t R, const T* x, const T* y, const T* t,
+                         const T* params, const T* act, const T* g_act, T* grad, unsigned char* ws,
+                         cudaStream_t st) {
+  const TrunkWS w = trunk_ws(d, sizeof(T), R);
+  cublasHandle_t h;
+  if (int rc = blas_handle(st, &h)) return rc;
+  const int F = d->rff, H = d->hidden, n = d->n_out;
+  double* part = (double*)(ws + w.part);
+  T* g0 = (T*)(ws + w.g0);
+  T* g1 = (T*)(ws + w.g1);
+  // adapter: GU = tanh_bwd(g_act); dWa = H_last^T GU; dba = colsum(GU0); G_H = GU Wa^T
+  const T* Hl = (const T*)(ws + (d->n_hidden ? w.h[d->n_hidden - 1] : w.h0));
+  const int Kl = d->n_hidden ? H : 2 * F;
+  tanh_bwd<T><<<grid_1d(R * n), 256, 0, st>>>(R, n, g_act, act, (const T*)(ws + w.ua), g1);
+  QPINN_CUDA_CHECK(cudaGetLastError());
+  if (int rc = gemm_rm<T>(h, true, false, Kl, n, 4 * R, Hl, Kl, g1, n, grad + d->off_adapter_w, n, T(0)))
+    return rc;
+  if (int rc = bias_grad<T>(R, n, g1, part, grad + d->off_adapter_b, st)) return rc;
+  if (int rc = gemm_rm<T>(h, false, true, 4 * R, Kl, n, g1, n, params + d->off_adapter_w, n, g0, Kl, T(0)))
+    return rc;
+  // hidden layers, last to first; g0 holds dL/dH_{i+1}
+  for (int i = d->n_hidden - 1; i >= 0; --i) {
+    const int K = i == 0 ? 2 * F : H;
+    const T* Hin = (const T*)(ws + (i == 0 ? w.h0 : w.h[i - 1]));
+    tanh_bwd<T><<<grid_1d(R * H), 256, 0, st>>>(R, H, g0, (const T*)(ws + w.h[i]),
+                                                 (const T*)(ws + w.u[i]), g1);
+    QPINN_CUDA_CHECK(cudaGetLastError());
+    if (int rc = gemm_rm<T>(h, true, false, K, H, 4 * R, Hin, K, g1, H, grad + d->off_w[i], H, T(0)))
+      return rc;
+    if (int rc = bias_grad<T>(R, H, g1, part, grad + d->off_b[i], st)) return rc;
+    if (int rc = gemm_rm<T>(h, false, true, 4 * R, K, H, g1, H, params + d->off_w[i], H, g0, K, T(0)))
+      return rc;
+  }
+  // tau_raw through the time features
+  double* tp = (double*)(ws + w.tau_part);
+  features_bwd<T><<<kTauBlocks, 256, 0, st>>>(R, F, x, y, t, (const T*)d->omega, params,
+                                               d->off_tau_raw, (T)d->t_domain, g0, tp);
+  tau_grad_reduce<T><<<1, 32, 0, st>>>(kTauBlocks, tp, params, d->off_tau_raw, (T)d->t_domain, grad);
+  QPINN_CUDA_CHECK(cudaGetLastError());
+  return QPINN_OK;
+}
+
+static int check_desc(const qpinn_trunk_desc* d, int dtype) {
+  if (!d) return fail(QPINN_ERR_CONFIG, "null trunk descriptor");
+  if (dtype != QPINN_F32 && dtype != QPINN_F64) return fail(QPINN_ERR_CONFIG, "bad dtype");
+  if (d->n_hidden < 0 || d->n_hidden > 8 || d->rff < 1 || d->hidden < 1 || d->n_out < 1 || !d->omega)
+    return fail(QPINN_ERR_CONFIG, "bad trunk descriptor");
+  return QPINN_OK;
+}
+
+}  // namespace qpinn
+
+using namespace qpinn;
+
+extern "C" {
+
+size_t qpinn_trunk_workspace_bytes(const qpinn_trunk_desc* d, int dtype, int64_t rows) {
+  if (!d || rows < 0) return 0;
+  return trunk_ws(d, dtype == QPINN_F64 ? 8 : 4, rows).total;
+}
+
+int qpinn_trunk_forward(const qpinn_trunk_desc* d, int dtype, int64_t rows, const void* x,
+                        const void* y, const void* t, const void* params, void* act,
+                        void* workspace, size_t workspace_bytes, void* stream) {
+  if (int rc = check_desc(d, dtype)) return rc;
+  if (workspace_bytes < qpinn_trunk_workspace_bytes(d, dtype, rows))
+    return fail(QPINN_ERR_CONFIG, "trunk workspace too small");
+  if (rows <= 0) return QPINN_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (dtype == QPINN_F32)
+    return forward_impl<float>(d, rows, (const float*)x, (const float*)y, (const float*)t,
+                               (const float*)params, (float*)act, (unsigned char*)workspace, st);
+  return forward_impl<double>(d, rows, (const double*)x, (const double*)y, (const double*)t,
+                              (const double*)params, (double*)act, (unsigned char*)workspace, st);
+}
+
+int qpinn_trunk_backward(const qpinn_trunk_desc* d, int dtype, int64_t rows, const void* x,
+                         const void* y, const void* t, const void* params, const void* act,
+                         const void* g_act, void* grad, void* workspace, size_t workspace_bytes,
+                         void* stream) {
+  if (int rc = check_desc(d, dtype)) return rc;
+  if (workspace_bytes < qpinn_trunk_workspace_bytes(d, dtype, rows))
+    return fail(QPINN_ERR_CONFIG, "trunk workspace too small");
+  if (rows <= 0) return QPINN_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (dtype == QPINN_F32)
+    return backward_impl<float>(d, rows, (const float*)x, (const float*)y, (const float*)t,
+                                (const float*)params, (const float*)act, (const float*)g_act,
+                                (float*)grad, (unsigned char*)workspace, st);
+  return backward_impl<double>(d, rows, (const double*)x, (const double*)y, (const double*)t,
+                               (const double*)params, (const double*)act, (const double*)g_act,
+                               (double*)grad, (unsigned char*)workspace, st);
+}
+
+}  // extern "C"

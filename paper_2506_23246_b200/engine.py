@@ -1,0 +1,149 @@
+"""Native epoch sweep for hybrid QPINN models: every kernel of the step is ours.
+
+One chunk of whole time slices runs (network.py:284-308, physics.py:352-414):
+
+    qpinn_trunk_forward          periodic map + RFF + tanh layers + adapter, with x/y/t tangents
+    qpinn_pqc_forward     (K1)   scaled embedding -> PQC -> <Z>, tangents, state hand-off
+    qpinn_loss_head_...   (K4)   linear head + residuals + every loss term + dL/dz, dL/dhead
+    qpinn_pqc_backward    (K2)   adjoint: dL/d(act, act tangents), dL/dqparams
+    qpinn_trunk_backward         dL/d(trunk weights, biases, tau_raw)
+
+There is no autograd graph: the engine calls the C ABI in order on the
+current stream, with all buffers preallocated per chunk, so a whole epoch
+is a fixed launch sequence (CUDA-graph capturable).
+"""
+from __future__ import annotations
+
+import ctypes as C
+from typing import List, Optional
+
+import numpy as np
+import torch
+
+from . import _native as N
+from .ansatz import _SCALE_CODE, ScaleKind, state_buffer
+
+
+class _ChunkBuffers:
+    def __init__(self, engine, ch):
+        R = ch.x.numel()
+        n, dev, dt = engine.n, engine.device, engine.dtype
+        self.R = R
+        self.act = torch.empty((4, R, n), dtype=dt, device=dev)
+        self.z = torch.empty((4, R, n), dtype=dt, device=dev)
+        self.gz = torch.empty((4, R, n), dtype=dt, device=dev)
+        self.gact = torch.empty((4, R, n), dtype=dt, device=dev)
+        self.states = state_buffer(engine.circuit, self.act[0])
+        self.sums = torch.zeros(N.LOSS_NSUMS, dtype=torch.float64, device=dev)
+
+
+class NativeEngine:
+    """Preallocated native trunk -> K1 -> K4 -> K2 -> trunk^T sweep."""
+
+    def __init__(self, model, evaluator):
+        if model.circuit is None:
+            raise ValueError("the native engine needs a hybrid model")
+        cfg = model.config
+        self.model, self.ev = model, evaluator
+        self.circuit = model.circuit
+        self.n = cfg.n_qubits
+        self.device, self.dtype = model.device, model.dtype
+        self.dcode = N.dtype_code(self.dtype)
+        self.scale = _SCALE_CODE[ScaleKind(cfg.scale)]
+        off = {name: o for name, o, _ in model.layout}
+        d = N.TrunkDesc()
+        d.n_hidden = model.n_hidden
+        d.rff = cfg.rff_features
+        d.hidden = cfg.hidden_width
+        d.n_out = self.n
+        for i in range(model.n_hidden):
+            d.off_w[i] = off[f"h{i}.W"]
+            d.off_b[i] = off[f"h{i}.b"]
+        d.off_adapter_w = off["adapter.W"]
+        d.off_adapter_b = off["adapter.b"]
+        d.off_tau_raw = off["tau_raw"]
+        d.t_domain = cfg.t_domain
+        self._omega = model.omega.contiguous()
+        d.omega = self._omega.data_ptr()
+        self.desc = d
+        self.off_out_w, self.off_out_b = off["out.W"], off["out.b"]
+        self.off_q = off["quantum"]
+        lib = N.lib()
+        self.chunks = evaluator.chunks
+        self.bufs: List[_ChunkBuffers] = [_ChunkBuffers(self, ch) for ch in self.chunks]
+        rmax = max((b.R for b in self.bufs), default=0)
+        self.trunk_ws = torch.empty(lib.qpinn_trunk_workspace_bytes(C.byref(d), self.dcode, rmax),
+                                    dtype=torch.uint8, device=self.device)
+        self.loss_ws = torch.empty(lib.qpinn_loss_workspace_bytes(None, 0, 0), dtype=torch.uint8,
+                                   device=self.device)
+        self.pqc_ws = self.circuit.workspace(self.dtype, self.device, rmax)
+        self._has_phase = any(s[0] == "phases" for s in self.circuit.fused_plan())
+        self.grad_chunk = (torch.empty(model.total_parameter_count, dtype=self.dtype,
+                                       device=self.device) if len(self.chunks) > 1 else None)
+
+    def sweep(self, flat: torch.Tensor, grad: Optional[torch.Tensor], weights_dev,
+              sums_out: torch.Tensor, tape: bool = True) -> None:
+        """Forward (+ full gradient into ``grad`` when tape) over every chunk;
+        raw loss sums accumulate into ``sums_out`` (float64 [23])."""
+        lib = N.lib()
+        st = N.stream_ptr()
+        fp = flat.data_ptr()
+        dc, n = self.dcode, self.n
+        es = flat.element_size()
+        wptr = N.ptr(weights_dev)
+        for i, (ch, b) in enumerate(zip(self.chunks, self.bufs)):
+            R = b.R
+            g = grad if (self.grad_chunk is None or grad is None) else self.grad_chunk
+            gp = g.data_ptr() if g is not None else 0
+            N.check(lib.qpinn_trunk_forward(C.byref(self.desc), dc, R, ch.x.data_ptr(),
+                                            ch.y.data_ptr(), ch.t.data_ptr(), fp,
+                                            b.act.data_ptr(), self.trunk_ws.data_ptr(),
+                                            self.trunk_ws.numel(), st), "qpinn_trunk_forward")
+            a0 = b.act.data_ptr()
+            a1 = a0 + R * n * es
+            with N.timed("pqc_forward"):
+                N.check(lib.qpinn_pqc_forward(self.circuit.handle, dc, self.scale, R, a0, a1,
+                                              fp + self.off_q * es, b.z.data_ptr(),
+                                              b.z.data_ptr() + R * n * es,
+                                              b.states.data_ptr() if tape else 0,
+                                              self.pqc_ws.data_ptr(), self.pqc_ws.numel(), st),
+                        "qpinn_pqc_forward")
+            scratch_w = g if g is not None else b.gact  # dL/dhead lands in grad (or scratch)
+            with N.timed("loss"):
+                N.check(lib.qpinn_loss_head_forward_backward(
+                    C.byref(ch.spec), dc, R, n, b.z.data_ptr(), fp + self.off_out_w * es,
+                    fp + self.off_out_b * es, wptr, b.gz.data_ptr(),
+                    (gp + self.off_out_w * es) if g is not None else scratch_w.data_ptr(),
+                    (gp + self.off_out_b * es) if g is not None else scratch_w.data_ptr() + 64 * es,
+                    b.sums.data_ptr(), self.loss_ws.data_ptr(), self.loss_ws.numel(), st),
+                    "qpinn_loss_head_forward_backward")
+            if tape:
+                gz0 = b.gz.data_ptr()
+                ga0 = b.gact.data_ptr()
+                with N.timed("pqc_backward"):
+                    N.check(lib.qpinn_pqc_backward(
+                        self.circuit.handle, dc, self.scale, R, a0, a1, fp + self.off_q * es,
+                        b.states.data_ptr(), gz0, gz0 + R * n * es, ga0, ga0 + R * n * es,
+                        gp + self.off_q * es, self.pqc_ws.data_ptr(), self.pqc_ws.numel(), st),
+                        "qpinn_pqc_backward")
+                N.check(lib.qpinn_trunk_backward(C.byref(self.desc), dc, R, ch.x.data_ptr(),
+                                                 ch.y.data_ptr(), ch.t.data_ptr(), fp, a0, ga0, gp,
+                                                 self.trunk_ws.data_ptr(), self.trunk_ws.numel(),
+                                                 st), "qpinn_trunk_backward")
+                if g is not grad:
+                    if i == 0:
+                        grad.copy_(g)
+                    else:
+                        grad.add_(g)
+            sums_out += b.sums
+            N.count_launches(self._launches(tape))
+
+    def _launches(self, tape: bool) -> int:
+        # our kernels only (the dense-layer GEMMs are cuBLAS)
+        L = self.model.n_hidden + 1             # dense layers incl. adapter
+        phase = 1 if self._has_phase else 0
+        n = (1 + L) + 2 + 2                     # features + tanh epilogues, K1 prep+main, K4+reduce
+        if tape:
+            n += 4 + phase                      # K2 prep, main, reduce, u1 grads (+ phase grads)
+            n += 3 * L + 2                      # per layer tanh_bwd + colsum x2; tau x2
+        return n

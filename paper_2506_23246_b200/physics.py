@@ -357,10 +357,28 @@ class LossEvaluator:
             return weights.to(device=self.device, dtype=torch.float64)
         return torch.as_tensor(np.asarray(weights, dtype=np.float64), device=self.device)
 
+    @property
+    def engine(self):
+        """Native trunk/K1/K4/K2 sweep (hybrid models); None for classical variants."""
+        if not hasattr(self, "_engine"):
+            from .engine import NativeEngine
+            self._engine = NativeEngine(self.model, self) if self.model.circuit is not None \
+                else None
+        return self._engine
+
+    def sweep_native(self, flat: torch.Tensor, grad: Optional[torch.Tensor], weights_dev,
+                     tape: bool, sums_out: torch.Tensor) -> None:
+        """All-native sweep: gradient into ``grad`` (when tape), sums into ``sums_out``."""
+        if weights_dev is not None and not self.bin_chunks:
+            raise ConfigError("time-bin weights require bin_chunks=True")
+        self.engine.sweep(flat, grad, weights_dev, sums_out, tape)
+
     def sweep(self, flat: torch.Tensor, weights_dev: Optional[torch.Tensor], tape: bool,
               sums_out: torch.Tensor) -> None:
-        """Forward (+ backward into ``flat.grad`` when tape) over every local chunk;
-        raw loss sums accumulate into ``sums_out`` (float64 [23])."""
+        """Autograd sweep (torch trunk + K1/K2/K4 autograd functions): backward into
+        ``flat.grad`` when tape; raw loss sums accumulate into ``sums_out``.  Used
+        for classical variants and as an independent cross-check of the native
+        engine."""
         if weights_dev is not None and not self.bin_chunks:
             raise ConfigError("time-bin weights require bin_chunks=True")
         for ch in self.chunks:
@@ -396,16 +414,23 @@ class LossEvaluator:
         return np.asarray(self.evaluate(params).breakdown.bin_phys)
 
     def evaluate(self, params, weights=None, tape: bool = False,
-                 reduce_fn: Optional[Callable[[torch.Tensor], None]] = None) -> EpochEval:
-        """One full pass (physics.py:334-428); grad is a device tensor when tape."""
+                 reduce_fn: Optional[Callable[[torch.Tensor], None]] = None,
+                 native: bool = True) -> EpochEval:
+        """One full pass (physics.py:334-428); grad is a device tensor when tape.
+        ``native=False`` runs the autograd cross-check path instead."""
         flat_src = params.flat if isinstance(params, ParameterStore) else params
-        flat = flat_src.detach().clone().requires_grad_(tape)
         wd = self._weights_dev(weights)
         sums = torch.zeros(N.LOSS_NSUMS, dtype=torch.float64, device=self.device)
-        self.sweep(flat, wd, tape, sums)
-        grad = flat.grad if tape else None
-        if tape and grad is None:
-            grad = torch.zeros_like(flat)
+        if native and self.engine is not None:
+            flat = flat_src.detach().contiguous()
+            grad = torch.empty_like(flat) if tape else None
+            self.sweep_native(flat, grad, wd, tape, sums)
+        else:
+            flat = flat_src.detach().clone().requires_grad_(tape)
+            self.sweep(flat, wd, tape, sums)
+            grad = flat.grad if tape else None
+            if tape and grad is None:
+                grad = torch.zeros_like(flat)
         if reduce_fn is not None:
             packed = torch.cat([grad.double() if tape else sums.new_zeros(0), sums])
             reduce_fn(packed)

@@ -227,7 +227,8 @@ class Trainer:
             flat[self.model.n_classical:] = init_quantum_params(
                 config.init_strategy, self.model.n_quantum, config.seed)
         self.params = self.model.params_from(flat)
-        self.flat = self.params.flat.requires_grad_(True)
+        self.flat = self.params.flat
+        self.grad = torch.zeros_like(self.flat)
         nx, ny, nt = config.grid
         self.grid = CollocationGrid(nx, ny, nt, t_end)
         self.material = MaterialMap(case=config.case, eps_r=config.eps_r, slab_x0=config.slab_x0)
@@ -275,13 +276,23 @@ class Trainer:
 
     def _evaluate_untaped(self):
         sums = torch.zeros(N.LOSS_NSUMS, dtype=torch.float64, device=self.device)
-        with torch.no_grad():
-            self.evaluator.sweep(self.flat.detach(), None, False, sums)
+        self._sweep(None, None, False, sums)
         if self.reduce_fn is not None:
             self.reduce_fn(sums)
         bd = self.evaluator.finalize(sums, None)
         self._check_domain()
         return bd[5:10].cpu().numpy()
+
+    def _sweep(self, grad, weights, tape, sums):
+        if self.evaluator.engine is not None:
+            self.evaluator.sweep_native(self.flat, grad, weights, tape, sums)
+            return grad
+        flat = self.flat.detach().requires_grad_(tape)
+        with torch.set_grad_enabled(tape):
+            self.evaluator.sweep(flat, weights, tape, sums)
+        if tape:
+            grad.copy_(flat.grad)
+        return grad
 
     def _check_domain(self):
         if self.model.circuit is not None:
@@ -299,14 +310,12 @@ class Trainer:
                 ch.y.copy_(hy, non_blocking=True)
                 ch.t.copy_(ht, non_blocking=True)
         self.sums.zero_()
-        self.flat.grad = None
-        self.evaluator.sweep(self.flat, self.weights, True, self.sums)
-        grad = self.flat.grad
+        grad = self._sweep(self.grad, self.weights, True, self.sums)
         if self.reduce_fn is not None:
             self._packed = reduce_packed(grad, self.sums, self.reduce_fn, self._packed)
         self.evaluator.finalize(self.sums, self.weights, cfg.kappa, self.bd,
                                 self.weights_next if self.weights is not None else None)
-        adam_step(self.flat.detach(), grad, self.adam, lr, loss_dev=self.bd[4:5],
+        adam_step(self.flat, grad, self.adam, lr, loss_dev=self.bd[4:5],
                   flag=self.flag, sync=False)
         host = self._host
         host[:10].copy_(self.bd, non_blocking=True)
@@ -366,6 +375,4 @@ def train(config: TrainConfig, outdir=None, on_epoch=None, device="cuda",
         import os
         save_checkpoint(os.path.join(str(outdir), "final.ckpt"), tr.model, tr.params)
         log.to_csv(os.path.join(str(outdir), "metrics.csv"))
-    params = ParameterStore(tr.flat.detach(), tr.params.n_classical, tr.params.n_quantum,
-                            tr.params.t_domain)
-    return TrainResult(log=log, model=tr.model, params=params)
+    return TrainResult(log=log, model=tr.model, params=tr.params)

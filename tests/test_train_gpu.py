@@ -51,6 +51,10 @@ def test_evaluate_tape_matches_reference(name, dtype):
     fields, derivs = model.forward(params, x, y, t, derivs=True)
     assert_close(torch.stack([fields.ez, fields.hx, fields.hy]), g["fields"], dtype, "fields")
     assert_close(torch.stack([derivs.ez, derivs.hx, derivs.hy]), g["derivs"], dtype, "derivs")
+    # independent cross-check: torch-autograd trunk + K1/K2/K4 autograd functions
+    ref = ev.evaluate(params, weights=w, tape=True, native=False)
+    assert_close(ref.grad, g["grad"], dtype, "autograd-path gradient",
+                 1.0 if dtype == torch.float64 else 3.0)
     plain = ev.evaluate(params, weights=w, tape=False)
     assert abs(plain.breakdown.total - float(g["plain_total"])) <= (1e-10 if dtype == torch.float64 else 1e-4) * abs(float(g["plain_total"]))
 
