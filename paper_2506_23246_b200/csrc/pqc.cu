@@ -541,6 +541,12 @@ int pqc_grid(int64_t R, int spw, int occ) { return grid_for(R, spw, occ); }
 // fixed-order grid reduction of the block partials, then gate-space -> slots
 template <typename T>
 int pqc_finish_grads(const qpinn_circuit* c, int grid, const KArgs<T>* a) {
+  const int ab = c->n <= 4 ? c->n : (c->n - 3 > 4 ? c->n - 3 : 4);  // Geo::AB
+  return pqc_finish_grads_ab<T>(c, grid, a, ab);
+}
+
+template <typename T>
+int pqc_finish_grads_ab(const qpinn_circuit* c, int grid, const KArgs<T>* a, int ab) {
   const PlanDev& p = c->dev;
   const int n_acc = 8 * p.n_u1 + (1 << p.n) * p.n_phase;
   if (n_acc > 0) {
@@ -550,7 +556,6 @@ int pqc_finish_grads(const qpinn_circuit* c, int grid, const KArgs<T>* a) {
   pqc_u1_grads<T><<<1, 256, 0, a->stream>>>(p, a->qp, a->tot, a->g_qp);
   QPINN_CUDA_CHECK(cudaGetLastError());
   if (p.n_phase) {
-    const int ab = c->n <= 4 ? c->n : (c->n - 3 > 4 ? c->n - 3 : 4);  // Geo::AB
     pqc_phase_grads<T><<<1, 256, 0, a->stream>>>(p, ab, a->tot, a->g_qp);
     QPINN_CUDA_CHECK(cudaGetLastError());
   }
@@ -558,6 +563,8 @@ int pqc_finish_grads(const qpinn_circuit* c, int grid, const KArgs<T>* a) {
 }
 template int pqc_finish_grads<float>(const qpinn_circuit*, int, const KArgs<float>*);
 template int pqc_finish_grads<double>(const qpinn_circuit*, int, const KArgs<double>*);
+template int pqc_finish_grads_ab<float>(const qpinn_circuit*, int, const KArgs<float>*, int);
+template int pqc_finish_grads_ab<double>(const qpinn_circuit*, int, const KArgs<double>*, int);
 
 // runtime n -> template instantiation
 #define QPINN_DISPATCH_N(MAXN, N_RT, CALL)                                         \
@@ -585,6 +592,18 @@ static size_t tables_bytes_bound(const qpinn_circuit* c) {  // any dtype
   return align_up(16 * (4 * (size_t)c->n_u1 + D * c->n_phase) + 4 * D * c->n_perm + 1024, 256);
 }
 
+// workspace carve-up of the cluster regime (must match big_workspace_bytes)
+static void big_ws(const qpinn_circuit* c, void* ws, double** partial, double** tot,
+                   unsigned char** tables) {
+  const size_t n_acc = n_acc_of(c), rows = (size_t)num_sms() * 2;
+  char* base = (char*)ws + 256;
+  *partial = (double*)base;
+  base += align_up(8 * n_acc * rows, 256);
+  *tot = (double*)base;
+  base += align_up(8 * n_acc, 256);
+  *tables = (unsigned char*)base;
+}
+
 }  // namespace qpinn
 
 using namespace qpinn;
@@ -608,7 +627,7 @@ int qpinn_pqc_max_qubits(int dtype) {
 size_t qpinn_pqc_workspace_bytes(const qpinn_circuit* c, int dtype, int64_t rows) {
   (void)rows;
   if (!c) return 0;
-  if (c->n > qpinn_pqc_max_qubits(dtype)) return 256;
+  if (c->n > qpinn_pqc_max_qubits(dtype)) return big_workspace_bytes(c, dtype);
   return 256 + partial_bytes(c) + align_up(sizeof(double) * n_acc_of(c), 256) +
          tables_bytes_bound(c);
 }
@@ -639,12 +658,27 @@ int qpinn_pqc_forward(const qpinn_circuit* cc, int dtype, int scale, int64_t row
   if ((act_tan == nullptr) != (dz == nullptr))
     return fail(QPINN_ERR_CONFIG, "act_tan and dz must both be given or both be NULL");
   const int n = c->n;
-  if (n > qpinn_pqc_max_qubits(dtype))
-    return fail(QPINN_ERR_CAPACITY, "n_qubits beyond the register-resident kernels");
   rc = ensure_device_plan(c);
   if (rc) return rc;
   cudaStream_t st = (cudaStream_t)stream;
   auto* maxabs = (unsigned long long*)workspace;  // running max, reset by domain_check
+  if (n > qpinn_pqc_max_qubits(dtype)) {  // cluster kernels (pqc_big.cu)
+    if (rows == 0) return QPINN_OK;
+    double* partial;
+    double* tot;
+    unsigned char* tables;
+    big_ws(c, workspace, &partial, &tot, &tables);
+    if (dtype == QPINN_F32) {
+      KArgs<float> a{scale, rows, (const float*)act_val, (const float*)act_tan, (const float*)qparams,
+                     (float*)z, (float*)dz, nullptr, maxabs, nullptr, nullptr, nullptr, nullptr,
+                     nullptr, partial, tot, st, tables};
+      return big_dispatch<float>(true, c, &a);
+    }
+    KArgs<double> a{scale, rows, (const double*)act_val, (const double*)act_tan,
+                    (const double*)qparams, (double*)z, (double*)dz, nullptr, maxabs, nullptr,
+                    nullptr, nullptr, nullptr, nullptr, partial, tot, st, tables};
+    return big_dispatch<double>(true, c, &a);
+  }
   unsigned char* tables = (unsigned char*)workspace + 256 + partial_bytes(c) +
                           align_up(sizeof(double) * n_acc_of(c), 256);
   if (rows == 0) return QPINN_OK;
@@ -687,11 +721,32 @@ int qpinn_pqc_backward(const qpinn_circuit* cc, int dtype, int scale, int64_t ro
   if (!act_tan || !g_z || !g_dz || !g_act_val || !g_act_tan || !g_qparams)
     return fail(QPINN_ERR_CONFIG, "backward needs tangents and all gradient buffers");
   const int n = c->n;
-  if (n > qpinn_pqc_max_qubits(dtype))
-    return fail(QPINN_ERR_CAPACITY, "n_qubits beyond the register-resident kernels");
   rc = ensure_device_plan(c);
   if (rc) return rc;
   cudaStream_t st = (cudaStream_t)stream;
+  if (n > qpinn_pqc_max_qubits(dtype)) {  // cluster kernels (pqc_big.cu), forward replayed
+    if (rows == 0) {
+      QPINN_CUDA_CHECK(cudaMemsetAsync(g_qparams, 0,
+                                       (dtype == QPINN_F64 ? 8 : 4) * (size_t)c->n_params, st));
+      return QPINN_OK;
+    }
+    double* bp;
+    double* bt;
+    unsigned char* btab;
+    big_ws(c, workspace, &bp, &bt, &btab);
+    if (dtype == QPINN_F32) {
+      KArgs<float> a{scale, rows, (const float*)act_val, (const float*)act_tan,
+                     (const float*)qparams, nullptr, nullptr, nullptr, nullptr, (const float*)g_z,
+                     (const float*)g_dz, (float*)g_act_val, (float*)g_act_tan, (float*)g_qparams,
+                     bp, bt, st, btab};
+      return big_dispatch<float>(false, c, &a);
+    }
+    KArgs<double> a{scale, rows, (const double*)act_val, (const double*)act_tan,
+                    (const double*)qparams, nullptr, nullptr, nullptr, nullptr,
+                    (const double*)g_z, (const double*)g_dz, (double*)g_act_val,
+                    (double*)g_act_tan, (double*)g_qparams, bp, bt, st, btab};
+    return big_dispatch<double>(false, c, &a);
+  }
   double* partial = (double*)((char*)workspace + 256);
   double* tot = (double*)((char*)workspace + 256 + partial_bytes(c));
   unsigned char* tables = (unsigned char*)workspace + 256 + partial_bytes(c) +

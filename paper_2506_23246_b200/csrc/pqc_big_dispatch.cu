@@ -1,0 +1,42 @@
+// Dispatch for the large-n cluster kernels; the kernels themselves are
+// instantiated per n in pqc_big_n*.cu so the build parallelises.
+#include "pqc_layer.h"
+
+namespace qpinn {
+
+template <typename T, int N>
+int big_n(bool fwd, int ent, const qpinn_circuit* c, const KArgs<T>* a);
+
+template <typename T>
+int big_dispatch(bool fwd, const qpinn_circuit* c, const KArgs<T>* a) {
+  const int ent = layer_entangler(c);
+  if (ent < 0) return fail(QPINN_ERR_CAPACITY, "large-n kernels need the standard layer plan");
+  switch (c->n) {
+    case 9: return big_n<T, 9>(fwd, ent, c, a);
+    case 10: return big_n<T, 10>(fwd, ent, c, a);
+    case 11: return big_n<T, 11>(fwd, ent, c, a);
+    case 12: return big_n<T, 12>(fwd, ent, c, a);
+    case 13: return big_n<T, 13>(fwd, ent, c, a);
+    case 14: return big_n<T, 14>(fwd, ent, c, a);
+    case 15: return big_n<T, 15>(fwd, ent, c, a);
+    case 16:
+      if constexpr (sizeof(T) == 4) return big_n<float, 16>(fwd, ent, c, (const KArgs<float>*)a);
+      return fail(QPINN_ERR_CAPACITY, "float64 large-n kernels cover n <= 15");
+    default: return fail(QPINN_ERR_CAPACITY, "n_qubits out of range");
+  }
+}
+
+template int big_dispatch<float>(bool, const qpinn_circuit*, const KArgs<float>*);
+template int big_dispatch<double>(bool, const qpinn_circuit*, const KArgs<double>*);
+
+size_t big_workspace_bytes(const qpinn_circuit* c, int dtype) {
+  const size_t D = (size_t)1 << c->n, es = dtype == QPINN_F64 ? 16 : 8;
+  const size_t n_acc = 8 * (size_t)c->n_u1 + D * c->n_phase;
+  const size_t rows = (size_t)num_sms() * 2;  // clusters never exceed SMs x 2 blocks
+  size_t o = 256 + align_up(8 * n_acc * rows, 256) + align_up(8 * n_acc, 256);
+  o += align_up(es * 4 * c->n_u1, 256) + 2 * align_up(4 * D * c->n_perm, 256) +
+       align_up(es * D * c->n_phase, 256);
+  return o;
+}
+
+}  // namespace qpinn

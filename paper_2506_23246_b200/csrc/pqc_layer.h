@@ -41,5 +41,14 @@ int layer_entangler(const qpinn_circuit* c);
 int pqc_grid(int64_t R, int spw, int occ);
 template <typename T>
 int pqc_finish_grads(const qpinn_circuit* c, int grid, const KArgs<T>* a);
+// ab = register bits of the phase-accumulator layout ((b & (2^ab-1)) 2^(n-ab) + (b >> ab));
+// ab = n means natural index order
+template <typename T>
+int pqc_finish_grads_ab(const qpinn_circuit* c, int grid, const KArgs<T>* a, int ab);
+
+// large-n cluster kernels (pqc_big.cu)
+template <typename T>
+int big_dispatch(bool fwd, const qpinn_circuit* c, const KArgs<T>* a);
+size_t big_workspace_bytes(const qpinn_circuit* c, int dtype);
 
 }  // namespace qpinn

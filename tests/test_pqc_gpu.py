@@ -170,3 +170,35 @@ def test_specialized_kernels_match_generic_and_oracle(kind, dtype):
         got = res[variant]
         for name, x, w in zip(("z", "dz", "ga", "gda", "gq"), got, (wz, wdz) + tuple(wg)):
             assert_close(x, w, dtype, f"{variant} {name}")
+
+
+BIG_CASES = [(9, 2, "strongly", True), (10, 1, "cross_mesh_2rot", True), (11, 2, "cross_mesh", True),
+             (12, 2, "strongly", True), (13, 1, "basic", True), (14, 1, "cross_mesh_cnot", True),
+             (15, 1, "strongly", False), (16, 1, "no_entanglement", False),
+             (16, 1, "cross_mesh", False)]
+
+
+@pytest.mark.parametrize("n,L,kind,bwd", BIG_CASES)
+def test_cluster_kernels_large_n_vs_oracle(n, L, kind, bwd):
+    """n = 9..16: thread-block-cluster kernels (DSMEM exchanges) vs the oracle."""
+    from paper_2506_23246_b200.ansatz import build_circuit, pqc_backward_raw, pqc_forward_raw
+    dtype = torch.float32
+    rng = np.random.default_rng(n * 7 + L)
+    c = build_circuit(kind, n, L)
+    R = 3
+    d = dict(a=rng.uniform(-0.9, 0.9, (R, n)), da=rng.normal(size=(3, R, n)),
+             qp=rng.uniform(0, 2 * np.pi, c.param_count), gz=rng.normal(size=(R, n)),
+             gdz=rng.normal(size=(3, R, n)))
+    a, da, qp = cuda(d["a"], dtype), cuda(d["da"], dtype), cuda(d["qp"], dtype)
+    z, dz = pqc_forward_raw(c, "acos", a, da, qp)
+    wz, wdz = O.pqc_forward(d["a"], d["da"], d["qp"], kind, "acos", L)
+    s = 4.0 if n >= 13 else 1.0
+    assert_close(z, wz, dtype, f"n={n} z", s)
+    assert_close(dz, wdz, dtype, f"n={n} dz", s)
+    if bwd:
+        ga, gda, gq = pqc_backward_raw(c, "acos", a, da, qp, cuda(d["gz"], dtype),
+                                       cuda(d["gdz"], dtype))
+        wga, wgda, wgq = O.pqc_backward(d["a"], d["da"], d["qp"], kind, "acos", L, d["gz"], d["gdz"])
+        assert_close(ga, wga, dtype, f"n={n} ga", s)
+        assert_close(gda, wgda, dtype, f"n={n} gda", s)
+        assert_close(gq, wgq, dtype, f"n={n} gq", s)
