@@ -127,6 +127,17 @@ __device__ __forceinline__ void rotate_regs(cplx<T> (&v)[1 << AB]) {
   for (int r = 0; r < A; ++r) v[r] = t[r];
 }
 
+// new[r] = old[r with its high and low AB/2-bit halves swapped] (an involution)
+template <typename T, int AB>
+__device__ __forceinline__ void swap_halves(cplx<T> (&v)[1 << AB]) {
+  constexpr int A = 1 << AB, H = AB / 2, HM = (1 << H) - 1;
+  cplx<T> t[A];
+#pragma unroll
+  for (int r = 0; r < A; ++r) t[r] = v[((r & HM) << H) | (r >> H)];
+#pragma unroll
+  for (int r = 0; r < A; ++r) v[r] = t[r];
+}
+
 // new[r] = old[rotr(r)] (inverse of rotate_regs)
 template <typename T, int AB>
 __device__ __forceinline__ void rotate_regs_left(cplx<T> (&v)[1 << AB]) {
@@ -186,12 +197,23 @@ pqc_forward_layer(PlanDev plan, const unsigned char* __restrict__ tables, int n_
         const cplx<T>* U = Ul + 4 * q;
         gate_lane<T, A, 1>(st, 1 << lb, (gl >> lb) & 1, U[0], U[1], U[2], U[3]);
       }
-      // register wires LB .. N-1: bit (AB-1) .. 0; rotate left so each wire's
-      // bit arrives at position AB-1 of one shared gate copy
-      for (int i = 0; i < AB; ++i) {
-        const cplx<T>* U = Ul + 4 * (LB + i);
-        gate_reg<AB - 1, T, A, 1>(st, U[0], U[1], U[2], U[3]);
-        if constexpr (AB > 1) rotate_regs_left<T, AB>(st[0]);
+      // register wires LB .. N-1 (bits AB-1 .. 0).  Gates of one layer commute,
+      // so with AB = 4 two gate copies (bits 3, 2) plus a half-swap of
+      // the register index cover all wires: fewer moves than single-bit rotation
+      // and far less code than unrolling every wire.
+      if constexpr (AB == 4) {
+        for (int i = 0; i < AB; i += 2) {
+          const cplx<T>* U = Ul + 4 * (LB + i);
+          gate_reg<AB - 1, T, A, 1>(st, U[0], U[1], U[2], U[3]);
+          gate_reg<AB - 2, T, A, 1>(st, U[4], U[5], U[6], U[7]);
+          swap_halves<T, AB>(st[0]);
+        }
+      } else {
+        for (int i = 0; i < AB; ++i) {
+          const cplx<T>* U = Ul + 4 * (LB + i);
+          gate_reg<AB - 1, T, A, 1>(st, U[0], U[1], U[2], U[3]);
+          if constexpr (AB > 1) rotate_regs_left<T, AB>(st[0]);
+        }
       }
       if constexpr (ENT == ENT_PERM) {
         permute<T, A, G, 1>(st, sm.pt + l * D, buf, gl, lane_hi);
@@ -335,14 +357,25 @@ pqc_backward_layer(PlanDev plan, const unsigned char* __restrict__ tables, int n
       }
       const cplx<T>* Ul = sm.U + 4 * N * l;
       T* accl = accU + 8 * N * l;
-      // register wires N-1 .. LB: one register-bit-0 gate copy, rotating the
-      // register index so the next wire's bit comes to position 0
-      for (int i = 0; i < AB; ++i) {
-        const int q = N - 1 - i;
-        gate_bwd<T, N, N - 1>(xa[0], xa[1], Ul + 4 * q, accl + 8 * q, gl, lane);
-        if constexpr (AB > 1) {
-          rotate_regs<T, AB>(xa[0]);
-          rotate_regs<T, AB>(xa[1]);
+      // register wires N-1 .. LB (bits 0 .. AB-1): two gate copies (bits 0, 1)
+      // plus a half-swap of the register index; with the permutation entangler
+      // (larger loop body) one copy + one-bit rotation keeps the I-cache happier
+      if constexpr (AB == 4 && ENT != ENT_PERM) {
+        for (int i = 0; i < AB; i += 2) {
+          const int q = N - 1 - i;
+          gate_bwd<T, N, N - 1>(xa[0], xa[1], Ul + 4 * q, accl + 8 * q, gl, lane);
+          gate_bwd<T, N, N - 2>(xa[0], xa[1], Ul + 4 * (q - 1), accl + 8 * (q - 1), gl, lane);
+          swap_halves<T, AB>(xa[0]);
+          swap_halves<T, AB>(xa[1]);
+        }
+      } else {
+        for (int i = 0; i < AB; ++i) {
+          const int q = N - 1 - i;
+          gate_bwd<T, N, N - 1>(xa[0], xa[1], Ul + 4 * q, accl + 8 * q, gl, lane);
+          if constexpr (AB > 1) {
+            rotate_regs<T, AB>(xa[0]);
+            rotate_regs<T, AB>(xa[1]);
+          }
         }
       }
       for (int q = LB - 1; q >= 0; --q)  // lane wires, one shared copy
