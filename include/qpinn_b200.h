@@ -93,14 +93,16 @@ int qpinn_pqc_max_qubits(int dtype);
 /* Device scratch needed by forward/backward for `rows` points. */
 size_t qpinn_pqc_workspace_bytes(const qpinn_circuit* c, int dtype, int64_t rows);
 
-/* Bytes of the optional final-state hand-off buffer (4 states x 2^n
- * amplitudes per row) that lets the backward skip re-running the circuit. */
+/* Bytes of the optional state hand-off buffer that lets the backward skip
+ * re-running the circuit: 4 states x 2^n amplitudes per row at each of the L
+ * layer boundaries for the layer-loop kernels (variant 0), the 4 final states
+ * for the generic kernels (variant 1).  The content is opaque. */
 size_t qpinn_pqc_state_bytes(const qpinn_circuit* c, int dtype, int64_t rows);
 
 /* z[R,n] = <Z_q>, dz[3,R,n] = d<Z_q>/d(x,y,t) of the scaled-angle-embedded
  * circuit; act_val [R,n], act_tan [3,R,n] row-major (act_tan/dz may be NULL
  * for value-only evaluation), qparams [P].  When `states` is not NULL (and
- * tangents are on) the final psi, d psi/dx,y,t are stored there for
+ * tangents are on) psi, d psi/dx,y,t are checkpointed there for
  * qpinn_pqc_backward.  Folds max|act_val| into the workspace's running
  * maximum for qpinn_pqc_domain_check. */
 int qpinn_pqc_forward(const qpinn_circuit* c, int dtype, int scale, int64_t rows,

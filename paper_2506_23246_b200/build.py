@@ -52,10 +52,24 @@ def build(force: bool = False, verbose: bool = False) -> str:
     objs = []
     logs = []
     procs = []
+    # per-source object cache: a source is recompiled only when it, a header or the flags change
+    odir = os.path.join(CSRC, ".obj")
+    os.makedirs(odir, exist_ok=True)
+    hdr = hashlib.sha256()
+    for f in sorted(os.listdir(CSRC)) + ["../../include/qpinn_b200.h"]:
+        if f.endswith((".h", ".cuh")):
+            with open(os.path.normpath(os.path.join(CSRC, f)), "rb") as fh:
+                hdr.update(f.encode() + fh.read())
+    hdr.update(" ".join(ARCH + FLAGS).encode())
     for src in SOURCES:
-        obj = os.path.join(CSRC, src.replace(".cu", ".o"))
+        with open(os.path.join(CSRC, src), "rb") as fh:
+            key = hashlib.sha256(hdr.digest() + fh.read()).hexdigest()[:16]
+        obj = os.path.join(odir, src.replace(".cu", f".{key}.o"))
+        if os.path.exists(obj):
+            objs.append(obj)
+            continue
         cmd = [nvcc, *ARCH, *FLAGS, "-I", os.path.join(ROOT, "include"), "-I", CSRC,
-               "-c", os.path.join(CSRC, src), "-o", obj]
+               "-c", os.path.join(CSRC, src), "-o", obj + ".tmp"]
         procs.append((src, obj, subprocess.Popen(cmd, stdout=subprocess.PIPE,
                                                  stderr=subprocess.PIPE, text=True)))
     for src, obj, pr in procs:
@@ -64,7 +78,12 @@ def build(force: bool = False, verbose: bool = False) -> str:
         if pr.returncode != 0:
             sys.stderr.write(out + err)
             raise RuntimeError(f"nvcc failed on {src}")
+        os.replace(obj + ".tmp", obj)
         objs.append(obj)
+    keep = set(objs)
+    for f in os.listdir(odir):
+        if os.path.join(odir, f) not in keep:
+            os.remove(os.path.join(odir, f))
     tmp = LIB + ".tmp"
     cmd = [nvcc, *ARCH, "-shared", "-o", tmp, *objs, "-lcudart", "-lcublas",
            "-Xlinker", "-rpath,/usr/local/cuda/lib64"]
@@ -73,12 +92,11 @@ def build(force: bool = False, verbose: bool = False) -> str:
         sys.stderr.write(r.stdout + r.stderr)
         raise RuntimeError("link failed")
     os.replace(tmp, LIB)
-    with open(os.path.join(CSRC, "ptxas.log"), "w") as f:
-        f.write("\n".join(logs))
+    if logs:
+        with open(os.path.join(CSRC, "ptxas.log"), "w") as f:
+            f.write("\n".join(logs))
     with open(stamp_file, "w") as f:
         f.write(stamp)
-    for o in objs:
-        os.remove(o)
     if verbose:
         print("built", LIB)
     return LIB

@@ -634,7 +634,11 @@ size_t qpinn_pqc_workspace_bytes(const qpinn_circuit* c, int dtype, int64_t rows
 
 size_t qpinn_pqc_state_bytes(const qpinn_circuit* c, int dtype, int64_t rows) {
   if (!c || rows < 0) return 0;
-  return (size_t)rows * 4 * ((size_t)1 << c->n) * 2 * (dtype == QPINN_F64 ? 8 : 4);
+  // layer-loop kernels: the 4 states at each of the L layer boundaries;
+  // generic kernels: the 4 final states (fits inside the former)
+  const size_t per = 4 * ((size_t)1 << c->n) * 2 * (dtype == QPINN_F64 ? 8 : 4);
+  const bool layer = c->n <= qpinn_pqc_max_qubits(dtype) && layer_entangler(c) >= 0;
+  return (size_t)rows * per * (layer && c->L > 1 ? (size_t)c->L : 1);
 }
 
 static int check_common(const qpinn_circuit* c, int dtype, int scale, int64_t rows,

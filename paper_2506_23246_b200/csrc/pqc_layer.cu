@@ -10,102 +10,55 @@
 // there is no per-gate dispatch and the loop-carried state only has to be
 // re-homed once per layer.  The body stays ~20 KB of SASS, inside the L1.5
 // instruction cache (a fully unrolled circuit does not: warps then stall on
-// instruction fetch).  Numerics, lane geometry, the K1 -> K2 state hand-off
-// layout and the deterministic reductions are those of the generic kernels
-// in pqc.cu, which remain the cross-check (kernel variant 1).
+// instruction fetch).  Numerics, lane geometry and the deterministic
+// reductions are those of the generic kernels in pqc.cu, which remain the
+// cross-check (kernel variant 1).  The hand-off differs: K1 stores the state
+// at every layer boundary (after the single-qubit gates), so K2 never
+// un-computes the state and only propagates the adjoint (see K2).
 #include "pqc_layer.h"
 
 namespace qpinn {
 
-// ---- single-qubit step on compile-time wire Q ---------------------------------------
-template <typename T, int N, int Q, int NR>
-__device__ __forceinline__ void gate_fwd(cplx<T> (&st)[NR][Geo<T, N, 4>::A], const cplx<T>* U,
-                                         int gl) {
-  using Gm = Geo<T, N, 4>;
-  constexpr int AB = Gm::AB, A = Gm::A, LB = Gm::LB;
-  const cplx<T> u00 = U[0], u01 = U[1], u10 = U[2], u11 = U[3];
-  if constexpr (Q < LB) {
-    constexpr int lb = LB - 1 - Q;
-    gate_lane<T, A, NR>(st, 1 << lb, (gl >> lb) & 1, u00, u01, u10, u11);
-  } else {
-    gate_reg<N - 1 - Q, T, A, NR>(st, u00, u01, u10, u11);
-  }
-  (void)AB;
+template <typename T>
+__device__ __forceinline__ cplx<T> conj(cplx<T> a) {
+  return {a.re, -a.im};
 }
 
-// reverse step on wire Q: un-compute x, propagate the adjoint a (both by U^dagger)
-// and accumulate the post-gate outer product M'_ij = sum conj(a_i) x_j
-template <typename T, int N, int Q>
-__device__ __forceinline__ void gate_bwd(cplx<T> (&x)[Geo<T, N, 4>::A],
-                                         cplx<T> (&a)[Geo<T, N, 4>::A], const cplx<T>* U,
-                                         T* __restrict__ acc, int gl, int lane) {
-  using Gm = Geo<T, N, 4>;
-  constexpr int A = Gm::A, LB = Gm::LB;
-  const cplx<T> h00 = {U[0].re, -U[0].im}, h01 = {U[2].re, -U[2].im};
-  const cplx<T> h10 = {U[1].re, -U[1].im}, h11 = {U[3].re, -U[3].im};
+// post-gate outer product M'_ij = sum conj(a_i) x_j of the single-qubit step on
+// the wire held by register bit RB, summed over the warp into acc[0..7]
+template <typename T, int A, int RB>
+__device__ __forceinline__ void outer_reg(const cplx<T> (&x)[A], const cplx<T> (&a)[A],
+                                          T* __restrict__ acc, int lane) {
+  constexpr int S = 1 << RB;
   T m[8] = {T(0), T(0), T(0), T(0), T(0), T(0), T(0), T(0)};
-  if constexpr (Q < LB) {
-    constexpr int lm = 1 << (LB - 1 - Q);
-    const bool beta = gl & lm;
-    const cplx<T> cs = beta ? h11 : h00, cp = beta ? h10 : h01;
-    T ms_re = 0, ms_im = 0, mc_re = 0, mc_im = 0;
 #pragma unroll
-    for (int r = 0; r < A; ++r) {
-      const cplx<T> xs = x[r], as = a[r];
-      const cplx<T> xp = shfl_xor_c(xs, lm), ap = shfl_xor_c(as, lm);
-      const cplx<T> t1 = cmulc(as, xs), t2 = cmulc(as, xp);
-      ms_re += t1.re; ms_im += t1.im; mc_re += t2.re; mc_im += t2.im;
-      x[r] = cmul2(cs, xs, cp, xp);
-      a[r] = cmul2(cs, as, cp, ap);
-    }
-    // own row i: beta = 0 -> M'(0,0), M'(0,1); beta = 1 -> M'(1,1), M'(1,0)
-    m[0] = beta ? T(0) : ms_re; m[1] = beta ? T(0) : ms_im;
-    m[2] = beta ? T(0) : mc_re; m[3] = beta ? T(0) : mc_im;
-    m[6] = beta ? ms_re : T(0); m[7] = beta ? ms_im : T(0);
-    m[4] = beta ? mc_re : T(0); m[5] = beta ? mc_im : T(0);
-  } else {
-    constexpr int S = 1 << (N - 1 - Q);
-#pragma unroll
-    for (int r = 0; r < A; ++r) {
-      if (r & S) continue;
-      const int r1 = r | S;
-      const cplx<T> x0 = x[r], x1 = x[r1], a0 = a[r], a1 = a[r1];
-      cplx<T> t;
-      t = cmulc(a0, x0); m[0] += t.re; m[1] += t.im;
-      t = cmulc(a0, x1); m[2] += t.re; m[3] += t.im;
-      t = cmulc(a1, x0); m[4] += t.re; m[5] += t.im;
-      t = cmulc(a1, x1); m[6] += t.re; m[7] += t.im;
-      x[r] = cmul2(h00, x0, h01, x1);
-      x[r1] = cmul2(h10, x0, h11, x1);
-      a[r] = cmul2(h00, a0, h01, a1);
-      a[r1] = cmul2(h10, a0, h11, a1);
-    }
+  for (int r = 0; r < A; ++r) {
+    if (r & S) continue;
+    const int r1 = r | S;
+    cplx<T> t;
+    t = cmulc(a[r], x[r]);   m[0] += t.re; m[1] += t.im;
+    t = cmulc(a[r], x[r1]);  m[2] += t.re; m[3] += t.im;
+    t = cmulc(a[r1], x[r]);  m[4] += t.re; m[5] += t.im;
+    t = cmulc(a[r1], x[r1]); m[6] += t.re; m[7] += t.im;
   }
   const T v = warp_reduce8(m, lane);
   if ((lane & 3) == 0) acc[lane >> 2] += v;
 }
 
-// lane-wire reverse step with a run-time lane mask: one code copy serves all
-// lane wires, which keeps K2's hot loop inside the instruction cache
-template <typename T, int N>
-__device__ __forceinline__ void gate_bwd_lane(cplx<T> (&x)[Geo<T, N, 4>::A],
-                                              cplx<T> (&a)[Geo<T, N, 4>::A], const cplx<T>* U,
-                                              T* __restrict__ acc, int lm, int gl, int lane) {
-  constexpr int A = Geo<T, N, 4>::A;
-  const cplx<T> h00 = {U[0].re, -U[0].im}, h01 = {U[2].re, -U[2].im};
-  const cplx<T> h10 = {U[1].re, -U[1].im}, h11 = {U[3].re, -U[3].im};
+// the same for a lane wire (run-time lane mask lm: one code copy serves all
+// lane wires, which keeps K2's hot loop inside the instruction cache)
+template <typename T, int A>
+__device__ __forceinline__ void outer_lane(const cplx<T> (&x)[A], const cplx<T> (&a)[A],
+                                           T* __restrict__ acc, int lm, int gl, int lane) {
   const bool beta = gl & lm;
-  const cplx<T> cs = beta ? h11 : h00, cp = beta ? h10 : h01;
   T ms_re = 0, ms_im = 0, mc_re = 0, mc_im = 0;
 #pragma unroll
   for (int r = 0; r < A; ++r) {
-    const cplx<T> xs = x[r], as = a[r];
-    const cplx<T> xp = shfl_xor_c(xs, lm), ap = shfl_xor_c(as, lm);
-    const cplx<T> t1 = cmulc(as, xs), t2 = cmulc(as, xp);
+    const cplx<T> xp = shfl_xor_c(x[r], lm);
+    const cplx<T> t1 = cmulc(a[r], x[r]), t2 = cmulc(a[r], xp);
     ms_re += t1.re; ms_im += t1.im; mc_re += t2.re; mc_im += t2.im;
-    x[r] = cmul2(cs, xs, cp, xp);
-    a[r] = cmul2(cs, as, cp, ap);
   }
+  // own row i: beta = 0 -> M'(0,0), M'(0,1); beta = 1 -> M'(1,1), M'(1,0)
   T m[8];
   m[0] = beta ? T(0) : ms_re; m[1] = beta ? T(0) : ms_im;
   m[2] = beta ? T(0) : mc_re; m[3] = beta ? T(0) : mc_im;
@@ -113,18 +66,6 @@ __device__ __forceinline__ void gate_bwd_lane(cplx<T> (&x)[Geo<T, N, 4>::A],
   m[4] = beta ? mc_re : T(0); m[5] = beta ? mc_im : T(0);
   const T v = warp_reduce8(m, lane);
   if ((lane & 3) == 0) acc[lane >> 2] += v;
-}
-
-// rotate the register index right by one bit: new[r] = old[rotl(r)]; after
-// AB rotations the layout is back to the original
-template <typename T, int AB>
-__device__ __forceinline__ void rotate_regs(cplx<T> (&v)[1 << AB]) {
-  constexpr int A = 1 << AB;
-  cplx<T> t[A];
-#pragma unroll
-  for (int r = 0; r < A; ++r) t[r] = v[((r << 1) | (r >> (AB - 1))) & (A - 1)];
-#pragma unroll
-  for (int r = 0; r < A; ++r) v[r] = t[r];
 }
 
 // new[r] = old[r with its high and low AB/2-bit halves swapped] (an involution)
@@ -138,7 +79,7 @@ __device__ __forceinline__ void swap_halves(cplx<T> (&v)[1 << AB]) {
   for (int r = 0; r < A; ++r) v[r] = t[r];
 }
 
-// new[r] = old[rotr(r)] (inverse of rotate_regs)
+// new[r] = old[rotr(r)]: after AB rotations the layout is back to the original
 template <typename T, int AB>
 __device__ __forceinline__ void rotate_regs_left(cplx<T> (&v)[1 << AB]) {
   constexpr int A = 1 << AB;
@@ -149,12 +90,33 @@ __device__ __forceinline__ void rotate_regs_left(cplx<T> (&v)[1 << AB]) {
   for (int r = 0; r < A; ++r) v[r] = t[r];
 }
 
-template <int I, typename F>  // I, I-1, ..., 0
-__device__ __forceinline__ void static_for_rev(F&& f) {
-  if constexpr (I >= 0) {
-    f(std::integral_constant<int, I>{});
-    static_for_rev<I - 1>(f);
-  }
+// K1 -> K2 hand-off: the 4 states of point s after the single-qubit gates of
+// layer l (before its entangler), register pairs innermost so that one
+// 16-byte (fp32) store / load per lane moves two amplitudes and a warp
+// instruction touches 32 consecutive pairs:
+//   states[(((s L + l) A/2 + r/2) 4G + sidx G + gl) 2 + (r & 1)]
+template <int G, int A>
+__device__ __forceinline__ int64_t boundary_offset(int64_t s, int n_layers, int l) {
+  return ((s * n_layers + l) * (A / 2)) * (4 * G) * 2;
+}
+__device__ __forceinline__ void st_pair(cplx<float>* p, cplx<float> a, cplx<float> b) {
+  *reinterpret_cast<float4*>(p) = make_float4(a.re, a.im, b.re, b.im);
+}
+__device__ __forceinline__ void st_pair(cplx<double>* p, cplx<double> a, cplx<double> b) {
+  p[0] = a;
+  p[1] = b;
+}
+__device__ __forceinline__ void ld_pair(const cplx<float>* p, cplx<float>& a, cplx<float>& b) {
+  const float4 v = __ldg(reinterpret_cast<const float4*>(p));
+  a = {v.x, v.y};
+  b = {v.z, v.w};
+}
+__device__ __forceinline__ void ld_pair(const cplx<double>* p, cplx<double>& a,
+                                        cplx<double>& b) {
+  const double2 u = __ldg(reinterpret_cast<const double2*>(p));
+  const double2 v = __ldg(reinterpret_cast<const double2*>(p + 1));
+  a = {u.x, u.y};
+  b = {v.x, v.y};
 }
 
 // ---- K1 -----------------------------------------------------------------------------------
@@ -215,6 +177,11 @@ pqc_forward_layer(PlanDev plan, const unsigned char* __restrict__ tables, int n_
           if constexpr (AB > 1) rotate_regs_left<T, AB>(st[0]);
         }
       }
+      if (NSL == 4 && states != nullptr && valid) {  // layer-boundary hand-off for K2
+        cplx<T>* sp = states + boundary_offset<G, A>(s, n_layers, l) + 2 * (sidx * G + gl);
+#pragma unroll
+        for (int r = 0; r < A; r += 2) st_pair(sp + r * 4 * G, st[0][r], st[0][r + 1]);
+      }
       if constexpr (ENT == ENT_PERM) {
         permute<T, A, G, 1>(st, sm.pt + l * D, buf, gl, lane_hi);
       } else if constexpr (ENT == ENT_PHASE) {
@@ -222,11 +189,6 @@ pqc_forward_layer(PlanDev plan, const unsigned char* __restrict__ tables, int n_
 #pragma unroll
         for (int r = 0; r < A; ++r) st[0][r] = cmul(st[0][r], ph[r * G + gl]);
       }
-    }
-    if (NSL == 4 && states != nullptr && valid) {  // hand-off for K2
-      cplx<T>* sp = states + s * (4 * D) + sidx * D;
-#pragma unroll
-      for (int r = 0; r < A; ++r) sp[r * G + gl] = st[0][r];
     }
     T out[N], tot = T(0);
 #pragma unroll
@@ -271,7 +233,7 @@ pqc_forward_layer(PlanDev plan, const unsigned char* __restrict__ tables, int n_
 
 // ---- K2 -----------------------------------------------------------------------------------
 template <typename T, int N, int ENT>
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kThreads, sizeof(T) == 4 && N <= 7 ? 3 : 1)
 pqc_backward_layer(PlanDev plan, const unsigned char* __restrict__ tables, int n_layers,
                    int scale, int64_t R, const T* __restrict__ act,
                    const T* __restrict__ act_tan, const T* __restrict__ qp,
@@ -305,11 +267,27 @@ pqc_backward_layer(PlanDev plan, const unsigned char* __restrict__ tables, int n
     T c[N], sn[N], dth[N], s1v[N], s2v[N], amax_unused = T(0);
     load_point_fast<T, N>(scale, act, act_tan, R, s, valid, sidx - 1, c, sn, dth, s1v, s2v,
                           amax_unused);
-    cplx<T> xa[2][A];  // [0] this lane's state, [1] its adjoint
-    {
-      const cplx<T>* sp = states + (valid ? s : 0) * (4 * D) + sidx * D;
+    cplx<T> xa[2][A];  // [0] this lane's layer-boundary state, [1] its adjoint
+    cplx<T>(&x1)[1][A] = reinterpret_cast<cplx<T>(&)[1][A]>(xa[0]);
+    cplx<T>(&a1)[1][A] = reinterpret_cast<cplx<T>(&)[1][A]>(xa[1]);
+    const cplx<T>* sp0 =
+        states + boundary_offset<G, A>(valid ? s : 0, n_layers, 0) + 2 * (sidx * G + gl);
+    auto load_boundary = [&](int l) {
+      const cplx<T>* sp = sp0 + (int64_t)l * (4 * D);
 #pragma unroll
-      for (int r = 0; r < A; ++r) xa[0][r] = valid ? sp[r * G + gl] : cplx<T>{T(0), T(0)};
+      for (int r = 0; r < A; r += 2) {
+        ld_pair(sp + r * 4 * G, xa[0][r], xa[0][r + 1]);
+        if (!valid) xa[0][r] = xa[0][r + 1] = cplx<T>{T(0), T(0)};
+      }
+    };
+    // final state = last entangler applied to the last boundary
+    load_boundary(n_layers - 1);
+    if constexpr (ENT == ENT_PERM) {
+      permute<T, A, G, 1>(x1, sm.pt + (n_layers - 1) * D, buf, gl, lane_hi);
+    } else if constexpr (ENT == ENT_PHASE) {
+      const cplx<T>* ph = sm.ph + (n_layers - 1) * D;
+#pragma unroll
+      for (int r = 0; r < A; ++r) xa[0][r] = cmul(xa[0][r], ph[r * G + gl]);
     }
     // adjoint seeds: lambda = 2 w psi + 2 sum_k v_k dpsi_k, mu_k = 2 v_k psi
     T gsel[N];
@@ -338,48 +316,50 @@ pqc_backward_layer(PlanDev plan, const unsigned char* __restrict__ tables, int n
       xa[1][r] = sidx == 0 ? t : cplx<T>{w * p.re, w * p.im};
     }
     // reverse sweep over layers
+    // Single-qubit gates of one layer act on distinct wires and commute, so
+    // each may be taken as the layer's last: its post-gate state is the stored
+    // boundary x_l and its post-gate adjoint the adjoint a_l at that boundary.
+    // Every M'_q of the layer is then an outer product of (a_l, x_l) and only
+    // the adjoint is propagated (a <- U_q^dagger a); no state is un-computed.
     for (int l = n_layers - 1; l >= 0; --l) {
+      load_boundary(l);
       if constexpr (ENT == ENT_PERM) {
-        permute<T, A, G, 2>(xa, sm.pti + l * D, buf, gl, lane_hi);
+        permute<T, A, G, 1>(a1, sm.pti + l * D, buf, gl, lane_hi);
       } else if constexpr (ENT == ENT_PHASE) {
         const cplx<T>* ph = sm.ph + l * D;
         T* acc = accP + l * D;
 #pragma unroll
         for (int r = 0; r < A; ++r) {
-          T pv = xa[1][r].im * xa[0][r].re - xa[1][r].re * xa[0][r].im;
+          const cplx<T> e = ph[r * G + gl];
+          const cplx<T> xp = cmul(xa[0][r], e);  // post-entangler state
+          T pv = xa[1][r].im * xp.re - xa[1][r].re * xp.im;
 #pragma unroll
           for (int mk = G; mk < 32; mk <<= 1) pv += __shfl_xor_sync(0xffffffffu, pv, mk);
           if (lane_hi == 0) acc[r * G + gl] += pv;
-          const cplx<T> e = {ph[r * G + gl].re, -ph[r * G + gl].im};
-          xa[0][r] = cmul(xa[0][r], e);
-          xa[1][r] = cmul(xa[1][r], e);
+          xa[1][r] = cmul(xa[1][r], cplx<T>{e.re, -e.im});
         }
       }
       const cplx<T>* Ul = sm.U + 4 * N * l;
       T* accl = accU + 8 * N * l;
-      // register wires N-1 .. LB (bits 0 .. AB-1): two gate copies (bits 0, 1)
-      // plus a half-swap of the register index; with the permutation entangler
-      // (larger loop body) one copy + one-bit rotation keeps the I-cache happier
-      if constexpr (AB == 4 && ENT != ENT_PERM) {
-        for (int i = 0; i < AB; i += 2) {
-          const int q = N - 1 - i;
-          gate_bwd<T, N, N - 1>(xa[0], xa[1], Ul + 4 * q, accl + 8 * q, gl, lane);
-          gate_bwd<T, N, N - 2>(xa[0], xa[1], Ul + 4 * (q - 1), accl + 8 * (q - 1), gl, lane);
-          swap_halves<T, AB>(xa[0]);
-          swap_halves<T, AB>(xa[1]);
-        }
-      } else {
-        for (int i = 0; i < AB; ++i) {
-          const int q = N - 1 - i;
-          gate_bwd<T, N, N - 1>(xa[0], xa[1], Ul + 4 * q, accl + 8 * q, gl, lane);
-          if constexpr (AB > 1) {
-            rotate_regs<T, AB>(xa[0]);
-            rotate_regs<T, AB>(xa[1]);
-          }
-        }
+      // outer products: register wires (compile-time pairings), then lane wires
+      static_for<0, AB>([&](auto rb_) {
+        constexpr int RB = decltype(rb_)::value;
+        outer_reg<T, A, RB>(xa[0], xa[1], accl + 8 * (N - 1 - RB), lane);
+      });
+      for (int q = 0; q < LB; ++q)
+        outer_lane<T, A>(xa[0], xa[1], accl + 8 * q, 1 << (LB - 1 - q), gl, lane);
+      // adjoint propagation through every U_q^dagger
+      static_for<0, AB>([&](auto rb_) {
+        constexpr int RB = decltype(rb_)::value;
+        const cplx<T>* U = Ul + 4 * (N - 1 - RB);
+        gate_reg<RB, T, A, 1>(a1, conj(U[0]), conj(U[2]), conj(U[1]), conj(U[3]));
+      });
+      for (int q = 0; q < LB; ++q) {
+        const cplx<T>* U = Ul + 4 * q;
+        const int lb = LB - 1 - q;
+        gate_lane<T, A, 1>(a1, 1 << lb, (gl >> lb) & 1, conj(U[0]), conj(U[2]), conj(U[1]),
+                           conj(U[3]));
       }
-      for (int q = LB - 1; q >= 0; --q)  // lane wires, one shared copy
-        gate_bwd_lane<T, N>(xa[0], xa[1], Ul + 4 * q, accl + 8 * q, 1 << (LB - 1 - q), gl, lane);
     }
     // embedding gradient: xa[1] = phibar (s = 0) or mu_k (s = k+1)
     embed<T, N, AB>(c, sn, dth, false, gl, xa[0]);

@@ -4,9 +4,10 @@ Conventions: 8 FLOP per complex MAC; a dense 2x2 gate on one
 state = D/2 pairs x 4 MACs = 16 D; a diagonal phase step = 6 D; a
 permutation = 0; 4 states (psi and its x/y/t tangents).
   F_fwd+tan = 4 (16 D n_u1 + 6 D n_phase) + 32 D (embedding) + 4 D (n + 4) (readout)
-  F_adjoint = 3 x the 4-state ansatz term (un-compute 4 states, propagate 4
-              adjoints, 2x2 outer-product accumulation per gate)
-For 7 qubits x 4 layers (strongly): 2.39e5 and 6.88e5 FLOP/point.
+  F_adjoint = 2 x the 4-state ansatz term (propagate 4 adjoints, 2x2
+              outer-product accumulation per gate); the layer-boundary states
+              K1 checkpoints mean no state is un-computed
+For 7 qubits x 4 layers (strongly): 2.39e5 and 4.59e5 FLOP/point.
 """
 from __future__ import annotations
 
@@ -19,7 +20,7 @@ def pqc_flops(circuit):
     n_ph = sum(1 for s in plan if s[0] == "phases")
     ansatz = 16 * D * n_u1 + 6 * D * n_ph
     f_fwd = 4 * ansatz + 32 * D + 4 * D * (n + 4)
-    f_adj = 3 * 4 * ansatz
+    f_adj = 2 * 4 * ansatz
     return f_fwd, f_adj
 
 

@@ -54,6 +54,9 @@ def main():
                 R = min(R, (1 << (24 if n <= 8 else 26)) >> n) if n > 8 else R
                 if quick:
                     R = min(R, 1 << 14)
+                # layer-boundary hand-off (n <= 8): 4 states x 2^n x L per row, keep <= 4 GiB
+                if n <= 8:
+                    R = min(R, (4 << 30) // (L * 4 * (1 << n) * 8))
                 c = build_circuit(kind, n, L)
                 a = torch.as_tensor(rng.uniform(-0.9, 0.9, (R, n)), dtype=torch.float32, device="cuda")
                 da = torch.as_tensor(rng.normal(size=(3, R, n)), dtype=torch.float32, device="cuda")
