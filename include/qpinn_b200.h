@@ -236,6 +236,17 @@ int qpinn_adam_step(int dtype, int64_t n, void* params, const void* grad, void* 
                     void* v, int64_t t, double lr, double beta1, double beta2,
                     double eps, const double* loss_dev, int32_t* flag_dev, void* stream);
 
+/* ---- FP32-accurate tensor-core GEMM (the trunk's dense layers) ------------ */
+/* C[m,n] = A[m,k] B[n,k]^T in float32 on the tcgen05 TF32 tensor cores with
+ * a 3-way hi/lo operand split (FP32-class accuracy).  Row-major, K
+ * contiguous; A, B, C 16-byte aligned with lda, ldb multiples of 4; n <= 256.
+ * Replaces the dense layers' stacked dual GEMM (ops.py:282-298 on
+ * network.py:294-298).  Workspace holds the split B. */
+size_t qpinn_gemm_f32_workspace_bytes(int n, int k);
+int qpinn_gemm_f32(int64_t m, int n, int k, const void* a, int64_t lda, const void* b,
+                   int64_t ldb, void* c, int64_t ldc, void* workspace,
+                   size_t workspace_bytes, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -83,6 +83,8 @@ SIGNATURES = [
     ("qpinn_trunk_backward", _I, [C.POINTER(TrunkDesc), _I, _I64, _VP, _VP, _VP, _VP, _VP, _VP,
                                   _VP, _VP, _SZ, _VP]),
     ("qpinn_adam_step", _I, [_I, _I64, _VP, _VP, _VP, _VP, _I64, _D, _D, _D, _D, _VP, _VP, _VP]),
+    ("qpinn_gemm_f32_workspace_bytes", _SZ, [_I, _I]),
+    ("qpinn_gemm_f32", _I, [_I64, _I, _I, _VP, _I64, _VP, _I64, _VP, _I64, _VP, _SZ, _VP]),
 ]
 
 _lib = None
@@ -146,8 +148,9 @@ def lib():
                 raise E.NativeLibraryError(
                     f"{LIB_PATH} is missing: build it with `python -m "
                     f"paper_2506_23246_b200.build` (there is no CPU fallback)")
+            path = os.environ.get("QPINN_LIB_OVERRIDE", LIB_PATH)  # kernel-variant experiments
             try:
-                h = C.CDLL(LIB_PATH)
+                h = C.CDLL(path)
             except OSError as e:  # pragma: no cover - depends on the box
                 raise E.NativeLibraryError(f"cannot load {LIB_PATH}: {e}") from e
             for name, res, args in SIGNATURES:

@@ -38,6 +38,14 @@ template <typename T>
 __device__ __forceinline__ cplx<T> cmulc(cplx<T> a, cplx<T> b) {
   return {a.re * b.re + a.im * b.im, a.re * b.im - a.im * b.re};
 }
+// (re, im) += conj(a) * b as four FMAs (no rounding of the product on its own)
+template <typename T>
+__device__ __forceinline__ void cmac_c(T& re, T& im, cplx<T> a, cplx<T> b) {
+  re = fma(a.re, b.re, re);
+  re = fma(a.im, b.im, re);
+  im = fma(a.re, b.im, im);
+  im = fma(-a.im, b.re, im);
+}
 // a*x + b*y
 template <typename T>
 __device__ __forceinline__ cplx<T> cmul2(cplx<T> a, cplx<T> x, cplx<T> b, cplx<T> y) {

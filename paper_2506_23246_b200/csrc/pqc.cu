@@ -245,8 +245,8 @@ pqc_backward_kernel(PlanDev plan, const __grid_constant__ StepTable steps, int s
           for (int r = 0; r < A; ++r) {
             const cplx<T> xs = xa[0][r], as = xa[1][r];
             const cplx<T> xp = shfl_xor_c(xs, 1 << lb), ap = shfl_xor_c(as, 1 << lb);
-            const cplx<T> t1 = cmulc(as, xs), t2 = cmulc(as, xp);
-            ms_re += t1.re; ms_im += t1.im; mc_re += t2.re; mc_im += t2.im;
+            cmac_c(ms_re, ms_im, as, xs);
+            cmac_c(mc_re, mc_im, as, xp);
             xa[0][r] = cmul2(cs, xs, cp, xp);
             xa[1][r] = cmul2(cs, as, cp, ap);
           }
@@ -263,11 +263,10 @@ pqc_backward_kernel(PlanDev plan, const __grid_constant__ StepTable steps, int s
               if (r & (1 << bsel)) continue;
               const int r1 = r | (1 << bsel);
               const cplx<T> x0 = xa[0][r], x1 = xa[0][r1], a0 = xa[1][r], a1 = xa[1][r1];
-              cplx<T> t;
-              t = cmulc(a0, x0); m[0] += t.re; m[1] += t.im;
-              t = cmulc(a0, x1); m[2] += t.re; m[3] += t.im;
-              t = cmulc(a1, x0); m[4] += t.re; m[5] += t.im;
-              t = cmulc(a1, x1); m[6] += t.re; m[7] += t.im;
+              cmac_c(m[0], m[1], a0, x0);
+              cmac_c(m[2], m[3], a0, x1);
+              cmac_c(m[4], m[5], a1, x0);
+              cmac_c(m[6], m[7], a1, x1);
               xa[0][r] = cmul2(h00, x0, h01, x1);
               xa[0][r1] = cmul2(h10, x0, h11, x1);
               xa[1][r] = cmul2(h00, a0, h01, a1);

@@ -339,11 +339,10 @@ __device__ __forceinline__ void gate_bwd_bit0(cplx<T> (&x)[A], cplx<T> (&a)[A], 
 #pragma unroll
   for (int r = 0; r < A; r += 2) {
     const cplx<T> x0 = x[r], x1 = x[r + 1], a0 = a[r], a1 = a[r + 1];
-    cplx<T> t;
-    t = cmulc(a0, x0); m[0] += t.re; m[1] += t.im;
-    t = cmulc(a0, x1); m[2] += t.re; m[3] += t.im;
-    t = cmulc(a1, x0); m[4] += t.re; m[5] += t.im;
-    t = cmulc(a1, x1); m[6] += t.re; m[7] += t.im;
+    cmac_c(m[0], m[1], a0, x0);
+    cmac_c(m[2], m[3], a0, x1);
+    cmac_c(m[4], m[5], a1, x0);
+    cmac_c(m[6], m[7], a1, x1);
     x[r] = cmul2(h00, x0, h01, x1);
     x[r + 1] = cmul2(h10, x0, h11, x1);
     a[r] = cmul2(h00, a0, h01, a1);
@@ -389,8 +388,8 @@ __device__ __forceinline__ void gate_bwd_x(cplx<T> (&x)[Geo::A], cplx<T> (&a)[Ge
   T ms_re = 0, ms_im = 0, mc_re = 0, mc_im = 0;
 #pragma unroll
   for (int r = 0; r < A; ++r) {
-    const cplx<T> t1 = cmulc(a[r], x[r]), t2 = cmulc(a[r], xp[r]);
-    ms_re += t1.re; ms_im += t1.im; mc_re += t2.re; mc_im += t2.im;
+    cmac_c(ms_re, ms_im, a[r], x[r]);
+    cmac_c(mc_re, mc_im, a[r], xp[r]);
     x[r] = cmul2(cs, x[r], cp, xp[r]);
     a[r] = cmul2(cs, a[r], cp, ap[r]);
   }

@@ -294,6 +294,37 @@ __device__ __forceinline__ void load_point_fast(int scale, const T* __restrict__
   }
 }
 
+// load_point_fast with the per-qubit transcendental work spread over the
+// point's lanes: lane j < N of the point evaluates qubit j once and the values
+// are broadcast with shuffles (the 4G lanes of a point otherwise repeat the
+// same N square roots and divisions).  Needs LPP >= N lanes per point (true
+// with tangents, NSL = 4); otherwise every lane evaluates every qubit.
+template <typename T, int N, int LPP>
+__device__ __forceinline__ void load_point_lanes(int scale, const T* __restrict__ act,
+                                                 const T* __restrict__ act_tan, int64_t R,
+                                                 int64_t s, bool valid, int k_own, int lane,
+                                                 T (&c)[N], T (&sn)[N], T (&dth)[N],
+                                                 T (&s1)[N], T (&s2)[N], T& amax) {
+  if constexpr (LPP < N) {
+    load_point_fast<T, N>(scale, act, act_tan, R, s, valid, k_own, c, sn, dth, s1, s2, amax);
+    return;
+  }
+  const int j = lane % LPP, src0 = lane - j;
+  T a = (valid && j < N) ? act[s * N + j] : T(0);
+  amax = fmax(amax, fabs(a));
+  a = fmin(fmax(a, T(-1)), T(1));
+  T cj, sj, s1j, s2j;
+  half_angle<T>(scale, a, cj, sj, s1j, s2j);
+#pragma unroll
+  for (int q = 0; q < N; ++q) {
+    c[q] = __shfl_sync(0xffffffffu, cj, src0 + q);
+    sn[q] = __shfl_sync(0xffffffffu, sj, src0 + q);
+    s1[q] = __shfl_sync(0xffffffffu, s1j, src0 + q);
+    s2[q] = __shfl_sync(0xffffffffu, s2j, src0 + q);
+    dth[q] = (valid && k_own >= 0) ? s1[q] * act_tan[((int64_t)k_own * R + s) * N + q] : T(0);
+  }
+}
+
 // Per-call gate tables (u1 matrices, phase diagonals, layout-mapped
 // permutations) built once by a small kernel into global memory with exactly
 // the shared-memory layout of smem_layout(bwd = true); the layer kernels'

@@ -35,11 +35,10 @@ __device__ __forceinline__ void outer_reg(const cplx<T> (&x)[A], const cplx<T> (
   for (int r = 0; r < A; ++r) {
     if (r & S) continue;
     const int r1 = r | S;
-    cplx<T> t;
-    t = cmulc(a[r], x[r]);   m[0] += t.re; m[1] += t.im;
-    t = cmulc(a[r], x[r1]);  m[2] += t.re; m[3] += t.im;
-    t = cmulc(a[r1], x[r]);  m[4] += t.re; m[5] += t.im;
-    t = cmulc(a[r1], x[r1]); m[6] += t.re; m[7] += t.im;
+    cmac_c(m[0], m[1], a[r], x[r]);
+    cmac_c(m[2], m[3], a[r], x[r1]);
+    cmac_c(m[4], m[5], a[r1], x[r]);
+    cmac_c(m[6], m[7], a[r1], x[r1]);
   }
   const T v = warp_reduce8(m, lane);
   if ((lane & 3) == 0) acc[lane >> 2] += v;
@@ -55,8 +54,8 @@ __device__ __forceinline__ void outer_lane(const cplx<T> (&x)[A], const cplx<T> 
 #pragma unroll
   for (int r = 0; r < A; ++r) {
     const cplx<T> xp = shfl_xor_c(x[r], lm);
-    const cplx<T> t1 = cmulc(a[r], x[r]), t2 = cmulc(a[r], xp);
-    ms_re += t1.re; ms_im += t1.im; mc_re += t2.re; mc_im += t2.im;
+    cmac_c(ms_re, ms_im, a[r], x[r]);
+    cmac_c(mc_re, mc_im, a[r], xp);
   }
   // own row i: beta = 0 -> M'(0,0), M'(0,1); beta = 1 -> M'(1,1), M'(1,0)
   T m[8];
@@ -119,9 +118,16 @@ __device__ __forceinline__ void ld_pair(const cplx<double>* p, cplx<double>& a,
   b = {v.x, v.y};
 }
 
+#ifndef QPINN_K1_MINB
+#define QPINN_K1_MINB 5
+#endif
+#ifndef QPINN_K2_MINB
+#define QPINN_K2_MINB 2
+#endif
+
 // ---- K1 -----------------------------------------------------------------------------------
 template <typename T, int N, int NSL, int ENT>
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kThreads, sizeof(T) == 4 && N <= 7 ? QPINN_K1_MINB : 1)
 pqc_forward_layer(PlanDev plan, const unsigned char* __restrict__ tables, int n_layers, int scale,
                   int64_t R, const T* __restrict__ act, const T* __restrict__ act_tan,
                   const T* __restrict__ qp, T* __restrict__ z,
@@ -149,7 +155,8 @@ pqc_forward_layer(PlanDev plan, const unsigned char* __restrict__ tables, int n_
     const int64_t s = base + warp * SPW + pw;
     const bool valid = s < R;
     T c[N], sn[N], dth[N], s1[N], s2[N];
-    load_point_fast<T, N>(scale, act, act_tan, R, s, valid, sidx - 1, c, sn, dth, s1, s2, amax);
+    load_point_lanes<T, N, LPP>(scale, act, act_tan, R, s, valid, sidx - 1, lane, c, sn, dth, s1, s2,
+                                amax);
     cplx<T> st[1][A];
     embed<T, N, AB>(c, sn, dth, sidx > 0, gl, st[0]);
     for (int l = 0; l < n_layers; ++l) {
@@ -233,7 +240,7 @@ pqc_forward_layer(PlanDev plan, const unsigned char* __restrict__ tables, int n_
 
 // ---- K2 -----------------------------------------------------------------------------------
 template <typename T, int N, int ENT>
-__global__ void __launch_bounds__(kThreads, sizeof(T) == 4 && N <= 7 ? 3 : 1)
+__global__ void __launch_bounds__(kThreads, sizeof(T) == 4 && N <= 7 ? QPINN_K2_MINB : 1)
 pqc_backward_layer(PlanDev plan, const unsigned char* __restrict__ tables, int n_layers,
                    int scale, int64_t R, const T* __restrict__ act,
                    const T* __restrict__ act_tan, const T* __restrict__ qp,
@@ -265,8 +272,8 @@ pqc_backward_layer(PlanDev plan, const unsigned char* __restrict__ tables, int n
     const int64_t s = base + warp * SPW + pw;
     const bool valid = s < R;
     T c[N], sn[N], dth[N], s1v[N], s2v[N], amax_unused = T(0);
-    load_point_fast<T, N>(scale, act, act_tan, R, s, valid, sidx - 1, c, sn, dth, s1v, s2v,
-                          amax_unused);
+    load_point_lanes<T, N, LPP>(scale, act, act_tan, R, s, valid, sidx - 1, lane, c, sn, dth,
+                                s1v, s2v, amax_unused);
     cplx<T> xa[2][A];  // [0] this lane's layer-boundary state, [1] its adjoint
     cplx<T>(&x1)[1][A] = reinterpret_cast<cplx<T>(&)[1][A]>(xa[0]);
     cplx<T>(&a1)[1][A] = reinterpret_cast<cplx<T>(&)[1][A]>(xa[1]);
@@ -385,23 +392,24 @@ pqc_backward_layer(PlanDev plan, const unsigned char* __restrict__ tables, int n
         rho[r].im += dth[LB + qi] * xa[1][r ^ Sm].im;
       }
     }
+    // H_q = Im sum conj(xa1) X_q phi, P_q = Re sum conj(rho) X_q phi (rho = 0 in
+    // the psi lanes, whose dtheta is 0): g_theta = H/2 (psi) or -P/4, g_dtheta = H/2
     T gt[N], gd[N];
 #pragma unroll
     for (int q = 0; q < N; ++q) {
-      gt[q] = T(0);
-      gd[q] = T(0);
+      T H = T(0), P = T(0);
 #pragma unroll
       for (int r = 0; r < A; ++r) {
         cplx<T> y;
         if (q < LB) y = shfl_xor_c(xa[0][r], 1 << (LB - 1 - q));
         else y = xa[0][r ^ (1 << (N - 1 - q))];
-        const T half = T(0.5) * (xa[1][r].re * y.im - xa[1][r].im * y.re);
-        if (sidx == 0) gt[q] += half;
-        else {
-          gt[q] -= T(0.25) * (rho[r].re * y.re + rho[r].im * y.im);
-          gd[q] += half;
-        }
+        H = fma(xa[1][r].re, y.im, H);
+        H = fma(-xa[1][r].im, y.re, H);
+        P = fma(rho[r].re, y.re, P);
+        P = fma(rho[r].im, y.im, P);
       }
+      gt[q] = (sidx == 0 ? T(0.5) * H : T(0)) - T(0.25) * P;
+      gd[q] = sidx == 0 ? T(0) : T(0.5) * H;
     }
 #pragma unroll
     for (int m = 1; m < G; m <<= 1)

@@ -1,0 +1,442 @@
+// FP32-accurate tensor-core GEMM (3xTF32 on tcgen05) for the trunk.
+//
+// C[M,N] = A[M,K] B[N,K]^T, fp32 in / fp32 out, both operands K-major
+// (row-major with K contiguous).  Persistent CTAs walk 128 x BN output tiles;
+// per CTA (352 threads):
+//   warp 8      TMA producer for A (fp32), 32 K-columns (one 128-byte swizzle
+//               row) per stage, 3 stages ahead
+//   warp 10     TMA producer for the pre-split B_hi / B_lo tiles (L2-resident)
+//   warps 0-3   split A into A_hi / A_lo operand buffers
+//   warp 9      MMA issuer (one thread): per stage 4 K-steps x 3 products
+//               A_lo B_hi + A_hi B_lo + A_hi B_hi into a fresh TMEM buffer
+//   warps 4-7   promote every k-block partial from TMEM into fp32 registers
+//               (the tensor core's own fp32 accumulation truncates, so long
+//               K chains drift; 32-deep partials + IEEE adds stay FP32-class)
+//               and run the fused epilogue, overlapping the next tile's MMAs
+// Epilogues: plain store, or the dual tanh of a dense layer with tangents
+// (network.py:294-298 on ops.py:282-298): rows are [value; d/dx; d/dy; d/dt]
+// blocks of the same 32 points, y = tanh(u0 + b), dy_k = (1 - y^2) du_k.
+// B (the layer weights, small) is split once per call into a workspace.
+#include <cudaTypedefs.h>
+
+#include <mutex>
+
+#include "tc_gemm.cuh"
+
+namespace qpinn {
+namespace tc {
+
+constexpr int kBM = 128, kBK = 32;
+constexpr int kABytes = kBM * kBK * 4;  // 16 KB fp32 tile
+constexpr int kThreadsGemm = 352;
+enum { EPI_STORE = 0, EPI_TANH = 1 };
+
+template <int BN>
+struct GemmCfg {
+  static constexpr int kBBytes = BN * kBK * 4;
+  static constexpr int kRaw = 3;   // fp32 A stages in flight from HBM
+  static constexpr int kOps = 2;   // split A buffers (A_hi, A_lo)
+  static constexpr int kOpBytes = 2 * kABytes;
+  static constexpr int kBS = 3;    // B_hi / B_lo stages (from L2)
+  static constexpr int kBStage = 2 * kBBytes;
+  static constexpr int kNB = 4;    // TMEM partial buffers
+  static constexpr int kTmemCols = kNB * BN;
+  static constexpr int kSbuf = 32 * BN * 4;
+  static constexpr int kSmem =
+      kRaw * kABytes + kOps * kOpBytes + kBS * kBStage + kSbuf + 1024 + 512;
+};
+
+struct GemmArgs {
+  int64_t M;      // rows of A / C (EPI_TANH: 4 R)
+  int64_t R;      // EPI_TANH: points per channel block
+  int N, K;
+  float* C;
+  int64_t ldc;
+  const float* bias;  // EPI_TANH
+};
+
+template <int BN, int EPI>
+__global__ void __launch_bounds__(kThreadsGemm, 1)
+gemm3_kernel(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUtensorMap mBhi,
+             const __grid_constant__ CUtensorMap mBlo, const GemmArgs g) {
+  using Cfg = GemmCfg<BN>;
+  constexpr int RS = Cfg::kRaw, OS = Cfg::kOps, BS = Cfg::kBS, NB = Cfg::kNB;
+  extern __shared__ unsigned char smem_raw[];
+  unsigned char* smem = (unsigned char*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  unsigned char* raw = smem;                        // [RS][16 KB] fp32 A tiles
+  unsigned char* ops = smem + RS * kABytes;         // [OS][A_hi | A_lo]
+  unsigned char* bst = ops + OS * Cfg::kOpBytes;    // [BS][B_hi | B_lo]
+  float* sbuf = (float*)(bst + BS * Cfg::kBStage);
+  uint64_t* raw_full = (uint64_t*)((unsigned char*)sbuf + Cfg::kSbuf);
+  uint64_t* raw_empty = raw_full + RS;
+  uint64_t* b_full = raw_empty + RS;
+  uint64_t* b_empty = b_full + BS;
+  uint64_t* conv = b_empty + BS;
+  uint64_t* op_empty = conv + OS;
+  uint64_t* tfull = op_empty + OS;
+  uint64_t* tempty = tfull + NB;
+  uint32_t* tmem_slot = (uint32_t*)(tempty + NB);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nk = (g.K + kBK - 1) / kBK;
+  const int64_t n_mt = EPI == EPI_TANH ? (g.R + 31) / 32 : (g.M + kBM - 1) / kBM;
+  const int n_nt = (g.N + BN - 1) / BN;
+  const int64_t n_tiles = n_mt * n_nt;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < RS; ++s) {
+      mbar_init(raw_full + s, 1);
+      mbar_init(raw_empty + s, 4);
+    }
+    for (int s = 0; s < OS; ++s) {
+      mbar_init(conv + s, 4);
+      mbar_init(op_empty + s, 1);
+    }
+    for (int s = 0; s < BS; ++s) {
+      mbar_init(b_full + s, 1);
+      mbar_init(b_empty + s, 1);
+    }
+    for (int b = 0; b < NB; ++b) {
+      mbar_init(tfull + b, 1);
+      mbar_init(tempty + b, 4);
+    }
+    mbar_init_fence();
+  }
+  if (warp == 8 && lane == 0) {
+    tma_prefetch(&mA);
+    tma_prefetch(&mBhi);
+    tma_prefetch(&mBlo);
+  }
+  if (warp == 9) tmem_alloc(tmem_slot, Cfg::kTmemCols);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 8) {  // ---- TMA producer for A (runs RS k-blocks ahead)
+    if (lane == 0) {
+      int64_t j = 0;
+      for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+        const int64_t mt = t / n_nt;
+        for (int kb = 0; kb < nk; ++kb, ++j) {
+          const int r = (int)(j % RS);
+          if (j >= RS) mbar_wait(raw_empty + r, (uint32_t)(((j / RS) - 1) & 1));
+          unsigned char* st = raw + r * kABytes;
+          mbar_expect_tx(raw_full + r, kABytes);
+          if constexpr (EPI == EPI_TANH) {
+#pragma unroll
+            for (int c = 0; c < 4; ++c)
+              tma_load_2d(st + c * (kABytes / 4), &mA, raw_full + r, kb * kBK,
+                          (int)(c * g.R + mt * 32));
+          } else {
+            tma_load_2d(st, &mA, raw_full + r, kb * kBK, (int)(mt * kBM));
+          }
+        }
+      }
+    }
+  } else if (warp == 10) {  // ---- TMA producer for the split B tiles (L2-resident)
+    if (lane == 0) {
+      int64_t j = 0;
+      for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+        const int nt = (int)(t % n_nt);
+        for (int kb = 0; kb < nk; ++kb, ++j) {
+          const int e = (int)(j % BS);
+          if (j >= BS) mbar_wait(b_empty + e, (uint32_t)(((j / BS) - 1) & 1));
+          unsigned char* st = bst + e * Cfg::kBStage;
+          mbar_expect_tx(b_full + e, 2 * Cfg::kBBytes);
+          tma_load_2d(st, &mBhi, b_full + e, kb * kBK, nt * BN);
+          tma_load_2d(st + Cfg::kBBytes, &mBlo, b_full + e, kb * kBK, nt * BN);
+        }
+      }
+    }
+  } else if (warp == 9) {  // ---- MMA issuer
+    if (lane == 0) {
+      constexpr uint32_t idesc = idesc_tf32(kBM, BN);
+      int64_t j = 0;
+      for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+        for (int kb = 0; kb < nk; ++kb, ++j) {
+          const int o = (int)(j % OS), e = (int)(j % BS), b = (int)(j % NB);
+          if (j >= NB) mbar_wait(tempty + b, (uint32_t)(((j / NB) - 1) & 1));
+          mbar_wait(conv + o, (uint32_t)((j / OS) & 1));
+          mbar_wait(b_full + e, (uint32_t)((j / BS) & 1));
+          tc_fence_after();
+          const uint32_t a_hi = smem_u32(ops + o * Cfg::kOpBytes);
+          const uint32_t a_lo = a_hi + kABytes;
+          const uint32_t b_hi = smem_u32(bst + e * Cfg::kBStage);
+          const uint32_t b_lo = b_hi + Cfg::kBBytes;
+          const uint32_t d = tmem + b * BN;
+#pragma unroll
+          for (int k = 0; k < kBK / 8; ++k) {
+            const uint32_t off = k * 32;  // 8 tf32 = 32 bytes along the swizzled row
+#ifndef QPINN_GEMM_ONEMMA
+            mma_tf32(d, desc_k_sw128(a_lo + off), desc_k_sw128(b_hi + off), idesc, k != 0);
+            mma_tf32(d, desc_k_sw128(a_hi + off), desc_k_sw128(b_lo + off), idesc, 1);
+            mma_tf32(d, desc_k_sw128(a_hi + off), desc_k_sw128(b_hi + off), idesc, 1);
+#else
+            mma_tf32(d, desc_k_sw128(a_hi + off), desc_k_sw128(b_hi + off), idesc, k != 0);
+#endif
+          }
+          mma_commit(op_empty + o);
+          mma_commit(b_empty + e);
+          mma_commit(tfull + b);
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp < 4) {  // ---- split A into an operand buffer
+    int64_t j = 0;
+    for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+      for (int kb = 0; kb < nk; ++kb, ++j) {
+        const int r = (int)(j % RS), o = (int)(j % OS);
+        if (j >= OS) mbar_wait(op_empty + o, (uint32_t)(((j / OS) - 1) & 1));
+        unsigned char* op = ops + o * Cfg::kOpBytes;
+        mbar_wait(raw_full + r, (uint32_t)((j / RS) & 1));
+        // layout-free: the swizzled tile is split as flat 16-byte chunks; all
+        // loads first (one latency per k-block), then split and store
+        const uint32_t a_src = smem_u32(raw + r * kABytes) + threadIdx.x * 16;
+        const uint32_t a_dst = smem_u32(op) + threadIdx.x * 16;
+        constexpr int CH = kABytes / 16 / 128;  // chunks per thread
+        float4 v[CH];
+#ifndef QPINN_GEMM_NOCONV
+#pragma unroll
+        for (int i = 0; i < CH; ++i) v[i] = lds128(a_src + i * 2048);
+#pragma unroll
+        for (int i = 0; i < CH; ++i) {
+          float4 h, l;
+          split_tf32(v[i].x, h.x, l.x);
+          split_tf32(v[i].y, h.y, l.y);
+          split_tf32(v[i].z, h.z, l.z);
+          split_tf32(v[i].w, h.w, l.w);
+          sts128(a_dst + i * 2048, h);
+          sts128(a_dst + kABytes + i * 2048, l);
+        }
+#else
+        (void)v; (void)a_src; (void)a_dst;
+#endif
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          mbar_arrive(raw_empty + r);
+          mbar_arrive(conv + o);
+        }
+      }
+    }
+  } else {  // ---- warps 4-7: promote partials, epilogue
+    const int q = warp - 4;  // TMEM lanes 32q .. 32q+31
+    const uint32_t lane_base = (uint32_t)(q * 32) << 16;
+    int64_t j = 0;
+    for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+      const int64_t mt = t / n_nt;
+      const int n0 = (int)(t % n_nt) * BN;
+      float acc[BN];
+#pragma unroll
+      for (int c = 0; c < BN; ++c) acc[c] = 0.f;
+      for (int kb = 0; kb < nk; ++kb, ++j) {
+        const int b = (int)(j % NB);
+        mbar_wait(tfull + b, (uint32_t)((j / NB) & 1));
+        tc_fence_after();
+#pragma unroll
+        for (int c0 = 0; c0 < BN; c0 += 32) {
+          float v[32];
+#ifndef QPINN_GEMM_NOPROMOTE
+          tmem_ld32(tmem + lane_base + b * BN + c0, v);
+#else
+#pragma unroll
+          for (int i = 0; i < 32; ++i) v[i] = 0.f;
+#endif
+#pragma unroll
+          for (int i = 0; i < 32; ++i) acc[c0 + i] += v[i];
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(tempty + b);
+      }
+      if constexpr (EPI == EPI_STORE) {
+        const int64_t row = mt * kBM + q * 32 + lane;
+        if (row < g.M) {
+          float* dst = g.C + row * g.ldc + n0;
+          if (n0 + BN <= g.N && (g.ldc & 3) == 0) {
+#pragma unroll
+            for (int c = 0; c < BN; c += 4)
+              *reinterpret_cast<float4*>(dst + c) =
+                  make_float4(acc[c], acc[c + 1], acc[c + 2], acc[c + 3]);
+          } else {
+#pragma unroll
+            for (int c = 0; c < BN; ++c)
+              if (n0 + c < g.N) dst[c] = acc[c];
+          }
+        }
+      } else {  // EPI_TANH: q = channel, lane = point
+        const int64_t p = mt * 32 + lane;
+        if (q == 0) {
+#pragma unroll
+          for (int c = 0; c < BN; ++c) {
+            const float bv = n0 + c < g.N ? __ldg(g.bias + n0 + c) : 0.f;
+            const float y = tanhf(acc[c] + bv);
+            sbuf[c * 32 + lane] = 1.f - y * y;
+            acc[c] = y;
+          }
+        }
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        if (q != 0) {
+#pragma unroll
+          for (int c = 0; c < BN; ++c) acc[c] *= sbuf[c * 32 + lane];
+        }
+        if (p < g.R) {
+          float* dst = g.C + ((int64_t)q * g.R + p) * g.ldc + n0;
+          if (n0 + BN <= g.N && (g.ldc & 3) == 0) {
+#pragma unroll
+            for (int c = 0; c < BN; c += 4)
+              *reinterpret_cast<float4*>(dst + c) =
+                  make_float4(acc[c], acc[c + 1], acc[c + 2], acc[c + 3]);
+          } else {
+#pragma unroll
+            for (int c = 0; c < BN; ++c)
+              if (n0 + c < g.N) dst[c] = acc[c];
+          }
+        }
+        asm volatile("bar.sync 1, 128;" ::: "memory");  // sbuf reused by the next tile
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 9) tmem_dealloc(tmem, Cfg::kTmemCols);
+}
+
+// B [N,K] (ld ldb) -> B_hi, B_lo [N, ldk] (zero padded to ldk)
+__global__ void split_rows(const float* __restrict__ B, int N, int K, int64_t ldb, int ldk,
+                           float* __restrict__ hi, float* __restrict__ lo) {
+  const int64_t n = (int64_t)N * ldk;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int r = (int)(i / ldk), c = (int)(i % ldk);
+    const float v = c < K ? B[r * ldb + c] : 0.f;
+    const float h = rna_tf32(v);
+    hi[i] = h;
+    lo[i] = rna_tf32(v - h);
+  }
+}
+
+// W [K,N] row-major (a layer's weights) -> (W^T)_hi, (W^T)_lo [N, ldk]
+__global__ void split_transpose(const float* __restrict__ W, int K, int N, int ldk,
+                                float* __restrict__ hi, float* __restrict__ lo) {
+  const int64_t n = (int64_t)N * ldk;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int r = (int)(i / ldk), c = (int)(i % ldk);
+    const float v = c < K ? W[(int64_t)c * N + r] : 0.f;
+    const float h = rna_tf32(v);
+    hi[i] = h;
+    lo[i] = rna_tf32(v - h);
+  }
+}
+
+// ---- host --------------------------------------------------------------------------------
+static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = (PFN_cuTensorMapEncodeTiled_v12000)p;
+  });
+  return fn;
+}
+
+// 2-D fp32 map over rows x cols (ld elements), box = 32 columns x box_rows, 128-byte swizzle
+static int make_map(CUtensorMap* m, const float* base, uint64_t rows, uint64_t cols, uint64_t ld,
+                    uint32_t box_rows) {
+  auto fn = encode_fn();
+  if (!fn) return fail(QPINN_ERR_CUDA, "cuTensorMapEncodeTiled is unavailable");
+  if (((uintptr_t)base & 15) || (ld & 3))
+    return fail(QPINN_ERR_CONFIG, "tensor-core GEMM operands need 16-byte aligned rows");
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {ld * 4};
+  cuuint32_t box[2] = {(cuuint32_t)kBK, box_rows};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides,
+                  box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(QPINN_ERR_CUDA, "cuTensorMapEncodeTiled failed");
+  return QPINN_OK;
+}
+
+static inline int ldk_of(int K) { return (K + 3) & ~3; }
+
+size_t gemm3_workspace_bytes(int N, int K) { return 2 * (size_t)N * ldk_of(K) * 4 + 256; }
+
+template <int BN, int EPI>
+static int launch_gemm3(const GemmArgs& g, const float* A, int64_t lda, const float* Bhi,
+                        const float* Blo, int ldk, cudaStream_t st) {
+  CUtensorMap mA, mBh, mBl;
+  const uint32_t a_box = EPI == EPI_TANH ? 32 : kBM;
+  if (int rc = make_map(&mA, A, (uint64_t)g.M, (uint64_t)g.K, (uint64_t)lda, a_box)) return rc;
+  if (int rc = make_map(&mBh, Bhi, (uint64_t)g.N, (uint64_t)ldk, (uint64_t)ldk, BN)) return rc;
+  if (int rc = make_map(&mBl, Blo, (uint64_t)g.N, (uint64_t)ldk, (uint64_t)ldk, BN)) return rc;
+  auto kern = gemm3_kernel<BN, EPI>;
+  QPINN_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        GemmCfg<BN>::kSmem));
+  const int64_t n_mt = EPI == EPI_TANH ? (g.R + 31) / 32 : (g.M + kBM - 1) / kBM;
+  const int64_t tiles = n_mt * ((g.N + BN - 1) / BN);
+  const int grid = (int)(tiles < num_sms() ? tiles : num_sms());
+  kern<<<grid, kThreadsGemm, GemmCfg<BN>::kSmem, st>>>(mA, mBh, mBl, g);
+  QPINN_CUDA_CHECK(cudaGetLastError());
+  return QPINN_OK;
+}
+
+template <int EPI>
+static int dispatch(const GemmArgs& g, const float* A, int64_t lda, const float* hi,
+                    const float* lo, int ldk, cudaStream_t st) {
+  if (g.N <= 64) return launch_gemm3<64, EPI>(g, A, lda, hi, lo, ldk, st);
+  return launch_gemm3<128, EPI>(g, A, lda, hi, lo, ldk, st);
+}
+
+int gemm3(int64_t M, int N, int K, const float* A, int64_t lda, const float* B, int64_t ldb,
+          float* C, int64_t ldc, void* ws, size_t ws_bytes, cudaStream_t st) {
+  if (M < 0 || N < 1 || K < 1) return fail(QPINN_ERR_CONFIG, "gemm3: bad shape");
+  if (ws_bytes < gemm3_workspace_bytes(N, K)) return fail(QPINN_ERR_CONFIG, "gemm3: workspace");
+  if (M == 0) return QPINN_OK;
+  const int ldk = ldk_of(K);
+  float* hi = (float*)(((uintptr_t)ws + 255) & ~(uintptr_t)255);
+  float* lo = hi + (size_t)N * ldk;
+  split_rows<<<64, 256, 0, st>>>(B, N, K, ldb, ldk, hi, lo);
+  QPINN_CUDA_CHECK(cudaGetLastError());
+  GemmArgs g{M, 0, N, K, C, ldc, nullptr};
+  return dispatch<EPI_STORE>(g, A, lda, hi, lo, ldk, st);
+}
+
+// H [4R, N] = dual tanh of X [4R, K] W [K, N] + b (channel blocks of R rows)
+int dense_tanh(int64_t R, int N, int K, const float* X, const float* W, const float* bias,
+               float* H, void* ws, size_t ws_bytes, cudaStream_t st) {
+  if (ws_bytes < gemm3_workspace_bytes(N, K)) return fail(QPINN_ERR_CONFIG, "dense: workspace");
+  if (R == 0) return QPINN_OK;
+  const int ldk = ldk_of(K);
+  float* hi = (float*)(((uintptr_t)ws + 255) & ~(uintptr_t)255);
+  float* lo = hi + (size_t)N * ldk;
+  split_transpose<<<64, 256, 0, st>>>(W, K, N, ldk, hi, lo);
+  QPINN_CUDA_CHECK(cudaGetLastError());
+  GemmArgs g{4 * R, R, N, K, H, N, bias};
+  return dispatch<EPI_TANH>(g, X, K, hi, lo, ldk, st);
+}
+
+}  // namespace tc
+}  // namespace qpinn
+
+using namespace qpinn;
+
+extern "C" {
+
+size_t qpinn_gemm_f32_workspace_bytes(int n, int k) {
+  return n < 1 || k < 1 ? 0 : tc::gemm3_workspace_bytes(n, k);
+}
+
+int qpinn_gemm_f32(int64_t m, int n, int k, const void* a, int64_t lda, const void* b, int64_t ldb,
+                   void* c, int64_t ldc, void* workspace, size_t workspace_bytes, void* stream) {
+  return tc::gemm3(m, n, k, (const float*)a, lda, (const float*)b, ldb, (float*)c, ldc, workspace,
+                   workspace_bytes, (cudaStream_t)stream);
+}
+
+}  // extern "C"

@@ -5,13 +5,16 @@
 // ops.py:282-298) and the tape's reverse pass through them.
 //
 // Activations are channel-major [4, R, width] (value, d/dx, d/dy, d/dt), so
-// every dense layer is ONE GEMM [4R, in] x [in, out] on the tensor cores.
-// float32 uses cuBLAS's FP32 emulation (BF16x9, FP32-accurate) -- a plain
-// library GEMM; float64 uses DGEMM.  Everything around the GEMMs is fused
-// here: the feature map + RFF with tangents, the dual tanh epilogue
-// (y = tanh(u0 + b), dy_k = (1 - y^2) du_k), its reverse
-// (g_u0 = g_y s - 2 y s sum_k g_dy_k du_k, g_du_k = g_dy_k s), deterministic
-// bias column sums, and the tau gradient through the learned time period.
+// every dense layer is ONE GEMM [4R, in] x [in, out].  float32: the forward
+// layers and the input-gradient GEMMs run on our tcgen05 3xTF32 kernels
+// (tc_gemm.cu, FP32-class accuracy) with the dual tanh fused into the
+// epilogue; the weight-gradient GEMMs (and the K = 7 adapter input gradient)
+// use cuBLAS FP32.  float64 uses cuBLAS DGEMM throughout.  Around the GEMMs:
+// the feature map + RFF with tangents, the dual tanh (y = tanh(u0 + b),
+// dy_k = (1 - y^2) du_k) and its reverse written on the stored outputs
+// (g_u0 = g_y s - 2 y sum_k g_dy_k dy_k, g_du_k = g_dy_k s, s = 1 - y^2),
+// deterministic bias column sums, and the tau gradient through the learned
+// time period.
 #include <cublas_v2.h>
 
 #include <cstdio>
@@ -19,6 +22,7 @@
 #include <mutex>
 
 #include "gates.cuh"
+#include "tc_gemm.h"
 
 namespace qpinn {
 
@@ -142,17 +146,18 @@ __global__ void tanh_fwd(int64_t R, int N, const T* __restrict__ U, const T* __r
   }
 }
 
-// reverse of the dual tanh: g_u0 = g_y s + sum_k g_dy_k du_k (-2 y s), g_du_k = g_dy_k s
+// reverse of the dual tanh on its outputs H (dy_k = s du_k):
+// g_u0 = g_y s - 2 y sum_k g_dy_k dy_k, g_du_k = g_dy_k s
 template <typename T>
 __global__ void tanh_bwd(int64_t R, int N, const T* __restrict__ GY, const T* __restrict__ Y,
-                         const T* __restrict__ U, T* __restrict__ GU) {
+                         T* __restrict__ GU) {
   const int64_t n = R * N;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
     const T yv = Y[i];
     const T s = T(1) - yv * yv;
     const T g1 = GY[n + i], g2 = GY[2 * n + i], g3 = GY[3 * n + i];
-    GU[i] = GY[i] * s + (g1 * U[n + i] + g2 * U[2 * n + i] + g3 * U[3 * n + i]) * (T(-2) * yv * s);
+    GU[i] = GY[i] * s + (g1 * Y[n + i] + g2 * Y[2 * n + i] + g3 * Y[3 * n + i]) * (T(-2) * yv);
     GU[n + i] = g1 * s;
     GU[2 * n + i] = g2 * s;
     GU[3 * n + i] = g3 * s;
@@ -256,7 +261,7 @@ __global__ void tau_grad_reduce(int nb, const double* __restrict__ partial, cons
 
 // ---- workspace plan ----------------------------------------------------------------------------
 struct TrunkWS {
-  size_t h0, u[8], h[8], ua, g0, g1, part, tau_part, total;
+  size_t h0, u, h[8], g0, g1, part, tau_part, wsplit, total;
 };
 
 constexpr int kColBlocks = 256;
@@ -272,11 +277,9 @@ static TrunkWS trunk_ws(const qpinn_trunk_desc* d, size_t es, int64_t R) {
   };
   const size_t F2 = 2 * (size_t)d->rff, H = d->hidden;
   w.h0 = take(4 * R * F2);
-  for (int i = 0; i < d->n_hidden; ++i) {
-    w.u[i] = take(4 * R * H);
-    w.h[i] = take(4 * R * H);
-  }
-  w.ua = take(4 * R * (size_t)d->n_out);
+  // GEMM output before the dual tanh (cuBLAS layers: float64, unaligned float32 widths)
+  w.u = take(4 * R * (H > (size_t)d->n_out ? H : d->n_out));
+  for (int i = 0; i < d->n_hidden; ++i) w.h[i] = take(4 * R * H);
   const size_t gmax = 4 * R * (F2 > H ? F2 : H);
   w.g0 = take(gmax);
   w.g1 = take(gmax);
@@ -284,6 +287,8 @@ static TrunkWS trunk_ws(const qpinn_trunk_desc* d, size_t es, int64_t R) {
   o += ((size_t)kColBlocks * (H > (size_t)d->n_out ? H : d->n_out) * 8 + 255) / 256 * 256;
   w.tau_part = o;
   o += (kTauBlocks * 8 + 255) / 256 * 256;
+  w.wsplit = o;  // float32: tf32 hi/lo split of one weight matrix
+  o += es == 4 ? tc::gemm3_workspace_bytes((int)(F2 > H ? F2 : H), (int)(F2 > H ? F2 : H)) : 0;
   w.total = o;
   return w;
 }
@@ -308,8 +313,6 @@ template <typename T>
 static int forward_impl(const qpinn_trunk_desc* d, int64_t R, const T* x, const T* y, const T* t,
                         const T* params, T* act, unsigned char* ws, cudaStream_t st) {
   const TrunkWS w = trunk_ws(d, sizeof(T), R);
-  cublasHandle_t h;
-  if (int rc = blas_handle(st, &h)) return rc;
   const int F = d->rff, H = d->hidden, n = d->n_out;
   T* H0 = (T*)(ws + w.h0);
   features_fwd<T><<<grid_1d(R * F), 256, 0, st>>>(R, F, x, y, t, (const T*)d->omega, params,
@@ -317,22 +320,29 @@ static int forward_impl(const qpinn_trunk_desc* d, int64_t R, const T* x, const 
   QPINN_CUDA_CHECK(cudaGetLastError());
   const T* in = H0;
   int K = 2 * F;
-  for (int i = 0; i < d->n_hidden; ++i) {
-    T* U = (T*)(ws + w.u[i]);
-    T* Hn = (T*)(ws + w.h[i]);
-    if (int rc = gemm_rm<T>(h, false, false, 4 * R, H, K, in, K, params + d->off_w[i], H, U, H, T(0)))
+  cublasHandle_t h;
+  if (int rc = blas_handle(st, &h)) return rc;
+  T* U = (T*)(ws + w.u);
+  // one dense layer + dual tanh: tensor cores (float32, 16-byte aligned rows) or cuBLAS
+  auto dense = [&](int Kin, int N, const T* X, int64_t off_w, int64_t off_b, T* out) -> int {
+    if constexpr (sizeof(T) == 4) {
+      if (Kin % 4 == 0)
+        return tc::dense_tanh(R, N, Kin, X, params + off_w, params + off_b, out, ws + w.wsplit,
+                              w.total - w.wsplit, st);
+    }
+    if (int rc = gemm_rm<T>(h, false, false, 4 * R, N, Kin, X, Kin, params + off_w, N, U, N, T(0)))
       return rc;
-    tanh_fwd<T><<<grid_1d(R * H), 256, 0, st>>>(R, H, U, params + d->off_b[i], Hn);
+    tanh_fwd<T><<<grid_1d(R * N), 256, 0, st>>>(R, N, U, params + off_b, out);
     QPINN_CUDA_CHECK(cudaGetLastError());
+    return QPINN_OK;
+  };
+  for (int i = 0; i < d->n_hidden; ++i) {
+    T* Hn = (T*)(ws + w.h[i]);
+    if (int rc = dense(K, H, in, d->off_w[i], d->off_b[i], Hn)) return rc;
     in = Hn;
     K = H;
   }
-  T* Ua = (T*)(ws + w.ua);
-  if (int rc = gemm_rm<T>(h, false, false, 4 * R, n, K, in, K, params + d->off_adapter_w, n, Ua, n, T(0)))
-    return rc;
-  tanh_fwd<T><<<grid_1d(R * n), 256, 0, st>>>(R, n, Ua, params + d->off_adapter_b, act);
-  QPINN_CUDA_CHECK(cudaGetLastError());
-  return QPINN_OK;
+  return dense(K, n, in, d->off_adapter_w, d->off_adapter_b, act);
 }
 
 template <typename T>
@@ -349,7 +359,7 @@ static int backward_impl(const qpinn_trunk_desc* d, int64_t R, const T* x, const
   // adapter: GU = tanh_bwd(g_act); dWa = H_last^T GU; dba = colsum(GU0); G_H = GU Wa^T
   const T* Hl = (const T*)(ws + (d->n_hidden ? w.h[d->n_hidden - 1] : w.h0));
   const int Kl = d->n_hidden ? H : 2 * F;
-  tanh_bwd<T><<<grid_1d(R * n), 256, 0, st>>>(R, n, g_act, act, (const T*)(ws + w.ua), g1);
+  tanh_bwd<T><<<grid_1d(R * n), 256, 0, st>>>(R, n, g_act, act, g1);
   QPINN_CUDA_CHECK(cudaGetLastError());
   if (int rc = gemm_rm<T>(h, true, false, Kl, n, 4 * R, Hl, Kl, g1, n, grad + d->off_adapter_w, n, T(0)))
     return rc;
@@ -360,14 +370,19 @@ static int backward_impl(const qpinn_trunk_desc* d, int64_t R, const T* x, const
   for (int i = d->n_hidden - 1; i >= 0; --i) {
     const int K = i == 0 ? 2 * F : H;
     const T* Hin = (const T*)(ws + (i == 0 ? w.h0 : w.h[i - 1]));
-    tanh_bwd<T><<<grid_1d(R * H), 256, 0, st>>>(R, H, g0, (const T*)(ws + w.h[i]),
-                                                 (const T*)(ws + w.u[i]), g1);
+    tanh_bwd<T><<<grid_1d(R * H), 256, 0, st>>>(R, H, g0, (const T*)(ws + w.h[i]), g1);
     QPINN_CUDA_CHECK(cudaGetLastError());
     if (int rc = gemm_rm<T>(h, true, false, K, H, 4 * R, Hin, K, g1, H, grad + d->off_w[i], H, T(0)))
       return rc;
     if (int rc = bias_grad<T>(R, H, g1, part, grad + d->off_b[i], st)) return rc;
-    if (int rc = gemm_rm<T>(h, false, true, 4 * R, K, H, g1, H, params + d->off_w[i], H, g0, K, T(0)))
+    if (sizeof(T) == 4 && H % 4 == 0) {  // dL/dH_in = GU W^T on the tensor cores
+      if (int rc = tc::gemm3(4 * R, K, H, (const float*)g1, H, (const float*)(params + d->off_w[i]),
+                             H, (float*)g0, K, ws + w.wsplit, w.total - w.wsplit, st))
+        return rc;
+    } else if (int rc = gemm_rm<T>(h, false, true, 4 * R, K, H, g1, H, params + d->off_w[i], H, g0,
+                                   K, T(0))) {
       return rc;
+    }
   }
   // tau_raw through the time features
   double* tp = (double*)(ws + w.tau_part);

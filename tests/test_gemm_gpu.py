@@ -1,0 +1,52 @@
+"""Tensor-core 3xTF32 GEMM (qpinn_gemm_f32, tc_gemm.cu) against float64.
+
+C = A B^T must be FP32-class: max |C - C_f64| <= 3e-6 max |C_f64| (cuBLAS
+SIMT fp32 lands at ~7e-7 on the same inputs at K = 256; the split-operand
+tensor-core path at ~3.5e-7).  Ragged M, N < 16, N > 128 (several N tiles)
+and K not a multiple of the 32-wide pipeline stage are covered."""
+import pytest
+import torch
+
+from paper_2506_23246_b200 import _native as N
+
+pytestmark = pytest.mark.gpu
+
+
+def _gemm(A, B):
+    lib = N.lib()
+    M, K = A.shape
+    n = B.shape[0]
+    C = torch.full((M, n), float("nan"), dtype=torch.float32, device="cuda")
+    ws = torch.empty(lib.qpinn_gemm_f32_workspace_bytes(n, K), dtype=torch.uint8, device="cuda")
+    N.check(lib.qpinn_gemm_f32(M, n, K, A.data_ptr(), A.stride(0), B.data_ptr(), B.stride(0),
+                               C.data_ptr(), C.stride(0), ws.data_ptr(), ws.numel(),
+                               N.stream_ptr()), "qpinn_gemm_f32")
+    return C
+
+
+@pytest.mark.parametrize("M,n,K", [(128, 128, 32), (1000, 128, 256), (300, 256, 128),
+                                   (513, 7, 128), (4096, 64, 96), (77, 200, 40), (1, 16, 4),
+                                   (70000, 128, 256)])
+def test_gemm_f32_matches_f64(M, n, K):
+    g = torch.Generator(device="cuda").manual_seed(M * 7 + n * 3 + K)
+    A = torch.randn(M, K, device="cuda", generator=g)
+    B = torch.randn(n, K, device="cuda", generator=g) / K ** 0.5
+    C = _gemm(A, B)
+    ref = A.double() @ B.double().T
+    assert torch.isfinite(C).all()
+    err = (C.double() - ref).abs().max().item()
+    assert err <= 3e-6 * ref.abs().max().item(), err
+
+
+def test_gemm_f32_deterministic():
+    g = torch.Generator(device="cuda").manual_seed(1)
+    A = torch.randn(20000, 256, device="cuda", generator=g)
+    B = torch.randn(128, 256, device="cuda", generator=g)
+    assert torch.equal(_gemm(A, B), _gemm(A, B))
+
+
+def test_gemm_rejects_unaligned_rows():
+    A = torch.randn(64, 10, device="cuda")
+    B = torch.randn(16, 10, device="cuda")
+    with pytest.raises(Exception):
+        _gemm(A, B)
