@@ -246,6 +246,14 @@ size_t qpinn_gemm_f32_workspace_bytes(int n, int k);
 int qpinn_gemm_f32(int64_t m, int n, int k, const void* a, int64_t lda, const void* b,
                    int64_t ldb, void* c, int64_t ldc, void* workspace,
                    size_t workspace_bytes, void* stream);
+/* C[m,n] = X[rows,m]^T G[rows,n] (the dense layers' weight gradients, a
+ * reduction over all rows): same split-operand tensor-core math, split over
+ * row chunks with a fixed-order float64 sum of the chunk partials
+ * (run-to-run deterministic).  ldx, ldg multiples of 4. */
+size_t qpinn_gemm_f32_atb_workspace_bytes(int64_t rows, int m, int n);
+int qpinn_gemm_f32_atb(int64_t rows, int m, int n, const void* x, int64_t ldx, const void* g,
+                       int64_t ldg, void* c, void* workspace, size_t workspace_bytes,
+                       void* stream);
 
 #ifdef __cplusplus
 }

@@ -85,6 +85,8 @@ SIGNATURES = [
     ("qpinn_adam_step", _I, [_I, _I64, _VP, _VP, _VP, _VP, _I64, _D, _D, _D, _D, _VP, _VP, _VP]),
     ("qpinn_gemm_f32_workspace_bytes", _SZ, [_I, _I]),
     ("qpinn_gemm_f32", _I, [_I64, _I, _I, _VP, _I64, _VP, _I64, _VP, _I64, _VP, _SZ, _VP]),
+    ("qpinn_gemm_f32_atb_workspace_bytes", _SZ, [_I64, _I, _I]),
+    ("qpinn_gemm_f32_atb", _I, [_I64, _I, _I, _VP, _I64, _VP, _I64, _VP, _VP, _SZ, _VP]),
 ]
 
 _lib = None

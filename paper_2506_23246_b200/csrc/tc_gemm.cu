@@ -303,6 +303,227 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUt
   if (warp == 9) tmem_dealloc(tmem, Cfg::kTmemCols);
 }
 
+// ---- weight gradient: dW[Kin, Nout] = X[rows, Kin]^T G[rows, Nout] ----------------------
+// Both operands are activations stored row-major, i.e. MN-major for the MMA
+// (the reduction runs over rows).  Work items are (128-row block of dW,
+// 128-column block, chunk of rows); each writes an fp32 partial tile and a
+// second kernel sums the chunks in a fixed order (deterministic split-K).
+// Both operands are split into tf32 hi/lo in shared memory.
+constexpr int kWRaw = 3, kWOps = 2, kWNB = 4;
+constexpr int kWRawBytes = 2 * kABytes;  // A (16 KB) | B (16 KB)
+constexpr int kWOpBytes = 4 * kABytes;   // A_hi | A_lo | B_hi | B_lo
+constexpr int kWSmem = kWRaw * kWRawBytes + kWOps * kWOpBytes + 1024 + 512;
+constexpr int kWPromote = 2;  // k-blocks accumulated in TMEM per promotion (64-deep chains)
+
+struct WgradArgs {
+  int64_t rows, chunk;  // rows per chunk (multiple of 32)
+  int Kin, Nout, n_mt, n_nt, n_kc;
+  float* partial;       // [n_kc][Kin][Nout]
+};
+
+__global__ void __launch_bounds__(kThreadsGemm - 32, 1)
+wgrad_kernel(const __grid_constant__ CUtensorMap mX, const __grid_constant__ CUtensorMap mG,
+             const WgradArgs g) {
+  constexpr int RS = kWRaw, OS = kWOps, NB = kWNB, P = kWPromote;
+  extern __shared__ unsigned char smem_raw[];
+  unsigned char* smem = (unsigned char*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  unsigned char* raw = smem;
+  unsigned char* ops = smem + RS * kWRawBytes;
+  uint64_t* raw_full = (uint64_t*)(ops + OS * kWOpBytes);
+  uint64_t* raw_empty = raw_full + RS;
+  uint64_t* conv = raw_empty + RS;
+  uint64_t* op_empty = conv + OS;
+  uint64_t* tfull = op_empty + OS;
+  uint64_t* tempty = tfull + NB;
+  uint32_t* tmem_slot = (uint32_t*)(tempty + NB);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t n_items = (int64_t)g.n_mt * g.n_nt * g.n_kc;
+  auto item = [&](int64_t it, int& mt, int& nt, int& kc, int64_t& row0, int& nkb) {
+    kc = (int)(it % g.n_kc);
+    const int64_t r = it / g.n_kc;
+    nt = (int)(r % g.n_nt);
+    mt = (int)(r / g.n_nt);
+    row0 = (int64_t)kc * g.chunk;
+    int64_t len = g.rows - row0;
+    if (len > g.chunk) len = g.chunk;
+    nkb = len > 0 ? (int)((len + kBK - 1) / kBK) : 0;
+  };
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < RS; ++s) {
+      mbar_init(raw_full + s, 1);
+      mbar_init(raw_empty + s, 4);
+    }
+    for (int s = 0; s < OS; ++s) {
+      mbar_init(conv + s, 4);
+      mbar_init(op_empty + s, 1);
+    }
+    for (int b = 0; b < NB; ++b) {
+      mbar_init(tfull + b, 1);
+      mbar_init(tempty + b, 4);
+    }
+    mbar_init_fence();
+  }
+  if (warp == 8 && lane == 0) {
+    tma_prefetch(&mX);
+    tma_prefetch(&mG);
+  }
+  if (warp == 9) tmem_alloc(tmem_slot, NB * 128);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 8) {  // ---- TMA producer: 4 x 4 boxes of 32 x 32 per k-block
+    if (lane == 0) {
+      int64_t j = 0;
+      for (int64_t it = blockIdx.x; it < n_items; it += gridDim.x) {
+        int mt, nt, kc, nkb;
+        int64_t row0;
+        item(it, mt, nt, kc, row0, nkb);
+        for (int kb = 0; kb < nkb; ++kb, ++j) {
+          const int r = (int)(j % RS);
+          if (j >= RS) mbar_wait(raw_empty + r, (uint32_t)(((j / RS) - 1) & 1));
+          unsigned char* st = raw + r * kWRawBytes;
+          mbar_expect_tx(raw_full + r, kWRawBytes);
+          const int rr = (int)(row0 + kb * kBK);
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            tma_load_2d(st + c * 4096, &mX, raw_full + r, mt * 128 + c * 32, rr);
+            tma_load_2d(st + kABytes + c * 4096, &mG, raw_full + r, nt * 128 + c * 32, rr);
+          }
+        }
+      }
+    }
+  } else if (warp == 9) {  // ---- MMA issuer (MN-major A and B)
+    if (lane == 0) {
+      constexpr uint32_t idesc = idesc_tf32(kBM, 128) | (1u << 15) | (1u << 16);
+      int64_t j = 0, grp = 0;
+      for (int64_t it = blockIdx.x; it < n_items; it += gridDim.x) {
+        int mt, nt, kc, nkb;
+        int64_t row0;
+        item(it, mt, nt, kc, row0, nkb);
+        for (int kb = 0; kb < nkb; ++kb, ++j) {
+          const int o = (int)(j % OS), b = (int)(grp % NB);
+          const bool first = kb % P == 0, last = kb % P == P - 1 || kb == nkb - 1;
+          if (first && grp >= NB) mbar_wait(tempty + b, (uint32_t)(((grp / NB) - 1) & 1));
+          mbar_wait(conv + o, (uint32_t)((j / OS) & 1));
+          tc_fence_after();
+          const uint32_t base = smem_u32(ops + o * kWOpBytes);
+          const uint32_t d = tmem + b * 128;
+#pragma unroll
+          for (int k = 0; k < kBK / 8; ++k) {
+            const uint32_t off = k * 1024;  // 8 K-rows = one 1024-byte swizzle atom
+            const uint32_t a_hi = base + off, a_lo = base + kABytes + off;
+            const uint32_t b_hi = base + 2 * kABytes + off, b_lo = base + 3 * kABytes + off;
+            mma_tf32(d, desc_mn_sw128_32b(a_lo), desc_mn_sw128_32b(b_hi), idesc, !(first && k == 0));
+            mma_tf32(d, desc_mn_sw128_32b(a_hi), desc_mn_sw128_32b(b_lo), idesc, 1);
+            mma_tf32(d, desc_mn_sw128_32b(a_hi), desc_mn_sw128_32b(b_hi), idesc, 1);
+          }
+          mma_commit(op_empty + o);
+          if (last) {
+            mma_commit(tfull + b);
+            ++grp;
+          }
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp < 4) {  // ---- split A and B (flat 16-byte chunks)
+    int64_t j = 0;
+    for (int64_t it = blockIdx.x; it < n_items; it += gridDim.x) {
+      int mt, nt, kc, nkb;
+      int64_t row0;
+      item(it, mt, nt, kc, row0, nkb);
+      for (int kb = 0; kb < nkb; ++kb, ++j) {
+        const int r = (int)(j % RS), o = (int)(j % OS);
+        if (j >= OS) mbar_wait(op_empty + o, (uint32_t)(((j / OS) - 1) & 1));
+        mbar_wait(raw_full + r, (uint32_t)((j / RS) & 1));
+        const uint32_t src = smem_u32(raw + r * kWRawBytes) + threadIdx.x * 16;
+        const uint32_t dst = smem_u32(ops + o * kWOpBytes) + threadIdx.x * 16;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {  // A, then B
+          float4 v[8];
+#pragma unroll
+          for (int i = 0; i < 8; ++i) v[i] = lds128(src + h * kABytes + i * 2048);
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            float4 hi, lo;
+            split_tf32(v[i].x, hi.x, lo.x);
+            split_tf32(v[i].y, hi.y, lo.y);
+            split_tf32(v[i].z, hi.z, lo.z);
+            split_tf32(v[i].w, hi.w, lo.w);
+            sts128(dst + h * 2 * kABytes + i * 2048, hi);
+            sts128(dst + h * 2 * kABytes + kABytes + i * 2048, lo);
+          }
+        }
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          mbar_arrive(raw_empty + r);
+          mbar_arrive(conv + o);
+        }
+      }
+    }
+  } else {  // ---- warps 4-7: promote, store the partial tile
+    const int q = warp - 4;
+    const uint32_t lane_base = (uint32_t)(q * 32) << 16;
+    int64_t grp = 0;
+    for (int64_t it = blockIdx.x; it < n_items; it += gridDim.x) {
+      int mt, nt, kc, nkb;
+      int64_t row0;
+      item(it, mt, nt, kc, row0, nkb);
+      float acc[128];
+#pragma unroll
+      for (int c = 0; c < 128; ++c) acc[c] = 0.f;
+      const int ngrp = (nkb + P - 1) / P;
+      for (int gi = 0; gi < ngrp; ++gi, ++grp) {
+        const int b = (int)(grp % NB);
+        mbar_wait(tfull + b, (uint32_t)((grp / NB) & 1));
+        tc_fence_after();
+#pragma unroll
+        for (int c0 = 0; c0 < 128; c0 += 32) {
+          float v[32];
+          tmem_ld32(tmem + lane_base + b * 128 + c0, v);
+#pragma unroll
+          for (int i = 0; i < 32; ++i) acc[c0 + i] += v[i];
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(tempty + b);
+      }
+      const int m = mt * 128 + q * 32 + lane, n0 = nt * 128;
+      if (m < g.Kin) {
+        float* dst = g.partial + ((int64_t)kc * g.Kin + m) * g.Nout + n0;
+        if (n0 + 128 <= g.Nout && (g.Nout & 3) == 0) {
+#pragma unroll
+          for (int c = 0; c < 128; c += 4)
+            *reinterpret_cast<float4*>(dst + c) =
+                make_float4(acc[c], acc[c + 1], acc[c + 2], acc[c + 3]);
+        } else {
+#pragma unroll
+          for (int c = 0; c < 128; ++c)
+            if (n0 + c < g.Nout) dst[c] = acc[c];
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 9) tmem_dealloc(tmem, NB * 128);
+}
+
+// dW = sum over chunks of the partial tiles, in chunk order (float64 sum)
+__global__ void wgrad_reduce(int n_kc, int64_t n, const float* __restrict__ partial,
+                             float* __restrict__ dW) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int k = 0; k < n_kc; ++k) s += (double)partial[(int64_t)k * n + i];
+    dW[i] = (float)s;
+  }
+}
+
 // B [N,K] (ld ldb) -> B_hi, B_lo [N, ldk] (zero padded to ldk)
 __global__ void split_rows(const float* __restrict__ B, int N, int K, int64_t ldb, int ldk,
                            float* __restrict__ hi, float* __restrict__ lo) {
@@ -348,7 +569,8 @@ static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 
 // 2-D fp32 map over rows x cols (ld elements), box = 32 columns x box_rows, 128-byte swizzle
 static int make_map(CUtensorMap* m, const float* base, uint64_t rows, uint64_t cols, uint64_t ld,
-                    uint32_t box_rows) {
+                    uint32_t box_rows,
+                    CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B) {
   auto fn = encode_fn();
   if (!fn) return fail(QPINN_ERR_CUDA, "cuTensorMapEncodeTiled is unavailable");
   if (((uintptr_t)base & 15) || (ld & 3))
@@ -358,7 +580,7 @@ static int make_map(CUtensorMap* m, const float* base, uint64_t rows, uint64_t c
   cuuint32_t box[2] = {(cuuint32_t)kBK, box_rows};
   cuuint32_t es[2] = {1, 1};
   CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides,
-                  box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(QPINN_ERR_CUDA, "cuTensorMapEncodeTiled failed");
   return QPINN_OK;
@@ -408,6 +630,57 @@ int gemm3(int64_t M, int N, int K, const float* A, int64_t lda, const float* B, 
   return dispatch<EPI_STORE>(g, A, lda, hi, lo, ldk, st);
 }
 
+static void wgrad_plan(int64_t rows, int Kin, int Nout, WgradArgs* a) {
+  a->rows = rows;
+  a->Kin = Kin;
+  a->Nout = Nout;
+  a->n_mt = (Kin + 127) / 128;
+  a->n_nt = (Nout + 127) / 128;
+  const int64_t kblocks = (rows + kBK - 1) / kBK;
+  int64_t kc = (num_sms() + a->n_mt * a->n_nt - 1) / (a->n_mt * a->n_nt);
+  if (kc > kblocks) kc = kblocks > 0 ? kblocks : 1;
+  const int64_t per = (kblocks + kc - 1) / kc;  // k-blocks per chunk
+  a->chunk = per * kBK;
+  a->n_kc = (int)((rows + a->chunk - 1) / a->chunk);
+  if (a->n_kc < 1) a->n_kc = 1;
+}
+
+size_t wgrad_workspace_bytes(int64_t rows, int Kin, int Nout) {
+  WgradArgs a{};
+  wgrad_plan(rows, Kin, Nout, &a);
+  return (size_t)a.n_kc * Kin * Nout * 4 + 256;
+}
+
+// dW [Kin, Nout] = X [rows, Kin]^T G [rows, Nout]
+int wgrad(int64_t rows, int Kin, int Nout, const float* X, int64_t ldx, const float* G,
+          int64_t ldg, float* dW, void* ws, size_t ws_bytes, cudaStream_t st) {
+  if (rows < 0 || Kin < 1 || Nout < 1) return fail(QPINN_ERR_CONFIG, "wgrad: bad shape");
+  if (ws_bytes < wgrad_workspace_bytes(rows, Kin, Nout))
+    return fail(QPINN_ERR_CONFIG, "wgrad: workspace");
+  if (rows == 0) {
+    QPINN_CUDA_CHECK(cudaMemsetAsync(dW, 0, (size_t)Kin * Nout * 4, st));
+    return QPINN_OK;
+  }
+  WgradArgs a{};
+  wgrad_plan(rows, Kin, Nout, &a);
+  a.partial = (float*)(((uintptr_t)ws + 255) & ~(uintptr_t)255);
+  CUtensorMap mX, mG;
+  constexpr CUtensorMapSwizzle kSw = CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B;
+  if (int rc = make_map(&mX, X, (uint64_t)rows, (uint64_t)Kin, (uint64_t)ldx, 32, kSw)) return rc;
+  if (int rc = make_map(&mG, G, (uint64_t)rows, (uint64_t)Nout, (uint64_t)ldg, 32, kSw)) return rc;
+  QPINN_CUDA_CHECK(
+      cudaFuncSetAttribute(wgrad_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kWSmem));
+  const int64_t items = (int64_t)a.n_mt * a.n_nt * a.n_kc;
+  const int grid = (int)(items < num_sms() ? items : num_sms());
+  wgrad_kernel<<<grid, kThreadsGemm - 32, kWSmem, st>>>(mX, mG, a);
+  QPINN_CUDA_CHECK(cudaGetLastError());
+  const int64_t n = (int64_t)Kin * Nout;
+  wgrad_reduce<<<(int)((n + 255) / 256 < 1024 ? (n + 255) / 256 : 1024), 256, 0, st>>>(
+      a.n_kc, n, a.partial, dW);
+  QPINN_CUDA_CHECK(cudaGetLastError());
+  return QPINN_OK;
+}
+
 // H [4R, N] = dual tanh of X [4R, K] W [K, N] + b (channel blocks of R rows)
 int dense_tanh(int64_t R, int N, int K, const float* X, const float* W, const float* bias,
                float* H, void* ws, size_t ws_bytes, cudaStream_t st) {
@@ -436,6 +709,17 @@ size_t qpinn_gemm_f32_workspace_bytes(int n, int k) {
 int qpinn_gemm_f32(int64_t m, int n, int k, const void* a, int64_t lda, const void* b, int64_t ldb,
                    void* c, int64_t ldc, void* workspace, size_t workspace_bytes, void* stream) {
   return tc::gemm3(m, n, k, (const float*)a, lda, (const float*)b, ldb, (float*)c, ldc, workspace,
+                   workspace_bytes, (cudaStream_t)stream);
+}
+
+size_t qpinn_gemm_f32_atb_workspace_bytes(int64_t rows, int m, int n) {
+  return rows < 0 || m < 1 || n < 1 ? 0 : tc::wgrad_workspace_bytes(rows, m, n);
+}
+
+int qpinn_gemm_f32_atb(int64_t rows, int m, int n, const void* x, int64_t ldx, const void* g,
+                       int64_t ldg, void* c, void* workspace, size_t workspace_bytes,
+                       void* stream) {
+  return tc::wgrad(rows, m, n, (const float*)x, ldx, (const float*)g, ldg, (float*)c, workspace,
                    workspace_bytes, (cudaStream_t)stream);
 }
 

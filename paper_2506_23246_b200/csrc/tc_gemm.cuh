@@ -130,6 +130,21 @@ __device__ __forceinline__ uint64_t desc_k_sw128(uint32_t saddr) {
   return d;
 }
 
+// MN-major tf32 operand.  The only MN-major swizzle the tf32 MMA takes is
+// "128B with 32-byte atomicity" (layout type 1): 128-byte rows of 32
+// MN-elements, 32-byte chunks XOR-permuted by (row mod 4), 4-row (512 B)
+// K atoms (SBO = 512 B, an 8-deep tf32 K step spans two), successive 32-wide
+// MN blocks LBO = 4096 B apart (one 32 x 32 TMA box each)
+__device__ __forceinline__ uint64_t desc_mn_sw128_32b(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)(4096 >> 4) << 16;
+  d |= (uint64_t)(512 >> 4) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)1 << 61;  // SWIZZLE_128B_BASE32B
+  return d;
+}
+
 // instruction descriptor: kind::tf32, fp32 accumulate, both operands K-major
 __host__ __device__ constexpr uint32_t idesc_tf32(int M, int N) {
   return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(N >> 3) << 17) |

@@ -11,6 +11,10 @@ size_t gemm3_workspace_bytes(int N, int K);
 // C[M,N] = A[M,K] B[N,K]^T (fp32, 3xTF32 tensor cores)
 int gemm3(int64_t M, int N, int K, const float* A, int64_t lda, const float* B, int64_t ldb,
           float* C, int64_t ldc, void* ws, size_t ws_bytes, cudaStream_t st);
+size_t wgrad_workspace_bytes(int64_t rows, int Kin, int Nout);
+// dW [Kin,Nout] = X [rows,Kin]^T G [rows,Nout] (split-K over rows, deterministic)
+int wgrad(int64_t rows, int Kin, int Nout, const float* X, int64_t ldx, const float* G,
+          int64_t ldg, float* dW, void* ws, size_t ws_bytes, cudaStream_t st);
 // H [4R,N] = dual tanh of X [4R,K] W [K,N] + b (value / tangent channel blocks)
 int dense_tanh(int64_t R, int N, int K, const float* X, const float* W, const float* bias,
                float* H, void* ws, size_t ws_bytes, cudaStream_t st);

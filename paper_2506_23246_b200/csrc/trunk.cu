@@ -8,8 +8,8 @@
 // every dense layer is ONE GEMM [4R, in] x [in, out].  float32: the forward
 // layers and the input-gradient GEMMs run on our tcgen05 3xTF32 kernels
 // (tc_gemm.cu, FP32-class accuracy) with the dual tanh fused into the
-// epilogue; the weight-gradient GEMMs (and the K = 7 adapter input gradient)
-// use cuBLAS FP32.  float64 uses cuBLAS DGEMM throughout.  Around the GEMMs:
+// epilogue, the weight gradients as a deterministic split-K; the adapter's
+// 7-wide GEMMs in the backward use cuBLAS FP32.  float64 uses cuBLAS DGEMM throughout.  Around the GEMMs:
 // the feature map + RFF with tangents, the dual tanh (y = tanh(u0 + b),
 // dy_k = (1 - y^2) du_k) and its reverse written on the stored outputs
 // (g_u0 = g_y s - 2 y sum_k g_dy_k dy_k, g_du_k = g_dy_k s, s = 1 - y^2),
@@ -287,8 +287,17 @@ static TrunkWS trunk_ws(const qpinn_trunk_desc* d, size_t es, int64_t R) {
   o += ((size_t)kColBlocks * (H > (size_t)d->n_out ? H : d->n_out) * 8 + 255) / 256 * 256;
   w.tau_part = o;
   o += (kTauBlocks * 8 + 255) / 256 * 256;
-  w.wsplit = o;  // float32: tf32 hi/lo split of one weight matrix
-  o += es == 4 ? tc::gemm3_workspace_bytes((int)(F2 > H ? F2 : H), (int)(F2 > H ? F2 : H)) : 0;
+  // float32 tensor-core scratch, used by one GEMM at a time: the tf32 hi/lo
+  // split of a weight matrix, or the split-K partials of a weight gradient
+  w.wsplit = o;
+  if (es == 4) {
+    const int KM = (int)(F2 > H ? F2 : H);
+    size_t b = tc::gemm3_workspace_bytes(KM, KM);
+    const size_t b1 = tc::wgrad_workspace_bytes(4 * R, (int)F2, (int)H);
+    const size_t b2 = tc::wgrad_workspace_bytes(4 * R, (int)H, (int)H);
+    b = b > b1 ? b : b1;
+    o += (b > b2 ? b : b2);
+  }
   w.total = o;
   return w;
 }
@@ -372,8 +381,14 @@ static int backward_impl(const qpinn_trunk_desc* d, int64_t R, const T* x, const
     const T* Hin = (const T*)(ws + (i == 0 ? w.h0 : w.h[i - 1]));
     tanh_bwd<T><<<grid_1d(R * H), 256, 0, st>>>(R, H, g0, (const T*)(ws + w.h[i]), g1);
     QPINN_CUDA_CHECK(cudaGetLastError());
-    if (int rc = gemm_rm<T>(h, true, false, K, H, 4 * R, Hin, K, g1, H, grad + d->off_w[i], H, T(0)))
+    if (sizeof(T) == 4 && K % 4 == 0 && H % 4 == 0) {  // dW = H_in^T GU on the tensor cores
+      if (int rc = tc::wgrad(4 * R, K, H, (const float*)Hin, K, (const float*)g1, H,
+                             (float*)(grad + d->off_w[i]), ws + w.wsplit, w.total - w.wsplit, st))
+        return rc;
+    } else if (int rc = gemm_rm<T>(h, true, false, K, H, 4 * R, Hin, K, g1, H, grad + d->off_w[i],
+                                   H, T(0))) {
       return rc;
+    }
     if (int rc = bias_grad<T>(R, H, g1, part, grad + d->off_b[i], st)) return rc;
     if (sizeof(T) == 4 && H % 4 == 0) {  // dL/dH_in = GU W^T on the tensor cores
       if (int rc = tc::gemm3(4 * R, K, H, (const float*)g1, H, (const float*)(params + d->off_w[i]),

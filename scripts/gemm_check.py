@@ -54,3 +54,43 @@ for (M, n, K) in [(128, 128, 32), (1000, 128, 256), (300, 256, 128), (513, 7, 12
         torch.cuda.synchronize()
         line += f" | torch fp32 {e0.elapsed_time(e1) / 20 * 1e3:.1f} us"
     print(line, flush=True)
+
+
+def atb(X, G):
+    lib = N.lib()
+    rows, m = X.shape
+    n = G.shape[1]
+    C_ = torch.empty((m, n), dtype=torch.float32, device="cuda")
+    ws = torch.empty(lib.qpinn_gemm_f32_atb_workspace_bytes(rows, m, n), dtype=torch.uint8,
+                     device="cuda")
+    N.check(lib.qpinn_gemm_f32_atb(rows, m, n, X.data_ptr(), X.stride(0), G.data_ptr(), G.stride(0),
+                                   C_.data_ptr(), ws.data_ptr(), ws.numel(), N.stream_ptr()), "atb")
+    return C_
+
+
+for (rows, m, n) in [(64, 128, 128), (1000, 96, 40), (262144, 256, 128), (262144, 128, 128),
+                     (70001, 132, 200)]:
+    X = torch.randn(rows, m, device="cuda")
+    G = torch.randn(rows, n, device="cuda")
+    Cg = atb(X, G)
+    torch.cuda.synchronize()
+    ref = X.double().T @ G.double()
+    err = (Cg.double() - ref).abs().max().item()
+    f32 = (X.T @ G).double()
+    line = (f"atb rows={rows} m={m} n={n}: max|err| {err:.3e} (rel {err / ref.abs().max().item():.2e});"
+            f" torch fp32 {(f32 - ref).abs().max().item():.3e}")
+    if rows >= 262144:
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(10):
+            atb(X, G)
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / 10
+        e0.record()
+        for _ in range(10):
+            torch.mm(X.T, G)
+        e1.record()
+        torch.cuda.synchronize()
+        line += f" | {ms * 1e3:.1f} us vs torch fp32 {e0.elapsed_time(e1) / 10 * 1e3:.1f} us"
+    print(line, flush=True)
