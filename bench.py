@@ -231,7 +231,7 @@ def run_ours(args):
     import torch
     import torch.distributed as dist
     from paper_2506_23246_b200 import _native as N
-    from paper_2506_23246_b200.roofline import pqc_flops
+    from paper_2506_23246_b200.roofline import pqc_flops, trunk_bytes
     from paper_2506_23246_b200.training import Trainer, allreduce_fn
 
     rank, world, local = dist_env()
@@ -313,6 +313,24 @@ def run_ours(args):
                             "ms_per_launch": round(mean_ms, 4),
                             "share_of_step": round(mean_ms * launches_per_step / (ms_prof / args.steps), 4),
                             "peak_source": peak_src}
+        # trunk passes (tensor-core GEMMs + fused elementwise): HBM-bound by design
+        mc = tr.model.config
+        tb_f, tb_b = trunk_bytes(mc.hidden_width, mc.rff_features, mc.n_qubits,
+                                 tr.model.n_hidden, 4 if dtype == torch.float32 else 8)
+        hbm = hbm_peak()
+        for name, per_pt in (("trunk_forward", tb_f), ("trunk_backward", tb_b)):
+            if name in kern and hbm:
+                nl, mean_ms = kern[name]
+                launches_per_step = nl / args.steps
+                pts_per_launch = R_local / launches_per_step
+                achieved = per_pt * pts_per_launch / (mean_ms * 1e-3) / 1e9
+                rl[name] = {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm,
+                            "unit": "GB/s", "frac": round(achieved / hbm, 4),
+                            "traffic": traffic_for(name, pts_per_launch),
+                            "bytes_per_point": per_pt, "points_per_launch": pts_per_launch,
+                            "ms_per_launch": round(mean_ms, 4),
+                            "share_of_step": round(mean_ms * launches_per_step / (ms_prof / args.steps), 4),
+                            "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy bandwidth)"}
         dom = max(rl, key=lambda k: rl[k]["share_of_step"]) if rl else None
         cpu = None
         if world == 1 and not args.no_cpu_baseline:
@@ -343,6 +361,16 @@ def run_ours(args):
         dist.destroy_process_group()
     if line is not None:
         print(json.dumps(line), flush=True)
+
+
+def hbm_peak():
+    """Measured HBM copy bandwidth (GB/s) from the driver-written MEASURED_PEAKS.json,
+    else the B200 profiling recipe's fallback."""
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"])
+    except Exception:
+        return 6500.0
 
 
 def traffic_for(name, pts):

@@ -266,20 +266,25 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUt
           }
         }
       } else {  // EPI_TANH: q = channel, lane = point
+        // the value channel's pre-activations go through shared memory so that
+        // all four warps share the tanh work (32 columns each)
         const int64_t p = mt * 32 + lane;
         if (q == 0) {
 #pragma unroll
-          for (int c = 0; c < BN; ++c) {
-            const float bv = n0 + c < g.N ? __ldg(g.bias + n0 + c) : 0.f;
-            const float y = tanhf(acc[c] + bv);
-            sbuf[c * 32 + lane] = 1.f - y * y;
-            acc[c] = y;
-          }
+          for (int c = 0; c < BN; ++c) sbuf[c * 32 + lane] = acc[c];
         }
         asm volatile("bar.sync 1, 128;" ::: "memory");
-        if (q != 0) {
+#pragma unroll 4
+        for (int c = q * (BN / 4); c < (q + 1) * (BN / 4); ++c) {
+          const float bv = n0 + c < g.N ? __ldg(g.bias + n0 + c) : 0.f;
+          const float y = tanhf(sbuf[c * 32 + lane] + bv);
+          sbuf[c * 32 + lane] = y;
+        }
+        asm volatile("bar.sync 1, 128;" ::: "memory");
 #pragma unroll
-          for (int c = 0; c < BN; ++c) acc[c] *= sbuf[c * 32 + lane];
+        for (int c = 0; c < BN; ++c) {
+          const float y = sbuf[c * 32 + lane];
+          acc[c] = q == 0 ? y : (1.f - y * y) * acc[c];
         }
         if (p < g.R) {
           float* dst = g.C + ((int64_t)q * g.R + p) * g.ldc + n0;

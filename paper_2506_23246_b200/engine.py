@@ -95,10 +95,11 @@ class NativeEngine:
             R = b.R
             g = grad if (self.grad_chunk is None or grad is None) else self.grad_chunk
             gp = g.data_ptr() if g is not None else 0
-            N.check(lib.qpinn_trunk_forward(C.byref(self.desc), dc, R, ch.x.data_ptr(),
-                                            ch.y.data_ptr(), ch.t.data_ptr(), fp,
-                                            b.act.data_ptr(), self.trunk_ws.data_ptr(),
-                                            self.trunk_ws.numel(), st), "qpinn_trunk_forward")
+            with N.timed("trunk_forward"):
+                N.check(lib.qpinn_trunk_forward(C.byref(self.desc), dc, R, ch.x.data_ptr(),
+                                                ch.y.data_ptr(), ch.t.data_ptr(), fp,
+                                                b.act.data_ptr(), self.trunk_ws.data_ptr(),
+                                                self.trunk_ws.numel(), st), "qpinn_trunk_forward")
             a0 = b.act.data_ptr()
             a1 = a0 + R * n * es
             with N.timed("pqc_forward"):
@@ -126,10 +127,12 @@ class NativeEngine:
                         b.states.data_ptr(), gz0, gz0 + R * n * es, ga0, ga0 + R * n * es,
                         gp + self.off_q * es, self.pqc_ws.data_ptr(), self.pqc_ws.numel(), st),
                         "qpinn_pqc_backward")
-                N.check(lib.qpinn_trunk_backward(C.byref(self.desc), dc, R, ch.x.data_ptr(),
-                                                 ch.y.data_ptr(), ch.t.data_ptr(), fp, a0, ga0, gp,
-                                                 self.trunk_ws.data_ptr(), self.trunk_ws.numel(),
-                                                 st), "qpinn_trunk_backward")
+                with N.timed("trunk_backward"):
+                    N.check(lib.qpinn_trunk_backward(C.byref(self.desc), dc, R, ch.x.data_ptr(),
+                                                     ch.y.data_ptr(), ch.t.data_ptr(), fp, a0,
+                                                     ga0, gp, self.trunk_ws.data_ptr(),
+                                                     self.trunk_ws.numel(), st),
+                            "qpinn_trunk_backward")
                 if g is not grad:
                     if i == 0:
                         grad.copy_(g)
@@ -139,11 +142,27 @@ class NativeEngine:
             N.count_launches(self._launches(tape))
 
     def _launches(self, tape: bool) -> int:
-        # our kernels only (the dense-layer GEMMs are cuBLAS)
-        L = self.model.n_hidden + 1             # dense layers incl. adapter
+        """Our kernels per chunk (cuBLAS GEMMs excluded), mirroring trunk.cu's
+        per-layer choice: float32 layers with 16-byte aligned widths run on the
+        tensor-core kernels (weight split + GEMM with fused dual tanh), the rest
+        on cuBLAS + a separate dual-tanh kernel."""
+        cfg = self.model.config
+        f32 = self.dtype == torch.float32
+        widths = [2 * cfg.rff_features] + [cfg.hidden_width] * self.model.n_hidden
         phase = 1 if self._has_phase else 0
-        n = (1 + L) + 2 + 2                     # features + tanh epilogues, K1 prep+main, K4+reduce
+        n = 1                                   # features
+        for k in widths:                        # hidden layers + adapter (input width k)
+            n += 2 if (f32 and k % 4 == 0) else 1
+        n += 2 + 2                              # K1 prep + main, K4 + reduce
         if tape:
             n += 4 + phase                      # K2 prep, main, reduce, u1 grads (+ phase grads)
-            n += 3 * L + 2                      # per layer tanh_bwd + colsum x2; tau x2
+            n += 1 + 2                          # adapter: tanh_bwd, bias colsum x2
+            H = cfg.hidden_width
+            for k in widths[:-1] if self.model.n_hidden else []:
+                n += 1 + 2                      # tanh_bwd, bias colsum x2
+                if f32 and k % 4 == 0 and H % 4 == 0:
+                    n += 2                      # weight gradient: split-K kernel + reduce
+                if f32 and H % 4 == 0:
+                    n += 2                      # input gradient: weight split + GEMM
+            n += 2                              # tau: features_bwd + reduce
         return n

@@ -30,3 +30,29 @@ def trunk_flops(hidden: int = 128, rff: int = 128, n_qubits: int = 7, n_hidden: 
     fwd = 2 * 4 * (6 * rff + w_in * hidden + (n_hidden - 1) * hidden * hidden
                    + hidden * n_qubits + n_qubits * 3)
     return fwd, 2 * fwd
+
+
+def trunk_bytes(hidden: int = 128, rff: int = 128, n_qubits: int = 7, n_hidden: int = 3,
+                elem: int = 4):
+    """HBM bytes per point the trunk passes must move (4 channels of every
+    activation; weights are L2-resident and not counted), per the fused
+    kernels of trunk.cu / tc_gemm.cu:
+      forward : features write H0, then every dense layer reads its input and
+                writes its dual-tanh output once
+      backward: per hidden layer the dual-tanh reverse (read dL/dH and H, write
+                dL/dU), the weight gradient (read H_in, dL/dU), the input
+                gradient (read dL/dU, write dL/dH_in) and the bias sum (read
+                dL/dU value channel); adapter likewise; tau (read dL/dH0)."""
+    c = 4 * elem
+    widths = [2 * rff] + [hidden] * n_hidden + [n_qubits]
+    fwd = 3 * elem + c * widths[0]
+    for k, n in zip(widths[:-1], widths[1:]):
+        fwd += c * (k + n)
+    bwd = 0
+    for k, n in zip(widths[:-1], widths[1:]):
+        bwd += 3 * c * n          # tanh reverse
+        bwd += c * (k + n)        # weight gradient
+        bwd += c * (n + k)        # input gradient
+        bwd += elem * n           # bias sum
+    bwd += c * widths[0] + 3 * elem
+    return fwd, bwd

@@ -1,4 +1,4 @@
-# Full GPU pass: parity suite, smoke, bench, launch list + ncu of the PQC kernels.
+# Full GPU pass: parity suite, smoke, bench, launch list + ncu captures of the top kernels.
 cd $GRAFT_REPO_ROOT
 mkdir -p gpurun_out
 timeout 900 python -m pytest tests -m gpu -q --timeout 300 -p no:cacheprovider > gpurun_out/pytest_gpu.log 2>&1
@@ -12,4 +12,9 @@ python bench.py --steps 2 --warmup 3 --no-cpu-baseline > gpurun_out/bench_small.
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv \
     python bench.py --steps 2 --warmup 3 --no-cpu-baseline > gpurun_out/ncu_launch.log 2>&1
 echo "ncu launches exit $?" >> gpurun_out/ncu_launch.log
-tail -2 gpurun_out/pytest_gpu.log; tail -2 gpurun_out/smoke.log; cat gpurun_out/bench.json; tail -1 gpurun_out/bench.err; head -3 gpurun_out/prof_step.txt
+# one full capture per hot kernel family, from the bench step itself (after warmup)
+ncu --set full --clock-control none --import-source on \
+    -k regex:'pqc_backward_layer|pqc_forward_layer|gemm3_kernel|wgrad_kernel' -s 60 -c 10 \
+    -o gpurun_out/step_full python bench.py --steps 2 --warmup 3 --no-cpu-baseline > gpurun_out/ncu_full.log 2>&1
+echo "ncu full exit $?" >> gpurun_out/ncu_full.log
+tail -2 gpurun_out/pytest_gpu.log; tail -2 gpurun_out/smoke.log; cat gpurun_out/bench.json; tail -1 gpurun_out/bench.err; head -3 gpurun_out/prof_step.txt; tail -1 gpurun_out/ncu_full.log
