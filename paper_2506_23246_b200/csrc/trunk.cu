@@ -164,6 +164,43 @@ __global__ void tanh_bwd(int64_t R, int N, const T* __restrict__ GY, const T* __
   }
 }
 
+// tanh_bwd fused with the bias gradient: block b owns rows [b*rows_per, ...),
+// thread t column t % N; the value-channel dL/du column sums of the block go
+// to partial[b][N] (reduced in block order by colsum_reduce: deterministic)
+template <typename T>
+__global__ void tanh_bwd_bias(int64_t R, int N, int64_t rows_per, const T* __restrict__ GY,
+                              const T* __restrict__ Y, T* __restrict__ GU,
+                              double* __restrict__ partial) {
+  extern __shared__ double red[];
+  const int per = blockDim.x / N;  // rows processed together
+  const int j = threadIdx.x % N, r_off = threadIdx.x / N;
+  const int64_t n = R * N;
+  const int64_t r0 = (int64_t)blockIdx.x * rows_per;
+  const int64_t r1 = r0 + rows_per < R ? r0 + rows_per : R;
+  double acc = 0.0;
+  if (r_off < per) {
+    for (int64_t r = r0 + r_off; r < r1; r += per) {
+      const int64_t i = r * N + j;
+      const T yv = Y[i];
+      const T s = T(1) - yv * yv;
+      const T g1 = GY[n + i], g2 = GY[2 * n + i], g3 = GY[3 * n + i];
+      const T gu = GY[i] * s + (g1 * Y[n + i] + g2 * Y[2 * n + i] + g3 * Y[3 * n + i]) * (T(-2) * yv);
+      GU[i] = gu;
+      GU[n + i] = g1 * s;
+      GU[2 * n + i] = g2 * s;
+      GU[3 * n + i] = g3 * s;
+      acc += (double)gu;
+    }
+  }
+  red[threadIdx.x] = acc;
+  __syncthreads();
+  if (threadIdx.x < N) {
+    double v = 0.0;
+    for (int k = 0; k < per; ++k) v += red[k * N + threadIdx.x];
+    partial[(int64_t)blockIdx.x * N + threadIdx.x] = v;
+  }
+}
+
 // deterministic column sums of X [R, N]: block b sums rows [b*rows_per, ...)
 template <typename T>
 __global__ void colsum_partial(int64_t R, int N, int64_t rows_per, const T* __restrict__ X,
@@ -177,12 +214,22 @@ __global__ void colsum_partial(int64_t R, int N, int64_t rows_per, const T* __re
   }
 }
 
+// out[j] = sum_b partial[b][j]: 32 columns x 8 interleaved block groups per CTA,
+// group sums combined in fixed order (deterministic)
 template <typename T>
 __global__ void colsum_reduce(int nb, int N, const double* __restrict__ partial, T* __restrict__ out) {
-  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < N; j += gridDim.x * blockDim.x) {
-    double acc = 0.0;
-    for (int b = 0; b < nb; ++b) acc += partial[(int64_t)b * N + j];
-    out[j] = T(acc);
+  __shared__ double red[8][32];
+  const int c = threadIdx.x & 31, grp = threadIdx.x >> 5;
+  const int j = blockIdx.x * 32 + c;
+  double acc = 0.0;
+  if (j < N)
+    for (int b = grp; b < nb; b += 8) acc += partial[(int64_t)b * N + j];
+  red[grp][c] = acc;
+  __syncthreads();
+  if (grp == 0 && j < N) {
+    double v = 0.0;
+    for (int g = 0; g < 8; ++g) v += red[g][c];
+    out[j] = T(v);
   }
 }
 
@@ -265,6 +312,7 @@ struct TrunkWS {
 };
 
 constexpr int kColBlocks = 256;
+constexpr int kTanhBlocks = 592;  // 4 per SM for the fused reverse dual tanh
 constexpr int kTauBlocks = 296;
 
 static TrunkWS trunk_ws(const qpinn_trunk_desc* d, size_t es, int64_t R) {
@@ -284,7 +332,8 @@ static TrunkWS trunk_ws(const qpinn_trunk_desc* d, size_t es, int64_t R) {
   w.g0 = take(gmax);
   w.g1 = take(gmax);
   w.part = o;
-  o += ((size_t)kColBlocks * (H > (size_t)d->n_out ? H : d->n_out) * 8 + 255) / 256 * 256;
+  o += ((size_t)(kColBlocks > kTanhBlocks ? kColBlocks : kTanhBlocks) *
+            (H > (size_t)d->n_out ? H : d->n_out) * 8 + 255) / 256 * 256;
   w.tau_part = o;
   o += (kTauBlocks * 8 + 255) / 256 * 256;
   // float32 tensor-core scratch, used by one GEMM at a time: the tf32 hi/lo
@@ -309,11 +358,32 @@ static int grid_1d(int64_t n) {
 }
 
 template <typename T>
+static int bias_grad(int64_t R, int N, const T* GU0, double* part, T* out, cudaStream_t st);
+
+// GU = reverse dual tanh (GY, Y) and out = column sums of GU's value channel
+template <typename T>
+static int tanh_bwd_and_bias(int64_t R, int N, const T* GY, const T* Y, T* GU, double* part,
+                             T* out, cudaStream_t st) {
+  const int threads = N <= 256 ? (256 / N) * N : 0;
+  if (threads == 0) {  // wide layers: separate kernels
+    tanh_bwd<T><<<grid_1d(R * N), 256, 0, st>>>(R, N, GY, Y, GU);
+    QPINN_CUDA_CHECK(cudaGetLastError());
+    return bias_grad<T>(R, N, GU, part, out, st);
+  }
+  const int64_t rows_per = (R + kTanhBlocks - 1) / kTanhBlocks;
+  const int nb = (int)((R + rows_per - 1) / rows_per);
+  tanh_bwd_bias<T><<<nb, threads, threads * sizeof(double), st>>>(R, N, rows_per, GY, Y, GU, part);
+  colsum_reduce<T><<<(N + 31) / 32, 256, 0, st>>>(nb, N, part, out);
+  QPINN_CUDA_CHECK(cudaGetLastError());
+  return QPINN_OK;
+}
+
+template <typename T>
 static int bias_grad(int64_t R, int N, const T* GU0, double* part, T* out, cudaStream_t st) {
   const int64_t rows_per = (R + kColBlocks - 1) / kColBlocks;
   const int nb = (int)((R + rows_per - 1) / rows_per);
   colsum_partial<T><<<nb, N < 128 ? 32 * ((N + 31) / 32) : 128, 0, st>>>(R, N, rows_per, GU0, part);
-  colsum_reduce<T><<<(N + 127) / 128, 128, 0, st>>>(nb, N, part, out);
+  colsum_reduce<T><<<(N + 31) / 32, 256, 0, st>>>(nb, N, part, out);
   QPINN_CUDA_CHECK(cudaGetLastError());
   return QPINN_OK;
 }
@@ -368,18 +438,20 @@ static int backward_impl(const qpinn_trunk_desc* d, int64_t R, const T* x, const
   // adapter: GU = tanh_bwd(g_act); dWa = H_last^T GU; dba = colsum(GU0); G_H = GU Wa^T
   const T* Hl = (const T*)(ws + (d->n_hidden ? w.h[d->n_hidden - 1] : w.h0));
   const int Kl = d->n_hidden ? H : 2 * F;
-  tanh_bwd<T><<<grid_1d(R * n), 256, 0, st>>>(R, n, g_act, act, g1);
+  if (int rc = tanh_bwd_and_bias<T>(R, n, g_act, act, g1, part, grad + d->off_adapter_b, st))
+    return rc;
   QPINN_CUDA_CHECK(cudaGetLastError());
   if (int rc = gemm_rm<T>(h, true, false, Kl, n, 4 * R, Hl, Kl, g1, n, grad + d->off_adapter_w, n, T(0)))
     return rc;
-  if (int rc = bias_grad<T>(R, n, g1, part, grad + d->off_adapter_b, st)) return rc;
   if (int rc = gemm_rm<T>(h, false, true, 4 * R, Kl, n, g1, n, params + d->off_adapter_w, n, g0, Kl, T(0)))
     return rc;
   // hidden layers, last to first; g0 holds dL/dH_{i+1}
   for (int i = d->n_hidden - 1; i >= 0; --i) {
     const int K = i == 0 ? 2 * F : H;
     const T* Hin = (const T*)(ws + (i == 0 ? w.h0 : w.h[i - 1]));
-    tanh_bwd<T><<<grid_1d(R * H), 256, 0, st>>>(R, H, g0, (const T*)(ws + w.h[i]), g1);
+    if (int rc = tanh_bwd_and_bias<T>(R, H, g0, (const T*)(ws + w.h[i]), g1, part,
+                                      grad + d->off_b[i], st))
+      return rc;
     QPINN_CUDA_CHECK(cudaGetLastError());
     if (sizeof(T) == 4 && K % 4 == 0 && H % 4 == 0) {  // dW = H_in^T GU on the tensor cores
       if (int rc = tc::wgrad(4 * R, K, H, (const float*)Hin, K, (const float*)g1, H,
@@ -389,7 +461,6 @@ static int backward_impl(const qpinn_trunk_desc* d, int64_t R, const T* x, const
                                    H, T(0))) {
       return rc;
     }
-    if (int rc = bias_grad<T>(R, H, g1, part, grad + d->off_b[i], st)) return rc;
     if (sizeof(T) == 4 && H % 4 == 0) {  // dL/dH_in = GU W^T on the tensor cores
       if (int rc = tc::gemm3(4 * R, K, H, (const float*)g1, H, (const float*)(params + d->off_w[i]),
                              H, (float*)g0, K, ws + w.wsplit, w.total - w.wsplit, st))

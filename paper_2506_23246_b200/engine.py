@@ -156,10 +156,10 @@ class NativeEngine:
         n += 2 + 2                              # K1 prep + main, K4 + reduce
         if tape:
             n += 4 + phase                      # K2 prep, main, reduce, u1 grads (+ phase grads)
-            n += 1 + 2                          # adapter: tanh_bwd, bias colsum x2
+            n += 2                              # adapter: reverse dual tanh + bias partials, reduce
             H = cfg.hidden_width
             for k in widths[:-1] if self.model.n_hidden else []:
-                n += 1 + 2                      # tanh_bwd, bias colsum x2
+                n += 2 if H <= 256 else 3       # reverse dual tanh (+ fused bias partials), reduce
                 if f32 and k % 4 == 0 and H % 4 == 0:
                     n += 2                      # weight gradient: split-K kernel + reduce
                 if f32 and H % 4 == 0:
