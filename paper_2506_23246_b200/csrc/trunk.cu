@@ -234,11 +234,13 @@ __global__ void colsum_reduce(int nb, int N, const double* __restrict__ partial,
 }
 
 // dL/dtau_raw through at = 2 pi t / tau and the t-tangent features (one warp per point)
+// (cos, sin of the projections are read back from the forward's H0 value channel)
 template <typename T>
 __global__ void features_bwd(int64_t R, int F, const T* __restrict__ x, const T* __restrict__ y,
                              const T* __restrict__ t, const T* __restrict__ omega,
                              const T* __restrict__ params, int64_t off_tau, T t_dom,
-                             const T* __restrict__ G0, double* __restrict__ partial) {
+                             const T* __restrict__ H0, const T* __restrict__ G0,
+                             double* __restrict__ partial) {
   const T tau = tau_of(params, off_tau, t_dom);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, warps = blockDim.x >> 5;
   const int64_t W = 2 * (int64_t)F;
@@ -253,11 +255,9 @@ __global__ void features_bwd(int64_t R, int F, const T* __restrict__ x, const T*
     T G4 = 0, G5 = 0, D4 = 0, D5 = 0;
     for (int f = lane; f < F; f += 32) {
       const T* om = omega + 6 * f;
-      const T proj = sx * om[0] + cx * om[1] + sy * om[2] + cy * om[3] + st * om[4] + ct * om[5];
       const T dps[3] = {T(kPi) * cx * om[0] - T(kPi) * sx * om[1],
                         T(kPi) * cy * om[2] - T(kPi) * sy * om[3], w * ct * om[4] - w * st * om[5]};
-      T sp, cp;
-      sincos_t(proj, &sp, &cp);
+      const T cp = H0[p * W + f], sp = H0[p * W + F + f];
       const T gc = G0[p * W + f], gs = G0[p * W + F + f];
       T gproj = -sp * gc + cp * gs, gdp2 = 0;
 #pragma unroll
@@ -295,15 +295,24 @@ __global__ void features_bwd(int64_t R, int F, const T* __restrict__ x, const T*
   }
 }
 
+// one block: strided per-thread sums, then a fixed-order tree (deterministic)
 template <typename T>
 __global__ void tau_grad_reduce(int nb, const double* __restrict__ partial, const T* __restrict__ params,
                                 int64_t off_tau, T t_dom, T* __restrict__ grad) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  __shared__ double red[256];
   double v = 0.0;
-  for (int b = 0; b < nb; ++b) v += partial[b];
-  const double raw = (double)params[off_tau];
-  const double sig = 0.5 * (1.0 + tanh(0.5 * raw));  // d softplus / d raw
-  grad[off_tau] = T(v * (double)t_dom * sig);
+  for (int b = threadIdx.x; b < nb; b += blockDim.x) v += partial[b];
+  red[threadIdx.x] = v;
+  __syncthreads();
+  for (int m = blockDim.x / 2; m > 0; m >>= 1) {
+    if (threadIdx.x < m) red[threadIdx.x] += red[threadIdx.x + m];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    const double raw = (double)params[off_tau];
+    const double sig = 0.5 * (1.0 + tanh(0.5 * raw));  // d softplus / d raw
+    grad[off_tau] = T(red[0] * (double)t_dom * sig);
+  }
 }
 
 // ---- workspace plan ----------------------------------------------------------------------------
@@ -313,7 +322,7 @@ struct TrunkWS {
 
 constexpr int kColBlocks = 256;
 constexpr int kTanhBlocks = 592;  // 4 per SM for the fused reverse dual tanh
-constexpr int kTauBlocks = 296;
+constexpr int kTauBlocks = 1184;  // 8 per SM: the tau pass is latency bound
 
 static TrunkWS trunk_ws(const qpinn_trunk_desc* d, size_t es, int64_t R) {
   TrunkWS w{};
@@ -473,8 +482,9 @@ static int backward_impl(const qpinn_trunk_desc* d, int64_t R, const T* x, const
   // tau_raw through the time features
   double* tp = (double*)(ws + w.tau_part);
   features_bwd<T><<<kTauBlocks, 256, 0, st>>>(R, F, x, y, t, (const T*)d->omega, params,
-                                               d->off_tau_raw, (T)d->t_domain, g0, tp);
-  tau_grad_reduce<T><<<1, 32, 0, st>>>(kTauBlocks, tp, params, d->off_tau_raw, (T)d->t_domain, grad);
+                                               d->off_tau_raw, (T)d->t_domain,
+                                               (const T*)(ws + w.h0), g0, tp);
+  tau_grad_reduce<T><<<1, 256, 0, st>>>(kTauBlocks, tp, params, d->off_tau_raw, (T)d->t_domain, grad);
   QPINN_CUDA_CHECK(cudaGetLastError());
   return QPINN_OK;
 }
