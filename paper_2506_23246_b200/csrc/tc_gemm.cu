@@ -2,10 +2,11 @@
 //
 // C[M,N] = A[M,K] B[N,K]^T, fp32 in / fp32 out, both operands K-major
 // (row-major with K contiguous).  Persistent CTAs walk 128 x BN output tiles;
-// per CTA (352 threads):
+// per CTA (320 threads):
 //   warp 8      TMA producer for A (fp32), 32 K-columns (one 128-byte swizzle
 //               row) per stage, 3 stages ahead
-//   warp 10     TMA producer for the pre-split B_hi / B_lo tiles (L2-resident)
+//   warp 8 / 1  TMA producer for the pre-split B_hi / B_lo tiles (L2-resident;
+//               a second lane of the producer warp, independently scheduled)
 //   warps 0-3   split A into A_hi / A_lo operand buffers
 //   warp 9      MMA issuer (one thread): per stage 4 K-steps x 3 products
 //               A_lo B_hi + A_hi B_lo + A_hi B_hi into a fresh TMEM buffer
@@ -19,6 +20,7 @@
 // B (the layer weights, small) is split once per call into a workspace.
 #include <cudaTypedefs.h>
 
+#include <cstring>
 #include <mutex>
 
 #include "tc_gemm.cuh"
@@ -28,22 +30,29 @@ namespace tc {
 
 constexpr int kBM = 128, kBK = 32;
 constexpr int kABytes = kBM * kBK * 4;  // 16 KB fp32 tile
-constexpr int kThreadsGemm = 352;
+constexpr int kThreadsGemm = 320;
 enum { EPI_STORE = 0, EPI_TANH = 1 };
 
 template <int BN>
 struct GemmCfg {
   static constexpr int kBBytes = BN * kBK * 4;
-  static constexpr int kRaw = 3;   // fp32 A stages in flight from HBM
+#ifndef QPINN_GEMM_RAW
+#define QPINN_GEMM_RAW 2
+#endif
+#ifndef QPINN_GEMM_BS
+#define QPINN_GEMM_BS 2
+#endif
+  static constexpr int kRaw = QPINN_GEMM_RAW;   // fp32 A stages in flight from HBM
   static constexpr int kOps = 2;   // split A buffers (A_hi, A_lo)
   static constexpr int kOpBytes = 2 * kABytes;
-  static constexpr int kBS = 3;    // B_hi / B_lo stages (from L2)
+  static constexpr int kBS = QPINN_GEMM_BS;    // B_hi / B_lo stages (from L2)
   static constexpr int kBStage = 2 * kBBytes;
   static constexpr int kNB = 4;    // TMEM partial buffers
   static constexpr int kTmemCols = kNB * BN;
   static constexpr int kSbuf = 32 * BN * 4;
+  static constexpr int kStg = 4 * 2 * 4096;  // per epilogue warp: 2 x (32 rows x 32 cols)
   static constexpr int kSmem =
-      kRaw * kABytes + kOps * kOpBytes + kBS * kBStage + kSbuf + 1024 + 512;
+      kRaw * kABytes + kOps * kOpBytes + kBS * kBStage + kSbuf + kStg + 1024 + 512;
 };
 
 struct GemmArgs {
@@ -53,12 +62,42 @@ struct GemmArgs {
   float* C;
   int64_t ldc;
   const float* bias;  // EPI_TANH
+  int tma_store;      // C goes out through TMA (16-byte aligned rows), else direct stores
 };
+
+// one epilogue warp's 32 rows x BN columns (lane = row) -> global through two
+// 4 KB staging buffers (128-byte swizzled, conflict-free) and TMA stores of
+// 32 x 32 boxes at (col0 + c, row0, blk) of the 3-D output map
+template <int BN>
+__device__ __forceinline__ void store_rows_tma(const float (&acc)[BN], unsigned char* stg,
+                                               const CUtensorMap* mC, int col0, int row0,
+                                               int blk, int lane, int& nbuf) {
+#pragma unroll
+  for (int c0 = 0; c0 < BN; c0 += 32) {
+    unsigned char* buf = stg + (nbuf & 1) * 4096;
+    if (lane == 0) bulk_wait_read1();  // the store that used this buffer has read it
+    __syncwarp();
+    const uint32_t base = smem_u32(buf) + lane * 128;
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      sts128(base + ((j ^ (lane & 7)) << 4),
+             make_float4(acc[c0 + 4 * j], acc[c0 + 4 * j + 1], acc[c0 + 4 * j + 2],
+                         acc[c0 + 4 * j + 3]));
+    fence_proxy_async_smem();
+    __syncwarp();
+    if (lane == 0) {
+      tma_store_3d(mC, buf, col0 + c0, row0, blk);
+      bulk_commit();
+    }
+    ++nbuf;
+  }
+}
 
 template <int BN, int EPI>
 __global__ void __launch_bounds__(kThreadsGemm, 1)
 gemm3_kernel(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUtensorMap mBhi,
-             const __grid_constant__ CUtensorMap mBlo, const GemmArgs g) {
+             const __grid_constant__ CUtensorMap mBlo, const __grid_constant__ CUtensorMap mC,
+             const GemmArgs g) {
   using Cfg = GemmCfg<BN>;
   constexpr int RS = Cfg::kRaw, OS = Cfg::kOps, BS = Cfg::kBS, NB = Cfg::kNB;
   extern __shared__ unsigned char smem_raw[];
@@ -67,7 +106,8 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUt
   unsigned char* ops = smem + RS * kABytes;         // [OS][A_hi | A_lo]
   unsigned char* bst = ops + OS * Cfg::kOpBytes;    // [BS][B_hi | B_lo]
   float* sbuf = (float*)(bst + BS * Cfg::kBStage);
-  uint64_t* raw_full = (uint64_t*)((unsigned char*)sbuf + Cfg::kSbuf);
+  unsigned char* stg = (unsigned char*)sbuf + Cfg::kSbuf;  // [4 warps][2][4 KB]
+  uint64_t* raw_full = (uint64_t*)(stg + Cfg::kStg);
   uint64_t* raw_empty = raw_full + RS;
   uint64_t* b_full = raw_empty + RS;
   uint64_t* b_empty = b_full + BS;
@@ -133,8 +173,9 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUt
         }
       }
     }
-  } else if (warp == 10) {  // ---- TMA producer for the split B tiles (L2-resident)
-    if (lane == 0) {
+  }
+  if (warp == 8) {  // ---- TMA producer for the split B tiles (L2-resident), lane 1
+    if (lane == 1) {
       int64_t j = 0;
       for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
         const int nt = (int)(t % n_nt);
@@ -223,6 +264,8 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUt
   } else {  // ---- warps 4-7: promote partials, epilogue
     const int q = warp - 4;  // TMEM lanes 32q .. 32q+31
     const uint32_t lane_base = (uint32_t)(q * 32) << 16;
+    unsigned char* my_stg = stg + q * 8192;
+    int nbuf = 0;
     int64_t j = 0;
     for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
       const int64_t mt = t / n_nt;
@@ -252,7 +295,9 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUt
       }
       if constexpr (EPI == EPI_STORE) {
         const int64_t row = mt * kBM + q * 32 + lane;
-        if (row < g.M) {
+        if (g.tma_store) {
+          store_rows_tma<BN>(acc, my_stg, &mC, n0, (int)(mt * kBM + q * 32), 0, lane, nbuf);
+        } else if (row < g.M) {
           float* dst = g.C + row * g.ldc + n0;
           if (n0 + BN <= g.N && (g.ldc & 3) == 0) {
 #pragma unroll
@@ -286,7 +331,9 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUt
           const float y = sbuf[c * 32 + lane];
           acc[c] = q == 0 ? y : (1.f - y * y) * acc[c];
         }
-        if (p < g.R) {
+        if (g.tma_store) {
+          store_rows_tma<BN>(acc, my_stg, &mC, n0, (int)(mt * 32), q, lane, nbuf);
+        } else if (p < g.R) {
           float* dst = g.C + ((int64_t)q * g.R + p) * g.ldc + n0;
           if (n0 + BN <= g.N && (g.ldc & 3) == 0) {
 #pragma unroll
@@ -303,6 +350,7 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUt
       }
     }
   }
+  if (warp >= 4 && warp < 8 && lane == 0) bulk_wait_all();
   tc_fence_before();
   __syncthreads();
   if (warp == 9) tmem_dealloc(tmem, Cfg::kTmemCols);
@@ -326,7 +374,7 @@ struct WgradArgs {
   float* partial;       // [n_kc][Kin][Nout]
 };
 
-__global__ void __launch_bounds__(kThreadsGemm - 32, 1)
+__global__ void __launch_bounds__(kThreadsGemm, 1)
 wgrad_kernel(const __grid_constant__ CUtensorMap mX, const __grid_constant__ CUtensorMap mG,
              const WgradArgs g) {
   constexpr int RS = kWRaw, OS = kWOps, NB = kWNB, P = kWPromote;
@@ -595,10 +643,36 @@ static inline int ldk_of(int K) { return (K + 3) & ~3; }
 
 size_t gemm3_workspace_bytes(int N, int K) { return 2 * (size_t)N * ldk_of(K) * 4 + 256; }
 
+// 3-D fp32 output map (cols, rows per block, blocks), 32 x 32 boxes, 128-byte swizzle
+static int make_out_map(CUtensorMap* m, const float* base, uint64_t cols, uint64_t rows,
+                        uint64_t blocks, uint64_t ld) {
+  auto fn = encode_fn();
+  if (!fn) return fail(QPINN_ERR_CUDA, "cuTensorMapEncodeTiled is unavailable");
+  cuuint64_t dims[3] = {cols, rows, blocks};
+  cuuint64_t strides[2] = {ld * 4, ld * 4 * rows};
+  cuuint32_t box[3] = {32, 32, 1};
+  cuuint32_t es[3] = {1, 1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(base), dims, strides,
+                  box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(QPINN_ERR_CUDA, "cuTensorMapEncodeTiled (output) failed");
+  return QPINN_OK;
+}
+
 template <int BN, int EPI>
-static int launch_gemm3(const GemmArgs& g, const float* A, int64_t lda, const float* Bhi,
+static int launch_gemm3(const GemmArgs& g0, const float* A, int64_t lda, const float* Bhi,
                         const float* Blo, int ldk, cudaStream_t st) {
-  CUtensorMap mA, mBh, mBl;
+  GemmArgs g = g0;
+  CUtensorMap mA, mBh, mBl, mC;
+  g.tma_store = ((uintptr_t)g.C & 15) == 0 && (g.ldc & 3) == 0;
+  if (g.tma_store) {
+    const uint64_t rows = EPI == EPI_TANH ? (uint64_t)g.R : (uint64_t)g.M;
+    if (int rc = make_out_map(&mC, g.C, (uint64_t)g.N, rows, EPI == EPI_TANH ? 4 : 1,
+                              (uint64_t)g.ldc))
+      return rc;
+  } else {
+    memset(&mC, 0, sizeof(mC));
+  }
   const uint32_t a_box = EPI == EPI_TANH ? 32 : kBM;
   if (int rc = make_map(&mA, A, (uint64_t)g.M, (uint64_t)g.K, (uint64_t)lda, a_box)) return rc;
   if (int rc = make_map(&mBh, Bhi, (uint64_t)g.N, (uint64_t)ldk, (uint64_t)ldk, BN)) return rc;
@@ -609,7 +683,7 @@ static int launch_gemm3(const GemmArgs& g, const float* A, int64_t lda, const fl
   const int64_t n_mt = EPI == EPI_TANH ? (g.R + 31) / 32 : (g.M + kBM - 1) / kBM;
   const int64_t tiles = n_mt * ((g.N + BN - 1) / BN);
   const int grid = (int)(tiles < num_sms() ? tiles : num_sms());
-  kern<<<grid, kThreadsGemm, GemmCfg<BN>::kSmem, st>>>(mA, mBh, mBl, g);
+  kern<<<grid, kThreadsGemm, GemmCfg<BN>::kSmem, st>>>(mA, mBh, mBl, mC, g);
   QPINN_CUDA_CHECK(cudaGetLastError());
   return QPINN_OK;
 }
@@ -631,7 +705,7 @@ int gemm3(int64_t M, int N, int K, const float* A, int64_t lda, const float* B, 
   float* lo = hi + (size_t)N * ldk;
   split_rows<<<64, 256, 0, st>>>(B, N, K, ldb, ldk, hi, lo);
   QPINN_CUDA_CHECK(cudaGetLastError());
-  GemmArgs g{M, 0, N, K, C, ldc, nullptr};
+  GemmArgs g{M, 0, N, K, C, ldc, nullptr, 0};
   return dispatch<EPI_STORE>(g, A, lda, hi, lo, ldk, st);
 }
 
@@ -677,7 +751,7 @@ int wgrad(int64_t rows, int Kin, int Nout, const float* X, int64_t ldx, const fl
       cudaFuncSetAttribute(wgrad_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kWSmem));
   const int64_t items = (int64_t)a.n_mt * a.n_nt * a.n_kc;
   const int grid = (int)(items < num_sms() ? items : num_sms());
-  wgrad_kernel<<<grid, kThreadsGemm - 32, kWSmem, st>>>(mX, mG, a);
+  wgrad_kernel<<<grid, kThreadsGemm, kWSmem, st>>>(mX, mG, a);
   QPINN_CUDA_CHECK(cudaGetLastError());
   const int64_t n = (int64_t)Kin * Nout;
   wgrad_reduce<<<(int)((n + 255) / 256 < 1024 ? (n + 255) / 256 : 1024), 256, 0, st>>>(
@@ -696,7 +770,7 @@ int dense_tanh(int64_t R, int N, int K, const float* X, const float* W, const fl
   float* lo = hi + (size_t)N * ldk;
   split_transpose<<<64, 256, 0, st>>>(W, K, N, ldk, hi, lo);
   QPINN_CUDA_CHECK(cudaGetLastError());
-  GemmArgs g{4 * R, R, N, K, H, N, bias};
+  GemmArgs g{4 * R, R, N, K, H, N, bias, 0};
   return dispatch<EPI_TANH>(g, X, K, hi, lo, ldk, st);
 }
 
