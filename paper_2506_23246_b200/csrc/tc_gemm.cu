@@ -2,15 +2,15 @@
 //
 // C[M,N] = A[M,K] B[N,K]^T, fp32 in / fp32 out, both operands K-major
 // (row-major with K contiguous).  Persistent CTAs walk 128 x BN output tiles;
-// per CTA (320 threads):
-//   warp 8      TMA producer for A (fp32), 32 K-columns (one 128-byte swizzle
-//               row) per stage, 3 stages ahead
-//   warp 8 / 1  TMA producer for the pre-split B_hi / B_lo tiles (L2-resident;
-//               a second lane of the producer warp, independently scheduled)
+// per CTA (448 threads):
+//   warp 12     TMA producer for A (fp32), 32 K-columns (one 128-byte swizzle
+//               row) per stage; lane 1 of the same warp (independently
+//               scheduled) produces the pre-split B_hi / B_lo tiles
 //   warps 0-3   split A into A_hi / A_lo operand buffers
-//   warp 9      MMA issuer (one thread): per stage 4 K-steps x 3 products
+//   warp 13     MMA issuer (one thread): per stage 4 K-steps x 3 products
 //               A_lo B_hi + A_hi B_lo + A_hi B_hi into a fresh TMEM buffer
-//   warps 4-7   promote every k-block partial from TMEM into fp32 registers
+//   warps 4-11  promote every k-block partial from TMEM into fp32 registers
+//               (warps w, w + 4 share TMEM lanes 32 (w % 4).., half the columns each)
 //               (the tensor core's own fp32 accumulation truncates, so long
 //               K chains drift; 32-deep partials + IEEE adds stay FP32-class)
 //               and run the fused epilogue, overlapping the next tile's MMAs
@@ -30,7 +30,8 @@ namespace tc {
 
 constexpr int kBM = 128, kBK = 32;
 constexpr int kABytes = kBM * kBK * 4;  // 16 KB fp32 tile
-constexpr int kThreadsGemm = 320;
+constexpr int kThreadsGemm = 448;  // 4 split + 8 epilogue + producer + MMA warps
+constexpr int kThreadsW = 320;      // weight gradient: 4 split + 4 epilogue + producer + MMA
 enum { EPI_STORE = 0, EPI_TANH = 1 };
 
 template <int BN>
@@ -50,7 +51,7 @@ struct GemmCfg {
   static constexpr int kNB = 4;    // TMEM partial buffers
   static constexpr int kTmemCols = kNB * BN;
   static constexpr int kSbuf = 32 * BN * 4;
-  static constexpr int kStg = 4 * 2 * 4096;  // per epilogue warp: 2 x (32 rows x 32 cols)
+  static constexpr int kStg = 8 * 4096;  // per epilogue warp: 32 rows x 32 cols
   static constexpr int kSmem =
       kRaw * kABytes + kOps * kOpBytes + kBS * kBStage + kSbuf + kStg + 1024 + 512;
 };
@@ -65,17 +66,16 @@ struct GemmArgs {
   int tma_store;      // C goes out through TMA (16-byte aligned rows), else direct stores
 };
 
-// one epilogue warp's 32 rows x BN columns (lane = row) -> global through two
-// 4 KB staging buffers (128-byte swizzled, conflict-free) and TMA stores of
+// one epilogue warp's 32 rows x CW columns (lane = row) -> global through a
+// 4 KB staging buffer (128-byte swizzled, conflict-free) and TMA stores of
 // 32 x 32 boxes at (col0 + c, row0, blk) of the 3-D output map
-template <int BN>
-__device__ __forceinline__ void store_rows_tma(const float (&acc)[BN], unsigned char* stg,
+template <int CW>
+__device__ __forceinline__ void store_rows_tma(const float (&acc)[CW], unsigned char* buf,
                                                const CUtensorMap* mC, int col0, int row0,
-                                               int blk, int lane, int& nbuf) {
+                                               int blk, int lane) {
 #pragma unroll
-  for (int c0 = 0; c0 < BN; c0 += 32) {
-    unsigned char* buf = stg + (nbuf & 1) * 4096;
-    if (lane == 0) bulk_wait_read1();  // the store that used this buffer has read it
+  for (int c0 = 0; c0 < CW; c0 += 32) {
+    if (lane == 0) bulk_wait_read0();  // the previous store has read the buffer
     __syncwarp();
     const uint32_t base = smem_u32(buf) + lane * 128;
 #pragma unroll
@@ -89,7 +89,6 @@ __device__ __forceinline__ void store_rows_tma(const float (&acc)[BN], unsigned 
       tma_store_3d(mC, buf, col0 + c0, row0, blk);
       bulk_commit();
     }
-    ++nbuf;
   }
 }
 
@@ -137,22 +136,22 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUt
     }
     for (int b = 0; b < NB; ++b) {
       mbar_init(tfull + b, 1);
-      mbar_init(tempty + b, 4);
+      mbar_init(tempty + b, 8);
     }
     mbar_init_fence();
   }
-  if (warp == 8 && lane == 0) {
+  if (warp == 12 && lane == 0) {
     tma_prefetch(&mA);
     tma_prefetch(&mBhi);
     tma_prefetch(&mBlo);
   }
-  if (warp == 9) tmem_alloc(tmem_slot, Cfg::kTmemCols);
+  if (warp == 13) tmem_alloc(tmem_slot, Cfg::kTmemCols);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  if (warp == 8) {  // ---- TMA producer for A (runs RS k-blocks ahead)
+  if (warp == 12) {  // ---- TMA producer for A (runs RS k-blocks ahead)
     if (lane == 0) {
       int64_t j = 0;
       for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
@@ -174,7 +173,7 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUt
       }
     }
   }
-  if (warp == 8) {  // ---- TMA producer for the split B tiles (L2-resident), lane 1
+  if (warp == 12) {  // ---- TMA producer for the split B tiles (L2-resident), lane 1
     if (lane == 1) {
       int64_t j = 0;
       for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
@@ -189,7 +188,7 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUt
         }
       }
     }
-  } else if (warp == 9) {  // ---- MMA issuer
+  } else if (warp == 13) {  // ---- MMA issuer
     if (lane == 0) {
       constexpr uint32_t idesc = idesc_tf32(kBM, BN);
       int64_t j = 0;
@@ -261,31 +260,27 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUt
         }
       }
     }
-  } else {  // ---- warps 4-7: promote partials, epilogue
-    const int q = warp - 4;  // TMEM lanes 32q .. 32q+31
+  } else {  // ---- warps 4-11: promote partials, epilogue
+    // warp w reads TMEM lanes 32 (w % 4) ..; warps w and w + 4 split the columns
+    const int q = warp & 3, h = (warp - 4) >> 2;
+    constexpr int CW = BN / 2;  // columns per epilogue warp
     const uint32_t lane_base = (uint32_t)(q * 32) << 16;
-    unsigned char* my_stg = stg + q * 8192;
-    int nbuf = 0;
+    unsigned char* my_stg = stg + (warp - 4) * 4096;
     int64_t j = 0;
     for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
       const int64_t mt = t / n_nt;
-      const int n0 = (int)(t % n_nt) * BN;
-      float acc[BN];
+      const int n0 = (int)(t % n_nt) * BN, c_off = h * CW;
+      float acc[CW];
 #pragma unroll
-      for (int c = 0; c < BN; ++c) acc[c] = 0.f;
+      for (int c = 0; c < CW; ++c) acc[c] = 0.f;
       for (int kb = 0; kb < nk; ++kb, ++j) {
         const int b = (int)(j % NB);
         mbar_wait(tfull + b, (uint32_t)((j / NB) & 1));
         tc_fence_after();
 #pragma unroll
-        for (int c0 = 0; c0 < BN; c0 += 32) {
+        for (int c0 = 0; c0 < CW; c0 += 32) {
           float v[32];
-#ifndef QPINN_GEMM_NOPROMOTE
-          tmem_ld32(tmem + lane_base + b * BN + c0, v);
-#else
-#pragma unroll
-          for (int i = 0; i < 32; ++i) v[i] = 0.f;
-#endif
+          tmem_ld32(tmem + lane_base + b * BN + c_off + c0, v);
 #pragma unroll
           for (int i = 0; i < 32; ++i) acc[c0 + i] += v[i];
         }
@@ -296,64 +291,50 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUt
       if constexpr (EPI == EPI_STORE) {
         const int64_t row = mt * kBM + q * 32 + lane;
         if (g.tma_store) {
-          store_rows_tma<BN>(acc, my_stg, &mC, n0, (int)(mt * kBM + q * 32), 0, lane, nbuf);
+          store_rows_tma<CW>(acc, my_stg, &mC, n0 + c_off, (int)(mt * kBM + q * 32), 0, lane);
         } else if (row < g.M) {
-          float* dst = g.C + row * g.ldc + n0;
-          if (n0 + BN <= g.N && (g.ldc & 3) == 0) {
+          float* dst = g.C + row * g.ldc + n0 + c_off;
 #pragma unroll
-            for (int c = 0; c < BN; c += 4)
-              *reinterpret_cast<float4*>(dst + c) =
-                  make_float4(acc[c], acc[c + 1], acc[c + 2], acc[c + 3]);
-          } else {
-#pragma unroll
-            for (int c = 0; c < BN; ++c)
-              if (n0 + c < g.N) dst[c] = acc[c];
-          }
+          for (int c = 0; c < CW; ++c)
+            if (n0 + c_off + c < g.N) dst[c] = acc[c];
         }
       } else {  // EPI_TANH: q = channel, lane = point
         // the value channel's pre-activations go through shared memory so that
-        // all four warps share the tanh work (32 columns each)
+        // all eight warps share the tanh work (BN / 8 columns each)
         const int64_t p = mt * 32 + lane;
         if (q == 0) {
 #pragma unroll
-          for (int c = 0; c < BN; ++c) sbuf[c * 32 + lane] = acc[c];
+          for (int c = 0; c < CW; ++c) sbuf[(c_off + c) * 32 + lane] = acc[c];
         }
-        asm volatile("bar.sync 1, 128;" ::: "memory");
+        asm volatile("bar.sync 1, 256;" ::: "memory");
+        const int e = warp - 4;
 #pragma unroll 4
-        for (int c = q * (BN / 4); c < (q + 1) * (BN / 4); ++c) {
+        for (int c = e * (BN / 8); c < (e + 1) * (BN / 8); ++c) {
           const float bv = n0 + c < g.N ? __ldg(g.bias + n0 + c) : 0.f;
-          const float y = tanhf(sbuf[c * 32 + lane] + bv);
-          sbuf[c * 32 + lane] = y;
+          sbuf[c * 32 + lane] = tanhf(sbuf[c * 32 + lane] + bv);
         }
-        asm volatile("bar.sync 1, 128;" ::: "memory");
+        asm volatile("bar.sync 1, 256;" ::: "memory");
 #pragma unroll
-        for (int c = 0; c < BN; ++c) {
-          const float y = sbuf[c * 32 + lane];
+        for (int c = 0; c < CW; ++c) {
+          const float y = sbuf[(c_off + c) * 32 + lane];
           acc[c] = q == 0 ? y : (1.f - y * y) * acc[c];
         }
         if (g.tma_store) {
-          store_rows_tma<BN>(acc, my_stg, &mC, n0, (int)(mt * 32), q, lane, nbuf);
+          store_rows_tma<CW>(acc, my_stg, &mC, n0 + c_off, (int)(mt * 32), q, lane);
         } else if (p < g.R) {
-          float* dst = g.C + ((int64_t)q * g.R + p) * g.ldc + n0;
-          if (n0 + BN <= g.N && (g.ldc & 3) == 0) {
+          float* dst = g.C + ((int64_t)q * g.R + p) * g.ldc + n0 + c_off;
 #pragma unroll
-            for (int c = 0; c < BN; c += 4)
-              *reinterpret_cast<float4*>(dst + c) =
-                  make_float4(acc[c], acc[c + 1], acc[c + 2], acc[c + 3]);
-          } else {
-#pragma unroll
-            for (int c = 0; c < BN; ++c)
-              if (n0 + c < g.N) dst[c] = acc[c];
-          }
+          for (int c = 0; c < CW; ++c)
+            if (n0 + c_off + c < g.N) dst[c] = acc[c];
         }
-        asm volatile("bar.sync 1, 128;" ::: "memory");  // sbuf reused by the next tile
+        asm volatile("bar.sync 1, 256;" ::: "memory");  // sbuf reused by the next tile
       }
     }
   }
-  if (warp >= 4 && warp < 8 && lane == 0) bulk_wait_all();
+  if (warp >= 4 && warp < 12 && lane == 0) bulk_wait_all();
   tc_fence_before();
   __syncthreads();
-  if (warp == 9) tmem_dealloc(tmem, Cfg::kTmemCols);
+  if (warp == 13) tmem_dealloc(tmem, Cfg::kTmemCols);
 }
 
 // ---- weight gradient: dW[Kin, Nout] = X[rows, Kin]^T G[rows, Nout] ----------------------
@@ -374,7 +355,7 @@ struct WgradArgs {
   float* partial;       // [n_kc][Kin][Nout]
 };
 
-__global__ void __launch_bounds__(kThreadsGemm, 1)
+__global__ void __launch_bounds__(kThreadsW, 1)
 wgrad_kernel(const __grid_constant__ CUtensorMap mX, const __grid_constant__ CUtensorMap mG,
              const WgradArgs g) {
   constexpr int RS = kWRaw, OS = kWOps, NB = kWNB, P = kWPromote;
@@ -751,7 +732,7 @@ int wgrad(int64_t rows, int Kin, int Nout, const float* X, int64_t ldx, const fl
       cudaFuncSetAttribute(wgrad_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kWSmem));
   const int64_t items = (int64_t)a.n_mt * a.n_nt * a.n_kc;
   const int grid = (int)(items < num_sms() ? items : num_sms());
-  wgrad_kernel<<<grid, kThreadsGemm, kWSmem, st>>>(mX, mG, a);
+  wgrad_kernel<<<grid, kThreadsW, kWSmem, st>>>(mX, mG, a);
   QPINN_CUDA_CHECK(cudaGetLastError());
   const int64_t n = (int64_t)Kin * Nout;
   wgrad_reduce<<<(int)((n + 255) / 256 < 1024 ? (n + 255) / 256 : 1024), 256, 0, st>>>(
