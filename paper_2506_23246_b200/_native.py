@@ -103,6 +103,10 @@ def count_launches(n: int) -> None:
     LAUNCHES["count"] += n
 
 
+def timing_enabled() -> bool:
+    return _TIMING["on"]
+
+
 def timing(on: bool) -> None:
     _TIMING["on"] = on
     if on:

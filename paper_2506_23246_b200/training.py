@@ -217,7 +217,7 @@ class Trainer:
 
     def __init__(self, config: TrainConfig, device="cuda", dtype=torch.float32,
                  rank: int = 0, world_size: int = 1, reduce_fn=None, log_grad: bool = False,
-                 max_points: int = 1 << 21):
+                 max_points: int = 1 << 21, graphs: bool = True):
         self.config = config
         self.device = torch.device(device)
         t_end = config.resolved_t_end()
@@ -257,6 +257,11 @@ class Trainer:
             self.weights_next = torch.empty_like(self.weights)
         self.epoch = 0
         self._host_inputs = None
+        # CUDA graphs of the step's device part (native engine, one rank): one
+        # graph per (bin-weight buffer, input mode); captured after a warm step
+        self.use_graphs = (graphs and dev.type == "cuda" and self.reduce_fn is None
+                           and self.evaluator.engine is not None)
+        self._graphs = {}
 
     # -- end-to-end mode: collocation inputs come from pinned host memory ------
     def set_host_inputs(self, on: bool) -> None:
@@ -294,16 +299,9 @@ class Trainer:
             grad.copy_(flat.grad)
         return grad
 
-    def _check_domain(self):
-        if self.model.circuit is not None:
-            from .ansatz import check_domain
-            check_domain(self.model.circuit, self.model.dtype, self.device)
-
-    def step(self) -> RunRow:
-        """One epoch: evaluate(tape=True) -> (all-reduce) -> finalize -> Adam."""
+    def _device_step(self):
+        """Input copies, sweep (forward + backward), collective, finalize."""
         cfg = self.config
-        epoch = self.epoch
-        lr = lr_at(epoch, cfg.lr0, cfg.lr_decay, cfg.lr_decay_every)
         if self._host_inputs is not None:
             for ch, (hx, hy, ht) in zip(self.evaluator.chunks, self._host_inputs):
                 ch.x.copy_(hx, non_blocking=True)
@@ -315,6 +313,40 @@ class Trainer:
             self._packed = reduce_packed(grad, self.sums, self.reduce_fn, self._packed)
         self.evaluator.finalize(self.sums, self.weights, cfg.kappa, self.bd,
                                 self.weights_next if self.weights is not None else None)
+        return grad
+
+    def _device_part(self):
+        """The device part of a step, replayed from a CUDA graph once warm (the
+        launch sequence is fixed and every buffer is preallocated); eager while
+        per-kernel event timing is on."""
+        if not self.use_graphs or self.epoch < 1 or N.timing_enabled():
+            return self._device_step()
+        key = (self.weights.data_ptr() if self.weights is not None else 0,
+               self._host_inputs is not None)
+        entry = self._graphs.get(key)
+        if entry is None:
+            g = torch.cuda.CUDAGraph()
+            l0 = N.LAUNCHES["count"]
+            with torch.cuda.graph(g):
+                self._device_step()
+            entry = (g, N.LAUNCHES["count"] - l0)
+            N.LAUNCHES["count"] = l0
+            self._graphs[key] = entry
+        entry[0].replay()
+        N.count_launches(entry[1])
+        return self.grad
+
+    def _check_domain(self):
+        if self.model.circuit is not None:
+            from .ansatz import check_domain
+            check_domain(self.model.circuit, self.model.dtype, self.device)
+
+    def step(self) -> RunRow:
+        """One epoch: evaluate(tape=True) -> (all-reduce) -> finalize -> Adam."""
+        cfg = self.config
+        epoch = self.epoch
+        lr = lr_at(epoch, cfg.lr0, cfg.lr_decay, cfg.lr_decay_every)
+        grad = self._device_part()
         adam_step(self.flat, grad, self.adam, lr, loss_dev=self.bd[4:5],
                   flag=self.flag, sync=False)
         host = self._host

@@ -90,3 +90,25 @@ def test_train_curve_matches_reference_vacuum7_fp64():
     rel = np.max(np.abs(tot - g["total"]) / np.abs(g["total"]))
     assert rel <= 1e-8, rel
     assert np.allclose(res.params.flat.cpu().numpy(), g["final_flat"], rtol=1e-7, atol=1e-9)
+
+
+@pytest.mark.parametrize("host_inputs", [False, True])
+def test_cuda_graph_steps_match_eager_bitwise(host_inputs):
+    """The replayed CUDA graph of the step's device part (several chunks,
+    alternating bin-weight buffers, optional pinned-host input copies) gives
+    bit-identical losses and parameters to eager launches."""
+    from paper_2506_23246_b200.network import ModelConfig
+    from paper_2506_23246_b200.training import TrainConfig, Trainer
+    cfg = TrainConfig(case="vacuum", model=ModelConfig(variant="hybrid", ansatz="strongly",
+                      scale="acos", seed=0), epochs=6, grid=(16, 16, 12), chunk_slices=4,
+                      eval_cadence=0, probe_cadence=0)
+    runs = []
+    for graphs in (False, True):
+        tr = Trainer(cfg, device="cuda", dtype=torch.float32, graphs=graphs)
+        tr.set_host_inputs(host_inputs)
+        rows = [tr.step().total for _ in range(6)]
+        runs.append((rows, tr.flat.detach().cpu().numpy().copy()))
+        if graphs:
+            assert tr._graphs, "no graph was captured"
+    assert runs[0][0] == runs[1][0]
+    assert np.array_equal(runs[0][1], runs[1][1])
