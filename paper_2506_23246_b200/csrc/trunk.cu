@@ -201,6 +201,104 @@ __global__ void tanh_bwd_bias(int64_t R, int N, int64_t rows_per, const T* __res
   }
 }
 
+// Adapter backward fused with the last hidden layer's reverse dual tanh:
+//   GUa = reverse dual tanh of the adapter (g_act, act)           [4, R, n]
+//   G_H = GUa Wa^T (n-term dot products)                          [4, R, Hd]
+//   GU  = reverse dual tanh of the last hidden layer (G_H, Hl)    [4, R, Hd]
+// plus block partials of dWa = Hl^T GUa, dba = sum GUa_0, db = sum GU_0 (all
+// four channels of a point meet in one block; reduced later in block order).
+// Replaces two library GEMMs and two elementwise passes; G_H never hits HBM.
+constexpr int kAdMaxN = 16;
+template <typename T, int NA>
+__global__ void __launch_bounds__(128) adapter_bwd(int64_t R, int Hd, int64_t rows_per, const T* __restrict__ g_act,
+                            const T* __restrict__ act, const T* __restrict__ Hl,
+                            const T* __restrict__ Wa, T* __restrict__ GU,
+                            double* __restrict__ part_wa, double* __restrict__ part_b,
+                            double* __restrict__ part_ba) {
+  constexpr int n = NA;
+  __shared__ T gua[32][4][NA];
+  const int tid = threadIdx.x;
+  const int j = tid;  // column of the hidden layer
+  const bool col = j < Hd;
+  const int64_t nA = R * n, nH = R * Hd;
+  const int64_t r0 = (int64_t)blockIdx.x * rows_per;
+  const int64_t r1 = r0 + rows_per < R ? r0 + rows_per : R;
+  T wrow[NA];
+#pragma unroll
+  for (int k = 0; k < NA; ++k) wrow[k] = col ? Wa[(int64_t)j * n + k] : T(0);
+  T acc_w[NA];  // per-thread partials over the block's points (fixed order)
+#pragma unroll
+  for (int k = 0; k < NA; ++k) acc_w[k] = T(0);
+  double acc_b = 0.0, acc_ba = 0.0;
+  for (int64_t p0 = r0; p0 < r1; p0 += 32) {
+    const int np = (int)(r1 - p0 < 32 ? r1 - p0 : 32);
+    for (int idx = tid; idx < 32 * n; idx += blockDim.x) {
+      const int pt = idx / n, k = idx % n;
+      T g[4] = {T(0), T(0), T(0), T(0)};
+      if (pt < np) {
+        const int64_t i = (p0 + pt) * n + k;
+        const T y0 = act[i], s = T(1) - y0 * y0;
+        const T a1 = g_act[nA + i], a2 = g_act[2 * nA + i], a3 = g_act[3 * nA + i];
+        g[0] = g_act[i] * s + (a1 * act[nA + i] + a2 * act[2 * nA + i] + a3 * act[3 * nA + i]) *
+                                  (T(-2) * y0);
+        g[1] = a1 * s;
+        g[2] = a2 * s;
+        g[3] = a3 * s;
+      }
+#pragma unroll
+      for (int c = 0; c < 4; ++c) gua[pt][c][k] = g[c];
+    }
+    __syncthreads();
+    if (tid < n)
+      for (int pt = 0; pt < np; ++pt) acc_ba += (double)gua[pt][0][tid];
+    if (col) {
+      // 8 points at a time with their 32 loads issued up front (latency bound otherwise)
+      for (int pb = 0; pb < np; pb += 8) {
+        T hb[8][4];
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+#pragma unroll
+          for (int c = 0; c < 4; ++c)
+            hb[u][c] = pb + u < np ? Hl[c * nH + (p0 + pb + u) * Hd + j] : T(0);
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int pt = pb + u;
+        if (pt >= np) break;
+        const int64_t i = (p0 + pt) * Hd + j;
+        T h[4], gh[4];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          h[c] = hb[u][c];
+          T v = T(0);
+#pragma unroll
+          for (int k = 0; k < NA; ++k) v += gua[pt][c][k] * wrow[k];
+          gh[c] = v;
+        }
+        const T s = T(1) - h[0] * h[0];
+        const T gu0 = gh[0] * s + (gh[1] * h[1] + gh[2] * h[2] + gh[3] * h[3]) * (T(-2) * h[0]);
+        GU[i] = gu0;
+        GU[nH + i] = gh[1] * s;
+        GU[2 * nH + i] = gh[2] * s;
+        GU[3 * nH + i] = gh[3] * s;
+        acc_b += (double)gu0;
+#pragma unroll
+        for (int k = 0; k < NA; ++k)
+          acc_w[k] += h[0] * gua[pt][0][k] + h[1] * gua[pt][1][k] + h[2] * gua[pt][2][k] +
+                      h[3] * gua[pt][3][k];
+      }
+      }
+    }
+    __syncthreads();
+  }
+  if (col) {
+    part_b[(int64_t)blockIdx.x * Hd + j] = acc_b;
+#pragma unroll
+    for (int k = 0; k < NA; ++k)
+      part_wa[(int64_t)blockIdx.x * Hd * n + (int64_t)j * n + k] = (double)acc_w[k];
+  }
+  if (tid < n) part_ba[(int64_t)blockIdx.x * n + tid] = acc_ba;
+}
+
 // deterministic column sums of X [R, N]: block b sums rows [b*rows_per, ...)
 template <typename T>
 __global__ void colsum_partial(int64_t R, int N, int64_t rows_per, const T* __restrict__ X,
@@ -317,11 +415,12 @@ __global__ void tau_grad_reduce(int nb, const double* __restrict__ partial, cons
 
 // ---- workspace plan ----------------------------------------------------------------------------
 struct TrunkWS {
-  size_t h0, u, h[8], g0, g1, part, tau_part, wsplit, total;
+  size_t h0, u, h[8], g0, g1, part, apart, tau_part, wsplit, total;
 };
 
 constexpr int kColBlocks = 256;
 constexpr int kTanhBlocks = 592;  // 4 per SM for the fused reverse dual tanh
+constexpr int kAdBlocks = 592;    // fused adapter backward (4 per SM)
 constexpr int kTauBlocks = 1184;  // 8 per SM: the tau pass is latency bound
 
 static TrunkWS trunk_ws(const qpinn_trunk_desc* d, size_t es, int64_t R) {
@@ -343,6 +442,8 @@ static TrunkWS trunk_ws(const qpinn_trunk_desc* d, size_t es, int64_t R) {
   w.part = o;
   o += ((size_t)(kColBlocks > kTanhBlocks ? kColBlocks : kTanhBlocks) *
             (H > (size_t)d->n_out ? H : d->n_out) * 8 + 255) / 256 * 256;
+  w.apart = o;  // adapter backward partials: [blocks][Hd * n + Hd + n] doubles
+  o += ((size_t)kAdBlocks * (H * d->n_out + H + d->n_out) * 8 + 255) / 256 * 256;
   w.tau_part = o;
   o += (kTauBlocks * 8 + 255) / 256 * 256;
   // float32 tensor-core scratch, used by one GEMM at a time: the tf32 hi/lo
@@ -447,21 +548,49 @@ static int backward_impl(const qpinn_trunk_desc* d, int64_t R, const T* x, const
   // adapter: GU = tanh_bwd(g_act); dWa = H_last^T GU; dba = colsum(GU0); G_H = GU Wa^T
   const T* Hl = (const T*)(ws + (d->n_hidden ? w.h[d->n_hidden - 1] : w.h0));
   const int Kl = d->n_hidden ? H : 2 * F;
-  if (int rc = tanh_bwd_and_bias<T>(R, n, g_act, act, g1, part, grad + d->off_adapter_b, st))
-    return rc;
-  QPINN_CUDA_CHECK(cudaGetLastError());
-  if (int rc = gemm_rm<T>(h, true, false, Kl, n, 4 * R, Hl, Kl, g1, n, grad + d->off_adapter_w, n, T(0)))
-    return rc;
-  if (int rc = gemm_rm<T>(h, false, true, 4 * R, Kl, n, g1, n, params + d->off_adapter_w, n, g0, Kl, T(0)))
-    return rc;
-  // hidden layers, last to first; g0 holds dL/dH_{i+1}
+  const bool fused = d->n_hidden > 0 && n <= kAdMaxN && H <= 128;
+  if (fused) {  // adapter + last hidden layer's reverse dual tanh in one pass (g1 = its dL/dU)
+    double* pa = (double*)(ws + w.apart);
+    double* pwa = pa;
+    double* pb = pwa + (size_t)kAdBlocks * H * n;
+    double* pba = pb + (size_t)kAdBlocks * H;
+    const int64_t rows_per = (R + kAdBlocks - 1) / kAdBlocks;
+    const int nb = (int)((R + rows_per - 1) / rows_per);
+    const int thr = (H + 31) / 32 * 32;
+    const T* Wa = params + d->off_adapter_w;
+    switch (n) {
+#define QPINN_AD(NN)                                                                        \
+  case NN:                                                                                  \
+    adapter_bwd<T, NN><<<nb, thr, 0, st>>>(R, H, rows_per, g_act, act, Hl, Wa, g1, pwa, pb, pba); \
+    break;
+      QPINN_AD(1) QPINN_AD(2) QPINN_AD(3) QPINN_AD(4) QPINN_AD(5) QPINN_AD(6) QPINN_AD(7)
+      QPINN_AD(8) QPINN_AD(9) QPINN_AD(10) QPINN_AD(11) QPINN_AD(12) QPINN_AD(13)
+      QPINN_AD(14) QPINN_AD(15) QPINN_AD(16)
+#undef QPINN_AD
+    }
+    colsum_reduce<T><<<(H * n + 31) / 32, 256, 0, st>>>(nb, H * n, pwa, grad + d->off_adapter_w);
+    colsum_reduce<T><<<(H + 31) / 32, 256, 0, st>>>(nb, H, pb, grad + d->off_b[d->n_hidden - 1]);
+    colsum_reduce<T><<<(n + 31) / 32, 256, 0, st>>>(nb, n, pba, grad + d->off_adapter_b);
+    QPINN_CUDA_CHECK(cudaGetLastError());
+  } else {
+    if (int rc = tanh_bwd_and_bias<T>(R, n, g_act, act, g1, part, grad + d->off_adapter_b, st))
+      return rc;
+    if (int rc = gemm_rm<T>(h, true, false, Kl, n, 4 * R, Hl, Kl, g1, n, grad + d->off_adapter_w,
+                            n, T(0)))
+      return rc;
+    if (int rc = gemm_rm<T>(h, false, true, 4 * R, Kl, n, g1, n, params + d->off_adapter_w, n, g0,
+                            Kl, T(0)))
+      return rc;
+  }
+  // hidden layers, last to first; g0 holds dL/dH_{i+1} (g1 already dL/dU_i when fused)
   for (int i = d->n_hidden - 1; i >= 0; --i) {
     const int K = i == 0 ? 2 * F : H;
     const T* Hin = (const T*)(ws + (i == 0 ? w.h0 : w.h[i - 1]));
-    if (int rc = tanh_bwd_and_bias<T>(R, H, g0, (const T*)(ws + w.h[i]), g1, part,
-                                      grad + d->off_b[i], st))
-      return rc;
-    QPINN_CUDA_CHECK(cudaGetLastError());
+    if (!(fused && i == d->n_hidden - 1)) {
+      if (int rc = tanh_bwd_and_bias<T>(R, H, g0, (const T*)(ws + w.h[i]), g1, part,
+                                        grad + d->off_b[i], st))
+        return rc;
+    }
     if (sizeof(T) == 4 && K % 4 == 0 && H % 4 == 0) {  // dW = H_in^T GU on the tensor cores
       if (int rc = tc::wgrad(4 * R, K, H, (const float*)Hin, K, (const float*)g1, H,
                              (float*)(grad + d->off_w[i]), ws + w.wsplit, w.total - w.wsplit, st))

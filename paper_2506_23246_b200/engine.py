@@ -156,10 +156,14 @@ class NativeEngine:
         n += 2 + 2                              # K1 prep + main, K4 + reduce
         if tape:
             n += 4 + phase                      # K2 prep, main, reduce, u1 grads (+ phase grads)
-            n += 2                              # adapter: reverse dual tanh + bias partials, reduce
             H = cfg.hidden_width
-            for k in widths[:-1] if self.model.n_hidden else []:
-                n += 2 if H <= 256 else 3       # reverse dual tanh (+ fused bias partials), reduce
+            fused = self.model.n_hidden > 0 and self.n <= 16 and H <= 128
+            # adapter: fused with the last hidden layer's reverse tanh (kernel + 3 reduces),
+            # else reverse dual tanh + bias reduce (its GEMMs are cuBLAS)
+            n += 4 if fused else 2
+            for li, k in enumerate(widths[:-1] if self.model.n_hidden else []):
+                if not (fused and li == self.model.n_hidden - 1):
+                    n += 2 if H <= 256 else 3   # reverse dual tanh (+ fused bias partials), reduce
                 if f32 and k % 4 == 0 and H % 4 == 0:
                     n += 2                      # weight gradient: split-K kernel + reduce
                 if f32 and H % 4 == 0:
