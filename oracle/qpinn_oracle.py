@@ -23,7 +23,9 @@ __all__ = [
     "permutation_for_cnots", "crz_mesh_phase_matrix", "u1_matrix", "u1_dmatrices",
     "scale_derivs", "pqc_forward", "pqc_backward", "OracleModel", "Grid",
     "Evaluator", "time_bin_weights", "lr_at", "adam_update", "init_quantum_params",
-    "train_curve",
+    "train_curve", "pqc_state", "meyer_wallach", "model_predict", "adapter_activations",
+    "probe_entanglement", "epsilon_at", "total_energy", "energy_probe", "bh_index",
+    "l2_against_reference", "fdtd_run",
 ]
 
 KINDS = ("basic", "strongly", "cross_mesh", "cross_mesh_2rot", "cross_mesh_cnot",
@@ -774,3 +776,142 @@ def train_curve(model: OracleModel, grid: Grid, epochs, case="vacuum", energy=Tr
         if adaptive:
             weights = time_bin_weights(bd["bin_phys"], kappa)
     return rows, flat
+
+
+# ---- diagnostic probes -------------------------------------------------
+def pqc_state(a, qp, kind, scale, n_layers):
+    """Final circuit state psi [R, 2^n] for value-only inputs (the state the
+    Meyer-Wallach probe reads); ansatz.py:215-227 via the fused plan."""
+    a = np.asarray(a, dtype=np.float64)
+    R, n = a.shape
+    gates, _ = build_circuit(kind, n, n_layers)
+    theta, _, _ = scale_derivs(scale, a)
+    return _run_steps(_product_state(theta, n), n, fused_plan(gates, n), qp)
+
+
+def meyer_wallach(psi):
+    """Q = 2 (1 - mean_k Tr rho_k^2) per row; qsim.py:384-406."""
+    psi = np.atleast_2d(psi)
+    R, D = psi.shape
+    n = int(round(math.log2(D)))
+    pur = np.zeros(R)
+    for k in range(n):
+        v = psi.reshape(R, 2 ** k, 2, 2 ** (n - k - 1))
+        v = np.moveaxis(v, 2, 1).reshape(R, 2, -1)
+        rho = v @ np.conj(np.swapaxes(v, 1, 2))
+        pur += np.sum(rho.real ** 2 + rho.imag ** 2, axis=(1, 2))
+    return 2.0 * (1.0 - pur / n)
+
+
+def model_predict(model: "OracleModel", flat, x, y, t):
+    """Value-only fields (E_z, H_x, H_y) [3, R]; network.py:310-321."""
+    out, _, _ = model.forward(flat, np.asarray(x, float), np.asarray(y, float),
+                              np.asarray(t, float))
+    return out.T
+
+
+def adapter_activations(model: "OracleModel", flat, x, y, t):
+    """Pre-embedding activations a [R, n]; network.py:323-335."""
+    _, _, cache = model.forward(flat, np.asarray(x, float), np.asarray(y, float),
+                                np.asarray(t, float))
+    return cache["pqc"][0]
+
+
+def probe_entanglement(model: "OracleModel", flat, x, y, t):
+    """Mean Meyer-Wallach Q at the probe inputs; training.py:174-184."""
+    a = adapter_activations(model, flat, x, y, t)
+    qp = model.views(flat)["quantum"]
+    return float(np.mean(meyer_wallach(pqc_state(a, qp, model.ansatz, model.scale,
+                                                  model.n_layers))))
+
+
+def epsilon_at(case, x, eps_r=4.0, slab_x0=0.3):
+    """physics.py:45-49."""
+    x = np.asarray(x, dtype=np.float64)
+    if case != "dielectric":
+        return np.ones_like(x)
+    return np.where(x >= slab_x0, eps_r, 1.0)
+
+
+def total_energy(ez, hx, hy, eps, dx, dy):
+    """0.5 Riemann sum of eps Ez^2 + Hx^2 + Hy^2; fdtd.py:194-197."""
+    return float(np.sum(0.5 * (eps * ez * ez + hx * hx + hy * hy)) * dx * dy)
+
+
+def energy_probe(model: "OracleModel", flat, case, nx, ny, times):
+    """U_theta(t_k) on the collocated nx x ny grid; training.py:187-200."""
+    xs = -1.0 + 2.0 * np.arange(nx) / nx
+    ys = -1.0 + 2.0 * np.arange(ny) / ny
+    yy, xx = np.meshgrid(ys, xs, indexing="ij")
+    xf, yf = xx.ravel(), yy.ravel()
+    eps = epsilon_at(case, xf)
+    out = np.zeros(len(times))
+    for k, tk in enumerate(times):
+        ez, hx, hy = model_predict(model, flat, xf, yf, np.full_like(xf, tk))
+        out[k] = total_energy(ez, hx, hy, eps, 2.0 / nx, 2.0 / ny)
+    return out
+
+
+def bh_index(u, times=None):
+    """(clamped, raw) 1 - min_{t > 0} U(t)/U(0); training.py:117-134."""
+    u = np.asarray(u, dtype=np.float64)
+    if u[0] <= 0.0:
+        raise OracleError("U(0) must be positive")
+    mask = (np.asarray(times) > 0.0) if times is not None else (np.arange(len(u)) > 0)
+    raw = 1.0 - float(np.min((u / u[0])[mask]))
+    return float(np.clip(raw, 0.0, 1.0)), raw
+
+
+def l2_against_reference(model: "OracleModel", flat, times, xs, ys, ez_ref):
+    """Relative L2 of E_z on the snapshot grid; training.py:203-217."""
+    yy, xx = np.meshgrid(ys, xs, indexing="ij")
+    xf, yf = xx.ravel(), yy.ravel()
+    num = den = 0.0
+    for k, tk in enumerate(times):
+        ez = model_predict(model, flat, xf, yf, np.full_like(xf, tk))[0]
+        ref = ez_ref[k].ravel()
+        num += float(np.sum((ez - ref) ** 2))
+        den += float(np.sum(ref * ref))
+    return float(np.sqrt(num / den))
+
+
+# ---- FDTD reference solver (SURVEY 8f row 4) ---------------------------------------------
+def fdtd_run(nx, ny, case="vacuum", t_end=1.5, cfl=0.5, ic="pulse", n_snapshots=100,
+             eps_r=4.0, slab_x0=0.3, center=(0.0, 0.0), stretch=(1.0, 1.0)):
+    """Yee TEz leapfrog on the periodic cell with collocated snapshots;
+    fdtd.py:115-181 (H at t = -dt/2 from a discrete half step, Ez update with
+    a pointwise epsilon, snapshots at the steps nearest linspace(0, t_end))."""
+    dx, dy = 2.0 / nx, 2.0 / ny
+    dt0 = cfl * min(dx, dy) / np.sqrt(2.0)
+    steps = max(1, int(np.ceil(t_end / dt0 - 1e-12)))
+    dt = t_end / steps
+    xs = -1.0 + dx * np.arange(nx)
+    ys = -1.0 + dy * np.arange(ny)
+    yy, xx = np.meshgrid(ys, xs, indexing="ij")
+    eps = epsilon_at(case, xx, eps_r, slab_x0)
+    if ic == "plane_wave":
+        ez = np.cos(np.pi * xx)
+        hx = np.zeros_like(ez)
+        hy = np.cos(np.pi * (xx + dx / 2.0 - dt / 2.0))
+    else:
+        ez = np.exp(-25.0 * (((xx - center[0]) / stretch[0]) ** 2
+                             + ((yy - center[1]) / stretch[1]) ** 2))
+        hx = (dt / 2.0) * (np.roll(ez, -1, axis=0) - ez) / dy
+        hy = -(dt / 2.0) * (np.roll(ez, -1, axis=1) - ez) / dx
+    wanted = np.linspace(0.0, t_end, n_snapshots)
+    snap = set(int(s) for s in np.unique(np.clip(np.round(wanted / dt).astype(int), 0, steps)))
+    times, rez, rhx, rhy = [], [], [], []
+    for step in range(steps + 1):
+        hx_new = hx - (dt / dy) * (np.roll(ez, -1, axis=0) - ez)
+        hy_new = hy + (dt / dx) * (np.roll(ez, -1, axis=1) - ez)
+        if step in snap:
+            hxm, hym = 0.5 * (hx + hx_new), 0.5 * (hy + hy_new)
+            times.append(step * dt)
+            rez.append(ez.copy())
+            rhx.append(0.5 * (hxm + np.roll(hxm, 1, axis=0)))
+            rhy.append(0.5 * (hym + np.roll(hym, 1, axis=1)))
+        hx, hy = hx_new, hy_new
+        ez = ez + (dt / eps) * ((hy - np.roll(hy, 1, axis=1)) / dx
+                                - (hx - np.roll(hx, 1, axis=0)) / dy)
+    return dict(times=np.array(times), ez=np.stack(rez), hx=np.stack(rhx), hy=np.stack(rhy),
+                xs=xs, ys=ys, dt=dt, steps=steps, eps=eps)
