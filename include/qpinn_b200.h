@@ -255,6 +255,21 @@ int qpinn_gemm_f32_atb(int64_t rows, int m, int n, const void* x, int64_t ldx, c
                        int64_t ldg, void* c, void* workspace, size_t workspace_bytes,
                        void* stream);
 
+/* ---- FDTD reference solver (fdtd.py:115-211) ----------------------------- */
+/* Yee TEz leapfrog on the periodic [-1,1)^2 cell, float64, `steps` steps of
+ * size dt on an nx x ny grid (arrays [ny][nx], x fastest).  ic: 0 Gaussian
+ * pulse with pulse = {cx, cy, sx, sy} (host, NULL = centred, unstretched),
+ * 1 the analytic plane wave.  Collocated snapshots (Ez, H averaged to the Ez
+ * nodes) are written at the host-given increasing step indices into rec_*
+ * [n_snaps][ny][nx] (device), and, when `energy` is not NULL, U at each
+ * snapshot (fdtd.py:194-197) into energy[n_snaps] (device).  Every update is
+ * rounded in the reference's order (no FMA contraction). */
+size_t qpinn_fdtd_workspace_bytes(int nx, int ny);
+int qpinn_fdtd_run(int nx, int ny, int steps, double dt, int ic, const double* pulse,
+                   int dielectric, double eps_r, double slab_x0, const int32_t* snap_steps,
+                   int n_snaps, double* rec_ez, double* rec_hx, double* rec_hy,
+                   double* energy, void* workspace, size_t workspace_bytes, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -87,6 +87,9 @@ SIGNATURES = [
     ("qpinn_gemm_f32", _I, [_I64, _I, _I, _VP, _I64, _VP, _I64, _VP, _I64, _VP, _SZ, _VP]),
     ("qpinn_gemm_f32_atb_workspace_bytes", _SZ, [_I64, _I, _I]),
     ("qpinn_gemm_f32_atb", _I, [_I64, _I, _I, _VP, _I64, _VP, _I64, _VP, _VP, _SZ, _VP]),
+    ("qpinn_fdtd_workspace_bytes", _SZ, [_I, _I]),
+    ("qpinn_fdtd_run", _I, [_I, _I, _I, _D, _I, C.POINTER(_D), _I, _D, _D, C.POINTER(C.c_int32),
+                            _I, _VP, _VP, _VP, _VP, _VP, _SZ, _VP]),
 ]
 
 _lib = None
