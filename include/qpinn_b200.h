@@ -110,6 +110,15 @@ int qpinn_pqc_forward(const qpinn_circuit* c, int dtype, int scale, int64_t rows
                       void* z, void* dz, void* states, void* workspace,
                       size_t workspace_bytes, void* stream);
 
+/* Value-only forward for the Meyer-Wallach probe (qsim.py:384-406): z [R,n]
+ * and coh [R,n] complex (interleaved re, im) with coh_k = sum over basis
+ * states b with bit k = 0 of psi_b conj(psi_{b with bit k set}), the reduced
+ * density matrix's off-diagonal (its diagonal is (1 +- z_k)/2).  Standard
+ * ansatze with the layer-loop kernels only (n <= 8 fp32, n <= 7 fp64). */
+int qpinn_pqc_forward_probe(const qpinn_circuit* c, int dtype, int scale, int64_t rows,
+                            const void* act_val, const void* qparams, void* z, void* coh,
+                            void* workspace, size_t workspace_bytes, void* stream);
+
 /* Gradients of L(z, dz) given g_z = dL/dz [R,n] and g_dz = dL/d(dz) [3,R,n]:
  * g_act_val [R,n], g_act_tan [3,R,n] and g_qparams [P] (summed over all rows
  * in a fixed, run-to-run deterministic order).  `states` is the buffer a
@@ -153,6 +162,14 @@ size_t qpinn_trunk_workspace_bytes(const qpinn_trunk_desc* d, int dtype, int64_t
 int qpinn_trunk_forward(const qpinn_trunk_desc* d, int dtype, int64_t rows, const void* x,
                         const void* y, const void* t, const void* params, void* act,
                         void* workspace, size_t workspace_bytes, void* stream);
+
+/* Value-only trunk for inference and the probes (network.py:310-335): act
+ * [R, n] = adapter activations without tangents.  Same descriptor and
+ * workspace as the dual forward. */
+int qpinn_trunk_forward_value(const qpinn_trunk_desc* d, int dtype, int64_t rows,
+                              const void* x, const void* y, const void* t,
+                              const void* params, void* act, void* workspace,
+                              size_t workspace_bytes, void* stream);
 /* Given g_act = dL/d(act) [4, R, n_out] (from qpinn_pqc_backward), writes the
  * gradients of every trunk weight, bias and tau_raw into `grad` (flat layout;
  * overwrites those entries). */
@@ -254,6 +271,20 @@ size_t qpinn_gemm_f32_atb_workspace_bytes(int64_t rows, int m, int n);
 int qpinn_gemm_f32_atb(int64_t rows, int m, int n, const void* x, int64_t ldx, const void* g,
                        int64_t ldg, void* c, void* workspace, size_t workspace_bytes,
                        void* stream);
+
+/* ---- value-only inference head and probe reductions ------ */
+/* fields [R, 3] = z [R, n] W_out [n, 3] + b_out (network.py:302). */
+int qpinn_head_forward(int dtype, int64_t rows, int n, const void* z, const void* w_out,
+                       const void* b_out, void* fields, void* stream);
+/* u[t] = dxdy * sum over slice t's `points` rows of 0.5 (eps Ez^2 + Hx^2 + Hy^2)
+ * (training.py:187-200, fdtd.py:194-197); fields [n_slices * points, 3], eps
+ * [points] and u [n_slices] float64 on the device; fixed-order sums. */
+int qpinn_probe_energy(int dtype, int n_slices, int64_t points, const void* fields,
+                       const double* eps, double dxdy, double* u, void* stream);
+/* sums[2t] = sum (Ez - ref)^2, sums[2t+1] = sum ref^2 over slice t
+ * (training.py:203-217); ref [n_slices * points] float64. */
+int qpinn_probe_l2(int dtype, int n_slices, int64_t points, const void* fields,
+                   const double* ref, double* sums, void* stream);
 
 /* ---- FDTD reference solver (fdtd.py:115-211) ----------------------------- */
 /* Yee TEz leapfrog on the periodic [-1,1)^2 cell, float64, `steps` steps of

@@ -70,6 +70,7 @@ SIGNATURES = [
     ("qpinn_pqc_forward", _I, [_VP, _I, _I, _I64, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _SZ, _VP]),
     ("qpinn_pqc_backward", _I, [_VP, _I, _I, _I64, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP,
                                 _VP, _VP, _SZ, _VP]),
+    ("qpinn_pqc_forward_probe", _I, [_VP, _I, _I, _I64, _VP, _VP, _VP, _VP, _VP, _SZ, _VP]),
     ("qpinn_pqc_domain_check", _I, [_VP, _VP, C.POINTER(_D), C.POINTER(_I)]),
     ("qpinn_loss_workspace_bytes", _SZ, [C.POINTER(LossSpec), _I, _I64]),
     ("qpinn_loss_forward_backward", _I, [C.POINTER(LossSpec), _I, _I64, _VP, _VP, _VP, _VP,
@@ -80,6 +81,8 @@ SIGNATURES = [
     ("qpinn_trunk_workspace_bytes", _SZ, [C.POINTER(TrunkDesc), _I, _I64]),
     ("qpinn_trunk_forward", _I, [C.POINTER(TrunkDesc), _I, _I64, _VP, _VP, _VP, _VP, _VP, _VP,
                                  _SZ, _VP]),
+    ("qpinn_trunk_forward_value", _I, [C.POINTER(TrunkDesc), _I, _I64, _VP, _VP, _VP, _VP, _VP,
+                                       _VP, _SZ, _VP]),
     ("qpinn_trunk_backward", _I, [C.POINTER(TrunkDesc), _I, _I64, _VP, _VP, _VP, _VP, _VP, _VP,
                                   _VP, _VP, _SZ, _VP]),
     ("qpinn_adam_step", _I, [_I, _I64, _VP, _VP, _VP, _VP, _I64, _D, _D, _D, _D, _VP, _VP, _VP]),
@@ -87,6 +90,9 @@ SIGNATURES = [
     ("qpinn_gemm_f32", _I, [_I64, _I, _I, _VP, _I64, _VP, _I64, _VP, _I64, _VP, _SZ, _VP]),
     ("qpinn_gemm_f32_atb_workspace_bytes", _SZ, [_I64, _I, _I]),
     ("qpinn_gemm_f32_atb", _I, [_I64, _I, _I, _VP, _I64, _VP, _I64, _VP, _VP, _SZ, _VP]),
+    ("qpinn_head_forward", _I, [_I, _I64, _I, _VP, _VP, _VP, _VP, _VP]),
+    ("qpinn_probe_energy", _I, [_I, _I, _I64, _VP, _VP, _D, _VP, _VP]),
+    ("qpinn_probe_l2", _I, [_I, _I, _I64, _VP, _VP, _VP, _VP]),
     ("qpinn_fdtd_workspace_bytes", _SZ, [_I, _I]),
     ("qpinn_fdtd_run", _I, [_I, _I, _I, _D, _I, C.POINTER(_D), _I, _D, _D, C.POINTER(C.c_int32),
                             _I, _VP, _VP, _VP, _VP, _VP, _SZ, _VP]),

@@ -238,10 +238,11 @@ def _check_rows(t: torch.Tensor, name: str):
         raise ConfigError(f"{name} must be a CUDA tensor (the kernels have no CPU path)")
 
 
-def check_domain(circuit: CircuitSpec, dtype, device, stream=None) -> float:
+def check_domain(circuit: CircuitSpec, dtype, device, stream=None, ws=None) -> float:
     """Synchronise and apply the reference domain rule (ansatz.py:51-58) to the
-    last forward launched on ``circuit``'s workspace; returns max|a|."""
-    ws = circuit.workspace(dtype, device, 0)
+    forwards launched on ``circuit``'s workspace (or ``ws``) since the last
+    check; returns max|a|."""
+    ws = circuit.workspace(dtype, device, 0) if ws is None else ws
     m = C.c_double()
     clamped = C.c_int()
     rc = N.lib().qpinn_pqc_domain_check(C.c_void_p(ws.data_ptr()),

@@ -791,6 +791,38 @@ int qpinn_pqc_backward(const qpinn_circuit* cc, int dtype, int scale, int64_t ro
   return fail(QPINN_ERR_CAPACITY, "unsupported n_qubits");
 }
 
+int qpinn_pqc_forward_probe(const qpinn_circuit* cc, int dtype, int scale, int64_t rows,
+                            const void* act_val, const void* qparams, void* z, void* coh,
+                            void* workspace, size_t workspace_bytes, void* stream) {
+  qpinn_circuit* c = const_cast<qpinn_circuit*>(cc);
+  int rc = check_common(c, dtype, scale, rows, workspace_bytes,
+                        qpinn_pqc_workspace_bytes(c, dtype, rows));
+  if (rc) return rc;
+  if (!z || !coh) return fail(QPINN_ERR_CONFIG, "probe needs z and coh");
+  if (c->n > qpinn_pqc_max_qubits(dtype) || layer_entangler(c) < 0)
+    return fail(QPINN_ERR_CAPACITY, "the entanglement probe needs the layer-loop kernels "
+                                    "(standard ansatz, n <= 8 fp32 / 7 fp64)");
+  rc = ensure_device_plan(c);
+  if (rc) return rc;
+  if (rows == 0) return QPINN_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  auto* maxabs = (unsigned long long*)workspace;
+  unsigned char* tables = (unsigned char*)workspace + 256 + partial_bytes(c) +
+                          align_up(sizeof(double) * n_acc_of(c), 256);
+  if (dtype == QPINN_F32) {
+    KArgs<float> a{scale, rows, (const float*)act_val, nullptr, (const float*)qparams, (float*)z,
+                   nullptr, nullptr, maxabs, nullptr, nullptr, nullptr, nullptr, nullptr,
+                   nullptr, nullptr, st, tables, (float*)coh};
+    rc = layer_dispatch<float>(true, c, &a);
+  } else {
+    KArgs<double> a{scale, rows, (const double*)act_val, nullptr, (const double*)qparams,
+                    (double*)z, nullptr, nullptr, maxabs, nullptr, nullptr, nullptr, nullptr,
+                    nullptr, nullptr, nullptr, st, tables, (double*)coh};
+    rc = layer_dispatch<double>(true, c, &a);
+  }
+  return rc == KERNEL_NONE ? fail(QPINN_ERR_CAPACITY, "probe: no layer kernel") : rc;
+}
+
 int qpinn_pqc_domain_check(const void* workspace, void* stream, double* max_abs, int* clamped) {
   unsigned long long bits = 0;
   QPINN_CUDA_CHECK(cudaStreamSynchronize((cudaStream_t)stream));

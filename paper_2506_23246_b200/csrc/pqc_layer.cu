@@ -132,7 +132,7 @@ pqc_forward_layer(PlanDev plan, const unsigned char* __restrict__ tables, int n_
                   int64_t R, const T* __restrict__ act, const T* __restrict__ act_tan,
                   const T* __restrict__ qp, T* __restrict__ z,
                   T* __restrict__ dz, cplx<T>* __restrict__ states,
-                  unsigned long long* __restrict__ maxabs) {
+                  unsigned long long* __restrict__ maxabs, cplx<T>* __restrict__ coh) {
   using Gm = Geo<T, N, NSL>;
   constexpr int AB = Gm::AB, A = Gm::A, LB = Gm::LB, G = Gm::G, LPP = Gm::LPP, SPW = Gm::SPW,
                 D = Gm::D;
@@ -230,6 +230,46 @@ pqc_forward_layer(PlanDev plan, const unsigned char* __restrict__ tables, int n_
         if ((q % G) != gl) continue;
         if (sidx == 0) z[s * N + q] = out[q];
         else dz[((int64_t)(sidx - 1) * R + s) * N + q] = out[q];
+      }
+    }
+    if constexpr (NSL == 1) {
+      // Meyer-Wallach probe (qsim.py:384-406): rho_k's coherence
+      // c_k = sum_{b: bit_k = 0} psi_b conj(psi_{b ^ bit_k}); its diagonal is (1 +- z_k)/2
+      if (coh != nullptr) {
+        T cre[N], cim[N];
+#pragma unroll
+        for (int q = 0; q < N; ++q) cre[q] = cim[q] = T(0);
+        static_for<0, AB>([&](auto rb_) {
+          constexpr int RB = decltype(rb_)::value, S = 1 << RB, q = N - 1 - RB;
+#pragma unroll
+          for (int r = 0; r < A; ++r) {
+            if (r & S) continue;
+            const cplx<T> a = st[0][r], b = st[0][r | S];
+            cre[q] += a.re * b.re + a.im * b.im;
+            cim[q] += a.im * b.re - a.re * b.im;
+          }
+        });
+#pragma unroll
+        for (int q = 0; q < LB; ++q) {
+          const int lm = 1 << (LB - 1 - q);
+          const T w = (gl & lm) ? T(0) : T(1);
+#pragma unroll
+          for (int r = 0; r < A; ++r) {
+            const cplx<T> a = st[0][r], b = shfl_xor_c(st[0][r], lm);
+            cre[q] += w * (a.re * b.re + a.im * b.im);
+            cim[q] += w * (a.im * b.re - a.re * b.im);
+          }
+        }
+#pragma unroll
+        for (int m = 1; m < G; m <<= 1)
+#pragma unroll
+          for (int q = 0; q < N; ++q) {
+            cre[q] += __shfl_xor_sync(0xffffffffu, cre[q], m);
+            cim[q] += __shfl_xor_sync(0xffffffffu, cim[q], m);
+          }
+        if (valid && gl == 0)
+#pragma unroll
+          for (int q = 0; q < N; ++q) coh[s * N + q] = cplx<T>{cre[q], cim[q]};
       }
     }
   }
@@ -496,7 +536,8 @@ static int layer_fwd(const qpinn_circuit* c, const KArgs<T>* a) {
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kThreads, smem);
     const int grid = pqc_grid(a->R, spw, occ > 0 ? occ : 1);
     kern<<<grid, kThreads, smem, a->stream>>>(p, a->tables, c->L, a->scale, a->R, a->act, a->tan,
-                                              a->qp, a->z, a->dz, (cplx<T>*)a->states, a->maxabs);
+                                              a->qp, a->z, a->dz, (cplx<T>*)a->states, a->maxabs,
+                                              (cplx<T>*)a->coh);
     QPINN_CUDA_CHECK(cudaGetLastError());
     return QPINN_OK;
   };

@@ -29,6 +29,7 @@ struct KArgs {
   double* tot;
   cudaStream_t stream;
   unsigned char* tables;  // workspace region for pqc_prepare_tables
+  T* coh = nullptr;       // value-only probe: per-qubit coherences [R, n] complex
 };
 
 // QPINN_OK / error code, or KERNEL_NONE when the circuit's plan does not have

@@ -32,7 +32,7 @@ constexpr int kBM = 128, kBK = 32;
 constexpr int kABytes = kBM * kBK * 4;  // 16 KB fp32 tile
 constexpr int kThreadsGemm = 448;  // 4 split + 8 epilogue + producer + MMA warps
 constexpr int kThreadsW = 320;      // weight gradient: 4 split + 4 epilogue + producer + MMA
-enum { EPI_STORE = 0, EPI_TANH = 1 };
+enum { EPI_STORE = 0, EPI_TANH = 1, EPI_TANH1 = 2 };  // TANH1: value channel only
 
 template <int BN>
 struct GemmCfg {
@@ -288,7 +288,14 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUt
         __syncwarp();
         if (lane == 0) mbar_arrive(tempty + b);
       }
-      if constexpr (EPI == EPI_STORE) {
+      if constexpr (EPI == EPI_STORE || EPI == EPI_TANH1) {
+        if constexpr (EPI == EPI_TANH1) {  // y = tanh(u + b), no tangents
+#pragma unroll
+          for (int c = 0; c < CW; ++c) {
+            const int col = n0 + c_off + c;
+            acc[c] = tanhf(acc[c] + (col < g.N ? __ldg(g.bias + col) : 0.f));
+          }
+        }
         const int64_t row = mt * kBM + q * 32 + lane;
         if (g.tma_store) {
           store_rows_tma<CW>(acc, my_stg, &mC, n0 + c_off, (int)(mt * kBM + q * 32), 0, lane);
@@ -739,6 +746,20 @@ int wgrad(int64_t rows, int Kin, int Nout, const float* X, int64_t ldx, const fl
       a.n_kc, n, a.partial, dW);
   QPINN_CUDA_CHECK(cudaGetLastError());
   return QPINN_OK;
+}
+
+// H [R, N] = tanh(X [R, K] W [K, N] + b): the value-only dense layer (inference)
+int dense_tanh1(int64_t R, int N, int K, const float* X, const float* W, const float* bias,
+                float* H, void* ws, size_t ws_bytes, cudaStream_t st) {
+  if (ws_bytes < gemm3_workspace_bytes(N, K)) return fail(QPINN_ERR_CONFIG, "dense: workspace");
+  if (R == 0) return QPINN_OK;
+  const int ldk = ldk_of(K);
+  float* hi = (float*)(((uintptr_t)ws + 255) & ~(uintptr_t)255);
+  float* lo = hi + (size_t)N * ldk;
+  split_transpose<<<64, 256, 0, st>>>(W, K, N, ldk, hi, lo);
+  QPINN_CUDA_CHECK(cudaGetLastError());
+  GemmArgs g{R, R, N, K, H, N, bias, 0};
+  return dispatch<EPI_TANH1>(g, X, K, hi, lo, ldk, st);
 }
 
 // H [4R, N] = dual tanh of X [4R, K] W [K, N] + b (channel blocks of R rows)

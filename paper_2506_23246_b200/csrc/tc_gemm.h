@@ -15,6 +15,9 @@ size_t wgrad_workspace_bytes(int64_t rows, int Kin, int Nout);
 // dW [Kin,Nout] = X [rows,Kin]^T G [rows,Nout] (split-K over rows, deterministic)
 int wgrad(int64_t rows, int Kin, int Nout, const float* X, int64_t ldx, const float* G,
           int64_t ldg, float* dW, void* ws, size_t ws_bytes, cudaStream_t st);
+// H [R,N] = tanh(X [R,K] W [K,N] + b) (value only)
+int dense_tanh1(int64_t R, int N, int K, const float* X, const float* W, const float* bias,
+                float* H, void* ws, size_t ws_bytes, cudaStream_t st);
 // H [4R,N] = dual tanh of X [4R,K] W [K,N] + b (value / tangent channel blocks)
 int dense_tanh(int64_t R, int N, int K, const float* X, const float* W, const float* bias,
                float* H, void* ws, size_t ws_bytes, cudaStream_t st);

@@ -96,7 +96,7 @@ template <typename T>
 __global__ void features_fwd(int64_t R, int F, const T* __restrict__ x, const T* __restrict__ y,
                              const T* __restrict__ t, const T* __restrict__ omega,
                              const T* __restrict__ params, int64_t off_tau, T t_dom,
-                             T* __restrict__ H0) {
+                             T* __restrict__ H0, int nch) {
   const T tau = tau_of(params, off_tau, t_dom);
   const int64_t n = R * F;
   const int64_t W = 2 * (int64_t)F;
@@ -119,6 +119,7 @@ __global__ void features_fwd(int64_t R, int F, const T* __restrict__ x, const T*
     sincos_t(proj, &sp, &cp);
     H0[p * W + f] = cp;
     H0[p * W + F + f] = sp;
+    if (nch == 1) continue;  // value only (inference)
     const T dps[3] = {dpx, dpy, dpt};
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
@@ -132,7 +133,7 @@ __global__ void features_fwd(int64_t R, int F, const T* __restrict__ x, const T*
 // dual tanh epilogue: H[0] = tanh(U[0] + b), H[k] = (1 - H[0]^2) U[k]
 template <typename T>
 __global__ void tanh_fwd(int64_t R, int N, const T* __restrict__ U, const T* __restrict__ b,
-                         T* __restrict__ H) {
+                         T* __restrict__ H, int nch) {
   const int64_t n = R * N;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
@@ -140,6 +141,7 @@ __global__ void tanh_fwd(int64_t R, int N, const T* __restrict__ U, const T* __r
     const T yv = tanh(U[i] + b[j]);
     const T s = T(1) - yv * yv;
     H[i] = yv;
+    if (nch == 1) continue;
     H[n + i] = s * U[n + i];
     H[2 * n + i] = s * U[2 * n + i];
     H[3 * n + i] = s * U[3 * n + i];
@@ -500,12 +502,13 @@ static int bias_grad(int64_t R, int N, const T* GU0, double* part, T* out, cudaS
 
 template <typename T>
 static int forward_impl(const qpinn_trunk_desc* d, int64_t R, const T* x, const T* y, const T* t,
-                        const T* params, T* act, unsigned char* ws, cudaStream_t st) {
+                        const T* params, T* act, unsigned char* ws, cudaStream_t st,
+                        int nch = 4) {
   const TrunkWS w = trunk_ws(d, sizeof(T), R);
   const int F = d->rff, H = d->hidden, n = d->n_out;
   T* H0 = (T*)(ws + w.h0);
   features_fwd<T><<<grid_1d(R * F), 256, 0, st>>>(R, F, x, y, t, (const T*)d->omega, params,
-                                                  d->off_tau_raw, (T)d->t_domain, H0);
+                                                  d->off_tau_raw, (T)d->t_domain, H0, nch);
   QPINN_CUDA_CHECK(cudaGetLastError());
   const T* in = H0;
   int K = 2 * F;
@@ -516,12 +519,15 @@ static int forward_impl(const qpinn_trunk_desc* d, int64_t R, const T* x, const 
   auto dense = [&](int Kin, int N, const T* X, int64_t off_w, int64_t off_b, T* out) -> int {
     if constexpr (sizeof(T) == 4) {
       if (Kin % 4 == 0)
-        return tc::dense_tanh(R, N, Kin, X, params + off_w, params + off_b, out, ws + w.wsplit,
-                              w.total - w.wsplit, st);
+        return nch == 4 ? tc::dense_tanh(R, N, Kin, X, params + off_w, params + off_b, out,
+                                         ws + w.wsplit, w.total - w.wsplit, st)
+                        : tc::dense_tanh1(R, N, Kin, X, params + off_w, params + off_b, out,
+                                          ws + w.wsplit, w.total - w.wsplit, st);
     }
-    if (int rc = gemm_rm<T>(h, false, false, 4 * R, N, Kin, X, Kin, params + off_w, N, U, N, T(0)))
+    if (int rc = gemm_rm<T>(h, false, false, nch * R, N, Kin, X, Kin, params + off_w, N, U, N,
+                            T(0)))
       return rc;
-    tanh_fwd<T><<<grid_1d(R * N), 256, 0, st>>>(R, N, U, params + off_b, out);
+    tanh_fwd<T><<<grid_1d(R * N), 256, 0, st>>>(R, N, U, params + off_b, out, nch);
     QPINN_CUDA_CHECK(cudaGetLastError());
     return QPINN_OK;
   };
@@ -650,6 +656,22 @@ int qpinn_trunk_forward(const qpinn_trunk_desc* d, int dtype, int64_t rows, cons
                                (const float*)params, (float*)act, (unsigned char*)workspace, st);
   return forward_impl<double>(d, rows, (const double*)x, (const double*)y, (const double*)t,
                               (const double*)params, (double*)act, (unsigned char*)workspace, st);
+}
+
+int qpinn_trunk_forward_value(const qpinn_trunk_desc* d, int dtype, int64_t rows, const void* x,
+                              const void* y, const void* t, const void* params, void* act,
+                              void* workspace, size_t workspace_bytes, void* stream) {
+  if (int rc = check_desc(d, dtype)) return rc;
+  if (workspace_bytes < qpinn_trunk_workspace_bytes(d, dtype, rows))
+    return fail(QPINN_ERR_CONFIG, "trunk workspace too small");
+  if (rows <= 0) return QPINN_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (dtype == QPINN_F32)
+    return forward_impl<float>(d, rows, (const float*)x, (const float*)y, (const float*)t,
+                               (const float*)params, (float*)act, (unsigned char*)workspace, st, 1);
+  return forward_impl<double>(d, rows, (const double*)x, (const double*)y, (const double*)t,
+                              (const double*)params, (double*)act, (unsigned char*)workspace, st,
+                              1);
 }
 
 int qpinn_trunk_backward(const qpinn_trunk_desc* d, int dtype, int64_t rows, const void* x,

@@ -24,6 +24,120 @@ from . import _native as N
 from .ansatz import _SCALE_CODE, ScaleKind, state_buffer
 
 
+def trunk_desc(model):
+    """``qpinn_trunk_desc`` for a hybrid model (offsets into its flat layout);
+    returns (desc, omega tensor kept alive, offsets)."""
+    cfg = model.config
+    off = {name: o for name, o, _ in model.layout}
+    d = N.TrunkDesc()
+    d.n_hidden = model.n_hidden
+    d.rff = cfg.rff_features
+    d.hidden = cfg.hidden_width
+    d.n_out = cfg.n_qubits
+    for i in range(model.n_hidden):
+        d.off_w[i] = off[f"h{i}.W"]
+        d.off_b[i] = off[f"h{i}.b"]
+    d.off_adapter_w = off["adapter.W"]
+    d.off_adapter_b = off["adapter.b"]
+    d.off_tau_raw = off["tau_raw"]
+    d.t_domain = cfg.t_domain
+    omega = model.omega.contiguous()
+    d.omega = omega.data_ptr()
+    return d, omega, off
+
+
+class InferenceEngine:
+    """Value-only evaluation of a hybrid model with our kernels only
+    (network.py:310-335): value trunk (tensor-core dense layers with the tanh
+    epilogue) -> K1 without tangents -> linear head, in fixed chunks.  Also
+    the Meyer-Wallach probe (K1 with the per-qubit coherence readout)."""
+
+    def __init__(self, model, chunk: int = 1 << 16):
+        if model.circuit is None:
+            raise ValueError("the inference engine needs a hybrid model")
+        self.model = model
+        self.chunk = chunk
+        cfg = model.config
+        self.n = cfg.n_qubits
+        self.device, self.dtype = model.device, model.dtype
+        self.dcode = N.dtype_code(self.dtype)
+        self.scale = _SCALE_CODE[ScaleKind(cfg.scale)]
+        self.desc, self._omega, off = trunk_desc(model)
+        self.off_out_w, self.off_out_b, self.off_q = off["out.W"], off["out.b"], off["quantum"]
+        lib = N.lib()
+        dev, dt, n = self.device, self.dtype, self.n
+        self.trunk_ws = torch.empty(lib.qpinn_trunk_workspace_bytes(C.byref(self.desc),
+                                                                    self.dcode, chunk),
+                                    dtype=torch.uint8, device=dev)
+        # private scratch: the running |a| maximum must not mix with training's
+        self.pqc_ws = torch.zeros(lib.qpinn_pqc_workspace_bytes(model.circuit.handle, self.dcode,
+                                                                chunk),
+                                  dtype=torch.uint8, device=dev)
+        self.act = torch.empty((chunk, n), dtype=dt, device=dev)
+        self.z = torch.empty((chunk, n), dtype=dt, device=dev)
+        self.coh = torch.empty((chunk, n, 2), dtype=dt, device=dev)
+
+    def _chunks(self, x):
+        for lo in range(0, x.shape[0], self.chunk):
+            yield lo, min(x.shape[0], lo + self.chunk)
+
+    def _trunk_pqc(self, flat, x, y, t, lo, hi, probe):
+        lib, st, es, dc = N.lib(), N.stream_ptr(), flat.element_size(), self.dcode
+        R = hi - lo
+        fp = flat.data_ptr()
+        N.check(lib.qpinn_trunk_forward_value(
+            C.byref(self.desc), dc, R, x[lo:].data_ptr(), y[lo:].data_ptr(), t[lo:].data_ptr(),
+            fp, self.act.data_ptr(), self.trunk_ws.data_ptr(), self.trunk_ws.numel(), st),
+            "qpinn_trunk_forward_value")
+        qp = fp + self.off_q * es
+        if probe:
+            N.check(lib.qpinn_pqc_forward_probe(
+                self.model.circuit.handle, dc, self.scale, R, self.act.data_ptr(), qp,
+                self.z.data_ptr(), self.coh.data_ptr(), self.pqc_ws.data_ptr(),
+                self.pqc_ws.numel(), st), "qpinn_pqc_forward_probe")
+        else:
+            N.check(lib.qpinn_pqc_forward(
+                self.model.circuit.handle, dc, self.scale, R, self.act.data_ptr(), 0, qp,
+                self.z.data_ptr(), 0, 0, self.pqc_ws.data_ptr(), self.pqc_ws.numel(), st),
+                "qpinn_pqc_forward")
+        widths = [2 * self.model.config.rff_features] + \
+            [self.model.config.hidden_width] * self.model.n_hidden
+        N.count_launches(1 + sum(2 if (self.dtype == torch.float32 and k % 4 == 0) else 1
+                                 for k in widths) + 2)
+
+    def check_domain(self):
+        """The reference's |a| <= 1 rule on every forward since the last check."""
+        from .ansatz import check_domain
+        return check_domain(self.model.circuit, self.dtype, self.device, ws=self.pqc_ws)
+
+    def fields(self, flat, x, y, t, out=None):
+        """(E_z, H_x, H_y) as a [R, 3] device tensor."""
+        lib, st = N.lib(), N.stream_ptr()
+        es = flat.element_size()
+        R = x.shape[0]
+        out = torch.empty((R, 3), dtype=self.dtype, device=self.device) if out is None else out
+        for lo, hi in self._chunks(x):
+            self._trunk_pqc(flat, x, y, t, lo, hi, False)
+            N.check(lib.qpinn_head_forward(self.dcode, hi - lo, self.n, self.z.data_ptr(),
+                                           flat.data_ptr() + self.off_out_w * es,
+                                           flat.data_ptr() + self.off_out_b * es,
+                                           out[lo:].data_ptr(), st), "qpinn_head_forward")
+            N.count_launches(1)
+        return out
+
+    def meyer_wallach(self, flat, x, y, t):
+        """Per-point Meyer-Wallach Q (qsim.py:384-406) of the circuit state."""
+        R = x.shape[0]
+        q = torch.empty(R, dtype=torch.float64, device=self.device)
+        for lo, hi in self._chunks(x):
+            self._trunk_pqc(flat, x, y, t, lo, hi, True)
+            z = self.z[:hi - lo].double()
+            c = self.coh[:hi - lo].double()
+            purity = 0.5 * (1.0 + z * z) + 2.0 * (c[..., 0] ** 2 + c[..., 1] ** 2)
+            q[lo:hi] = 2.0 * (1.0 - purity.mean(dim=1))
+        return q
+
+
 class _ChunkBuffers:
     def __init__(self, engine, ch):
         R = ch.x.numel()
@@ -50,29 +164,15 @@ class NativeEngine:
         self.device, self.dtype = model.device, model.dtype
         self.dcode = N.dtype_code(self.dtype)
         self.scale = _SCALE_CODE[ScaleKind(cfg.scale)]
-        off = {name: o for name, o, _ in model.layout}
-        d = N.TrunkDesc()
-        d.n_hidden = model.n_hidden
-        d.rff = cfg.rff_features
-        d.hidden = cfg.hidden_width
-        d.n_out = self.n
-        for i in range(model.n_hidden):
-            d.off_w[i] = off[f"h{i}.W"]
-            d.off_b[i] = off[f"h{i}.b"]
-        d.off_adapter_w = off["adapter.W"]
-        d.off_adapter_b = off["adapter.b"]
-        d.off_tau_raw = off["tau_raw"]
-        d.t_domain = cfg.t_domain
-        self._omega = model.omega.contiguous()
-        d.omega = self._omega.data_ptr()
-        self.desc = d
+        self.desc, self._omega, off = trunk_desc(model)
         self.off_out_w, self.off_out_b = off["out.W"], off["out.b"]
         self.off_q = off["quantum"]
         lib = N.lib()
         self.chunks = evaluator.chunks
         self.bufs: List[_ChunkBuffers] = [_ChunkBuffers(self, ch) for ch in self.chunks]
         rmax = max((b.R for b in self.bufs), default=0)
-        self.trunk_ws = torch.empty(lib.qpinn_trunk_workspace_bytes(C.byref(d), self.dcode, rmax),
+        self.trunk_ws = torch.empty(lib.qpinn_trunk_workspace_bytes(C.byref(self.desc),
+                                                                    self.dcode, rmax),
                                     dtype=torch.uint8, device=self.device)
         self.loss_ws = torch.empty(lib.qpinn_loss_workspace_bytes(None, 0, 0), dtype=torch.uint8,
                                    device=self.device)

@@ -193,8 +193,13 @@ class RunRow:
 
 @dataclass
 class RunLog:
+    """training.py:236-252."""
     rows: List[RunRow] = field(default_factory=list)
     wall_s: float = 0.0
+    final_i_bh: Optional[float] = None
+    final_i_bh_raw: Optional[float] = None
+    final_l2: Optional[float] = None
+    energy_history: Optional[np.ndarray] = None
 
     def to_csv(self, path) -> None:
         with open(path, "w") as f:
@@ -209,11 +214,33 @@ class TrainResult:
     model: Model
     params: ParameterStore
 
+    def summary(self, config: "TrainConfig", thresholds=None) -> dict:
+        """training.py:264-300."""
+        from .probes import detect_collapse
+        last = self.log.rows[-1]
+        report = detect_collapse(self.log, thresholds) if self.log.final_i_bh is not None \
+            else None
+        return {
+            "case": config.case, "variant": config.model.variant,
+            "ansatz": config.model.ansatz, "scale": config.model.scale,
+            "energy_loss_enabled": config.energy_loss_enabled, "seed": config.seed,
+            "epochs": len(self.log.rows),
+            "counts": {"classical": self.model.n_classical, "quantum": self.model.n_quantum,
+                       "total": self.model.total_parameter_count},
+            "final": {"phys": last.phys, "ic": last.ic, "sym": last.sym,
+                      "energy": last.energy, "total": last.total},
+            "first_total": self.log.rows[0].total,
+            "final_l2": self.log.final_l2, "i_bh": self.log.final_i_bh,
+            "i_bh_raw": self.log.final_i_bh_raw,
+            "collapsed": report.collapsed if report else None,
+            "wall_s": self.log.wall_s,
+        }
+
 
 # -- the step engine ---------------------------------------------------------------------
 
 class Trainer:
-    """Device-resident QPINN epoch step (training.py:359-407 without probes)."""
+    """Device-resident QPINN epoch step (training.py:359-407; probes run in ``train``)."""
 
     def __init__(self, config: TrainConfig, device="cuda", dtype=torch.float32,
                  rank: int = 0, world_size: int = 1, reduce_fn=None, log_grad: bool = False,
@@ -382,16 +409,51 @@ class Trainer:
         return row
 
 
-def train(config: TrainConfig, outdir=None, on_epoch=None, device="cuda",
+def train(config: TrainConfig, reference=None, outdir=None, on_epoch=None, device="cuda",
           dtype=torch.float32, rank: int = 0, world_size: int = 1, reduce_fn=None) -> TrainResult:
-    """Full-batch Adam training (training.py:309-414), probes excluded."""
+    """Full-batch Adam training with the reference's probes (training.py:309-414).
+
+    Per epoch, on the pre-update parameters as in the reference: the
+    Meyer-Wallach Q on 32 seeded probe points (hybrid models), the energy
+    probe and black-hole index every ``probe_cadence`` epochs and on the last,
+    and the L2 error against ``reference`` (an FDTD ``FieldHistory``) every
+    ``eval_cadence`` epochs and on the last.  Probes run on the native
+    inference engine; on ranks > 0 of a data-parallel run they are skipped.
+    """
+    from .probes import bh_index, energy_probe, l2_against_reference, probe_entanglement
+    if config.eval_cadence > 0 and reference is None:
+        raise ConfigError("eval_cadence > 0 requires a reference solution "
+                          "(set eval_cadence=0 to disable L2 evaluation)")
     t0 = time.perf_counter()
     tr = Trainer(config, device=device, dtype=dtype, rank=rank, world_size=world_size,
                  reduce_fn=reduce_fn, log_grad=True)
+    t_end = config.resolved_t_end()
+    prng = np.random.default_rng([config.seed, 9])  # training.py:342-345
+    mw_x = prng.uniform(-1.0, 1.0, config.mw_probe_points)
+    mw_y = prng.uniform(-1.0, 1.0, config.mw_probe_points)
+    mw_t = prng.uniform(0.0, t_end, config.mw_probe_points)
+    probe_times = np.linspace(0.0, t_end, config.probe_grid[2])
+    probes_here = rank == 0
     log = RunLog()
     try:
-        for _ in range(config.epochs):
+        for epoch in range(config.epochs):
+            last = epoch == config.epochs - 1
+            mw = i_bh = l2 = None
+            if probes_here and tr.model.n_quantum:
+                mw = probe_entanglement(tr.model, tr.params, mw_x, mw_y, mw_t)
+            if probes_here and config.probe_cadence > 0 and (
+                    epoch % config.probe_cadence == 0 or last):
+                u_hist = energy_probe(tr.model, tr.params, tr.material, config.probe_grid[0],
+                                      config.probe_grid[1], probe_times)
+                i_bh, raw = bh_index(u_hist, probe_times)
+                log.final_i_bh, log.final_i_bh_raw = i_bh, raw
+                log.energy_history = u_hist
+            if probes_here and config.eval_cadence > 0 and reference is not None and (
+                    epoch % config.eval_cadence == 0 or last):
+                l2 = l2_against_reference(tr.model, tr.params, reference)
+                log.final_l2 = l2
             row = tr.step()
+            row.mw_q, row.i_bh, row.l2_err = mw, i_bh, l2
             log.rows.append(row)
             if on_epoch is not None:
                 on_epoch(row)
