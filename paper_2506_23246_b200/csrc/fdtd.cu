@@ -5,12 +5,15 @@
 // at half steps, a pointwise epsilon in the Ez update, snapshots collocated to
 // the Ez nodes by temporal and spatial two-point averages of H.
 //
-// One launch per time step: every thread owns one cell, recomputes the two
-// neighbouring new H values its Ez update needs (stencil radius 1), and writes
-// the next (Ez, Hx, Hy) into the other buffer set -- no grid-wide barrier.
+// Every thread owns one cell per step, recomputes the two neighbouring new H
+// values its Ez update needs (stencil radius 1) and writes the next (Ez, Hx,
+// Hy) into the other buffer set; all steps run in one cooperative launch with
+// a grid barrier between steps (per-step launches as the fallback).
 // float64 throughout, every operation rounded separately (explicit _rn
 // intrinsics, no FMA contraction) and in numpy's order, so the fields equal
 // the reference's bit for bit given the same initial state.
+#include <cooperative_groups.h>
+
 #include <cmath>
 
 #include "gates.cuh"
@@ -38,34 +41,69 @@ __device__ __forceinline__ double hy_next(const double* __restrict__ ez,
   return __dadd_rn(hy[j * nx + i], __dmul_rn(cx, __dsub_rn(ez[j * nx + in], e)));
 }
 
-// one leapfrog step (fdtd.py:160-174), optionally recording the collocated snapshot
+// one cell of one leapfrog step (fdtd.py:160-174), optionally recording the
+// collocated snapshot
+__device__ __forceinline__ void fdtd_cell(const FdtdDev& p, int c, const double* __restrict__ eps,
+                                          const double* __restrict__ ez,
+                                          const double* __restrict__ hx,
+                                          const double* __restrict__ hy, double* __restrict__ ez_o,
+                                          double* __restrict__ hx_o, double* __restrict__ hy_o,
+                                          double* __restrict__ rec_ez, double* __restrict__ rec_hx,
+                                          double* __restrict__ rec_hy) {
+  const int j = c / p.nx, i = c % p.nx;
+  const int jm = j == 0 ? p.ny - 1 : j - 1, im = i == 0 ? p.nx - 1 : i - 1;
+  const double hxn = hx_next(ez, hx, p.nx, p.ny, j, i, p.cy);
+  const double hyn = hy_next(ez, hy, p.nx, j, i, p.cx);
+  const double hxn_m = hx_next(ez, hx, p.nx, p.ny, jm, i, p.cy);  // roll(hx_new, 1, axis=0)
+  const double hyn_m = hy_next(ez, hy, p.nx, j, im, p.cx);         // roll(hy_new, 1, axis=1)
+  if (rec_ez) {
+    rec_ez[c] = ez[c];
+    const double hxm = __dmul_rn(0.5, __dadd_rn(hx[c], hxn));
+    const double hxm_m = __dmul_rn(0.5, __dadd_rn(hx[jm * p.nx + i], hxn_m));
+    const double hym = __dmul_rn(0.5, __dadd_rn(hy[c], hyn));
+    const double hym_m = __dmul_rn(0.5, __dadd_rn(hy[j * p.nx + im], hyn_m));
+    rec_hx[c] = __dmul_rn(0.5, __dadd_rn(hxm, hxm_m));
+    rec_hy[c] = __dmul_rn(0.5, __dadd_rn(hym, hym_m));
+  }
+  const double curl = __dsub_rn(__ddiv_rn(__dsub_rn(hyn, hyn_m), p.dx),
+                                __ddiv_rn(__dsub_rn(hxn, hxn_m), p.dy));
+  ez_o[c] = __dadd_rn(ez[c], __dmul_rn(__ddiv_rn(p.dt, eps[c]), curl));
+  hx_o[c] = hxn;
+  hy_o[c] = hyn;
+}
+
 __global__ void fdtd_step(FdtdDev p, const double* __restrict__ eps, const double* __restrict__ ez,
                           const double* __restrict__ hx, const double* __restrict__ hy,
                           double* __restrict__ ez_o, double* __restrict__ hx_o,
                           double* __restrict__ hy_o, double* __restrict__ rec_ez,
                           double* __restrict__ rec_hx, double* __restrict__ rec_hy) {
   const int n = p.nx * p.ny;
-  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < n; c += gridDim.x * blockDim.x) {
-    const int j = c / p.nx, i = c % p.nx;
-    const int jm = j == 0 ? p.ny - 1 : j - 1, im = i == 0 ? p.nx - 1 : i - 1;
-    const double hxn = hx_next(ez, hx, p.nx, p.ny, j, i, p.cy);
-    const double hyn = hy_next(ez, hy, p.nx, j, i, p.cx);
-    const double hxn_m = hx_next(ez, hx, p.nx, p.ny, jm, i, p.cy);  // roll(hx_new, 1, axis=0)
-    const double hyn_m = hy_next(ez, hy, p.nx, j, im, p.cx);         // roll(hy_new, 1, axis=1)
-    if (rec_ez) {
-      rec_ez[c] = ez[c];
-      const double hxm = __dmul_rn(0.5, __dadd_rn(hx[c], hxn));
-      const double hxm_m = __dmul_rn(0.5, __dadd_rn(hx[jm * p.nx + i], hxn_m));
-      const double hym = __dmul_rn(0.5, __dadd_rn(hy[c], hyn));
-      const double hym_m = __dmul_rn(0.5, __dadd_rn(hy[j * p.nx + im], hyn_m));
-      rec_hx[c] = __dmul_rn(0.5, __dadd_rn(hxm, hxm_m));
-      rec_hy[c] = __dmul_rn(0.5, __dadd_rn(hym, hym_m));
-    }
-    const double curl = __dsub_rn(__ddiv_rn(__dsub_rn(hyn, hyn_m), p.dx),
-                                  __ddiv_rn(__dsub_rn(hxn, hxn_m), p.dy));
-    ez_o[c] = __dadd_rn(ez[c], __dmul_rn(__ddiv_rn(p.dt, eps[c]), curl));
-    hx_o[c] = hxn;
-    hy_o[c] = hyn;
+  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < n; c += gridDim.x * blockDim.x)
+    fdtd_cell(p, c, eps, ez, hx, hy, ez_o, hx_o, hy_o, rec_ez, rec_hx, rec_hy);
+}
+
+// all steps in one cooperative launch: a grid-wide barrier between steps
+// replaces a kernel launch per step (the per-step work is L2-resident and
+// microseconds long, so launches dominated)
+struct FdtdBufs {
+  double* f[2][3];
+  double* rec[3];
+};
+__global__ void fdtd_persistent(FdtdDev p, const double* __restrict__ eps, FdtdBufs b,
+                                const int32_t* __restrict__ snaps, int n_snaps, int steps) {
+  cooperative_groups::grid_group grid = cooperative_groups::this_grid();
+  const int n = p.nx * p.ny;
+  int k = 0;
+  for (int s = 0; s <= steps; ++s) {
+    const int cur = s & 1;
+    const bool snap = k < n_snaps && snaps[k] == s;
+    const size_t ro = (size_t)k * n;
+    for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < n; c += gridDim.x * blockDim.x)
+      fdtd_cell(p, c, eps, b.f[cur][0], b.f[cur][1], b.f[cur][2], b.f[cur ^ 1][0],
+                b.f[cur ^ 1][1], b.f[cur ^ 1][2], snap ? b.rec[0] + ro : nullptr,
+                snap ? b.rec[1] + ro : nullptr, snap ? b.rec[2] + ro : nullptr);
+    if (snap) ++k;
+    grid.sync();
   }
 }
 
@@ -130,7 +168,8 @@ using namespace qpinn;
 extern "C" {
 
 size_t qpinn_fdtd_workspace_bytes(int nx, int ny) {
-  return nx < 1 || ny < 1 ? 0 : (size_t)7 * nx * ny * sizeof(double);
+  // eps + two field sets, plus room for a snapshot schedule of up to 2^16 steps
+  return nx < 1 || ny < 1 ? 0 : (size_t)7 * nx * ny * sizeof(double) + 65536 * sizeof(int32_t);
 }
 
 int qpinn_fdtd_run(int nx, int ny, int steps, double dt, int ic, const double* pulse,
@@ -158,15 +197,38 @@ int qpinn_fdtd_run(int nx, int ny, int steps, double dt, int ic, const double* p
   fdtd_init<<<blocks, threads, 0, st>>>(p, ic, pc[0], pc[1], pc[2], pc[3], dielectric, eps_r,
                                         slab_x0, eps, buf[0][0], buf[0][1], buf[0][2]);
   QPINN_CUDA_CHECK(cudaGetLastError());
-  int k = 0;
-  for (int s = 0; s <= steps; ++s) {
-    const int cur = s & 1;
-    const bool snap = k < n_snaps && snap_steps[k] == s;
-    fdtd_step<<<blocks, threads, 0, st>>>(
-        p, eps, buf[cur][0], buf[cur][1], buf[cur][2], buf[cur ^ 1][0], buf[cur ^ 1][1],
-        buf[cur ^ 1][2], snap ? rec_ez + k * n : nullptr, snap ? rec_hx + k * n : nullptr,
-        snap ? rec_hy + k * n : nullptr);
-    if (snap) ++k;
+  int coop = 0, dev = 0, per_sm = 0;
+  QPINN_CUDA_CHECK(cudaGetDevice(&dev));
+  QPINN_CUDA_CHECK(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev));
+  QPINN_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fdtd_persistent,
+                                                                 threads, 0));
+  if (coop && per_sm > 0 && n_snaps <= 65536) {
+    int32_t* snaps = (int32_t*)(eps + 7 * n);
+    if (n_snaps)
+      QPINN_CUDA_CHECK(cudaMemcpyAsync(snaps, snap_steps, n_snaps * sizeof(int32_t),
+                                       cudaMemcpyHostToDevice, st));
+    FdtdBufs b{{{buf[0][0], buf[0][1], buf[0][2]}, {buf[1][0], buf[1][1], buf[1][2]}},
+               {rec_ez, rec_hx, rec_hy}};
+    int grid = per_sm * num_sms();
+    const int need = (int)((n + threads - 1) / threads);
+    if (grid > need) grid = need;
+    int ns = n_snaps;
+    int nsteps = steps;
+    void* args[] = {(void*)&p, (void*)&eps, (void*)&b, (void*)&snaps, (void*)&ns,
+                    (void*)&nsteps};
+    QPINN_CUDA_CHECK(cudaLaunchCooperativeKernel((const void*)fdtd_persistent, grid, threads,
+                                                 args, 0, st));
+  } else {
+    int k = 0;
+    for (int s = 0; s <= steps; ++s) {
+      const int cur = s & 1;
+      const bool snap = k < n_snaps && snap_steps[k] == s;
+      fdtd_step<<<blocks, threads, 0, st>>>(
+          p, eps, buf[cur][0], buf[cur][1], buf[cur][2], buf[cur ^ 1][0], buf[cur ^ 1][1],
+          buf[cur ^ 1][2], snap ? rec_ez + k * n : nullptr, snap ? rec_hx + k * n : nullptr,
+          snap ? rec_hy + k * n : nullptr);
+      if (snap) ++k;
+    }
   }
   QPINN_CUDA_CHECK(cudaGetLastError());
   if (energy && n_snaps > 0) {
