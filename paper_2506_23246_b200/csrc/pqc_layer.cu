@@ -311,9 +311,6 @@ pqc_backward_layer(PlanDev plan, const unsigned char* __restrict__ tables, int n
   for (int64_t base = (int64_t)blockIdx.x * per_block; base < R; base += stride) {
     const int64_t s = base + warp * SPW + pw;
     const bool valid = s < R;
-    T c[N], sn[N], dth[N], s1v[N], s2v[N], amax_unused = T(0);
-    load_point_lanes<T, N, LPP>(scale, act, act_tan, R, s, valid, sidx - 1, lane, c, sn, dth,
-                                s1v, s2v, amax_unused);
     cplx<T> xa[2][A];  // [0] this lane's layer-boundary state, [1] its adjoint
     cplx<T>(&x1)[1][A] = reinterpret_cast<cplx<T>(&)[1][A]>(xa[0]);
     cplx<T>(&a1)[1][A] = reinterpret_cast<cplx<T>(&)[1][A]>(xa[1]);
@@ -408,7 +405,11 @@ pqc_backward_layer(PlanDev plan, const unsigned char* __restrict__ tables, int n
                            conj(U[3]));
       }
     }
-    // embedding gradient: xa[1] = phibar (s = 0) or mu_k (s = k+1)
+    // embedding gradient: xa[1] = phibar (s = 0) or mu_k (s = k+1); the point's
+    // angles are loaded only now, so they are not live across the layer loop
+    T c[N], sn[N], dth[N], s1v[N], s2v[N], amax_unused = T(0);
+    load_point_lanes<T, N, LPP>(scale, act, act_tan, R, s, valid, sidx - 1, lane, c, sn, dth,
+                                s1v, s2v, amax_unused);
     embed<T, N, AB>(c, sn, dth, false, gl, xa[0]);
     cplx<T> rho[A];
 #pragma unroll
