@@ -29,6 +29,10 @@ namespace qpinn {
 namespace tc {
 
 constexpr int kBM = 128, kBK = 32;
+// k-blocks accumulated in one TMEM buffer before the epilogue warps add it into
+// fp32 registers (1: 32-deep tensor-core chains, 3.5e-7 relative at K = 256;
+// 2 measured 6.3e-7 at the same speed)
+constexpr int kPromote = 1;
 constexpr int kABytes = kBM * kBK * 4;  // 16 KB fp32 tile
 constexpr int kThreadsGemm = 448;  // 4 split + 8 epilogue + producer + MMA warps
 constexpr int kThreadsW = 320;      // weight gradient: 4 split + 4 epilogue + producer + MMA
@@ -38,7 +42,7 @@ template <int BN>
 struct GemmCfg {
   static constexpr int kBBytes = BN * kBK * 4;
 #ifndef QPINN_GEMM_RAW
-#define QPINN_GEMM_RAW 2
+#define QPINN_GEMM_RAW 3
 #endif
 #ifndef QPINN_GEMM_BS
 #define QPINN_GEMM_BS 2
@@ -51,7 +55,7 @@ struct GemmCfg {
   static constexpr int kNB = 4;    // TMEM partial buffers
   static constexpr int kTmemCols = kNB * BN;
   static constexpr int kSbuf = 32 * BN * 4;
-  static constexpr int kStg = 8 * 4096;  // per epilogue warp: 32 rows x 32 cols
+  static constexpr int kStg = 8 * 2048;  // per epilogue warp: 16 rows x 32 cols
   static constexpr int kSmem =
       kRaw * kABytes + kOps * kOpBytes + kBS * kBStage + kSbuf + kStg + 1024 + 512;
 };
@@ -67,27 +71,33 @@ struct GemmArgs {
 };
 
 // one epilogue warp's 32 rows x CW columns (lane = row) -> global through a
-// 4 KB staging buffer (128-byte swizzled, conflict-free) and TMA stores of
-// 32 x 32 boxes at (col0 + c, row0, blk) of the 3-D output map
+// 2 KB staging buffer (16 rows x 32 columns, 128-byte swizzled, conflict-free)
+// and TMA stores of 32 x 16 boxes at (col0 + c, row0 + 16 h, blk) of the
+// 3-D output map
 template <int CW>
 __device__ __forceinline__ void store_rows_tma(const float (&acc)[CW], unsigned char* buf,
                                                const CUtensorMap* mC, int col0, int row0,
                                                int blk, int lane) {
 #pragma unroll
   for (int c0 = 0; c0 < CW; c0 += 32) {
-    if (lane == 0) bulk_wait_read0();  // the previous store has read the buffer
-    __syncwarp();
-    const uint32_t base = smem_u32(buf) + lane * 128;
 #pragma unroll
-    for (int j = 0; j < 8; ++j)
-      sts128(base + ((j ^ (lane & 7)) << 4),
-             make_float4(acc[c0 + 4 * j], acc[c0 + 4 * j + 1], acc[c0 + 4 * j + 2],
-                         acc[c0 + 4 * j + 3]));
-    fence_proxy_async_smem();
-    __syncwarp();
-    if (lane == 0) {
-      tma_store_3d(mC, buf, col0 + c0, row0, blk);
-      bulk_commit();
+    for (int h = 0; h < 2; ++h) {
+      if (lane == 0) bulk_wait_read0();  // the previous store has read the buffer
+      __syncwarp();
+      if ((lane >> 4) == h) {
+        const uint32_t base = smem_u32(buf) + (lane & 15) * 128;
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          sts128(base + ((j ^ (lane & 7)) << 4),
+                 make_float4(acc[c0 + 4 * j], acc[c0 + 4 * j + 1], acc[c0 + 4 * j + 2],
+                             acc[c0 + 4 * j + 3]));
+      }
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) {
+        tma_store_3d(mC, buf, col0 + c0, row0 + 16 * h, blk);
+        bulk_commit();
+      }
     }
   }
 }
@@ -191,11 +201,13 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUt
   } else if (warp == 13) {  // ---- MMA issuer
     if (lane == 0) {
       constexpr uint32_t idesc = idesc_tf32(kBM, BN);
-      int64_t j = 0;
+      int64_t j = 0, grp = 0;
       for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
         for (int kb = 0; kb < nk; ++kb, ++j) {
-          const int o = (int)(j % OS), e = (int)(j % BS), b = (int)(j % NB);
-          if (j >= NB) mbar_wait(tempty + b, (uint32_t)(((j / NB) - 1) & 1));
+          const int o = (int)(j % OS), e = (int)(j % BS), b = (int)(grp % NB);
+          const bool first = kb % kPromote == 0;
+          const bool last = kb % kPromote == kPromote - 1 || kb == nk - 1;
+          if (first && grp >= NB) mbar_wait(tempty + b, (uint32_t)(((grp / NB) - 1) & 1));
           mbar_wait(conv + o, (uint32_t)((j / OS) & 1));
           mbar_wait(b_full + e, (uint32_t)((j / BS) & 1));
           tc_fence_after();
@@ -207,17 +219,17 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUt
 #pragma unroll
           for (int k = 0; k < kBK / 8; ++k) {
             const uint32_t off = k * 32;  // 8 tf32 = 32 bytes along the swizzled row
-#ifndef QPINN_GEMM_ONEMMA
-            mma_tf32(d, desc_k_sw128(a_lo + off), desc_k_sw128(b_hi + off), idesc, k != 0);
+            mma_tf32(d, desc_k_sw128(a_lo + off), desc_k_sw128(b_hi + off), idesc,
+                     !(first && k == 0));
             mma_tf32(d, desc_k_sw128(a_hi + off), desc_k_sw128(b_lo + off), idesc, 1);
             mma_tf32(d, desc_k_sw128(a_hi + off), desc_k_sw128(b_hi + off), idesc, 1);
-#else
-            mma_tf32(d, desc_k_sw128(a_hi + off), desc_k_sw128(b_hi + off), idesc, k != 0);
-#endif
           }
           mma_commit(op_empty + o);
           mma_commit(b_empty + e);
-          mma_commit(tfull + b);
+          if (last) {
+            mma_commit(tfull + b);
+            ++grp;
+          }
         }
       }
     }
@@ -236,7 +248,6 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUt
         const uint32_t a_dst = smem_u32(op) + threadIdx.x * 16;
         constexpr int CH = kABytes / 16 / 128;  // chunks per thread
         float4 v[CH];
-#ifndef QPINN_GEMM_NOCONV
 #pragma unroll
         for (int i = 0; i < CH; ++i) v[i] = lds128(a_src + i * 2048);
 #pragma unroll
@@ -249,9 +260,6 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUt
           sts128(a_dst + i * 2048, h);
           sts128(a_dst + kABytes + i * 2048, l);
         }
-#else
-        (void)v; (void)a_src; (void)a_dst;
-#endif
         fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) {
@@ -265,7 +273,7 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUt
     const int q = warp & 3, h = (warp - 4) >> 2;
     constexpr int CW = BN / 2;  // columns per epilogue warp
     const uint32_t lane_base = (uint32_t)(q * 32) << 16;
-    unsigned char* my_stg = stg + (warp - 4) * 4096;
+    unsigned char* my_stg = stg + (warp - 4) * 2048;
     int64_t j = 0;
     for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
       const int64_t mt = t / n_nt;
@@ -273,7 +281,8 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUt
       float acc[CW];
 #pragma unroll
       for (int c = 0; c < CW; ++c) acc[c] = 0.f;
-      for (int kb = 0; kb < nk; ++kb, ++j) {
+      const int ngrp = (nk + kPromote - 1) / kPromote;
+      for (int gi = 0; gi < ngrp; ++gi, ++j) {  // j counts promotion groups here
         const int b = (int)(j % NB);
         mbar_wait(tfull + b, (uint32_t)((j / NB) & 1));
         tc_fence_after();
@@ -638,7 +647,7 @@ static int make_out_map(CUtensorMap* m, const float* base, uint64_t cols, uint64
   if (!fn) return fail(QPINN_ERR_CUDA, "cuTensorMapEncodeTiled is unavailable");
   cuuint64_t dims[3] = {cols, rows, blocks};
   cuuint64_t strides[2] = {ld * 4, ld * 4 * rows};
-  cuuint32_t box[3] = {32, 32, 1};
+  cuuint32_t box[3] = {32, 16, 1};
   cuuint32_t es[3] = {1, 1, 1};
   CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(base), dims, strides,
                   box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
