@@ -170,7 +170,16 @@ pqc_forward_layer(PlanDev plan, const unsigned char* __restrict__ tables, int n_
       // so with AB = 4 two gate copies (bits 3, 2) plus a half-swap of
       // the register index cover all wires: fewer moves than single-bit rotation
       // and far less code than unrolling every wire.
-      if constexpr (AB == 4) {
+#ifndef QPINN_K1_UNROLL_REG
+#define QPINN_K1_UNROLL_REG 0
+#endif
+      if constexpr (AB == 4 && QPINN_K1_UNROLL_REG) {  // every register wire its own copy
+        static_for<0, AB>([&](auto qi_) {
+          constexpr int qi = decltype(qi_)::value;
+          const cplx<T>* U = Ul + 4 * (LB + qi);
+          gate_reg<AB - 1 - qi, T, A, 1>(st, U[0], U[1], U[2], U[3]);
+        });
+      } else if constexpr (AB == 4) {
         for (int i = 0; i < AB; i += 2) {
           const cplx<T>* U = Ul + 4 * (LB + i);
           gate_reg<AB - 1, T, A, 1>(st, U[0], U[1], U[2], U[3]);
