@@ -372,19 +372,16 @@ __global__ void features_bwd(int64_t R, int F, const T* __restrict__ x, const T*
       D4 += gdp2 * om[4];
       D5 += gdp2 * om[5];
     }
-#pragma unroll
-    for (int m = 16; m >= 1; m >>= 1) {
-      G4 += __shfl_xor_sync(0xffffffffu, G4, m);
-      G5 += __shfl_xor_sync(0xffffffffu, G5, m);
-      D4 += __shfl_xor_sync(0xffffffffu, D4, m);
-      D5 += __shfl_xor_sync(0xffffffffu, D5, m);
-    }
+    // gt is linear in the feature sums, so each lane folds its partial sums with
+    // the point's coefficients and the warp reduces once, after the last point
     const T dat = -at / tau;
     const T w2 = T(2.0 * kPi) / (tau * tau);
     const T gt = G4 * ct * dat + G5 * (-st) * dat + D4 * (-w2 * ct + w2 * at * st) +
                  D5 * (w2 * st + w2 * at * ct);
     acc += (double)gt;
   }
+#pragma unroll
+  for (int m = 16; m >= 1; m >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, m);
   __shared__ double red[32];
   if (lane == 0) red[warp] = acc;
   __syncthreads();
