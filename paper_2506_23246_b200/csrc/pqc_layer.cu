@@ -89,6 +89,30 @@ __device__ __forceinline__ void rotate_regs_left(cplx<T> (&v)[1 << AB]) {
   for (int r = 0; r < A; ++r) v[r] = t[r];
 }
 
+// reduce-scatter of K values over the lanes that differ in mask bits M, M/2, .., G:
+// at each level a lane keeps the half its mask bit selects and adds the
+// partner's copy of it; the survivors (sums over all those lanes) go to
+// acc[(rbase + i) G + gl]
+template <int M, int G, typename T, int K>
+__device__ __forceinline__ void reduce_scatter_acc(const T (&v)[K], int lane, T* __restrict__ acc,
+                                                   int gl, int rbase) {
+  if constexpr (M < G) {
+#pragma unroll
+    for (int i = 0; i < K; ++i) acc[(rbase + i) * G + gl] += v[i];
+  } else {
+    static_assert(K >= 2, "reduce-scatter needs at least two values per level");
+    const bool up = lane & M;
+    T nv[K / 2];
+#pragma unroll
+    for (int i = 0; i < K / 2; ++i) {
+      const T send = up ? v[i] : v[i + K / 2];
+      const T keep = up ? v[i + K / 2] : v[i];
+      nv[i] = keep + __shfl_xor_sync(0xffffffffu, send, M);
+    }
+    reduce_scatter_acc<M / 2, G, T, K / 2>(nv, lane, acc, gl, rbase + (up ? K / 2 : 0));
+  }
+}
+
 // K1 -> K2 hand-off: the 4 states of point s after the single-qubit gates of
 // layer l (before its entangler), register pairs innermost so that one
 // 16-byte (fp32) store / load per lane moves two amplitudes and a warp
@@ -381,15 +405,29 @@ pqc_backward_layer(PlanDev plan, const unsigned char* __restrict__ tables, int n
       } else if constexpr (ENT == ENT_PHASE) {
         const cplx<T>* ph = sm.ph + l * D;
         T* acc = accP + l * D;
+        if constexpr (A >= 32 / G) {
+          // the D-wide phase gradient summed over the lanes sharing gl by a
+          // reduce-scatter: every lane ends up owning A / (32 / G) sums
+          T pv[A];
 #pragma unroll
-        for (int r = 0; r < A; ++r) {
-          const cplx<T> e = ph[r * G + gl];
-          const cplx<T> xp = cmul(xa[0][r], e);  // post-entangler state
-          T pv = xa[1][r].im * xp.re - xa[1][r].re * xp.im;
+          for (int r = 0; r < A; ++r) {
+            const cplx<T> e = ph[r * G + gl];
+            const cplx<T> xp = cmul(xa[0][r], e);  // post-entangler state
+            pv[r] = xa[1][r].im * xp.re - xa[1][r].re * xp.im;
+            xa[1][r] = cmul(xa[1][r], cplx<T>{e.re, -e.im});
+          }
+          reduce_scatter_acc<16, G, T, A>(pv, lane, acc, gl, 0);
+        } else {
 #pragma unroll
-          for (int mk = G; mk < 32; mk <<= 1) pv += __shfl_xor_sync(0xffffffffu, pv, mk);
-          if (lane_hi == 0) acc[r * G + gl] += pv;
-          xa[1][r] = cmul(xa[1][r], cplx<T>{e.re, -e.im});
+          for (int r = 0; r < A; ++r) {
+            const cplx<T> e = ph[r * G + gl];
+            const cplx<T> xp = cmul(xa[0][r], e);
+            T pv = xa[1][r].im * xp.re - xa[1][r].re * xp.im;
+#pragma unroll
+            for (int mk = G; mk < 32; mk <<= 1) pv += __shfl_xor_sync(0xffffffffu, pv, mk);
+            if (lane_hi == 0) acc[r * G + gl] += pv;
+            xa[1][r] = cmul(xa[1][r], cplx<T>{e.re, -e.im});
+          }
         }
       }
       const cplx<T>* Ul = sm.U + 4 * N * l;
