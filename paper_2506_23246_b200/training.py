@@ -284,10 +284,9 @@ class Trainer:
             self.weights_next = torch.empty_like(self.weights)
         self.epoch = 0
         self._host_inputs = None
-        # CUDA graphs of the step's device part (native engine, one rank): one
-        # graph per (bin-weight buffer, input mode); captured after a warm step
-        self.use_graphs = (graphs and dev.type == "cuda" and self.reduce_fn is None
-                           and self.evaluator.engine is not None)
+        # CUDA graphs of the step's local sweep (native engine): one graph per
+        # (bin-weight buffer, input mode); captured after a warm step
+        self.use_graphs = graphs and dev.type == "cuda" and self.evaluator.engine is not None
         self._graphs = {}
 
     # -- end-to-end mode: collocation inputs come from pinned host memory ------
@@ -326,42 +325,48 @@ class Trainer:
             grad.copy_(flat.grad)
         return grad
 
-    def _device_step(self):
-        """Input copies, sweep (forward + backward), collective, finalize."""
-        cfg = self.config
+    def _local_sweep(self):
+        """Input copies and the sweep (forward + backward) over this rank's chunks."""
         if self._host_inputs is not None:
             for ch, (hx, hy, ht) in zip(self.evaluator.chunks, self._host_inputs):
                 ch.x.copy_(hx, non_blocking=True)
                 ch.y.copy_(hy, non_blocking=True)
                 ch.t.copy_(ht, non_blocking=True)
         self.sums.zero_()
-        grad = self._sweep(self.grad, self.weights, True, self.sums)
+        return self._sweep(self.grad, self.weights, True, self.sums)
+
+    def _reduce_finalize(self, grad):
+        """The step's one collective (data parallel), then the loss finalisation."""
         if self.reduce_fn is not None:
             self._packed = reduce_packed(grad, self.sums, self.reduce_fn, self._packed)
-        self.evaluator.finalize(self.sums, self.weights, cfg.kappa, self.bd,
+        self.evaluator.finalize(self.sums, self.weights, self.config.kappa, self.bd,
                                 self.weights_next if self.weights is not None else None)
-        return grad
 
     def _device_part(self):
-        """The device part of a step, replayed from a CUDA graph once warm (the
-        launch sequence is fixed and every buffer is preallocated); eager while
-        per-kernel event timing is on."""
+        """The device part of a step.  Once warm, the local sweep (the whole
+        fixed launch sequence over preallocated buffers) replays from a CUDA
+        graph; the collective and the finalisation run eagerly after it, so the
+        NCCL all-reduce is never captured.  Eager throughout while per-kernel
+        event timing is on."""
         if not self.use_graphs or self.epoch < 1 or N.timing_enabled():
-            return self._device_step()
-        key = (self.weights.data_ptr() if self.weights is not None else 0,
-               self._host_inputs is not None)
-        entry = self._graphs.get(key)
-        if entry is None:
-            g = torch.cuda.CUDAGraph()
-            l0 = N.LAUNCHES["count"]
-            with torch.cuda.graph(g):
-                self._device_step()
-            entry = (g, N.LAUNCHES["count"] - l0)
-            N.LAUNCHES["count"] = l0
-            self._graphs[key] = entry
-        entry[0].replay()
-        N.count_launches(entry[1])
-        return self.grad
+            grad = self._local_sweep()
+        else:
+            key = (self.weights.data_ptr() if self.weights is not None else 0,
+                   self._host_inputs is not None)
+            entry = self._graphs.get(key)
+            if entry is None:
+                g = torch.cuda.CUDAGraph()
+                l0 = N.LAUNCHES["count"]
+                with torch.cuda.graph(g):
+                    self._local_sweep()
+                entry = (g, N.LAUNCHES["count"] - l0)
+                N.LAUNCHES["count"] = l0
+                self._graphs[key] = entry
+            entry[0].replay()
+            N.count_launches(entry[1])
+            grad = self.grad
+        self._reduce_finalize(grad)
+        return grad
 
     def _check_domain(self):
         if self.model.circuit is not None:
