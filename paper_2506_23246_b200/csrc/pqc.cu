@@ -560,6 +560,22 @@ int pqc_finish_grads_ab(const qpinn_circuit* c, int grid, const KArgs<T>* a, int
   }
   return QPINN_OK;
 }
+template <typename T>
+int pqc_param_grads(const qpinn_circuit* c, const double* tot, int ab, const T* qp, T* g_qp,
+                    cudaStream_t st) {
+  pqc_u1_grads<T><<<1, 256, 0, st>>>(c->dev, qp, tot, g_qp);
+  QPINN_CUDA_CHECK(cudaGetLastError());
+  if (c->dev.n_phase) {
+    pqc_phase_grads<T><<<1, 256, 0, st>>>(c->dev, ab, tot, g_qp);
+    QPINN_CUDA_CHECK(cudaGetLastError());
+  }
+  return QPINN_OK;
+}
+template int pqc_param_grads<float>(const qpinn_circuit*, const double*, int, const float*,
+                                    float*, cudaStream_t);
+template int pqc_param_grads<double>(const qpinn_circuit*, const double*, int, const double*,
+                                     double*, cudaStream_t);
+
 template int pqc_finish_grads<float>(const qpinn_circuit*, int, const KArgs<float>*);
 template int pqc_finish_grads<double>(const qpinn_circuit*, int, const KArgs<double>*);
 template int pqc_finish_grads_ab<float>(const qpinn_circuit*, int, const KArgs<float>*, int);
@@ -626,7 +642,9 @@ int qpinn_pqc_max_qubits(int dtype) {
 size_t qpinn_pqc_workspace_bytes(const qpinn_circuit* c, int dtype, int64_t rows) {
   (void)rows;
   if (!c) return 0;
-  if (c->n > qpinn_pqc_max_qubits(dtype)) return big_workspace_bytes(c, dtype);
+  if (c->n > qpinn_pqc_max_qubits(dtype))
+    return big_workspace_bytes(c, dtype) +
+           (big_bwd_supported(c, dtype) ? 0 : global_adjoint_workspace_bytes(c, dtype));
   return 256 + partial_bytes(c) + align_up(sizeof(double) * n_acc_of(c), 256) +
          tables_bytes_bound(c);
 }
@@ -737,6 +755,23 @@ int qpinn_pqc_backward(const qpinn_circuit* cc, int dtype, int scale, int64_t ro
     double* bt;
     unsigned char* btab;
     big_ws(c, workspace, &bp, &bt, &btab);
+    if (!big_bwd_supported(c, dtype)) {  // HBM regime (pqc_global.cu)
+      const size_t off = align_up(big_workspace_bytes(c, dtype), 256);
+      unsigned char* gws = (unsigned char*)workspace + off;
+      const size_t gbytes = workspace_bytes > off ? workspace_bytes - off : 0;
+      if (dtype == QPINN_F32) {
+        KArgs<float> a{scale, rows, (const float*)act_val, (const float*)act_tan,
+                       (const float*)qparams, nullptr, nullptr, nullptr, nullptr,
+                       (const float*)g_z, (const float*)g_dz, (float*)g_act_val,
+                       (float*)g_act_tan, (float*)g_qparams, nullptr, nullptr, st, nullptr};
+        return global_backward<float>(c, &a, gws, gbytes);
+      }
+      KArgs<double> a{scale, rows, (const double*)act_val, (const double*)act_tan,
+                      (const double*)qparams, nullptr, nullptr, nullptr, nullptr,
+                      (const double*)g_z, (const double*)g_dz, (double*)g_act_val,
+                      (double*)g_act_tan, (double*)g_qparams, nullptr, nullptr, st, nullptr};
+      return global_backward<double>(c, &a, gws, gbytes);
+    }
     if (dtype == QPINN_F32) {
       KArgs<float> a{scale, rows, (const float*)act_val, (const float*)act_tan,
                      (const float*)qparams, nullptr, nullptr, nullptr, nullptr, (const float*)g_z,

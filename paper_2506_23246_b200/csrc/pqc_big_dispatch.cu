@@ -1,6 +1,6 @@
 // Dispatch for the large-n cluster kernels; the kernels themselves are
 // instantiated per n in pqc_big_n*.cu so the build parallelises.
-#include "pqc_layer.h"
+#include "pqc_big.cuh"
 
 namespace qpinn {
 
@@ -28,6 +28,24 @@ int big_dispatch(bool fwd, const qpinn_circuit* c, const KArgs<T>* a) {
 
 template int big_dispatch<float>(bool, const qpinn_circuit*, const KArgs<float>*);
 template int big_dispatch<double>(bool, const qpinn_circuit*, const KArgs<double>*);
+
+bool big_bwd_supported(const qpinn_circuit* c, int dtype) {
+  auto ok = [&](auto tag) -> bool {
+    using T = decltype(tag);
+    switch (c->n) {
+      case 9: return BigGeo<T, 9, 4, true>::CB <= 4;
+      case 10: return BigGeo<T, 10, 4, true>::CB <= 4;
+      case 11: return BigGeo<T, 11, 4, true>::CB <= 4;
+      case 12: return BigGeo<T, 12, 4, true>::CB <= 4;
+      case 13: return BigGeo<T, 13, 4, true>::CB <= 4;
+      case 14: return BigGeo<T, 14, 4, true>::CB <= 4;
+      case 15: return BigGeo<T, 15, 4, true>::CB <= 4;
+      case 16: return sizeof(T) == 4 && BigGeo<T, 16, 4, true>::CB <= 4;
+      default: return false;
+    }
+  };
+  return dtype == QPINN_F64 ? ok(double{}) : ok(float{});
+}
 
 size_t big_workspace_bytes(const qpinn_circuit* c, int dtype) {
   const size_t D = (size_t)1 << c->n, es = dtype == QPINN_F64 ? 16 : 8;

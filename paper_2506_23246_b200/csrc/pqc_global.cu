@@ -1,0 +1,453 @@
+// K2 in the HBM regime (n = 15, 16): the adjoint beyond what a 16-CTA cluster
+// can hold resident (x and the adjoint together need 64 D bytes per point at
+// fp32 -- 4 MB at n = 16).
+//
+// Same algorithm as the layer kernels (pqc_layer.cu): the forward is re-run
+// for a batch of B points with the four states (psi, d psi/dx,y,t) in global
+// memory, storing the state at every layer boundary (after the layer's
+// single-qubit gates); the reverse sweep then keeps only the adjoint live,
+// takes every gate's post-gate state from the boundary checkpoint (gates of
+// one layer commute), and propagates the adjoint through U^dagger.  Each gate
+// is one bandwidth-bound pass over the batch's [B][4][D] array; the per-gate
+// 2x2 outer products and the per-basis-state phase sums are reduced in a
+// fixed order (deterministic), and the embedding gradient follows the oracle
+// (qpinn_oracle.pqc_backward).  Reference: the taped backward of
+// quantum_layer_forward via="gates" (ansatz.py:341-400, tape.py:118-148).
+#include "pqc_layer.h"
+
+namespace qpinn {
+
+namespace {
+
+constexpr int kGbThreads = 256;
+
+inline int gb_blocks(int64_t n) {
+  const int64_t b = (n + kGbThreads - 1) / kGbThreads;
+  const int64_t cap = (int64_t)num_sms() * 8;
+  return (int)(b < 1 ? 1 : b > cap ? cap : b);
+}
+
+// u1 matrices [n_u1][4] and phase diagonals [n_phase][D], natural basis order
+template <typename T>
+__global__ void gb_tables(PlanDev p, const T* __restrict__ qp, cplx<T>* __restrict__ U,
+                          cplx<T>* __restrict__ ph) {
+  const int D = 1 << p.n;
+  const int tid = blockIdx.x * blockDim.x + threadIdx.x, nt = gridDim.x * blockDim.x;
+  for (int i = tid; i < p.n_u1; i += nt) {
+    const int kind = p.u1[i * 4];
+    double th[3] = {0, 0, 0};
+    for (int j = 0; j < u1_nslots(kind); ++j) th[j] = (double)qp[p.u1[i * 4 + 1 + j]];
+    double M[8];
+    u1_matrix_d(kind, th, M);
+    for (int e = 0; e < 4; ++e) U[i * 4 + e] = {T(M[2 * e]), T(M[2 * e + 1])};
+  }
+  for (int i = tid; i < p.n_phase * D; i += nt) {
+    const int st = i / D, b = i % D;
+    double phi = 0.0;
+    for (int k = p.phase_off[st]; k < p.phase_off[st + 1]; ++k) {
+      const int c = p.pairs[3 * k], t = p.pairs[3 * k + 1], s = p.pairs[3 * k + 2];
+      const int on = (b >> (p.n - 1 - c)) & 1, tb = (b >> (p.n - 1 - t)) & 1;
+      phi += on * (tb - 0.5) * (double)qp[s];  // qsim.py:212-225
+    }
+    double sp, cp;
+    sincos(phi, &sp, &cp);
+    ph[i] = {T(cp), T(sp)};
+  }
+}
+
+// per point and qubit: cos, sin of theta/2, S', S'', dtheta_k (k = x, y, t)
+template <typename T>
+__global__ void gb_point(int n, int scale, int64_t R, int64_t p0, int B,
+                         const T* __restrict__ act, const T* __restrict__ tan, T* __restrict__ PT) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < B * n; i += gridDim.x * blockDim.x) {
+    const int pb = i / n, q = i % n;
+    const int64_t s = p0 + pb;
+    T* o = PT + (int64_t)i * 8;
+    if (s >= R) {
+      for (int k = 0; k < 8; ++k) o[k] = T(0);
+      continue;
+    }
+    T a = act[s * n + q];
+    a = fmin(fmax(a, T(-1)), T(1));
+    T c, sn, s1, s2;
+    half_angle<T>(scale, a, c, sn, s1, s2);
+    o[0] = c;
+    o[1] = sn;
+    o[2] = s1;
+    o[3] = s2;
+    for (int k = 0; k < 3; ++k) o[4 + k] = s1 * tan[((int64_t)k * R + s) * n + q];
+  }
+}
+
+// embedded state and its tangents (ansatz.py:233-243, :380-390); wire q is bit n-1-q
+template <typename T>
+__global__ void gb_embed(int n, int B, int nstates, const T* __restrict__ PT,
+                         cplx<T>* __restrict__ X) {
+  const int64_t D = (int64_t)1 << n;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < B * D;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int pb = (int)(i / D);
+    const int64_t b = i % D;
+    const T* pt = PT + (int64_t)pb * n * 8;
+    T pre[17];
+    pre[0] = T(1);
+    for (int q = 0; q < n; ++q) {
+      const int bit = (b >> (n - 1 - q)) & 1;
+      pre[q + 1] = pre[q] * (bit ? pt[q * 8 + 1] : pt[q * 8]);
+    }
+    T tk[3] = {T(0), T(0), T(0)}, suf = T(1);
+    for (int q = n - 1; q >= 0; --q) {
+      const int bit = (b >> (n - 1 - q)) & 1;
+      const T df = bit ? T(0.5) * pt[q * 8] : T(-0.5) * pt[q * 8 + 1];
+      const T rest = pre[q] * suf;
+      for (int k = 0; k < 3; ++k) tk[k] += pt[q * 8 + 4 + k] * df * rest;
+      suf *= bit ? pt[q * 8 + 1] : pt[q * 8];
+    }
+    const int ph = __popcll(b) & 3;  // (-i)^popcount
+    auto put = [&](int s, T m) {
+      X[((int64_t)pb * 4 + s) * D + b] = {ph == 0 ? m : ph == 2 ? -m : T(0),
+                                           ph == 1 ? -m : ph == 3 ? m : T(0)};
+    };
+    put(0, pre[n]);
+    if (nstates == 4)
+      for (int k = 0; k < 3; ++k) put(k + 1, tk[k]);
+  }
+}
+
+// one single-qubit step on every state of the batch (U or U^dagger)
+template <typename T>
+__global__ void gb_u1(int n, int64_t rows, cplx<T>* __restrict__ X, int q,
+                      const cplx<T>* __restrict__ U, int dagger) {
+  const int64_t half = (int64_t)1 << (n - 1), D = half * 2;
+  const int pos = n - 1 - q;
+  cplx<T> u00 = U[0], u01 = U[1], u10 = U[2], u11 = U[3];
+  if (dagger) {
+    const cplx<T> t01 = u01;
+    u00 = {u00.re, -u00.im};
+    u11 = {u11.re, -u11.im};
+    u01 = {u10.re, -u10.im};
+    u10 = {t01.re, -t01.im};
+  }
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < rows * half;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t row = i / half, k = i % half;
+    const int64_t i0 = ((k >> pos) << (pos + 1)) | (k & (((int64_t)1 << pos) - 1));
+    cplx<T>* x = X + row * D;
+    const cplx<T> a = x[i0], b = x[i0 | ((int64_t)1 << pos)];
+    x[i0] = cmul2(u00, a, u01, b);
+    x[i0 | ((int64_t)1 << pos)] = cmul2(u10, a, u11, b);
+  }
+}
+
+// out[row][b] = in[row][tab[b]] (a fused CNOT run or its inverse, qsim.py:198-209)
+template <typename T>
+__global__ void gb_perm(int n, int64_t rows, const cplx<T>* __restrict__ in,
+                        cplx<T>* __restrict__ out, const uint16_t* __restrict__ tab) {
+  const int64_t D = (int64_t)1 << n;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < rows * D;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = in[(i / D) * D + tab[i % D]];
+}
+
+template <typename T>
+__global__ void gb_phase(int n, int64_t rows, cplx<T>* __restrict__ X,
+                         const cplx<T>* __restrict__ ph, int conj_) {
+  const int64_t D = (int64_t)1 << n;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < rows * D;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    cplx<T> e = ph[i % D];
+    if (conj_) e.im = -e.im;
+    X[i] = cmul(X[i], e);
+  }
+}
+
+// adjoint seeds: lambda = 2 w psi + 2 sum_k v_k dpsi_k, mu_k = 2 v_k psi
+template <typename T>
+__global__ void gb_seed(int n, int B, int64_t p0, int64_t R, const T* __restrict__ gz,
+                        const T* __restrict__ gdz, const cplx<T>* __restrict__ X,
+                        cplx<T>* __restrict__ A) {
+  const int64_t D = (int64_t)1 << n;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < B * D;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int pb = (int)(i / D);
+    const int64_t b = i % D, s = p0 + pb;
+    cplx<T>* a = A + (int64_t)pb * 4 * D + b;
+    if (s >= R) {
+      for (int k = 0; k < 4; ++k) a[k * D] = {T(0), T(0)};
+      continue;
+    }
+    T w = T(0), v[3] = {T(0), T(0), T(0)};
+    for (int q = 0; q < n; ++q) {
+      const T sg = ((b >> (n - 1 - q)) & 1) ? T(-1) : T(1);
+      w += sg * gz[s * n + q];
+      for (int k = 0; k < 3; ++k) v[k] += sg * gdz[((int64_t)k * R + s) * n + q];
+    }
+    const cplx<T>* x = X + (int64_t)pb * 4 * D + b;
+    const cplx<T> psi = x[0];
+    cplx<T> l = {T(2) * w * psi.re, T(2) * w * psi.im};
+    for (int k = 0; k < 3; ++k) {
+      const cplx<T> d = x[(k + 1) * D];
+      l.re += T(2) * v[k] * d.re;
+      l.im += T(2) * v[k] * d.im;
+      a[(k + 1) * D] = {T(2) * v[k] * psi.re, T(2) * v[k] * psi.im};
+    }
+    a[0] = l;
+  }
+}
+
+// block partials of the post-gate outer product M'_ij = sum conj(a_i) x_j on wire q
+template <typename T>
+__global__ void gb_outer(int n, int64_t rows, const cplx<T>* __restrict__ X,
+                         const cplx<T>* __restrict__ A, int q, double* __restrict__ part) {
+  __shared__ double red[8][kGbThreads];
+  const int64_t half = (int64_t)1 << (n - 1), D = half * 2;
+  const int pos = n - 1 - q;
+  T m[8] = {T(0), T(0), T(0), T(0), T(0), T(0), T(0), T(0)};
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < rows * half;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t row = i / half, k = i % half;
+    const int64_t i0 = row * D + (((k >> pos) << (pos + 1)) | (k & (((int64_t)1 << pos) - 1)));
+    const int64_t i1 = i0 + ((int64_t)1 << pos);
+    const cplx<T> x0 = X[i0], x1 = X[i1], a0 = A[i0], a1 = A[i1];
+    cmac_c(m[0], m[1], a0, x0);
+    cmac_c(m[2], m[3], a0, x1);
+    cmac_c(m[4], m[5], a1, x0);
+    cmac_c(m[6], m[7], a1, x1);
+  }
+  for (int k = 0; k < 8; ++k) red[k][threadIdx.x] = (double)m[k];
+  __syncthreads();
+  for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+    if (threadIdx.x < s)
+      for (int k = 0; k < 8; ++k) red[k][threadIdx.x] += red[k][threadIdx.x + s];
+    __syncthreads();
+  }
+  if (threadIdx.x < 8) part[(size_t)blockIdx.x * 8 + threadIdx.x] = red[threadIdx.x][0];
+}
+
+// acc[0..8) += sum over blocks in order
+__global__ void gb_sum8(int nblk, const double* __restrict__ part, double* __restrict__ acc) {
+  if (threadIdx.x < 8) {
+    double v = 0.0;
+    for (int b = 0; b < nblk; ++b) v += part[(size_t)b * 8 + threadIdx.x];
+    acc[threadIdx.x] += v;
+  }
+}
+
+// phase step gradient per basis state: accP[b] += sum over the batch's rows of
+// Im(conj(a_b) x'_b), x' = x ph (the post-entangler state)
+template <typename T>
+__global__ void gb_phase_grad(int n, int64_t rows, const cplx<T>* __restrict__ X,
+                              const cplx<T>* __restrict__ A, const cplx<T>* __restrict__ ph,
+                              double* __restrict__ accP) {
+  const int64_t D = (int64_t)1 << n;
+  for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < D;
+       b += (int64_t)gridDim.x * blockDim.x) {
+    const cplx<T> e = ph[b];
+    double v = 0.0;
+    for (int64_t r = 0; r < rows; ++r) {
+      const cplx<T> xp = cmul(X[r * D + b], e), a = A[r * D + b];
+      v += (double)(a.im * xp.re - a.re * xp.im);
+    }
+    accP[b] += v;
+  }
+}
+
+// embedding gradient partials (qpinn_oracle.pqc_backward):
+//   eta = (i/2) phibar - 1/4 sum_k sum_q dth_kq X_q mu_k
+//   g_th[q] = Re sum conj(eta) X_q phi, g_dth[k][q] = Re sum conj((i/2) mu_k) X_q phi
+template <typename T>
+__global__ void gb_embed_grad(int n, int chunks, const T* __restrict__ PT,
+                              const cplx<T>* __restrict__ PHI, const cplx<T>* __restrict__ A,
+                              double* __restrict__ egp) {
+  extern __shared__ double eg_red[];  // [4 n][blockDim]
+  const int64_t D = (int64_t)1 << n;
+  const int pb = blockIdx.y;
+  const T* pt = PT + (int64_t)pb * n * 8;
+  const cplx<T>* phi = PHI + (int64_t)pb * 4 * D;  // state 0 of the re-embedded batch
+  const cplx<T>* ab = A + (int64_t)pb * 4 * D;
+  T acc[4 * 16];
+  for (int j = 0; j < 4 * n; ++j) acc[j] = T(0);
+  const int64_t per = (D + chunks - 1) / chunks;
+  const int64_t b0 = blockIdx.x * per, b1 = b0 + per < D ? b0 + per : D;
+  for (int64_t b = b0 + threadIdx.x; b < b1; b += blockDim.x) {
+    const cplx<T> phib = ab[b];
+    cplx<T> eta = {T(-0.5) * phib.im, T(0.5) * phib.re};  // (i/2) phibar
+    for (int q = 0; q < n; ++q) {
+      const int64_t f = b ^ ((int64_t)1 << (n - 1 - q));
+      for (int k = 0; k < 3; ++k) {
+        const cplx<T> m = ab[(k + 1) * D + f];
+        const T w = T(0.25) * pt[q * 8 + 4 + k];
+        eta.re -= w * m.re;
+        eta.im -= w * m.im;
+      }
+    }
+    for (int q = 0; q < n; ++q) {
+      const cplx<T> y = phi[b ^ ((int64_t)1 << (n - 1 - q))];
+      acc[q] += eta.re * y.re + eta.im * y.im;  // Re(conj(eta) y)
+      for (int k = 0; k < 3; ++k) {
+        const cplx<T> m = ab[(k + 1) * D + b];
+        // (i/2) mu = (-mu.im/2, mu.re/2); Re(conj(that) y)
+        acc[n + k * n + q] += T(-0.5) * m.im * y.re + T(0.5) * m.re * y.im;
+      }
+    }
+  }
+  for (int j = 0; j < 4 * n; ++j) eg_red[j * blockDim.x + threadIdx.x] = (double)acc[j];
+  __syncthreads();
+  for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+    if (threadIdx.x < s)
+      for (int j = 0; j < 4 * n; ++j)
+        eg_red[j * blockDim.x + threadIdx.x] += eg_red[j * blockDim.x + threadIdx.x + s];
+    __syncthreads();
+  }
+  for (int j = threadIdx.x; j < 4 * n; j += blockDim.x)
+    egp[((int64_t)pb * chunks + blockIdx.x) * 4 * n + j] = eg_red[j * blockDim.x];
+}
+
+template <typename T>
+__global__ void gb_embed_final(int n, int B, int chunks, int64_t p0, int64_t R,
+                               const double* __restrict__ egp, const T* __restrict__ PT,
+                               const T* __restrict__ tan, T* __restrict__ g_act,
+                               T* __restrict__ g_tan) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < B * n; i += gridDim.x * blockDim.x) {
+    const int pb = i / n, q = i % n;
+    const int64_t s = p0 + pb;
+    if (s >= R) continue;
+    double g[4] = {0, 0, 0, 0};
+    for (int c = 0; c < chunks; ++c) {
+      const double* e = egp + ((int64_t)pb * chunks + c) * 4 * n;
+      for (int k = 0; k < 4; ++k) g[k] += e[k * n + q];
+    }
+    const T* pt = PT + ((int64_t)pb * n + q) * 8;
+    const T s1 = pt[2], s2 = pt[3];
+    T ga = T(g[0]) * s1;
+    for (int k = 0; k < 3; ++k) {
+      ga += T(g[1 + k]) * tan[((int64_t)k * R + s) * n + q] * s2;
+      g_tan[((int64_t)k * R + s) * n + q] = T(g[1 + k]) * s1;
+    }
+    g_act[s * n + q] = ga;
+  }
+}
+
+constexpr int kGbChunks = 32;  // blocks per point for the embedding gradient
+
+struct GbLayout {
+  int B;
+  size_t acc, part, U, ph, PT, X, A, TMP, CK, EG, total;
+};
+
+template <typename T>
+GbLayout gb_layout(const qpinn_circuit* c) {
+  const size_t D = (size_t)1 << c->n, es = sizeof(cplx<T>);
+  const size_t per_point = (3 + (size_t)c->L) * 4 * D * es;
+  int B = (int)((size_t)(1u << 30) / per_point);  // ~1 GB of batch state
+  B = B < 1 ? 1 : B > 16 ? 16 : B;
+  GbLayout g{};
+  g.B = B;
+  size_t o = 0;
+  auto take = [&](size_t bytes) {
+    const size_t at = o;
+    o += align_up(bytes, 256);
+    return at;
+  };
+  g.acc = take(8 * (8 * (size_t)c->n_u1 + D * c->n_phase));
+  g.part = take(8 * 8 * (size_t)num_sms() * 8);
+  g.U = take(es * 4 * c->n_u1);
+  g.ph = take(es * D * c->n_phase);
+  g.PT = take(sizeof(T) * 8 * (size_t)B * c->n);
+  g.X = take(4 * D * B * es);
+  g.A = take(4 * D * B * es);
+  g.TMP = take(4 * D * B * es);
+  g.CK = take((size_t)c->L * 4 * D * B * es);
+  g.EG = take(8 * (size_t)B * kGbChunks * 4 * c->n);
+  g.total = o;
+  return g;
+}
+
+}  // namespace
+
+size_t global_adjoint_workspace_bytes(const qpinn_circuit* c, int dtype) {
+  return dtype == QPINN_F64 ? gb_layout<double>(c).total : gb_layout<float>(c).total;
+}
+
+template <typename T>
+int global_backward(const qpinn_circuit* c, const KArgs<T>* a, unsigned char* ws, size_t bytes) {
+  const PlanDev& p = c->dev;
+  const int n = c->n, L = c->L;
+  const int64_t D = (int64_t)1 << n;
+  const int ent = layer_entangler(c);
+  if (ent < 0) return fail(QPINN_ERR_CAPACITY, "HBM-regime adjoint needs the standard layer plan");
+  const GbLayout g = gb_layout<T>(c);
+  if (bytes < g.total) return fail(QPINN_ERR_CONFIG, "HBM-regime adjoint: workspace too small");
+  cudaStream_t st = a->stream;
+  double* acc = (double*)(ws + g.acc);
+  double* part = (double*)(ws + g.part);
+  cplx<T>* U = (cplx<T>*)(ws + g.U);
+  cplx<T>* ph = (cplx<T>*)(ws + g.ph);
+  T* PT = (T*)(ws + g.PT);
+  cplx<T>* X = (cplx<T>*)(ws + g.X);
+  cplx<T>* A = (cplx<T>*)(ws + g.A);
+  cplx<T>* TMP = (cplx<T>*)(ws + g.TMP);
+  cplx<T>* CK = (cplx<T>*)(ws + g.CK);
+  double* EG = (double*)(ws + g.EG);
+  const int n_acc = 8 * p.n_u1 + (int)D * p.n_phase;
+  const int eg_smem = 4 * n * 128 * (int)sizeof(double);
+  QPINN_CUDA_CHECK(cudaFuncSetAttribute(gb_embed_grad<T>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, eg_smem));
+  QPINN_CUDA_CHECK(cudaMemsetAsync(acc, 0, 8 * (size_t)n_acc, st));
+  gb_tables<T><<<64, 256, 0, st>>>(p, a->qp, U, ph);
+  const int B = g.B;
+  const int64_t rows = (int64_t)B * 4;
+  const int ob = gb_blocks(rows * (D / 2));
+  for (int64_t p0 = 0; p0 < a->R; p0 += B) {
+    gb_point<T><<<gb_blocks(B * n), kGbThreads, 0, st>>>(n, a->scale, a->R, p0, B, a->act, a->tan,
+                                                         PT);
+    gb_embed<T><<<gb_blocks(B * D), kGbThreads, 0, st>>>(n, B, 4, PT, X);
+    // forward with layer-boundary checkpoints
+    for (int l = 0; l < L; ++l) {
+      for (int q = 0; q < n; ++q)
+        gb_u1<T><<<ob, kGbThreads, 0, st>>>(n, rows, X, q, U + 4 * (l * n + q), 0);
+      QPINN_CUDA_CHECK(cudaMemcpyAsync(CK + (size_t)l * rows * D, X, rows * D * sizeof(cplx<T>),
+                                       cudaMemcpyDeviceToDevice, st));
+      if (ent == ENT_PERM) {
+        gb_perm<T><<<gb_blocks(rows * D), kGbThreads, 0, st>>>(n, rows, X, TMP, p.perm + l * D);
+        std::swap(X, TMP);
+      } else if (ent == ENT_PHASE) {
+        gb_phase<T><<<gb_blocks(rows * D), kGbThreads, 0, st>>>(n, rows, X, ph + l * D, 0);
+      }
+    }
+    gb_seed<T><<<gb_blocks(B * D), kGbThreads, 0, st>>>(n, B, p0, a->R, a->gz, a->gdz, X, A);
+    // reverse sweep: only the adjoint is propagated
+    for (int l = L - 1; l >= 0; --l) {
+      const cplx<T>* xl = CK + (size_t)l * rows * D;
+      if (ent == ENT_PERM) {
+        gb_perm<T><<<gb_blocks(rows * D), kGbThreads, 0, st>>>(n, rows, A, TMP, p.iperm + l * D);
+        std::swap(A, TMP);
+      } else if (ent == ENT_PHASE) {
+        gb_phase_grad<T><<<gb_blocks(D), kGbThreads, 0, st>>>(n, rows, xl, A, ph + l * D,
+                                                               acc + 8 * p.n_u1 + l * D);
+        gb_phase<T><<<gb_blocks(rows * D), kGbThreads, 0, st>>>(n, rows, A, ph + l * D, 1);
+      }
+      for (int q = 0; q < n; ++q) {
+        gb_outer<T><<<ob, kGbThreads, 0, st>>>(n, rows, xl, A, q, part);
+        gb_sum8<<<1, 32, 0, st>>>(ob, part, acc + 8 * (l * n + q));
+      }
+      for (int q = 0; q < n; ++q)
+        gb_u1<T><<<ob, kGbThreads, 0, st>>>(n, rows, A, q, U + 4 * (l * n + q), 1);
+    }
+    // embedding gradient against the re-embedded state
+    gb_embed<T><<<gb_blocks(B * D), kGbThreads, 0, st>>>(n, B, 1, PT, X);
+    gb_embed_grad<T><<<dim3(kGbChunks, B), 128, eg_smem, st>>>(
+        n, kGbChunks, PT, X, A, EG);
+    gb_embed_final<T><<<gb_blocks(B * n), kGbThreads, 0, st>>>(n, B, kGbChunks, p0, a->R, EG, PT,
+                                                                a->tan, a->g_act, a->g_tan);
+    QPINN_CUDA_CHECK(cudaGetLastError());
+  }
+  return pqc_param_grads<T>(c, acc, n, a->qp, a->g_qp, st);
+}
+
+template int global_backward<float>(const qpinn_circuit*, const KArgs<float>*, unsigned char*,
+                                    size_t);
+template int global_backward<double>(const qpinn_circuit*, const KArgs<double>*, unsigned char*,
+                                     size_t);
+
+}  // namespace qpinn

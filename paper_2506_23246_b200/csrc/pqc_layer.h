@@ -51,5 +51,15 @@ int pqc_finish_grads_ab(const qpinn_circuit* c, int grid, const KArgs<T>* a, int
 template <typename T>
 int big_dispatch(bool fwd, const qpinn_circuit* c, const KArgs<T>* a);
 size_t big_workspace_bytes(const qpinn_circuit* c, int dtype);
+// whether the cluster-resident adjoint covers this circuit (else the HBM regime)
+bool big_bwd_supported(const qpinn_circuit* c, int dtype);
+// gate-space sums tot [8 n_u1 | D n_phase] -> parameter gradients (pqc.cu)
+template <typename T>
+int pqc_param_grads(const qpinn_circuit* c, const double* tot, int ab, const T* qp, T* g_qp,
+                    cudaStream_t st);
+// HBM-regime adjoint (pqc_global.cu)
+size_t global_adjoint_workspace_bytes(const qpinn_circuit* c, int dtype);
+template <typename T>
+int global_backward(const qpinn_circuit* c, const KArgs<T>* a, unsigned char* ws, size_t bytes);
 
 }  // namespace qpinn

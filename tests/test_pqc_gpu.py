@@ -174,13 +174,14 @@ def test_specialized_kernels_match_generic_and_oracle(kind, dtype):
 
 BIG_CASES = [(9, 2, "strongly", True), (10, 1, "cross_mesh_2rot", True), (11, 2, "cross_mesh", True),
              (12, 2, "strongly", True), (13, 1, "basic", True), (14, 1, "cross_mesh_cnot", True),
-             (15, 1, "strongly", False), (16, 1, "no_entanglement", False),
-             (16, 1, "cross_mesh", False)]
+             (15, 1, "strongly", True), (16, 1, "no_entanglement", True),
+             (16, 1, "cross_mesh", True), (15, 2, "cross_mesh_2rot", True)]
 
 
 @pytest.mark.parametrize("n,L,kind,bwd", BIG_CASES)
 def test_cluster_kernels_large_n_vs_oracle(n, L, kind, bwd):
-    """n = 9..16: thread-block-cluster kernels (DSMEM exchanges) vs the oracle."""
+    """n = 9..16: thread-block-cluster kernels (DSMEM exchanges) vs the oracle; the
+    adjoint at n = 15, 16 runs the HBM-regime path (pqc_global.cu)."""
     from paper_2506_23246_b200.ansatz import build_circuit, pqc_backward_raw, pqc_forward_raw
     dtype = torch.float32
     rng = np.random.default_rng(n * 7 + L)
@@ -202,3 +203,23 @@ def test_cluster_kernels_large_n_vs_oracle(n, L, kind, bwd):
         assert_close(ga, wga, dtype, f"n={n} ga", s)
         assert_close(gda, wgda, dtype, f"n={n} gda", s)
         assert_close(gq, wgq, dtype, f"n={n} gq", s)
+
+
+@pytest.mark.parametrize("n,L,kind", [(16, 1, "strongly"), (15, 1, "cross_mesh")])
+def test_hbm_regime_adjoint_float64(n, L, kind):
+    """float64 adjoint beyond the cluster-resident range vs the oracle (1e-10)."""
+    from paper_2506_23246_b200.ansatz import build_circuit, pqc_backward_raw
+    dtype = torch.float64
+    rng = np.random.default_rng(n * 11 + L)
+    c = build_circuit(kind, n, L)
+    R = 2
+    d = dict(a=rng.uniform(-0.9, 0.9, (R, n)), da=rng.normal(size=(3, R, n)),
+             qp=rng.uniform(0, 2 * np.pi, c.param_count), gz=rng.normal(size=(R, n)),
+             gdz=rng.normal(size=(3, R, n)))
+    ga, gda, gq = pqc_backward_raw(c, "acos", cuda(d["a"], dtype), cuda(d["da"], dtype),
+                                   cuda(d["qp"], dtype), cuda(d["gz"], dtype),
+                                   cuda(d["gdz"], dtype))
+    wga, wgda, wgq = O.pqc_backward(d["a"], d["da"], d["qp"], kind, "acos", L, d["gz"], d["gdz"])
+    assert_close(ga, wga, dtype, f"n={n} ga")
+    assert_close(gda, wgda, dtype, f"n={n} gda")
+    assert_close(gq, wgq, dtype, f"n={n} gq")
