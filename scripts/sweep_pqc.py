@@ -44,6 +44,9 @@ def main():
     quick = "--quick" in sys.argv
     rng = np.random.default_rng(0)
     ns = range(4, 17)
+    for arg in sys.argv[1:]:
+        if arg.startswith("--n="):  # e.g. --n=15,16
+            ns = [int(v) for v in arg[4:].split(",")]
     Ls = (1, 4) if quick else (1, 4, 8)
     kinds = ("strongly", "cross_mesh", "no_entanglement")
     for n in ns:
@@ -79,6 +82,8 @@ def main():
                 except CapacityError as e:
                     row["k2"] = f"unsupported: {e}"
                 row["regime"] = "warp" if n <= 8 else ("cta" if n <= 12 else "cluster")
+                if n >= 15:
+                    row["k2_regime"] = "hbm (global-memory checkpoints)"
                 print(json.dumps(row), flush=True)
                 del a, da, g, gd, st
                 torch.cuda.empty_cache()
