@@ -643,8 +643,8 @@ size_t qpinn_pqc_workspace_bytes(const qpinn_circuit* c, int dtype, int64_t rows
   (void)rows;
   if (!c) return 0;
   if (c->n > qpinn_pqc_max_qubits(dtype))
-    return big_workspace_bytes(c, dtype) +
-           (big_bwd_supported(c, dtype) ? 0 : global_adjoint_workspace_bytes(c, dtype));
+    return align_up(big_workspace_bytes(c, dtype), 256) +
+           global_adjoint_workspace_bytes(c, dtype);
   return 256 + partial_bytes(c) + align_up(sizeof(double) * n_acc_of(c), 256) +
          tables_bytes_bound(c);
 }
@@ -689,6 +689,21 @@ int qpinn_pqc_forward(const qpinn_circuit* cc, int dtype, int scale, int64_t row
     double* tot;
     unsigned char* tables;
     big_ws(c, workspace, &partial, &tot, &tables);
+    if (!act_tan || !big_fwd_supported(c, dtype)) {  // global-memory forward (pqc_global.cu)
+      const size_t off = align_up(big_workspace_bytes(c, dtype), 256);
+      unsigned char* gws = (unsigned char*)workspace + off;
+      const size_t gbytes = workspace_bytes > off ? workspace_bytes - off : 0;
+      if (dtype == QPINN_F32) {
+        KArgs<float> a{scale, rows, (const float*)act_val, (const float*)act_tan,
+                       (const float*)qparams, (float*)z, (float*)dz, nullptr, maxabs, nullptr,
+                       nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, st, nullptr};
+        return global_forward<float>(c, &a, gws, gbytes);
+      }
+      KArgs<double> a{scale, rows, (const double*)act_val, (const double*)act_tan,
+                      (const double*)qparams, (double*)z, (double*)dz, nullptr, maxabs, nullptr,
+                      nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, st, nullptr};
+      return global_forward<double>(c, &a, gws, gbytes);
+    }
     if (dtype == QPINN_F32) {
       KArgs<float> a{scale, rows, (const float*)act_val, (const float*)act_tan, (const float*)qparams,
                      (float*)z, (float*)dz, nullptr, maxabs, nullptr, nullptr, nullptr, nullptr,

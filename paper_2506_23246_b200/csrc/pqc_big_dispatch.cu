@@ -47,6 +47,10 @@ bool big_bwd_supported(const qpinn_circuit* c, int dtype) {
   return dtype == QPINN_F64 ? ok(double{}) : ok(float{});
 }
 
+bool big_fwd_supported(const qpinn_circuit* c, int dtype) {
+  return c->n >= 9 && (c->n <= 15 || (c->n == 16 && dtype == QPINN_F32));
+}
+
 size_t big_workspace_bytes(const qpinn_circuit* c, int dtype) {
   const size_t D = (size_t)1 << c->n, es = dtype == QPINN_F64 ? 16 : 8;
   const size_t n_acc = 8 * (size_t)c->n_u1 + D * c->n_phase;

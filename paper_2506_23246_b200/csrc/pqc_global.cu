@@ -75,7 +75,7 @@ __global__ void gb_point(int n, int scale, int64_t R, int64_t p0, int B,
     o[1] = sn;
     o[2] = s1;
     o[3] = s2;
-    for (int k = 0; k < 3; ++k) o[4 + k] = s1 * tan[((int64_t)k * R + s) * n + q];
+    for (int k = 0; k < 3; ++k) o[4 + k] = tan ? s1 * tan[((int64_t)k * R + s) * n + q] : T(0);
   }
 }
 
@@ -328,7 +328,72 @@ __global__ void gb_embed_final(int n, int B, int chunks, int64_t p0, int64_t R,
   }
 }
 
-constexpr int kGbChunks = 32;  // blocks per point for the embedding gradient
+// readout partials (qsim.py:369-381, ansatz.py:395-399): per point
+// z_q = sum_b |psi_b|^2 s_bq, dz_kq = sum_b 2 Re(conj(psi_b) dpsi_kb) s_bq
+template <typename T>
+__global__ void gb_readout(int n, int chunks, int nstates, const cplx<T>* __restrict__ X,
+                           double* __restrict__ rp) {
+  extern __shared__ double ro_red[];  // [4 n][blockDim]
+  const int64_t D = (int64_t)1 << n;
+  const int pb = blockIdx.y;
+  const cplx<T>* x = X + (int64_t)pb * 4 * D;
+  T acc[4 * 16];
+  for (int j = 0; j < 4 * n; ++j) acc[j] = T(0);
+  const int64_t per = (D + chunks - 1) / chunks;
+  const int64_t b0 = blockIdx.x * per, b1 = b0 + per < D ? b0 + per : D;
+  for (int64_t b = b0 + threadIdx.x; b < b1; b += blockDim.x) {
+    const cplx<T> psi = x[b];
+    T v[4];
+    v[0] = psi.re * psi.re + psi.im * psi.im;
+    for (int k = 1; k < nstates; ++k) {
+      const cplx<T> d = x[k * D + b];
+      v[k] = T(2) * (psi.re * d.re + psi.im * d.im);
+    }
+    for (int q = 0; q < n; ++q) {
+      const T sg = ((b >> (n - 1 - q)) & 1) ? T(-1) : T(1);
+      for (int k = 0; k < nstates; ++k) acc[k * n + q] += sg * v[k];
+    }
+  }
+  for (int j = 0; j < 4 * n; ++j) ro_red[j * blockDim.x + threadIdx.x] = (double)acc[j];
+  __syncthreads();
+  for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+    if (threadIdx.x < s)
+      for (int j = 0; j < 4 * n; ++j)
+        ro_red[j * blockDim.x + threadIdx.x] += ro_red[j * blockDim.x + threadIdx.x + s];
+    __syncthreads();
+  }
+  for (int j = threadIdx.x; j < 4 * n; j += blockDim.x)
+    rp[((int64_t)pb * chunks + blockIdx.x) * 4 * n + j] = ro_red[j * blockDim.x];
+}
+
+template <typename T>
+__global__ void gb_readout_final(int n, int B, int chunks, int nstates, int64_t p0, int64_t R,
+                                 const double* __restrict__ rp, T* __restrict__ z,
+                                 T* __restrict__ dz) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < B * n; i += gridDim.x * blockDim.x) {
+    const int pb = i / n, q = i % n;
+    const int64_t s = p0 + pb;
+    if (s >= R) continue;
+    double g[4] = {0, 0, 0, 0};
+    for (int c = 0; c < chunks; ++c)
+      for (int k = 0; k < nstates; ++k) g[k] += rp[((int64_t)pb * chunks + c) * 4 * n + k * n + q];
+    z[s * n + q] = T(g[0]);
+    for (int k = 1; k < nstates; ++k) dz[((int64_t)(k - 1) * R + s) * n + q] = T(g[k]);
+  }
+}
+
+template <typename T>
+__global__ void gb_maxabs(int64_t count, const T* __restrict__ act,
+                          unsigned long long* __restrict__ maxabs) {
+  T m = T(0);
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count;
+       i += (int64_t)gridDim.x * blockDim.x)
+    m = fmax(m, fabs(act[i]));
+  for (int s = 16; s >= 1; s >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, s));
+  if ((threadIdx.x & 31) == 0) atomic_max_abs(maxabs, m);
+}
+
+constexpr int kGbChunks = 32;  // blocks per point for the embedding gradient / readout
 
 struct GbLayout {
   int B;
@@ -445,6 +510,60 @@ int global_backward(const qpinn_circuit* c, const KArgs<T>* a, unsigned char* ws
   return pqc_param_grads<T>(c, acc, n, a->qp, a->g_qp, st);
 }
 
+// forward in global memory: value-only for any n beyond the register kernels,
+// and with tangents where no cluster kernel exists (float64, n = 16)
+template <typename T>
+int global_forward(const qpinn_circuit* c, const KArgs<T>* a, unsigned char* ws, size_t bytes) {
+  const PlanDev& p = c->dev;
+  const int n = c->n, L = c->L;
+  const int64_t D = (int64_t)1 << n;
+  const int ent = layer_entangler(c);
+  if (ent < 0) return fail(QPINN_ERR_CAPACITY, "global-memory PQC needs the standard layer plan");
+  const GbLayout g = gb_layout<T>(c);
+  if (bytes < g.total) return fail(QPINN_ERR_CONFIG, "global-memory PQC: workspace too small");
+  cudaStream_t st = a->stream;
+  cplx<T>* U = (cplx<T>*)(ws + g.U);
+  cplx<T>* ph = (cplx<T>*)(ws + g.ph);
+  T* PT = (T*)(ws + g.PT);
+  cplx<T>* X = (cplx<T>*)(ws + g.X);
+  cplx<T>* TMP = (cplx<T>*)(ws + g.TMP);
+  double* RP = (double*)(ws + g.EG);
+  const int ns = a->tan ? 4 : 1;
+  const int ro_smem = 4 * n * 128 * (int)sizeof(double);
+  QPINN_CUDA_CHECK(cudaFuncSetAttribute(gb_readout<T>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, ro_smem));
+  gb_tables<T><<<64, 256, 0, st>>>(p, a->qp, U, ph);
+  if (a->maxabs)
+    gb_maxabs<T><<<gb_blocks(a->R * n), kGbThreads, 0, st>>>(a->R * n, a->act, a->maxabs);
+  const int B = g.B;
+  const int64_t rows = (int64_t)B * 4;
+  const int ob = gb_blocks(rows * (D / 2));
+  for (int64_t p0 = 0; p0 < a->R; p0 += B) {
+    gb_point<T><<<gb_blocks(B * n), kGbThreads, 0, st>>>(n, a->scale, a->R, p0, B, a->act,
+                                                         a->tan, PT);
+    gb_embed<T><<<gb_blocks(B * D), kGbThreads, 0, st>>>(n, B, ns, PT, X);
+    for (int l = 0; l < L; ++l) {
+      for (int q = 0; q < n; ++q)
+        gb_u1<T><<<ob, kGbThreads, 0, st>>>(n, rows, X, q, U + 4 * (l * n + q), 0);
+      if (ent == ENT_PERM) {
+        gb_perm<T><<<gb_blocks(rows * D), kGbThreads, 0, st>>>(n, rows, X, TMP, p.perm + l * D);
+        std::swap(X, TMP);
+      } else if (ent == ENT_PHASE) {
+        gb_phase<T><<<gb_blocks(rows * D), kGbThreads, 0, st>>>(n, rows, X, ph + l * D, 0);
+      }
+    }
+    gb_readout<T><<<dim3(kGbChunks, B), 128, ro_smem, st>>>(n, kGbChunks, ns, X, RP);
+    gb_readout_final<T><<<gb_blocks(B * n), kGbThreads, 0, st>>>(n, B, kGbChunks, ns, p0, a->R,
+                                                                  RP, a->z, a->dz);
+    QPINN_CUDA_CHECK(cudaGetLastError());
+  }
+  return QPINN_OK;
+}
+
+template int global_forward<float>(const qpinn_circuit*, const KArgs<float>*, unsigned char*,
+                                   size_t);
+template int global_forward<double>(const qpinn_circuit*, const KArgs<double>*, unsigned char*,
+                                    size_t);
 template int global_backward<float>(const qpinn_circuit*, const KArgs<float>*, unsigned char*,
                                     size_t);
 template int global_backward<double>(const qpinn_circuit*, const KArgs<double>*, unsigned char*,

@@ -61,5 +61,9 @@ int pqc_param_grads(const qpinn_circuit* c, const double* tot, int ab, const T* 
 size_t global_adjoint_workspace_bytes(const qpinn_circuit* c, int dtype);
 template <typename T>
 int global_backward(const qpinn_circuit* c, const KArgs<T>* a, unsigned char* ws, size_t bytes);
+template <typename T>
+int global_forward(const qpinn_circuit* c, const KArgs<T>* a, unsigned char* ws, size_t bytes);
+// whether a cluster forward kernel with tangents exists for this circuit
+bool big_fwd_supported(const qpinn_circuit* c, int dtype);
 
 }  // namespace qpinn

@@ -57,9 +57,7 @@ def test_pqc_mid_sizes(dtype):
 @pytest.mark.parametrize("dtype", DTYPES)
 @pytest.mark.parametrize("n,L", [(1, 3), (2, 2), (8, 2)])
 def test_pqc_vs_oracle_other_sizes(dtype, n, L):
-    from paper_2506_23246_b200 import _native as N
-    if n > N.lib().qpinn_pqc_max_qubits(0 if dtype == torch.float32 else 1):
-        pytest.skip("beyond the register regime for this dtype")
+    # float64 n = 8 is beyond the register kernels: it runs the global-memory path
     rng = np.random.default_rng(n * 100 + L)
     for kind in (("no_entanglement",) if n == 1 else ("strongly", "cross_mesh_2rot", "cross_mesh_cnot")):
         P = O.build_circuit(kind, n, L)[1]
@@ -223,3 +221,26 @@ def test_hbm_regime_adjoint_float64(n, L, kind):
     assert_close(ga, wga, dtype, f"n={n} ga")
     assert_close(gda, wgda, dtype, f"n={n} gda")
     assert_close(gq, wgq, dtype, f"n={n} gq")
+
+
+@pytest.mark.parametrize("n,L,kind,dtype", [(9, 2, "strongly", torch.float32),
+                                            (12, 1, "cross_mesh", torch.float64),
+                                            (16, 1, "strongly", torch.float64),
+                                            (15, 1, "cross_mesh_2rot", torch.float32)])
+def test_global_memory_forward_vs_oracle(n, L, kind, dtype):
+    """Value-only forward beyond the register kernels (any n) and the float64
+    n = 16 forward with tangents run in global memory (pqc_global.cu)."""
+    from paper_2506_23246_b200.ansatz import build_circuit, pqc_forward_raw
+    rng = np.random.default_rng(n * 13 + L)
+    c = build_circuit(kind, n, L)
+    R = 3
+    a = rng.uniform(-0.9, 0.9, (R, n))
+    da = rng.normal(size=(3, R, n))
+    qp = rng.uniform(0, 2 * np.pi, c.param_count)
+    wz, wdz = O.pqc_forward(a, da, qp, kind, "acos", L)
+    z, _ = pqc_forward_raw(c, "acos", cuda(a, dtype), None, cuda(qp, dtype))
+    assert_close(z, wz, dtype, f"n={n} value-only z")
+    if dtype == torch.float64 and n == 16:
+        z, dz = pqc_forward_raw(c, "acos", cuda(a, dtype), cuda(da, dtype), cuda(qp, dtype))
+        assert_close(z, wz, dtype, "z")
+        assert_close(dz, wdz, dtype, "dz")
