@@ -4,8 +4,19 @@
 
 namespace qpinn {
 
-template <typename T, int N>
-int big_n(bool fwd, int ent, const qpinn_circuit* c, const KArgs<T>* a);
+// instantiated in pqc_big_n*.cu; extern here so this TU does not compile every kernel again
+#define QPINN_BIG_EXTERN(N)                                                              \
+  extern template int big_n<float, N>(bool, int, const qpinn_circuit*, const KArgs<float>*); \
+  extern template int big_n<double, N>(bool, int, const qpinn_circuit*, const KArgs<double>*);
+QPINN_BIG_EXTERN(9)
+QPINN_BIG_EXTERN(10)
+QPINN_BIG_EXTERN(11)
+QPINN_BIG_EXTERN(12)
+QPINN_BIG_EXTERN(13)
+QPINN_BIG_EXTERN(14)
+QPINN_BIG_EXTERN(15)
+extern template int big_n<float, 16>(bool, int, const qpinn_circuit*, const KArgs<float>*);
+#undef QPINN_BIG_EXTERN
 
 template <typename T>
 int big_dispatch(bool fwd, const qpinn_circuit* c, const KArgs<T>* a) {
