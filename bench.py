@@ -231,7 +231,7 @@ def run_ours(args):
     import torch
     import torch.distributed as dist
     from paper_2506_23246_b200 import _native as N
-    from paper_2506_23246_b200.roofline import pqc_flops, trunk_bytes
+    from paper_2506_23246_b200.roofline import pqc_flops, transfer_bytes, transfer_flops, trunk_bytes
     from paper_2506_23246_b200.training import Trainer, allreduce_fn
 
     rank, world, local = dist_env()
@@ -299,8 +299,30 @@ def run_ours(args):
         R_local = tr.evaluator.n_local_points
         f_fwd, f_adj = pqc_flops(circuit)
         rl = {}
+        hbm = hbm_peak()
+        transfer = circuit.uses_transfer(dtype)
+        if transfer:  # K1/K2 as tensor-core GEMMs over HBM-staged operands
+            tb = transfer_bytes(circuit.n_qubits)
+            tf = transfer_flops(circuit.n_qubits)
+            for name, per_pt, fl in (("pqc_forward", tb[0], tf[0]), ("pqc_backward", tb[1], tf[1])):
+                if name not in kern:
+                    continue
+                nl, mean_ms = kern[name]
+                launches_per_step = nl / args.steps
+                pts_per_launch = R_local / launches_per_step
+                achieved = per_pt * pts_per_launch / (mean_ms * 1e-3) / 1e9
+                rl[name] = {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm,
+                            "unit": "GB/s", "frac": round(achieved / hbm, 4),
+                            "traffic": traffic_for(name, pts_per_launch),
+                            "bytes_per_point": per_pt, "points_per_launch": pts_per_launch,
+                            "gemm_flop_per_point": fl,
+                            "gemm_tflops": round(fl * pts_per_launch / (mean_ms * 1e-3) / 1e12, 2),
+                            "ms_per_launch": round(mean_ms, 4),
+                            "share_of_step": round(mean_ms * launches_per_step / (ms_prof / args.steps), 4),
+                            "path": "transfer matrix (3xTF32 tcgen05 GEMMs)",
+                            "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy bandwidth)"}
         for name, per_pt in (("pqc_forward", f_fwd), ("pqc_backward", f_adj)):
-            if name in kern:
+            if name in kern and not transfer:
                 nl, mean_ms = kern[name]
                 launches_per_step = nl / args.steps
                 pts_per_launch = R_local / launches_per_step
@@ -317,7 +339,6 @@ def run_ours(args):
         mc = tr.model.config
         tb_f, tb_b = trunk_bytes(mc.hidden_width, mc.rff_features, mc.n_qubits,
                                  tr.model.n_hidden, 4 if dtype == torch.float32 else 8)
-        hbm = hbm_peak()
         for name, per_pt in (("trunk_forward", tb_f), ("trunk_backward", tb_b)):
             if name in kern and hbm:
                 nl, mean_ms = kern[name]

@@ -78,25 +78,34 @@ size_t qpinn_circuit_dump(const qpinn_circuit* c, char* buf, size_t len);
 /* One line per fused step: "u1 <kind> <wire> <slots>" | "perm <p0,p1,...>" |
  * "phases <c:t:slot ...>". */
 size_t qpinn_circuit_plan_dump(const qpinn_circuit* c, char* buf, size_t len);
-/* Kernel choice for this circuit: 0 (default) uses the layer-loop K1/K2
- * (wires unrolled at compile time) when the fused plan has the uniform layer
- * shape every build_circuit ansatz has, 1 forces the generic runtime-plan
- * kernels.  Set it before the forward whose states feed a backward (the two
- * must use the same variant). */
+/* Kernel choice for this circuit: 0 (default) uses the transfer-matrix K1/K2
+ * for float32 n = 6, 7 and the layer-loop K1/K2 (wires unrolled at compile
+ * time) otherwise, when the fused plan has the uniform layer shape every
+ * build_circuit ansatz has; 1 forces the generic runtime-plan kernels; 2
+ * forces the transfer-matrix kernels (float32, 5 <= n <= 7: the circuit as
+ * one [2^(n+1), 2^(n+1)] real map applied on the tensor cores, the
+ * reference's via="matrix" formulation, ansatz.py:300-338).  Set it before
+ * the forward whose states feed a backward (the two must use the same
+ * variant). */
 int qpinn_circuit_set_kernel_variant(qpinn_circuit* c, int variant);
 /* 1 if the layer-loop kernels apply to this circuit. */
 int qpinn_circuit_specialized(const qpinn_circuit* c);
+/* 1 if forward/backward run the transfer-matrix kernels for `dtype`. */
+int qpinn_pqc_uses_transfer(const qpinn_circuit* c, int dtype);
 /* Largest n_qubits the register-resident kernels accept for `dtype`. */
 int qpinn_pqc_max_qubits(int dtype);
 
 /* ---- PQC forward + tangents (K1) and adjoint backward (K2) -------------- */
-/* Device scratch needed by forward/backward for `rows` points. */
+/* Device scratch needed by forward/backward for `rows` points (the
+ * transfer-matrix kernels stage [4 rows, 2^(n+1)] float32 operands here). */
 size_t qpinn_pqc_workspace_bytes(const qpinn_circuit* c, int dtype, int64_t rows);
 
 /* Bytes of the optional state hand-off buffer that lets the backward skip
  * re-running the circuit: 4 states x 2^n amplitudes per row at each of the L
  * layer boundaries for the layer-loop kernels (variant 0), the 4 final states
- * for the generic kernels (variant 1).  The content is opaque. */
+ * for the generic kernels (variant 1); the transfer-matrix kernels keep the
+ * final states and (L >= 2) the embedded states in it.  The content is
+ * opaque. */
 size_t qpinn_pqc_state_bytes(const qpinn_circuit* c, int dtype, int64_t rows);
 
 /* z[R,n] = <Z_q>, dz[3,R,n] = d<Z_q>/d(x,y,t) of the scaled-angle-embedded

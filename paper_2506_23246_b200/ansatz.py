@@ -168,9 +168,14 @@ class CircuitSpec:
         """Compile-time specialised K1/K2 exist for this (ansatz, n, L)."""
         return bool(N.lib().qpinn_circuit_specialized(self._h))
 
+    def uses_transfer(self, dtype) -> bool:
+        """K1/K2 run as the transfer-matrix map on the tensor cores for ``dtype``."""
+        return bool(N.lib().qpinn_pqc_uses_transfer(self._h, N.dtype_code(dtype)))
+
     def set_kernel_variant(self, variant: str) -> None:
-        """"auto" (specialised kernels when available) or "generic"."""
-        code = {"auto": 0, "generic": 1}[variant]
+        """"auto" (specialised kernels when available), "generic", or "transfer"
+        (float32, 5 <= n <= 7: the transfer-matrix map on the tensor cores)."""
+        code = {"auto": 0, "generic": 1, "transfer": 2}[variant]
         N.check(N.lib().qpinn_circuit_set_kernel_variant(self._h, code), "set_kernel_variant")
 
     def __repr__(self):

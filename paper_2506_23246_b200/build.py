@@ -16,7 +16,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libqpinn_b200.so")
 SOURCES = (["circuit.cu", "pqc.cu", "pqc_layer.cu", "pqc_layer_f64.cu", "pqc_big_dispatch.cu", "trunk.cu", "loss.cu",
-            "adam.cu", "tc_gemm.cu", "fdtd.cu", "probes.cu", "pqc_global.cu"] + [f"pqc_big_n{n}.cu" for n in range(9, 17)])
+            "adam.cu", "tc_gemm.cu", "fdtd.cu", "probes.cu", "pqc_global.cu", "pqc_transfer.cu"] + [f"pqc_big_n{n}.cu" for n in range(9, 17)])
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
          "-Xptxas", "-v"]

@@ -626,7 +626,7 @@ using namespace qpinn;
 extern "C" {
 
 int qpinn_circuit_set_kernel_variant(qpinn_circuit* c, int variant) {
-  if (!c || variant < 0 || variant > 1) return fail(QPINN_ERR_CONFIG, "bad kernel variant");
+  if (!c || variant < 0 || variant > 2) return fail(QPINN_ERR_CONFIG, "bad kernel variant");
   c->variant = variant;
   return QPINN_OK;
 }
@@ -639,14 +639,31 @@ int qpinn_pqc_max_qubits(int dtype) {
   return dtype == QPINN_F64 ? max_qubits<double>() : max_qubits<float>();
 }
 
+static size_t small_ws_bytes(const qpinn_circuit* c) {
+  return 256 + partial_bytes(c) + align_up(sizeof(double) * n_acc_of(c), 256) +
+         tables_bytes_bound(c);
+}
+
+// the transfer-matrix kernels (pqc_transfer.cu): variant 2, and the default for
+// float32 n = 6, 7 (measured, 2^16 points, L = 4, K1 + K2: n = 7 1.07 ms vs
+// 1.74 ms for the layer kernels, n = 6 0.50 vs 0.83; n = 5 is a tie)
+static bool use_transfer(const qpinn_circuit* c, int dtype) {
+  if (!transfer_supported(c, dtype)) return false;
+  return c->variant == 2 || (c->variant == 0 && c->n >= 6);
+}
+
+int qpinn_pqc_uses_transfer(const qpinn_circuit* c, int dtype) {
+  return c && use_transfer(c, dtype) ? 1 : 0;
+}
+
 size_t qpinn_pqc_workspace_bytes(const qpinn_circuit* c, int dtype, int64_t rows) {
-  (void)rows;
   if (!c) return 0;
   if (c->n > qpinn_pqc_max_qubits(dtype))
     return align_up(big_workspace_bytes(c, dtype), 256) +
            global_adjoint_workspace_bytes(c, dtype);
-  return 256 + partial_bytes(c) + align_up(sizeof(double) * n_acc_of(c), 256) +
-         tables_bytes_bound(c);
+  size_t b = small_ws_bytes(c);
+  if (transfer_supported(c, dtype)) b += transfer_workspace_bytes(c, rows);
+  return b;
 }
 
 size_t qpinn_pqc_state_bytes(const qpinn_circuit* c, int dtype, int64_t rows) {
@@ -718,6 +735,13 @@ int qpinn_pqc_forward(const qpinn_circuit* cc, int dtype, int scale, int64_t row
   unsigned char* tables = (unsigned char*)workspace + 256 + partial_bytes(c) +
                           align_up(sizeof(double) * n_acc_of(c), 256);
   if (rows == 0) return QPINN_OK;
+  if (use_transfer(c, dtype)) {
+    KArgs<float> a{scale, rows, (const float*)act_val, (const float*)act_tan,
+                   (const float*)qparams, (float*)z, (float*)dz, states, maxabs, nullptr,
+                   nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, st, nullptr};
+    const size_t off = small_ws_bytes(c);
+    return transfer_forward(c, &a, (unsigned char*)workspace + off, workspace_bytes - off);
+  }
   if (c->variant == 0) {  // layer-loop kernels for every standard plan
     if (dtype == QPINN_F32) {
       KArgs<float> a{scale, rows, (const float*)act_val, (const float*)act_tan,
@@ -808,6 +832,14 @@ int qpinn_pqc_backward(const qpinn_circuit* cc, int dtype, int scale, int64_t ro
     QPINN_CUDA_CHECK(cudaMemsetAsync(g_qparams, 0,
                                      (dtype == QPINN_F64 ? 8 : 4) * (size_t)c->n_params, st));
     return QPINN_OK;
+  }
+  if (use_transfer(c, dtype)) {
+    KArgs<float> a{scale, rows, (const float*)act_val, (const float*)act_tan,
+                   (const float*)qparams, nullptr, nullptr, const_cast<void*>(states), nullptr,
+                   (const float*)g_z, (const float*)g_dz, (float*)g_act_val, (float*)g_act_tan,
+                   (float*)g_qparams, nullptr, nullptr, st, nullptr};
+    const size_t off = small_ws_bytes(c);
+    return transfer_backward(c, &a, (unsigned char*)workspace + off, workspace_bytes - off);
   }
   if (c->variant == 0) {
     if (dtype == QPINN_F32) {

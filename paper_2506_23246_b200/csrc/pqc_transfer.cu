@@ -1,0 +1,696 @@
+// K1 / K2 as tensor-core GEMMs: the transfer-matrix formulation of the PQC.
+//
+// The circuit after the embedding is one fixed unitary per step, so the
+// reference's default path (quantum_layer_forward via="matrix",
+// ansatz.py:300-338) builds its transfer matrix once and maps every embedded
+// state through it.  Here that matrix is built on the device by running the
+// circuit on the D basis states (one CTA per basis row), and the map itself
+// is a real GEMM on the tcgen05 tensor cores (3xTF32, tc_gemm.cu):
+//
+//   rows of B:   B[j] = circuit(e_j)                     (complex [D][D])
+//   W          = [[Br, Bi], [-Bi, Br]]                    (real [2D][2D])
+//   Psi        = Phi W       with Phi = [Re phi | Im phi] per state row,
+//                [4R][2D]    rows s R + p (s = 0: phi, 1..3: d phi/dx,y,t)
+//
+// For n = 7 that is 2 (4 8 D^2) flops per point instead of the gate-by-gate
+// 2.4e5, but at tensor-core rate.  The backward is the GEMM's backward:
+//   Abar  = seeds(Psi, dL/dz, dL/ddz)                     (qpinn_oracle.pqc_backward)
+//   gPhi  = Abar W^T  -> the embedding gradient, per point
+//   gW    = Phi^T Abar (deterministic split-K)  -> adjoint of the rows of B
+//   the circuit's adjoint on the D basis rows (one CTA per row, checkpointed
+//   at the layer boundaries like K2) -> the gate-space sums -> dL/dqparams.
+// Float32 only (the GEMM is 3xTF32); chosen for 5 <= n <= 7, where the dense
+// map costs at most 2 D / (n L) times the gate-by-gate flops.
+#include "pqc_layer.h"
+#include "tc_gemm.h"
+
+namespace qpinn {
+
+namespace {
+
+constexpr int kTrThreads = 64;  // circuit kernels: one thread per amplitude pair (D <= 128)
+
+// u1 matrices [n_u1][4] and phase diagonals [n_phase][D] (as gb_tables, pqc_global.cu)
+__global__ void tr_tables(PlanDev p, const float* __restrict__ qp, cplx<float>* __restrict__ U,
+                          cplx<float>* __restrict__ ph) {
+  const int D = 1 << p.n;
+  const int tid = blockIdx.x * blockDim.x + threadIdx.x, nt = gridDim.x * blockDim.x;
+  for (int i = tid; i < p.n_u1; i += nt) {
+    const int kind = p.u1[i * 4];
+    double th[3] = {0, 0, 0};
+    for (int j = 0; j < u1_nslots(kind); ++j) th[j] = (double)qp[p.u1[i * 4 + 1 + j]];
+    double M[8];
+    u1_matrix_d(kind, th, M);
+    for (int e = 0; e < 4; ++e) U[i * 4 + e] = {float(M[2 * e]), float(M[2 * e + 1])};
+  }
+  for (int i = tid; i < p.n_phase * D; i += nt) {
+    const int st = i / D, b = i % D;
+    double phi = 0.0;
+    for (int k = p.phase_off[st]; k < p.phase_off[st + 1]; ++k) {
+      const int c = p.pairs[3 * k], t = p.pairs[3 * k + 1], s = p.pairs[3 * k + 2];
+      const int on = (b >> (p.n - 1 - c)) & 1, tb = (b >> (p.n - 1 - t)) & 1;
+      phi += on * (tb - 0.5) * (double)qp[s];  // qsim.py:212-225
+    }
+    double sp, cp;
+    sincos(phi, &sp, &cp);
+    ph[i] = {float(cp), float(sp)};
+  }
+}
+
+__device__ __forceinline__ void pair_index(int k, int pos, int& i0, int& i1) {
+  i0 = ((k >> pos) << (pos + 1)) | (k & ((1 << pos) - 1));
+  i1 = i0 | (1 << pos);
+}
+
+// B[j] = circuit(e_j); CK[l][j] = the state after layer l's single-qubit gates
+__global__ void __launch_bounds__(kTrThreads) tr_circuit_fwd(
+    int n, int L, int ent, const cplx<float>* __restrict__ U, const cplx<float>* __restrict__ ph,
+    const uint16_t* __restrict__ perm, cplx<float>* __restrict__ B, cplx<float>* __restrict__ CK) {
+  __shared__ cplx<float> s[2][128];
+  const int D = 1 << n, j = blockIdx.x, t = threadIdx.x;
+  int cur = 0;
+  for (int b = t; b < D; b += kTrThreads) s[0][b] = {b == j ? 1.f : 0.f, 0.f};
+  __syncthreads();
+  for (int l = 0; l < L; ++l) {
+    for (int q = 0; q < n; ++q) {
+      const cplx<float>* u = U + 4 * (l * n + q);
+      for (int k = t; k < D / 2; k += kTrThreads) {
+        int i0, i1;
+        pair_index(k, n - 1 - q, i0, i1);
+        const cplx<float> a = s[cur][i0], c = s[cur][i1];
+        s[cur][i0] = cmul2(u[0], a, u[1], c);
+        s[cur][i1] = cmul2(u[2], a, u[3], c);
+      }
+      __syncthreads();
+    }
+    if (CK)
+      for (int b = t; b < D; b += kTrThreads) CK[((size_t)l * D + j) * D + b] = s[cur][b];
+    if (ent == ENT_PERM) {
+      for (int b = t; b < D; b += kTrThreads) s[cur ^ 1][b] = s[cur][perm[l * D + b]];
+      cur ^= 1;
+    } else if (ent == ENT_PHASE) {
+      for (int b = t; b < D; b += kTrThreads) s[cur][b] = cmul(s[cur][b], ph[l * D + b]);
+    }
+    __syncthreads();
+  }
+  for (int b = t; b < D; b += kTrThreads) B[(size_t)j * D + b] = s[cur][b];
+}
+
+template <int NV>
+__device__ __forceinline__ void block_sum(double (&v)[NV], double* red /* [2][NV] */) {
+#pragma unroll
+  for (int e = 0; e < NV; ++e)
+    for (int m = 16; m >= 1; m >>= 1) v[e] += __shfl_xor_sync(0xffffffffu, v[e], m);
+  const int w = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0)
+    for (int e = 0; e < NV; ++e) red[w * NV + e] = v[e];
+  __syncthreads();
+  for (int e = 0; e < NV; ++e) v[e] = red[e] + red[NV + e];  // fixed order: warp 0 + warp 1
+  __syncthreads();
+}
+
+// reverse sweep for basis row j from the adjoint of B[j]: per gate the 2x2
+// post-gate outer product M'_ab = sum conj(abar_a) x_b (gates of one layer
+// commute, so each is the layer's last), per phase layer Im(conj(abar) x');
+// per-row partials, reduced over rows in fixed order by tr_reduce
+__global__ void __launch_bounds__(kTrThreads) tr_circuit_bwd(
+    int n, int L, int ent, const cplx<float>* __restrict__ U, const cplx<float>* __restrict__ ph,
+    const uint16_t* __restrict__ iperm, const cplx<float>* __restrict__ Abar,
+    const cplx<float>* __restrict__ CK, double* __restrict__ part_u1,
+    double* __restrict__ part_ph) {
+  __shared__ cplx<float> s[2][128];
+  __shared__ double red[2 * 8];
+  const int D = 1 << n, j = blockIdx.x, t = threadIdx.x, n_u1 = n * L;
+  int cur = 0;
+  for (int b = t; b < D; b += kTrThreads) s[0][b] = Abar[(size_t)j * D + b];
+  __syncthreads();
+  for (int l = L - 1; l >= 0; --l) {
+    const cplx<float>* xl = CK + ((size_t)l * D + j) * D;
+    if (ent == ENT_PERM) {
+      for (int b = t; b < D; b += kTrThreads) s[cur ^ 1][b] = s[cur][iperm[l * D + b]];
+      cur ^= 1;
+      __syncthreads();
+    } else if (ent == ENT_PHASE) {
+      for (int b = t; b < D; b += kTrThreads) {
+        const cplx<float> e = ph[l * D + b], xp = cmul(xl[b], e), a = s[cur][b];
+        part_ph[((size_t)j * L + l) * D + b] = (double)(a.im * xp.re - a.re * xp.im);
+        s[cur][b] = cmul(a, cplx<float>{e.re, -e.im});
+      }
+      __syncthreads();
+    }
+    for (int q = 0; q < n; ++q) {
+      double m[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+      for (int k = t; k < D / 2; k += kTrThreads) {
+        int i0, i1;
+        pair_index(k, n - 1 - q, i0, i1);
+        const cplx<float> x0 = xl[i0], x1 = xl[i1], a0 = s[cur][i0], a1 = s[cur][i1];
+        float f[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        cmac_c(f[0], f[1], a0, x0);
+        cmac_c(f[2], f[3], a0, x1);
+        cmac_c(f[4], f[5], a1, x0);
+        cmac_c(f[6], f[7], a1, x1);
+        for (int e = 0; e < 8; ++e) m[e] += (double)f[e];
+      }
+      block_sum<8>(m, red);
+      if (t < 8) part_u1[((size_t)j * n_u1 + l * n + q) * 8 + t] = m[t];
+    }
+    for (int q = 0; q < n; ++q) {
+      const cplx<float>* u = U + 4 * (l * n + q);
+      const cplx<float> d00 = {u[0].re, -u[0].im}, d01 = {u[2].re, -u[2].im},
+                        d10 = {u[1].re, -u[1].im}, d11 = {u[3].re, -u[3].im};
+      for (int k = t; k < D / 2; k += kTrThreads) {
+        int i0, i1;
+        pair_index(k, n - 1 - q, i0, i1);
+        const cplx<float> a = s[cur][i0], c = s[cur][i1];
+        s[cur][i0] = cmul2(d00, a, d01, c);
+        s[cur][i1] = cmul2(d10, a, d11, c);
+      }
+      __syncthreads();
+    }
+  }
+}
+
+// acc[i] = sum over the D basis rows of the partials, in row order
+__global__ void tr_reduce(int D, int n_u1, int n_ph, const double* __restrict__ part_u1,
+                          const double* __restrict__ part_ph, double* __restrict__ acc) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < 8 * n_u1) {
+    double v = 0.0;
+    for (int j = 0; j < D; ++j) v += part_u1[(size_t)j * 8 * n_u1 + i];
+    acc[i] = v;
+  } else if (i < 8 * n_u1 + n_ph) {
+    const int k = i - 8 * n_u1;
+    double v = 0.0;
+    for (int j = 0; j < D; ++j) v += part_ph[(size_t)j * n_ph + k];
+    acc[i] = v;
+  }
+}
+
+// Wt [2D][2D] = W^T (forward GEMM operand) and W (backward operand)
+__global__ void tr_wmat(int n, const cplx<float>* __restrict__ B, float* __restrict__ W,
+                        float* __restrict__ Wt) {
+  const int D = 1 << n, D2 = 2 * D;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < D2 * D2; i += gridDim.x * blockDim.x) {
+    const int r = i / D2, c = i % D2;  // W[r][c]
+    const cplx<float> b = B[(size_t)(r % D) * D + (c % D)];
+    const bool rlo = r < D, clo = c < D;
+    const float v = rlo == clo ? b.re : rlo ? b.im : -b.im;
+    W[i] = v;
+    Wt[(size_t)c * D2 + r] = v;
+  }
+}
+
+// complex adjoint of the rows of B from dL/dW: dL/dBr = gW11 + gW22, dL/dBi = gW12 - gW21
+__global__ void tr_gb(int n, const float* __restrict__ gW, cplx<float>* __restrict__ Ab) {
+  const int D = 1 << n, D2 = 2 * D;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < D * D; i += gridDim.x * blockDim.x) {
+    const int j = i / D, k = i % D;
+    Ab[i] = {gW[(size_t)j * D2 + k] + gW[(size_t)(D + j) * D2 + D + k],
+             gW[(size_t)j * D2 + D + k] - gW[(size_t)(D + j) * D2 + k]};
+  }
+}
+
+// ---- per-point kernels: 8 warps per block, kPB points per block iteration ----
+// The per-qubit angle data of a block's points is staged once into shared
+// memory with coalesced loads (one DRAM round trip per kPB points); each warp
+// then owns one point at a time, lane l holding the amplitudes b = l + 32 j.
+constexpr int kPB = 64;
+constexpr int kAng = 10;  // c, s, s1, dth_x, dth_y, dth_z, s2 tan_x, s2 tan_y, s2 tan_z, -
+
+template <int NQ>
+__device__ __forceinline__ void stage_angles(int scale, int64_t R, int64_t p0,
+                                             const float* __restrict__ act,
+                                             const float* __restrict__ tan, float* ang,
+                                             float& amax) {
+  for (int i = threadIdx.x; i < kPB * NQ; i += blockDim.x) {
+    const int64_t p = p0 + i / NQ;
+    const int q = i % NQ;
+    float c = 1.f, sn = 0.f, s1 = 0.f, s2 = 0.f, tv[3] = {0.f, 0.f, 0.f};
+    if (p < R) {
+      float a = act[p * NQ + q];
+      amax = fmaxf(amax, fabsf(a));
+      a = fminf(fmaxf(a, -1.f), 1.f);
+      half_angle<float>(scale, a, c, sn, s1, s2);
+      if (tan)
+        for (int k = 0; k < 3; ++k) tv[k] = tan[((int64_t)k * R + p) * NQ + q];
+    }
+    float* o = ang + i * kAng;
+    o[0] = c;
+    o[1] = sn;
+    o[2] = s1;
+    for (int k = 0; k < 3; ++k) {
+      o[3 + k] = s1 * tv[k];
+      o[6 + k] = s2 * tv[k];
+    }
+  }
+}
+
+template <int NQ>
+struct PointAngles {
+  float c[NQ], s[NQ], d[3][NQ];
+};
+
+template <int NQ>
+__device__ __forceinline__ void read_angles(const float* ang, PointAngles<NQ>& pa) {
+#pragma unroll
+  for (int q = 0; q < NQ; ++q) {
+    pa.c[q] = ang[q * kAng];
+    pa.s[q] = ang[q * kAng + 1];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) pa.d[k][q] = ang[q * kAng + 3 + k];
+  }
+}
+
+// embedded amplitude of basis state b and its x/y/t tangents (ansatz.py:233-243,
+// :380-390; wire q is bit NQ-1-q), before the (-i)^popcount phase
+template <int NQ>
+__device__ __forceinline__ void embed_amp(const PointAngles<NQ>& pa, int b, bool tangents,
+                                          float& m0, float (&mk)[3]) {
+  float pre[NQ + 1];
+  pre[0] = 1.f;
+#pragma unroll
+  for (int q = 0; q < NQ; ++q) pre[q + 1] = pre[q] * (((b >> (NQ - 1 - q)) & 1) ? pa.s[q] : pa.c[q]);
+  m0 = pre[NQ];
+  mk[0] = mk[1] = mk[2] = 0.f;
+  if (!tangents) return;
+  float suf = 1.f;
+#pragma unroll
+  for (int q = NQ - 1; q >= 0; --q) {
+    const bool bit = (b >> (NQ - 1 - q)) & 1;
+    const float df = bit ? 0.5f * pa.c[q] : -0.5f * pa.s[q];
+    const float rest = pre[q] * suf;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) mk[k] += pa.d[k][q] * df * rest;
+    suf *= bit ? pa.s[q] : pa.c[q];
+  }
+}
+
+__device__ __forceinline__ void put_phase(float m, int b, float& re, float& im) {
+  const int ph = __popc(b) & 3;  // (-i)^popcount
+  re = ph == 0 ? m : ph == 2 ? -m : 0.f;
+  im = ph == 1 ? -m : ph == 3 ? m : 0.f;
+}
+
+// lane l ends with the warp total of value index l (recursive halving, 31 shuffles)
+__device__ __forceinline__ void reduce_scatter32(float (&v)[32]) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int m = 16; m >= 1; m >>= 1) {
+    const bool up = lane & m;
+#pragma unroll
+    for (int i = 0; i < m; ++i) {
+      const float send = up ? v[i] : v[i + m];
+      const float keep = up ? v[i + m] : v[i];
+      v[i] = keep + __shfl_xor_sync(0xffffffffu, send, m);
+    }
+  }
+}
+
+template <typename F>
+__device__ __forceinline__ void for_points(int64_t R, F&& body) {
+  // block iteration over kPB-point groups; warp w takes points w, w + 8, ...
+  for (int64_t p0 = (int64_t)blockIdx.x * kPB; p0 < R; p0 += (int64_t)gridDim.x * kPB)
+    body(p0);
+}
+
+// Phi rows: [Re | Im] of the embedded state and its tangents
+template <int NQ>
+__global__ void __launch_bounds__(256) tr_embed(int scale, int64_t R, const float* __restrict__ act,
+                                                const float* __restrict__ tan,
+                                                float* __restrict__ Phi,
+                                                unsigned long long* __restrict__ maxabs) {
+  constexpr int D = 1 << NQ, D2 = 2 * D;
+  __shared__ float ang[kPB * NQ * kAng];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  float amax = 0.f;
+  for_points(R, [&](int64_t p0) {
+    stage_angles<NQ>(scale, R, p0, act, tan, ang, amax);
+    __syncthreads();
+    for (int pl = w; pl < kPB && p0 + pl < R; pl += 8) {
+      const int64_t p = p0 + pl;
+      PointAngles<NQ> pa;
+      read_angles<NQ>(ang + pl * NQ * kAng, pa);
+#pragma unroll
+      for (int b = lane; b < D; b += 32) {
+        float m0, mk[3];
+        embed_amp<NQ>(pa, b, tan != nullptr, m0, mk);
+        float re, im;
+        put_phase(m0, b, re, im);
+        Phi[p * D2 + b] = re;
+        Phi[p * D2 + D + b] = im;
+        if (tan)
+          for (int k = 0; k < 3; ++k) {
+            put_phase(mk[k], b, re, im);
+            float* row = Phi + ((int64_t)(k + 1) * R + p) * D2;
+            row[b] = re;
+            row[D + b] = im;
+          }
+      }
+    }
+    __syncthreads();
+  });
+  if (maxabs) {
+    for (int m = 16; m >= 1; m >>= 1) amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, m));
+    if (lane == 0) atomic_max_abs(maxabs, amax);
+  }
+}
+
+// z_q = sum_b |psi_b|^2 s_bq, dz_kq = sum_b 2 Re(conj(psi_b) dpsi_kb) s_bq (qsim.py:369-381)
+template <int NQ>
+__global__ void __launch_bounds__(256) tr_readout(int64_t R, int ns, const float* __restrict__ Psi,
+                                                  float* __restrict__ z, float* __restrict__ dz) {
+  constexpr int D = 1 << NQ, D2 = 2 * D;
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t p = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; p < R; p += nw) {
+    float acc[32];
+#pragma unroll
+    for (int e = 0; e < 32; ++e) acc[e] = 0.f;
+#pragma unroll
+    for (int b = lane; b < D; b += 32) {
+      const float pr = Psi[p * D2 + b], pi = Psi[p * D2 + D + b];
+      float v[4];
+      v[0] = pr * pr + pi * pi;
+#pragma unroll
+      for (int k = 1; k < 4; ++k) {
+        if (k < ns) {
+          const float* row = Psi + ((int64_t)k * R + p) * D2;
+          v[k] = 2.f * (pr * row[b] + pi * row[D + b]);
+        } else {
+          v[k] = 0.f;
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) {
+        const bool neg = (b >> (NQ - 1 - q)) & 1;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) acc[k * NQ + q] += neg ? -v[k] : v[k];
+      }
+    }
+    reduce_scatter32(acc);
+    const int k = lane / NQ, q = lane % NQ;
+    if (k == 0) z[p * NQ + q] = acc[0];
+    else if (k < ns) dz[((int64_t)(k - 1) * R + p) * NQ + q] = acc[0];
+  }
+}
+
+// adjoint seeds as real-block rows:
+// lambda = 2 w psi + 2 sum_k v_k dpsi_k, mu_k = 2 v_k psi
+template <int NQ>
+__global__ void __launch_bounds__(256) tr_seed(int64_t R, const float* __restrict__ gz,
+                                               const float* __restrict__ gdz,
+                                               const float* __restrict__ Psi,
+                                               float* __restrict__ Abar) {
+  constexpr int D = 1 << NQ, D2 = 2 * D;
+  __shared__ float sg[kPB][4][NQ];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for_points(R, [&](int64_t p0) {
+    for (int i = threadIdx.x; i < kPB * NQ; i += blockDim.x) {
+      const int64_t p = p0 + i / NQ;
+      const int q = i % NQ;
+      const bool ok = p < R;
+      sg[i / NQ][0][q] = ok ? gz[p * NQ + q] : 0.f;
+      for (int k = 0; k < 3; ++k) sg[i / NQ][k + 1][q] = ok ? gdz[((int64_t)k * R + p) * NQ + q] : 0.f;
+    }
+    __syncthreads();
+    for (int pl = w; pl < kPB && p0 + pl < R; pl += 8) {
+      const int64_t p = p0 + pl;
+#pragma unroll
+      for (int b = lane; b < D; b += 32) {
+        float wv[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) {
+          const bool neg = (b >> (NQ - 1 - q)) & 1;
+#pragma unroll
+          for (int k = 0; k < 4; ++k) wv[k] += neg ? -sg[pl][k][q] : sg[pl][k][q];
+        }
+        const float pr = Psi[p * D2 + b], pi = Psi[p * D2 + D + b];
+        float lr = 2.f * wv[0] * pr, li = 2.f * wv[0] * pi;
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+          const float* row = Psi + ((int64_t)(k + 1) * R + p) * D2;
+          lr += 2.f * wv[k + 1] * row[b];
+          li += 2.f * wv[k + 1] * row[D + b];
+          float* o = Abar + ((int64_t)(k + 1) * R + p) * D2;
+          o[b] = 2.f * wv[k + 1] * pr;
+          o[D + b] = 2.f * wv[k + 1] * pi;
+        }
+        Abar[p * D2 + b] = lr;
+        Abar[p * D2 + D + b] = li;
+      }
+    }
+    __syncthreads();
+  });
+}
+
+// value of register j at the partner index b ^ bit(q) (lane bits: shuffle; j bits: register)
+template <int NQ, int J>
+__device__ __forceinline__ float flip_get(const float (&v)[J], int j, int q) {
+  const int pos = NQ - 1 - q;
+  if (pos < 5) return __shfl_xor_sync(0xffffffffu, v[j], 1 << pos);
+  return v[j ^ (1 << (pos - 5))];
+}
+
+// embedding gradient (qpinn_oracle.pqc_backward):
+//   eta = (i/2) phibar - 1/4 sum_q X_q nu_q,  nu_q = sum_k dth_kq mu_k
+//   g_th[q] = Re sum conj(eta) X_q phi, g_dth[k][q] = Re sum conj((i/2) mu_k) X_q phi
+// phibar, mu_k = rows of gPhi; phi is re-embedded in registers
+template <int NQ>
+__global__ void __launch_bounds__(256) tr_embed_grad(int scale, int64_t R,
+                                                     const float* __restrict__ act,
+                                                     const float* __restrict__ tan,
+                                                     const float* __restrict__ gPhi,
+                                                     float* __restrict__ g_act,
+                                                     float* __restrict__ g_tan) {
+  constexpr int D = 1 << NQ, D2 = 2 * D, J = D / 32;
+  __shared__ float ang[kPB * NQ * kAng];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  float amax = 0.f;
+  for_points(R, [&](int64_t p0) {
+    stage_angles<NQ>(scale, R, p0, act, tan, ang, amax);
+    __syncthreads();
+    for (int pl = w; pl < kPB && p0 + pl < R; pl += 8) {
+      const int64_t p = p0 + pl;
+      const float* pang = ang + pl * NQ * kAng;
+      PointAngles<NQ> pa;
+      read_angles<NQ>(pang, pa);
+      float fr[J], fi[J], er[J], ei[J], mr[3][J], mi[3][J];
+#pragma unroll
+      for (int j = 0; j < J; ++j) {
+        const int b = lane + 32 * j;
+        float m0, mk[3];
+        embed_amp<NQ>(pa, b, false, m0, mk);
+        put_phase(m0, b, fr[j], fi[j]);
+        er[j] = -0.5f * gPhi[p * D2 + D + b];  // (i/2) phibar
+        ei[j] = 0.5f * gPhi[p * D2 + b];
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+          const float* row = gPhi + ((int64_t)(k + 1) * R + p) * D2;
+          mr[k][j] = row[b];
+          mi[k][j] = row[D + b];
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) {
+        float nr[J], ni[J];
+#pragma unroll
+        for (int j = 0; j < J; ++j) {
+          nr[j] = pa.d[0][q] * mr[0][j] + pa.d[1][q] * mr[1][j] + pa.d[2][q] * mr[2][j];
+          ni[j] = pa.d[0][q] * mi[0][j] + pa.d[1][q] * mi[1][j] + pa.d[2][q] * mi[2][j];
+        }
+#pragma unroll
+        for (int j = 0; j < J; ++j) {
+          er[j] -= 0.25f * flip_get<NQ, J>(nr, j, q);
+          ei[j] -= 0.25f * flip_get<NQ, J>(ni, j, q);
+        }
+      }
+      float acc[32];
+#pragma unroll
+      for (int e = 0; e < 32; ++e) acc[e] = 0.f;
+#pragma unroll
+      for (int q = 0; q < NQ; ++q) {
+#pragma unroll
+        for (int j = 0; j < J; ++j) {
+          const float yr = flip_get<NQ, J>(fr, j, q), yi = flip_get<NQ, J>(fi, j, q);
+          acc[q] += er[j] * yr + ei[j] * yi;
+#pragma unroll
+          for (int k = 0; k < 3; ++k) acc[NQ + k * NQ + q] += -0.5f * mi[k][j] * yr + 0.5f * mr[k][j] * yi;
+        }
+      }
+      reduce_scatter32(acc);
+      // lane l holds value l: g_th[q] on lanes 0..NQ-1, g_dth[k][q] on NQ + k NQ + q
+      const int q = lane < NQ ? lane : 0;
+      float gd[3];
+#pragma unroll
+      for (int k = 0; k < 3; ++k) gd[k] = __shfl_sync(0xffffffffu, acc[0], NQ + k * NQ + q);
+      if (lane < NQ) {
+        const float* a = pang + q * kAng;
+        float ga = acc[0] * a[2];
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+          ga += gd[k] * a[6 + k];
+          g_tan[((int64_t)k * R + p) * NQ + q] = gd[k] * a[2];
+        }
+        g_act[p * NQ + q] = ga;
+      }
+    }
+    __syncthreads();
+  });
+}
+
+struct TrLayout {
+  size_t U, ph, B, CK, Ab, W, Wt, gW, pu, pp, acc, g3, wg, BUF1, BUF2, total;
+};
+
+TrLayout tr_layout(const qpinn_circuit* c, int64_t R) {
+  const size_t D = (size_t)1 << c->n, D2 = 2 * D, cs = sizeof(cplx<float>);
+  TrLayout t{};
+  size_t o = 0;
+  auto take = [&](size_t bytes) {
+    const size_t at = o;
+    o += align_up(bytes, 256);
+    return at;
+  };
+  t.U = take(cs * 4 * c->n_u1);
+  t.ph = take(cs * D * c->n_phase);
+  t.B = take(cs * D * D);
+  t.CK = take(cs * D * D * c->L);
+  t.Ab = take(cs * D * D);
+  t.W = take(4 * D2 * D2);
+  t.Wt = take(4 * D2 * D2);
+  t.gW = take(4 * D2 * D2);
+  t.pu = take(8 * D * 8 * (size_t)c->n_u1);
+  t.pp = take(8 * D * D * c->n_phase);
+  t.acc = take(8 * (8 * (size_t)c->n_u1 + D * c->n_phase));
+  t.g3 = take(tc::gemm3_workspace_bytes((int)D2, (int)D2));
+  t.wg = take(tc::wgrad_workspace_bytes(4 * R, (int)D2, (int)D2));
+  t.BUF1 = take(4 * (size_t)R * D2 * 4);
+  t.BUF2 = take(4 * (size_t)R * D2 * 4);
+  t.total = o;
+  return t;
+}
+
+int grid_points(int64_t R) {  // 8 warps per block, kPB points per block iteration
+  const int64_t b = (R + kPB - 1) / kPB, cap = (int64_t)num_sms() * 8;
+  return (int)(b < 1 ? 1 : b > cap ? cap : b);
+}
+
+// B (and the layer checkpoints) on the device, then W / W^T
+int build_transfer(const qpinn_circuit* c, const float* qp, unsigned char* ws, const TrLayout& t,
+                   bool checkpoints, cudaStream_t st) {
+  const PlanDev& p = c->dev;
+  const int n = c->n, D = 1 << n;
+  const int ent = layer_entangler(c);
+  auto* U = (cplx<float>*)(ws + t.U);
+  auto* ph = (cplx<float>*)(ws + t.ph);
+  auto* B = (cplx<float>*)(ws + t.B);
+  tr_tables<<<32, 256, 0, st>>>(p, qp, U, ph);
+  tr_circuit_fwd<<<D, kTrThreads, 0, st>>>(n, c->L, ent, U, ph, p.perm, B,
+                                           checkpoints ? (cplx<float>*)(ws + t.CK) : nullptr);
+  tr_wmat<<<(4 * D * D + 255) / 256, 256, 0, st>>>(n, B, (float*)(ws + t.W), (float*)(ws + t.Wt));
+  QPINN_CUDA_CHECK(cudaGetLastError());
+  return QPINN_OK;
+}
+
+template <int NQ>
+int fwd_n(const qpinn_circuit* c, const KArgs<float>* a, unsigned char* ws, const TrLayout& t) {
+  constexpr int D2 = 2 << NQ;
+  cudaStream_t st = a->stream;
+  if (int rc = build_transfer(c, a->qp, ws, t, false, st)) return rc;
+  // hand-off: Psi, then (L >= 2: the buffer holds L state sets) Phi for the weight gradient
+  auto* Psi = a->states ? (float*)a->states : (float*)(ws + t.BUF2);
+  auto* Phi = a->states && a->tan && c->L >= 2 ? (float*)a->states + 4 * a->R * D2
+                                               : (float*)(ws + t.BUF1);
+  const int ns = a->tan ? 4 : 1;
+  tr_embed<NQ><<<grid_points(a->R), 256, 0, st>>>(a->scale, a->R, a->act, a->tan, Phi, a->maxabs);
+  QPINN_CUDA_CHECK(cudaGetLastError());
+  if (int rc = tc::gemm3(ns * a->R, D2, D2, Phi, D2, (const float*)(ws + t.Wt), D2, Psi, D2,
+                         ws + t.g3, tc::gemm3_workspace_bytes(D2, D2), st))
+    return rc;
+  tr_readout<NQ><<<grid_points(a->R), 256, 0, st>>>(a->R, ns, Psi, a->z, a->dz);
+  QPINN_CUDA_CHECK(cudaGetLastError());
+  return QPINN_OK;
+}
+
+template <int NQ>
+int bwd_n(const qpinn_circuit* c, const KArgs<float>* a, unsigned char* ws, const TrLayout& t) {
+  constexpr int D = 1 << NQ, D2 = 2 * D;
+  cudaStream_t st = a->stream;
+  const PlanDev& p = c->dev;
+  const int ent = layer_entangler(c), L = c->L, n_u1 = c->n_u1;
+  if (int rc = build_transfer(c, a->qp, ws, t, true, st)) return rc;
+  auto* Abar = (float*)(ws + t.BUF1);
+  auto* G = (float*)(ws + t.BUF2);
+  const int gp = grid_points(a->R);
+  const float* Psi = (const float*)a->states;
+  if (!Psi) {  // no hand-off: replay the forward map into BUF2
+    tr_embed<NQ><<<gp, 256, 0, st>>>(a->scale, a->R, a->act, a->tan, Abar, nullptr);
+    QPINN_CUDA_CHECK(cudaGetLastError());
+    if (int rc = tc::gemm3(4 * a->R, D2, D2, Abar, D2, (const float*)(ws + t.Wt), D2, G, D2,
+                           ws + t.g3, tc::gemm3_workspace_bytes(D2, D2), st))
+      return rc;
+    Psi = G;
+  }
+  tr_seed<NQ><<<gp, 256, 0, st>>>(a->R, a->gz, a->gdz, Psi, Abar);
+  QPINN_CUDA_CHECK(cudaGetLastError());
+  // gPhi = Abar W^T
+  if (int rc = tc::gemm3(4 * a->R, D2, D2, Abar, D2, (const float*)(ws + t.W), D2, G, D2,
+                         ws + t.g3, tc::gemm3_workspace_bytes(D2, D2), st))
+    return rc;
+  tr_embed_grad<NQ><<<gp, 256, 0, st>>>(a->scale, a->R, a->act, a->tan, G, a->g_act, a->g_tan);
+  // gW = Phi^T Abar (Phi from the hand-off, else re-embedded over gPhi)
+  const float* Phi = a->states && c->L >= 2 ? (const float*)a->states + 4 * a->R * D2 : G;
+  if (Phi == G) tr_embed<NQ><<<gp, 256, 0, st>>>(a->scale, a->R, a->act, a->tan, G, nullptr);
+  QPINN_CUDA_CHECK(cudaGetLastError());
+  if (int rc = tc::wgrad(4 * a->R, D2, D2, Phi, D2, Abar, D2, (float*)(ws + t.gW), ws + t.wg,
+                         tc::wgrad_workspace_bytes(4 * a->R, D2, D2), st))
+    return rc;
+  auto* Ab = (cplx<float>*)(ws + t.Ab);
+  tr_gb<<<(D * D + 255) / 256, 256, 0, st>>>(NQ, (const float*)(ws + t.gW), Ab);
+  auto* pu = (double*)(ws + t.pu);
+  auto* pp = (double*)(ws + t.pp);
+  auto* acc = (double*)(ws + t.acc);
+  tr_circuit_bwd<<<D, kTrThreads, 0, st>>>(NQ, L, ent, (const cplx<float>*)(ws + t.U),
+                                           (const cplx<float>*)(ws + t.ph), p.iperm, Ab,
+                                           (const cplx<float>*)(ws + t.CK), pu, pp);
+  const int n_ph = D * c->n_phase, n_acc = 8 * n_u1 + n_ph;
+  tr_reduce<<<(n_acc + 127) / 128, 128, 0, st>>>(D, n_u1, n_ph, pu, pp, acc);
+  QPINN_CUDA_CHECK(cudaGetLastError());
+  return pqc_param_grads<float>(c, acc, NQ, a->qp, a->g_qp, st);
+}
+
+}  // namespace
+
+bool transfer_supported(const qpinn_circuit* c, int dtype) {
+  return c && dtype == QPINN_F32 && c->n >= 5 && c->n <= 7 && layer_entangler(c) >= 0;
+}
+
+size_t transfer_workspace_bytes(const qpinn_circuit* c, int64_t R) {
+  return tr_layout(c, R < 1 ? 1 : R).total;
+}
+
+int transfer_forward(const qpinn_circuit* c, const KArgs<float>* a, unsigned char* ws,
+                     size_t bytes) {
+  const TrLayout t = tr_layout(c, a->R);
+  if (bytes < t.total) return fail(QPINN_ERR_CONFIG, "transfer PQC: workspace too small");
+  switch (c->n) {
+    case 5: return fwd_n<5>(c, a, ws, t);
+    case 6: return fwd_n<6>(c, a, ws, t);
+    case 7: return fwd_n<7>(c, a, ws, t);
+    default: return fail(QPINN_ERR_CAPACITY, "transfer PQC covers 5 <= n <= 7");
+  }
+}
+
+int transfer_backward(const qpinn_circuit* c, const KArgs<float>* a, unsigned char* ws,
+                      size_t bytes) {
+  const TrLayout t = tr_layout(c, a->R);
+  if (bytes < t.total) return fail(QPINN_ERR_CONFIG, "transfer PQC: workspace too small");
+  switch (c->n) {
+    case 5: return bwd_n<5>(c, a, ws, t);
+    case 6: return bwd_n<6>(c, a, ws, t);
+    case 7: return bwd_n<7>(c, a, ws, t);
+    default: return fail(QPINN_ERR_CAPACITY, "transfer PQC covers 5 <= n <= 7");
+  }
+}
+
+}  // namespace qpinn

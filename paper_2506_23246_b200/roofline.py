@@ -24,6 +24,26 @@ def pqc_flops(circuit):
     return f_fwd, f_adj
 
 
+def transfer_bytes(n: int):
+    """HBM bytes per point of the transfer-matrix K1/K2 (pqc_transfer.cu, float32):
+    every [4 rows, 2D] operand is 4 x 2D x 4 = 32 D bytes per point.
+      forward : embed writes Phi; the GEMM reads Phi, writes Psi; the readout reads
+                Psi (4 x 32 D) + a, da in and z, dz out (2 x 16 n)
+      backward: seeds read Psi, write Abar; the GEMM reads Abar, writes gPhi; the
+                embedding gradient reads gPhi; the weight-gradient GEMM reads Phi
+                and Abar (7 x 32 D) + dL/dz, dL/ddz, a, da in, g_a, g_da out (3 x 16 n)
+    The D x D transfer matrix and its adjoint are L2-resident and not counted."""
+    D = 1 << n
+    return 4 * 32 * D + 2 * 16 * n, 7 * 32 * D + 3 * 16 * n
+
+
+def transfer_flops(n: int):
+    """Algorithmic (fp32) GEMM flops per point: Psi = Phi W is [4, 2D] x [2D, 2D];
+    the backward has gPhi = Abar W^T and gW += Phi^T Abar."""
+    D2 = 2 << n
+    return 2 * 4 * D2 * D2, 2 * 2 * 4 * D2 * D2
+
+
 def trunk_flops(hidden: int = 128, rff: int = 128, n_qubits: int = 7, n_hidden: int = 3):
     """Trunk forward with tangents (4 channels) and backward (~2x), SURVEY 8d."""
     w_in = 2 * rff

@@ -23,7 +23,7 @@ def gemm(A, B, C_=None):
 
 torch.manual_seed(0)
 for (M, n, K) in [(128, 128, 32), (1000, 128, 256), (300, 256, 128), (513, 7, 128), (4096, 64, 96),
-                  (262144, 128, 256), (262144, 128, 128), (262144, 256, 128)]:
+                  (262144, 128, 256), (262144, 128, 128), (262144, 256, 128), (262144, 256, 256)]:
     A = torch.randn(M, K, device="cuda")
     B = torch.randn(n, K, device="cuda") / K ** 0.5
     Cg = gemm(A, B)
@@ -68,7 +68,7 @@ def atb(X, G):
     return C_
 
 
-for (rows, m, n) in [(64, 128, 128), (1000, 96, 40), (262144, 256, 128), (262144, 128, 128),
+for (rows, m, n) in [(64, 128, 128), (1000, 96, 40), (262144, 256, 128), (262144, 128, 128), (262144, 256, 256),
                      (70001, 132, 200)]:
     X = torch.randn(rows, m, device="cuda")
     G = torch.randn(rows, n, device="cuda")

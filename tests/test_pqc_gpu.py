@@ -244,3 +244,36 @@ def test_global_memory_forward_vs_oracle(n, L, kind, dtype):
         z, dz = pqc_forward_raw(c, "acos", cuda(a, dtype), cuda(da, dtype), cuda(qp, dtype))
         assert_close(z, wz, dtype, "z")
         assert_close(dz, wdz, dtype, "dz")
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n", [5, 6, 7])
+@pytest.mark.parametrize("kind", O.KINDS)
+def test_transfer_matrix_kernels_vs_oracle(kind, n):
+    """Transfer-matrix K1/K2 (variant "transfer": the circuit as one [2D, 2D]
+    real map on the tensor cores, its adjoint on the D basis rows) vs the
+    oracle, with and without the state hand-off, FP32 tolerance."""
+    from paper_2506_23246_b200.ansatz import (build_circuit, pqc_backward_raw, pqc_forward_raw,
+                                              state_buffer)
+    dtype = torch.float32
+    rng = np.random.default_rng(100 + n)
+    L, R = 4, 1000
+    c = build_circuit(kind, n, L)
+    c.set_kernel_variant("transfer")
+    d = dict(a=rng.uniform(-0.9, 0.9, (R, n)), da=rng.normal(size=(3, R, n)),
+             qp=rng.uniform(0, 2 * np.pi, c.param_count), gz=rng.normal(size=(R, n)),
+             gdz=rng.normal(size=(3, R, n)))
+    a, da, qp = cuda(d["a"], dtype), cuda(d["da"], dtype), cuda(d["qp"], dtype)
+    gz, gdz = cuda(d["gz"], dtype), cuda(d["gdz"], dtype)
+    st = state_buffer(c, a)
+    z, dz = pqc_forward_raw(c, "acos", a, da, qp, st)
+    zp, _ = pqc_forward_raw(c, "acos", a, None, qp)
+    g = pqc_backward_raw(c, "acos", a, da, qp, gz, gdz, st)
+    g2 = pqc_backward_raw(c, "acos", a, da, qp, gz, gdz, None)
+    wz, wdz = O.pqc_forward(d["a"], d["da"], d["qp"], kind, "acos", L)
+    wg = O.pqc_backward(d["a"], d["da"], d["qp"], kind, "acos", L, d["gz"], d["gdz"])
+    for name, x, w in zip(("z", "dz", "zp", "ga", "gda", "gq"), (z, dz, zp) + tuple(g),
+                          (wz, wdz, wz) + tuple(wg)):
+        assert_close(x, w, dtype, f"transfer {name}")
+    for x, y in zip(g, g2):  # replayed forward: same launches, same bits
+        assert torch.equal(x, y)
