@@ -672,7 +672,10 @@ size_t qpinn_pqc_state_bytes(const qpinn_circuit* c, int dtype, int64_t rows) {
   // generic kernels: the 4 final states (fits inside the former)
   const size_t per = 4 * ((size_t)1 << c->n) * 2 * (dtype == QPINN_F64 ? 8 : 4);
   const bool layer = c->n <= qpinn_pqc_max_qubits(dtype) && layer_entangler(c) >= 0;
-  return (size_t)rows * per * (layer && c->L > 1 ? (size_t)c->L : 1);
+  const size_t b = (size_t)rows * per * (layer && c->L > 1 ? (size_t)c->L : 1);
+  if (!transfer_supported(c, dtype)) return b;
+  const size_t t = transfer_state_bytes(c, rows);  // Psi, Phi, W, checkpoints, tables
+  return t > b ? t : b;
 }
 
 static int check_common(const qpinn_circuit* c, int dtype, int scale, int64_t rows,

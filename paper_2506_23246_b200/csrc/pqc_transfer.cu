@@ -173,17 +173,16 @@ __global__ void __launch_bounds__(kTrThreads) tr_circuit_bwd(
 // acc[i] = sum over the D basis rows of the partials, in row order
 __global__ void tr_reduce(int D, int n_u1, int n_ph, const double* __restrict__ part_u1,
                           const double* __restrict__ part_ph, double* __restrict__ acc) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < 8 * n_u1) {
-    double v = 0.0;
-    for (int j = 0; j < D; ++j) v += part_u1[(size_t)j * 8 * n_u1 + i];
-    acc[i] = v;
-  } else if (i < 8 * n_u1 + n_ph) {
-    const int k = i - 8 * n_u1;
-    double v = 0.0;
-    for (int j = 0; j < D; ++j) v += part_ph[(size_t)j * n_ph + k];
-    acc[i] = v;
-  }
+  // one warp per entry: lane-strided row sums, then a fixed xor tree (deterministic)
+  const int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (i >= 8 * n_u1 + n_ph) return;
+  const bool u1 = i < 8 * n_u1;
+  const double* src = u1 ? part_u1 + i : part_ph + (i - 8 * n_u1);
+  const size_t stride = u1 ? (size_t)8 * n_u1 : (size_t)n_ph;
+  double v = 0.0;
+  for (int j = lane; j < D; j += 32) v += src[(size_t)j * stride];
+  for (int m = 16; m >= 1; m >>= 1) v += __shfl_xor_sync(0xffffffffu, v, m);
+  if (lane == 0) acc[i] = v;
 }
 
 // Wt [2D][2D] = W^T (forward GEMM operand) and W (backward operand)
@@ -575,37 +574,80 @@ int grid_points(int64_t R) {  // 8 warps per block, kPB points per block iterati
   return (int)(b < 1 ? 1 : b > cap ? cap : b);
 }
 
-// B (and the layer checkpoints) on the device, then W / W^T
-int build_transfer(const qpinn_circuit* c, const float* qp, unsigned char* ws, const TrLayout& t,
-                   bool checkpoints, cudaStream_t st) {
+// The circuit's device tables: u1 matrices, phase diagonals, the layer
+// checkpoints of the basis rows, W (backward operand) and W^T (forward operand).
+struct TrCircuit {
+  cplx<float>* U;
+  cplx<float>* ph;
+  cplx<float>* CK;
+  float* W;
+  float* Wt;
+};
+
+// hand-off layout (after the forward with tangents): [Psi | Phi | W | CK | U | ph]
+struct TrHandoff {
+  size_t psi, phi, W, CK, U, ph, total;
+};
+
+TrHandoff tr_handoff(const qpinn_circuit* c, int64_t R) {
+  const size_t D = (size_t)1 << c->n, D2 = 2 * D, cs = sizeof(cplx<float>);
+  TrHandoff h{};
+  size_t o = 0;
+  auto take = [&](size_t bytes) {
+    const size_t at = o;
+    o += align_up(bytes, 256);
+    return at;
+  };
+  h.psi = take(4 * (size_t)R * D2 * 4);
+  h.phi = take(4 * (size_t)R * D2 * 4);
+  h.W = take(4 * D2 * D2);
+  h.CK = take(cs * D * D * c->L);
+  h.U = take(cs * 4 * c->n_u1);
+  h.ph = take(cs * D * c->n_phase);
+  h.total = o;
+  return h;
+}
+
+// B = the circuit on the basis rows (with the layer checkpoints), then W / W^T
+int build_transfer(const qpinn_circuit* c, const float* qp, const TrCircuit& tc_,
+                   cplx<float>* B, cudaStream_t st) {
   const PlanDev& p = c->dev;
   const int n = c->n, D = 1 << n;
   const int ent = layer_entangler(c);
-  auto* U = (cplx<float>*)(ws + t.U);
-  auto* ph = (cplx<float>*)(ws + t.ph);
-  auto* B = (cplx<float>*)(ws + t.B);
-  tr_tables<<<32, 256, 0, st>>>(p, qp, U, ph);
-  tr_circuit_fwd<<<D, kTrThreads, 0, st>>>(n, c->L, ent, U, ph, p.perm, B,
-                                           checkpoints ? (cplx<float>*)(ws + t.CK) : nullptr);
-  tr_wmat<<<(4 * D * D + 255) / 256, 256, 0, st>>>(n, B, (float*)(ws + t.W), (float*)(ws + t.Wt));
+  tr_tables<<<32, 256, 0, st>>>(p, qp, tc_.U, tc_.ph);
+  tr_circuit_fwd<<<D, kTrThreads, 0, st>>>(n, c->L, ent, tc_.U, tc_.ph, p.perm, B, tc_.CK);
+  tr_wmat<<<(4 * D * D + 255) / 256, 256, 0, st>>>(n, B, tc_.W, tc_.Wt);
   QPINN_CUDA_CHECK(cudaGetLastError());
   return QPINN_OK;
+}
+
+TrCircuit ws_circuit(unsigned char* ws, const TrLayout& t) {
+  return {(cplx<float>*)(ws + t.U), (cplx<float>*)(ws + t.ph), (cplx<float>*)(ws + t.CK),
+          (float*)(ws + t.W), (float*)(ws + t.Wt)};
 }
 
 template <int NQ>
 int fwd_n(const qpinn_circuit* c, const KArgs<float>* a, unsigned char* ws, const TrLayout& t) {
   constexpr int D2 = 2 << NQ;
   cudaStream_t st = a->stream;
-  if (int rc = build_transfer(c, a->qp, ws, t, false, st)) return rc;
-  // hand-off: Psi, then (L >= 2: the buffer holds L state sets) Phi for the weight gradient
-  auto* Psi = a->states ? (float*)a->states : (float*)(ws + t.BUF2);
-  auto* Phi = a->states && a->tan && c->L >= 2 ? (float*)a->states + 4 * a->R * D2
-                                               : (float*)(ws + t.BUF1);
+  const bool handoff = a->states && a->tan;
+  auto* hs = (unsigned char*)a->states;
+  const TrHandoff h = tr_handoff(c, a->R);
+  TrCircuit cc = ws_circuit(ws, t);
+  if (handoff) {  // the backward reuses the circuit tables, checkpoints and W
+    cc.U = (cplx<float>*)(hs + h.U);
+    cc.ph = (cplx<float>*)(hs + h.ph);
+    cc.CK = (cplx<float>*)(hs + h.CK);
+    cc.W = (float*)(hs + h.W);
+  }
+  if (int rc = build_transfer(c, a->qp, cc, (cplx<float>*)(ws + t.B), st)) return rc;
+  auto* Psi = a->states ? (float*)(hs + h.psi) : (float*)(ws + t.BUF2);
+  auto* Phi = handoff ? (float*)(hs + h.phi) : (float*)(ws + t.BUF1);
   const int ns = a->tan ? 4 : 1;
   tr_embed<NQ><<<grid_points(a->R), 256, 0, st>>>(a->scale, a->R, a->act, a->tan, Phi, a->maxabs);
   QPINN_CUDA_CHECK(cudaGetLastError());
-  if (int rc = tc::gemm3(ns * a->R, D2, D2, Phi, D2, (const float*)(ws + t.Wt), D2, Psi, D2,
-                         ws + t.g3, tc::gemm3_workspace_bytes(D2, D2), st))
+  if (int rc = tc::gemm3(ns * a->R, D2, D2, Phi, D2, cc.Wt, D2, Psi, D2, ws + t.g3,
+                         tc::gemm3_workspace_bytes(D2, D2), st))
     return rc;
   tr_readout<NQ><<<grid_points(a->R), 256, 0, st>>>(a->R, ns, Psi, a->z, a->dz);
   QPINN_CUDA_CHECK(cudaGetLastError());
@@ -618,29 +660,43 @@ int bwd_n(const qpinn_circuit* c, const KArgs<float>* a, unsigned char* ws, cons
   cudaStream_t st = a->stream;
   const PlanDev& p = c->dev;
   const int ent = layer_entangler(c), L = c->L, n_u1 = c->n_u1;
-  if (int rc = build_transfer(c, a->qp, ws, t, true, st)) return rc;
   auto* Abar = (float*)(ws + t.BUF1);
   auto* G = (float*)(ws + t.BUF2);
   const int gp = grid_points(a->R);
-  const float* Psi = (const float*)a->states;
-  if (!Psi) {  // no hand-off: replay the forward map into BUF2
+  const float* Psi;
+  const float* Phi;
+  TrCircuit cc = ws_circuit(ws, t);
+  if (a->states) {  // hand-off of the matching forward
+    auto* hs = (unsigned char*)a->states;
+    const TrHandoff h = tr_handoff(c, a->R);
+    Psi = (const float*)(hs + h.psi);
+    Phi = (const float*)(hs + h.phi);
+    cc.U = (cplx<float>*)(hs + h.U);
+    cc.ph = (cplx<float>*)(hs + h.ph);
+    cc.CK = (cplx<float>*)(hs + h.CK);
+    cc.W = (float*)(hs + h.W);
+  } else {  // replay the forward map: Phi into BUF1, Psi into BUF2
+    if (int rc = build_transfer(c, a->qp, cc, (cplx<float>*)(ws + t.B), st)) return rc;
     tr_embed<NQ><<<gp, 256, 0, st>>>(a->scale, a->R, a->act, a->tan, Abar, nullptr);
     QPINN_CUDA_CHECK(cudaGetLastError());
-    if (int rc = tc::gemm3(4 * a->R, D2, D2, Abar, D2, (const float*)(ws + t.Wt), D2, G, D2,
-                           ws + t.g3, tc::gemm3_workspace_bytes(D2, D2), st))
+    if (int rc = tc::gemm3(4 * a->R, D2, D2, Abar, D2, cc.Wt, D2, G, D2, ws + t.g3,
+                           tc::gemm3_workspace_bytes(D2, D2), st))
       return rc;
     Psi = G;
+    Phi = nullptr;  // re-embedded after the embedding gradient
   }
   tr_seed<NQ><<<gp, 256, 0, st>>>(a->R, a->gz, a->gdz, Psi, Abar);
   QPINN_CUDA_CHECK(cudaGetLastError());
   // gPhi = Abar W^T
-  if (int rc = tc::gemm3(4 * a->R, D2, D2, Abar, D2, (const float*)(ws + t.W), D2, G, D2,
-                         ws + t.g3, tc::gemm3_workspace_bytes(D2, D2), st))
+  if (int rc = tc::gemm3(4 * a->R, D2, D2, Abar, D2, cc.W, D2, G, D2, ws + t.g3,
+                         tc::gemm3_workspace_bytes(D2, D2), st))
     return rc;
   tr_embed_grad<NQ><<<gp, 256, 0, st>>>(a->scale, a->R, a->act, a->tan, G, a->g_act, a->g_tan);
-  // gW = Phi^T Abar (Phi from the hand-off, else re-embedded over gPhi)
-  const float* Phi = a->states && c->L >= 2 ? (const float*)a->states + 4 * a->R * D2 : G;
-  if (Phi == G) tr_embed<NQ><<<gp, 256, 0, st>>>(a->scale, a->R, a->act, a->tan, G, nullptr);
+  // gW = Phi^T Abar
+  if (!Phi) {
+    tr_embed<NQ><<<gp, 256, 0, st>>>(a->scale, a->R, a->act, a->tan, G, nullptr);
+    Phi = G;
+  }
   QPINN_CUDA_CHECK(cudaGetLastError());
   if (int rc = tc::wgrad(4 * a->R, D2, D2, Phi, D2, Abar, D2, (float*)(ws + t.gW), ws + t.wg,
                          tc::wgrad_workspace_bytes(4 * a->R, D2, D2), st))
@@ -650,11 +706,9 @@ int bwd_n(const qpinn_circuit* c, const KArgs<float>* a, unsigned char* ws, cons
   auto* pu = (double*)(ws + t.pu);
   auto* pp = (double*)(ws + t.pp);
   auto* acc = (double*)(ws + t.acc);
-  tr_circuit_bwd<<<D, kTrThreads, 0, st>>>(NQ, L, ent, (const cplx<float>*)(ws + t.U),
-                                           (const cplx<float>*)(ws + t.ph), p.iperm, Ab,
-                                           (const cplx<float>*)(ws + t.CK), pu, pp);
+  tr_circuit_bwd<<<D, kTrThreads, 0, st>>>(NQ, L, ent, cc.U, cc.ph, p.iperm, Ab, cc.CK, pu, pp);
   const int n_ph = D * c->n_phase, n_acc = 8 * n_u1 + n_ph;
-  tr_reduce<<<(n_acc + 127) / 128, 128, 0, st>>>(D, n_u1, n_ph, pu, pp, acc);
+  tr_reduce<<<(n_acc + 7) / 8, 256, 0, st>>>(D, n_u1, n_ph, pu, pp, acc);
   QPINN_CUDA_CHECK(cudaGetLastError());
   return pqc_param_grads<float>(c, acc, NQ, a->qp, a->g_qp, st);
 }
@@ -663,6 +717,10 @@ int bwd_n(const qpinn_circuit* c, const KArgs<float>* a, unsigned char* ws, cons
 
 bool transfer_supported(const qpinn_circuit* c, int dtype) {
   return c && dtype == QPINN_F32 && c->n >= 5 && c->n <= 7 && layer_entangler(c) >= 0;
+}
+
+size_t transfer_state_bytes(const qpinn_circuit* c, int64_t R) {
+  return R <= 0 ? 0 : tr_handoff(c, R).total;
 }
 
 size_t transfer_workspace_bytes(const qpinn_circuit* c, int64_t R) {
