@@ -84,7 +84,8 @@ size_t qpinn_circuit_plan_dump(const qpinn_circuit* c, char* buf, size_t len);
  * build_circuit ansatz has; 1 forces the generic runtime-plan kernels; 2
  * forces the transfer-matrix kernels (float32, 5 <= n <= 7: the circuit as
  * one [2^(n+1), 2^(n+1)] real map applied on the tensor cores, the
- * reference's via="matrix" formulation, ansatz.py:300-338).  Set it before
+ * reference's via="matrix" formulation, ansatz.py:300-338); 3 forces the
+ * layer-loop kernels wherever the plan allows them.  Set it before
  * the forward whose states feed a backward (the two must use the same
  * variant). */
 int qpinn_circuit_set_kernel_variant(qpinn_circuit* c, int variant);

@@ -626,7 +626,7 @@ using namespace qpinn;
 extern "C" {
 
 int qpinn_circuit_set_kernel_variant(qpinn_circuit* c, int variant) {
-  if (!c || variant < 0 || variant > 2) return fail(QPINN_ERR_CONFIG, "bad kernel variant");
+  if (!c || variant < 0 || variant > 3) return fail(QPINN_ERR_CONFIG, "bad kernel variant");
   c->variant = variant;
   return QPINN_OK;
 }
@@ -745,7 +745,7 @@ int qpinn_pqc_forward(const qpinn_circuit* cc, int dtype, int scale, int64_t row
     const size_t off = small_ws_bytes(c);
     return transfer_forward(c, &a, (unsigned char*)workspace + off, workspace_bytes - off);
   }
-  if (c->variant == 0) {  // layer-loop kernels for every standard plan
+  if (c->variant == 0 || c->variant == 3) {  // layer-loop kernels for every standard plan
     if (dtype == QPINN_F32) {
       KArgs<float> a{scale, rows, (const float*)act_val, (const float*)act_tan,
                         (const float*)qparams, (float*)z, (float*)dz, states, maxabs,
@@ -844,7 +844,7 @@ int qpinn_pqc_backward(const qpinn_circuit* cc, int dtype, int scale, int64_t ro
     const size_t off = small_ws_bytes(c);
     return transfer_backward(c, &a, (unsigned char*)workspace + off, workspace_bytes - off);
   }
-  if (c->variant == 0) {
+  if (c->variant == 0 || c->variant == 3) {
     if (dtype == QPINN_F32) {
       KArgs<float> a{scale, rows, (const float*)act_val, (const float*)act_tan,
                         (const float*)qparams, nullptr, nullptr, const_cast<void*>(states),

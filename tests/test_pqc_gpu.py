@@ -148,7 +148,7 @@ def test_specialized_kernels_match_generic_and_oracle(kind, dtype):
     rng = np.random.default_rng(11)
     n, L, R = 7, 4, 301
     res = {}
-    for variant in ("auto", "generic"):
+    for variant in ("layer", "generic", "auto"):
         c = build_circuit(kind, n, L)
         assert c.specialized
         c.set_kernel_variant(variant)
@@ -164,7 +164,7 @@ def test_specialized_kernels_match_generic_and_oracle(kind, dtype):
     d = res["d"]
     wz, wdz = O.pqc_forward(d["a"], d["da"], d["qp"], kind, "acos", L)
     wg = O.pqc_backward(d["a"], d["da"], d["qp"], kind, "acos", L, d["gz"], d["gdz"])
-    for variant in ("auto", "generic"):
+    for variant in ("layer", "generic", "auto"):
         got = res[variant]
         for name, x, w in zip(("z", "dz", "ga", "gda", "gq"), got, (wz, wdz) + tuple(wg)):
             assert_close(x, w, dtype, f"{variant} {name}")
@@ -247,17 +247,20 @@ def test_global_memory_forward_vs_oracle(n, L, kind, dtype):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("R", [1000, 1, 65])
 @pytest.mark.parametrize("n", [5, 6, 7])
 @pytest.mark.parametrize("kind", O.KINDS)
-def test_transfer_matrix_kernels_vs_oracle(kind, n):
+def test_transfer_matrix_kernels_vs_oracle(kind, n, R):
     """Transfer-matrix K1/K2 (variant "transfer": the circuit as one [2D, 2D]
     real map on the tensor cores, its adjoint on the D basis rows) vs the
     oracle, with and without the state hand-off, FP32 tolerance."""
     from paper_2506_23246_b200.ansatz import (build_circuit, pqc_backward_raw, pqc_forward_raw,
                                               state_buffer)
+    if R != 1000 and kind not in ("strongly", "cross_mesh"):
+        pytest.skip("ragged batch sizes: one permutation and one phase ansatz")
     dtype = torch.float32
     rng = np.random.default_rng(100 + n)
-    L, R = 4, 1000
+    L = 4
     c = build_circuit(kind, n, L)
     c.set_kernel_variant("transfer")
     d = dict(a=rng.uniform(-0.9, 0.9, (R, n)), da=rng.normal(size=(3, R, n)),
@@ -272,8 +275,11 @@ def test_transfer_matrix_kernels_vs_oracle(kind, n):
     g2 = pqc_backward_raw(c, "acos", a, da, qp, gz, gdz, None)
     wz, wdz = O.pqc_forward(d["a"], d["da"], d["qp"], kind, "acos", L)
     wg = O.pqc_backward(d["a"], d["da"], d["qp"], kind, "acos", L, d["gz"], d["gdz"])
+    # a handful of points: the absolute floor (1e-6 of the largest entry) is taken over
+    # only 7 .. 455 values; both K2 paths sit at ~1e-6 of it there (scripts/dbg_transfer_r1.py)
+    scale = 1.0 if R >= 1000 else 2.0
     for name, x, w in zip(("z", "dz", "zp", "ga", "gda", "gq"), (z, dz, zp) + tuple(g),
                           (wz, wdz, wz) + tuple(wg)):
-        assert_close(x, w, dtype, f"transfer {name}")
+        assert_close(x, w, dtype, f"transfer {name}", scale)
     for x, y in zip(g, g2):  # replayed forward: same launches, same bits
         assert torch.equal(x, y)
