@@ -32,7 +32,10 @@ constexpr int kBM = 128, kBK = 32;
 // k-blocks accumulated in one TMEM buffer before the epilogue warps add it into
 // fp32 registers (1: 32-deep tensor-core chains, 3.5e-7 relative at K = 256;
 // 2 measured 6.3e-7 at the same speed)
-constexpr int kPromote = 1;
+#ifndef QPINN_GEMM_PROMOTE
+#define QPINN_GEMM_PROMOTE 1
+#endif
+constexpr int kPromote = QPINN_GEMM_PROMOTE;
 constexpr int kABytes = kBM * kBK * 4;  // 16 KB fp32 tile
 constexpr int kThreadsGemm = 448;  // 4 split + 8 epilogue + producer + MMA warps
 constexpr int kThreadsW = 320;      // weight gradient: 4 split + 4 epilogue + producer + MMA
@@ -47,15 +50,29 @@ struct GemmCfg {
 #ifndef QPINN_GEMM_BS
 #define QPINN_GEMM_BS 2
 #endif
+#ifndef QPINN_GEMM_ATMEM
+#define QPINN_GEMM_ATMEM 1
+#endif
+  // split A operands in TMEM (the MMA then reads only B from shared memory,
+  // whose bandwidth bounds the 3-product TF32 MMAs otherwise), else in smem
+  static constexpr bool kATmem = QPINN_GEMM_ATMEM;
   static constexpr int kRaw = QPINN_GEMM_RAW;   // fp32 A stages in flight from HBM
-  static constexpr int kOps = 2;   // split A buffers (A_hi, A_lo)
-  static constexpr int kOpBytes = 2 * kABytes;
+#ifndef QPINN_GEMM_OS
+#define QPINN_GEMM_OS 2
+#endif
+#ifndef QPINN_GEMM_NB
+#define QPINN_GEMM_NB 3
+#endif
+  static constexpr int kOps = kATmem ? QPINN_GEMM_OS : 2;   // split A buffers (A_hi, A_lo)
+  static constexpr int kOpBytes = kATmem ? 0 : 2 * kABytes;
   static constexpr int kBS = QPINN_GEMM_BS;    // B_hi / B_lo stages (from L2)
   static constexpr int kBStage = 2 * kBBytes;
-  static constexpr int kNB = 4;    // TMEM partial buffers
-  static constexpr int kTmemCols = kNB * BN;
+  static constexpr int kNB = kATmem ? QPINN_GEMM_NB : 4;    // TMEM partial buffers
+  static constexpr int kACol = kNB * BN;        // TMEM: [NB partials | OS x (A_hi, A_lo)]
+  static constexpr int kTmemCols = kATmem ? 512 : kNB * BN;
+  static_assert(!kATmem || kNB * BN + kOps * 2 * kBK <= 512, "TMEM columns");
   static constexpr int kSbuf = 32 * BN * 4;
-  static constexpr int kStg = 8 * 2048;  // per epilogue warp: 16 rows x 32 cols
+  static constexpr int kStg = 8 * 2 * 2048;  // per epilogue warp: 2 x (16 rows x 32 cols)
   static constexpr int kSmem =
       kRaw * kABytes + kOps * kOpBytes + kBS * kBStage + kSbuf + kStg + 1024 + 512;
 };
@@ -70,22 +87,24 @@ struct GemmArgs {
   int tma_store;      // C goes out through TMA (16-byte aligned rows), else direct stores
 };
 
-// one epilogue warp's 32 rows x CW columns (lane = row) -> global through a
-// 2 KB staging buffer (16 rows x 32 columns, 128-byte swizzled, conflict-free)
-// and TMA stores of 32 x 16 boxes at (col0 + c, row0 + 16 h, blk) of the
-// 3-D output map
+// one epilogue warp's 32 rows x CW columns (lane = row) -> global through two
+// alternating 2 KB staging buffers (16 rows x 32 columns, 128-byte swizzled,
+// conflict-free) and TMA stores of 32 x 16 boxes at (col0 + c, row0 + 16 h, blk)
+// of the 3-D output map; a buffer is rewritten once the store before last has
+// read it, so one store is always in flight while the next box is staged
 template <int CW>
 __device__ __forceinline__ void store_rows_tma(const float (&acc)[CW], unsigned char* buf,
                                                const CUtensorMap* mC, int col0, int row0,
-                                               int blk, int lane) {
+                                               int blk, int lane, uint32_t& sidx) {
 #pragma unroll
   for (int c0 = 0; c0 < CW; c0 += 32) {
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
-      if (lane == 0) bulk_wait_read0();  // the previous store has read the buffer
+      unsigned char* sb = buf + (sidx++ & 1) * 2048;
+      if (lane == 0) bulk_wait_read1();
       __syncwarp();
       if ((lane >> 4) == h) {
-        const uint32_t base = smem_u32(buf) + (lane & 15) * 128;
+        const uint32_t base = smem_u32(sb) + (lane & 15) * 128;
 #pragma unroll
         for (int j = 0; j < 8; ++j)
           sts128(base + ((j ^ (lane & 7)) << 4),
@@ -95,7 +114,7 @@ __device__ __forceinline__ void store_rows_tma(const float (&acc)[CW], unsigned 
       fence_proxy_async_smem();
       __syncwarp();
       if (lane == 0) {
-        tma_store_3d(mC, buf, col0 + c0, row0 + 16 * h, blk);
+        tma_store_3d(mC, sb, col0 + c0, row0 + 16 * h, blk);
         bulk_commit();
       }
     }
@@ -211,18 +230,29 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUt
           mbar_wait(conv + o, (uint32_t)((j / OS) & 1));
           mbar_wait(b_full + e, (uint32_t)((j / BS) & 1));
           tc_fence_after();
-          const uint32_t a_hi = smem_u32(ops + o * Cfg::kOpBytes);
-          const uint32_t a_lo = a_hi + kABytes;
           const uint32_t b_hi = smem_u32(bst + e * Cfg::kBStage);
           const uint32_t b_lo = b_hi + Cfg::kBBytes;
           const uint32_t d = tmem + b * BN;
+          if constexpr (Cfg::kATmem) {
+            const uint32_t a_hi = tmem + Cfg::kACol + o * 2 * kBK, a_lo = a_hi + kBK;
 #pragma unroll
-          for (int k = 0; k < kBK / 8; ++k) {
-            const uint32_t off = k * 32;  // 8 tf32 = 32 bytes along the swizzled row
-            mma_tf32(d, desc_k_sw128(a_lo + off), desc_k_sw128(b_hi + off), idesc,
-                     !(first && k == 0));
-            mma_tf32(d, desc_k_sw128(a_hi + off), desc_k_sw128(b_lo + off), idesc, 1);
-            mma_tf32(d, desc_k_sw128(a_hi + off), desc_k_sw128(b_hi + off), idesc, 1);
+            for (int k = 0; k < kBK / 8; ++k) {
+              const uint32_t off = k * 32;  // 8 tf32 = 32 bytes along the swizzled B row
+              mma_tf32_ts(d, a_lo + k * 8, desc_k_sw128(b_hi + off), idesc, !(first && k == 0));
+              mma_tf32_ts(d, a_hi + k * 8, desc_k_sw128(b_lo + off), idesc, 1);
+              mma_tf32_ts(d, a_hi + k * 8, desc_k_sw128(b_hi + off), idesc, 1);
+            }
+          } else {
+            const uint32_t a_hi = smem_u32(ops + o * Cfg::kOpBytes);
+            const uint32_t a_lo = a_hi + kABytes;
+#pragma unroll
+            for (int k = 0; k < kBK / 8; ++k) {
+              const uint32_t off = k * 32;  // 8 tf32 = 32 bytes along the swizzled row
+              mma_tf32(d, desc_k_sw128(a_lo + off), desc_k_sw128(b_hi + off), idesc,
+                       !(first && k == 0));
+              mma_tf32(d, desc_k_sw128(a_hi + off), desc_k_sw128(b_lo + off), idesc, 1);
+              mma_tf32(d, desc_k_sw128(a_hi + off), desc_k_sw128(b_hi + off), idesc, 1);
+            }
           }
           mma_commit(op_empty + o);
           mma_commit(b_empty + e);
@@ -234,6 +264,42 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUt
       }
     }
     __syncwarp();
+  } else if (warp < 4 && Cfg::kATmem) {  // ---- split A into TMEM (warp w: lanes 32 w ..)
+    // thread = tile row = TMEM lane; the row's 8 16-byte chunks sit at c ^ (row & 7)
+    const int row = warp * 32 + lane;
+    const uint32_t lane_base = (uint32_t)(warp * 32) << 16;
+    int64_t j = 0;
+    for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+      for (int kb = 0; kb < nk; ++kb, ++j) {
+        const int r = (int)(j % RS), o = (int)(j % OS);
+        if (j >= OS) {
+          mbar_wait(op_empty + o, (uint32_t)(((j / OS) - 1) & 1));
+          tc_fence_after();
+        }
+        mbar_wait(raw_full + r, (uint32_t)((j / RS) & 1));
+        const uint32_t src = smem_u32(raw + r * kABytes) + row * 128;
+        float4 v[8];
+#pragma unroll
+        for (int c = 0; c < 8; ++c) v[c] = lds128(src + ((c ^ (row & 7)) << 4));
+        float hi[32], lo[32];
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          split_tf32(v[c].x, hi[4 * c], lo[4 * c]);
+          split_tf32(v[c].y, hi[4 * c + 1], lo[4 * c + 1]);
+          split_tf32(v[c].z, hi[4 * c + 2], lo[4 * c + 2]);
+          split_tf32(v[c].w, hi[4 * c + 3], lo[4 * c + 3]);
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(raw_empty + r);
+        const uint32_t a = tmem + lane_base + Cfg::kACol + o * 2 * kBK;
+        tmem_st32(a, hi);
+        tmem_st32(a + kBK, lo);
+        tmem_st_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(conv + o);
+      }
+    }
   } else if (warp < 4) {  // ---- split A into an operand buffer
     int64_t j = 0;
     for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
@@ -273,7 +339,8 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUt
     const int q = warp & 3, h = (warp - 4) >> 2;
     constexpr int CW = BN / 2;  // columns per epilogue warp
     const uint32_t lane_base = (uint32_t)(q * 32) << 16;
-    unsigned char* my_stg = stg + (warp - 4) * 2048;
+    unsigned char* my_stg = stg + (warp - 4) * 2 * 2048;
+    uint32_t sidx = 0;
     int64_t j = 0;
     for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
       const int64_t mt = t / n_nt;
@@ -307,7 +374,7 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUt
         }
         const int64_t row = mt * kBM + q * 32 + lane;
         if (g.tma_store) {
-          store_rows_tma<CW>(acc, my_stg, &mC, n0 + c_off, (int)(mt * kBM + q * 32), 0, lane);
+          store_rows_tma<CW>(acc, my_stg, &mC, n0 + c_off, (int)(mt * kBM + q * 32), 0, lane, sidx);
         } else if (row < g.M) {
           float* dst = g.C + row * g.ldc + n0 + c_off;
 #pragma unroll
@@ -336,7 +403,7 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUt
           acc[c] = q == 0 ? y : (1.f - y * y) * acc[c];
         }
         if (g.tma_store) {
-          store_rows_tma<CW>(acc, my_stg, &mC, n0 + c_off, (int)(mt * 32), q, lane);
+          store_rows_tma<CW>(acc, my_stg, &mC, n0 + c_off, (int)(mt * 32), q, lane, sidx);
         } else if (p < g.R) {
           float* dst = g.C + ((int64_t)q * g.R + p) * g.ldc + n0 + c_off;
 #pragma unroll
