@@ -28,6 +28,18 @@
 namespace qpinn {
 namespace tc {
 
+#ifdef QPINN_GEMM_PROF
+__device__ unsigned long long g_gemm_prof[16];
+#define GPROF(slot, call)                                                    \
+  do {                                                                       \
+    const long long _t0 = clock64();                                         \
+    call;                                                                    \
+    if (blockIdx.x == 0 && (threadIdx.x & 31) == 0)                          \
+      atomicAdd(&g_gemm_prof[slot], (unsigned long long)(clock64() - _t0));  \
+  } while (0)
+#else
+#define GPROF(slot, call) call
+#endif
 constexpr int kBM = 128, kBK = 32;
 // k-blocks accumulated in one TMEM buffer before the epilogue warps add it into
 // fp32 registers (1: 32-deep tensor-core chains, 3.5e-7 relative at K = 256;
@@ -145,6 +157,9 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUt
   uint64_t* tempty = tfull + NB;
   uint32_t* tmem_slot = (uint32_t*)(tempty + NB);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#ifdef QPINN_GEMM_PROF
+  const long long prof_t0 = clock64();
+#endif
   const int nk = (g.K + kBK - 1) / kBK;
   const int64_t n_mt = EPI == EPI_TANH ? (g.R + 31) / 32 : (g.M + kBM - 1) / kBM;
   const int n_nt = (g.N + BN - 1) / BN;
@@ -187,7 +202,7 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUt
         const int64_t mt = t / n_nt;
         for (int kb = 0; kb < nk; ++kb, ++j) {
           const int r = (int)(j % RS);
-          if (j >= RS) mbar_wait(raw_empty + r, (uint32_t)(((j / RS) - 1) & 1));
+          if (j >= RS) GPROF(0, mbar_wait(raw_empty + r, (uint32_t)(((j / RS) - 1) & 1)));
           unsigned char* st = raw + r * kABytes;
           mbar_expect_tx(raw_full + r, kABytes);
           if constexpr (EPI == EPI_TANH) {
@@ -209,7 +224,7 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUt
         const int nt = (int)(t % n_nt);
         for (int kb = 0; kb < nk; ++kb, ++j) {
           const int e = (int)(j % BS);
-          if (j >= BS) mbar_wait(b_empty + e, (uint32_t)(((j / BS) - 1) & 1));
+          if (j >= BS) GPROF(1, mbar_wait(b_empty + e, (uint32_t)(((j / BS) - 1) & 1)));
           unsigned char* st = bst + e * Cfg::kBStage;
           mbar_expect_tx(b_full + e, 2 * Cfg::kBBytes);
           tma_load_2d(st, &mBhi, b_full + e, kb * kBK, nt * BN);
@@ -226,9 +241,9 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUt
           const int o = (int)(j % OS), e = (int)(j % BS), b = (int)(grp % NB);
           const bool first = kb % kPromote == 0;
           const bool last = kb % kPromote == kPromote - 1 || kb == nk - 1;
-          if (first && grp >= NB) mbar_wait(tempty + b, (uint32_t)(((grp / NB) - 1) & 1));
-          mbar_wait(conv + o, (uint32_t)((j / OS) & 1));
-          mbar_wait(b_full + e, (uint32_t)((j / BS) & 1));
+          if (first && grp >= NB) GPROF(2, mbar_wait(tempty + b, (uint32_t)(((grp / NB) - 1) & 1)));
+          GPROF(3, mbar_wait(conv + o, (uint32_t)((j / OS) & 1)));
+          GPROF(4, mbar_wait(b_full + e, (uint32_t)((j / BS) & 1)));
           tc_fence_after();
           const uint32_t b_hi = smem_u32(bst + e * Cfg::kBStage);
           const uint32_t b_lo = b_hi + Cfg::kBBytes;
@@ -273,10 +288,12 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUt
       for (int kb = 0; kb < nk; ++kb, ++j) {
         const int r = (int)(j % RS), o = (int)(j % OS);
         if (j >= OS) {
-          mbar_wait(op_empty + o, (uint32_t)(((j / OS) - 1) & 1));
+          if (warp == 0) GPROF(5, mbar_wait(op_empty + o, (uint32_t)(((j / OS) - 1) & 1)));
+          else mbar_wait(op_empty + o, (uint32_t)(((j / OS) - 1) & 1));
           tc_fence_after();
         }
-        mbar_wait(raw_full + r, (uint32_t)((j / RS) & 1));
+        if (warp == 0) GPROF(6, mbar_wait(raw_full + r, (uint32_t)((j / RS) & 1)));
+        else mbar_wait(raw_full + r, (uint32_t)((j / RS) & 1));
         const uint32_t src = smem_u32(raw + r * kABytes) + row * 128;
         float4 v[8];
 #pragma unroll
@@ -351,7 +368,8 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUt
       const int ngrp = (nk + kPromote - 1) / kPromote;
       for (int gi = 0; gi < ngrp; ++gi, ++j) {  // j counts promotion groups here
         const int b = (int)(j % NB);
-        mbar_wait(tfull + b, (uint32_t)((j / NB) & 1));
+        if (warp == 4) GPROF(7, mbar_wait(tfull + b, (uint32_t)((j / NB) & 1)));
+        else mbar_wait(tfull + b, (uint32_t)((j / NB) & 1));
         tc_fence_after();
 #pragma unroll
         for (int c0 = 0; c0 < CW; c0 += 32) {
@@ -374,7 +392,11 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUt
         }
         const int64_t row = mt * kBM + q * 32 + lane;
         if (g.tma_store) {
-          store_rows_tma<CW>(acc, my_stg, &mC, n0 + c_off, (int)(mt * kBM + q * 32), 0, lane, sidx);
+          if (warp == 4)
+            GPROF(8, (store_rows_tma<CW>(acc, my_stg, &mC, n0 + c_off, (int)(mt * kBM + q * 32), 0,
+                                         lane, sidx)));
+          else
+            store_rows_tma<CW>(acc, my_stg, &mC, n0 + c_off, (int)(mt * kBM + q * 32), 0, lane, sidx);
         } else if (row < g.M) {
           float* dst = g.C + row * g.ldc + n0 + c_off;
 #pragma unroll
@@ -418,6 +440,9 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUt
   tc_fence_before();
   __syncthreads();
   if (warp == 13) tmem_dealloc(tmem, Cfg::kTmemCols);
+#ifdef QPINN_GEMM_PROF
+  if (blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(&g_gemm_prof[9], (unsigned long long)(clock64() - prof_t0));
+#endif
 }
 
 // ---- weight gradient: dW[Kin, Nout] = X[rows, Kin]^T G[rows, Nout] ----------------------
@@ -868,6 +893,15 @@ int qpinn_gemm_f32(int64_t m, int n, int k, const void* a, int64_t lda, const vo
   return tc::gemm3(m, n, k, (const float*)a, lda, (const float*)b, ldb, (float*)c, ldc, workspace,
                    workspace_bytes, (cudaStream_t)stream);
 }
+
+#ifdef QPINN_GEMM_PROF
+int qpinn_gemm_prof(unsigned long long* out) {
+  cudaMemcpyFromSymbol(out, qpinn::tc::g_gemm_prof, sizeof(unsigned long long) * 16);
+  unsigned long long z[16] = {0};
+  cudaMemcpyToSymbol(qpinn::tc::g_gemm_prof, z, sizeof(z));
+  return 0;
+}
+#endif
 
 size_t qpinn_gemm_f32_atb_workspace_bytes(int64_t rows, int m, int n) {
   return rows < 0 || m < 1 || n < 1 ? 0 : tc::wgrad_workspace_bytes(rows, m, n);
