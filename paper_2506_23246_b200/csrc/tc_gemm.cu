@@ -656,13 +656,24 @@ wgrad_kernel(const __grid_constant__ CUtensorMap mX, const __grid_constant__ CUt
 }
 
 // dW = sum over chunks of the partial tiles, in chunk order (float64 sum)
-__global__ void wgrad_reduce(int n_kc, int64_t n, const float* __restrict__ partial,
-                             float* __restrict__ dW) {
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    double s = 0.0;
-    for (int k = 0; k < n_kc; ++k) s += (double)partial[(int64_t)k * n + i];
-    dW[i] = (float)s;
+// dW = sum over the chunks of the partial tiles, in a fixed order: block = 32
+// entries x 8 chunk groups (group g sums chunks g, g + 8, ...), then the groups in order
+__global__ void __launch_bounds__(256) wgrad_reduce(int n_kc, int64_t n,
+                                                    const float* __restrict__ partial,
+                                                    float* __restrict__ dW) {
+  __shared__ double red[8][33];
+  const int c = threadIdx.x & 31, grp = threadIdx.x >> 5;
+  const int64_t i = (int64_t)blockIdx.x * 32 + c;
+  double s = 0.0;
+  if (i < n)
+    for (int k = grp; k < n_kc; k += 8) s += (double)partial[(int64_t)k * n + i];
+  red[grp][c] = s;
+  __syncthreads();
+  if (grp == 0 && i < n) {
+    double v = 0.0;
+#pragma unroll
+    for (int g = 0; g < 8; ++g) v += red[g][c];
+    dW[i] = (float)v;
   }
 }
 
@@ -843,8 +854,7 @@ int wgrad(int64_t rows, int Kin, int Nout, const float* X, int64_t ldx, const fl
   wgrad_kernel<<<grid, kThreadsW, kWSmem, st>>>(mX, mG, a);
   QPINN_CUDA_CHECK(cudaGetLastError());
   const int64_t n = (int64_t)Kin * Nout;
-  wgrad_reduce<<<(int)((n + 255) / 256 < 1024 ? (n + 255) / 256 : 1024), 256, 0, st>>>(
-      a.n_kc, n, a.partial, dW);
+  wgrad_reduce<<<(int)((n + 31) / 32), 256, 0, st>>>(a.n_kc, n, a.partial, dW);
   QPINN_CUDA_CHECK(cudaGetLastError());
   return QPINN_OK;
 }

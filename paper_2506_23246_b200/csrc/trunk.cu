@@ -317,18 +317,21 @@ __global__ void colsum_partial(int64_t R, int N, int64_t rows_per, const T* __re
 // out[j] = sum_b partial[b][j]: 32 columns x 8 interleaved block groups per CTA,
 // group sums combined in fixed order (deterministic)
 template <typename T>
-__global__ void colsum_reduce(int nb, int N, const double* __restrict__ partial, T* __restrict__ out) {
-  __shared__ double red[8][32];
-  const int c = threadIdx.x & 31, grp = threadIdx.x >> 5;
+__global__ void __launch_bounds__(1024) colsum_reduce(int nb, int N, const double* __restrict__ partial,
+                                                      T* __restrict__ out) {
+  // block = 32 columns x (blockDim / 32) row groups; group g sums rows g, g + G, ...,
+  // then the groups are added in order (deterministic)
+  __shared__ double red[32][33];
+  const int c = threadIdx.x & 31, grp = threadIdx.x >> 5, G = blockDim.x >> 5;
   const int j = blockIdx.x * 32 + c;
   double acc = 0.0;
   if (j < N)
-    for (int b = grp; b < nb; b += 8) acc += partial[(int64_t)b * N + j];
+    for (int b = grp; b < nb; b += G) acc += partial[(int64_t)b * N + j];
   red[grp][c] = acc;
   __syncthreads();
   if (grp == 0 && j < N) {
     double v = 0.0;
-    for (int g = 0; g < 8; ++g) v += red[g][c];
+    for (int g = 0; g < G; ++g) v += red[g][c];
     out[j] = T(v);
   }
 }
@@ -482,7 +485,7 @@ static int tanh_bwd_and_bias(int64_t R, int N, const T* GY, const T* Y, T* GU, d
   const int64_t rows_per = (R + kTanhBlocks - 1) / kTanhBlocks;
   const int nb = (int)((R + rows_per - 1) / rows_per);
   tanh_bwd_bias<T><<<nb, threads, threads * sizeof(double), st>>>(R, N, rows_per, GY, Y, GU, part);
-  colsum_reduce<T><<<(N + 31) / 32, 256, 0, st>>>(nb, N, part, out);
+  colsum_reduce<T><<<(N + 31) / 32, 1024, 0, st>>>(nb, N, part, out);
   QPINN_CUDA_CHECK(cudaGetLastError());
   return QPINN_OK;
 }
@@ -492,7 +495,7 @@ static int bias_grad(int64_t R, int N, const T* GU0, double* part, T* out, cudaS
   const int64_t rows_per = (R + kColBlocks - 1) / kColBlocks;
   const int nb = (int)((R + rows_per - 1) / rows_per);
   colsum_partial<T><<<nb, N < 128 ? 32 * ((N + 31) / 32) : 128, 0, st>>>(R, N, rows_per, GU0, part);
-  colsum_reduce<T><<<(N + 31) / 32, 256, 0, st>>>(nb, N, part, out);
+  colsum_reduce<T><<<(N + 31) / 32, 1024, 0, st>>>(nb, N, part, out);
   QPINN_CUDA_CHECK(cudaGetLastError());
   return QPINN_OK;
 }
@@ -571,9 +574,9 @@ static int backward_impl(const qpinn_trunk_desc* d, int64_t R, const T* x, const
       QPINN_AD(14) QPINN_AD(15) QPINN_AD(16)
 #undef QPINN_AD
     }
-    colsum_reduce<T><<<(H * n + 31) / 32, 256, 0, st>>>(nb, H * n, pwa, grad + d->off_adapter_w);
-    colsum_reduce<T><<<(H + 31) / 32, 256, 0, st>>>(nb, H, pb, grad + d->off_b[d->n_hidden - 1]);
-    colsum_reduce<T><<<(n + 31) / 32, 256, 0, st>>>(nb, n, pba, grad + d->off_adapter_b);
+    colsum_reduce<T><<<(H * n + 31) / 32, 1024, 0, st>>>(nb, H * n, pwa, grad + d->off_adapter_w);
+    colsum_reduce<T><<<(H + 31) / 32, 1024, 0, st>>>(nb, H, pb, grad + d->off_b[d->n_hidden - 1]);
+    colsum_reduce<T><<<(n + 31) / 32, 1024, 0, st>>>(nb, n, pba, grad + d->off_adapter_b);
     QPINN_CUDA_CHECK(cudaGetLastError());
   } else {
     if (int rc = tanh_bwd_and_bias<T>(R, n, g_act, act, g1, part, grad + d->off_adapter_b, st))
