@@ -91,42 +91,53 @@ __device__ __forceinline__ T tau_of(const T* params, int64_t off_tau, T t_dom) {
   return (T(1) + sp) * t_dom;
 }
 
-// periodic map (network.py:133-141) + RFF (network.py:144-147) with tangents
+// periodic map (network.py:133-141) + RFF (network.py:144-147) with tangents.
+// The per-point trig (x, y, t) is computed once per point into shared memory
+// (kFeatPB points per block iteration); the (point, feature) items then stream.
+constexpr int kFeatPB = 32;
 template <typename T>
-__global__ void features_fwd(int64_t R, int F, const T* __restrict__ x, const T* __restrict__ y,
-                             const T* __restrict__ t, const T* __restrict__ omega,
-                             const T* __restrict__ params, int64_t off_tau, T t_dom,
-                             T* __restrict__ H0, int nch) {
+__global__ void __launch_bounds__(256) features_fwd(int64_t R, int F, const T* __restrict__ x,
+                                                    const T* __restrict__ y, const T* __restrict__ t,
+                                                    const T* __restrict__ omega,
+                                                    const T* __restrict__ params, int64_t off_tau,
+                                                    T t_dom, T* __restrict__ H0, int nch) {
+  __shared__ T trig[kFeatPB][6];
   const T tau = tau_of(params, off_tau, t_dom);
-  const int64_t n = R * F;
+  const T w = T(2.0 * kPi) / tau;
   const int64_t W = 2 * (int64_t)F;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t p = i / F;
-    const int f = (int)(i % F);
-    T sx, cx, sy, cy, st, ct;
-    sincospi_t(x[p], &sx, &cx);  // x * 2 pi / lx, lx = 2
-    sincospi_t(y[p], &sy, &cy);
-    const T at = (t[p] * T(2.0 * kPi)) / tau;
-    sincos_t(at, &st, &ct);
-    const T w = T(2.0 * kPi) / tau;
-    const T* om = omega + 6 * f;
-    const T proj = sx * om[0] + cx * om[1] + sy * om[2] + cy * om[3] + st * om[4] + ct * om[5];
-    const T dpx = T(kPi) * cx * om[0] - T(kPi) * sx * om[1];
-    const T dpy = T(kPi) * cy * om[2] - T(kPi) * sy * om[3];
-    const T dpt = w * ct * om[4] - w * st * om[5];
-    T sp, cp;
-    sincos_t(proj, &sp, &cp);
-    H0[p * W + f] = cp;
-    H0[p * W + F + f] = sp;
-    if (nch == 1) continue;  // value only (inference)
-    const T dps[3] = {dpx, dpy, dpt};
-#pragma unroll
-    for (int k = 0; k < 3; ++k) {
-      T* Hk = H0 + (int64_t)(k + 1) * R * W + p * W;
-      Hk[f] = -sp * dps[k];
-      Hk[F + f] = cp * dps[k];
+  for (int64_t p0 = (int64_t)blockIdx.x * kFeatPB; p0 < R; p0 += (int64_t)gridDim.x * kFeatPB) {
+    if (threadIdx.x < kFeatPB && p0 + threadIdx.x < R) {
+      const int64_t p = p0 + threadIdx.x;
+      T* tr = trig[threadIdx.x];
+      sincospi_t(x[p], &tr[0], &tr[1]);  // x * 2 pi / lx, lx = 2
+      sincospi_t(y[p], &tr[2], &tr[3]);
+      const T at = (t[p] * T(2.0 * kPi)) / tau;
+      sincos_t(at, &tr[4], &tr[5]);
     }
+    __syncthreads();
+    const int np = R - p0 < kFeatPB ? (int)(R - p0) : kFeatPB;
+    for (int i = threadIdx.x; i < np * F; i += blockDim.x) {
+      const int pl = i / F, f = i % F;
+      const int64_t p = p0 + pl;
+      const T* tr = trig[pl];
+      const T sx = tr[0], cx = tr[1], sy = tr[2], cy = tr[3], st = tr[4], ct = tr[5];
+      const T* om = omega + 6 * f;
+      const T proj = sx * om[0] + cx * om[1] + sy * om[2] + cy * om[3] + st * om[4] + ct * om[5];
+      T sp, cp;
+      sincos_t(proj, &sp, &cp);
+      H0[p * W + f] = cp;
+      H0[p * W + F + f] = sp;
+      if (nch == 1) continue;  // value only (inference)
+      const T dps[3] = {T(kPi) * cx * om[0] - T(kPi) * sx * om[1],
+                        T(kPi) * cy * om[2] - T(kPi) * sy * om[3], w * ct * om[4] - w * st * om[5]};
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        T* Hk = H0 + (int64_t)(k + 1) * R * W + p * W;
+        Hk[f] = -sp * dps[k];
+        Hk[F + f] = cp * dps[k];
+      }
+    }
+    __syncthreads();
   }
 }
 
@@ -336,52 +347,68 @@ __global__ void __launch_bounds__(1024) colsum_reduce(int nb, int N, const doubl
   }
 }
 
-// dL/dtau_raw through at = 2 pi t / tau and the t-tangent features (one warp per point)
+// dL/dtau_raw through at = 2 pi t / tau and the t-tangent features (one warp per point;
+// the per-point trig of a block's kFeatBPB points is computed once into shared memory)
 // (cos, sin of the projections are read back from the forward's H0 value channel)
+constexpr int kFeatBPB = 64;
 template <typename T>
-__global__ void features_bwd(int64_t R, int F, const T* __restrict__ x, const T* __restrict__ y,
-                             const T* __restrict__ t, const T* __restrict__ omega,
-                             const T* __restrict__ params, int64_t off_tau, T t_dom,
-                             const T* __restrict__ H0, const T* __restrict__ G0,
-                             double* __restrict__ partial) {
+__global__ void __launch_bounds__(256) features_bwd(int64_t R, int F, const T* __restrict__ x,
+                                                    const T* __restrict__ y, const T* __restrict__ t,
+                                                    const T* __restrict__ omega,
+                                                    const T* __restrict__ params, int64_t off_tau,
+                                                    T t_dom, const T* __restrict__ H0,
+                                                    const T* __restrict__ G0,
+                                                    double* __restrict__ partial) {
+  __shared__ T trig[kFeatBPB][7];
   const T tau = tau_of(params, off_tau, t_dom);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, warps = blockDim.x >> 5;
   const int64_t W = 2 * (int64_t)F;
+  const T w = T(2.0 * kPi) / tau;
   double acc = 0.0;
-  for (int64_t p = (int64_t)blockIdx.x * warps + warp; p < R; p += (int64_t)gridDim.x * warps) {
-    T sx, cx, sy, cy, st, ct;
-    sincospi_t(x[p], &sx, &cx);
-    sincospi_t(y[p], &sy, &cy);
-    const T at = (t[p] * T(2.0 * kPi)) / tau;
-    sincos_t(at, &st, &ct);
-    const T w = T(2.0 * kPi) / tau;
-    T G4 = 0, G5 = 0, D4 = 0, D5 = 0;
-    for (int f = lane; f < F; f += 32) {
-      const T* om = omega + 6 * f;
-      const T dps[3] = {T(kPi) * cx * om[0] - T(kPi) * sx * om[1],
-                        T(kPi) * cy * om[2] - T(kPi) * sy * om[3], w * ct * om[4] - w * st * om[5]};
-      const T cp = H0[p * W + f], sp = H0[p * W + F + f];
-      const T gc = G0[p * W + f], gs = G0[p * W + F + f];
-      T gproj = -sp * gc + cp * gs, gdp2 = 0;
-#pragma unroll
-      for (int k = 0; k < 3; ++k) {
-        const T* Gk = G0 + (int64_t)(k + 1) * R * W + p * W;
-        const T gdc = Gk[f], gds = Gk[F + f];
-        gproj += -cp * dps[k] * gdc - sp * dps[k] * gds;
-        if (k == 2) gdp2 = -sp * gdc + cp * gds;
-      }
-      G4 += gproj * om[4];
-      G5 += gproj * om[5];
-      D4 += gdp2 * om[4];
-      D5 += gdp2 * om[5];
+  for (int64_t p0 = (int64_t)blockIdx.x * kFeatBPB; p0 < R; p0 += (int64_t)gridDim.x * kFeatBPB) {
+    if (threadIdx.x < kFeatBPB && p0 + threadIdx.x < R) {
+      const int64_t p = p0 + threadIdx.x;
+      T* tr = trig[threadIdx.x];
+      sincospi_t(x[p], &tr[0], &tr[1]);
+      sincospi_t(y[p], &tr[2], &tr[3]);
+      const T at = (t[p] * T(2.0 * kPi)) / tau;
+      sincos_t(at, &tr[4], &tr[5]);
+      tr[6] = at;
     }
-    // gt is linear in the feature sums, so each lane folds its partial sums with
-    // the point's coefficients and the warp reduces once, after the last point
-    const T dat = -at / tau;
-    const T w2 = T(2.0 * kPi) / (tau * tau);
-    const T gt = G4 * ct * dat + G5 * (-st) * dat + D4 * (-w2 * ct + w2 * at * st) +
-                 D5 * (w2 * st + w2 * at * ct);
-    acc += (double)gt;
+    __syncthreads();
+    for (int pl = warp; pl < kFeatBPB && p0 + pl < R; pl += warps) {
+      const int64_t p = p0 + pl;
+      const T* tr = trig[pl];
+      const T sx = tr[0], cx = tr[1], sy = tr[2], cy = tr[3], st = tr[4], ct = tr[5], at = tr[6];
+      T G4 = 0, G5 = 0, D4 = 0, D5 = 0;
+      for (int f = lane; f < F; f += 32) {
+        const T* om = omega + 6 * f;
+        const T dps[3] = {T(kPi) * cx * om[0] - T(kPi) * sx * om[1],
+                          T(kPi) * cy * om[2] - T(kPi) * sy * om[3], w * ct * om[4] - w * st * om[5]};
+        const T cp = H0[p * W + f], sp = H0[p * W + F + f];
+        const T gc = G0[p * W + f], gs = G0[p * W + F + f];
+        T gproj = -sp * gc + cp * gs, gdp2 = 0;
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+          const T* Gk = G0 + (int64_t)(k + 1) * R * W + p * W;
+          const T gdc = Gk[f], gds = Gk[F + f];
+          gproj += -cp * dps[k] * gdc - sp * dps[k] * gds;
+          if (k == 2) gdp2 = -sp * gdc + cp * gds;
+        }
+        G4 += gproj * om[4];
+        G5 += gproj * om[5];
+        D4 += gdp2 * om[4];
+        D5 += gdp2 * om[5];
+      }
+      // gt is linear in the feature sums, so each lane folds its partial sums with
+      // the point's coefficients and the warp reduces once, after the last point
+      const T dat = -at / tau;
+      const T w2 = T(2.0 * kPi) / (tau * tau);
+      const T gt = G4 * ct * dat + G5 * (-st) * dat + D4 * (-w2 * ct + w2 * at * st) +
+                   D5 * (w2 * st + w2 * at * ct);
+      acc += (double)gt;
+    }
+    __syncthreads();
   }
 #pragma unroll
   for (int m = 16; m >= 1; m >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, m);
@@ -390,7 +417,7 @@ __global__ void features_bwd(int64_t R, int F, const T* __restrict__ x, const T*
   __syncthreads();
   if (threadIdx.x == 0) {
     double v = 0.0;
-    for (int w2 = 0; w2 < warps; ++w2) v += red[w2];
+    for (int w3 = 0; w3 < warps; ++w3) v += red[w3];
     partial[blockIdx.x] = v;
   }
 }
@@ -507,7 +534,9 @@ static int forward_impl(const qpinn_trunk_desc* d, int64_t R, const T* x, const 
   const TrunkWS w = trunk_ws(d, sizeof(T), R);
   const int F = d->rff, H = d->hidden, n = d->n_out;
   T* H0 = (T*)(ws + w.h0);
-  features_fwd<T><<<grid_1d(R * F), 256, 0, st>>>(R, F, x, y, t, (const T*)d->omega, params,
+  const int fb = (int)((R + kFeatPB - 1) / kFeatPB < num_sms() * 8 ? (R + kFeatPB - 1) / kFeatPB
+                                                                   : num_sms() * 8);
+  features_fwd<T><<<fb > 0 ? fb : 1, 256, 0, st>>>(R, F, x, y, t, (const T*)d->omega, params,
                                                   d->off_tau_raw, (T)d->t_domain, H0, nch);
   QPINN_CUDA_CHECK(cudaGetLastError());
   const T* in = H0;
