@@ -190,6 +190,7 @@ class _DevChunk:
     bins: torch.Tensor
     is_ic: torch.Tensor
     spec: N.LossSpec = field(default=None)
+    xyt: torch.Tensor = field(default=None)  # [3, R]; x, y, t are its rows (one H2D copy)
 
 
 class _LossFn(torch.autograd.Function):
@@ -320,12 +321,11 @@ class LossEvaluator:
     def _dev_chunk(self, sl):
         g, dev, dt = self.grid, self.device, self.dtype
         k = len(sl)
-        x = torch.as_tensor(np.tile(g.x_slice, k), dtype=dt, device=dev)
-        y = torch.as_tensor(np.tile(g.y_slice, k), dtype=dt, device=dev)
-        t = torch.as_tensor(np.repeat(g.ts[sl], g.slice_size), dtype=dt, device=dev)
+        xyt = torch.as_tensor(np.stack([np.tile(g.x_slice, k), np.tile(g.y_slice, k),
+                                        np.repeat(g.ts[sl], g.slice_size)]), dtype=dt, device=dev)
         bins = torch.as_tensor(self.bin_slices[sl].astype(np.int32), device=dev)
         is_ic = torch.as_tensor((np.asarray(sl) == 0).astype(np.int32), device=dev)
-        ch = _DevChunk(list(sl), x, y, t, bins, is_ic)
+        ch = _DevChunk(list(sl), xyt[0], xyt[1], xyt[2], bins, is_ic, xyt=xyt)
         ch.spec = self._spec(ch)
         return ch
 

@@ -294,13 +294,13 @@ class Trainer:
         if not on:
             self._host_inputs = None
             return
-        self._host_inputs = [tuple(v.detach().cpu().pin_memory() for v in (ch.x, ch.y, ch.t))
-                             for ch in self.evaluator.chunks]
+        # one pinned [3, R] block per chunk (x, y, t rows): one H2D copy per chunk
+        self._host_inputs = [ch.xyt.detach().cpu().pin_memory() for ch in self.evaluator.chunks]
 
     def host_input_bytes(self) -> int:
         if not self._host_inputs:
             return 0
-        return sum(v.numel() * v.element_size() for hs in self._host_inputs for v in hs)
+        return sum(v.numel() * v.element_size() for v in self._host_inputs)
 
     def readback_bytes(self) -> int:
         return 11 * 8 + (32 if self.log_grad else 0)
@@ -328,10 +328,8 @@ class Trainer:
     def _local_sweep(self):
         """Input copies and the sweep (forward + backward) over this rank's chunks."""
         if self._host_inputs is not None:
-            for ch, (hx, hy, ht) in zip(self.evaluator.chunks, self._host_inputs):
-                ch.x.copy_(hx, non_blocking=True)
-                ch.y.copy_(hy, non_blocking=True)
-                ch.t.copy_(ht, non_blocking=True)
+            for ch, h in zip(self.evaluator.chunks, self._host_inputs):
+                ch.xyt.copy_(h, non_blocking=True)
         self.sums.zero_()
         return self._sweep(self.grad, self.weights, True, self.sums)
 
