@@ -146,6 +146,11 @@ int qpinn_pqc_backward(const qpinn_circuit* c, int dtype, int scale, int64_t row
  * clamp those values, as the reference does with a warning). */
 int qpinn_pqc_domain_check(const void* workspace, void* stream, double* max_abs,
                            int* clamped);
+/* Asynchronous half of the check, for a caller that synchronises anyway: enqueues
+ * on `stream` the copy of the running max|act_val| (a double) into `host_dst`
+ * (8 bytes, pinned) and its reset; apply the rule above to the value after the
+ * caller's own synchronisation (no extra host round trip per step). */
+int qpinn_pqc_domain_fetch(const void* workspace, void* host_dst, void* stream);
 
 /* ---- classical trunk with forward-mode tangents (network.py:133-147, :284-298)
  * periodic map -> frozen RFF -> tanh hidden layers -> tanh adapter, carried as

@@ -73,6 +73,7 @@ SIGNATURES = [
                                 _VP, _VP, _SZ, _VP]),
     ("qpinn_pqc_forward_probe", _I, [_VP, _I, _I, _I64, _VP, _VP, _VP, _VP, _VP, _SZ, _VP]),
     ("qpinn_pqc_domain_check", _I, [_VP, _VP, C.POINTER(_D), C.POINTER(_I)]),
+    ("qpinn_pqc_domain_fetch", _I, [_VP, _VP, _VP]),
     ("qpinn_loss_workspace_bytes", _SZ, [C.POINTER(LossSpec), _I, _I64]),
     ("qpinn_loss_forward_backward", _I, [C.POINTER(LossSpec), _I, _I64, _VP, _VP, _VP, _VP,
                                          _VP, _VP, _VP, _SZ, _VP]),

@@ -263,6 +263,15 @@ def check_domain(circuit: CircuitSpec, dtype, device, stream=None, ws=None) -> f
     return m.value
 
 
+def domain_rule(m: float) -> None:
+    """The reference domain rule (ansatz.py:51-58) on a fetched max|a|."""
+    over = m - 1.0
+    if over > 1e-12:
+        raise DomainError(f"scale input exceeds [-1, 1] by {over:.3e}")
+    if over > 0.0:
+        warnings.warn("scale input clamped into [-1, 1] (excursion <= 1e-12)", stacklevel=3)
+
+
 def state_buffer(circuit: CircuitSpec, a) -> torch.Tensor:
     """Final-state hand-off buffer K1 -> K2 (4 states x 2^n complex per row)."""
     nbytes = N.lib().qpinn_pqc_state_bytes(circuit.handle, N.dtype_code(a.dtype), a.shape[0])

@@ -908,6 +908,14 @@ int qpinn_pqc_forward_probe(const qpinn_circuit* cc, int dtype, int scale, int64
   return rc == KERNEL_NONE ? fail(QPINN_ERR_CAPACITY, "probe: no layer kernel") : rc;
 }
 
+int qpinn_pqc_domain_fetch(const void* workspace, void* host_dst, void* stream) {
+  if (!workspace || !host_dst) return fail(QPINN_ERR_CONFIG, "domain fetch: null pointer");
+  QPINN_CUDA_CHECK(cudaMemcpyAsync(host_dst, workspace, 8, cudaMemcpyDeviceToHost,
+                                   (cudaStream_t)stream));
+  QPINN_CUDA_CHECK(cudaMemsetAsync(const_cast<void*>(workspace), 0, 8, (cudaStream_t)stream));
+  return QPINN_OK;
+}
+
 int qpinn_pqc_domain_check(const void* workspace, void* stream, double* max_abs, int* clamped) {
   unsigned long long bits = 0;
   QPINN_CUDA_CHECK(cudaStreamSynchronize((cudaStream_t)stream));

@@ -16,6 +16,7 @@ step path and are not part of this engine.
 """
 from __future__ import annotations
 
+import ctypes as C
 import time
 from dataclasses import dataclass, field, replace
 from typing import Callable, List, Optional, Sequence
@@ -276,6 +277,7 @@ class Trainer:
         self._packed = None
         self.log_grad = log_grad
         self._host = torch.zeros(16, dtype=torch.float64, pin_memory=True)
+        self._host_dom = torch.zeros(1, dtype=torch.float64, pin_memory=True)
         if config.adaptive_weighting:
             # untaped initial pass (training.py:336-339)
             bins = self._evaluate_untaped()
@@ -303,7 +305,7 @@ class Trainer:
         return sum(v.numel() * v.element_size() for v in self._host_inputs)
 
     def readback_bytes(self) -> int:
-        return 11 * 8 + (32 if self.log_grad else 0)
+        return 11 * 8 + 8 + (32 if self.log_grad else 0)  # loss record + flag, max|a|
 
     def _evaluate_untaped(self):
         sums = torch.zeros(N.LOSS_NSUMS, dtype=torch.float64, device=self.device)
@@ -391,8 +393,15 @@ class Trainer:
             if q.numel():
                 host[13:14].copy_(torch.linalg.vector_norm(q).reshape(1), non_blocking=True)
                 host[14:15].copy_(torch.var(q, unbiased=False).reshape(1), non_blocking=True)
+        if self.model.circuit is not None:  # max|a| rides along with the step's one sync
+            ws = self.model.circuit.workspace(self.model.dtype, self.device, 0)
+            N.check(N.lib().qpinn_pqc_domain_fetch(C.c_void_p(ws.data_ptr()),
+                                                   C.c_void_p(self._host_dom.data_ptr()),
+                                                   C.c_void_p(N.stream_ptr())), "domain fetch")
         torch.cuda.current_stream().synchronize()
-        self._check_domain()
+        if self.model.circuit is not None:
+            from .ansatz import domain_rule
+            domain_rule(float(self._host_dom[0]))
         v = host.numpy()
         f = int(v[10])
         if f:
