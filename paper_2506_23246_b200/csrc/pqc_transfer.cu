@@ -29,6 +29,7 @@ namespace qpinn {
 namespace {
 
 constexpr int kTrThreads = 64;  // circuit kernels: one thread per amplitude pair (D <= 128)
+constexpr int kTrMaxN = 7;      // transfer-matrix path: n <= 7
 
 // u1 matrices [n_u1][4] and phase diagonals [n_phase][D] (as gb_tables, pqc_global.cu)
 __global__ void tr_tables(PlanDev p, const float* __restrict__ qp, cplx<float>* __restrict__ U,
@@ -119,7 +120,7 @@ __global__ void __launch_bounds__(kTrThreads) tr_circuit_bwd(
     const cplx<float>* __restrict__ CK, double* __restrict__ part_u1,
     double* __restrict__ part_ph) {
   __shared__ cplx<float> s[2][128];
-  __shared__ double red[2 * 8];
+  __shared__ double red[2 * 8 * kTrMaxN];
   const int D = 1 << n, j = blockIdx.x, t = threadIdx.x, n_u1 = n * L;
   int cur = 0;
   for (int b = t; b < D; b += kTrThreads) s[0][b] = Abar[(size_t)j * D + b];
@@ -138,21 +139,36 @@ __global__ void __launch_bounds__(kTrThreads) tr_circuit_bwd(
       }
       __syncthreads();
     }
-    for (int q = 0; q < n; ++q) {
-      double m[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-      for (int k = t; k < D / 2; k += kTrThreads) {
-        int i0, i1;
-        pair_index(k, n - 1 - q, i0, i1);
-        const cplx<float> x0 = xl[i0], x1 = xl[i1], a0 = s[cur][i0], a1 = s[cur][i1];
-        float f[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-        cmac_c(f[0], f[1], a0, x0);
-        cmac_c(f[2], f[3], a0, x1);
-        cmac_c(f[4], f[5], a1, x0);
-        cmac_c(f[6], f[7], a1, x1);
-        for (int e = 0; e < 8; ++e) m[e] += (double)f[e];
+    // all of the layer's outer products from the same (adjoint, checkpoint) pair,
+    // then one block reduction for the layer (8 n sums)
+    double m[8 * kTrMaxN];
+#pragma unroll
+    for (int e = 0; e < 8 * kTrMaxN; ++e) m[e] = 0.0;
+#pragma unroll
+    for (int q = 0; q < kTrMaxN; ++q) {
+      if (q < n) {
+        for (int k = t; k < D / 2; k += kTrThreads) {
+          int i0, i1;
+          pair_index(k, n - 1 - q, i0, i1);
+          const cplx<float> x0 = xl[i0], x1 = xl[i1], a0 = s[cur][i0], a1 = s[cur][i1];
+          float f[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+          cmac_c(f[0], f[1], a0, x0);
+          cmac_c(f[2], f[3], a0, x1);
+          cmac_c(f[4], f[5], a1, x0);
+          cmac_c(f[6], f[7], a1, x1);
+#pragma unroll
+          for (int e = 0; e < 8; ++e) m[8 * q + e] += (double)f[e];
+        }
       }
-      block_sum<8>(m, red);
-      if (t < 8) part_u1[((size_t)j * n_u1 + l * n + q) * 8 + t] = m[t];
+    }
+    block_sum<8 * kTrMaxN>(m, red);
+    if (t < 8 * n) {
+      // m is uniform after the sum: pick entry t without dynamic register indexing
+      double v = 0.0;
+#pragma unroll
+      for (int e = 0; e < 8 * kTrMaxN; ++e)
+        if (e == t) v = m[e];
+      part_u1[((size_t)j * n_u1 + l * n) * 8 + t] = v;
     }
     for (int q = 0; q < n; ++q) {
       const cplx<float>* u = U + 4 * (l * n + q);
