@@ -222,6 +222,28 @@ __global__ void tanh_bwd_bias(int64_t R, int N, int64_t rows_per, const T* __res
 // four channels of a point meet in one block; reduced later in block order).
 // Replaces two library GEMMs and two elementwise passes; G_H never hits HBM.
 constexpr int kAdMaxN = 16;
+
+// NV contiguous values from 16-byte aligned shared memory with vector loads
+template <typename T, int NV>
+__device__ __forceinline__ void lds_vec(const T* src, T (&dst)[NV]) {
+  if constexpr (sizeof(T) == 4) {
+#pragma unroll
+    for (int i = 0; i < NV / 4; ++i) {
+      const float4 v = reinterpret_cast<const float4*>(src)[i];
+      dst[4 * i] = v.x;
+      dst[4 * i + 1] = v.y;
+      dst[4 * i + 2] = v.z;
+      dst[4 * i + 3] = v.w;
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < NV / 2; ++i) {
+      const double2 v = reinterpret_cast<const double2*>(src)[i];
+      dst[2 * i] = v.x;
+      dst[2 * i + 1] = v.y;
+    }
+  }
+}
 template <typename T, int NA>
 __global__ void __launch_bounds__(128) adapter_bwd(int64_t R, int Hd, int64_t rows_per, const T* __restrict__ g_act,
                             const T* __restrict__ act, const T* __restrict__ Hl,
@@ -229,7 +251,8 @@ __global__ void __launch_bounds__(128) adapter_bwd(int64_t R, int Hd, int64_t ro
                             double* __restrict__ part_wa, double* __restrict__ part_b,
                             double* __restrict__ part_ba) {
   constexpr int n = NA;
-  __shared__ T gua[32][4][NA];
+  constexpr int NAP = (NA + 3) / 4 * 4;  // padded rows: vector shared-memory loads
+  __shared__ __align__(16) T gua[32][4][NAP];
   const int tid = threadIdx.x;
   const int j = tid;  // column of the hidden layer
   const bool col = j < Hd;
@@ -278,13 +301,16 @@ __global__ void __launch_bounds__(128) adapter_bwd(int64_t R, int Hd, int64_t ro
         const int pt = pb + u;
         if (pt >= np) break;
         const int64_t i = (p0 + pt) * Hd + j;
+        T gv[4][NAP];  // the point's adapter gradients, 16-byte shared loads (broadcast)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) lds_vec<T, NAP>(&gua[pt][c][0], gv[c]);
         T h[4], gh[4];
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
           h[c] = hb[u][c];
           T v = T(0);
 #pragma unroll
-          for (int k = 0; k < NA; ++k) v += gua[pt][c][k] * wrow[k];
+          for (int k = 0; k < NA; ++k) v += gv[c][k] * wrow[k];
           gh[c] = v;
         }
         const T s = T(1) - h[0] * h[0];
@@ -296,8 +322,7 @@ __global__ void __launch_bounds__(128) adapter_bwd(int64_t R, int Hd, int64_t ro
         acc_b += (double)gu0;
 #pragma unroll
         for (int k = 0; k < NA; ++k)
-          acc_w[k] += h[0] * gua[pt][0][k] + h[1] * gua[pt][1][k] + h[2] * gua[pt][2][k] +
-                      h[3] * gua[pt][3][k];
+          acc_w[k] += h[0] * gv[0][k] + h[1] * gv[1][k] + h[2] * gv[2][k] + h[3] * gv[3][k];
       }
       }
     }
