@@ -471,7 +471,7 @@ __device__ __forceinline__ float flip_get(const float (&v)[J], int j, int q) {
 //   g_th[q] = Re sum conj(eta) X_q phi, g_dth[k][q] = Re sum conj((i/2) mu_k) X_q phi
 // phibar, mu_k = rows of gPhi; phi is re-embedded in registers
 #ifndef QPINN_TR_EG_MINB
-#define QPINN_TR_EG_MINB 1
+#define QPINN_TR_EG_MINB 3
 #endif
 template <int NQ>
 __global__ void __launch_bounds__(256, QPINN_TR_EG_MINB) tr_embed_grad(int scale, int64_t R,
