@@ -329,8 +329,11 @@ __device__ __forceinline__ void for_points(int64_t R, F&& body) {
 }
 
 // Phi rows: [Re | Im] of the embedded state and its tangents
+#ifndef QPINN_TR_EMB_MINB
+#define QPINN_TR_EMB_MINB 4
+#endif
 template <int NQ>
-__global__ void __launch_bounds__(256) tr_embed(int scale, int64_t R, const float* __restrict__ act,
+__global__ void __launch_bounds__(256, QPINN_TR_EMB_MINB) tr_embed(int scale, int64_t R, const float* __restrict__ act,
                                                 const float* __restrict__ tan,
                                                 float* __restrict__ Phi,
                                                 unsigned long long* __restrict__ maxabs) {
