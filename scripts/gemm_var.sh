@@ -1,5 +1,5 @@
 cd $GRAFT_REPO_ROOT
-for v in nb2os4 nb2os4p2 nb2os2; do
+for v in default p2 p4; do
   if [ $v = default ]; then unset QPINN_LIB_OVERRIDE; else export QPINN_LIB_OVERRIDE=$PWD/exp/$v.so; fi
   echo "== $v"; python scripts/gemm_check.py 2>&1 | grep -E "262144|atb rows=262144" | sed 's/torch fp32 [0-9.e-]*;//'
 done
