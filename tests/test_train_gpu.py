@@ -27,7 +27,9 @@ def _build(g, dtype):
 
 
 EVALS = ["eval_micro_vacuum.npz", "eval_micro_diel.npz", "eval_micro_asym.npz", "eval_desk.npz",
-         "eval_vacuum7.npz", "eval_diel7.npz"]
+         "eval_vacuum7.npz", "eval_diel7.npz",
+         # 6 qubits: the transfer-matrix PQC kernels (permutation and phase entanglers)
+         "eval_n6_strongly.npz", "eval_n6_crossmesh.npz"]
 
 
 @pytest.mark.parametrize("dtype", [torch.float64, torch.float32])
