@@ -293,11 +293,52 @@ class Trainer:
 
     # -- end-to-end mode: collocation inputs come from pinned host memory ------
     def set_host_inputs(self, on: bool) -> None:
+        """End-to-end mode: every step's collocation inputs come from pinned host
+        memory, one [3, R] H2D copy per chunk.  The device inputs are double
+        buffered: step k runs on buffer k % 2 while the copy of step k+1's inputs
+        fills the other buffer on a side stream (an input pipeline's prefetch;
+        each step still moves its own inputs host -> device)."""
+        if self._host_inputs is not None:
+            self._bind_inputs(0)
         if not on:
             self._host_inputs = None
             return
-        # one pinned [3, R] block per chunk (x, y, t rows): one H2D copy per chunk
-        self._host_inputs = [ch.xyt.detach().cpu().pin_memory() for ch in self.evaluator.chunks]
+        chunks = self.evaluator.chunks
+        self._host_inputs = [ch.xyt.detach().cpu().pin_memory() for ch in chunks]
+        self._in_bufs = [(ch.xyt, torch.empty_like(ch.xyt)) for ch in chunks]
+        self._in_par = 0
+        self._copy_stream = torch.cuda.Stream(device=self.device)
+        self._copy_done = [torch.cuda.Event(), torch.cuda.Event()]
+        for (b0, _), h in zip(self._in_bufs, self._host_inputs):  # the first step's inputs
+            b0.copy_(h)
+        torch.cuda.current_stream().synchronize()
+        self._copy_pending = [False, False]
+
+    def _bind_inputs(self, par: int) -> None:
+        for ch, bufs in zip(self.evaluator.chunks, self._in_bufs):
+            b = bufs[par]
+            ch.xyt, ch.x, ch.y, ch.t = b, b[0], b[1], b[2]
+
+    def _use_inputs(self) -> int:
+        """Bind this step's input buffer (waiting for its copy); returns its parity."""
+        par = self._in_par
+        if self._copy_pending[par]:
+            torch.cuda.current_stream().wait_event(self._copy_done[par])
+            self._copy_pending[par] = False
+        self._bind_inputs(par)
+        return par
+
+    def _prefetch_inputs(self) -> None:
+        """Start the next step's H2D copy into the other buffer (enqueued after this
+        step's launches, so the host work overlaps the device work); the other
+        buffer's last reader, the previous step, has finished: step() synchronises."""
+        nxt = 1 - self._in_par
+        with torch.cuda.stream(self._copy_stream):
+            for bufs, h in zip(self._in_bufs, self._host_inputs):
+                bufs[nxt].copy_(h, non_blocking=True)
+            self._copy_done[nxt].record(self._copy_stream)
+        self._copy_pending[nxt] = True
+        self._in_par = nxt
 
     def host_input_bytes(self) -> int:
         if not self._host_inputs:
@@ -328,10 +369,7 @@ class Trainer:
         return grad
 
     def _local_sweep(self):
-        """Input copies and the sweep (forward + backward) over this rank's chunks."""
-        if self._host_inputs is not None:
-            for ch, h in zip(self.evaluator.chunks, self._host_inputs):
-                ch.xyt.copy_(h, non_blocking=True)
+        """The sweep (forward + backward) over this rank's chunks."""
         self.sums.zero_()
         return self._sweep(self.grad, self.weights, True, self.sums)
 
@@ -348,11 +386,11 @@ class Trainer:
         graph; the collective and the finalisation run eagerly after it, so the
         NCCL all-reduce is never captured.  Eager throughout while per-kernel
         event timing is on."""
+        par = self._use_inputs() if self._host_inputs is not None else -1
         if not self.use_graphs or self.epoch < 1 or N.timing_enabled():
             grad = self._local_sweep()
         else:
-            key = (self.weights.data_ptr() if self.weights is not None else 0,
-                   self._host_inputs is not None)
+            key = (self.weights.data_ptr() if self.weights is not None else 0, par)
             entry = self._graphs.get(key)
             if entry is None:
                 g = torch.cuda.CUDAGraph()
@@ -365,6 +403,8 @@ class Trainer:
             entry[0].replay()
             N.count_launches(entry[1])
             grad = self.grad
+        if self._host_inputs is not None:
+            self._prefetch_inputs()
         self._reduce_finalize(grad)
         return grad
 
