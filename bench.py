@@ -148,6 +148,51 @@ def fp32_peak():
                                    f"(imm {a.value:.1f}, reg {b.value:.1f} TFLOP/s)")
 
 
+def tensor_gemm_roofline(n_qubits: int, R: int):
+    """The transfer map's 3xTF32 tcgen05 GEMM ([4R, 2D] x [2D, 2D]) timed alone with CUDA
+    events, against cuBLAS's own TF32 peak measured in the same run (8192^3, the
+    ceiling for this MMA kind on this box; MEASURED_PEAKS.json has bf16 only).
+    achieved = the TF32 MMA work issued (3 products) / time."""
+    import torch
+    from paper_2506_23246_b200 import _native as N
+    lib = N.lib()
+    M, n = 4 * R, 2 << n_qubits
+    A = torch.randn(M, n, device="cuda")
+    B = torch.randn(n, n, device="cuda")
+    Cm = torch.empty(M, n, device="cuda")
+    ws = torch.empty(lib.qpinn_gemm_f32_workspace_bytes(n, n), dtype=torch.uint8, device="cuda")
+
+    def gemm():
+        N.check(lib.qpinn_gemm_f32(M, n, n, A.data_ptr(), n, B.data_ptr(), n, Cm.data_ptr(), n,
+                                   ws.data_ptr(), ws.numel(), N.stream_ptr()), "gemm")
+
+    def timed(fn, k):
+        for _ in range(3):
+            fn()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(k):
+            fn()
+        e1.record()
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) / k
+
+    ms = timed(gemm, 20)
+    prev = torch.backends.cuda.matmul.allow_tf32
+    torch.backends.cuda.matmul.allow_tf32 = True
+    a = torch.randn(8192, 8192, device="cuda")
+    b = torch.randn(8192, 8192, device="cuda")
+    ms_pk = timed(lambda: a @ b, 10)
+    torch.backends.cuda.matmul.allow_tf32 = prev
+    peak = 2 * 8192 ** 3 / (ms_pk * 1e-3) / 1e12
+    achieved = 3 * 2 * M * n * n / (ms * 1e-3) / 1e12
+    return {"bound": "tensor", "achieved": round(achieved, 1), "peak": round(peak, 1),
+            "unit": "TFLOP/s", "frac": round(achieved / peak, 4), "traffic": None,
+            "shape": [M, n, n], "ms_per_launch": round(ms, 4),
+            "flop_counting": "TF32 MMA work issued: 3 products x 2 M N K (3xTF32, FP32-class)",
+            "peak_source": "measured in-run: cuBLAS TF32 GEMM 8192^3 (torch, allow_tf32)"}
+
+
 # -- CPU reference (baseline/_ref qpinn, else the oracle port) --------------------------
 
 def _import_reference():
@@ -353,6 +398,8 @@ def run_ours(args):
                             "share_of_step": round(mean_ms * launches_per_step / (ms_prof / args.steps), 4),
                             "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy bandwidth)"}
         dom = max(rl, key=lambda k: rl[k]["share_of_step"]) if rl else None
+        if transfer and dtype == torch.float32:  # the tensor-core kernel inside the PQC passes
+            rl["transfer_gemm"] = tensor_gemm_roofline(circuit.n_qubits, R_local)
         cpu = None
         if world == 1 and not args.no_cpu_baseline:
             v, kind, cores, sample, _ = cpu_reference_rate(grid, args.cpu_seconds)
