@@ -25,7 +25,11 @@ for r in data:
         if m not in col:
             out.append(f"{'-':>12s}")
             continue
-        v = float(r[col[m]].replace(",", "") or 0)
+        try:
+            v = float(r[col[m]].replace(",", "") or 0)
+        except ValueError:  # "no data" for this kernel
+            out.append(f"{'n/a':>12s}")
+            continue
         if sc is None:
             v *= scale_mb.get(units[col[m]], 1e-6)
         elif label == "time_us":
