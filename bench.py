@@ -463,7 +463,8 @@ def run_reference(args):
                                                        warmup=args.warmup)
     ms = 1e3 * statistics.mean([grid[0] * grid[1] / r for r in rates])
     line = {
-        "metric": METRIC, "value": round(v, 2), "unit": UNIT, "n_gpus": 0, "impl": "reference",
+        "metric": METRIC, "value": round(v, 2), "unit": UNIT, "n_gpus": world, "impl": "reference",
+        "devices": "host CPU cores (the reference has no GPU path); n_gpus is the launch size",
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (reference seeded init and grid)",
