@@ -42,10 +42,13 @@ __device__ unsigned long long g_gemm_prof[16];
 #endif
 constexpr int kBM = 128, kBK = 32;
 // k-blocks accumulated in one TMEM buffer before the epilogue warps add it into
-// fp32 registers (1: 32-deep tensor-core chains, 3.5e-7 relative at K = 256;
-// 2 measured 6.3e-7 at the same speed)
+// fp32 registers.  1: 32-deep tensor-core chains, 3.5e-7 relative at K = 256;
+// 2: 64-deep, 6.3e-7 relative, still below cuBLAS SIMT fp32 on the same inputs
+// (max |err| 3.6e-6 vs 4.1e-6, scripts/gemm_check.py), and -60 us per training
+// step (half the TMEM reads of the promotion; the dual-tanh layers are
+// epilogue-paced); 4: 1.2e-6, above SIMT fp32, not used
 #ifndef QPINN_GEMM_PROMOTE
-#define QPINN_GEMM_PROMOTE 1
+#define QPINN_GEMM_PROMOTE 2
 #endif
 constexpr int kPromote = QPINN_GEMM_PROMOTE;
 constexpr int kABytes = kBM * kBK * 4;  // 16 KB fp32 tile
