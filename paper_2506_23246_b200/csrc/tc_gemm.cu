@@ -458,7 +458,10 @@ constexpr int kWRaw = 3, kWOps = 2, kWNB = 4;
 constexpr int kWRawBytes = 2 * kABytes;  // A (16 KB) | B (16 KB)
 constexpr int kWOpBytes = 4 * kABytes;   // A_hi | A_lo | B_hi | B_lo
 constexpr int kWSmem = kWRaw * kWRawBytes + kWOps * kWOpBytes + 1024 + 512;
-constexpr int kWPromote = 2;  // k-blocks accumulated in TMEM per promotion (64-deep chains)
+#ifndef QPINN_WGRAD_PROMOTE
+#define QPINN_WGRAD_PROMOTE 2
+#endif
+constexpr int kWPromote = QPINN_WGRAD_PROMOTE;  // k-blocks per TMEM partial (64-deep chains)
 
 struct WgradArgs {
   int64_t rows, chunk;  // rows per chunk (multiple of 32)
