@@ -86,6 +86,12 @@ class ClockSampler:
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
+            # nvidia-smi needs ~0.1-0.5 s before its first sample: do not
+            # start the timed region before it is sampling
+            t0 = time.time()
+            while not self.lines and time.time() - t0 < 3.0 and self.proc.poll() is None:
+                time.sleep(0.01)
+            self.lines.clear()
         except OSError:
             self.proc = None
         return self
@@ -317,8 +323,9 @@ def run_ours(args):
     for _ in range(max(args.warmup, 3)):
         tr.step()
     launches0 = N.LAUNCHES["count"]
-    with ClockSampler(gpu_id_for(local)) as clk:
-        ms = timed_steps(args.steps)
+    # clocks are sampled across the three timed passes (value, per-kernel, e2e)
+    clk = ClockSampler(gpu_id_for(local)).__enter__()
+    ms = timed_steps(args.steps)
     launches = (N.LAUNCHES["count"] - launches0)
     value = n_total * args.steps / (ms / 1e3)
 
@@ -333,6 +340,7 @@ def run_ours(args):
     for _ in range(2):
         tr.step()
     ms_e2e = timed_steps(args.steps)
+    clk.__exit__(None, None, None)
     e2e_value = n_total * args.steps / (ms_e2e / 1e3)
     h2d = tr.host_input_bytes()
     d2h = tr.readback_bytes()
@@ -349,19 +357,28 @@ def run_ours(args):
         if transfer:  # K1/K2 as tensor-core GEMMs over HBM-staged operands
             tb = transfer_bytes(circuit.n_qubits)
             tf = transfer_flops(circuit.n_qubits)
-            for name, per_pt, fl in (("pqc_forward", tb[0], tf[0]), ("pqc_backward", tb[1], tf[1])):
+            for name, per_pt, fl, fc in (("pqc_forward", tb[0], tf[0], f_fwd),
+                                         ("pqc_backward", tb[1], tf[1], f_adj)):
                 if name not in kern:
                     continue
                 nl, mean_ms = kern[name]
                 launches_per_step = nl / args.steps
                 pts_per_launch = R_local / launches_per_step
                 achieved = per_pt * pts_per_launch / (mean_ms * 1e-3) / 1e9
+                # the north_star's "fraction of the FP32 compute roofline": the
+                # circuit's algorithmic FLOPs (SURVEY 8d gate-sweep count,
+                # roofline.pqc_flops) per second against the FFMA peak
+                circ = fc * pts_per_launch / (mean_ms * 1e-3) / 1e12
                 rl[name] = {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm,
                             "unit": "GB/s", "frac": round(achieved / hbm, 4),
                             "traffic": traffic_for(name, pts_per_launch),
                             "bytes_per_point": per_pt, "points_per_launch": pts_per_launch,
                             "gemm_flop_per_point": fl,
                             "gemm_tflops": round(fl * pts_per_launch / (mean_ms * 1e-3) / 1e12, 2),
+                            "circuit_flop_per_point": fc,
+                            "circuit_tflops": round(circ, 2),
+                            "fp32_peak_tflops": round(peak, 3) if peak else None,
+                            "fp32_frac": round(circ / peak, 4) if peak else None,
                             "ms_per_launch": round(mean_ms, 4),
                             "share_of_step": round(mean_ms * launches_per_step / (ms_prof / args.steps), 4),
                             "path": "transfer matrix (3xTF32 tcgen05 GEMMs)",

@@ -13,6 +13,7 @@ from __future__ import annotations
 
 import ctypes as C
 import warnings
+import weakref
 from dataclasses import dataclass, field
 from enum import Enum
 from typing import Optional, Tuple
@@ -313,29 +314,87 @@ def pqc_backward_raw(circuit: CircuitSpec, scale_kind, a, da, qp, gz, gdz, state
     return ga, gda, gq
 
 
-class _PQC(torch.autograd.Function):
-    """K1 forward; K2 adjoint backward (gradients of values *and* tangents)."""
+# -- torch custom ops (SURVEY §8 b): torch.ops.qpinn_b200.pqc_fwd_tangent / pqc_bwd_adjoint --
+#
+# The plan descriptor crosses the op boundary as an integer token for a live
+# CircuitSpec (ops schemas carry tensors and scalars only); the K1 -> K2 state
+# hand-off is an ordinary tensor output, so the ops are functional.
 
-    @staticmethod
-    def forward(ctx, a, da, qp, circuit, scale_kind):
-        need_grad = any(ctx.needs_input_grad[:3])
-        states = state_buffer(circuit, a) if need_grad else None
-        z, dz = pqc_forward_raw(circuit, scale_kind, a, da, qp, states)
-        ctx.states = states
-        ctx.save_for_backward(a, da, qp)
-        ctx.circuit = circuit
-        ctx.scale_kind = scale_kind
-        return z, dz
+_PLANS: "weakref.WeakValueDictionary[int, CircuitSpec]" = weakref.WeakValueDictionary()
 
-    @staticmethod
-    def backward(ctx, gz, gdz):
-        a, da, qp = ctx.saved_tensors
-        gz = torch.zeros_like(a) if gz is None else gz.contiguous()
-        gdz = torch.zeros_like(da) if gdz is None else gdz.contiguous()
-        ga, gda, gq = pqc_backward_raw(ctx.circuit, ctx.scale_kind, a, da, qp, gz, gdz,
-                                       ctx.states)
-        ctx.states = None
-        return ga, gda, gq, None, None
+
+def plan_token(circuit: CircuitSpec) -> int:
+    """Integer handle of ``circuit`` for the ``torch.ops.qpinn_b200`` schemas."""
+    tok = id(circuit)
+    _PLANS[tok] = circuit
+    return tok
+
+
+def _plan(tok: int) -> CircuitSpec:
+    c = _PLANS.get(tok)
+    if c is None:
+        raise ConfigError(f"unknown circuit plan token {tok}")
+    return c
+
+
+@torch.library.custom_op("qpinn_b200::pqc_fwd_tangent", mutates_args=())
+def pqc_fwd_tangent(plan: int, scale_kind: str, act_val: torch.Tensor, act_tan: torch.Tensor,
+                    qparams: torch.Tensor, save_states: bool
+                    ) -> Tuple[torch.Tensor, torch.Tensor, torch.Tensor]:
+    """K1: (z [R,n], dz [3,R,n], states); ``states`` is empty unless
+    ``save_states`` (ansatz.py:341-400)."""
+    c = _plan(plan)
+    states = (state_buffer(c, act_val) if save_states
+              else act_val.new_empty(0))
+    z, dz = pqc_forward_raw(c, scale_kind, act_val, act_tan, qparams,
+                            states if save_states else None)
+    return z, dz, states
+
+
+@pqc_fwd_tangent.register_fake
+def _(plan, scale_kind, act_val, act_tan, qparams, save_states):
+    c = _plan(plan)
+    n_states = 0
+    if save_states:
+        nbytes = N.lib().qpinn_pqc_state_bytes(c.handle, N.dtype_code(act_val.dtype),
+                                              act_val.shape[0])
+        n_states = nbytes // act_val.element_size()
+    return (torch.empty_like(act_val), torch.empty_like(act_tan),
+            act_val.new_empty(n_states))
+
+
+@torch.library.custom_op("qpinn_b200::pqc_bwd_adjoint", mutates_args=())
+def pqc_bwd_adjoint(plan: int, scale_kind: str, act_val: torch.Tensor, act_tan: torch.Tensor,
+                    qparams: torch.Tensor, states: torch.Tensor, g_z: torch.Tensor,
+                    g_dz: torch.Tensor) -> Tuple[torch.Tensor, torch.Tensor, torch.Tensor]:
+    """K2: (g_act_val [R,n], g_act_tan [3,R,n], g_qparams [P]); an empty
+    ``states`` replays the circuit instead of reading the K1 hand-off."""
+    return pqc_backward_raw(_plan(plan), scale_kind, act_val, act_tan, qparams,
+                            g_z.contiguous(), g_dz.contiguous(),
+                            states if states.numel() else None)
+
+
+@pqc_bwd_adjoint.register_fake
+def _(plan, scale_kind, act_val, act_tan, qparams, states, g_z, g_dz):
+    return torch.empty_like(act_val), torch.empty_like(act_tan), torch.empty_like(qparams)
+
+
+def _fwd_setup_context(ctx, inputs, output):
+    plan, scale_kind, a, da, qp, _ = inputs
+    ctx.plan, ctx.scale_kind = plan, scale_kind
+    ctx.save_for_backward(a, da, qp, output[2])
+
+
+def _fwd_backward(ctx, gz, gdz, _gstates):
+    a, da, qp, states = ctx.saved_tensors
+    gz = torch.zeros_like(a) if gz is None else gz
+    gdz = torch.zeros_like(da) if gdz is None else gdz
+    ga, gda, gq = torch.ops.qpinn_b200.pqc_bwd_adjoint(ctx.plan, ctx.scale_kind, a, da, qp,
+                                                       states, gz, gdz)
+    return None, None, ga, gda, gq, None
+
+
+pqc_fwd_tangent.register_autograd(_fwd_backward, setup_context=_fwd_setup_context)
 
 
 class _PQCValue(torch.autograd.Function):
@@ -392,7 +451,10 @@ def quantum_layer_forward(activations, qparams, circuit: CircuitSpec | AnsatzKin
         da = activations.tan.to(dtype=a.dtype).contiguous()
         if tuple(da.shape) != (3,) + tuple(a.shape):
             raise ConfigError("activation tangents must have shape [3, R, n]")
-        z, dz = _PQC.apply(a, da, qp, circuit, ScaleKind(scale_kind))
+        save = torch.is_grad_enabled() and (a.requires_grad or da.requires_grad
+                                            or qp.requires_grad)
+        z, dz, _ = torch.ops.qpinn_b200.pqc_fwd_tangent(
+            plan_token(circuit), ScaleKind(scale_kind).value, a, da, qp, save)
         if check:
             check_domain(circuit, a.dtype, a.device)
         return BatchedDual(z, dz)

@@ -49,3 +49,20 @@ def test_grid_bins_and_mirrors_match_oracle():
     g = CollocationGrid(64, 64, 16, 1.5)
     pops = [sum(1 for i in range(16) if g.bin_of_slice(i) == m) for m in range(5)]
     assert pops == [3, 3, 3, 3, 4]
+
+
+def test_torch_ops_registered_with_shapes():
+    """The custom-op boundary (SURVEY §8 b) is registered and shape-infers on
+    meta tensors without a GPU (no compute)."""
+    import torch
+    from paper_2506_23246_b200.ansatz import build_circuit, plan_token
+    c = build_circuit("cross_mesh", 7, 4)
+    a = torch.empty(10, 7, device="meta")
+    da = torch.empty(3, 10, 7, device="meta")
+    qp = torch.empty(c.param_count, device="meta")
+    z, dz, st = torch.ops.qpinn_b200.pqc_fwd_tangent(plan_token(c), "acos", a, da, qp, True)
+    assert z.shape == (10, 7) and dz.shape == (3, 10, 7) and st.numel() > 0
+    _, _, st0 = torch.ops.qpinn_b200.pqc_fwd_tangent(plan_token(c), "acos", a, da, qp, False)
+    assert st0.numel() == 0
+    ga, gda, gq = torch.ops.qpinn_b200.pqc_bwd_adjoint(plan_token(c), "acos", a, da, qp, st, z, dz)
+    assert ga.shape == (10, 7) and gda.shape == (3, 10, 7) and gq.shape == (c.param_count,)

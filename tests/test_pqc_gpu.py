@@ -283,3 +283,31 @@ def test_transfer_matrix_kernels_vs_oracle(kind, n, R):
         assert_close(x, w, dtype, f"transfer {name}", scale)
     for x, y in zip(g, g2):  # replayed forward: same launches, same bits
         assert torch.equal(x, y)
+
+
+@pytest.mark.parametrize("dtype", DTYPES)
+def test_torch_ops_boundary_default_7q_4l(dtype):
+    """torch.ops.qpinn_b200.pqc_fwd_tangent / pqc_bwd_adjoint (SURVEY §8 b) with
+    the K1 -> K2 state hand-off as a tensor, against the reference golden
+    vectors, plus torch.library.opcheck of schema, fake and autograd
+    registration."""
+    from paper_2506_23246_b200.ansatz import build_circuit, plan_token
+    for key, d in golden_cases("pqc_n7.npz").items():
+        kind, scale = key.split("/")[:2]
+        c = build_circuit(kind, 7, 4)
+        tok = plan_token(c)
+        a, da, qp = cuda(d["a"], dtype), cuda(d["da"], dtype), cuda(d["qp"], dtype)
+        z, dz, st = torch.ops.qpinn_b200.pqc_fwd_tangent(tok, scale, a, da, qp, True)
+        assert st.numel() > 0
+        ga, gda, gq = torch.ops.qpinn_b200.pqc_bwd_adjoint(
+            tok, scale, a, da, qp, st, cuda(d["gz"], dtype), cuda(d["gdz"], dtype))
+        s = 30.0 if "edge" in key and dtype == torch.float32 else 1.0
+        assert_close(z, d["z"], dtype, f"{key} z", s)
+        assert_close(dz, d["dz"], dtype, f"{key} dz", s)
+        assert_close(ga, d["ga"], dtype, f"{key} g_a", s)
+        assert_close(gda, d["gda"], dtype, f"{key} g_da", s)
+        assert_close(gq, d["gq"], dtype, f"{key} g_qparams", s)
+    torch.library.opcheck(torch.ops.qpinn_b200.pqc_fwd_tangent.default,
+                          (tok, scale, a, da, qp, True),
+                          test_utils=("test_schema", "test_faketensor",
+                                      "test_autograd_registration"))
