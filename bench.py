@@ -288,10 +288,18 @@ def run_ours(args):
     rank, world, local = dist_env()
     if world != args.gpus:
         args.gpus = world if world > 1 else args.gpus
+    # QPINN_BENCH_FUNCTIONAL_DP=1: functional check of the N>1 path on a one-GPU box
+    # (every rank on cuda:0, gloo collectives); its numbers are not bench values
+    functional = os.environ.get("QPINN_BENCH_FUNCTIONAL_DP") == "1"
+    if functional:
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if functional:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
     wl = args.workload if args.workload != "auto" else ("config2" if world == 1 else "config3")
     grid = WORKLOADS[wl]["grid"]
     dtype = torch.float32 if args.dtype == "f32" else torch.float64
@@ -302,7 +310,7 @@ def run_ours(args):
 
     def barrier():
         if world > 1:
-            dist.barrier(device_ids=[local])
+            dist.barrier(**({} if functional else {"device_ids": [local]}))
 
     def timed_steps(k):
         barrier()
@@ -441,8 +449,10 @@ def run_ours(args):
             "cpu_baseline": cpu,
             "clocks": clk.summary(),
         }
+        if functional:
+            line["functional_check"] = "all ranks on cuda:0 over gloo: not a bench value"
     if world > 1:
-        dist.barrier(device_ids=[local])
+        dist.barrier(**({} if functional else {"device_ids": [local]}))
         dist.destroy_process_group()
     if line is not None:
         print(json.dumps(line), flush=True)
