@@ -490,7 +490,9 @@ __global__ void __launch_bounds__(256, QPINN_TR_EG_MINB) tr_embed_grad(int scale
   for_points(R, [&](int64_t p0) {
     stage_angles<NQ>(scale, R, p0, act, tan, ang, amax);
     __syncthreads();
-    for (int pl = w; pl < kPB && p0 + pl < R; pl += 8) {
+    // loop exit through a warp vote: provably warp-uniform, so the shuffles below
+    // compile to plain SHFL (no WARPSYNC / ENDCOLLECTIVE divergence wrappers)
+    for (int pl = w; __all_sync(0xffffffffu, pl < kPB && p0 + pl < R); pl += 8) {
       const int64_t p = p0 + pl;
       const float* pang = ang + pl * NQ * kAng;
       PointAngles<NQ> pa;
