@@ -155,21 +155,22 @@ def fp32_peak():
 
 
 def tensor_gemm_roofline(n_qubits: int, R: int):
-    """The transfer map's 3xTF32 tcgen05 GEMM ([4R, 2D] x [2D, 2D]) timed alone with CUDA
-    events, against cuBLAS's own TF32 peak measured in the same run (8192^3, the
-    ceiling for this MMA kind on this box; MEASURED_PEAKS.json has bf16 only).
-    achieved = the TF32 MMA work issued (3 products) / time."""
+    """The transfer map's 3xTF32 tcgen05 GEMM (the forward map Psi = m W':
+    [4R, D] x [D, 2D]) timed alone with CUDA events, against cuBLAS's own TF32 peak
+    measured in the same run (8192^3, the ceiling for this MMA kind on this box;
+    MEASURED_PEAKS.json has bf16 only).  achieved = the TF32 MMA work issued (3
+    products) / time."""
     import torch
     from paper_2506_23246_b200 import _native as N
     lib = N.lib()
-    M, n = 4 * R, 2 << n_qubits
-    A = torch.randn(M, n, device="cuda")
-    B = torch.randn(n, n, device="cuda")
+    M, n, k = 4 * R, 2 << n_qubits, 1 << n_qubits
+    A = torch.randn(M, k, device="cuda")
+    B = torch.randn(n, k, device="cuda")
     Cm = torch.empty(M, n, device="cuda")
-    ws = torch.empty(lib.qpinn_gemm_f32_workspace_bytes(n, n), dtype=torch.uint8, device="cuda")
+    ws = torch.empty(lib.qpinn_gemm_f32_workspace_bytes(n, k), dtype=torch.uint8, device="cuda")
 
     def gemm():
-        N.check(lib.qpinn_gemm_f32(M, n, n, A.data_ptr(), n, B.data_ptr(), n, Cm.data_ptr(), n,
+        N.check(lib.qpinn_gemm_f32(M, n, k, A.data_ptr(), k, B.data_ptr(), k, Cm.data_ptr(), n,
                                    ws.data_ptr(), ws.numel(), N.stream_ptr()), "gemm")
 
     def timed(fn, k):
@@ -191,10 +192,10 @@ def tensor_gemm_roofline(n_qubits: int, R: int):
     ms_pk = timed(lambda: a @ b, 10)
     torch.backends.cuda.matmul.allow_tf32 = prev
     peak = 2 * 8192 ** 3 / (ms_pk * 1e-3) / 1e12
-    achieved = 3 * 2 * M * n * n / (ms * 1e-3) / 1e12
+    achieved = 3 * 2 * M * n * k / (ms * 1e-3) / 1e12
     return {"bound": "tensor", "achieved": round(achieved, 1), "peak": round(peak, 1),
             "unit": "TFLOP/s", "frac": round(achieved / peak, 4), "traffic": None,
-            "shape": [M, n, n], "ms_per_launch": round(ms, 4),
+            "shape": [M, n, k], "ms_per_launch": round(ms, 4),
             "flop_counting": "TF32 MMA work issued: 3 products x 2 M N K (3xTF32, FP32-class)",
             "peak_source": "measured in-run: cuBLAS TF32 GEMM 8192^3 (torch, allow_tf32)"}
 

@@ -9,14 +9,15 @@
 //
 //   rows of B:   B[j] = circuit(e_j)                     (complex [D][D])
 //   W          = [[Br, Bi], [-Bi, Br]]                    (real [2D][2D])
-//   Psi        = Phi W       with Phi = [Re phi | Im phi] per state row,
-//                [4R][2D]    rows s R + p (s = 0: phi, 1..3: d phi/dx,y,t)
+//   W'         = W with rows b, D+b folded by the embedding phase (tr_wmat)  [D][2D]
+//   Psi        = m W'        with m = the real magnitudes of phi per state row
+//                [4R][2D]    ([4R][D]), rows s R + p (s = 0: phi, 1..3: d phi/dx,y,t)
 //
-// For n = 7 that is 2 (4 8 D^2) flops per point instead of the gate-by-gate
+// For n = 7 that is 2 (4 2 D^2) flops per point instead of the gate-by-gate
 // 2.4e5, but at tensor-core rate.  The backward is the GEMM's backward:
 //   Abar  = seeds(Psi, dL/dz, dL/ddz)                     (qpinn_oracle.pqc_backward)
-//   gPhi  = Abar W^T  -> the embedding gradient, per point
-//   gW    = Phi^T Abar (deterministic split-K)  -> adjoint of the rows of B
+//   dL/dm = Abar W'^T  -> the embedding gradient, per point
+//   dL/dW' = m^T Abar (deterministic split-K)  -> adjoint of the rows of B
 //   the circuit's adjoint on the D basis rows (one CTA per row, checkpointed
 //   at the layer boundaries like K2) -> the gate-space sums -> dL/dqparams.
 // Float32 only (the GEMM is 3xTF32); chosen for 5 <= n <= 7, where the dense
@@ -201,27 +202,48 @@ __global__ void tr_reduce(int D, int n_u1, int n_ph, const double* __restrict__ 
   if (lane == 0) acc[i] = v;
 }
 
-// Wt [2D][2D] = W^T (forward GEMM operand) and W (backward operand)
+// phase of embedded amplitude b: (-i)^popcount(b) = (pr, pi)
+__device__ __forceinline__ void embed_phase(int b, float& pr, float& pi) {
+  const int ph = __popc(b) & 3;
+  pr = ph == 0 ? 1.f : ph == 2 ? -1.f : 0.f;
+  pi = ph == 1 ? -1.f : ph == 3 ? 1.f : 0.f;
+}
+
+// Every embedded row (state or tangent) is phi_b = p_b m_b with a real
+// magnitude m_b and the point-independent phase p_b = (-i)^popcount(b), so in
+// the real-block form [Re phi | Im phi] half of the 2D entries are zero in a
+// fixed pattern.  The map is therefore applied to the D magnitudes only:
+//   W'[b][c] = Re p_b W[b][c] + Im p_b W[D + b][c],   W = [[Br, Bi], [-Bi, Br]]
+//   Psi = m W'   (K = D instead of 2D),   dL/dm = Abar W'^T   (N = D),
+//   dL/dW' = m^T Abar   (D x 2D),   dL/dW[b] = Re p_b dL/dW'[b], dL/dW[D+b] = Im p_b dL/dW'[b]
+// which halves all three transfer GEMMs and the embedded-state traffic.
+// Wt [2D][D] = W'^T (forward GEMM operand) and W [D][2D] = W' (backward operand).
 __global__ void tr_wmat(int n, const cplx<float>* __restrict__ B, float* __restrict__ W,
                         float* __restrict__ Wt) {
   const int D = 1 << n, D2 = 2 * D;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < D2 * D2; i += gridDim.x * blockDim.x) {
-    const int r = i / D2, c = i % D2;  // W[r][c]
-    const cplx<float> b = B[(size_t)(r % D) * D + (c % D)];
-    const bool rlo = r < D, clo = c < D;
-    const float v = rlo == clo ? b.re : rlo ? b.im : -b.im;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < D * D2; i += gridDim.x * blockDim.x) {
+    const int r = i / D2, c = i % D2;  // W'[r][c]
+    const cplx<float> b = B[(size_t)r * D + (c % D)];
+    const float top = c < D ? b.re : b.im;    // W[r][c]
+    const float bot = c < D ? -b.im : b.re;   // W[D + r][c]
+    float pr, pi;
+    embed_phase(r, pr, pi);
+    const float v = pr * top + pi * bot;
     W[i] = v;
-    Wt[(size_t)c * D2 + r] = v;
+    Wt[(size_t)c * D + r] = v;
   }
 }
 
-// complex adjoint of the rows of B from dL/dW: dL/dBr = gW11 + gW22, dL/dBi = gW12 - gW21
+// complex adjoint of the rows of B from dL/dW' [D][2D] (see tr_wmat):
+// dL/dBr = gW11 + gW22, dL/dBi = gW12 - gW21 on the expanded dL/dW
 __global__ void tr_gb(int n, const float* __restrict__ gW, cplx<float>* __restrict__ Ab) {
   const int D = 1 << n, D2 = 2 * D;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < D * D; i += gridDim.x * blockDim.x) {
     const int j = i / D, k = i % D;
-    Ab[i] = {gW[(size_t)j * D2 + k] + gW[(size_t)(D + j) * D2 + D + k],
-             gW[(size_t)j * D2 + D + k] - gW[(size_t)(D + j) * D2 + k]};
+    float pr, pi;
+    embed_phase(j, pr, pi);
+    const float g0 = gW[(size_t)j * D2 + k], g1 = gW[(size_t)j * D2 + D + k];
+    Ab[i] = {pr * g0 + pi * g1, pr * g1 - pi * g0};
   }
 }
 
@@ -328,7 +350,7 @@ __device__ __forceinline__ void for_points(int64_t R, F&& body) {
     body(p0);
 }
 
-// Phi rows: [Re | Im] of the embedded state and its tangents
+// Phi rows: the magnitudes m_b of the embedded state and its tangents (D per row)
 #ifndef QPINN_TR_EMB_MINB
 #define QPINN_TR_EMB_MINB 4
 #endif
@@ -337,7 +359,7 @@ __global__ void __launch_bounds__(256, QPINN_TR_EMB_MINB) tr_embed(int scale, in
                                                 const float* __restrict__ tan,
                                                 float* __restrict__ Phi,
                                                 unsigned long long* __restrict__ maxabs) {
-  constexpr int D = 1 << NQ, D2 = 2 * D;
+  constexpr int D = 1 << NQ;
   __shared__ float ang[kPB * NQ * kAng];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   float amax = 0.f;
@@ -352,17 +374,9 @@ __global__ void __launch_bounds__(256, QPINN_TR_EMB_MINB) tr_embed(int scale, in
       for (int b = lane; b < D; b += 32) {
         float m0, mk[3];
         embed_amp<NQ>(pa, b, tan != nullptr, m0, mk);
-        float re, im;
-        put_phase(m0, b, re, im);
-        Phi[p * D2 + b] = re;
-        Phi[p * D2 + D + b] = im;
+        Phi[p * D + b] = m0;  // magnitudes: the phase (-i)^popcount(b) lives in W' (tr_wmat)
         if (tan)
-          for (int k = 0; k < 3; ++k) {
-            put_phase(mk[k], b, re, im);
-            float* row = Phi + ((int64_t)(k + 1) * R + p) * D2;
-            row[b] = re;
-            row[D + b] = im;
-          }
+          for (int k = 0; k < 3; ++k) Phi[((int64_t)(k + 1) * R + p) * D + b] = mk[k];
       }
     }
     __syncthreads();
@@ -483,7 +497,7 @@ __global__ void __launch_bounds__(256, QPINN_TR_EG_MINB) tr_embed_grad(int scale
                                                      const float* __restrict__ gPhi,
                                                      float* __restrict__ g_act,
                                                      float* __restrict__ g_tan) {
-  constexpr int D = 1 << NQ, D2 = 2 * D, J = D / 32;
+  constexpr int D = 1 << NQ, J = D / 32;
   __shared__ float ang[kPB * NQ * kAng];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   float amax = 0.f;
@@ -497,20 +511,27 @@ __global__ void __launch_bounds__(256, QPINN_TR_EG_MINB) tr_embed_grad(int scale
       const float* pang = ang + pl * NQ * kAng;
       PointAngles<NQ> pa;
       read_angles<NQ>(pang, pa);
-      float fr[J], fi[J], er[J], ei[J], mr[3][J], mi[3][J];
+      float fr[J], fi[J], er[J], ei[J], mr[3][J], mi[3][J], g[4][J];
+#pragma unroll
+      for (int r = 0; r < 4; ++r)  // all the point's loads in flight before any use
+#pragma unroll
+        for (int j = 0; j < J; ++j) g[r][j] = gPhi[((int64_t)r * R + p) * D + lane + 32 * j];
 #pragma unroll
       for (int j = 0; j < J; ++j) {
         const int b = lane + 32 * j;
         float m0, mk[3];
         embed_amp<NQ>(pa, b, false, m0, mk);
         put_phase(m0, b, fr[j], fi[j]);
-        er[j] = -0.5f * gPhi[p * D2 + D + b];  // (i/2) phibar
-        ei[j] = 0.5f * gPhi[p * D2 + b];
+        // gPhi holds dL/dm_b; the phase-aligned phibar_b = p_b dL/dm_b is the only
+        // component the embedding gradient sees (d phi_b / d theta is p_b x real)
+        float pr, pi;
+        embed_phase(b, pr, pi);
+        er[j] = -0.5f * pi * g[0][j];  // (i/2) phibar
+        ei[j] = 0.5f * pr * g[0][j];
 #pragma unroll
         for (int k = 0; k < 3; ++k) {
-          const float* row = gPhi + ((int64_t)(k + 1) * R + p) * D2;
-          mr[k][j] = row[b];
-          mi[k][j] = row[D + b];
+          mr[k][j] = pr * g[k + 1][j];
+          mi[k][j] = pi * g[k + 1][j];
         }
       }
 #pragma unroll
@@ -623,8 +644,8 @@ TrHandoff tr_handoff(const qpinn_circuit* c, int64_t R) {
     return at;
   };
   h.psi = take(4 * (size_t)R * D2 * 4);
-  h.phi = take(4 * (size_t)R * D2 * 4);
-  h.W = take(4 * D2 * D2);
+  h.phi = take(4 * (size_t)R * D * 4);
+  h.W = take(4 * D * D2);
   h.CK = take(cs * D * D * c->L);
   h.U = take(cs * 4 * c->n_u1);
   h.ph = take(cs * D * c->n_phase);
@@ -640,7 +661,7 @@ int build_transfer(const qpinn_circuit* c, const float* qp, const TrCircuit& tc_
   const int ent = layer_entangler(c);
   tr_tables<<<32, 256, 0, st>>>(p, qp, tc_.U, tc_.ph);
   tr_circuit_fwd<<<D, kTrThreads, 0, st>>>(n, c->L, ent, tc_.U, tc_.ph, p.perm, B, tc_.CK);
-  tr_wmat<<<(4 * D * D + 255) / 256, 256, 0, st>>>(n, B, tc_.W, tc_.Wt);
+  tr_wmat<<<(2 * D * D + 255) / 256, 256, 0, st>>>(n, B, tc_.W, tc_.Wt);
   QPINN_CUDA_CHECK(cudaGetLastError());
   return QPINN_OK;
 }
@@ -652,7 +673,7 @@ TrCircuit ws_circuit(unsigned char* ws, const TrLayout& t) {
 
 template <int NQ>
 int fwd_n(const qpinn_circuit* c, const KArgs<float>* a, unsigned char* ws, const TrLayout& t) {
-  constexpr int D2 = 2 << NQ;
+  constexpr int D = 1 << NQ, D2 = 2 * D;
   cudaStream_t st = a->stream;
   const bool handoff = a->states && a->tan;
   auto* hs = (unsigned char*)a->states;
@@ -670,7 +691,7 @@ int fwd_n(const qpinn_circuit* c, const KArgs<float>* a, unsigned char* ws, cons
   const int ns = a->tan ? 4 : 1;
   tr_embed<NQ><<<grid_points(a->R), 256, 0, st>>>(a->scale, a->R, a->act, a->tan, Phi, a->maxabs);
   QPINN_CUDA_CHECK(cudaGetLastError());
-  if (int rc = tc::gemm3(ns * a->R, D2, D2, Phi, D2, cc.Wt, D2, Psi, D2, ws + t.g3,
+  if (int rc = tc::gemm3(ns * a->R, D2, D, Phi, D, cc.Wt, D, Psi, D2, ws + t.g3,
                          tc::gemm3_workspace_bytes(D2, D2), st))
     return rc;
   tr_readout<NQ><<<grid_points(a->R), 256, 0, st>>>(a->R, ns, Psi, a->z, a->dz);
@@ -703,7 +724,7 @@ int bwd_n(const qpinn_circuit* c, const KArgs<float>* a, unsigned char* ws, cons
     if (int rc = build_transfer(c, a->qp, cc, (cplx<float>*)(ws + t.B), st)) return rc;
     tr_embed<NQ><<<gp, 256, 0, st>>>(a->scale, a->R, a->act, a->tan, Abar, nullptr);
     QPINN_CUDA_CHECK(cudaGetLastError());
-    if (int rc = tc::gemm3(4 * a->R, D2, D2, Abar, D2, cc.Wt, D2, G, D2, ws + t.g3,
+    if (int rc = tc::gemm3(4 * a->R, D2, D, Abar, D, cc.Wt, D, G, D2, ws + t.g3,
                            tc::gemm3_workspace_bytes(D2, D2), st))
       return rc;
     Psi = G;
@@ -711,18 +732,18 @@ int bwd_n(const qpinn_circuit* c, const KArgs<float>* a, unsigned char* ws, cons
   }
   tr_seed<NQ><<<gp, 256, 0, st>>>(a->R, a->gz, a->gdz, Psi, Abar);
   QPINN_CUDA_CHECK(cudaGetLastError());
-  // gPhi = Abar W^T
-  if (int rc = tc::gemm3(4 * a->R, D2, D2, Abar, D2, cc.W, D2, G, D2, ws + t.g3,
+  // dL/dm = Abar W'^T  (D per row)
+  if (int rc = tc::gemm3(4 * a->R, D, D2, Abar, D2, cc.W, D2, G, D, ws + t.g3,
                          tc::gemm3_workspace_bytes(D2, D2), st))
     return rc;
   tr_embed_grad<NQ><<<gp, 256, 0, st>>>(a->scale, a->R, a->act, a->tan, G, a->g_act, a->g_tan);
-  // gW = Phi^T Abar
+  // dL/dW' = m^T Abar  (D x 2D)
   if (!Phi) {
     tr_embed<NQ><<<gp, 256, 0, st>>>(a->scale, a->R, a->act, a->tan, G, nullptr);
     Phi = G;
   }
   QPINN_CUDA_CHECK(cudaGetLastError());
-  if (int rc = tc::wgrad(4 * a->R, D2, D2, Phi, D2, Abar, D2, (float*)(ws + t.gW), ws + t.wg,
+  if (int rc = tc::wgrad(4 * a->R, D, D2, Phi, D, Abar, D2, (float*)(ws + t.gW), ws + t.wg,
                          tc::wgrad_workspace_bytes(4 * a->R, D2, D2), st))
     return rc;
   auto* Ab = (cplx<float>*)(ws + t.Ab);

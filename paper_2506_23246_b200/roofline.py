@@ -25,23 +25,25 @@ def pqc_flops(circuit):
 
 
 def transfer_bytes(n: int):
-    """HBM bytes per point of the transfer-matrix K1/K2 (pqc_transfer.cu, float32):
-    every [4 rows, 2D] operand is 4 x 2D x 4 = 32 D bytes per point.
-      forward : embed writes Phi; the GEMM reads Phi, writes Psi; the readout reads
-                Psi (4 x 32 D) + a, da in and z, dz out (2 x 16 n)
-      backward: seeds read Psi, write Abar; the GEMM reads Abar, writes gPhi; the
-                embedding gradient reads gPhi; the weight-gradient GEMM reads Phi
-                and Abar (7 x 32 D) + dL/dz, dL/ddz, a, da in, g_a, g_da out (3 x 16 n)
-    The D x D transfer matrix and its adjoint are L2-resident and not counted."""
+    """HBM bytes per point of the transfer-matrix K1/K2 (pqc_transfer.cu, float32).
+    A [4 rows, 2D] operand (Psi, Abar) is 4 x 2D x 4 = 32 D bytes per point; the
+    embedded magnitudes m and dL/dm (the phase lives in W', tr_wmat) are 16 D.
+      forward : embed writes m (16 D); the GEMM reads m, writes Psi (16 D + 32 D);
+                the readout reads Psi (32 D) + a, da in and z, dz out (2 x 16 n)
+      backward: seeds read Psi, write Abar (2 x 32 D); the GEMM reads Abar, writes
+                dL/dm (32 D + 16 D); the embedding gradient reads dL/dm (16 D); the
+                weight-gradient GEMM reads m and Abar (16 D + 32 D) + dL/dz, dL/ddz,
+                a, da in, g_a, g_da out (3 x 16 n)
+    The D x 2D transfer matrix and its adjoint are L2-resident and not counted."""
     D = 1 << n
-    return 4 * 32 * D + 2 * 16 * n, 7 * 32 * D + 3 * 16 * n
+    return 96 * D + 2 * 16 * n, 176 * D + 3 * 16 * n
 
 
 def transfer_flops(n: int):
-    """Algorithmic (fp32) GEMM flops per point: Psi = Phi W is [4, 2D] x [2D, 2D];
-    the backward has gPhi = Abar W^T and gW += Phi^T Abar."""
-    D2 = 2 << n
-    return 2 * 4 * D2 * D2, 2 * 2 * 4 * D2 * D2
+    """Algorithmic (fp32) GEMM flops per point: Psi = m W' is [4, D] x [D, 2D];
+    the backward has dL/dm = Abar W'^T and dL/dW' += m^T Abar."""
+    D = 1 << n
+    return 2 * 4 * D * 2 * D, 2 * 2 * 4 * D * 2 * D
 
 
 def trunk_flops(hidden: int = 128, rff: int = 128, n_qubits: int = 7, n_hidden: int = 3):
