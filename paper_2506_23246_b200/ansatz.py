@@ -174,7 +174,7 @@ class CircuitSpec:
         return bool(N.lib().qpinn_pqc_uses_transfer(self._h, N.dtype_code(dtype)))
 
     def set_kernel_variant(self, variant: str) -> None:
-        """"auto" (transfer-matrix kernels for float32 n = 6, 7, else the
+        """"auto" (transfer-matrix kernels for float32 n = 5, 6, 7, else the
         layer-loop kernels when available), "generic", "transfer" (float32,
         5 <= n <= 7: the transfer-matrix map on the tensor cores) or "layer"
         (the layer-loop kernels wherever they apply)."""

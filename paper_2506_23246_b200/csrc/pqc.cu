@@ -645,11 +645,12 @@ static size_t small_ws_bytes(const qpinn_circuit* c) {
 }
 
 // the transfer-matrix kernels (pqc_transfer.cu): variant 2, and the default for
-// float32 n = 6, 7 (measured, 2^16 points, L = 4, K1 + K2: n = 7 1.07 ms vs
-// 1.74 ms for the layer kernels, n = 6 0.50 vs 0.83; n = 5 is a tie)
+// float32 n = 5, 6, 7 (measured with the phase-folded map, 2^16 points, L = 4,
+// K1 + K2: n = 7 0.69 ms vs 1.74 ms for the layer kernels, n = 6 0.41 vs 0.82,
+// n = 5 0.32 vs 0.37-0.39; profiles/r01/transfer_vs_layer_folded.txt)
 static bool use_transfer(const qpinn_circuit* c, int dtype) {
   if (!transfer_supported(c, dtype)) return false;
-  return c->variant == 2 || (c->variant == 0 && c->n >= 6);
+  return c->variant == 2 || c->variant == 0;
 }
 
 int qpinn_pqc_uses_transfer(const qpinn_circuit* c, int dtype) {
