@@ -486,7 +486,8 @@ __device__ __forceinline__ float flip_get(const float (&v)[J], int j, int q) {
 // embedding gradient (qpinn_oracle.pqc_backward):
 //   eta = (i/2) phibar - 1/4 sum_q X_q nu_q,  nu_q = sum_k dth_kq mu_k
 //   g_th[q] = Re sum conj(eta) X_q phi, g_dth[k][q] = Re sum conj((i/2) mu_k) X_q phi
-// phibar, mu_k = rows of gPhi; phi is re-embedded in registers
+// phibar, mu_k = p_b x the rows of dL/dm; phi = p_b m is re-embedded in registers;
+// with the common phase p_b factored out the sums are real (see the kernel body)
 #ifndef QPINN_TR_EG_MINB
 #define QPINN_TR_EG_MINB 3
 #endif
@@ -511,41 +512,33 @@ __global__ void __launch_bounds__(256, QPINN_TR_EG_MINB) tr_embed_grad(int scale
       const float* pang = ang + pl * NQ * kAng;
       PointAngles<NQ> pa;
       read_angles<NQ>(pang, pa);
-      float fr[J], fi[J], er[J], ei[J], mr[3][J], mi[3][J], g[4][J];
+      // Every factor here is p_b x real (phi_b = p_b m_b, phibar_b = p_b dL/dm_b,
+      // p_b = (-i)^popcount(b)), so the complex formulas reduce to real ones on the
+      // magnitudes (sigma_q(b) = +1 if wire q is set in b, else -1):
+      //   nu_q(b)  = sum_k dth_kq g_k(b)                      (g_k = dL/dm of tangent row k)
+      //   eta(b)   = g_0(b) / 2 - 1/4 sum_q sigma_q(b) nu_q(b ^ q)
+      //   g_th[q]  = sum_b sigma_q(b) eta(b) m(b ^ q),  g_dth[k][q] = 1/2 sum_b sigma_q(b) g_k(b) m(b ^ q)
+      float m[J], et[J], g[4][J];
 #pragma unroll
       for (int r = 0; r < 4; ++r)  // all the point's loads in flight before any use
 #pragma unroll
         for (int j = 0; j < J; ++j) g[r][j] = gPhi[((int64_t)r * R + p) * D + lane + 32 * j];
 #pragma unroll
       for (int j = 0; j < J; ++j) {
-        const int b = lane + 32 * j;
-        float m0, mk[3];
-        embed_amp<NQ>(pa, b, false, m0, mk);
-        put_phase(m0, b, fr[j], fi[j]);
-        // gPhi holds dL/dm_b; the phase-aligned phibar_b = p_b dL/dm_b is the only
-        // component the embedding gradient sees (d phi_b / d theta is p_b x real)
-        float pr, pi;
-        embed_phase(b, pr, pi);
-        er[j] = -0.5f * pi * g[0][j];  // (i/2) phibar
-        ei[j] = 0.5f * pr * g[0][j];
-#pragma unroll
-        for (int k = 0; k < 3; ++k) {
-          mr[k][j] = pr * g[k + 1][j];
-          mi[k][j] = pi * g[k + 1][j];
-        }
+        float mk[3];
+        embed_amp<NQ>(pa, lane + 32 * j, false, m[j], mk);
+        et[j] = 0.5f * g[0][j];
       }
 #pragma unroll
       for (int q = 0; q < NQ; ++q) {
-        float nr[J], ni[J];
+        float nu[J];
+#pragma unroll
+        for (int j = 0; j < J; ++j)
+          nu[j] = pa.d[0][q] * g[1][j] + pa.d[1][q] * g[2][j] + pa.d[2][q] * g[3][j];
 #pragma unroll
         for (int j = 0; j < J; ++j) {
-          nr[j] = pa.d[0][q] * mr[0][j] + pa.d[1][q] * mr[1][j] + pa.d[2][q] * mr[2][j];
-          ni[j] = pa.d[0][q] * mi[0][j] + pa.d[1][q] * mi[1][j] + pa.d[2][q] * mi[2][j];
-        }
-#pragma unroll
-        for (int j = 0; j < J; ++j) {
-          er[j] -= 0.25f * flip_get<NQ, J>(nr, j, q);
-          ei[j] -= 0.25f * flip_get<NQ, J>(ni, j, q);
+          const float f = 0.25f * flip_get<NQ, J>(nu, j, q);
+          et[j] += ((lane + 32 * j) >> (NQ - 1 - q)) & 1 ? -f : f;
         }
       }
       float acc[32];
@@ -555,10 +548,11 @@ __global__ void __launch_bounds__(256, QPINN_TR_EG_MINB) tr_embed_grad(int scale
       for (int q = 0; q < NQ; ++q) {
 #pragma unroll
         for (int j = 0; j < J; ++j) {
-          const float yr = flip_get<NQ, J>(fr, j, q), yi = flip_get<NQ, J>(fi, j, q);
-          acc[q] += er[j] * yr + ei[j] * yi;
+          const float mf = flip_get<NQ, J>(m, j, q);
+          const float y = ((lane + 32 * j) >> (NQ - 1 - q)) & 1 ? mf : -mf;
+          acc[q] = fmaf(et[j], y, acc[q]);
 #pragma unroll
-          for (int k = 0; k < 3; ++k) acc[NQ + k * NQ + q] += -0.5f * mi[k][j] * yr + 0.5f * mr[k][j] * yi;
+          for (int k = 0; k < 3; ++k) acc[NQ + k * NQ + q] = fmaf(g[k + 1][j], y, acc[NQ + k * NQ + q]);
         }
       }
       reduce_scatter32(acc);
@@ -566,7 +560,7 @@ __global__ void __launch_bounds__(256, QPINN_TR_EG_MINB) tr_embed_grad(int scale
       const int q = lane < NQ ? lane : 0;
       float gd[3];
 #pragma unroll
-      for (int k = 0; k < 3; ++k) gd[k] = __shfl_sync(0xffffffffu, acc[0], NQ + k * NQ + q);
+      for (int k = 0; k < 3; ++k) gd[k] = 0.5f * __shfl_sync(0xffffffffu, acc[0], NQ + k * NQ + q);
       if (lane < NQ) {
         const float* a = pang + q * kAng;
         float ga = acc[0] * a[2];
