@@ -66,3 +66,30 @@ def test_torch_ops_registered_with_shapes():
     assert st0.numel() == 0
     ga, gda, gq = torch.ops.qpinn_b200.pqc_bwd_adjoint(plan_token(c), "acos", a, da, qp, st, z, dz)
     assert ga.shape == (10, 7) and gda.shape == (3, 10, 7) and gq.shape == (c.param_count,)
+
+
+def test_embedding_phase_folding_identity():
+    """The transfer path's phase folding (csrc/pqc_transfer.cu tr_wmat / tr_gb):
+    every embedded row is phi_b = (-i)^popcount(b) m_b with real m_b, so the
+    real-block map [Re phi | Im phi] W equals m W' with W' = Re p W[:D] + Im p W[D:],
+    and dL/dW is recovered from dL/dW' = m^T Abar row by row."""
+    import numpy as np
+    rng = np.random.default_rng(3)
+    n, R = 5, 9
+    D = 1 << n
+    B = rng.normal(size=(D, D)) + 1j * rng.normal(size=(D, D))
+    W = np.block([[B.real, B.imag], [-B.imag, B.real]])
+    p = (-1j) ** np.array([bin(b).count("1") for b in range(D)])
+    m = rng.normal(size=(R, D))
+    phi = m * p
+    Phi = np.concatenate([phi.real, phi.imag], axis=1)
+    Wf = p.real[:, None] * W[:D] + p.imag[:, None] * W[D:]
+    np.testing.assert_allclose(Phi @ W, m @ Wf, rtol=0, atol=1e-12)
+    Abar = rng.normal(size=(R, 2 * D))
+    # dL/dm is the phase-aligned projection of dL/dPhi
+    gPhi = Abar @ W.T
+    np.testing.assert_allclose(Abar @ Wf.T, p.real * gPhi[:, :D] + p.imag * gPhi[:, D:], atol=1e-12)
+    gW = Phi.T @ Abar
+    gWf = m.T @ Abar
+    np.testing.assert_allclose(gW[:D], p.real[:, None] * gWf, atol=1e-12)
+    np.testing.assert_allclose(gW[D:], p.imag[:, None] * gWf, atol=1e-12)
