@@ -81,7 +81,8 @@ def main():
                     row["k2_tflops"] = round(fa * R / ms_b / 1e9, 2)
                 except CapacityError as e:
                     row["k2"] = f"unsupported: {e}"
-                row["regime"] = "warp" if n <= 8 else ("cta" if n <= 12 else "cluster")
+                row["regime"] = ("transfer (tcgen05 GEMMs)" if c.uses_transfer(torch.float32) else
+                                 "warp" if n <= 8 else ("cta" if n <= 12 else "cluster"))
                 if n >= 15:
                     row["k2_regime"] = "hbm (global-memory checkpoints)"
                 print(json.dumps(row), flush=True)
