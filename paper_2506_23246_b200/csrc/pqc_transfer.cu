@@ -22,6 +22,9 @@
 //   at the layer boundaries like K2) -> the gate-space sums -> dL/dqparams.
 // Float32 only (the GEMM is 3xTF32); chosen for 5 <= n <= 7, where the dense
 // map costs at most 2 D / (n L) times the gate-by-gate flops.
+#include <cstdlib>
+#include <mutex>
+
 #include "pqc_layer.h"
 #include "tc_gemm.h"
 
@@ -660,6 +663,29 @@ int build_transfer(const qpinn_circuit* c, const float* qp, const TrCircuit& tc_
   return QPINN_OK;
 }
 
+// side stream per device for the backward's weight-gradient chain (fork/join
+// through events, so it is captured as a parallel branch of the step's CUDA graph)
+struct SideStream {
+  cudaStream_t s = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
+};
+SideStream g_side[64];
+std::mutex g_side_mu;
+
+int side_stream(SideStream** out) {
+  int dev = 0;
+  QPINN_CUDA_CHECK(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(g_side_mu);
+  SideStream& ss = g_side[dev & 63];
+  if (!ss.s) {
+    QPINN_CUDA_CHECK(cudaStreamCreateWithFlags(&ss.s, cudaStreamNonBlocking));
+    QPINN_CUDA_CHECK(cudaEventCreateWithFlags(&ss.fork, cudaEventDisableTiming));
+    QPINN_CUDA_CHECK(cudaEventCreateWithFlags(&ss.join, cudaEventDisableTiming));
+  }
+  *out = &ss;
+  return QPINN_OK;
+}
+
 TrCircuit ws_circuit(unsigned char* ws, const TrLayout& t) {
   return {(cplx<float>*)(ws + t.U), (cplx<float>*)(ws + t.ph), (cplx<float>*)(ws + t.CK),
           (float*)(ws + t.W), (float*)(ws + t.Wt)};
@@ -726,30 +752,50 @@ int bwd_n(const qpinn_circuit* c, const KArgs<float>* a, unsigned char* ws, cons
   }
   tr_seed<NQ><<<gp, 256, 0, st>>>(a->R, a->gz, a->gdz, Psi, Abar);
   QPINN_CUDA_CHECK(cudaGetLastError());
+  // the weight-gradient chain (dL/dW' -> adjoint on the basis rows -> dL/dqparams)
+  // needs only m and Abar: with the hand-off it runs on a side stream, overlapping
+  // the dL/dm GEMM and the embedding gradient (the replay path reuses G for m, so
+  // it stays serial)
+  auto weight_chain = [&](cudaStream_t s2) -> int {
+    if (int rc = tc::wgrad(4 * a->R, D, D2, Phi, D, Abar, D2, (float*)(ws + t.gW), ws + t.wg,
+                           tc::wgrad_workspace_bytes(4 * a->R, D2, D2), s2))
+      return rc;
+    auto* Ab = (cplx<float>*)(ws + t.Ab);
+    tr_gb<<<(D * D + 255) / 256, 256, 0, s2>>>(NQ, (const float*)(ws + t.gW), Ab);
+    auto* pu = (double*)(ws + t.pu);
+    auto* pp = (double*)(ws + t.pp);
+    auto* acc = (double*)(ws + t.acc);
+    tr_circuit_bwd<<<D, kTrThreads, 0, s2>>>(NQ, L, ent, cc.U, cc.ph, p.iperm, Ab, cc.CK, pu, pp);
+    const int n_ph = D * c->n_phase, n_acc = 8 * n_u1 + n_ph;
+    tr_reduce<<<(n_acc + 7) / 8, 256, 0, s2>>>(D, n_u1, n_ph, pu, pp, acc);
+    QPINN_CUDA_CHECK(cudaGetLastError());
+    return pqc_param_grads<float>(c, acc, NQ, a->qp, a->g_qp, s2);
+  };
+  SideStream* side = nullptr;
+  static const bool serial = getenv("QPINN_SERIAL_BWD") != nullptr;  // A/B switch
+  if (Phi && !serial) {
+    if (int rc = side_stream(&side)) return rc;
+    QPINN_CUDA_CHECK(cudaEventRecord(side->fork, st));
+    QPINN_CUDA_CHECK(cudaStreamWaitEvent(side->s, side->fork, 0));
+  }
   // dL/dm = Abar W'^T  (D per row)
   if (int rc = tc::gemm3(4 * a->R, D, D2, Abar, D2, cc.W, D2, G, D, ws + t.g3,
                          tc::gemm3_workspace_bytes(D2, D2), st))
     return rc;
+  if (side)
+    if (int rc = weight_chain(side->s)) return rc;
   tr_embed_grad<NQ><<<gp, 256, 0, st>>>(a->scale, a->R, a->act, a->tan, G, a->g_act, a->g_tan);
-  // dL/dW' = m^T Abar  (D x 2D)
-  if (!Phi) {
-    tr_embed<NQ><<<gp, 256, 0, st>>>(a->scale, a->R, a->act, a->tan, G, nullptr);
-    Phi = G;
+  QPINN_CUDA_CHECK(cudaGetLastError());
+  if (side) {  // join
+    QPINN_CUDA_CHECK(cudaEventRecord(side->join, side->s));
+    QPINN_CUDA_CHECK(cudaStreamWaitEvent(st, side->join, 0));
+    return QPINN_OK;
   }
+  // replay path: re-embed m into G once the embedding gradient has read it
+  tr_embed<NQ><<<gp, 256, 0, st>>>(a->scale, a->R, a->act, a->tan, G, nullptr);
+  Phi = G;
   QPINN_CUDA_CHECK(cudaGetLastError());
-  if (int rc = tc::wgrad(4 * a->R, D, D2, Phi, D, Abar, D2, (float*)(ws + t.gW), ws + t.wg,
-                         tc::wgrad_workspace_bytes(4 * a->R, D2, D2), st))
-    return rc;
-  auto* Ab = (cplx<float>*)(ws + t.Ab);
-  tr_gb<<<(D * D + 255) / 256, 256, 0, st>>>(NQ, (const float*)(ws + t.gW), Ab);
-  auto* pu = (double*)(ws + t.pu);
-  auto* pp = (double*)(ws + t.pp);
-  auto* acc = (double*)(ws + t.acc);
-  tr_circuit_bwd<<<D, kTrThreads, 0, st>>>(NQ, L, ent, cc.U, cc.ph, p.iperm, Ab, cc.CK, pu, pp);
-  const int n_ph = D * c->n_phase, n_acc = 8 * n_u1 + n_ph;
-  tr_reduce<<<(n_acc + 7) / 8, 256, 0, st>>>(D, n_u1, n_ph, pu, pp, acc);
-  QPINN_CUDA_CHECK(cudaGetLastError());
-  return pqc_param_grads<float>(c, acc, NQ, a->qp, a->g_qp, st);
+  return weight_chain(st);
 }
 
 }  // namespace
