@@ -132,7 +132,12 @@ int qpinn_pqc_forward_probe(const qpinn_circuit* c, int dtype, int scale, int64_
 /* Gradients of L(z, dz) given g_z = dL/dz [R,n] and g_dz = dL/d(dz) [3,R,n]:
  * g_act_val [R,n], g_act_tan [3,R,n] and g_qparams [P] (summed over all rows
  * in a fixed, run-to-run deterministic order).  `states` is the buffer a
- * forward on the same inputs filled, or NULL to recompute the circuit. */
+ * forward on the same inputs filled, or NULL to recompute the circuit.
+ * Transfer-matrix path with `states`: part of the work runs on a per-device
+ * side stream forked from and joined back into `stream` before the call
+ * returns (CUDA-graph capturable once the first call has created it); calls
+ * on one device are not to be issued concurrently from several host threads
+ * (the reference is single-threaded). */
 int qpinn_pqc_backward(const qpinn_circuit* c, int dtype, int scale, int64_t rows,
                        const void* act_val, const void* act_tan, const void* qparams,
                        const void* states, const void* g_z, const void* g_dz,
