@@ -325,12 +325,6 @@ __device__ __forceinline__ void embed_amp(const PointAngles<NQ>& pa, int b, bool
   }
 }
 
-__device__ __forceinline__ void put_phase(float m, int b, float& re, float& im) {
-  const int ph = __popc(b) & 3;  // (-i)^popcount
-  re = ph == 0 ? m : ph == 2 ? -m : 0.f;
-  im = ph == 1 ? -m : ph == 3 ? m : 0.f;
-}
-
 // lane l ends with the warp total of value index l (recursive halving, 31 shuffles)
 __device__ __forceinline__ void reduce_scatter32(float (&v)[32]) {
   const int lane = threadIdx.x & 31;
@@ -672,12 +666,18 @@ struct SideStream {
 SideStream g_side[64];
 std::mutex g_side_mu;
 
-int side_stream(SideStream** out) {
+// *out = nullptr (serial fallback) when the stream and events do not exist yet
+// and `st` is being captured (creating them would invalidate the capture)
+int side_stream(cudaStream_t st, SideStream** out) {
   int dev = 0;
   QPINN_CUDA_CHECK(cudaGetDevice(&dev));
   std::lock_guard<std::mutex> lk(g_side_mu);
   SideStream& ss = g_side[dev & 63];
+  *out = nullptr;
   if (!ss.s) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    QPINN_CUDA_CHECK(cudaStreamIsCapturing(st, &cs));
+    if (cs != cudaStreamCaptureStatusNone) return QPINN_OK;
     QPINN_CUDA_CHECK(cudaStreamCreateWithFlags(&ss.s, cudaStreamNonBlocking));
     QPINN_CUDA_CHECK(cudaEventCreateWithFlags(&ss.fork, cudaEventDisableTiming));
     QPINN_CUDA_CHECK(cudaEventCreateWithFlags(&ss.join, cudaEventDisableTiming));
@@ -773,8 +773,9 @@ int bwd_n(const qpinn_circuit* c, const KArgs<float>* a, unsigned char* ws, cons
   };
   SideStream* side = nullptr;
   static const bool serial = getenv("QPINN_SERIAL_BWD") != nullptr;  // A/B switch
-  if (Phi && !serial) {
-    if (int rc = side_stream(&side)) return rc;
+  if (Phi && !serial)
+    if (int rc = side_stream(st, &side)) return rc;
+  if (side) {
     QPINN_CUDA_CHECK(cudaEventRecord(side->fork, st));
     QPINN_CUDA_CHECK(cudaStreamWaitEvent(side->s, side->fork, 0));
   }
