@@ -385,8 +385,11 @@ __global__ void __launch_bounds__(256, QPINN_TR_EMB_MINB) tr_embed(int scale, in
 }
 
 // z_q = sum_b |psi_b|^2 s_bq, dz_kq = sum_b 2 Re(conj(psi_b) dpsi_kb) s_bq (qsim.py:369-381)
+#ifndef QPINN_TR_RD_MINB
+#define QPINN_TR_RD_MINB 1
+#endif
 template <int NQ>
-__global__ void __launch_bounds__(256) tr_readout(int64_t R, int ns, const float* __restrict__ Psi,
+__global__ void __launch_bounds__(256, QPINN_TR_RD_MINB) tr_readout(int64_t R, int ns, const float* __restrict__ Psi,
                                                   float* __restrict__ z, float* __restrict__ dz) {
   constexpr int D = 1 << NQ, D2 = 2 * D;
   const int lane = threadIdx.x & 31;
@@ -425,8 +428,11 @@ __global__ void __launch_bounds__(256) tr_readout(int64_t R, int ns, const float
 
 // adjoint seeds as real-block rows:
 // lambda = 2 w psi + 2 sum_k v_k dpsi_k, mu_k = 2 v_k psi
+#ifndef QPINN_TR_SD_MINB
+#define QPINN_TR_SD_MINB 1
+#endif
 template <int NQ>
-__global__ void __launch_bounds__(256) tr_seed(int64_t R, const float* __restrict__ gz,
+__global__ void __launch_bounds__(256, QPINN_TR_SD_MINB) tr_seed(int64_t R, const float* __restrict__ gz,
                                                const float* __restrict__ gdz,
                                                const float* __restrict__ Psi,
                                                float* __restrict__ Abar) {
