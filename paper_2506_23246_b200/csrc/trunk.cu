@@ -375,6 +375,9 @@ __global__ void __launch_bounds__(1024) colsum_reduce(int nb, int N, const doubl
 // dL/dtau_raw through at = 2 pi t / tau and the t-tangent features (one warp per point;
 // the per-point trig of a block's kFeatBPB points is computed once into shared memory)
 // (cos, sin of the projections are read back from the forward's H0 value channel)
+#ifndef QPINN_FEATB_RECOMP
+#define QPINN_FEATB_RECOMP 1  // 81 vs 88 us: the pass is latency-bound, the trig is cheaper than the loads
+#endif
 constexpr int kFeatBPB = 64;
 #ifndef QPINN_FEATB_UNROLL
 #define QPINN_FEATB_UNROLL 2  // with the 4-deep feature loop: 89 vs 95 us (measured)
@@ -416,7 +419,14 @@ __global__ void __launch_bounds__(256) features_bwd(int64_t R, int F, const T* _
         const T* om = omega + 6 * f;
         const T dps[3] = {T(kPi) * cx * om[0] - T(kPi) * sx * om[1],
                           T(kPi) * cy * om[2] - T(kPi) * sy * om[3], w * ct * om[4] - w * st * om[5]};
+#if QPINN_FEATB_RECOMP
+        // cos/sin of the projection recomputed (as features_fwd) instead of read back
+        const T proj = sx * om[0] + cx * om[1] + sy * om[2] + cy * om[3] + st * om[4] + ct * om[5];
+        T sp, cp;
+        sincos_t(proj, &sp, &cp);
+#else
         const T cp = H0[p * W + f], sp = H0[p * W + F + f];
+#endif
         const T gc = G0[p * W + f], gs = G0[p * W + F + f];
         T gproj = -sp * gc + cp * gs, gdp2 = 0;
 #pragma unroll
