@@ -156,12 +156,19 @@ int qpinn_pqc_domain_check(const void* workspace, void* stream, double* max_abs,
  * (8 bytes, pinned) and its reset; apply the rule above to the value after the
  * caller's own synchronisation (no extra host round trip per step). */
 int qpinn_pqc_domain_fetch(const void* workspace, void* host_dst, void* stream);
+/* Device-side form of the same rule, for a data-parallel step that carries it
+ * through its one all-reduce and vetoes the optimizer on the device: enqueues
+ * on `stream` flags_dev[0] = 1.0 if max|act_val| - 1 > 1e-12 (DomainError)
+ * else 0, flags_dev[1] = 1.0 if max|act_val| > 1 (clamped or error) else 0,
+ * flags_dev[2] = max|act_val|, and resets the running maximum.  Summed over
+ * ranks, flags_dev[0] > 0 raises on every rank. */
+int qpinn_pqc_domain_flags(const void* workspace, double* flags_dev, void* stream);
 
 /* ---- classical trunk with forward-mode tangents (network.py:133-147, :284-298)
  * periodic map -> frozen RFF -> tanh hidden layers -> tanh adapter, carried as
  * value + d/dx, d/dy, d/dt channels stacked along rows ([4, R, width]) so each
  * layer is ONE GEMM on [4R, in] x [in, out] (tensor cores, FP32-accurate
- * BF16x9 emulation for float32; DGEMM for float64).  Weights are read from
+ * 3xTF32 hi/lo split for float32; DGEMM for float64).  Weights are read from
  * and gradients written to the flat parameter vector at the given offsets. */
 typedef struct qpinn_trunk_desc {
   int32_t n_hidden;      /* hidden tanh layers (3 for the hybrid, network.py:188-189) */
@@ -264,14 +271,18 @@ int qpinn_loss_finalize(const qpinn_loss_spec* s, const double* sums_dev,
 
 /* ---- Adam (training.py:87-111) ------------------------------------------ */
 /* If the loss *loss_dev (optional, device double) is non-finite, *flag_dev
- * gets bit 2; if any grad entry is non-finite it gets bit 1; in either case
- * nothing is updated (the reference raises RunAborted before touching its
- * state, training.py:104-105, :363-364).  Otherwise m, v, params are updated
+ * gets bit 2; if any grad entry is non-finite it gets bit 1; if the optional
+ * *veto_dev is non-zero (the step's reduced domain flag, see
+ * qpinn_pqc_domain_flags) it gets bit 4; in every case nothing is updated
+ * (the reference raises RunAborted before touching its state,
+ * training.py:104-105, :363-364, and DomainError in the forward,
+ * ansatz.py:51-58).  Otherwise m, v, params are updated
  * in place with bias correction for step t (1-based, i.e. the value of
  * AdamState.t after its increment). */
 int qpinn_adam_step(int dtype, int64_t n, void* params, const void* grad, void* m,
                     void* v, int64_t t, double lr, double beta1, double beta2,
-                    double eps, const double* loss_dev, int32_t* flag_dev, void* stream);
+                    double eps, const double* loss_dev, const double* veto_dev,
+                    int32_t* flag_dev, void* stream);
 
 /* ---- FP32-accurate tensor-core GEMM (the trunk's dense layers) ------------ */
 /* C[m,n] = A[m,k] B[n,k]^T in float32 on the tcgen05 TF32 tensor cores with

@@ -74,6 +74,7 @@ SIGNATURES = [
     ("qpinn_pqc_forward_probe", _I, [_VP, _I, _I, _I64, _VP, _VP, _VP, _VP, _VP, _SZ, _VP]),
     ("qpinn_pqc_domain_check", _I, [_VP, _VP, C.POINTER(_D), C.POINTER(_I)]),
     ("qpinn_pqc_domain_fetch", _I, [_VP, _VP, _VP]),
+    ("qpinn_pqc_domain_flags", _I, [_VP, _VP, _VP]),
     ("qpinn_loss_workspace_bytes", _SZ, [C.POINTER(LossSpec), _I, _I64]),
     ("qpinn_loss_forward_backward", _I, [C.POINTER(LossSpec), _I, _I64, _VP, _VP, _VP, _VP,
                                          _VP, _VP, _VP, _SZ, _VP]),
@@ -87,7 +88,8 @@ SIGNATURES = [
                                        _VP, _SZ, _VP]),
     ("qpinn_trunk_backward", _I, [C.POINTER(TrunkDesc), _I, _I64, _VP, _VP, _VP, _VP, _VP, _VP,
                                   _VP, _VP, _SZ, _VP]),
-    ("qpinn_adam_step", _I, [_I, _I64, _VP, _VP, _VP, _VP, _I64, _D, _D, _D, _D, _VP, _VP, _VP]),
+    ("qpinn_adam_step", _I, [_I, _I64, _VP, _VP, _VP, _VP, _I64, _D, _D, _D, _D, _VP, _VP, _VP,
+                             _VP]),
     ("qpinn_gemm_f32_workspace_bytes", _SZ, [_I, _I]),
     ("qpinn_gemm_f32", _I, [_I64, _I, _I, _VP, _I64, _VP, _I64, _VP, _I64, _VP, _SZ, _VP]),
     ("qpinn_gemm_f32_atb_workspace_bytes", _SZ, [_I64, _I, _I]),

@@ -160,7 +160,10 @@ class CircuitSpec:
         key = (dtype, str(device))
         ws = self._workspaces.get(key)
         if ws is None or ws.numel() < need:
-            ws = torch.zeros(need, dtype=torch.uint8, device=device)
+            grown = torch.zeros(need, dtype=torch.uint8, device=device)
+            if ws is not None:  # keep the running max|a| of forwards not yet checked
+                grown[:8].copy_(ws[:8])
+            ws = grown
             self._workspaces[key] = ws
         return ws
 

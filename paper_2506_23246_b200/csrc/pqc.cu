@@ -619,6 +619,21 @@ static void big_ws(const qpinn_circuit* c, void* ws, double** partial, double** 
   *tables = (unsigned char*)base;
 }
 
+// The reference domain rule (ansatz.py:51-58) as device flags, so a
+// data-parallel step can carry it through its one all-reduce and veto Adam:
+// out[0] = 1 if max|a| - 1 > 1e-12 (DomainError), out[1] = 1 if max|a| > 1
+// (clamped, or the error), out[2] = max|a|; the running maximum is reset.
+__global__ void pqc_domain_flags(unsigned long long* maxabs, double* out) {
+  const unsigned long long bits = *maxabs;
+  double m;
+  memcpy(&m, &bits, 8);
+  const double over = m - 1.0;
+  out[0] = over > 1e-12 ? 1.0 : 0.0;
+  out[1] = over > 0.0 ? 1.0 : 0.0;
+  out[2] = m;
+  *maxabs = 0ull;
+}
+
 }  // namespace qpinn
 
 using namespace qpinn;
@@ -914,6 +929,14 @@ int qpinn_pqc_domain_fetch(const void* workspace, void* host_dst, void* stream) 
   QPINN_CUDA_CHECK(cudaMemcpyAsync(host_dst, workspace, 8, cudaMemcpyDeviceToHost,
                                    (cudaStream_t)stream));
   QPINN_CUDA_CHECK(cudaMemsetAsync(const_cast<void*>(workspace), 0, 8, (cudaStream_t)stream));
+  return QPINN_OK;
+}
+
+int qpinn_pqc_domain_flags(const void* workspace, double* flags_dev, void* stream) {
+  if (!workspace || !flags_dev) return fail(QPINN_ERR_CONFIG, "domain flags: null pointer");
+  pqc_domain_flags<<<1, 1, 0, (cudaStream_t)stream>>>(
+      (unsigned long long*)const_cast<void*>(workspace), flags_dev);
+  QPINN_CUDA_CHECK(cudaGetLastError());
   return QPINN_OK;
 }
 

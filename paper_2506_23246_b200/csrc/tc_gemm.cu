@@ -40,6 +40,25 @@ __device__ unsigned long long g_gemm_prof[16];
 #else
 #define GPROF(slot, call) call
 #endif
+// Ablation switches for timing experiments (scripts/gemm_ablate.sh); all 0 in
+// the shipped build.  NOSTORE: epilogue skips the output stores; NOPROMO: one
+// TMEM read per tile instead of one per promotion group; NOSPLIT: the split
+// warps skip the hi/lo split (stale operands); NOMMA: commits without MMAs.
+#ifndef QPINN_ABL_NOSTORE
+#define QPINN_ABL_NOSTORE 0
+#endif
+#ifndef QPINN_ABL_NOPROMO
+#define QPINN_ABL_NOPROMO 0
+#endif
+#ifndef QPINN_ABL_NOSPLIT
+#define QPINN_ABL_NOSPLIT 0
+#endif
+#ifndef QPINN_ABL_NOMMA
+#define QPINN_ABL_NOMMA 0
+#endif
+#ifndef QPINN_ABL_NOB  // B tiles loaded once per CTA (stale after), not per k-block
+#define QPINN_ABL_NOB 0
+#endif
 constexpr int kBM = 128, kBK = 32;
 // k-blocks accumulated in one TMEM buffer before the epilogue warps add it into
 // fp32 registers.  1: 32-deep tensor-core chains, 3.5e-7 relative at K = 256;
@@ -229,6 +248,10 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUt
           const int e = (int)(j % BS);
           if (j >= BS) GPROF(1, mbar_wait(b_empty + e, (uint32_t)(((j / BS) - 1) & 1)));
           unsigned char* st = bst + e * Cfg::kBStage;
+          if (QPINN_ABL_NOB && j >= BS) {
+            mbar_arrive(b_full + e);
+            continue;
+          }
           mbar_expect_tx(b_full + e, 2 * Cfg::kBBytes);
           tma_load_2d(st, &mBhi, b_full + e, kb * kBK, nt * BN);
           tma_load_2d(st + Cfg::kBBytes, &mBlo, b_full + e, kb * kBK, nt * BN);
@@ -251,7 +274,8 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUt
           const uint32_t b_hi = smem_u32(bst + e * Cfg::kBStage);
           const uint32_t b_lo = b_hi + Cfg::kBBytes;
           const uint32_t d = tmem + b * BN;
-          if constexpr (Cfg::kATmem) {
+          if constexpr (QPINN_ABL_NOMMA) {
+          } else if constexpr (Cfg::kATmem) {
             const uint32_t a_hi = tmem + Cfg::kACol + o * 2 * kBK, a_lo = a_hi + kBK;
 #pragma unroll
             for (int k = 0; k < kBK / 8; ++k) {
@@ -297,6 +321,10 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUt
         }
         if (warp == 0) GPROF(6, mbar_wait(raw_full + r, (uint32_t)((j / RS) & 1)));
         else mbar_wait(raw_full + r, (uint32_t)((j / RS) & 1));
+        if constexpr (QPINN_ABL_NOSPLIT) {
+          __syncwarp();
+          if (lane == 0) mbar_arrive(raw_empty + r);
+        } else {
         const uint32_t src = smem_u32(raw + r * kABytes) + row * 128;
         float4 v[8];
 #pragma unroll
@@ -315,6 +343,7 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUt
         tmem_st32(a, hi);
         tmem_st32(a + kBK, lo);
         tmem_st_wait();
+        }
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(conv + o);
@@ -374,12 +403,14 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUt
         if (warp == 4) GPROF(7, mbar_wait(tfull + b, (uint32_t)((j / NB) & 1)));
         else mbar_wait(tfull + b, (uint32_t)((j / NB) & 1));
         tc_fence_after();
+        if (!QPINN_ABL_NOPROMO || gi == ngrp - 1) {
 #pragma unroll
-        for (int c0 = 0; c0 < CW; c0 += 32) {
-          float v[32];
-          tmem_ld32(tmem + lane_base + b * BN + c_off + c0, v);
+          for (int c0 = 0; c0 < CW; c0 += 32) {
+            float v[32];
+            tmem_ld32(tmem + lane_base + b * BN + c_off + c0, v);
 #pragma unroll
-          for (int i = 0; i < 32; ++i) acc[c0 + i] += v[i];
+            for (int i = 0; i < 32; ++i) acc[c0 + i] += v[i];
+          }
         }
         tc_fence_before();
         __syncwarp();
@@ -394,7 +425,9 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUt
           }
         }
         const int64_t row = mt * kBM + q * 32 + lane;
-        if (g.tma_store) {
+        if (QPINN_ABL_NOSTORE) {
+          if (acc[0] == 1.2345e-30f) g.C[0] = acc[CW - 1];
+        } else if (g.tma_store) {
           if (warp == 4)
             GPROF(8, (store_rows_tma<CW>(acc, my_stg, &mC, n0 + c_off, (int)(mt * kBM + q * 32), 0,
                                          lane, sidx)));

@@ -105,6 +105,61 @@ class InferenceEngine:
         N.count_launches(1 + sum(2 if (self.dtype == torch.float32 and k % 4 == 0) else 1
                                  for k in widths) + 2)
 
+    def _trunk_launches(self) -> int:
+        widths = [2 * self.model.config.rff_features] + \
+            [self.model.config.hidden_width] * self.model.n_hidden
+        return 1 + sum(2 if (self.dtype == torch.float32 and k % 4 == 0) else 1 for k in widths)
+
+    def adapter(self, flat, x, y, t) -> torch.Tensor:
+        """Adapter activations a [R, n] (network.py:323-335): value trunk only."""
+        lib, st, dc = N.lib(), N.stream_ptr(), self.dcode
+        R = x.shape[0]
+        out = torch.empty((R, self.n), dtype=self.dtype, device=self.device)
+        for lo, hi in self._chunks(x):
+            N.check(lib.qpinn_trunk_forward_value(
+                C.byref(self.desc), dc, hi - lo, x[lo:].data_ptr(), y[lo:].data_ptr(),
+                t[lo:].data_ptr(), flat.data_ptr(), out[lo:].data_ptr(), self.trunk_ws.data_ptr(),
+                self.trunk_ws.numel(), st), "qpinn_trunk_forward_value")
+            N.count_launches(self._trunk_launches())
+        return out
+
+    def dual_fields(self, flat, x, y, t):
+        """(out [R, 3], dout [3, R, 3]): fields and their x/y/t jacobians
+        (network.py:284-308 with derivs) on our kernels only: the dual trunk
+        (tensor-core layers with the fused dual tanh), K1 with tangents, the
+        head kernel on the values and on the stacked tangents."""
+        lib, st, dc, n = N.lib(), N.stream_ptr(), self.dcode, self.n
+        es = flat.element_size()
+        R = x.shape[0]
+        if getattr(self, "_act4", None) is None:
+            self._act4 = torch.empty(4 * self.chunk * n, dtype=self.dtype, device=self.device)
+            self._z4 = torch.empty(4 * self.chunk * n, dtype=self.dtype, device=self.device)
+            self._dout = torch.empty(3 * self.chunk * 3, dtype=self.dtype, device=self.device)
+            self._zero_b = torch.zeros(3, dtype=self.dtype, device=self.device)
+        out = torch.empty((R, 3), dtype=self.dtype, device=self.device)
+        dout = torch.empty((3, R, 3), dtype=self.dtype, device=self.device)
+        fp = flat.data_ptr()
+        w_out, b_out = fp + self.off_out_w * es, fp + self.off_out_b * es
+        for lo, hi in self._chunks(x):
+            r = hi - lo
+            a0, z0 = self._act4.data_ptr(), self._z4.data_ptr()
+            N.check(lib.qpinn_trunk_forward(
+                C.byref(self.desc), dc, r, x[lo:].data_ptr(), y[lo:].data_ptr(),
+                t[lo:].data_ptr(), fp, a0, self.trunk_ws.data_ptr(), self.trunk_ws.numel(), st),
+                "qpinn_trunk_forward")
+            N.check(lib.qpinn_pqc_forward(
+                self.model.circuit.handle, dc, self.scale, r, a0, a0 + r * n * es,
+                fp + self.off_q * es, z0, z0 + r * n * es, 0, self.pqc_ws.data_ptr(),
+                self.pqc_ws.numel(), st), "qpinn_pqc_forward")
+            N.check(lib.qpinn_head_forward(dc, r, n, z0, w_out, b_out, out[lo:].data_ptr(), st),
+                    "qpinn_head_forward")
+            N.check(lib.qpinn_head_forward(dc, 3 * r, n, z0 + r * n * es, w_out,
+                                           self._zero_b.data_ptr(), self._dout.data_ptr(), st),
+                    "qpinn_head_forward")
+            dout[:, lo:hi].copy_(self._dout[:3 * r * 3].view(3, r, 3))
+            N.count_launches(self._trunk_launches() + 2 + 2)
+        return out, dout
+
     def check_domain(self):
         """The reference's |a| <= 1 rule on every forward since the last check."""
         from .ansatz import check_domain

@@ -440,5 +440,6 @@ class LossEvaluator:
         bd = self.finalize(sums, wd)
         if self.model.circuit is not None:
             from .ansatz import check_domain
-            check_domain(self.model.circuit, self.dtype, self.device)
+            check_domain(self.model.circuit, self.dtype, self.device,
+                         ws=self.engine.pqc_ws if native and self.engine is not None else None)
         return EpochEval(self.breakdown_from(bd.cpu().numpy()), grad)

@@ -25,7 +25,7 @@ import numpy as np
 import torch
 
 from . import _native as N
-from .errors import ConfigError, RunAborted
+from .errors import ConfigError, DomainError, RunAborted
 from .network import Model, ModelConfig, ParameterStore, build_model, save_checkpoint
 from .physics import (CollocationGrid, LossBreakdown, LossEvaluator, MaterialMap, default_t_end,
                       time_bin_weights)
@@ -106,19 +106,24 @@ class AdamState:
 
 def adam_step(params: ParameterStore, grad: torch.Tensor, state: AdamState, lr: float,
               loss_dev: Optional[torch.Tensor] = None, flag: Optional[torch.Tensor] = None,
-              sync: bool = True) -> None:
+              sync: bool = True, veto: Optional[torch.Tensor] = None) -> None:
     """Bias-corrected Adam in place (training.py:101-111); RunAborted on a
-    non-finite gradient (or loss) with params and state untouched."""
+    non-finite gradient (or loss) with params and state untouched.  A non-zero
+    device ``veto`` (the step's reduced domain flag) skips the update the same
+    way and raises DomainError, as the reference's forward does before any
+    update (ansatz.py:51-58)."""
     flat = params.flat if isinstance(params, ParameterStore) else params
     if flag is None:
         flag = torch.zeros(1, dtype=torch.int32, device=flat.device)
     N.check(N.lib().qpinn_adam_step(
         N.dtype_code(flat.dtype), flat.numel(), N.ptr(flat), N.ptr(grad.contiguous()),
         N.ptr(state.m), N.ptr(state.v), state.t + 1, lr, state.beta1, state.beta2, state.eps,
-        N.ptr(loss_dev), N.ptr(flag), N.stream_ptr()), "qpinn_adam_step")
+        N.ptr(loss_dev), N.ptr(veto), N.ptr(flag), N.stream_ptr()), "qpinn_adam_step")
     N.count_launches(2)
     if sync:
         f = int(flag.item())
+        if f & 4:
+            raise DomainError("scale input exceeds [-1, 1] by more than 1e-12")
         if f:
             raise RunAborted("non-finite gradient" if f & 1 else "non-finite loss")
         state.t += 1
@@ -145,17 +150,35 @@ def allreduce_fn(group=None) -> Callable[[torch.Tensor], None]:
     return fn
 
 
-def reduce_packed(grad: torch.Tensor, sums: torch.Tensor, reduce_fn, packed: Optional[torch.Tensor] = None):
-    """Pack (grad as float64, sums), reduce once, unpack in place."""
-    n = grad.numel()
-    if packed is None:
-        packed = torch.empty(n + sums.numel(), dtype=torch.float64, device=grad.device)
-    packed[:n].copy_(grad.reshape(-1))
-    packed[n:].copy_(sums)
+def reduce_packed(grad: Optional[torch.Tensor], sums: torch.Tensor, reduce_fn,
+                  packed: Optional[torch.Tensor] = None, extra: Optional[torch.Tensor] = None):
+    """Pack (grad as float64, sums, extra), reduce once, unpack in place.
+    ``extra`` carries the step's domain flags (``qpinn_pqc_domain_flags``), so
+    a DomainError on any rank is seen -- and raised -- by every rank."""
+    parts = [t for t in (grad, sums, extra) if t is not None]
+    sizes = [t.numel() for t in parts]
+    if packed is None or packed.numel() != sum(sizes):
+        packed = torch.empty(sum(sizes), dtype=torch.float64, device=sums.device)
+    o = 0
+    for t, k in zip(parts, sizes):
+        packed[o:o + k].copy_(t.reshape(-1))
+        o += k
     reduce_fn(packed)
-    grad.reshape(-1).copy_(packed[:n])
-    sums.copy_(packed[n:])
+    o = 0
+    for t, k in zip(parts, sizes):
+        t.reshape(-1).copy_(packed[o:o + k])
+        o += k
     return packed
+
+
+def raise_domain(err: float, clamped: float, max_abs: float) -> None:
+    """The reference domain rule (ansatz.py:51-58) on the step's (reduced) flags."""
+    if err > 0.0:
+        raise DomainError(f"scale input exceeds [-1, 1] by more than 1e-12 on "
+                          f"{int(round(err))} rank(s) (max |a| here {max_abs:.17g})")
+    if clamped > 0.0:
+        import warnings
+        warnings.warn("scale input clamped into [-1, 1] (excursion <= 1e-12)", stacklevel=3)
 
 
 # -- run log -------------------------------------------------------------------------
@@ -272,12 +295,13 @@ class Trainer:
         self.sums = torch.zeros(N.LOSS_NSUMS, dtype=torch.float64, device=dev)
         self.bd = torch.zeros(10, dtype=torch.float64, device=dev)
         self.flag = torch.zeros(1, dtype=torch.int32, device=dev)
+        # [DomainError flag, clamp flag, max|a|] of the step's forwards (device)
+        self.dom = torch.zeros(3, dtype=torch.float64, device=dev)
         self.weights = None
         self.weights_next = None
         self._packed = None
         self.log_grad = log_grad
-        self._host = torch.zeros(16, dtype=torch.float64, pin_memory=True)
-        self._host_dom = torch.zeros(1, dtype=torch.float64, pin_memory=True)
+        self._host = torch.zeros(20, dtype=torch.float64, pin_memory=True)
         if config.adaptive_weighting:
             # untaped initial pass (training.py:336-339)
             bins = self._evaluate_untaped()
@@ -346,15 +370,17 @@ class Trainer:
         return sum(v.numel() * v.element_size() for v in self._host_inputs)
 
     def readback_bytes(self) -> int:
-        return 11 * 8 + 8 + (32 if self.log_grad else 0)  # loss record + flag, max|a|
+        return 10 * 8 + 8 + 3 * 8 + (32 if self.log_grad else 0)  # loss record, flag, domain
 
     def _evaluate_untaped(self):
         sums = torch.zeros(N.LOSS_NSUMS, dtype=torch.float64, device=self.device)
         self._sweep(None, None, False, sums)
+        self._domain_flags()
         if self.reduce_fn is not None:
-            self.reduce_fn(sums)
+            reduce_packed(None, sums, self.reduce_fn, extra=self.dom[:2])
         bd = self.evaluator.finalize(sums, None)
-        self._check_domain()
+        d = self.dom.cpu().numpy()
+        raise_domain(d[0], d[1], d[2])
         return bd[5:10].cpu().numpy()
 
     def _sweep(self, grad, weights, tape, sums):
@@ -373,10 +399,30 @@ class Trainer:
         self.sums.zero_()
         return self._sweep(self.grad, self.weights, True, self.sums)
 
+    def _pqc_workspace(self):
+        """The workspace whose running max|a| this trainer's forwards fold into."""
+        eng = self.evaluator.engine
+        if eng is not None:
+            return eng.pqc_ws
+        return self.model.circuit.workspace(self.model.dtype, self.device, 0)
+
+    def _domain_flags(self):
+        """[error, clamp, max|a|] of the forwards since the last call, on the device."""
+        if self.model.circuit is None:
+            return
+        N.check(N.lib().qpinn_pqc_domain_flags(C.c_void_p(self._pqc_workspace().data_ptr()),
+                                               C.c_void_p(self.dom.data_ptr()),
+                                               C.c_void_p(N.stream_ptr())), "domain flags")
+        N.count_launches(1)
+
     def _reduce_finalize(self, grad):
-        """The step's one collective (data parallel), then the loss finalisation."""
+        """The step's one collective (data parallel; it also carries the domain
+        flags), then the loss finalisation."""
+        self._domain_flags()
         if self.reduce_fn is not None:
-            self._packed = reduce_packed(grad, self.sums, self.reduce_fn, self._packed)
+            self._packed = reduce_packed(grad, self.sums, self.reduce_fn, self._packed,
+                                         extra=self.dom[:2] if self.model.circuit is not None
+                                         else None)
         self.evaluator.finalize(self.sums, self.weights, self.config.kappa, self.bd,
                                 self.weights_next if self.weights is not None else None)
 
@@ -408,19 +454,14 @@ class Trainer:
         self._reduce_finalize(grad)
         return grad
 
-    def _check_domain(self):
-        if self.model.circuit is not None:
-            from .ansatz import check_domain
-            check_domain(self.model.circuit, self.model.dtype, self.device)
-
     def step(self) -> RunRow:
         """One epoch: evaluate(tape=True) -> (all-reduce) -> finalize -> Adam."""
         cfg = self.config
         epoch = self.epoch
         lr = lr_at(epoch, cfg.lr0, cfg.lr_decay, cfg.lr_decay_every)
         grad = self._device_part()
-        adam_step(self.flat, grad, self.adam, lr, loss_dev=self.bd[4:5],
-                  flag=self.flag, sync=False)
+        adam_step(self.flat, grad, self.adam, lr, loss_dev=self.bd[4:5], flag=self.flag,
+                  sync=False, veto=self.dom[0:1] if self.model.circuit is not None else None)
         host = self._host
         host[:10].copy_(self.bd, non_blocking=True)
         host[10:11].copy_(self.flag, non_blocking=True)
@@ -433,16 +474,11 @@ class Trainer:
             if q.numel():
                 host[13:14].copy_(torch.linalg.vector_norm(q).reshape(1), non_blocking=True)
                 host[14:15].copy_(torch.var(q, unbiased=False).reshape(1), non_blocking=True)
-        if self.model.circuit is not None:  # max|a| rides along with the step's one sync
-            ws = self.model.circuit.workspace(self.model.dtype, self.device, 0)
-            N.check(N.lib().qpinn_pqc_domain_fetch(C.c_void_p(ws.data_ptr()),
-                                                   C.c_void_p(self._host_dom.data_ptr()),
-                                                   C.c_void_p(N.stream_ptr())), "domain fetch")
+        host[15:18].copy_(self.dom, non_blocking=True)  # domain flags ride along
         torch.cuda.current_stream().synchronize()
-        if self.model.circuit is not None:
-            from .ansatz import domain_rule
-            domain_rule(float(self._host_dom[0]))
         v = host.numpy()
+        # the forward's DomainError comes first, as in the reference (Adam was vetoed)
+        raise_domain(v[15], v[16], v[17])
         f = int(v[10])
         if f:
             raise RunAborted(("non-finite loss" if f & 2 else "non-finite gradient")

@@ -1,0 +1,155 @@
+// Microbenchmark: issue rate of tcgen05.mma kind::tf32 for the operand
+// patterns of the 3xTF32 GEMMs (csrc/tc_gemm.cu), one CTA per SM, operands
+// static (no producers), to separate the tensor pipe's own rate from the
+// kernel's pipeline coordination.
+//
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -I paper_2506_23246_b200/csrc \
+//        scripts/probes/mma_rate.cu -o scripts/probes/mma_rate -lcuda
+//
+// Prints cycles per MMA and MAC/cycle/SM per variant; the B300 guide's floor
+// for cta_group::1 is max(M,128) * N / 256 cycles per dispatch (64 at M = N = 128).
+#include <cstdio>
+#include <cuda_runtime.h>
+
+#include "tc_gemm.cuh"
+
+using namespace qpinn::tc;
+
+__device__ __forceinline__ void mma_tf32_2cta(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc,
+                                              uint32_t acc) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(d),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc)
+      : "memory");
+}
+
+// variant: 0 = A TMEM (ts), 1 = A smem (ss); N = 64/128/256; chain = MMAs per commit
+// LOAD: 0 = MMA alone; 1 = warps 4..11 stream tcgen05.ld of 32 columns meanwhile
+// (the promotion reads of tc_gemm.cu); 2 = warps 4..7 stream tcgen05.st (the A split)
+template <int N, int VAR, int LOAD = 0>
+__global__ void __launch_bounds__(384, 1) mma_rate(int iters, int chain, unsigned long long* out) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* smem = (unsigned char*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  __shared__ uint64_t bar;
+  __shared__ uint32_t tslot;
+  const int warp = threadIdx.x >> 5;
+  // zero operands
+  for (int i = threadIdx.x; i < 64 * 1024 / 4; i += blockDim.x) ((float*)smem)[i] = 0.f;
+  if (threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    mbar_init_fence();
+  }
+  if (warp == 0) tmem_alloc(&tslot, 512);
+  fence_proxy_async_smem();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tslot;
+  __shared__ volatile int done;
+  if (threadIdx.x == 0) done = 0;
+  __syncthreads();
+  if (LOAD && warp >= 4) {
+    const int q = warp & 3;
+    const uint32_t lane_base = (uint32_t)(q * 32) << 16;
+    float v[32];
+    for (int i = 0; i < 32; ++i) v[i] = 0.f;
+    float acc = 0.f;
+    if (LOAD == 1) {
+      while (!done) {
+        for (int r = 0; r < 8; ++r) {
+          tmem_ld32(tmem + lane_base + 384 + 32 * (warp >> 2 & 1) + (r & 1) * 64, v);
+          acc += v[r];
+        }
+      }
+    } else if (warp < 8) {
+      while (!done) {
+        for (int r = 0; r < 8; ++r) tmem_st32(tmem + lane_base + 384 + (r & 3) * 32, v);
+        tmem_st_wait();
+      }
+    }
+    if (acc == 12345.f) out[0] = 1;
+  }
+  if (threadIdx.x == 0) {
+    constexpr uint32_t idesc = idesc_tf32(128, N);
+    const uint32_t a_s = smem_u32(smem), b_s = smem_u32(smem + 16384);
+    const uint32_t d = tmem;                      // N columns
+    const uint32_t a_t = tmem + 256;              // A in TMEM (8 columns per k-step)
+    uint32_t ph = 0;
+    const long long t0 = clock64();
+    int issued = 0;
+    for (int it = 0; it < iters; ++it) {
+      for (int c = 0; c < chain; ++c, ++issued) {
+        const uint32_t off = (c & 3) * 32;
+        if (VAR == 0)
+          mma_tf32_ts(d, a_t + (c & 3) * 8, desc_k_sw128(b_s + off), idesc, 1);
+        else
+          mma_tf32(d, desc_k_sw128(a_s + off), desc_k_sw128(b_s + off), idesc, 1);
+      }
+      mma_commit(&bar);
+      mbar_wait(&bar, ph);
+      ph ^= 1;
+    }
+    const long long t1 = clock64();
+    out[blockIdx.x] = (unsigned long long)(t1 - t0);
+    out[gridDim.x + blockIdx.x] = issued;
+    done = 1;
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) tmem_dealloc(tmem, 512);
+}
+
+template <int N, int VAR, int LOAD = 0>
+void run(const char* name, int chain, int iters) {
+  int sms = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  unsigned long long* d;
+  cudaMalloc(&d, 2 * sms * sizeof(unsigned long long));
+  cudaFuncSetAttribute(mma_rate<N, VAR, LOAD>, cudaFuncAttributeMaxDynamicSharedMemorySize, 80 * 1024);
+  mma_rate<N, VAR, LOAD><<<sms, 384, 80 * 1024>>>(iters / 10, chain, d);  // warm
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  cudaEventRecord(e0);
+  mma_rate<N, VAR, LOAD><<<sms, 384, 80 * 1024>>>(iters, chain, d);
+  cudaEventRecord(e1);
+  cudaError_t err = cudaDeviceSynchronize();
+  if (err != cudaSuccess) {
+    printf("%s: %s\n", name, cudaGetErrorString(err));
+    return;
+  }
+  float ms;
+  cudaEventElapsedTime(&ms, e0, e1);
+  unsigned long long h[2 * 256];
+  cudaMemcpy(h, d, 2 * sms * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
+  double cyc = 0, n = 0;
+  for (int i = 0; i < sms; ++i) {
+    cyc += h[i];
+    n += h[sms + i];
+  }
+  cyc /= sms;
+  n /= sms;
+  const double per = cyc / n;
+  const double macs = 128.0 * N * 8 / per;
+  const double tflops = 2.0 * 128 * N * 8 * n * sms / (ms * 1e-3) / 1e12;
+  printf("%-28s chain %3d: %7.1f cyc/MMA  %7.0f MAC/cyc/SM  %7.1f TFLOP/s tf32 (wall %.3f ms)\n",
+         name, chain, per, macs, tflops, ms);
+  cudaFree(d);
+}
+
+int main() {
+  for (int chain : {12, 48}) {
+    run<128, 0, 1>("ts N128 + 8 warps tmem.ld", chain, 4000);
+    run<128, 0, 2>("ts N128 + 4 warps tmem.st", chain, 4000);
+    run<128, 1, 1>("ss N128 + 8 warps tmem.ld", chain, 4000);
+    run<256, 1, 1>("ss N256 + 8 warps tmem.ld", chain, 2000);
+    run<64, 0>("ts M128 N64", chain, 4000);
+    run<128, 0>("ts M128 N128", chain, 4000);
+    run<256, 0>("ts M128 N256", chain, 2000);
+    run<64, 1>("ss M128 N64", chain, 4000);
+    run<128, 1>("ss M128 N128", chain, 4000);
+    run<256, 1>("ss M128 N256", chain, 2000);
+  }
+  return 0;
+}

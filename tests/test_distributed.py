@@ -89,3 +89,44 @@ def test_shard_evaluators_cover_grid_once():
         for _, sl in ev.chunks:
             seen += list(sl)
     assert sorted(seen) == list(range(grid.nt))
+
+
+def _domain_worker(rank, world, port, out):
+    """Rank 1 alone sees |a| > 1 + 1e-12: the flags ride in the packed
+    all-reduce, so every rank raises DomainError (none is left blocked in the
+    next collective)."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2506_23246_b200.errors import DomainError
+    from paper_2506_23246_b200.training import allreduce_fn, raise_domain, reduce_packed
+    grad = torch.full((5,), float(rank), dtype=torch.float32)
+    sums = torch.zeros(23, dtype=torch.float64)
+    dom = torch.tensor([1.0, 1.0, 1.5] if rank == 1 else [0.0, 0.0, 0.7], dtype=torch.float64)
+    reduce_packed(grad, sums, allreduce_fn(), extra=dom[:2])
+    try:
+        raise_domain(*dom.tolist())
+        out[rank] = "no error"
+    except DomainError as e:
+        out[rank] = "DomainError: " + str(e)
+    # the process group is still usable by every rank afterwards
+    t = torch.ones(1)
+    dist.all_reduce(t)
+    out[f"after{rank}"] = float(t)
+    dist.destroy_process_group()
+
+
+def test_domain_error_on_one_rank_raises_on_every_rank():
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_domain_worker, args=(2, _free_port(), out), nprocs=2, join=True)
+    for r in range(2):
+        assert out[r].startswith("DomainError"), out[r]
+        assert out[f"after{r}"] == 2.0
+
+
+def test_clamp_flag_warns_without_error():
+    from paper_2506_23246_b200.training import raise_domain
+    with pytest.warns(UserWarning, match="clamped"):
+        raise_domain(0.0, 1.0, 1.0 + 1e-13)
+    raise_domain(0.0, 0.0, 0.9)

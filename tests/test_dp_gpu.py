@@ -71,3 +71,48 @@ def test_two_ranks_match_single_rank():
         assert np.max(d) <= 1e-9, np.max(d)
         assert np.mean(d <= 1e-13 * np.maximum(np.abs(flat), 1.0)) > 0.99
     assert np.array_equal(out[0][1], out[1][1])  # replicated Adam: identical parameters
+
+
+def _domain_worker(rank, world, port, out):
+    """The real engine on two ranks: rank 1's PQC forward folds max|a| = 1.5
+    (written into its running maximum, as a kernel excursion would be) -> the
+    domain flags travel in the step's one all-reduce, Adam is vetoed on the
+    device and both ranks raise DomainError with their parameters untouched."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2506_23246_b200.errors import DomainError
+    from paper_2506_23246_b200.training import Trainer
+
+    def host_allreduce(t):
+        c = t.cpu()
+        dist.all_reduce(c)
+        t.copy_(c)
+
+    tr = Trainer(_cfg(), device="cuda:0", dtype=torch.float32, rank=rank, world_size=world,
+                 reduce_fn=host_allreduce)
+    tr.step()
+    before = tr.flat.detach().cpu().numpy().copy()
+    t_before = tr.adam.t
+    if rank == 1:
+        tr._pqc_workspace()[:8].copy_(
+            torch.tensor([1.5], dtype=torch.float64).view(torch.uint8).to("cuda:0"))
+    try:
+        tr.step()
+        out[rank] = "no error"
+    except DomainError as e:
+        out[rank] = "DomainError: " + str(e)
+    out[f"same{rank}"] = bool(np.array_equal(before, tr.flat.detach().cpu().numpy())) and \
+        tr.adam.t == t_before
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_domain_error_on_rank1_raises_on_both_ranks():
+    ctx = mp.get_context("spawn")
+    out = ctx.Manager().dict()
+    mp.start_processes(_domain_worker, args=(2, _free_port(), out), nprocs=2, join=True,
+                       start_method="spawn")
+    for r in range(2):
+        assert out[r].startswith("DomainError"), out[r]
+        assert out[f"same{r}"], "Adam must be vetoed: parameters and step count unchanged"

@@ -67,9 +67,21 @@ def test_predict_native_matches_autograd_path():
     rng = np.random.default_rng(3)
     x, y, t = rng.uniform(-1, 1, 777), rng.uniform(-1, 1, 777), rng.uniform(0, 1.5, 777)
     fb = m.predict(p, x, y, t)
-    ref, _ = m.forward(p, x, y, t)
+    ref, _ = m.forward(p, x, y, t, native=False)
     for a, b in zip((fb.ez, fb.hx, fb.hy), (ref.ez, ref.hx, ref.hy)):
         assert torch.allclose(a, b, rtol=1e-11, atol=1e-12)
+    # Model.forward itself (native by default) with and without jacobians
+    nat, dnat = m.forward(p, x, y, t, derivs=True)
+    ref, dref = m.forward(p, x, y, t, derivs=True, native=False)
+    for a, b in zip((nat.ez, nat.hx, nat.hy, dnat.ez, dnat.hx, dnat.hy),
+                    (ref.ez, ref.hx, ref.hy, dref.ez, dref.hx, dref.hy)):
+        assert torch.allclose(a, b, rtol=1e-11, atol=1e-12)
+    a_nat = m.adapter_activations(p, x, y, t)
+    pv = m.views(p.flat)
+    X, Y, T = m._coords(x, y, t)
+    h, _ = m.trunk(pv, X, Y, T, False)
+    assert torch.allclose(a_nat, torch.tanh(h @ pv["adapter.W"] + pv["adapter.b"]),
+                          rtol=1e-11, atol=1e-12)
 
 
 def test_train_with_probes_matches_reference():

@@ -6,7 +6,7 @@ import pytest
 import torch
 
 from conftest import load_golden
-from gpu_util import assert_close
+from gpu_util import assert_close, norm_rel
 
 pytestmark = pytest.mark.gpu
 
@@ -26,6 +26,29 @@ def _build(g, dtype):
     return model, ev
 
 
+def _check_grad(got, want, dtype, what):
+    """float64: 1e-10 elementwise; float32: the flat gradient (66,932 entries,
+    many at rounding level) within 1e-5 norm-relative (north_star's 1e-5 on
+    the vector)."""
+    if dtype == torch.float64:
+        assert_close(got, want, dtype, what)
+    else:
+        e = norm_rel(got, want)
+        assert e <= 1e-5, f"{what}: norm-relative {e:.3e}"
+
+
+def _check_fields(got, want, dtype, what):
+    """Model outputs through the whole chain (trunk, PQC, head): float64
+    elementwise 1e-10; float32 norm-relative 1e-5 (SURVEY 8.C's alternative
+    definition; elementwise errors and their input-rounding floors are in
+    profiles/r02/fp32_error_budget.json)."""
+    if dtype == torch.float64:
+        assert_close(got, want, dtype, what)
+    else:
+        e = norm_rel(got, want)
+        assert e <= 1e-5, f"{what}: norm-relative {e:.3e}"
+
+
 EVALS = ["eval_micro_vacuum.npz", "eval_micro_diel.npz", "eval_micro_asym.npz", "eval_desk.npz",
          "eval_vacuum7.npz", "eval_diel7.npz",
          # 6 qubits: the transfer-matrix PQC kernels (permutation and phase entanglers)
@@ -43,20 +66,17 @@ def test_evaluate_tape_matches_reference(name, dtype):
     res = ev.evaluate(params, weights=w, tape=True)
     bd = res.breakdown
     got = np.array([bd.phys, bd.ic, bd.sym, bd.energy, bd.total])
-    # scalar losses are sums of many squares: FP32 carries ~1e-6 relative
-    s = 1.0 if dtype == torch.float64 else 10.0
-    assert_close(got, g["breakdown"], dtype, "breakdown", s)
-    assert_close(np.array(bd.bin_phys), g["bin_phys"], dtype, "bin_phys", s)
-    assert_close(res.grad, g["grad"], dtype, "flat gradient", 1.0 if dtype == torch.float64 else 3.0)
+    assert_close(got, g["breakdown"], dtype, "breakdown")
+    assert_close(np.array(bd.bin_phys), g["bin_phys"], dtype, "bin_phys")
+    _check_grad(res.grad, g["grad"], dtype, "flat gradient")
     from paper_2506_23246_b200.network import FieldBatch
     x, y, t = ev.grid.flat_points()
     fields, derivs = model.forward(params, x, y, t, derivs=True)
-    assert_close(torch.stack([fields.ez, fields.hx, fields.hy]), g["fields"], dtype, "fields")
-    assert_close(torch.stack([derivs.ez, derivs.hx, derivs.hy]), g["derivs"], dtype, "derivs")
+    _check_fields(torch.stack([fields.ez, fields.hx, fields.hy]), g["fields"], dtype, "fields")
+    _check_fields(torch.stack([derivs.ez, derivs.hx, derivs.hy]), g["derivs"], dtype, "derivs")
     # independent cross-check: torch-autograd trunk + K1/K2/K4 autograd functions
     ref = ev.evaluate(params, weights=w, tape=True, native=False)
-    assert_close(ref.grad, g["grad"], dtype, "autograd-path gradient",
-                 1.0 if dtype == torch.float64 else 3.0)
+    _check_grad(ref.grad, g["grad"], dtype, "autograd-path gradient")
     plain = ev.evaluate(params, weights=w, tape=False)
     assert abs(plain.breakdown.total - float(g["plain_total"])) <= (1e-10 if dtype == torch.float64 else 1e-4) * abs(float(g["plain_total"]))
 
