@@ -781,9 +781,24 @@ int bwd_n(const qpinn_circuit* c, const KArgs<float>* a, unsigned char* ws, cons
   static const bool serial = getenv("QPINN_SERIAL_BWD") != nullptr;  // A/B switch
   if (Phi && !serial)
     if (int rc = side_stream(st, &side)) return rc;
+  // once forked, every return path (errors included) joins the side stream back
+  // into `st`, so a graph capture never ends with an unjoined fork and an eager
+  // caller never gets control back while side work still writes g_qp
+  struct Join {
+    SideStream* side = nullptr;
+    cudaStream_t st = nullptr;
+    ~Join() {
+      if (side) {
+        cudaEventRecord(side->join, side->s);
+        cudaStreamWaitEvent(st, side->join, 0);
+      }
+    }
+  } join;
   if (side) {
     QPINN_CUDA_CHECK(cudaEventRecord(side->fork, st));
     QPINN_CUDA_CHECK(cudaStreamWaitEvent(side->s, side->fork, 0));
+    join.side = side;
+    join.st = st;
   }
   // dL/dm = Abar W'^T  (D per row)
   if (int rc = tc::gemm3(4 * a->R, D, D2, Abar, D2, cc.W, D2, G, D, ws + t.g3,
@@ -793,11 +808,7 @@ int bwd_n(const qpinn_circuit* c, const KArgs<float>* a, unsigned char* ws, cons
     if (int rc = weight_chain(side->s)) return rc;
   tr_embed_grad<NQ><<<gp, 256, 0, st>>>(a->scale, a->R, a->act, a->tan, G, a->g_act, a->g_tan);
   QPINN_CUDA_CHECK(cudaGetLastError());
-  if (side) {  // join
-    QPINN_CUDA_CHECK(cudaEventRecord(side->join, side->s));
-    QPINN_CUDA_CHECK(cudaStreamWaitEvent(st, side->join, 0));
-    return QPINN_OK;
-  }
+  if (side) return QPINN_OK;  // joined by `join`
   // replay path: re-embed m into G once the embedding gradient has read it
   tr_embed<NQ><<<gp, 256, 0, st>>>(a->scale, a->R, a->act, a->tan, G, nullptr);
   Phi = G;

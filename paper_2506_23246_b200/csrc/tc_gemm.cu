@@ -20,6 +20,7 @@
 // B (the layer weights, small) is split once per call into a workspace.
 #include <cudaTypedefs.h>
 
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 
@@ -481,6 +482,277 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUt
 #endif
 }
 
+
+// ---- CTA-pair variant (cta_group::2) ------------------------------------------------
+// Same roles and numerics as gemm3_kernel, on a cluster of two CTAs (one TPC):
+// each pair tile is 256 rows x BN columns, CTA r owning rows 128 r.. (A operand
+// and accumulator in its own TMEM).  The leader (r = 0) issues
+// tcgen05.mma.cta_group::2; B's BN rows are split in halves between the CTAs'
+// shared memory (scripts/probes/mma_2cta.cu), so every SM stores and feeds the
+// tensor core only half of B per MMA.  B (the layer weights, split hi/lo) stays
+// RESIDENT in shared memory for the whole kernel: a pair walks M-tiles of one
+// fixed N-tile, so no B traffic per k-block at all.  Together this halves the
+// shared-memory bandwidth the single-CTA kernel needs per k-block (~157 B/cycle
+// at the MMA rate by a per-cycle budget, against 128 B/cycle per SM).  Measured:
+// slower than the single-CTA kernel (see use_pair), so it is opt-in.
+// Cross-CTA signalling: the split and epilogue warps of CTA 1 arrive on the
+// leader's conv / tempty barriers remotely; the leader's commits multicast to
+// both CTAs' op_empty / tfull.
+template <int BN>
+struct PairCfg {
+  static constexpr int HB = BN / 2;                 // B rows held per CTA
+  static constexpr int kSlab = HB * kBK * 4;        // one k-block of B_hi (or B_lo) half
+  static constexpr int RS = 3, OS = 2, NB = 3;
+  static constexpr int kACol = NB * BN;
+  static_assert(NB * BN + OS * 2 * kBK <= 512, "TMEM columns");
+  static constexpr int kSbuf = 32 * BN * 4;
+  static constexpr int kStg = 8 * 2 * 2048;
+  static size_t smem(int nk) {
+    return (size_t)RS * kABytes + 2 * (size_t)nk * kSlab + kSbuf + kStg + 1024 + 512;
+  }
+};
+
+template <int BN, int EPI>
+__global__ void __launch_bounds__(kThreadsGemm, 1)
+gemm3_pair_kernel(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUtensorMap mBhi,
+                  const __grid_constant__ CUtensorMap mBlo, const __grid_constant__ CUtensorMap mC,
+                  const GemmArgs g) {
+  using Cfg = PairCfg<BN>;
+  constexpr int RS = Cfg::RS, OS = Cfg::OS, NB = Cfg::NB, HB = Cfg::HB;
+  extern __shared__ unsigned char smem_raw[];
+  unsigned char* smem = (unsigned char*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  const int nk = (g.K + kBK - 1) / kBK;
+  unsigned char* raw = smem;                                  // [RS][16 KB] fp32 A tiles
+  unsigned char* bres = raw + RS * kABytes;                   // [hi: nk slabs][lo: nk slabs]
+  float* sbuf = (float*)(bres + 2 * (size_t)nk * Cfg::kSlab);
+  unsigned char* stg = (unsigned char*)sbuf + Cfg::kSbuf;
+  uint64_t* raw_full = (uint64_t*)(stg + Cfg::kStg);
+  uint64_t* raw_empty = raw_full + RS;
+  uint64_t* b_full = raw_empty + RS;
+  uint64_t* conv = b_full + 1;
+  uint64_t* op_empty = conv + OS;
+  uint64_t* tfull = op_empty + OS;
+  uint64_t* tempty = tfull + NB;
+  uint32_t* tmem_slot = (uint32_t*)(tempty + NB);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_rank();
+  const int64_t pair = blockIdx.x >> 1, n_pairs = gridDim.x >> 1;
+  const int64_t n_mt = EPI == EPI_TANH ? (g.R + 63) / 64 : (g.M + 255) / 256;
+  const int n_nt = (g.N + BN - 1) / BN;
+  const int64_t G = n_pairs / n_nt;                // pairs per N-tile
+  const bool active = pair < G * n_nt;
+  const int nt = (int)(pair % n_nt);
+  const int64_t mt0 = active ? pair / n_nt : n_mt, mstep = G > 0 ? G : 1;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < RS; ++s) {
+      mbar_init(raw_full + s, 1);
+      mbar_init(raw_empty + s, 4);
+    }
+    mbar_init(b_full, 1);
+    for (int s = 0; s < OS; ++s) {
+      mbar_init(conv + s, 8);      // 4 split warps x 2 CTAs (leader's barrier)
+      mbar_init(op_empty + s, 1);  // multicast commit
+    }
+    for (int b = 0; b < NB; ++b) {
+      mbar_init(tfull + b, 1);     // multicast commit
+      mbar_init(tempty + b, 16);   // 8 epilogue warps x 2 CTAs (leader's barrier)
+    }
+    mbar_init_fence();
+  }
+  if (warp == 12 && lane == 0) {
+    tma_prefetch(&mA);
+    tma_prefetch(&mBhi);
+    tma_prefetch(&mBlo);
+  }
+  if (warp == 13) tmem_alloc2(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  // this CTA's half of the split B, resident for the whole kernel
+  if (warp == 12 && lane == 1 && active) {
+    mbar_expect_tx(b_full, 2u * nk * Cfg::kSlab);
+    for (int kb = 0; kb < nk; ++kb) {
+      tma_load_2d(bres + (size_t)kb * Cfg::kSlab, &mBhi, b_full, kb * kBK, nt * BN + rank * HB);
+      tma_load_2d(bres + (size_t)(nk + kb) * Cfg::kSlab, &mBlo, b_full, kb * kBK,
+                  nt * BN + rank * HB);
+    }
+  }
+  if (active) mbar_wait(b_full, 0);
+  cluster_sync();  // the leader's MMAs read both halves from here on
+
+  if (warp == 12) {  // ---- TMA producer for A (this CTA's 128 rows of the pair tile)
+    if (lane == 0) {
+      int64_t j = 0;
+      for (int64_t mt = mt0; mt < n_mt; mt += mstep) {
+        for (int kb = 0; kb < nk; ++kb, ++j) {
+          const int r = (int)(j % RS);
+          if (j >= RS) mbar_wait(raw_empty + r, (uint32_t)(((j / RS) - 1) & 1));
+          unsigned char* st = raw + r * kABytes;
+          mbar_expect_tx(raw_full + r, kABytes);
+          if constexpr (EPI == EPI_TANH) {
+#pragma unroll
+            for (int c = 0; c < 4; ++c)
+              tma_load_2d(st + c * (kABytes / 4), &mA, raw_full + r, kb * kBK,
+                          (int)(c * g.R + mt * 64 + rank * 32));
+          } else {
+            tma_load_2d(st, &mA, raw_full + r, kb * kBK, (int)(mt * 256 + rank * 128));
+          }
+        }
+      }
+    }
+  } else if (warp == 13) {  // ---- MMA issuer (leader CTA only)
+    if (lane == 0 && rank == 0) {
+      constexpr uint32_t idesc = idesc_tf32(256, BN);
+      const uint32_t b_hi0 = smem_u32(bres), b_lo0 = b_hi0 + nk * Cfg::kSlab;
+      int64_t j = 0, grp = 0;
+      for (int64_t mt = mt0; mt < n_mt; mt += mstep) {
+        for (int kb = 0; kb < nk; ++kb, ++j) {
+          const int o = (int)(j % OS), b = (int)(grp % NB);
+          const bool first = kb % kPromote == 0;
+          const bool last = kb % kPromote == kPromote - 1 || kb == nk - 1;
+          if (first && grp >= NB) mbar_wait(tempty + b, (uint32_t)(((grp / NB) - 1) & 1));
+          mbar_wait(conv + o, (uint32_t)((j / OS) & 1));
+          tc_fence_after();
+          const uint32_t b_hi = b_hi0 + kb * Cfg::kSlab, b_lo = b_lo0 + kb * Cfg::kSlab;
+          const uint32_t d = tmem + b * BN;
+          const uint32_t a_hi = tmem + Cfg::kACol + o * 2 * kBK, a_lo = a_hi + kBK;
+#pragma unroll
+          for (int k = 0; k < kBK / 8; ++k) {
+            const uint32_t off = k * 32;
+            mma2_tf32_ts(d, a_lo + k * 8, desc_k_sw128(b_hi + off), idesc, !(first && k == 0));
+            mma2_tf32_ts(d, a_hi + k * 8, desc_k_sw128(b_lo + off), idesc, 1);
+            mma2_tf32_ts(d, a_hi + k * 8, desc_k_sw128(b_hi + off), idesc, 1);
+          }
+          mma_commit2(op_empty + o);
+          if (last) {
+            mma_commit2(tfull + b);
+            ++grp;
+          }
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp < 4) {  // ---- split A into this CTA's TMEM, signal the leader
+    const int row = warp * 32 + lane;
+    const uint32_t lane_base = (uint32_t)(warp * 32) << 16;
+    int64_t j = 0;
+    for (int64_t mt = mt0; mt < n_mt; mt += mstep) {
+      for (int kb = 0; kb < nk; ++kb, ++j) {
+        const int r = (int)(j % RS), o = (int)(j % OS);
+        if (j >= OS) {
+          mbar_wait(op_empty + o, (uint32_t)(((j / OS) - 1) & 1));
+          tc_fence_after();
+        }
+        mbar_wait(raw_full + r, (uint32_t)((j / RS) & 1));
+        const uint32_t src = smem_u32(raw + r * kABytes) + row * 128;
+        float4 v[8];
+#pragma unroll
+        for (int c = 0; c < 8; ++c) v[c] = lds128(src + ((c ^ (row & 7)) << 4));
+        float hi[32], lo[32];
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          split_tf32(v[c].x, hi[4 * c], lo[4 * c]);
+          split_tf32(v[c].y, hi[4 * c + 1], lo[4 * c + 1]);
+          split_tf32(v[c].z, hi[4 * c + 2], lo[4 * c + 2]);
+          split_tf32(v[c].w, hi[4 * c + 3], lo[4 * c + 3]);
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(raw_empty + r);
+        const uint32_t a = tmem + lane_base + Cfg::kACol + o * 2 * kBK;
+        tmem_st32(a, hi);
+        tmem_st32(a + kBK, lo);
+        tmem_st_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cluster(conv + o, 0);
+      }
+    }
+  } else {  // ---- warps 4-11: promote partials, epilogue (this CTA's rows)
+    const int q = warp & 3, h = (warp - 4) >> 2;
+    constexpr int CW = BN / 2;
+    const uint32_t lane_base = (uint32_t)(q * 32) << 16;
+    unsigned char* my_stg = stg + (warp - 4) * 2 * 2048;
+    uint32_t sidx = 0;
+    int64_t j = 0;
+    const int n0 = nt * BN, c_off = h * CW;
+    for (int64_t mt = mt0; mt < n_mt; mt += mstep) {
+      float acc[CW];
+#pragma unroll
+      for (int c = 0; c < CW; ++c) acc[c] = 0.f;
+      const int ngrp = (nk + kPromote - 1) / kPromote;
+      for (int gi = 0; gi < ngrp; ++gi, ++j) {
+        const int b = (int)(j % NB);
+        mbar_wait(tfull + b, (uint32_t)((j / NB) & 1));
+        tc_fence_after();
+#pragma unroll
+        for (int c0 = 0; c0 < CW; c0 += 32) {
+          float v[32];
+          tmem_ld32(tmem + lane_base + b * BN + c_off + c0, v);
+#pragma unroll
+          for (int i = 0; i < 32; ++i) acc[c0 + i] += v[i];
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cluster(tempty + b, 0);
+      }
+      if constexpr (EPI == EPI_STORE || EPI == EPI_TANH1) {
+        if constexpr (EPI == EPI_TANH1) {
+#pragma unroll
+          for (int c = 0; c < CW; ++c) {
+            const int col = n0 + c_off + c;
+            acc[c] = tanhf(acc[c] + (col < g.N ? __ldg(g.bias + col) : 0.f));
+          }
+        }
+        const int64_t row0 = mt * 256 + rank * 128 + q * 32;
+        if (g.tma_store) {
+          store_rows_tma<CW>(acc, my_stg, &mC, n0 + c_off, (int)row0, 0, lane, sidx);
+        } else if (row0 + lane < g.M) {
+          float* dst = g.C + (row0 + lane) * g.ldc + n0 + c_off;
+#pragma unroll
+          for (int c = 0; c < CW; ++c)
+            if (n0 + c_off + c < g.N) dst[c] = acc[c];
+        }
+      } else {  // EPI_TANH: q = channel, lane = point
+        const int64_t p0 = mt * 64 + rank * 32;
+        if (q == 0) {
+#pragma unroll
+          for (int c = 0; c < CW; ++c) sbuf[(c_off + c) * 32 + lane] = acc[c];
+        }
+        asm volatile("bar.sync 1, 256;" ::: "memory");
+        const int e = warp - 4;
+#pragma unroll 4
+        for (int c = e * (BN / 8); c < (e + 1) * (BN / 8); ++c) {
+          const float bv = n0 + c < g.N ? __ldg(g.bias + n0 + c) : 0.f;
+          sbuf[c * 32 + lane] = tanhf(sbuf[c * 32 + lane] + bv);
+        }
+        asm volatile("bar.sync 1, 256;" ::: "memory");
+#pragma unroll
+        for (int c = 0; c < CW; ++c) {
+          const float y = sbuf[(c_off + c) * 32 + lane];
+          acc[c] = q == 0 ? y : (1.f - y * y) * acc[c];
+        }
+        if (g.tma_store) {
+          store_rows_tma<CW>(acc, my_stg, &mC, n0 + c_off, (int)p0, q, lane, sidx);
+        } else if (p0 + lane < g.R) {
+          float* dst = g.C + ((int64_t)q * g.R + p0 + lane) * g.ldc + n0 + c_off;
+#pragma unroll
+          for (int c = 0; c < CW; ++c)
+            if (n0 + c_off + c < g.N) dst[c] = acc[c];
+        }
+        asm volatile("bar.sync 1, 256;" ::: "memory");
+      }
+    }
+  }
+  if (warp >= 4 && warp < 12 && lane == 0) bulk_wait_all();
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();  // no CTA leaves while its pair may still signal it
+  if (warp == 13) tmem_dealloc2(tmem, 512);
+}
+
 // ---- weight gradient: dW[Kin, Nout] = X[rows, Kin]^T G[rows, Nout] ----------------------
 // Both operands are activations stored row-major, i.e. MN-major for the MMA
 // (the reduction runs over rows).  Work items are (128-row block of dW,
@@ -827,10 +1099,77 @@ static int launch_gemm3(const GemmArgs& g0, const float* A, int64_t lda, const f
   return QPINN_OK;
 }
 
+template <int BN, int EPI>
+static int launch_gemm3_pair(const GemmArgs& g0, const float* A, int64_t lda, const float* Bhi,
+                             const float* Blo, int ldk, cudaStream_t st) {
+  using Cfg = PairCfg<BN>;
+  GemmArgs g = g0;
+  CUtensorMap mA, mBh, mBl, mC;
+  g.tma_store = ((uintptr_t)g.C & 15) == 0 && (g.ldc & 3) == 0;
+  if (g.tma_store) {
+    const uint64_t rows = EPI == EPI_TANH ? (uint64_t)g.R : (uint64_t)g.M;
+    if (int rc = make_out_map(&mC, g.C, (uint64_t)g.N, rows, EPI == EPI_TANH ? 4 : 1,
+                              (uint64_t)g.ldc))
+      return rc;
+  } else {
+    memset(&mC, 0, sizeof(mC));
+  }
+  const uint32_t a_box = EPI == EPI_TANH ? 32 : kBM;
+  if (int rc = make_map(&mA, A, (uint64_t)g.M, (uint64_t)g.K, (uint64_t)lda, a_box)) return rc;
+  if (int rc = make_map(&mBh, Bhi, (uint64_t)g.N, (uint64_t)ldk, (uint64_t)ldk, Cfg::HB)) return rc;
+  if (int rc = make_map(&mBl, Blo, (uint64_t)g.N, (uint64_t)ldk, (uint64_t)ldk, Cfg::HB)) return rc;
+  const int nk = (g.K + kBK - 1) / kBK;
+  const size_t smem = Cfg::smem(nk);
+  auto kern = gemm3_pair_kernel<BN, EPI>;
+  QPINN_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  const int64_t n_mt = EPI == EPI_TANH ? (g.R + 63) / 64 : (g.M + 255) / 256;
+  const int n_nt = (g.N + BN - 1) / BN;
+  int64_t pairs = num_sms() / 2;
+  if (pairs > n_mt * n_nt) pairs = n_mt * n_nt;
+  pairs = pairs / n_nt * n_nt;  // every pair serves one N-tile (B resident)
+  if (pairs < n_nt) pairs = n_nt;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(2 * pairs));
+  cfg.blockDim = dim3(kThreadsGemm);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  QPINN_CUDA_CHECK(cudaLaunchKernelEx(&cfg, kern, mA, mBh, mBl, mC, g));
+  return QPINN_OK;
+}
+
+// CTA-pair kernel (QPINN_GEMM_PAIR=1) when this CTA's half of the split B fits in
+// shared memory next to the A pipeline (K <= 256 at BN = 128).  Correct (same
+// errors as the single-CTA kernel, scripts/gemm_check.py) but measured SLOWER:
+// 150 vs 105 us at 262144 x 128 x 256 -- the kernel is bound by the per-k-block
+// handshake chain (TMA -> split -> MMA commit -> op_empty with 2 TMEM A stages),
+// not by shared-memory bandwidth or the MMA rate, and the pair adds cross-SM
+// signalling latency to that chain.  Off by default.
+static bool use_pair(int BN, int K) {
+  static const int env = [] {
+    const char* e = getenv("QPINN_GEMM_PAIR");
+    return e ? atoi(e) : 0;
+  }();
+  if (!env) return false;
+  const int nk = (K + kBK - 1) / kBK;
+  const size_t need = BN == 64 ? PairCfg<64>::smem(nk) : PairCfg<128>::smem(nk);
+  return need <= 232448;
+}
+
 template <int EPI>
 static int dispatch(const GemmArgs& g, const float* A, int64_t lda, const float* hi,
                     const float* lo, int ldk, cudaStream_t st) {
-  if (g.N <= 64) return launch_gemm3<64, EPI>(g, A, lda, hi, lo, ldk, st);
+  if (g.N <= 64) {
+    if (use_pair(64, g.K)) return launch_gemm3_pair<64, EPI>(g, A, lda, hi, lo, ldk, st);
+    return launch_gemm3<64, EPI>(g, A, lda, hi, lo, ldk, st);
+  }
+  if (use_pair(128, g.K)) return launch_gemm3_pair<128, EPI>(g, A, lda, hi, lo, ldk, st);
   return launch_gemm3<128, EPI>(g, A, lda, hi, lo, ldk, st);
 }
 

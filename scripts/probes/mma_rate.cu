@@ -62,6 +62,16 @@ __global__ void __launch_bounds__(384, 1) mma_rate(int iters, int chain, unsigne
           acc += v[r];
         }
       }
+    } else if (LOAD == 3) {  // 8 warps stream 16-byte shared loads (the split / epilogue traffic)
+      const uint32_t base = smem_u32(smem) + 40960 + ((threadIdx.x * 16) & 16383);
+      float4 x = make_float4(0, 0, 0, 0);
+      while (!done) {
+        for (int r = 0; r < 16; ++r) {
+          const float4 y = lds128(base + ((r * 4096) & 16383));
+          x.x += y.x;
+        }
+      }
+      if (x.x == 12345.f) out[0] = 1;
     } else if (warp < 8) {
       while (!done) {
         for (int r = 0; r < 8; ++r) tmem_st32(tmem + lane_base + 384 + (r & 3) * 32, v);
@@ -139,6 +149,11 @@ void run(const char* name, int chain, int iters) {
 }
 
 int main() {
+  for (int chain : {48}) {
+    run<128, 0, 3>("ts N128 + 8 warps lds.128", chain, 4000);
+    run<128, 1, 3>("ss N128 + 8 warps lds.128", chain, 4000);
+    run<256, 0, 3>("ts N256 + 8 warps lds.128", chain, 2000);
+  }
   for (int chain : {12, 48}) {
     run<128, 0, 1>("ts N128 + 8 warps tmem.ld", chain, 4000);
     run<128, 0, 2>("ts N128 + 4 warps tmem.st", chain, 4000);
