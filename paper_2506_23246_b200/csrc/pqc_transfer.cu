@@ -692,6 +692,15 @@ int side_stream(cudaStream_t st, SideStream** out) {
   return QPINN_OK;
 }
 
+// QPINN_TR_FUSED_READOUT=0: the separate tr_readout pass (A/B experiments)
+bool fused_readout_off() {
+  static const bool off = [] {
+    const char* e = getenv("QPINN_TR_FUSED_READOUT");
+    return e && atoi(e) == 0;
+  }();
+  return off;
+}
+
 TrCircuit ws_circuit(unsigned char* ws, const TrLayout& t) {
   return {(cplx<float>*)(ws + t.U), (cplx<float>*)(ws + t.ph), (cplx<float>*)(ws + t.CK),
           (float*)(ws + t.W), (float*)(ws + t.Wt)};
@@ -717,6 +726,10 @@ int fwd_n(const qpinn_circuit* c, const KArgs<float>* a, unsigned char* ws, cons
   const int ns = a->tan ? 4 : 1;
   tr_embed<NQ><<<grid_points(a->R), 256, 0, st>>>(a->scale, a->R, a->act, a->tan, Phi, a->maxabs);
   QPINN_CUDA_CHECK(cudaGetLastError());
+  if (NQ == 7 && ns == 4 && !fused_readout_off()) {  // map + readout in one tensor-core pass
+    return tc::gemm3_readout(a->R, Phi, cc.Wt, Psi, a->z, a->dz, ws + t.g3,
+                             tc::gemm3_workspace_bytes(D2, D2), st);
+  }
   if (int rc = tc::gemm3(ns * a->R, D2, D, Phi, D, cc.Wt, D, Psi, D2, ws + t.g3,
                          tc::gemm3_workspace_bytes(D2, D2), st))
     return rc;

@@ -74,7 +74,15 @@ constexpr int kPromote = QPINN_GEMM_PROMOTE;
 constexpr int kABytes = kBM * kBK * 4;  // 16 KB fp32 tile
 constexpr int kThreadsGemm = 448;  // 4 split + 8 epilogue + producer + MMA warps
 constexpr int kThreadsW = 320;      // weight gradient: 4 split + 4 epilogue + producer + MMA
-enum { EPI_STORE = 0, EPI_TANH = 1, EPI_TANH1 = 2 };  // TANH1: value channel only
+enum { EPI_STORE = 0, EPI_TANH = 1, EPI_TANH1 = 2, EPI_READOUT = 3 };  // TANH1: value channel only
+// EPI_READOUT: the transfer-matrix map of the PQC (pqc_transfer.cu): rows are the
+// embedded magnitudes of 32 points x [state; d/dx; d/dy; d/dt] (as EPI_TANH), the
+// N = 2D output columns are [Re psi | Im psi]; besides storing Psi the epilogue
+// reduces the Pauli-Z readout z_q = sum_b s_bq |psi_b|^2, dz_kq = sum_b s_bq
+// 2 Re(conj psi_b dpsi_kb) (qsim.py:369-381), which is separable over the Re and
+// Im halves, so a CTA runs both N-tiles of its M-tile back to back and adds them
+template <int EPI>
+constexpr bool kRowsByPoint = EPI == EPI_TANH || EPI == EPI_READOUT;
 
 template <int BN>
 struct GemmCfg {
@@ -108,8 +116,9 @@ struct GemmCfg {
   static_assert(!kATmem || kNB * BN + kOps * 2 * kBK <= 512, "TMEM columns");
   static constexpr int kSbuf = 32 * BN * 4;
   static constexpr int kStg = 8 * 2 * 2048;  // per epilogue warp: 2 x (16 rows x 32 cols)
+  static constexpr int kRed = 4 * 32 * 8 * 4;  // EPI_READOUT: column-half partials
   static constexpr int kSmem =
-      kRaw * kABytes + kOps * kOpBytes + kBS * kBStage + kSbuf + kStg + 1024 + 512;
+      kRaw * kABytes + kOps * kOpBytes + kBS * kBStage + kSbuf + kStg + kRed + 1024 + 512;
 };
 
 struct GemmArgs {
@@ -120,6 +129,8 @@ struct GemmArgs {
   int64_t ldc;
   const float* bias;  // EPI_TANH
   int tma_store;      // C goes out through TMA (16-byte aligned rows), else direct stores
+  float* z;           // EPI_READOUT: z [R, NQ], dz [3, R, NQ]
+  float* dz;
 };
 
 // one epilogue warp's 32 rows x CW columns (lane = row) -> global through two
@@ -170,7 +181,8 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUt
   unsigned char* bst = ops + OS * Cfg::kOpBytes;    // [BS][B_hi | B_lo]
   float* sbuf = (float*)(bst + BS * Cfg::kBStage);
   unsigned char* stg = (unsigned char*)sbuf + Cfg::kSbuf;  // [4 warps][2][4 KB]
-  uint64_t* raw_full = (uint64_t*)(stg + Cfg::kStg);
+  float* red = (float*)(stg + Cfg::kStg);                    // [4][32][8]
+  uint64_t* raw_full = (uint64_t*)(stg + Cfg::kStg + Cfg::kRed);
   uint64_t* raw_empty = raw_full + RS;
   uint64_t* b_full = raw_empty + RS;
   uint64_t* b_empty = b_full + BS;
@@ -184,9 +196,9 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUt
   const long long prof_t0 = clock64();
 #endif
   const int nk = (g.K + kBK - 1) / kBK;
-  const int64_t n_mt = EPI == EPI_TANH ? (g.R + 31) / 32 : (g.M + kBM - 1) / kBM;
+  const int64_t n_mt = kRowsByPoint<EPI> ? (g.R + 31) / 32 : (g.M + kBM - 1) / kBM;
   const int n_nt = (g.N + BN - 1) / BN;
-  const int64_t n_tiles = n_mt * n_nt;
+  // tiles: a CTA walks M-tiles and runs all N-tiles of each back to back
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < RS; ++s) {
@@ -221,14 +233,14 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUt
   if (warp == 12) {  // ---- TMA producer for A (runs RS k-blocks ahead)
     if (lane == 0) {
       int64_t j = 0;
-      for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
-        const int64_t mt = t / n_nt;
+      for (int64_t mt = blockIdx.x; mt < n_mt; mt += gridDim.x)
+      for (int nt = 0; nt < n_nt; ++nt) {
         for (int kb = 0; kb < nk; ++kb, ++j) {
           const int r = (int)(j % RS);
           if (j >= RS) GPROF(0, mbar_wait(raw_empty + r, (uint32_t)(((j / RS) - 1) & 1)));
           unsigned char* st = raw + r * kABytes;
           mbar_expect_tx(raw_full + r, kABytes);
-          if constexpr (EPI == EPI_TANH) {
+          if constexpr (kRowsByPoint<EPI>) {
 #pragma unroll
             for (int c = 0; c < 4; ++c)
               tma_load_2d(st + c * (kABytes / 4), &mA, raw_full + r, kb * kBK,
@@ -243,8 +255,8 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUt
   if (warp == 12) {  // ---- TMA producer for the split B tiles (L2-resident), lane 1
     if (lane == 1) {
       int64_t j = 0;
-      for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
-        const int nt = (int)(t % n_nt);
+      for (int64_t mt = blockIdx.x; mt < n_mt; mt += gridDim.x)
+      for (int nt = 0; nt < n_nt; ++nt) {
         for (int kb = 0; kb < nk; ++kb, ++j) {
           const int e = (int)(j % BS);
           if (j >= BS) GPROF(1, mbar_wait(b_empty + e, (uint32_t)(((j / BS) - 1) & 1)));
@@ -263,7 +275,8 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUt
     if (lane == 0) {
       constexpr uint32_t idesc = idesc_tf32(kBM, BN);
       int64_t j = 0, grp = 0;
-      for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+      for (int64_t mt = blockIdx.x; mt < n_mt; mt += gridDim.x)
+      for (int nt = 0; nt < n_nt; ++nt) {
         for (int kb = 0; kb < nk; ++kb, ++j) {
           const int o = (int)(j % OS), e = (int)(j % BS), b = (int)(grp % NB);
           const bool first = kb % kPromote == 0;
@@ -312,7 +325,8 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUt
     const int row = warp * 32 + lane;
     const uint32_t lane_base = (uint32_t)(warp * 32) << 16;
     int64_t j = 0;
-    for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+    for (int64_t mt = blockIdx.x; mt < n_mt; mt += gridDim.x)
+      for (int nt = 0; nt < n_nt; ++nt) {
       for (int kb = 0; kb < nk; ++kb, ++j) {
         const int r = (int)(j % RS), o = (int)(j % OS);
         if (j >= OS) {
@@ -352,7 +366,8 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUt
     }
   } else if (warp < 4) {  // ---- split A into an operand buffer
     int64_t j = 0;
-    for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+    for (int64_t mt = blockIdx.x; mt < n_mt; mt += gridDim.x)
+      for (int nt = 0; nt < n_nt; ++nt) {
       for (int kb = 0; kb < nk; ++kb, ++j) {
         const int r = (int)(j % RS), o = (int)(j % OS);
         if (j >= OS) mbar_wait(op_empty + o, (uint32_t)(((j / OS) - 1) & 1));
@@ -392,9 +407,10 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUt
     unsigned char* my_stg = stg + (warp - 4) * 2 * 2048;
     uint32_t sidx = 0;
     int64_t j = 0;
-    for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
-      const int64_t mt = t / n_nt;
-      const int n0 = (int)(t % n_nt) * BN, c_off = h * CW;
+    float zr[8];  // EPI_READOUT: readout partials of this row over the N-tiles
+    for (int64_t mt = blockIdx.x; mt < n_mt; mt += gridDim.x)
+      for (int nt = 0; nt < n_nt; ++nt) {
+      const int n0 = nt * BN, c_off = h * CW;
       float acc[CW];
 #pragma unroll
       for (int c = 0; c < CW; ++c) acc[c] = 0.f;
@@ -440,6 +456,47 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUt
           for (int c = 0; c < CW; ++c)
             if (n0 + c_off + c < g.N) dst[c] = acc[c];
         }
+      } else if constexpr (EPI == EPI_READOUT) {  // q = channel, lane = point, b = c_off + c
+        static_assert(BN == 128, "readout epilogue: one N-tile = the Re or Im half (D = 128)");
+        const int64_t p = mt * 32 + lane;
+        if (g.tma_store) store_rows_tma<CW>(acc, my_stg, &mC, n0 + c_off, (int)(mt * 32), q, lane, sidx);
+        if (q == 0) {
+#pragma unroll
+          for (int c = 0; c < CW; ++c) sbuf[(c_off + c) * 32 + lane] = acc[c];
+        }
+        asm volatile("bar.sync 1, 256;" ::: "memory");
+        // v_b = psi_b^2 (state row) or 2 psi_b dpsi_kb (tangent row k); wire w of the
+        // 7 qubits is bit 6 - w of b: bit 6 is this warp's column half h, bits 0-5 of c
+        float part[7];
+#pragma unroll
+        for (int w = 0; w < 7; ++w) part[w] = 0.f;
+#pragma unroll
+        for (int c = 0; c < CW; ++c) {
+          const float ps = sbuf[(c_off + c) * 32 + lane];
+          const float v = q == 0 ? acc[c] * acc[c] : 2.f * ps * acc[c];
+          part[0] += v;
+#pragma unroll
+          for (int w = 1; w < 7; ++w) part[w] += ((c >> (6 - w)) & 1) ? -v : v;
+        }
+        if (h) part[0] = -part[0];
+        if (h == 1) {
+#pragma unroll
+          for (int w = 0; w < 7; ++w) red[(q * 32 + lane) * 8 + w] = part[w];
+        }
+        asm volatile("bar.sync 1, 256;" ::: "memory");
+        if (h == 0) {
+#pragma unroll
+          for (int w = 0; w < 7; ++w) {
+            const float t = part[w] + red[(q * 32 + lane) * 8 + w];
+            zr[w] = nt == 0 ? t : zr[w] + t;
+          }
+          if (nt == n_nt - 1 && p < g.R) {
+            float* dst = q == 0 ? g.z + p * 7 : g.dz + ((int64_t)(q - 1) * g.R + p) * 7;
+#pragma unroll
+            for (int w = 0; w < 7; ++w) dst[w] = zr[w];
+          }
+        }
+        asm volatile("bar.sync 1, 256;" ::: "memory");  // sbuf / red reused by the next tile
       } else {  // EPI_TANH: q = channel, lane = point
         // the value channel's pre-activations go through shared memory so that
         // all eight warps share the tanh work (BN / 8 columns each)
@@ -1076,24 +1133,25 @@ static int launch_gemm3(const GemmArgs& g0, const float* A, int64_t lda, const f
   GemmArgs g = g0;
   CUtensorMap mA, mBh, mBl, mC;
   g.tma_store = ((uintptr_t)g.C & 15) == 0 && (g.ldc & 3) == 0;
+  if (EPI == EPI_READOUT && !g.tma_store)
+    return fail(QPINN_ERR_CONFIG, "gemm3 readout: Psi needs 16-byte aligned rows");
   if (g.tma_store) {
-    const uint64_t rows = EPI == EPI_TANH ? (uint64_t)g.R : (uint64_t)g.M;
-    if (int rc = make_out_map(&mC, g.C, (uint64_t)g.N, rows, EPI == EPI_TANH ? 4 : 1,
+    const uint64_t rows = kRowsByPoint<EPI> ? (uint64_t)g.R : (uint64_t)g.M;
+    if (int rc = make_out_map(&mC, g.C, (uint64_t)g.N, rows, kRowsByPoint<EPI> ? 4 : 1,
                               (uint64_t)g.ldc))
       return rc;
   } else {
     memset(&mC, 0, sizeof(mC));
   }
-  const uint32_t a_box = EPI == EPI_TANH ? 32 : kBM;
+  const uint32_t a_box = kRowsByPoint<EPI> ? 32 : kBM;
   if (int rc = make_map(&mA, A, (uint64_t)g.M, (uint64_t)g.K, (uint64_t)lda, a_box)) return rc;
   if (int rc = make_map(&mBh, Bhi, (uint64_t)g.N, (uint64_t)ldk, (uint64_t)ldk, BN)) return rc;
   if (int rc = make_map(&mBl, Blo, (uint64_t)g.N, (uint64_t)ldk, (uint64_t)ldk, BN)) return rc;
   auto kern = gemm3_kernel<BN, EPI>;
   QPINN_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         GemmCfg<BN>::kSmem));
-  const int64_t n_mt = EPI == EPI_TANH ? (g.R + 31) / 32 : (g.M + kBM - 1) / kBM;
-  const int64_t tiles = n_mt * ((g.N + BN - 1) / BN);
-  const int grid = (int)(tiles < num_sms() ? tiles : num_sms());
+  const int64_t n_mt = kRowsByPoint<EPI> ? (g.R + 31) / 32 : (g.M + kBM - 1) / kBM;
+  const int grid = (int)(n_mt < num_sms() ? n_mt : num_sms());
   kern<<<grid, kThreadsGemm, GemmCfg<BN>::kSmem, st>>>(mA, mBh, mBl, mC, g);
   QPINN_CUDA_CHECK(cudaGetLastError());
   return QPINN_OK;
@@ -1183,8 +1241,24 @@ int gemm3(int64_t M, int N, int K, const float* A, int64_t lda, const float* B, 
   float* lo = hi + (size_t)N * ldk;
   split_rows<<<64, 256, 0, st>>>(B, N, K, ldb, ldk, hi, lo);
   QPINN_CUDA_CHECK(cudaGetLastError());
-  GemmArgs g{M, 0, N, K, C, ldc, nullptr, 0};
+  GemmArgs g{M, 0, N, K, C, ldc, nullptr, 0, nullptr, nullptr};
   return dispatch<EPI_STORE>(g, A, lda, hi, lo, ldk, st);
+}
+
+// Psi [4R, 256] = Phi [4R, 128] Wt^T (Wt [256, 128]) with the fused Pauli-Z readout:
+// z [R, 7], dz [3, R, 7] (the n = 7 transfer-matrix forward with tangents)
+int gemm3_readout(int64_t R, const float* Phi, const float* Wt, float* Psi, float* z, float* dz,
+                  void* ws, size_t ws_bytes, cudaStream_t st) {
+  constexpr int N = 256, K = 128;
+  if (ws_bytes < gemm3_workspace_bytes(N, K)) return fail(QPINN_ERR_CONFIG, "gemm3: workspace");
+  if (R == 0) return QPINN_OK;
+  const int ldk = ldk_of(K);
+  float* hi = (float*)(((uintptr_t)ws + 255) & ~(uintptr_t)255);
+  float* lo = hi + (size_t)N * ldk;
+  split_rows<<<64, 256, 0, st>>>(Wt, N, K, K, ldk, hi, lo);
+  QPINN_CUDA_CHECK(cudaGetLastError());
+  GemmArgs g{4 * R, R, N, K, Psi, N, nullptr, 0, z, dz};
+  return launch_gemm3<128, EPI_READOUT>(g, Phi, K, hi, lo, ldk, st);
 }
 
 static void wgrad_plan(int64_t rows, int Kin, int Nout, WgradArgs* a) {
@@ -1247,7 +1321,7 @@ int dense_tanh1(int64_t R, int N, int K, const float* X, const float* W, const f
   float* lo = hi + (size_t)N * ldk;
   split_transpose<<<64, 256, 0, st>>>(W, K, N, ldk, hi, lo);
   QPINN_CUDA_CHECK(cudaGetLastError());
-  GemmArgs g{R, R, N, K, H, N, bias, 0};
+  GemmArgs g{R, R, N, K, H, N, bias, 0, nullptr, nullptr};
   return dispatch<EPI_TANH1>(g, X, K, hi, lo, ldk, st);
 }
 
@@ -1261,7 +1335,7 @@ int dense_tanh(int64_t R, int N, int K, const float* X, const float* W, const fl
   float* lo = hi + (size_t)N * ldk;
   split_transpose<<<64, 256, 0, st>>>(W, K, N, ldk, hi, lo);
   QPINN_CUDA_CHECK(cudaGetLastError());
-  GemmArgs g{4 * R, R, N, K, H, N, bias, 0};
+  GemmArgs g{4 * R, R, N, K, H, N, bias, 0, nullptr, nullptr};
   return dispatch<EPI_TANH>(g, X, K, hi, lo, ldk, st);
 }
 

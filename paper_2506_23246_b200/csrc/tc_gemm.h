@@ -11,6 +11,10 @@ size_t gemm3_workspace_bytes(int N, int K);
 // C[M,N] = A[M,K] B[N,K]^T (fp32, 3xTF32 tensor cores)
 int gemm3(int64_t M, int N, int K, const float* A, int64_t lda, const float* B, int64_t ldb,
           float* C, int64_t ldc, void* ws, size_t ws_bytes, cudaStream_t st);
+// Psi [4R, 256] = Phi [4R, 128] Wt[256, 128]^T with the fused n = 7 Pauli-Z readout
+// z [R, 7], dz [3, R, 7] (transfer-matrix PQC forward with tangents)
+int gemm3_readout(int64_t R, const float* Phi, const float* Wt, float* Psi, float* z, float* dz,
+                  void* ws, size_t ws_bytes, cudaStream_t st);
 size_t wgrad_workspace_bytes(int64_t rows, int Kin, int Nout);
 // dW [Kin,Nout] = X [rows,Kin]^T G [rows,Nout] (split-K over rows, deterministic)
 int wgrad(int64_t rows, int Kin, int Nout, const float* X, int64_t ldx, const float* G,
