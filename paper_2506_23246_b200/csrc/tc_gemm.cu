@@ -174,6 +174,10 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUt
              const GemmArgs g) {
   using Cfg = GemmCfg<BN>;
   constexpr int RS = Cfg::kRaw, OS = Cfg::kOps, BS = Cfg::kBS, NB = Cfg::kNB;
+#ifndef QPINN_GEMM_SHARE_EMPTY
+#define QPINN_GEMM_SHARE_EMPTY 1
+#endif
+  constexpr bool kShareEmpty = QPINN_GEMM_SHARE_EMPTY && OS == BS;
   extern __shared__ unsigned char smem_raw[];
   unsigned char* smem = (unsigned char*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   unsigned char* raw = smem;                        // [RS][16 KB] fp32 A tiles
@@ -259,7 +263,11 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUt
       for (int nt = 0; nt < n_nt; ++nt) {
         for (int kb = 0; kb < nk; ++kb, ++j) {
           const int e = (int)(j % BS);
-          if (j >= BS) GPROF(1, mbar_wait(b_empty + e, (uint32_t)(((j / BS) - 1) & 1)));
+          // with as many B stages as A operand stages one MMA commit frees both
+          // (each tcgen05.commit costs tensor-pipe throughput while TMA loads are in
+          // flight: scripts/probes/mma_rate.cu, 72 -> 97 cycles per MMA at 2 per k-block)
+          uint64_t* freed = kShareEmpty ? op_empty : b_empty;
+          if (j >= BS) GPROF(1, mbar_wait(freed + e, (uint32_t)(((j / BS) - 1) & 1)));
           unsigned char* st = bst + e * Cfg::kBStage;
           if (QPINN_ABL_NOB && j >= BS) {
             mbar_arrive(b_full + e);
@@ -311,7 +319,7 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUt
             }
           }
           mma_commit(op_empty + o);
-          mma_commit(b_empty + e);
+          if (!kShareEmpty) mma_commit(b_empty + e);
           if (last) {
             mma_commit(tfull + b);
             ++grp;

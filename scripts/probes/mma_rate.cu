@@ -11,9 +11,13 @@
 #include <cstdio>
 #include <cuda_runtime.h>
 
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include "tc_gemm.cuh"
 
 using namespace qpinn::tc;
+static CUtensorMap g_map;
 
 __device__ __forceinline__ void mma_tf32_2cta(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc,
                                               uint32_t acc) {
@@ -27,17 +31,20 @@ __device__ __forceinline__ void mma_tf32_2cta(uint32_t d, uint64_t a, uint64_t b
 // variant: 0 = A TMEM (ts), 1 = A smem (ss); N = 64/128/256; chain = MMAs per commit
 // LOAD: 0 = MMA alone; 1 = warps 4..11 stream tcgen05.ld of 32 columns meanwhile
 // (the promotion reads of tc_gemm.cu); 2 = warps 4..7 stream tcgen05.st (the A split)
-template <int N, int VAR, int LOAD = 0>
-__global__ void __launch_bounds__(384, 1) mma_rate(int iters, int chain, unsigned long long* out) {
+template <int N, int VAR, int LOAD = 0, int NCOMMIT = 0, int CPER = 12>
+__global__ void __launch_bounds__(384, 1) mma_rate(int iters, int chain, unsigned long long* out,
+                                                   const __grid_constant__ CUtensorMap amap) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   unsigned char* smem = (unsigned char*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   __shared__ uint64_t bar;
+  __shared__ uint64_t dummy[4];
   __shared__ uint32_t tslot;
-  const int warp = threadIdx.x >> 5;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // zero operands
   for (int i = threadIdx.x; i < 64 * 1024 / 4; i += blockDim.x) ((float*)smem)[i] = 0.f;
   if (threadIdx.x == 0) {
     mbar_init(&bar, 1);
+    for (int i = 0; i < 4; ++i) mbar_init(dummy + i, 1);
     mbar_init_fence();
   }
   if (warp == 0) tmem_alloc(&tslot, 512);
@@ -49,7 +56,25 @@ __global__ void __launch_bounds__(384, 1) mma_rate(int iters, int chain, unsigne
   __shared__ volatile int done;
   if (threadIdx.x == 0) done = 0;
   __syncthreads();
-  if (LOAD && warp >= 4) {
+  if (LOAD == 4 && warp == 4) {
+    if (lane == 0) {
+      __shared__ uint64_t tb[4];
+      for (int i = 0; i < 4; ++i) mbar_init(tb + i, 1);
+      mbar_init_fence();
+      int64_t j = 0;
+      const int64_t tiles = 262144 / 128;
+      while (!done) {
+        const int s = (int)(j & 3);
+        if (j >= 4) mbar_wait(tb + s, (uint32_t)(((j >> 2) - 1) & 1));
+        mbar_expect_tx(tb + s, 16384);
+        const int64_t t = (blockIdx.x + (j / 8) * gridDim.x) % tiles;
+        tma_load_2d(smem + 32768 + s * 16384, &amap, tb + s, (int)(j % 8) * 32, (int)(t * 128));
+        ++j;
+      }
+      for (int64_t i = (j > 4 ? j - 4 : 0); i < j; ++i) mbar_wait(tb + (int)(i & 3), (uint32_t)((i >> 2) & 1));
+      out[2 * gridDim.x + blockIdx.x] = j;
+    }
+  } else if (LOAD && LOAD != 4 && warp >= 4) {
     const int q = warp & 3;
     const uint32_t lane_base = (uint32_t)(q * 32) << 16;
     float v[32];
@@ -95,6 +120,8 @@ __global__ void __launch_bounds__(384, 1) mma_rate(int iters, int chain, unsigne
           mma_tf32_ts(d, a_t + (c & 3) * 8, desc_k_sw128(b_s + off), idesc, 1);
         else
           mma_tf32(d, desc_k_sw128(a_s + off), desc_k_sw128(b_s + off), idesc, 1);
+        if (NCOMMIT && c % CPER == CPER - 1)
+          for (int k = 0; k < NCOMMIT; ++k) mma_commit(dummy + k);
       }
       mma_commit(&bar);
       mbar_wait(&bar, ph);
@@ -110,19 +137,19 @@ __global__ void __launch_bounds__(384, 1) mma_rate(int iters, int chain, unsigne
   if (warp == 0) tmem_dealloc(tmem, 512);
 }
 
-template <int N, int VAR, int LOAD = 0>
+template <int N, int VAR, int LOAD = 0, int NCOMMIT = 0, int CPER = 12>
 void run(const char* name, int chain, int iters) {
   int sms = 0;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   unsigned long long* d;
-  cudaMalloc(&d, 2 * sms * sizeof(unsigned long long));
-  cudaFuncSetAttribute(mma_rate<N, VAR, LOAD>, cudaFuncAttributeMaxDynamicSharedMemorySize, 80 * 1024);
-  mma_rate<N, VAR, LOAD><<<sms, 384, 80 * 1024>>>(iters / 10, chain, d);  // warm
+  cudaMalloc(&d, 3 * sms * sizeof(unsigned long long));
+  cudaFuncSetAttribute(mma_rate<N, VAR, LOAD, NCOMMIT, CPER>, cudaFuncAttributeMaxDynamicSharedMemorySize, 120 * 1024);
+  mma_rate<N, VAR, LOAD, NCOMMIT, CPER><<<sms, 384, 120 * 1024>>>(iters / 10, chain, d, g_map);  // warm
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
   cudaEventRecord(e0);
-  mma_rate<N, VAR, LOAD><<<sms, 384, 80 * 1024>>>(iters, chain, d);
+  mma_rate<N, VAR, LOAD, NCOMMIT, CPER><<<sms, 384, 120 * 1024>>>(iters, chain, d, g_map);
   cudaEventRecord(e1);
   cudaError_t err = cudaDeviceSynchronize();
   if (err != cudaSuccess) {
@@ -131,8 +158,13 @@ void run(const char* name, int chain, int iters) {
   }
   float ms;
   cudaEventElapsedTime(&ms, e0, e1);
-  unsigned long long h[2 * 256];
-  cudaMemcpy(h, d, 2 * sms * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
+  unsigned long long h[3 * 256];
+  cudaMemcpy(h, d, 3 * sms * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
+  if (LOAD == 4) {
+    double nb = 0;
+    for (int i = 0; i < sms; ++i) nb += h[2 * sms + i];
+    printf("   concurrent TMA loads: %.0f GB/s\n", nb * 16384 / (ms * 1e-3) / 1e9);
+  }
   double cyc = 0, n = 0;
   for (int i = 0; i < sms; ++i) {
     cyc += h[i];
@@ -149,6 +181,36 @@ void run(const char* name, int chain, int iters) {
 }
 
 int main() {
+  {
+    float* A;
+    cudaMalloc(&A, 262144LL * 256 * 4);
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q);
+    auto enc = (PFN_cuTensorMapEncodeTiled_v12000)p;
+    cuuint64_t dims[2] = {256, 262144};
+    cuuint64_t strides[1] = {256 * 4};
+    cuuint32_t bx[2] = {32, 128};
+    cuuint32_t es[2] = {1, 1};
+    enc(&g_map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, A, dims, strides, bx, es,
+        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  }
+  run<128, 0, 4, 0>("TMA + 0 commits", 48, 4000);
+  run<128, 0, 4, 1, 12>("TMA + 1 commit / 12", 48, 4000);
+  run<128, 0, 4, 2, 12>("TMA + 2 commits / 12", 48, 4000);
+  run<128, 0, 4, 3, 12>("TMA + 3 commits / 12", 48, 4000);
+  run<128, 0, 4, 1, 24>("TMA + 1 commit / 24", 48, 4000);
+  run<128, 0, 4, 2, 24>("TMA + 2 commits / 24", 48, 4000);
+  run<128, 0, 4, 1, 48>("TMA + 1 commit / 48", 96, 2000);
+  run<128, 0, 0, 1, 24>("no TMA, 1 commit / 24", 48, 4000);
+  return 0;
+  run<128, 0, 0, 0>("ts N128 no commits", 48, 4000);
+  run<128, 0, 0, 1>("ts N128 1 commit / 12 MMAs", 48, 4000);
+  run<128, 0, 0, 2>("ts N128 2 commits / 12 MMAs", 48, 4000);
+  run<128, 0, 0, 3>("ts N128 3 commits / 12 MMAs", 48, 4000);
+  run<128, 0, 0, 2>("ts N128 2 commits / 12, wait/96", 96, 2000);
+  return 0;
   for (int chain : {48}) {
     run<128, 0, 3>("ts N128 + 8 warps lds.128", chain, 4000);
     run<128, 1, 3>("ss N128 + 8 warps lds.128", chain, 4000);
