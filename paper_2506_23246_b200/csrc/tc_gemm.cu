@@ -116,7 +116,9 @@ struct GemmCfg {
   static_assert(!kATmem || kNB * BN + kOps * 2 * kBK <= 512, "TMEM columns");
   static constexpr int kSbuf = 32 * BN * 4;
   static constexpr int kStg = 8 * 2 * 2048;  // per epilogue warp: 2 x (16 rows x 32 cols)
-  static constexpr int kRed = 4 * 32 * 8 * 4;  // EPI_READOUT: column-half partials
+  // EPI_READOUT / fused adapter: column-half partials [4][32][8], adapter
+  // weights [BN][8], adapter values [32][8]
+  static constexpr int kRed = (4 * 32 * 8 + BN * 8 + 32 * 8) * 4;
   static constexpr int kSmem =
       kRaw * kABytes + kOps * kOpBytes + kBS * kBStage + kSbuf + kStg + kRed + 1024 + 512;
 };
@@ -131,6 +133,12 @@ struct GemmArgs {
   int tma_store;      // C goes out through TMA (16-byte aligned rows), else direct stores
   float* z;           // EPI_READOUT: z [R, NQ], dz [3, R, NQ]
   float* dz;
+  // EPI_TANH with a fused adapter (network.py:298-299): act [4, R, n_ad] = dual
+  // tanh(y Wa + ba) of this layer's output y, Wa [N, n_ad] row-major (N <= BN)
+  const float* ad_w;
+  const float* ad_b;
+  float* act;
+  int n_ad;
 };
 
 // one epilogue warp's 32 rows x CW columns (lane = row) -> global through two
@@ -416,6 +424,14 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUt
     uint32_t sidx = 0;
     int64_t j = 0;
     float zr[8];  // EPI_READOUT: readout partials of this row over the N-tiles
+    float* s_wa = red + 4 * 32 * 8;   // fused adapter weights [BN][8]
+    float* s_a = s_wa + BN * 8;        // adapter values of the tile's points [32][8]
+    if (EPI == EPI_TANH && g.ad_w) {
+      for (int i = threadIdx.x - 128; i < BN * 8; i += 256) {
+        const int c = i >> 3, jj = i & 7;
+        s_wa[i] = (c < g.N && jj < g.n_ad) ? g.ad_w[(int64_t)c * g.n_ad + jj] : 0.f;
+      }
+    }
     for (int64_t mt = blockIdx.x; mt < n_mt; mt += gridDim.x)
       for (int nt = 0; nt < n_nt; ++nt) {
       const int n0 = nt * BN, c_off = h * CW;
@@ -533,6 +549,46 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUt
 #pragma unroll
           for (int c = 0; c < CW; ++c)
             if (n0 + c_off + c < g.N) dst[c] = acc[c];
+        }
+        if (g.ad_w) {  // fused adapter: u = y Wa per row (fp32 FMA, two column halves)
+          float u[8];
+#pragma unroll
+          for (int jj = 0; jj < 8; ++jj) u[jj] = 0.f;
+#pragma unroll
+          for (int c = 0; c < CW; ++c) {
+            const float4 w0 = *reinterpret_cast<const float4*>(s_wa + (c_off + c) * 8);
+            const float4 w1 = *reinterpret_cast<const float4*>(s_wa + (c_off + c) * 8 + 4);
+            u[0] = fmaf(acc[c], w0.x, u[0]);
+            u[1] = fmaf(acc[c], w0.y, u[1]);
+            u[2] = fmaf(acc[c], w0.z, u[2]);
+            u[3] = fmaf(acc[c], w0.w, u[3]);
+            u[4] = fmaf(acc[c], w1.x, u[4]);
+            u[5] = fmaf(acc[c], w1.y, u[5]);
+            u[6] = fmaf(acc[c], w1.z, u[6]);
+            u[7] = fmaf(acc[c], w1.w, u[7]);
+          }
+          if (h == 1) {
+#pragma unroll
+            for (int jj = 0; jj < 8; ++jj) red[(q * 32 + lane) * 8 + jj] = u[jj];
+          }
+          asm volatile("bar.sync 1, 256;" ::: "memory");
+          if (h == 0) {
+#pragma unroll
+            for (int jj = 0; jj < 8; ++jj) u[jj] += red[(q * 32 + lane) * 8 + jj];
+            if (q == 0) {
+#pragma unroll
+              for (int jj = 0; jj < 8; ++jj)
+                s_a[lane * 8 + jj] = jj < g.n_ad ? tanhf(u[jj] + __ldg(g.ad_b + jj)) : 0.f;
+            }
+          }
+          asm volatile("bar.sync 1, 256;" ::: "memory");
+          if (h == 0 && p < g.R) {  // a = tanh(u0 + ba); da_k = (1 - a^2) u_k
+            float* dst = g.act + ((int64_t)q * g.R + p) * g.n_ad;
+            for (int jj = 0; jj < g.n_ad; ++jj) {
+              const float a = s_a[lane * 8 + jj];
+              dst[jj] = q == 0 ? a : (1.f - a * a) * u[jj];
+            }
+          }
         }
         asm volatile("bar.sync 1, 256;" ::: "memory");  // sbuf reused by the next tile
       }
@@ -1249,7 +1305,7 @@ int gemm3(int64_t M, int N, int K, const float* A, int64_t lda, const float* B, 
   float* lo = hi + (size_t)N * ldk;
   split_rows<<<64, 256, 0, st>>>(B, N, K, ldb, ldk, hi, lo);
   QPINN_CUDA_CHECK(cudaGetLastError());
-  GemmArgs g{M, 0, N, K, C, ldc, nullptr, 0, nullptr, nullptr};
+  GemmArgs g{M, 0, N, K, C, ldc, nullptr, 0, nullptr, nullptr, nullptr, nullptr, nullptr, 0};
   return dispatch<EPI_STORE>(g, A, lda, hi, lo, ldk, st);
 }
 
@@ -1265,7 +1321,7 @@ int gemm3_readout(int64_t R, const float* Phi, const float* Wt, float* Psi, floa
   float* lo = hi + (size_t)N * ldk;
   split_rows<<<64, 256, 0, st>>>(Wt, N, K, K, ldk, hi, lo);
   QPINN_CUDA_CHECK(cudaGetLastError());
-  GemmArgs g{4 * R, R, N, K, Psi, N, nullptr, 0, z, dz};
+  GemmArgs g{4 * R, R, N, K, Psi, N, nullptr, 0, z, dz, nullptr, nullptr, nullptr, 0};
   return launch_gemm3<128, EPI_READOUT>(g, Phi, K, hi, lo, ldk, st);
 }
 
@@ -1329,7 +1385,7 @@ int dense_tanh1(int64_t R, int N, int K, const float* X, const float* W, const f
   float* lo = hi + (size_t)N * ldk;
   split_transpose<<<64, 256, 0, st>>>(W, K, N, ldk, hi, lo);
   QPINN_CUDA_CHECK(cudaGetLastError());
-  GemmArgs g{R, R, N, K, H, N, bias, 0, nullptr, nullptr};
+  GemmArgs g{R, R, N, K, H, N, bias, 0, nullptr, nullptr, nullptr, nullptr, nullptr, 0};
   return dispatch<EPI_TANH1>(g, X, K, hi, lo, ldk, st);
 }
 
@@ -1343,8 +1399,25 @@ int dense_tanh(int64_t R, int N, int K, const float* X, const float* W, const fl
   float* lo = hi + (size_t)N * ldk;
   split_transpose<<<64, 256, 0, st>>>(W, K, N, ldk, hi, lo);
   QPINN_CUDA_CHECK(cudaGetLastError());
-  GemmArgs g{4 * R, R, N, K, H, N, bias, 0, nullptr, nullptr};
+  GemmArgs g{4 * R, R, N, K, H, N, bias, 0, nullptr, nullptr, nullptr, nullptr, nullptr, 0};
   return dispatch<EPI_TANH>(g, X, K, hi, lo, ldk, st);
+}
+
+// dense_tanh with the tanh adapter fused into its epilogue: also
+// act [4R, n_ad] = dual tanh(H Wa + ba) (N <= 128, n_ad <= 8)
+int dense_tanh_adapter(int64_t R, int N, int K, const float* X, const float* W, const float* bias,
+                       float* H, const float* Wa, const float* ba, int n_ad, float* act, void* ws,
+                       size_t ws_bytes, cudaStream_t st) {
+  if (ws_bytes < gemm3_workspace_bytes(N, K)) return fail(QPINN_ERR_CONFIG, "dense: workspace");
+  if (N > 128 || n_ad < 1 || n_ad > 8) return fail(QPINN_ERR_CONFIG, "fused adapter: shape");
+  if (R == 0) return QPINN_OK;
+  const int ldk = ldk_of(K);
+  float* hi = (float*)(((uintptr_t)ws + 255) & ~(uintptr_t)255);
+  float* lo = hi + (size_t)N * ldk;
+  split_transpose<<<64, 256, 0, st>>>(W, K, N, ldk, hi, lo);
+  QPINN_CUDA_CHECK(cudaGetLastError());
+  GemmArgs g{4 * R, R, N, K, H, N, bias, 0, nullptr, nullptr, Wa, ba, act, n_ad};
+  return launch_gemm3<128, EPI_TANH>(g, X, K, hi, lo, ldk, st);
 }
 
 }  // namespace tc

@@ -25,5 +25,10 @@ int dense_tanh1(int64_t R, int N, int K, const float* X, const float* W, const f
 // H [4R,N] = dual tanh of X [4R,K] W [K,N] + b (value / tangent channel blocks)
 int dense_tanh(int64_t R, int N, int K, const float* X, const float* W, const float* bias,
                float* H, void* ws, size_t ws_bytes, cudaStream_t st);
+// dense_tanh with the tanh adapter fused into the epilogue: also
+// act [4R, n_ad] = dual tanh(H Wa + ba)  (N <= 128, n_ad <= 8)
+int dense_tanh_adapter(int64_t R, int N, int K, const float* X, const float* W, const float* bias,
+                       float* H, const float* Wa, const float* ba, int n_ad, float* act, void* ws,
+                       size_t ws_bytes, cudaStream_t st);
 }  // namespace tc
 }  // namespace qpinn

@@ -568,6 +568,15 @@ static int bias_grad(int64_t R, int N, const T* GU0, double* part, T* out, cudaS
   return QPINN_OK;
 }
 
+// QPINN_FUSE_ADAPTER=0: the adapter as its own tensor-core layer (A/B experiments)
+static bool adapter_fusion_off() {
+  static const bool off = [] {
+    const char* e = getenv("QPINN_FUSE_ADAPTER");
+    return e && atoi(e) == 0;
+  }();
+  return off;
+}
+
 template <typename T>
 static int forward_impl(const qpinn_trunk_desc* d, int64_t R, const T* x, const T* y, const T* t,
                         const T* params, T* act, unsigned char* ws, cudaStream_t st,
@@ -601,8 +610,21 @@ static int forward_impl(const qpinn_trunk_desc* d, int64_t R, const T* x, const 
     QPINN_CUDA_CHECK(cudaGetLastError());
     return QPINN_OK;
   };
+  // the tanh adapter (128 -> n) rides in the last hidden layer's epilogue when
+  // that layer runs on the tensor cores with a single N-tile
+  bool fuse_adapter = false;
+  if constexpr (sizeof(T) == 4)
+    fuse_adapter = nch == 4 && d->n_hidden > 0 && H <= 128 && H % 4 == 0 && n <= 8 &&
+                   !adapter_fusion_off();
   for (int i = 0; i < d->n_hidden; ++i) {
     T* Hn = (T*)(ws + w.h[i]);
+    if constexpr (sizeof(T) == 4) {
+      if (fuse_adapter && i == d->n_hidden - 1 && K % 4 == 0)
+        return tc::dense_tanh_adapter(R, H, K, (const float*)in, params + d->off_w[i],
+                                      params + d->off_b[i], Hn, params + d->off_adapter_w,
+                                      params + d->off_adapter_b, n, act, ws + w.wsplit,
+                                      w.total - w.wsplit, st);
+    }
     if (int rc = dense(K, H, in, d->off_w[i], d->off_b[i], Hn)) return rc;
     in = Hn;
     K = H;

@@ -24,6 +24,16 @@ from . import _native as N
 from .ansatz import _SCALE_CODE, ScaleKind, state_buffer
 
 
+def adapter_fused(model) -> bool:
+    """trunk.cu's rule: the float32 dual forward computes the tanh adapter in the
+    last hidden layer's tensor-core epilogue (QPINN_FUSE_ADAPTER=0 turns it off)."""
+    import os
+    cfg = model.config
+    H = cfg.hidden_width
+    return (model.dtype == torch.float32 and model.n_hidden > 0 and H <= 128 and H % 4 == 0
+            and cfg.n_qubits <= 8 and os.environ.get("QPINN_FUSE_ADAPTER", "1") != "0")
+
+
 def trunk_desc(model):
     """``qpinn_trunk_desc`` for a hybrid model (offsets into its flat layout);
     returns (desc, omega tensor kept alive, offsets)."""
@@ -105,10 +115,11 @@ class InferenceEngine:
         N.count_launches(1 + sum(2 if (self.dtype == torch.float32 and k % 4 == 0) else 1
                                  for k in widths) + 2)
 
-    def _trunk_launches(self) -> int:
+    def _trunk_launches(self, dual: bool = False) -> int:
         widths = [2 * self.model.config.rff_features] + \
             [self.model.config.hidden_width] * self.model.n_hidden
-        return 1 + sum(2 if (self.dtype == torch.float32 and k % 4 == 0) else 1 for k in widths)
+        n = 1 + sum(2 if (self.dtype == torch.float32 and k % 4 == 0) else 1 for k in widths)
+        return n - 2 if dual and adapter_fused(self.model) else n
 
     def adapter(self, flat, x, y, t) -> torch.Tensor:
         """Adapter activations a [R, n] (network.py:323-335): value trunk only."""
@@ -157,7 +168,7 @@ class InferenceEngine:
                                            self._zero_b.data_ptr(), self._dout.data_ptr(), st),
                     "qpinn_head_forward")
             dout[:, lo:hi].copy_(self._dout[:3 * r * 3].view(3, r, 3))
-            N.count_launches(self._trunk_launches() + 2 + 2)
+            N.count_launches(self._trunk_launches(dual=True) + 2 + 2)
         return out, dout
 
     def check_domain(self):
@@ -308,6 +319,8 @@ class NativeEngine:
         n = 1                                   # features
         for k in widths:                        # hidden layers + adapter (input width k)
             n += 2 if (f32 and k % 4 == 0) else 1
+        if adapter_fused(self.model):           # the adapter rides in the last layer's epilogue
+            n -= 2
         n += 2 + 2                              # K1 prep + main, K4 + reduce
         if tape:
             n += 4 + phase                      # K2 prep, main, reduce, u1 grads (+ phase grads)
