@@ -204,13 +204,7 @@ def tensor_gemm_roofline(n_qubits: int, R: int):
         return e0.elapsed_time(e1) / k
 
     ms = timed(gemm, 20)
-    prev = torch.backends.cuda.matmul.allow_tf32
-    torch.backends.cuda.matmul.allow_tf32 = True
-    a = torch.randn(8192, 8192, device="cuda")
-    b = torch.randn(8192, 8192, device="cuda")
-    ms_pk = timed(lambda: a @ b, 10)
-    torch.backends.cuda.matmul.allow_tf32 = prev
-    peak = 2 * 8192 ** 3 / (ms_pk * 1e-3) / 1e12
+    peak = tf32_peak()
     achieved = 3 * 2 * M * n * k / (ms * 1e-3) / 1e12
     return {"bound": "tensor", "achieved": round(achieved, 1), "peak": round(peak, 1),
             "unit": "TFLOP/s", "frac": round(achieved / peak, 4), "traffic": None,
@@ -303,7 +297,6 @@ def run_ours(args):
     import torch
     import torch.distributed as dist
     from paper_2506_23246_b200 import _native as N
-    from paper_2506_23246_b200.roofline import pqc_flops, transfer_bytes, transfer_flops, trunk_bytes
     from paper_2506_23246_b200.training import Trainer, allreduce_fn
 
     rank, world, local = dist_env()
@@ -384,72 +377,9 @@ def run_ours(args):
         peak, peak_src = fp32_peak()
         circuit = tr.model.circuit
         R_local = tr.evaluator.n_local_points
-        f_fwd, f_adj = pqc_flops(circuit)
-        rl = {}
-        hbm = hbm_peak()
-        transfer = circuit.uses_transfer(dtype)
-        if transfer:  # K1/K2 as tensor-core GEMMs over HBM-staged operands
-            tb = transfer_bytes(circuit.n_qubits)
-            tf = transfer_flops(circuit.n_qubits)
-            for name, per_pt, fl, fc in (("pqc_forward", tb[0], tf[0], f_fwd),
-                                         ("pqc_backward", tb[1], tf[1], f_adj)):
-                if name not in kern:
-                    continue
-                nl, mean_ms = kern[name]
-                launches_per_step = nl / args.steps
-                pts_per_launch = R_local / launches_per_step
-                achieved = per_pt * pts_per_launch / (mean_ms * 1e-3) / 1e9
-                # the north_star's "fraction of the FP32 compute roofline": the
-                # circuit's algorithmic FLOPs (SURVEY 8d gate-sweep count,
-                # roofline.pqc_flops) per second against the FFMA peak
-                circ = fc * pts_per_launch / (mean_ms * 1e-3) / 1e12
-                rl[name] = {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm,
-                            "unit": "GB/s", "frac": round(achieved / hbm, 4),
-                            "traffic": traffic_for(name, pts_per_launch),
-                            "bytes_per_point": per_pt, "points_per_launch": pts_per_launch,
-                            "gemm_flop_per_point": fl,
-                            "gemm_tflops": round(fl * pts_per_launch / (mean_ms * 1e-3) / 1e12, 2),
-                            "circuit_flop_per_point": fc,
-                            "circuit_tflops": round(circ, 2),
-                            "fp32_peak_tflops": round(peak, 3) if peak else None,
-                            "fp32_frac": round(circ / peak, 4) if peak else None,
-                            "ms_per_launch": round(mean_ms, 4),
-                            "share_of_step": round(mean_ms * launches_per_step / (ms_prof / args.steps), 4),
-                            "path": "transfer matrix (3xTF32 tcgen05 GEMMs)",
-                            "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy bandwidth)"}
-        for name, per_pt in (("pqc_forward", f_fwd), ("pqc_backward", f_adj)):
-            if name in kern and not transfer:
-                nl, mean_ms = kern[name]
-                launches_per_step = nl / args.steps
-                pts_per_launch = R_local / launches_per_step
-                achieved = per_pt * pts_per_launch / (mean_ms * 1e-3) / 1e12
-                rl[name] = {"bound": "fp32", "achieved": round(achieved, 3),
-                            "peak": round(peak, 3) if peak else None, "unit": "TFLOP/s",
-                            "frac": round(achieved / peak, 4) if peak else None,
-                            "traffic": traffic_for(name, pts_per_launch),
-                            "flop_per_point": per_pt, "points_per_launch": pts_per_launch,
-                            "ms_per_launch": round(mean_ms, 4),
-                            "share_of_step": round(mean_ms * launches_per_step / (ms_prof / args.steps), 4),
-                            "peak_source": peak_src}
-        # trunk passes (tensor-core GEMMs + fused elementwise): HBM-bound by design
-        mc = tr.model.config
-        tb_f, tb_b = trunk_bytes(mc.hidden_width, mc.rff_features, mc.n_qubits,
-                                 tr.model.n_hidden, 4 if dtype == torch.float32 else 8)
-        for name, per_pt in (("trunk_forward", tb_f), ("trunk_backward", tb_b)):
-            if name in kern and hbm:
-                nl, mean_ms = kern[name]
-                launches_per_step = nl / args.steps
-                pts_per_launch = R_local / launches_per_step
-                achieved = per_pt * pts_per_launch / (mean_ms * 1e-3) / 1e9
-                rl[name] = {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm,
-                            "unit": "GB/s", "frac": round(achieved / hbm, 4),
-                            "traffic": traffic_for(name, pts_per_launch),
-                            "bytes_per_point": per_pt, "points_per_launch": pts_per_launch,
-                            "ms_per_launch": round(mean_ms, 4),
-                            "share_of_step": round(mean_ms * launches_per_step / (ms_prof / args.steps), 4),
-                            "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy bandwidth)"}
+        rl = roofline_passes(tr, kern, args.steps, ms_prof, dtype, peak, peak_src)
         dom = max(rl, key=lambda k: rl[k]["share_of_step"]) if rl else None
-        if transfer and dtype == torch.float32:  # the tensor-core kernel inside the PQC passes
+        if circuit.uses_transfer(dtype) and dtype == torch.float32:
             rl["transfer_gemm"] = tensor_gemm_roofline(circuit.n_qubits, R_local)
         cpu = None
         if world == 1 and not args.no_cpu_baseline:
@@ -479,6 +409,98 @@ def run_ours(args):
         dist.destroy_process_group()
     if line is not None:
         print(json.dumps(line), flush=True)
+
+
+_TF32 = {}
+
+
+def tf32_peak():
+    """cuBLAS TF32 GEMM throughput measured in this run (8192^3, allow_tf32): the
+    ceiling of the tensor-core MMA kind our FP32-class GEMMs use.  Dividing by the 3
+    products of the 3xTF32 split gives the FP32-class ceiling (MEASURED_PEAKS.json
+    carries bf16 only)."""
+    if "v" not in _TF32:
+        import torch
+        prev = torch.backends.cuda.matmul.allow_tf32
+        torch.backends.cuda.matmul.allow_tf32 = True
+        a = torch.randn(8192, 8192, device="cuda")
+        b = torch.randn(8192, 8192, device="cuda")
+        for _ in range(3):
+            a @ b
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(10):
+            a @ b
+        e1.record()
+        torch.cuda.synchronize()
+        torch.backends.cuda.matmul.allow_tf32 = prev
+        _TF32["v"] = 2 * 8192 ** 3 / (e0.elapsed_time(e1) / 10 * 1e-3) / 1e12
+    return _TF32["v"]
+
+
+def roofline_passes(tr, kern, steps, ms_prof, dtype, ffma_peak, ffma_src):
+    """Per pass of the step: achieved ALGORITHMIC FLOP/s (SURVEY 8d per-point counts:
+    roofline.pqc_flops for the circuit -- the gate-sweep count, whatever formulation
+    runs it -- and roofline.trunk_flops for the trunk) over the pass's CUDA-event
+    time, against the ceiling of the units that run it:
+      * tensor-core passes (the trunk; the transfer-matrix PQC at fp32 n = 5..7):
+        the FP32-class ceiling of 3xTF32 = the in-run cuBLAS TF32 peak / 3;
+      * CUDA-core passes (the layer-loop PQC kernels): the in-run FFMA peak.
+    ``hbm_staged`` is the same pass seen as HBM traffic: the bytes its kernels stage
+    through HBM by design (roofline.transfer_bytes / trunk_bytes) and ``traffic`` the
+    DRAM bytes ncu measured for it (profiles/traffic.json), per launch."""
+    import torch
+    from paper_2506_23246_b200.roofline import pqc_flops, transfer_bytes, trunk_bytes, trunk_flops
+    circuit = tr.model.circuit
+    mc = tr.model.config
+    R_local = tr.evaluator.n_local_points
+    hbm = hbm_peak()
+    transfer = circuit.uses_transfer(dtype)
+    f_fwd, f_adj = pqc_flops(circuit)
+    t_fwd, t_bwd = trunk_flops(mc.hidden_width, mc.rff_features, mc.n_qubits, tr.model.n_hidden)
+    tb_f, tb_b = trunk_bytes(mc.hidden_width, mc.rff_features, mc.n_qubits, tr.model.n_hidden,
+                             4 if dtype == torch.float32 else 8)
+    pb_f, pb_b = transfer_bytes(circuit.n_qubits) if transfer else (None, None)
+    tensor_ceiling = tf32_peak() / 3 if dtype == torch.float32 else None
+    spec = {"pqc_forward": (f_fwd, pb_f, transfer), "pqc_backward": (f_adj, pb_b, transfer),
+            "trunk_forward": (t_fwd, tb_f, dtype == torch.float32),
+            "trunk_backward": (t_bwd, tb_b, dtype == torch.float32)}
+    rl = {}
+    for name, (flop_pp, bytes_pp, on_tensor) in spec.items():
+        if name not in kern:
+            continue
+        nl, mean_ms = kern[name]
+        per_step = nl / steps
+        pts = R_local / per_step
+        achieved = flop_pp * pts / (mean_ms * 1e-3) / 1e12
+        if on_tensor:
+            peak, unit_src = tensor_ceiling, ("in-run cuBLAS TF32 GEMM 8192^3 / 3 (the FP32-class "
+                                              "ceiling of the 3xTF32 split; MEASURED_PEAKS.json "
+                                              "has bf16 only)")
+        else:
+            peak, unit_src = ffma_peak, ffma_src
+        e = {"bound": "tensor" if on_tensor else "fp32", "achieved": round(achieved, 2),
+             "peak": round(peak, 1) if peak else None, "unit": "TFLOP/s",
+             "frac": round(achieved / peak, 4) if peak else None,
+             "traffic": traffic_for(name, pts), "flop_per_point": flop_pp,
+             "points_per_launch": pts, "ms_per_launch": round(mean_ms, 4),
+             "share_of_step": round(mean_ms * per_step / (ms_prof / steps), 4),
+             "peak_source": unit_src,
+             "flop_counting": ("SURVEY 8(d) gate-sweep count of the circuit (roofline.pqc_flops)"
+                               if name.startswith("pqc") else
+                               "SURVEY 8(d) trunk count with tangents (roofline.trunk_flops)")}
+        if name.startswith("pqc") and ffma_peak:
+            e["fp32_simt_frac"] = round(achieved / ffma_peak, 4)  # north_star's FP32-peak view
+        if bytes_pp:
+            gbs = bytes_pp * pts / (mean_ms * 1e-3) / 1e9
+            e["hbm_staged"] = {"bytes_per_point": bytes_pp, "achieved": round(gbs, 1),
+                               "peak": hbm, "unit": "GB/s", "frac": round(gbs / hbm, 4),
+                               "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy bandwidth)"}
+        if name.startswith("pqc"):
+            e["path"] = ("transfer matrix (3xTF32 tcgen05 GEMMs)" if transfer
+                         else "layer-loop gate sweep (CUDA cores)")
+        rl[name] = e
+    return rl
 
 
 def bench_config(wl, world):

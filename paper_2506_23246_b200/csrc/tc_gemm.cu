@@ -623,7 +623,11 @@ template <int BN>
 struct PairCfg {
   static constexpr int HB = BN / 2;                 // B rows held per CTA
   static constexpr int kSlab = HB * kBK * 4;        // one k-block of B_hi (or B_lo) half
-  static constexpr int RS = 3, OS = 2, NB = 3;
+  // 4 TMEM A stages, 2 partial buffers: one MMA commit per promotion group (2
+  // k-blocks) frees the group's A stages AND publishes its partial
+  // (tcgen05.commit costs ~150 tensor-pipe cycles while TMA loads are in flight,
+  // scripts/probes/mma_rate.cu), instead of one per k-block plus one per group
+  static constexpr int RS = 3, OS = 4, NB = 2;
   static constexpr int kACol = NB * BN;
   static_assert(NB * BN + OS * 2 * kBK <= 512, "TMEM columns");
   static constexpr int kSbuf = 32 * BN * 4;
@@ -651,9 +655,8 @@ gemm3_pair_kernel(const __grid_constant__ CUtensorMap mA, const __grid_constant_
   uint64_t* raw_empty = raw_full + RS;
   uint64_t* b_full = raw_empty + RS;
   uint64_t* conv = b_full + 1;
-  uint64_t* op_empty = conv + OS;
-  uint64_t* tfull = op_empty + OS;
-  uint64_t* tempty = tfull + NB;
+  uint64_t* gdone = conv + OS;    // per partial buffer: the group's MMAs completed
+  uint64_t* tempty = gdone + NB;
   uint32_t* tmem_slot = (uint32_t*)(tempty + NB);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = cluster_rank();
@@ -671,12 +674,9 @@ gemm3_pair_kernel(const __grid_constant__ CUtensorMap mA, const __grid_constant_
       mbar_init(raw_empty + s, 4);
     }
     mbar_init(b_full, 1);
-    for (int s = 0; s < OS; ++s) {
-      mbar_init(conv + s, 8);      // 4 split warps x 2 CTAs (leader's barrier)
-      mbar_init(op_empty + s, 1);  // multicast commit
-    }
+    for (int s = 0; s < OS; ++s) mbar_init(conv + s, 8);  // 4 split warps x 2 CTAs (leader)
     for (int b = 0; b < NB; ++b) {
-      mbar_init(tfull + b, 1);     // multicast commit
+      mbar_init(gdone + b, 1);     // multicast commit
       mbar_init(tempty + b, 16);   // 8 epilogue warps x 2 CTAs (leader's barrier)
     }
     mbar_init_fence();
@@ -747,9 +747,8 @@ gemm3_pair_kernel(const __grid_constant__ CUtensorMap mA, const __grid_constant_
             mma2_tf32_ts(d, a_hi + k * 8, desc_k_sw128(b_lo + off), idesc, 1);
             mma2_tf32_ts(d, a_hi + k * 8, desc_k_sw128(b_hi + off), idesc, 1);
           }
-          mma_commit2(op_empty + o);
           if (last) {
-            mma_commit2(tfull + b);
+            mma_commit2(gdone + b);
             ++grp;
           }
         }
@@ -759,14 +758,24 @@ gemm3_pair_kernel(const __grid_constant__ CUtensorMap mA, const __grid_constant_
   } else if (warp < 4) {  // ---- split A into this CTA's TMEM, signal the leader
     const int row = warp * 32 + lane;
     const uint32_t lane_base = (uint32_t)(warp * 32) << 16;
-    int64_t j = 0;
+    int64_t j = 0, grp = 0;
+    int64_t grp_of[OS];  // promotion group of the k-block last written to each A stage
+    for (int i = 0; i < OS; ++i) grp_of[i] = -1;
     for (int64_t mt = mt0; mt < n_mt; mt += mstep) {
       for (int kb = 0; kb < nk; ++kb, ++j) {
         const int r = (int)(j % RS), o = (int)(j % OS);
-        if (j >= OS) {
-          mbar_wait(op_empty + o, (uint32_t)(((j / OS) - 1) & 1));
+        int64_t gprev = -1;
+#pragma unroll
+        for (int i = 0; i < OS; ++i)
+          if (i == o) gprev = grp_of[i];
+        if (gprev >= 0) {  // that group's MMAs must have completed
+          mbar_wait(gdone + (int)(gprev % NB), (uint32_t)((gprev / NB) & 1));
           tc_fence_after();
         }
+#pragma unroll
+        for (int i = 0; i < OS; ++i)
+          if (i == o) grp_of[i] = grp;
+        if (kb % kPromote == kPromote - 1 || kb == nk - 1) ++grp;
         mbar_wait(raw_full + r, (uint32_t)((j / RS) & 1));
         const uint32_t src = smem_u32(raw + r * kABytes) + row * 128;
         float4 v[8];
@@ -806,7 +815,7 @@ gemm3_pair_kernel(const __grid_constant__ CUtensorMap mA, const __grid_constant_
       const int ngrp = (nk + kPromote - 1) / kPromote;
       for (int gi = 0; gi < ngrp; ++gi, ++j) {
         const int b = (int)(j % NB);
-        mbar_wait(tfull + b, (uint32_t)((j / NB) & 1));
+        mbar_wait(gdone + b, (uint32_t)((j / NB) & 1));
         tc_fence_after();
 #pragma unroll
         for (int c0 = 0; c0 < CW; c0 += 32) {
@@ -1280,6 +1289,7 @@ static bool use_pair(int BN, int K) {
   }();
   if (!env) return false;
   const int nk = (K + kBK - 1) / kBK;
+  if (nk % kPromote) return false;  // whole promotion groups (the A-stage reuse rule)
   const size_t need = BN == 64 ? PairCfg<64>::smem(nk) : PairCfg<128>::smem(nk);
   return need <= 232448;
 }

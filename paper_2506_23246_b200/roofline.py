@@ -28,15 +28,17 @@ def transfer_bytes(n: int):
     """HBM bytes per point of the transfer-matrix K1/K2 (pqc_transfer.cu, float32).
     A [4 rows, 2D] operand (Psi, Abar) is 4 x 2D x 4 = 32 D bytes per point; the
     embedded magnitudes m and dL/dm (the phase lives in W', tr_wmat) are 16 D.
-      forward : embed writes m (16 D); the GEMM reads m, writes Psi (16 D + 32 D);
-                the readout reads Psi (32 D) + a, da in and z, dz out (2 x 16 n)
+      forward : embed writes m (16 D); the GEMM reads m, writes Psi (16 D + 32 D)
+                and reduces the readout in its epilogue (n = 7); a, da in and
+                z, dz out (2 x 16 n)
       backward: seeds read Psi, write Abar (2 x 32 D); the GEMM reads Abar, writes
                 dL/dm (32 D + 16 D); the embedding gradient reads dL/dm (16 D); the
                 weight-gradient GEMM reads m and Abar (16 D + 32 D) + dL/dz, dL/ddz,
                 a, da in, g_a, g_da out (3 x 16 n)
     The D x 2D transfer matrix and its adjoint are L2-resident and not counted."""
     D = 1 << n
-    return 96 * D + 2 * 16 * n, 176 * D + 3 * 16 * n
+    fwd = (64 if n == 7 else 96) * D  # n = 7: the readout is fused into the map's epilogue
+    return fwd + 2 * 16 * n, 176 * D + 3 * 16 * n
 
 
 def transfer_flops(n: int):

@@ -1,5 +1,5 @@
 """Run K1 and K2 alone at config-2 size (R = 2^16, 7q x 4L strongly/acos) for
-ncu captures and CUDA-event timing.  Usage: pqc_only.py [R] [kind] [iters]"""
+ncu captures and CUDA-event timing.  Usage: pqc_only.py [R] [kind] [iters] [--variant=layer] [--f64]"""
 import os
 import sys
 
@@ -11,12 +11,16 @@ from paper_2506_23246_b200.ansatz import (build_circuit, pqc_backward_raw,  # no
                                           pqc_forward_raw, state_buffer)
 from paper_2506_23246_b200.roofline import pqc_flops  # noqa: E402
 
-R = int(sys.argv[1]) if len(sys.argv) > 1 else 1 << 16
-kind = sys.argv[2] if len(sys.argv) > 2 else "strongly"
-iters = int(sys.argv[3]) if len(sys.argv) > 3 else 20
+pos = [a for a in sys.argv[1:] if not a.startswith("--")]
+R = int(pos[0]) if len(pos) > 0 else 1 << 16
+kind = pos[1] if len(pos) > 1 else "strongly"
+iters = int(pos[2]) if len(pos) > 2 else 20
 dtype = torch.float64 if "--f64" in sys.argv else torch.float32
 rng = np.random.default_rng(0)
 c = build_circuit(kind, 7, 4)
+for arg in sys.argv[1:]:
+    if arg.startswith("--variant="):  # auto | transfer | layer | generic
+        c.set_kernel_variant(arg.split("=", 1)[1])
 dev = "cuda"
 a = torch.as_tensor(rng.uniform(-0.9, 0.9, (R, 7)), dtype=dtype, device=dev)
 da = torch.as_tensor(rng.normal(size=(3, R, 7)), dtype=dtype, device=dev)

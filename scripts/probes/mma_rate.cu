@@ -74,6 +74,49 @@ __global__ void __launch_bounds__(384, 1) mma_rate(int iters, int chain, unsigne
       for (int64_t i = (j > 4 ? j - 4 : 0); i < j; ++i) mbar_wait(tb + (int)(i & 3), (uint32_t)((i >> 2) & 1));
       out[2 * gridDim.x + blockIdx.x] = j;
     }
+  } else if (LOAD == 5 && warp >= 4) {
+    const int q = warp & 3;
+    const uint32_t lane_base = (uint32_t)(q * 32) << 16;
+    if (warp == 4) {
+      if (lane == 0) {
+        __shared__ uint64_t tb[4];
+        for (int i = 0; i < 4; ++i) mbar_init(tb + i, 1);
+        mbar_init_fence();
+        int64_t j = 0;
+        const int64_t tiles = 262144 / 128;
+        while (!done) {
+          const int s = (int)(j & 3);
+          if (j >= 4) mbar_wait(tb + s, (uint32_t)(((j >> 2) - 1) & 1));
+          mbar_expect_tx(tb + s, 16384);
+          const int64_t t = (blockIdx.x + (j / 8) * gridDim.x) % tiles;
+          tma_load_2d(smem + 32768 + s * 16384, &amap, tb + s, (int)(j % 8) * 32, (int)(t * 128));
+          ++j;
+        }
+        for (int64_t i = (j > 4 ? j - 4 : 0); i < j; ++i) mbar_wait(tb + (int)(i & 3), (uint32_t)((i >> 2) & 1));
+        out[2 * gridDim.x + blockIdx.x] = j;
+      }
+    } else if (warp < 8) {
+      float v[32];
+      for (int i = 0; i < 32; ++i) v[i] = 0.f;
+      while (!done) {
+        for (int r = 0; r < 8; ++r) {
+          const uint32_t src = smem_u32(smem) + 98304 + (lane * 128 + r * 16) % 16384;
+          float4 x = lds128(src);
+          v[r] += x.x;
+        }
+        tmem_st32(tmem + lane_base + 384, v);
+        tmem_st32(tmem + lane_base + 416, v);
+        tmem_st_wait();
+      }
+    } else {
+      float v[32];
+      float acc = 0.f;
+      while (!done) {
+        tmem_ld32(tmem + lane_base + 448 + 32 * (warp >> 2 & 1), v);
+        acc += v[3];
+      }
+      if (acc == 12345.f) out[0] = 1;
+    }
   } else if (LOAD && LOAD != 4 && warp >= 4) {
     const int q = warp & 3;
     const uint32_t lane_base = (uint32_t)(q * 32) << 16;
@@ -160,7 +203,7 @@ void run(const char* name, int chain, int iters) {
   cudaEventElapsedTime(&ms, e0, e1);
   unsigned long long h[3 * 256];
   cudaMemcpy(h, d, 3 * sms * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
-  if (LOAD == 4) {
+  if (LOAD == 4 || LOAD == 5) {
     double nb = 0;
     for (int i = 0; i < sms; ++i) nb += h[2 * sms + i];
     printf("   concurrent TMA loads: %.0f GB/s\n", nb * 16384 / (ms * 1e-3) / 1e9);
@@ -196,6 +239,9 @@ int main() {
         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   }
+  run<128, 0, 5, 0>("sink + 0 commits", 48, 4000);
+  run<128, 0, 5, 1, 12>("sink + 1 commit / 12", 48, 4000);
+  run<128, 0, 5, 2, 12>("sink + 2 commits / 12", 48, 4000);
   run<128, 0, 4, 0>("TMA + 0 commits", 48, 4000);
   run<128, 0, 4, 1, 12>("TMA + 1 commit / 12", 48, 4000);
   run<128, 0, 4, 2, 12>("TMA + 2 commits / 12", 48, 4000);
