@@ -186,6 +186,17 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUt
 #define QPINN_GEMM_SHARE_EMPTY 1
 #endif
   constexpr bool kShareEmpty = QPINN_GEMM_SHARE_EMPTY && OS == BS;
+#ifndef QPINN_GEMM_GC
+#define QPINN_GEMM_GC 0
+#endif
+  // group commit (experiment): one MMA commit per promotion group (tfull) frees
+  // that group's A operand stages and B stages too; needs nk % kPromote == 0
+  constexpr bool kGC = QPINN_GEMM_GC;
+  const int ngrp_t = (g.K + kBK * kPromote - 1) / (kBK * kPromote);  // groups per tile
+  auto group_of = [&](int64_t jj) -> int64_t {  // promotion group of global k-block jj
+    const int nkk = (g.K + kBK - 1) / kBK;
+    return (jj / nkk) * ngrp_t + (jj % nkk) / kPromote;
+  };
   extern __shared__ unsigned char smem_raw[];
   unsigned char* smem = (unsigned char*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   unsigned char* raw = smem;                        // [RS][16 KB] fp32 A tiles
@@ -275,7 +286,12 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUt
           // (each tcgen05.commit costs tensor-pipe throughput while TMA loads are in
           // flight: scripts/probes/mma_rate.cu, 72 -> 97 cycles per MMA at 2 per k-block)
           uint64_t* freed = kShareEmpty ? op_empty : b_empty;
-          if (j >= BS) GPROF(1, mbar_wait(freed + e, (uint32_t)(((j / BS) - 1) & 1)));
+          if (kGC) {
+            if (j >= BS) {
+              const int64_t gq = group_of(j - BS);
+              mbar_wait(tfull + (int)(gq % NB), (uint32_t)((gq / NB) & 1));
+            }
+          } else if (j >= BS) GPROF(1, mbar_wait(freed + e, (uint32_t)(((j / BS) - 1) & 1)));
           unsigned char* st = bst + e * Cfg::kBStage;
           if (QPINN_ABL_NOB && j >= BS) {
             mbar_arrive(b_full + e);
@@ -326,8 +342,8 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUt
               mma_tf32(d, desc_k_sw128(a_hi + off), desc_k_sw128(b_hi + off), idesc, 1);
             }
           }
-          mma_commit(op_empty + o);
-          if (!kShareEmpty) mma_commit(b_empty + e);
+          if (!kGC) mma_commit(op_empty + o);
+          if (!kGC && !kShareEmpty) mma_commit(b_empty + e);
           if (last) {
             mma_commit(tfull + b);
             ++grp;
@@ -346,7 +362,10 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUt
       for (int kb = 0; kb < nk; ++kb, ++j) {
         const int r = (int)(j % RS), o = (int)(j % OS);
         if (j >= OS) {
-          if (warp == 0) GPROF(5, mbar_wait(op_empty + o, (uint32_t)(((j / OS) - 1) & 1)));
+          if (kGC) {
+            const int64_t gq = group_of(j - OS);
+            mbar_wait(tfull + (int)(gq % NB), (uint32_t)((gq / NB) & 1));
+          } else if (warp == 0) GPROF(5, mbar_wait(op_empty + o, (uint32_t)(((j / OS) - 1) & 1)));
           else mbar_wait(op_empty + o, (uint32_t)(((j / OS) - 1) & 1));
           tc_fence_after();
         }

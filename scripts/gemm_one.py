@@ -31,5 +31,8 @@ for _ in range(reps):
 e1.record()
 torch.cuda.synchronize()
 us = e0.elapsed_time(e1) / reps * 1e3
+idx = torch.randint(0, M, (4096,), device="cuda")
+ref = A[idx].double() @ B.double().T
+err = ((C[idx].double() - ref).abs().max() / ref.abs().max()).item()
 print(f"M={M} N={n} K={K}: {us:.1f} us, A {4 * M * K / us / 1e3:.0f} GB/s, "
-      f"A+C {4 * M * (K + n) / us / 1e3:.0f} GB/s")
+      f"A+C {4 * M * (K + n) / us / 1e3:.0f} GB/s, rel err {err:.2e}")
