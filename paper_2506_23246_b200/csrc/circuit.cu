@@ -205,6 +205,8 @@ int qpinn_circuit_create(int kind, int n, int L, qpinn_circuit** out) {
         cn.push_back({gates[j].w0, gates[j].w1});
         ++j;
       }
+      c->cnot_off.push_back((int)(c->cnot_ct.size() / 2));
+      for (auto& ct : cn) c->cnot_ct.insert(c->cnot_ct.end(), {ct.first, ct.second});
       std::vector<uint16_t> p = cnot_perm(cn, n);
       std::vector<uint16_t> ip(D);
       for (int k = 0; k < D; ++k) ip[p[k]] = (uint16_t)k;
@@ -245,6 +247,7 @@ int qpinn_circuit_create(int kind, int n, int L, qpinn_circuit** out) {
     }
   }
   c->phase_off.push_back((int)(c->pairs.size() / 3));
+  c->cnot_off.push_back((int)(c->cnot_ct.size() / 2));
   c->plan_dump = pd.str();
   const int n_steps = (int)c->steps.size() / 3;
   if (n_steps > kMaxSteps) {

@@ -87,6 +87,9 @@ struct qpinn_circuit {
   // host copies
   std::vector<int> steps, u1, pairs, phase_off;
   std::vector<uint16_t> perm, iperm;
+  // the CNOTs of each fused permutation step, in gate order: perm step k holds
+  // pairs cnot_ct[2 j], cnot_ct[2 j + 1] (control, target) for cnot_off[k] <= j < cnot_off[k + 1]
+  std::vector<int> cnot_ct, cnot_off;
   int n_u1 = 0, n_perm = 0, n_phase = 0;
   int variant = 0;  // 0: specialised kernels when available, 1: generic only
   int device = -1;

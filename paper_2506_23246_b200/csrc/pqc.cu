@@ -725,6 +725,14 @@ int qpinn_pqc_forward(const qpinn_circuit* cc, int dtype, int scale, int64_t row
     double* tot;
     unsigned char* tables;
     big_ws(c, workspace, &partial, &tot, &tables);
+    if (hbm_fwd_supported(c, dtype)) {  // several gates per HBM pass (pqc_global.cu)
+      const size_t off = align_up(big_workspace_bytes(c, dtype), 256);
+      KArgs<float> a{scale, rows, (const float*)act_val, (const float*)act_tan,
+                     (const float*)qparams, (float*)z, (float*)dz, nullptr, maxabs, nullptr,
+                     nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, st, nullptr};
+      return hbm_forward(c, &a, (unsigned char*)workspace + off,
+                         workspace_bytes > off ? workspace_bytes - off : 0);
+    }
     if (!act_tan || !big_fwd_supported(c, dtype)) {  // global-memory forward (pqc_global.cu)
       const size_t off = align_up(big_workspace_bytes(c, dtype), 256);
       unsigned char* gws = (unsigned char*)workspace + off;

@@ -13,6 +13,9 @@
 // fixed order (deterministic), and the embedding gradient follows the oracle
 // (qpinn_oracle.pqc_backward).  Reference: the taped backward of
 // quantum_layer_forward via="gates" (ansatz.py:341-400, tape.py:118-148).
+#include <cstdlib>
+#include <vector>
+
 #include "pqc_layer.h"
 
 namespace qpinn {
@@ -333,37 +336,56 @@ __global__ void gb_embed_final(int n, int B, int chunks, int64_t p0, int64_t R,
 template <typename T>
 __global__ void gb_readout(int n, int chunks, int nstates, const cplx<T>* __restrict__ X,
                            double* __restrict__ rp) {
-  extern __shared__ double ro_red[];  // [4 n][blockDim]
+  // per-thread partial sums, then a fixed warp-shuffle tree and a fixed
+  // cross-warp order (deterministic); the dynamic shared memory is [warps][4 n]
+  extern __shared__ double ro_red[];
   const int64_t D = (int64_t)1 << n;
   const int pb = blockIdx.y;
   const cplx<T>* x = X + (int64_t)pb * 4 * D;
   T acc[4 * 16];
-  for (int j = 0; j < 4 * n; ++j) acc[j] = T(0);
+#pragma unroll
+  for (int j = 0; j < 4 * 16; ++j) acc[j] = T(0);
   const int64_t per = (D + chunks - 1) / chunks;
   const int64_t b0 = blockIdx.x * per, b1 = b0 + per < D ? b0 + per : D;
   for (int64_t b = b0 + threadIdx.x; b < b1; b += blockDim.x) {
     const cplx<T> psi = x[b];
     T v[4];
     v[0] = psi.re * psi.re + psi.im * psi.im;
-    for (int k = 1; k < nstates; ++k) {
-      const cplx<T> d = x[k * D + b];
-      v[k] = T(2) * (psi.re * d.re + psi.im * d.im);
+#pragma unroll
+    for (int k = 1; k < 4; ++k) {
+      if (k < nstates) {
+        const cplx<T> d = x[k * D + b];
+        v[k] = T(2) * (psi.re * d.re + psi.im * d.im);
+      } else {
+        v[k] = T(0);
+      }
     }
-    for (int q = 0; q < n; ++q) {
-      const T sg = ((b >> (n - 1 - q)) & 1) ? T(-1) : T(1);
-      for (int k = 0; k < nstates; ++k) acc[k * n + q] += sg * v[k];
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+      if (q < n) {
+        const bool neg = (b >> (n - 1 - q)) & 1;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) acc[k * 16 + q] += neg ? -v[k] : v[k];
+      }
     }
   }
-  for (int j = 0; j < 4 * n; ++j) ro_red[j * blockDim.x + threadIdx.x] = (double)acc[j];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+#pragma unroll
+  for (int j = 0; j < 4 * 16; ++j) {
+    T v = acc[j];
+    for (int m = 16; m >= 1; m >>= 1) v += __shfl_xor_sync(0xffffffffu, v, m);
+    acc[j] = v;
+  }
+  if (lane == 0)
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      for (int q = 0; q < n; ++q) ro_red[w * 4 * n + k * n + q] = (double)acc[k * 16 + q];
   __syncthreads();
-  for (int s = blockDim.x / 2; s > 0; s >>= 1) {
-    if (threadIdx.x < s)
-      for (int j = 0; j < 4 * n; ++j)
-        ro_red[j * blockDim.x + threadIdx.x] += ro_red[j * blockDim.x + threadIdx.x + s];
-    __syncthreads();
+  for (int j = threadIdx.x; j < 4 * n; j += blockDim.x) {
+    double t = 0.0;
+    for (int i = 0; i < nw; ++i) t += ro_red[i * 4 * n + j];
+    rp[((int64_t)pb * chunks + blockIdx.x) * 4 * n + j] = t;
   }
-  for (int j = threadIdx.x; j < 4 * n; j += blockDim.x)
-    rp[((int64_t)pb * chunks + blockIdx.x) * 4 * n + j] = ro_red[j * blockDim.x];
 }
 
 template <typename T>
@@ -428,7 +450,417 @@ GbLayout gb_layout(const qpinn_circuit* c) {
   return g;
 }
 
+// ---- several gates per HBM pass (forward with tangents, fp32, n >= 13) -------------
+// The one-pass-per-gate forward above streams the [B][4][D] state through HBM once
+// per gate.  Here the basis index is split as b = (s, l): the top h = n - kHbT bits
+// s (wires 0 .. h-1) and the low kHbT bits l.  Two pass kinds each apply a run of
+// gates in one read + write of the state:
+//   SM pass: one CTA per (row, s) holds the 2^kHbT amplitudes of that slice in
+//            shared memory -- gates on low wires, CNOTs whose target is a low wire
+//            (a high control is fixed per slice), phase diagonals;
+//   CS pass: one thread per (row, l) holds the 2^h amplitudes (s, l) in registers --
+//            gates on high wires, CNOTs whose target is a high wire (a low control
+//            is fixed per thread), phase diagonals.
+// The CNOT runs are kept as individual CNOTs (qpinn_circuit::cnot_ct): a CNOT is
+// local to the pass kind of its TARGET wire.  A host scheduler places every op of
+// the fused plan (in gate order) into the earliest pass of its kind that follows
+// every op it does not commute with, so a strongly-entangling layer costs one SM
+// and one CS pass instead of n + 1 gate passes (plus one per CNOT run).
+constexpr int kHbT = 12;  // low bits per SM tile: 2^12 complex = 32 KB of shared memory
+enum { HB_U1 = 0, HB_CNOT = 1, HB_PHASE = 2 };
+enum { HB_SM = 0, HB_CS = 1, HB_ANY = 2 };
+struct HbOp {
+  int type, a, b, idx;  // U1: a = bit, idx = u1 index; CNOT: a = control bit, b = target bit;
+};                      // PHASE: idx = phase step
+struct HbPass {
+  int kind, op0, nops;
+};
+struct HbPlan {
+  std::vector<HbOp> ops;
+  std::vector<HbPass> passes;
+};
+
+HbPlan hb_plan(const qpinn_circuit* c) {
+  const int n = c->n, h = n - kHbT;
+  struct Op {
+    HbOp op;
+    int kind;
+    std::vector<int> wires;
+  };
+  std::vector<Op> seq;
+  const int n_steps = (int)c->steps.size() / 3;
+  for (int i = 0; i < n_steps; ++i) {
+    const int type = c->steps[3 * i], wire = c->steps[3 * i + 1], idx = c->steps[3 * i + 2];
+    if (type == STEP_U1) {
+      seq.push_back({{HB_U1, n - 1 - wire, 0, idx}, wire < h ? HB_CS : HB_SM, {wire}});
+    } else if (type == STEP_PERM) {
+      for (int j = c->cnot_off[idx]; j < c->cnot_off[idx + 1]; ++j) {
+        const int cw = c->cnot_ct[2 * j], tw = c->cnot_ct[2 * j + 1];
+        seq.push_back({{HB_CNOT, n - 1 - cw, n - 1 - tw, 0}, tw < h ? HB_CS : HB_SM, {cw, tw}});
+      }
+    } else {
+      std::vector<int> ws;
+      for (int k = c->phase_off[idx]; k < c->phase_off[idx + 1]; ++k) {
+        ws.push_back(c->pairs[3 * k]);
+        ws.push_back(c->pairs[3 * k + 1]);
+      }
+      seq.push_back({{HB_PHASE, 0, 0, idx}, HB_ANY, ws});
+    }
+  }
+  auto has = [](const std::vector<int>& v, int w) {
+    for (int x : v)
+      if (x == w) return true;
+    return false;
+  };
+  auto commute = [&](const Op& x, const Op& y) {
+    if (x.op.type == HB_PHASE && y.op.type == HB_PHASE) return true;
+    if (x.op.type == HB_PHASE || y.op.type == HB_PHASE) {
+      const Op& ph = x.op.type == HB_PHASE ? x : y;
+      const Op& o = x.op.type == HB_PHASE ? y : x;
+      if (o.op.type == HB_U1) return !has(ph.wires, o.wires[0]);
+      return !has(ph.wires, o.wires[1]);  // a diagonal commutes with CNOT unless it reads the target
+    }
+    if (x.op.type == HB_U1 && y.op.type == HB_U1) return x.wires[0] != y.wires[0];
+    if (x.op.type == HB_U1 || y.op.type == HB_U1) {
+      const Op& u = x.op.type == HB_U1 ? x : y;
+      const Op& cn = x.op.type == HB_U1 ? y : x;
+      return !has(cn.wires, u.wires[0]);
+    }
+    return x.wires[1] != y.wires[0] && x.wires[0] != y.wires[1];  // CNOT, CNOT
+  };
+  std::vector<int> kinds;
+  std::vector<std::vector<int>> members;  // op indices per pass, in gate order
+  for (int i = 0; i < (int)seq.size(); ++i) {
+    int kstar = -1;
+    for (int k = 0; k < (int)members.size(); ++k)
+      for (int j : members[k])
+        if (!commute(seq[j], seq[i])) kstar = k;
+    int k = kstar < 0 ? 0 : kstar;
+    if (seq[i].kind == HB_ANY) {
+      if (members.empty()) {
+        kinds.push_back(HB_SM);
+        members.emplace_back();
+      }
+    } else {
+      while (k < (int)members.size() && kinds[k] != seq[i].kind) ++k;
+      if (k == (int)members.size()) {
+        kinds.push_back(seq[i].kind);
+        members.emplace_back();
+      }
+    }
+    members[k].push_back(i);
+  }
+  HbPlan plan;
+  for (size_t k = 0; k < members.size(); ++k) {
+    plan.passes.push_back({kinds[k], (int)plan.ops.size(), (int)members[k].size()});
+    for (int j : members[k]) plan.ops.push_back(seq[j].op);
+  }
+  return plan;
+}
+
+__device__ __forceinline__ int hb_insert0(int k, int bit) {
+  return ((k >> bit) << (bit + 1)) | (k & ((1 << bit) - 1));
+}
+
+// SM pass: CTA = (row, slice s); ops on the 2^kHbT low-bit amplitudes in shared memory.
+// Runs of up to 3 single-qubit gates on distinct bits are applied together (8
+// amplitudes per work item in registers, one barrier per run), and a run of CNOTs is
+// one gather through the composed index map (one barrier per run).
+template <int G>
+__device__ __forceinline__ void hb_sm_u1_group(cplx<float>* t, const HbOp* op,
+                                               const cplx<float>* __restrict__ U) {
+  constexpr int TS = 1 << kHbT, M = 1 << G;
+  int bits[G], sorted[G];
+  cplx<float> u[G][4];
+#pragma unroll
+  for (int g = 0; g < G; ++g) {
+    bits[g] = op[g].a;
+    sorted[g] = op[g].a;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) u[g][e] = U[4 * op[g].idx + e];
+  }
+#pragma unroll
+  for (int i = 0; i < G; ++i)
+#pragma unroll
+    for (int j = i + 1; j < G; ++j)
+      if (sorted[j] < sorted[i]) {
+        const int x = sorted[i];
+        sorted[i] = sorted[j];
+        sorted[j] = x;
+      }
+  for (int k = threadIdx.x; k < TS / M; k += blockDim.x) {
+    int base = k;
+#pragma unroll
+    for (int g = 0; g < G; ++g) base = hb_insert0(base, sorted[g]);
+    int idx[M];
+    cplx<float> v[M];
+#pragma unroll
+    for (int m = 0; m < M; ++m) {
+      int i = base;
+#pragma unroll
+      for (int g = 0; g < G; ++g)
+        if ((m >> g) & 1) i |= 1 << bits[g];
+      idx[m] = i;
+      v[m] = t[i];
+    }
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+#pragma unroll
+      for (int m = 0; m < M; ++m) {
+        if ((m >> g) & 1) continue;
+        const int m1 = m | (1 << g);
+        const cplx<float> a0 = v[m], a1 = v[m1];
+        v[m] = cmul2(u[g][0], a0, u[g][1], a1);
+        v[m1] = cmul2(u[g][2], a0, u[g][3], a1);
+      }
+    }
+#pragma unroll
+    for (int m = 0; m < M; ++m) t[idx[m]] = v[m];
+  }
+}
+
+#ifndef QPINN_HB_MINB
+#define QPINN_HB_MINB 4
+#endif
+#ifndef QPINN_HB_G
+#define QPINN_HB_G 2
+#endif
+__global__ void __launch_bounds__(256, QPINN_HB_MINB) hb_sm_pass(int n, cplx<float>* __restrict__ X,
+                                                  const HbOp* __restrict__ ops, int nops,
+                                                  const cplx<float>* __restrict__ U,
+                                                  const cplx<float>* __restrict__ ph) {
+  constexpr int TS = 1 << kHbT, PER = TS / 256;
+  __shared__ cplx<float> t[TS];
+  const int h = n - kHbT;
+  const int64_t D = (int64_t)1 << n;
+  const int64_t row = blockIdx.x >> h;
+  const int s = blockIdx.x & ((1 << h) - 1);
+  cplx<float>* x = X + row * D + ((int64_t)s << kHbT);
+  for (int i = threadIdx.x; i < TS; i += blockDim.x) t[i] = x[i];
+  __syncthreads();
+  int o = 0;
+  while (o < nops) {
+    const HbOp op = ops[o];
+    if (op.type == HB_U1) {
+      int g = 1;  // run of single-qubit gates on distinct bits
+      while (g < QPINN_HB_G && o + g < nops && ops[o + g].type == HB_U1) {
+        bool distinct = true;
+        for (int j = 0; j < g; ++j) distinct &= ops[o + j].a != ops[o + g].a;
+        if (!distinct) break;
+        ++g;
+      }
+      if (QPINN_HB_G >= 3 && g == 3) hb_sm_u1_group<3>(t, ops + o, U);
+      else if (QPINN_HB_G >= 2 && g == 2) hb_sm_u1_group<2>(t, ops + o, U);
+      else hb_sm_u1_group<1>(t, ops + o, U);
+      o += g;
+    } else if (op.type == HB_CNOT) {
+      int e = o + 1;  // run of CNOTs: new[i] = old[f(i)], f = C_o o C_o+1 o ... (last first)
+      while (e < nops && ops[e].type == HB_CNOT) ++e;
+      cplx<float> v[PER];
+#pragma unroll
+      for (int r = 0; r < PER; ++r) {
+        const int i = threadIdx.x + r * 256;
+        int j = i;
+        for (int q = e - 1; q >= o; --q) {
+          const HbOp c = ops[q];
+          const int on = c.a >= kHbT ? (s >> (c.a - kHbT)) & 1 : (j >> c.a) & 1;
+          j ^= on << c.b;
+        }
+        v[r] = t[j];
+      }
+      __syncthreads();
+#pragma unroll
+      for (int r = 0; r < PER; ++r) t[threadIdx.x + r * 256] = v[r];
+      o = e;
+    } else {
+      const cplx<float>* ep = ph + (int64_t)op.idx * D + ((int64_t)s << kHbT);
+      for (int i = threadIdx.x; i < TS; i += blockDim.x) t[i] = cmul(t[i], ep[i]);
+      ++o;
+    }
+    __syncthreads();
+  }
+  for (int i = threadIdx.x; i < TS; i += blockDim.x) x[i] = t[i];
+}
+
+// CS pass: thread = (row, low index l); the 2^H amplitudes (s, l) in registers
+template <int H>
+__device__ __forceinline__ void hb_swap_bit(cplx<float> (&v)[1 << H], int rb, int rc) {
+  // swap v[j] <-> v[j | 1 << rb] for j with bit rb clear (and bit rc set when rc >= 0)
+#pragma unroll
+  for (int j = 0; j < (1 << H); ++j) {
+    if (((j >> rb) & 1) == 0 && (rc < 0 || ((j >> rc) & 1))) {
+      const cplx<float> a = v[j];
+      v[j] = v[j | (1 << rb)];
+      v[j | (1 << rb)] = a;
+    }
+  }
+}
+
+template <int H, int RB>
+__device__ __forceinline__ void hb_gate_bit(cplx<float> (&v)[1 << H], cplx<float> u00,
+                                            cplx<float> u01, cplx<float> u10, cplx<float> u11) {
+#pragma unroll
+  for (int j = 0; j < (1 << H); ++j) {
+    if ((j >> RB) & 1) continue;
+    const cplx<float> a = v[j], b = v[j | (1 << RB)];
+    v[j] = cmul2(u00, a, u01, b);
+    v[j | (1 << RB)] = cmul2(u10, a, u11, b);
+  }
+}
+
+template <int H>
+__global__ void __launch_bounds__(256) hb_cs_pass(int n, int64_t rows, cplx<float>* __restrict__ X,
+                                                  const HbOp* __restrict__ ops, int nops,
+                                                  const cplx<float>* __restrict__ U,
+                                                  const cplx<float>* __restrict__ ph) {
+  constexpr int V = 1 << H, TS = 1 << kHbT;
+  const int64_t D = (int64_t)1 << n;
+  for (int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; gid < rows * TS;
+       gid += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t row = gid >> kHbT;
+    const int l = (int)(gid & (TS - 1));
+    cplx<float>* x = X + row * D + l;
+    cplx<float> v[V];
+#pragma unroll
+    for (int j = 0; j < V; ++j) v[j] = x[(int64_t)j << kHbT];
+    for (int o = 0; o < nops; ++o) {
+      const HbOp op = ops[o];
+      if (op.type == HB_U1) {
+        const cplx<float>* u = U + 4 * op.idx;
+        const cplx<float> u00 = u[0], u01 = u[1], u10 = u[2], u11 = u[3];
+        const int rb = op.a - kHbT;
+        if (rb == 0) hb_gate_bit<H, 0>(v, u00, u01, u10, u11);
+        if constexpr (H > 1) if (rb == 1) hb_gate_bit<H, 1>(v, u00, u01, u10, u11);
+        if constexpr (H > 2) if (rb == 2) hb_gate_bit<H, 2>(v, u00, u01, u10, u11);
+        if constexpr (H > 3) if (rb == 3) hb_gate_bit<H, 3>(v, u00, u01, u10, u11);
+      } else if (op.type == HB_CNOT) {
+        const int rb = op.b - kHbT;
+        if (op.a < kHbT) {  // low control: fixed for this thread
+          if ((l >> op.a) & 1) {
+#pragma unroll
+            for (int q = 0; q < H; ++q)
+              if (q == rb) hb_swap_bit<H>(v, q, -1);
+          }
+        } else {
+          const int rc = op.a - kHbT;
+#pragma unroll
+          for (int q = 0; q < H; ++q)
+#pragma unroll
+            for (int r = 0; r < H; ++r)
+              if (q == rb && r == rc) hb_swap_bit<H>(v, q, r);
+        }
+      } else {
+        const cplx<float>* e = ph + (int64_t)op.idx * D + l;
+#pragma unroll
+        for (int j = 0; j < V; ++j) v[j] = cmul(v[j], e[(int64_t)j << kHbT]);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < V; ++j) x[(int64_t)j << kHbT] = v[j];
+  }
+}
+
+struct HbLayout {
+  int B;
+  size_t U, ph, PT, RP, ops, X, total;
+};
+
+HbLayout hb_layout(const qpinn_circuit* c, int64_t B, int nops) {
+  const size_t D = (size_t)1 << c->n, es = sizeof(cplx<float>);
+  HbLayout g{};
+  g.B = (int)B;
+  size_t o = 0;
+  auto take = [&](size_t bytes) {
+    const size_t at = o;
+    o += align_up(bytes, 256);
+    return at;
+  };
+  g.U = take(es * 4 * c->n_u1);
+  g.ph = take(es * D * c->n_phase);
+  g.PT = take(sizeof(float) * 8 * (size_t)B * c->n);
+  g.RP = take(8 * (size_t)B * kGbChunks * 4 * c->n);
+  g.ops = take(sizeof(HbOp) * (size_t)(nops > 0 ? nops : 1));
+  g.X = take(4 * D * (size_t)B * es);
+  g.total = o;
+  return g;
+}
+
+int hb_launch_cs(int h, int n, int64_t rows, cplx<float>* X, const HbOp* ops, int nops,
+                 const cplx<float>* U, const cplx<float>* ph, cudaStream_t st) {
+  const int64_t threads = rows << kHbT;
+  const int grid = (int)((threads + 255) / 256 < (int64_t)num_sms() * 8 ? (threads + 255) / 256
+                                                                       : (int64_t)num_sms() * 8);
+  switch (h) {
+    case 1: hb_cs_pass<1><<<grid, 256, 0, st>>>(n, rows, X, ops, nops, U, ph); break;
+    case 2: hb_cs_pass<2><<<grid, 256, 0, st>>>(n, rows, X, ops, nops, U, ph); break;
+    case 3: hb_cs_pass<3><<<grid, 256, 0, st>>>(n, rows, X, ops, nops, U, ph); break;
+    case 4: hb_cs_pass<4><<<grid, 256, 0, st>>>(n, rows, X, ops, nops, U, ph); break;
+    default: return fail(QPINN_ERR_CAPACITY, "multi-gate HBM pass: 13 <= n <= 16");
+  }
+  QPINN_CUDA_CHECK(cudaGetLastError());
+  return QPINN_OK;
+}
+
 }  // namespace
+
+bool hbm_fwd_supported(const qpinn_circuit* c, int dtype) {
+  if (!c || dtype != QPINN_F32 || c->n <= kHbT || c->n > kHbT + 4) return false;
+  if (getenv("QPINN_PQC_HBM_MULTIGATE") && atoi(getenv("QPINN_PQC_HBM_MULTIGATE")) == 0) return false;
+  return true;
+}
+
+// forward with tangents (or value only), several gates per HBM pass (see hb_plan)
+int hbm_forward(const qpinn_circuit* c, const KArgs<float>* a, unsigned char* ws, size_t bytes) {
+  const PlanDev& p = c->dev;
+  const int n = c->n, h = n - kHbT;
+  const int64_t D = (int64_t)1 << n;
+  const HbPlan plan = hb_plan(c);
+  const int nops = (int)plan.ops.size();
+  // largest batch of points that fits the workspace
+  int64_t B = a->R < 1024 ? a->R : 1024;
+  while (B > 1 && hb_layout(c, B, nops).total > bytes) B = B * 3 / 4;
+  const HbLayout g = hb_layout(c, B < 1 ? 1 : B, nops);
+  if (bytes < g.total) return fail(QPINN_ERR_CONFIG, "multi-gate HBM PQC: workspace too small");
+  cudaStream_t st = a->stream;
+  auto* U = (cplx<float>*)(ws + g.U);
+  auto* ph = (cplx<float>*)(ws + g.ph);
+  auto* PT = (float*)(ws + g.PT);
+  auto* RP = (double*)(ws + g.RP);
+  auto* dops = (HbOp*)(ws + g.ops);
+  auto* X = (cplx<float>*)(ws + g.X);
+  QPINN_CUDA_CHECK(cudaMemcpyAsync(dops, plan.ops.data(), sizeof(HbOp) * nops,
+                                   cudaMemcpyHostToDevice, st));
+  const int ns = a->tan ? 4 : 1;
+  const int ro_smem = 4 * n * 4 * (int)sizeof(double);  // [4 warps][4 n]
+  QPINN_CUDA_CHECK(cudaFuncSetAttribute(gb_readout<float>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, ro_smem));
+  gb_tables<float><<<64, 256, 0, st>>>(p, a->qp, U, ph);
+  if (a->maxabs)
+    gb_maxabs<float><<<gb_blocks(a->R * n), kGbThreads, 0, st>>>(a->R * n, a->act, a->maxabs);
+  for (int64_t p0 = 0; p0 < a->R; p0 += g.B) {
+    const int Bc = (int)(a->R - p0 < g.B ? a->R - p0 : g.B);
+    const int64_t rows = (int64_t)Bc * 4;
+    gb_point<float><<<gb_blocks(Bc * n), kGbThreads, 0, st>>>(n, a->scale, a->R, p0, Bc, a->act,
+                                                              a->tan, PT);
+    gb_embed<float><<<gb_blocks(Bc * D), kGbThreads, 0, st>>>(n, Bc, ns, PT, X);
+    for (const HbPass& ps : plan.passes) {
+      if (ps.kind == HB_SM) {
+        hb_sm_pass<<<(unsigned)(rows << h), 256, 0, st>>>(n, X, dops + ps.op0, ps.nops, U, ph);
+        QPINN_CUDA_CHECK(cudaGetLastError());
+      } else if (int rc = hb_launch_cs(h, n, rows, X, dops + ps.op0, ps.nops, U, ph, st)) {
+        return rc;
+      }
+    }
+    gb_readout<float><<<dim3(kGbChunks, Bc), 128, ro_smem, st>>>(n, kGbChunks, ns, X, RP);
+    gb_readout_final<float><<<gb_blocks(Bc * n), kGbThreads, 0, st>>>(n, Bc, kGbChunks, ns, p0,
+                                                                      a->R, RP, a->z, a->dz);
+    QPINN_CUDA_CHECK(cudaGetLastError());
+  }
+  return QPINN_OK;
+}
+
+// number of HBM passes per forward of the multi-gate path (diagnostics)
+int hbm_forward_passes(const qpinn_circuit* c) { return (int)hb_plan(c).passes.size(); }
 
 size_t global_adjoint_workspace_bytes(const qpinn_circuit* c, int dtype) {
   return dtype == QPINN_F64 ? gb_layout<double>(c).total : gb_layout<float>(c).total;
@@ -529,7 +961,7 @@ int global_forward(const qpinn_circuit* c, const KArgs<T>* a, unsigned char* ws,
   cplx<T>* TMP = (cplx<T>*)(ws + g.TMP);
   double* RP = (double*)(ws + g.EG);
   const int ns = a->tan ? 4 : 1;
-  const int ro_smem = 4 * n * 128 * (int)sizeof(double);
+  const int ro_smem = 4 * n * 4 * (int)sizeof(double);  // [4 warps][4 n]
   QPINN_CUDA_CHECK(cudaFuncSetAttribute(gb_readout<T>,
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, ro_smem));
   gb_tables<T><<<64, 256, 0, st>>>(p, a->qp, U, ph);

@@ -65,6 +65,10 @@ template <typename T>
 int global_forward(const qpinn_circuit* c, const KArgs<T>* a, unsigned char* ws, size_t bytes);
 // whether a cluster forward kernel with tangents exists for this circuit
 bool big_fwd_supported(const qpinn_circuit* c, int dtype);
+// forward with several gates per HBM pass (pqc_global.cu): fp32, 13 <= n <= 16
+bool hbm_fwd_supported(const qpinn_circuit* c, int dtype);
+int hbm_forward(const qpinn_circuit* c, const KArgs<float>* a, unsigned char* ws, size_t bytes);
+int hbm_forward_passes(const qpinn_circuit* c);
 // transfer-matrix K1 / K2 on the tensor cores (pqc_transfer.cu)
 bool transfer_supported(const qpinn_circuit* c, int dtype);
 size_t transfer_workspace_bytes(const qpinn_circuit* c, int64_t R);
