@@ -13,6 +13,7 @@
 // fixed order (deterministic), and the embedding gradient follows the oracle
 // (qpinn_oracle.pqc_backward).  Reference: the taped backward of
 // quantum_layer_forward via="gates" (ansatz.py:341-400, tape.py:118-148).
+#include <cstdio>
 #include <cstdlib>
 #include <vector>
 
@@ -478,7 +479,9 @@ struct HbPass {
 struct HbPlan {
   std::vector<HbOp> ops;
   std::vector<HbPass> passes;
+  std::vector<int> luts;  // per CNOT run of an SM pass: [64 low | 64 high | 16 slice] index maps
 };
+constexpr int kHbLut = 64 + 64 + 16;
 
 HbPlan hb_plan(const qpinn_circuit* c) {
   const int n = c->n, h = n - kHbT;
@@ -555,6 +558,46 @@ HbPlan hb_plan(const qpinn_circuit* c) {
     plan.passes.push_back({kinds[k], (int)plan.ops.size(), (int)members[k].size()});
     for (int j : members[k]) plan.ops.push_back(seq[j].op);
   }
+  // A run of CNOTs in an SM pass is one GF(2)-linear index map on the 12 low bits
+  // (plus the slice bits as fixed controls): new[i] = old[f(i, s)] with
+  // f = g_first o ... o g_last, g(j) = j ^ (bit_c(j) << t).  f is tabulated as
+  // f(i, s) = lo[i & 63] ^ hi[i >> 6] ^ sl[s]; the run head's idx is its table
+  // offset and b its length (all of the run's CNOTs are then skipped).
+  for (const HbPass& ps : plan.passes) {
+    if (ps.kind != HB_SM) continue;
+    int o = ps.op0;
+    const int end = ps.op0 + ps.nops;
+    while (o < end) {
+      if (plan.ops[o].type != HB_CNOT) {
+        ++o;
+        continue;
+      }
+      int e = o + 1;
+      while (e < end && plan.ops[e].type == HB_CNOT) ++e;
+      auto f = [&](int i, int sl) {  // the run's map on a combined index
+        int j = i;
+        for (int q = e - 1; q >= o; --q) {
+          const HbOp& c = plan.ops[q];
+          const int on = c.a >= kHbT ? (sl >> (c.a - kHbT)) & 1 : (j >> c.a) & 1;
+          j ^= on << c.b;
+        }
+        return j;
+      };
+      const int off = (int)plan.luts.size();
+      plan.luts.resize(off + kHbLut, 0);
+      int* lo = plan.luts.data() + off;
+      int* hi = lo + 64;
+      int* sl = hi + 64;
+      for (int v = 0; v < 64; ++v) {
+        lo[v] = f(v, 0);
+        hi[v] = f(v << 6, 0);
+      }
+      for (int v = 0; v < 16; ++v) sl[v] = f(0, v);
+      plan.ops[o].idx = off;
+      plan.ops[o].b = plan.ops[o].b | ((e - o) << 8);  // run length rides in b's upper bits
+      o = e;
+    }
+  }
   return plan;
 }
 
@@ -627,6 +670,7 @@ __device__ __forceinline__ void hb_sm_u1_group(cplx<float>* t, const HbOp* op,
 #endif
 __global__ void __launch_bounds__(256, QPINN_HB_MINB) hb_sm_pass(int n, cplx<float>* __restrict__ X,
                                                   const HbOp* __restrict__ ops, int nops,
+                                                  const int* __restrict__ luts,
                                                   const cplx<float>* __restrict__ U,
                                                   const cplx<float>* __restrict__ ph) {
   constexpr int TS = 1 << kHbT, PER = TS / 256;
@@ -636,7 +680,13 @@ __global__ void __launch_bounds__(256, QPINN_HB_MINB) hb_sm_pass(int n, cplx<flo
   const int64_t row = blockIdx.x >> h;
   const int s = blockIdx.x & ((1 << h) - 1);
   cplx<float>* x = X + row * D + ((int64_t)s << kHbT);
-  for (int i = threadIdx.x; i < TS; i += blockDim.x) t[i] = x[i];
+  {  // all of the thread's loads in flight before any shared-memory store
+    cplx<float> r[PER];
+#pragma unroll
+    for (int j = 0; j < PER; ++j) r[j] = x[threadIdx.x + 256 * j];
+#pragma unroll
+    for (int j = 0; j < PER; ++j) t[threadIdx.x + 256 * j] = r[j];
+  }
   __syncthreads();
   int o = 0;
   while (o < nops) {
@@ -654,32 +704,32 @@ __global__ void __launch_bounds__(256, QPINN_HB_MINB) hb_sm_pass(int n, cplx<flo
       else hb_sm_u1_group<1>(t, ops + o, U);
       o += g;
     } else if (op.type == HB_CNOT) {
-      int e = o + 1;  // run of CNOTs: new[i] = old[f(i)], f = C_o o C_o+1 o ... (last first)
-      while (e < nops && ops[e].type == HB_CNOT) ++e;
+      // a run of CNOTs: new[i] = old[f(i, s)] through the run's tabulated index map
+      const int* lut = luts + op.idx;
+      const int fs = lut[128 + s];
       cplx<float> v[PER];
 #pragma unroll
       for (int r = 0; r < PER; ++r) {
         const int i = threadIdx.x + r * 256;
-        int j = i;
-        for (int q = e - 1; q >= o; --q) {
-          const HbOp c = ops[q];
-          const int on = c.a >= kHbT ? (s >> (c.a - kHbT)) & 1 : (j >> c.a) & 1;
-          j ^= on << c.b;
-        }
-        v[r] = t[j];
+        v[r] = t[__ldg(lut + (i & 63)) ^ __ldg(lut + 64 + (i >> 6)) ^ fs];
       }
       __syncthreads();
 #pragma unroll
       for (int r = 0; r < PER; ++r) t[threadIdx.x + r * 256] = v[r];
-      o = e;
+      o += op.b >> 8;
     } else {
       const cplx<float>* ep = ph + (int64_t)op.idx * D + ((int64_t)s << kHbT);
-      for (int i = threadIdx.x; i < TS; i += blockDim.x) t[i] = cmul(t[i], ep[i]);
+      cplx<float> e[PER];
+#pragma unroll
+      for (int j = 0; j < PER; ++j) e[j] = ep[threadIdx.x + 256 * j];
+#pragma unroll
+      for (int j = 0; j < PER; ++j) t[threadIdx.x + 256 * j] = cmul(t[threadIdx.x + 256 * j], e[j]);
       ++o;
     }
     __syncthreads();
   }
-  for (int i = threadIdx.x; i < TS; i += blockDim.x) x[i] = t[i];
+#pragma unroll
+  for (int j = 0; j < PER; ++j) x[threadIdx.x + 256 * j] = t[threadIdx.x + 256 * j];
 }
 
 // CS pass: thread = (row, low index l); the 2^H amplitudes (s, l) in registers
@@ -765,7 +815,7 @@ struct HbLayout {
   size_t U, ph, PT, RP, ops, X, total;
 };
 
-HbLayout hb_layout(const qpinn_circuit* c, int64_t B, int nops) {
+HbLayout hb_layout(const qpinn_circuit* c, int64_t B, int nops, int nluts) {
   const size_t D = (size_t)1 << c->n, es = sizeof(cplx<float>);
   HbLayout g{};
   g.B = (int)B;
@@ -779,7 +829,7 @@ HbLayout hb_layout(const qpinn_circuit* c, int64_t B, int nops) {
   g.ph = take(es * D * c->n_phase);
   g.PT = take(sizeof(float) * 8 * (size_t)B * c->n);
   g.RP = take(8 * (size_t)B * kGbChunks * 4 * c->n);
-  g.ops = take(sizeof(HbOp) * (size_t)(nops > 0 ? nops : 1));
+  g.ops = take(sizeof(HbOp) * (size_t)(nops > 0 ? nops : 1) + sizeof(int) * (size_t)nluts);
   g.X = take(4 * D * (size_t)B * es);
   g.total = o;
   return g;
@@ -816,10 +866,17 @@ int hbm_forward(const qpinn_circuit* c, const KArgs<float>* a, unsigned char* ws
   const int64_t D = (int64_t)1 << n;
   const HbPlan plan = hb_plan(c);
   const int nops = (int)plan.ops.size();
+  if (getenv("QPINN_VERBOSE")) {
+    fprintf(stderr, "[qpinn] multi-gate HBM forward: n = %d, L = %d, %d ops in %d passes:", n,
+            c->L, nops, (int)plan.passes.size());
+    for (const HbPass& ps : plan.passes) fprintf(stderr, " %s%d", ps.kind == HB_SM ? "S" : "C", ps.nops);
+    fprintf(stderr, "\n");
+  }
   // largest batch of points that fits the workspace
   int64_t B = a->R < 1024 ? a->R : 1024;
-  while (B > 1 && hb_layout(c, B, nops).total > bytes) B = B * 3 / 4;
-  const HbLayout g = hb_layout(c, B < 1 ? 1 : B, nops);
+  const int nluts = (int)plan.luts.size();
+  while (B > 1 && hb_layout(c, B, nops, nluts).total > bytes) B = B * 3 / 4;
+  const HbLayout g = hb_layout(c, B < 1 ? 1 : B, nops, nluts);
   if (bytes < g.total) return fail(QPINN_ERR_CONFIG, "multi-gate HBM PQC: workspace too small");
   cudaStream_t st = a->stream;
   auto* U = (cplx<float>*)(ws + g.U);
@@ -828,8 +885,12 @@ int hbm_forward(const qpinn_circuit* c, const KArgs<float>* a, unsigned char* ws
   auto* RP = (double*)(ws + g.RP);
   auto* dops = (HbOp*)(ws + g.ops);
   auto* X = (cplx<float>*)(ws + g.X);
+  auto* dluts = (int*)(dops + nops);
   QPINN_CUDA_CHECK(cudaMemcpyAsync(dops, plan.ops.data(), sizeof(HbOp) * nops,
                                    cudaMemcpyHostToDevice, st));
+  if (nluts)
+    QPINN_CUDA_CHECK(cudaMemcpyAsync(dluts, plan.luts.data(), sizeof(int) * nluts,
+                                     cudaMemcpyHostToDevice, st));
   const int ns = a->tan ? 4 : 1;
   const int ro_smem = 4 * n * 4 * (int)sizeof(double);  // [4 warps][4 n]
   QPINN_CUDA_CHECK(cudaFuncSetAttribute(gb_readout<float>,
@@ -845,7 +906,8 @@ int hbm_forward(const qpinn_circuit* c, const KArgs<float>* a, unsigned char* ws
     gb_embed<float><<<gb_blocks(Bc * D), kGbThreads, 0, st>>>(n, Bc, ns, PT, X);
     for (const HbPass& ps : plan.passes) {
       if (ps.kind == HB_SM) {
-        hb_sm_pass<<<(unsigned)(rows << h), 256, 0, st>>>(n, X, dops + ps.op0, ps.nops, U, ph);
+        hb_sm_pass<<<(unsigned)(rows << h), 256, 0, st>>>(n, X, dops + ps.op0, ps.nops, dluts, U,
+                                                          ph);
         QPINN_CUDA_CHECK(cudaGetLastError());
       } else if (int rc = hb_launch_cs(h, n, rows, X, dops + ps.op0, ps.nops, U, ph, st)) {
         return rc;
@@ -863,7 +925,15 @@ int hbm_forward(const qpinn_circuit* c, const KArgs<float>* a, unsigned char* ws
 int hbm_forward_passes(const qpinn_circuit* c) { return (int)hb_plan(c).passes.size(); }
 
 size_t global_adjoint_workspace_bytes(const qpinn_circuit* c, int dtype) {
-  return dtype == QPINN_F64 ? gb_layout<double>(c).total : gb_layout<float>(c).total;
+  if (dtype == QPINN_F64) return gb_layout<double>(c).total;
+  // the multi-gate forward reuses this region with batches of ~256 MB of state
+  // (1024 points at n = 13), so few launches carry the batch loop
+  const size_t g = gb_layout<float>(c).total;
+  if (!hbm_fwd_supported(c, dtype)) return g;
+  const int64_t B = ((int64_t)256 << 20) / (4 * ((int64_t)8 << c->n));
+  const HbPlan plan = hb_plan(c);
+  const size_t h = hb_layout(c, B < 1 ? 1 : B, (int)plan.ops.size(), (int)plan.luts.size()).total;
+  return h > g ? h : g;
 }
 
 template <typename T>
