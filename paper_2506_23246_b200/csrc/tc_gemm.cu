@@ -1118,21 +1118,24 @@ wgrad_kernel(const __grid_constant__ CUtensorMap mX, const __grid_constant__ CUt
 // dW = sum over chunks of the partial tiles, in chunk order (float64 sum)
 // dW = sum over the chunks of the partial tiles, in a fixed order: block = 32
 // entries x 8 chunk groups (group g sums chunks g, g + 8, ...), then the groups in order
-__global__ void __launch_bounds__(256) wgrad_reduce(int n_kc, int64_t n,
-                                                    const float* __restrict__ partial,
-                                                    float* __restrict__ dW) {
-  __shared__ double red[8][33];
+// 32 chunk groups per 32 entries (1024 threads): every thread has at most a few
+// partials to load, so the launch is not latency-bound on a serial load chain
+__global__ void __launch_bounds__(1024) wgrad_reduce(int n_kc, int64_t n,
+                                                     const float* __restrict__ partial,
+                                                     float* __restrict__ dW) {
+  __shared__ double red[32][33];
   const int c = threadIdx.x & 31, grp = threadIdx.x >> 5;
   const int64_t i = (int64_t)blockIdx.x * 32 + c;
   double s = 0.0;
   if (i < n)
-    for (int k = grp; k < n_kc; k += 8) s += (double)partial[(int64_t)k * n + i];
+#pragma unroll 4
+    for (int k = grp; k < n_kc; k += 32) s += (double)partial[(int64_t)k * n + i];
   red[grp][c] = s;
   __syncthreads();
   if (grp == 0 && i < n) {
     double v = 0.0;
 #pragma unroll
-    for (int g = 0; g < 8; ++g) v += red[g][c];
+    for (int g = 0; g < 32; ++g) v += red[g][c];
     dW[i] = (float)v;
   }
 }
@@ -1399,7 +1402,7 @@ int wgrad(int64_t rows, int Kin, int Nout, const float* X, int64_t ldx, const fl
   wgrad_kernel<<<grid, kThreadsW, kWSmem, st>>>(mX, mG, a);
   QPINN_CUDA_CHECK(cudaGetLastError());
   const int64_t n = (int64_t)Kin * Nout;
-  wgrad_reduce<<<(int)((n + 31) / 32), 256, 0, st>>>(a.n_kc, n, a.partial, dW);
+  wgrad_reduce<<<(int)((n + 31) / 32), 1024, 0, st>>>(a.n_kc, n, a.partial, dW);
   QPINN_CUDA_CHECK(cudaGetLastError());
   return QPINN_OK;
 }
