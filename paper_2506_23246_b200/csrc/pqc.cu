@@ -821,6 +821,15 @@ int qpinn_pqc_backward(const qpinn_circuit* cc, int dtype, int scale, int64_t ro
     double* bt;
     unsigned char* btab;
     big_ws(c, workspace, &bp, &bt, &btab);
+    if (hbm_bwd_supported(c, dtype)) {  // several gates per HBM pass (pqc_global.cu)
+      const size_t off = align_up(big_workspace_bytes(c, dtype), 256);
+      KArgs<float> a{scale, rows, (const float*)act_val, (const float*)act_tan,
+                     (const float*)qparams, nullptr, nullptr, nullptr, nullptr,
+                     (const float*)g_z, (const float*)g_dz, (float*)g_act_val,
+                     (float*)g_act_tan, (float*)g_qparams, nullptr, nullptr, st, nullptr};
+      return hbm_backward(c, &a, (unsigned char*)workspace + off,
+                          workspace_bytes > off ? workspace_bytes - off : 0);
+    }
     if (!big_bwd_supported(c, dtype)) {  // HBM regime (pqc_global.cu)
       const size_t off = align_up(big_workspace_bytes(c, dtype), 256);
       unsigned char* gws = (unsigned char*)workspace + off;

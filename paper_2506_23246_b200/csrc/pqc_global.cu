@@ -13,6 +13,7 @@
 // fixed order (deterministic), and the embedding gradient follows the oracle
 // (qpinn_oracle.pqc_backward).  Reference: the taped backward of
 // quantum_layer_forward via="gates" (ansatz.py:341-400, tape.py:118-148).
+#include <algorithm>
 #include <cstdio>
 #include <cstdlib>
 #include <vector>
@@ -263,48 +264,68 @@ template <typename T>
 __global__ void gb_embed_grad(int n, int chunks, const T* __restrict__ PT,
                               const cplx<T>* __restrict__ PHI, const cplx<T>* __restrict__ A,
                               double* __restrict__ egp) {
-  extern __shared__ double eg_red[];  // [4 n][blockDim]
+  // per-thread partial sums, a fixed warp-shuffle tree and a fixed cross-warp
+  // order (deterministic); dynamic shared memory [warps][4 n]
+  extern __shared__ double eg_red[];
   const int64_t D = (int64_t)1 << n;
   const int pb = blockIdx.y;
   const T* pt = PT + (int64_t)pb * n * 8;
   const cplx<T>* phi = PHI + (int64_t)pb * 4 * D;  // state 0 of the re-embedded batch
   const cplx<T>* ab = A + (int64_t)pb * 4 * D;
   T acc[4 * 16];
-  for (int j = 0; j < 4 * n; ++j) acc[j] = T(0);
+#pragma unroll
+  for (int j = 0; j < 4 * 16; ++j) acc[j] = T(0);
   const int64_t per = (D + chunks - 1) / chunks;
   const int64_t b0 = blockIdx.x * per, b1 = b0 + per < D ? b0 + per : D;
   for (int64_t b = b0 + threadIdx.x; b < b1; b += blockDim.x) {
     const cplx<T> phib = ab[b];
     cplx<T> eta = {T(-0.5) * phib.im, T(0.5) * phib.re};  // (i/2) phibar
-    for (int q = 0; q < n; ++q) {
-      const int64_t f = b ^ ((int64_t)1 << (n - 1 - q));
-      for (int k = 0; k < 3; ++k) {
-        const cplx<T> m = ab[(k + 1) * D + f];
-        const T w = T(0.25) * pt[q * 8 + 4 + k];
-        eta.re -= w * m.re;
-        eta.im -= w * m.im;
+    cplx<T> mb[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) mb[k] = ab[(k + 1) * D + b];
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+      if (q < n) {
+        const int64_t f = b ^ ((int64_t)1 << (n - 1 - q));
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+          const cplx<T> m = ab[(k + 1) * D + f];
+          const T wk = T(0.25) * __ldg(pt + q * 8 + 4 + k);
+          eta.re -= wk * m.re;
+          eta.im -= wk * m.im;
+        }
       }
     }
-    for (int q = 0; q < n; ++q) {
-      const cplx<T> y = phi[b ^ ((int64_t)1 << (n - 1 - q))];
-      acc[q] += eta.re * y.re + eta.im * y.im;  // Re(conj(eta) y)
-      for (int k = 0; k < 3; ++k) {
-        const cplx<T> m = ab[(k + 1) * D + b];
-        // (i/2) mu = (-mu.im/2, mu.re/2); Re(conj(that) y)
-        acc[n + k * n + q] += T(-0.5) * m.im * y.re + T(0.5) * m.re * y.im;
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+      if (q < n) {
+        const cplx<T> y = phi[b ^ ((int64_t)1 << (n - 1 - q))];
+        acc[q] += eta.re * y.re + eta.im * y.im;  // Re(conj(eta) y)
+#pragma unroll
+        for (int k = 0; k < 3; ++k)  // (i/2) mu = (-mu.im/2, mu.re/2); Re(conj(that) y)
+          acc[16 + k * 16 + q] += T(-0.5) * mb[k].im * y.re + T(0.5) * mb[k].re * y.im;
       }
     }
   }
-  for (int j = 0; j < 4 * n; ++j) eg_red[j * blockDim.x + threadIdx.x] = (double)acc[j];
+  const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+#pragma unroll
+  for (int j = 0; j < 4 * 16; ++j) {
+    T v = acc[j];
+    for (int m = 16; m >= 1; m >>= 1) v += __shfl_xor_sync(0xffffffffu, v, m);
+    acc[j] = v;
+  }
+  if (lane == 0)
+#pragma unroll
+    for (int g = 0; g < 4; ++g)
+#pragma unroll
+      for (int q = 0; q < 16; ++q)
+        if (q < n) eg_red[wp * 4 * n + g * n + q] = (double)acc[g * 16 + q];
   __syncthreads();
-  for (int s = blockDim.x / 2; s > 0; s >>= 1) {
-    if (threadIdx.x < s)
-      for (int j = 0; j < 4 * n; ++j)
-        eg_red[j * blockDim.x + threadIdx.x] += eg_red[j * blockDim.x + threadIdx.x + s];
-    __syncthreads();
+  for (int j = threadIdx.x; j < 4 * n; j += blockDim.x) {
+    double t = 0.0;
+    for (int i = 0; i < nw; ++i) t += eg_red[i * 4 * n + j];
+    egp[((int64_t)pb * chunks + blockIdx.x) * 4 * n + j] = t;
   }
-  for (int j = threadIdx.x; j < 4 * n; j += blockDim.x)
-    egp[((int64_t)pb * chunks + blockIdx.x) * 4 * n + j] = eg_red[j * blockDim.x];
 }
 
 template <typename T>
@@ -380,7 +401,9 @@ __global__ void gb_readout(int n, int chunks, int nstates, const cplx<T>* __rest
   if (lane == 0)
 #pragma unroll
     for (int k = 0; k < 4; ++k)
-      for (int q = 0; q < n; ++q) ro_red[w * 4 * n + k * n + q] = (double)acc[k * 16 + q];
+#pragma unroll
+      for (int q = 0; q < 16; ++q)
+        if (q < n) ro_red[w * 4 * n + k * n + q] = (double)acc[k * 16 + q];
   __syncthreads();
   for (int j = threadIdx.x; j < 4 * n; j += blockDim.x) {
     double t = 0.0;
@@ -451,11 +474,11 @@ GbLayout gb_layout(const qpinn_circuit* c) {
   return g;
 }
 
-// ---- several gates per HBM pass (forward with tangents, fp32, n >= 13) -------------
-// The one-pass-per-gate forward above streams the [B][4][D] state through HBM once
-// per gate.  Here the basis index is split as b = (s, l): the top h = n - kHbT bits
-// s (wires 0 .. h-1) and the low kHbT bits l.  Two pass kinds each apply a run of
-// gates in one read + write of the state:
+// ---- several gates per HBM pass (fp32, 13 <= n <= 16) --------------------------------
+// The one-pass-per-gate kernels above stream the [B][4][D] states through HBM once per
+// gate.  Here the basis index is split as b = (s, l): the top h = n - kHbT bits s
+// (wires 0 .. h-1) and the low kHbT bits l.  Two pass kinds each apply a run of ops in
+// one read + write of the state:
 //   SM pass: one CTA per (row, s) holds the 2^kHbT amplitudes of that slice in
 //            shared memory -- gates on low wires, CNOTs whose target is a low wire
 //            (a high control is fixed per slice), phase diagonals;
@@ -463,18 +486,37 @@ GbLayout gb_layout(const qpinn_circuit* c) {
 //            gates on high wires, CNOTs whose target is a high wire (a low control
 //            is fixed per thread), phase diagonals.
 // The CNOT runs are kept as individual CNOTs (qpinn_circuit::cnot_ct): a CNOT is
-// local to the pass kind of its TARGET wire.  A host scheduler places every op of
-// the fused plan (in gate order) into the earliest pass of its kind that follows
-// every op it does not commute with, so a strongly-entangling layer costs one SM
-// and one CS pass instead of n + 1 gate passes (plus one per CNOT run).
+// local to the pass kind of its TARGET wire.  A host scheduler places every op (in
+// circuit order) into the earliest pass of its kind that follows every op it does not
+// commute with, so a strongly-entangling layer costs one SM and one CS pass instead
+// of n + 1 gate passes (plus one per CNOT run).
+//
+// The adjoint (hbm_backward) uses the same passes: a forward that checkpoints the
+// states after every layer's single-qubit gates (a copy after the segment that ends
+// there), the seeds, then a reverse op sequence per layer l = L-1 .. 0:
+//   entangler(l)^dagger (CNOTs in reverse order | the conjugate phase),
+//   OUTER_q: the post-gate outer product M'_q = sum conj(abar) x_l of every wire q
+//            from the boundary adjoint and checkpoint (gates of a layer commute, so
+//            each is the layer's last, as the layer kernels' K2),
+//   U_q^dagger for every wire q,
+// scheduled like the forward: OUTER ops commute only with each other, so a layer
+// costs about two passes.  OUTER partials are reduced per CTA and then across CTAs
+// in a fixed order (deterministic).
 constexpr int kHbT = 12;  // low bits per SM tile: 2^12 complex = 32 KB of shared memory
-enum { HB_U1 = 0, HB_CNOT = 1, HB_PHASE = 2 };
+enum { HB_U1 = 0, HB_CNOT = 1, HB_PHASE = 2, HB_OUTER = 3 };
 enum { HB_SM = 0, HB_CS = 1, HB_ANY = 2 };
 struct HbOp {
-  int type, a, b, idx;  // U1: a = bit, idx = u1 index; CNOT: a = control bit, b = target bit;
-};                      // PHASE: idx = phase step
+  // U1: a = bit, b = dagger, idx = u1 index;  CNOT: a = control bit, b = target bit
+  // (| run length << 8 at an SM run head, whose idx is then its table offset);
+  // PHASE: b = conjugate, idx = phase step;  OUTER: a = bit, idx = u1 index (acc slot)
+  int type, a, b, idx;
+};
 struct HbPass {
   int kind, op0, nops;
+  int ck;         // forward with checkpoints: copy the state to checkpoint ck after this pass
+  int layer;      // OUTER passes: the checkpoint layer they read (-1: none)
+  int phase_grad; // reverse: the phase-step gradient to take before this pass (-1: none)
+  int n_outer;    // OUTER ops in this pass
 };
 struct HbPlan {
   std::vector<HbOp> ops;
@@ -483,86 +525,90 @@ struct HbPlan {
 };
 constexpr int kHbLut = 64 + 64 + 16;
 
-HbPlan hb_plan(const qpinn_circuit* c) {
-  const int n = c->n, h = n - kHbT;
-  struct Op {
-    HbOp op;
-    int kind;
-    std::vector<int> wires;
-  };
-  std::vector<Op> seq;
-  const int n_steps = (int)c->steps.size() / 3;
-  for (int i = 0; i < n_steps; ++i) {
-    const int type = c->steps[3 * i], wire = c->steps[3 * i + 1], idx = c->steps[3 * i + 2];
-    if (type == STEP_U1) {
-      seq.push_back({{HB_U1, n - 1 - wire, 0, idx}, wire < h ? HB_CS : HB_SM, {wire}});
-    } else if (type == STEP_PERM) {
-      for (int j = c->cnot_off[idx]; j < c->cnot_off[idx + 1]; ++j) {
-        const int cw = c->cnot_ct[2 * j], tw = c->cnot_ct[2 * j + 1];
-        seq.push_back({{HB_CNOT, n - 1 - cw, n - 1 - tw, 0}, tw < h ? HB_CS : HB_SM, {cw, tw}});
-      }
-    } else {
-      std::vector<int> ws;
-      for (int k = c->phase_off[idx]; k < c->phase_off[idx + 1]; ++k) {
-        ws.push_back(c->pairs[3 * k]);
-        ws.push_back(c->pairs[3 * k + 1]);
-      }
-      seq.push_back({{HB_PHASE, 0, 0, idx}, HB_ANY, ws});
-    }
-  }
+struct HbSOp {  // an op being scheduled
+  HbOp op;
+  int kind;
+  std::vector<int> wires;
+  int layer;
+  bool barrier;  // must start a fresh pass (a phase step whose gradient is taken first)
+};
+
+bool hb_commute(const HbSOp& x, const HbSOp& y) {
   auto has = [](const std::vector<int>& v, int w) {
-    for (int x : v)
-      if (x == w) return true;
+    for (int e : v)
+      if (e == w) return true;
     return false;
   };
-  auto commute = [&](const Op& x, const Op& y) {
-    if (x.op.type == HB_PHASE && y.op.type == HB_PHASE) return true;
-    if (x.op.type == HB_PHASE || y.op.type == HB_PHASE) {
-      const Op& ph = x.op.type == HB_PHASE ? x : y;
-      const Op& o = x.op.type == HB_PHASE ? y : x;
-      if (o.op.type == HB_U1) return !has(ph.wires, o.wires[0]);
-      return !has(ph.wires, o.wires[1]);  // a diagonal commutes with CNOT unless it reads the target
-    }
-    if (x.op.type == HB_U1 && y.op.type == HB_U1) return x.wires[0] != y.wires[0];
-    if (x.op.type == HB_U1 || y.op.type == HB_U1) {
-      const Op& u = x.op.type == HB_U1 ? x : y;
-      const Op& cn = x.op.type == HB_U1 ? y : x;
-      return !has(cn.wires, u.wires[0]);
-    }
-    return x.wires[1] != y.wires[0] && x.wires[0] != y.wires[1];  // CNOT, CNOT
-  };
+  if (x.op.type == HB_OUTER || y.op.type == HB_OUTER)
+    return x.op.type == HB_OUTER && y.op.type == HB_OUTER;  // reads the adjoint as it is
+  if (x.op.type == HB_PHASE && y.op.type == HB_PHASE) return true;
+  if (x.op.type == HB_PHASE || y.op.type == HB_PHASE) {
+    const HbSOp& ph = x.op.type == HB_PHASE ? x : y;
+    const HbSOp& o = x.op.type == HB_PHASE ? y : x;
+    if (o.op.type == HB_U1) return !has(ph.wires, o.wires[0]);
+    return !has(ph.wires, o.wires[1]);  // a diagonal commutes with CNOT unless it reads the target
+  }
+  if (x.op.type == HB_U1 && y.op.type == HB_U1) return x.wires[0] != y.wires[0];
+  if (x.op.type == HB_U1 || y.op.type == HB_U1) {
+    const HbSOp& u = x.op.type == HB_U1 ? x : y;
+    const HbSOp& cn = x.op.type == HB_U1 ? y : x;
+    return !has(cn.wires, u.wires[0]);
+  }
+  return x.wires[1] != y.wires[0] && x.wires[0] != y.wires[1];  // CNOT, CNOT
+}
+
+// earliest-legal-pass list scheduling of an op sequence; appends to plan
+void hb_schedule(const std::vector<HbSOp>& seq, HbPlan& plan) {
   std::vector<int> kinds;
-  std::vector<std::vector<int>> members;  // op indices per pass, in gate order
+  std::vector<std::vector<int>> members;
+  std::vector<int> pgrad;
   for (int i = 0; i < (int)seq.size(); ++i) {
     int kstar = -1;
     for (int k = 0; k < (int)members.size(); ++k)
       for (int j : members[k])
-        if (!commute(seq[j], seq[i])) kstar = k;
-    int k = kstar < 0 ? 0 : kstar;
-    if (seq[i].kind == HB_ANY) {
-      if (members.empty()) {
-        kinds.push_back(HB_SM);
-        members.emplace_back();
-      }
+        if (!hb_commute(seq[j], seq[i])) kstar = k;
+    int k;
+    if (seq[i].barrier) {
+      k = (int)members.size();
+      kinds.push_back(HB_SM);
+      members.emplace_back();
+      pgrad.push_back(seq[i].op.idx);
     } else {
-      while (k < (int)members.size() && kinds[k] != seq[i].kind) ++k;
-      if (k == (int)members.size()) {
-        kinds.push_back(seq[i].kind);
-        members.emplace_back();
+      k = kstar < 0 ? 0 : kstar;
+      if (seq[i].kind == HB_ANY) {
+        if (members.empty()) {
+          kinds.push_back(HB_SM);
+          members.emplace_back();
+          pgrad.push_back(-1);
+        }
+      } else {
+        while (k < (int)members.size() && kinds[k] != seq[i].kind) ++k;
+        if (k == (int)members.size()) {
+          kinds.push_back(seq[i].kind);
+          members.emplace_back();
+          pgrad.push_back(-1);
+        }
       }
     }
     members[k].push_back(i);
   }
-  HbPlan plan;
   for (size_t k = 0; k < members.size(); ++k) {
-    plan.passes.push_back({kinds[k], (int)plan.ops.size(), (int)members[k].size()});
-    for (int j : members[k]) plan.ops.push_back(seq[j].op);
+    HbPass ps{kinds[k], (int)plan.ops.size(), (int)members[k].size(), -1, -1, pgrad[k], 0};
+    for (int j : members[k]) {
+      plan.ops.push_back(seq[j].op);
+      if (seq[j].op.type == HB_OUTER) {
+        ps.layer = seq[j].layer;
+        ++ps.n_outer;
+      }
+    }
+    plan.passes.push_back(ps);
   }
-  // A run of CNOTs in an SM pass is one GF(2)-linear index map on the 12 low bits
-  // (plus the slice bits as fixed controls): new[i] = old[f(i, s)] with
-  // f = g_first o ... o g_last, g(j) = j ^ (bit_c(j) << t).  f is tabulated as
-  // f(i, s) = lo[i & 63] ^ hi[i >> 6] ^ sl[s]; the run head's idx is its table
-  // offset and b its length (all of the run's CNOTs are then skipped).
+}
+
+// A run of CNOTs in an SM pass is one GF(2)-linear index map on the 12 low bits (plus
+// the slice bits as fixed controls): new[i] = old[f(i, s)] with f = g_first o ... o
+// g_last, g(j) = j ^ (bit_c(j) << t), tabulated as f(i, s) = lo[i & 63] ^ hi[i >> 6] ^ sl[s]
+void hb_tabulate(HbPlan& plan) {
   for (const HbPass& ps : plan.passes) {
     if (ps.kind != HB_SM) continue;
     int o = ps.op0;
@@ -574,12 +620,12 @@ HbPlan hb_plan(const qpinn_circuit* c) {
       }
       int e = o + 1;
       while (e < end && plan.ops[e].type == HB_CNOT) ++e;
-      auto f = [&](int i, int sl) {  // the run's map on a combined index
+      auto f = [&](int i, int sl) {
         int j = i;
         for (int q = e - 1; q >= o; --q) {
           const HbOp& c = plan.ops[q];
           const int on = c.a >= kHbT ? (sl >> (c.a - kHbT)) & 1 : (j >> c.a) & 1;
-          j ^= on << c.b;
+          j ^= on << (c.b & 0xff);
         }
         return j;
       };
@@ -594,21 +640,154 @@ HbPlan hb_plan(const qpinn_circuit* c) {
       }
       for (int v = 0; v < 16; ++v) sl[v] = f(0, v);
       plan.ops[o].idx = off;
-      plan.ops[o].b = plan.ops[o].b | ((e - o) << 8);  // run length rides in b's upper bits
+      plan.ops[o].b = (plan.ops[o].b & 0xff) | ((e - o) << 8);
       o = e;
     }
   }
+}
+
+// the fused plan as per-layer op lists (u1 ops, entangler ops) in circuit order
+struct HbLayerOps {
+  std::vector<HbSOp> u1, ent;
+};
+
+std::vector<HbLayerOps> hb_layers(const qpinn_circuit* c) {
+  const int n = c->n, h = n - kHbT;
+  std::vector<HbLayerOps> layers(c->L);
+  const int n_steps = (int)c->steps.size() / 3;
+  int l = 0, in_layer = 0;
+  for (int i = 0; i < n_steps; ++i) {
+    const int type = c->steps[3 * i], wire = c->steps[3 * i + 1], idx = c->steps[3 * i + 2];
+    if (type == STEP_U1) {
+      if (in_layer == n) {  // a layer without an entangler step ended
+        ++l;
+        in_layer = 0;
+      }
+      layers[l].u1.push_back({{HB_U1, n - 1 - wire, 0, idx}, wire < h ? HB_CS : HB_SM, {wire}, l,
+                              false});
+      ++in_layer;
+    } else if (type == STEP_PERM) {
+      for (int j = c->cnot_off[idx]; j < c->cnot_off[idx + 1]; ++j) {
+        const int cw = c->cnot_ct[2 * j], tw = c->cnot_ct[2 * j + 1];
+        layers[l].ent.push_back({{HB_CNOT, n - 1 - cw, n - 1 - tw, 0}, tw < h ? HB_CS : HB_SM,
+                                 {cw, tw}, l, false});
+      }
+      ++l;
+      in_layer = 0;
+    } else {
+      std::vector<int> ws;
+      for (int k = c->phase_off[idx]; k < c->phase_off[idx + 1]; ++k) {
+        ws.push_back(c->pairs[3 * k]);
+        ws.push_back(c->pairs[3 * k + 1]);
+      }
+      layers[l].ent.push_back({{HB_PHASE, 0, 0, idx}, HB_ANY, ws, l, false});
+      ++l;
+      in_layer = 0;
+    }
+  }
+  return layers;
+}
+
+// forward (no checkpoints): the whole circuit as one schedule
+HbPlan hb_plan(const qpinn_circuit* c) {
+  std::vector<HbSOp> seq;
+  for (const HbLayerOps& lo : hb_layers(c)) {
+    seq.insert(seq.end(), lo.u1.begin(), lo.u1.end());
+    seq.insert(seq.end(), lo.ent.begin(), lo.ent.end());
+  }
+  HbPlan plan;
+  hb_schedule(seq, plan);
+  hb_tabulate(plan);
   return plan;
+}
+
+// adjoint: forward segments ending at each layer's checkpoint, then the reverse sweep
+struct HbBwdPlan {
+  HbPlan fwd, rev;
+};
+
+HbBwdPlan hb_plan_bwd(const qpinn_circuit* c) {
+  const std::vector<HbLayerOps> layers = hb_layers(c);
+  const int L = (int)layers.size();
+  HbBwdPlan bp;
+  for (int l = 0; l <= L; ++l) {  // segment l: entangler(l-1), u1(l); checkpoint l after it
+    std::vector<HbSOp> seq;
+    if (l > 0) seq.insert(seq.end(), layers[l - 1].ent.begin(), layers[l - 1].ent.end());
+    if (l < L) seq.insert(seq.end(), layers[l].u1.begin(), layers[l].u1.end());
+    if (seq.empty()) continue;
+    hb_schedule(seq, bp.fwd);
+    if (l < L) bp.fwd.passes.back().ck = l;
+  }
+  std::vector<HbSOp> seq;
+  for (int l = L - 1; l >= 0; --l) {
+    for (int j = (int)layers[l].ent.size() - 1; j >= 0; --j) {
+      HbSOp e = layers[l].ent[j];
+      if (e.op.type == HB_PHASE) {
+        e.op.b = 1;        // conjugate phase
+        e.barrier = true;  // its parameter gradient is taken from the adjoint just before
+      }
+      seq.push_back(e);
+    }
+    for (const HbSOp& u : layers[l].u1) {
+      HbSOp o = u;
+      o.op.type = HB_OUTER;
+      seq.push_back(o);
+    }
+    for (const HbSOp& u : layers[l].u1) {
+      HbSOp d = u;
+      d.op.b = 1;  // U^dagger
+      seq.push_back(d);
+    }
+  }
+  hb_schedule(seq, bp.rev);
+  hb_tabulate(bp.fwd);
+  hb_tabulate(bp.rev);
+  return bp;
 }
 
 __device__ __forceinline__ int hb_insert0(int k, int bit) {
   return ((k >> bit) << (bit + 1)) | (k & ((1 << bit) - 1));
 }
 
+__device__ __forceinline__ void hb_load_u(const cplx<float>* __restrict__ U, const HbOp& op,
+                                          cplx<float> (&u)[4]) {
+  const cplx<float>* g = U + 4 * op.idx;
+  if (op.b) {  // U^dagger
+    u[0] = {g[0].re, -g[0].im};
+    u[1] = {g[2].re, -g[2].im};
+    u[2] = {g[1].re, -g[1].im};
+    u[3] = {g[3].re, -g[3].im};
+  } else {
+    u[0] = g[0];
+    u[1] = g[1];
+    u[2] = g[2];
+    u[3] = g[3];
+  }
+}
+
+// the CTA's 8 outer-product sums (fixed shuffle tree, fixed warp order) -> part[slot]
+__device__ __forceinline__ void hb_outer_commit(float (&m)[8], double* __restrict__ red,
+                                                double* __restrict__ part) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+#pragma unroll
+  for (int k = 0; k < 8; ++k)
+    for (int s = 16; s >= 1; s >>= 1) m[k] += __shfl_xor_sync(0xffffffffu, m[k], s);
+  __syncthreads();
+  if (lane == 0)
+#pragma unroll
+    for (int k = 0; k < 8; ++k) red[w * 8 + k] = (double)m[k];
+  __syncthreads();
+  if (threadIdx.x < 8) {
+    double v = 0.0;
+    for (int i = 0; i < nw; ++i) v += red[i * 8 + threadIdx.x];
+    part[threadIdx.x] = v;
+  }
+}
+
 // SM pass: CTA = (row, slice s); ops on the 2^kHbT low-bit amplitudes in shared memory.
-// Runs of up to 3 single-qubit gates on distinct bits are applied together (8
-// amplitudes per work item in registers, one barrier per run), and a run of CNOTs is
-// one gather through the composed index map (one barrier per run).
+// Runs of up to QPINN_HB_G single-qubit gates on distinct bits are applied together
+// (one barrier per run), and a run of CNOTs is one gather through its tabulated index
+// map.  OUTER ops read the checkpoint tile xc (loaded into a second buffer).
 template <int G>
 __device__ __forceinline__ void hb_sm_u1_group(cplx<float>* t, const HbOp* op,
                                                const cplx<float>* __restrict__ U) {
@@ -619,8 +798,7 @@ __device__ __forceinline__ void hb_sm_u1_group(cplx<float>* t, const HbOp* op,
   for (int g = 0; g < G; ++g) {
     bits[g] = op[g].a;
     sorted[g] = op[g].a;
-#pragma unroll
-    for (int e = 0; e < 4; ++e) u[g][e] = U[4 * op[g].idx + e];
+    hb_load_u(U, op[g], u[g]);
   }
 #pragma unroll
   for (int i = 0; i < G; ++i)
@@ -668,13 +846,16 @@ __device__ __forceinline__ void hb_sm_u1_group(cplx<float>* t, const HbOp* op,
 #ifndef QPINN_HB_G
 #define QPINN_HB_G 2
 #endif
-__global__ void __launch_bounds__(256, QPINN_HB_MINB) hb_sm_pass(int n, cplx<float>* __restrict__ X,
-                                                  const HbOp* __restrict__ ops, int nops,
-                                                  const int* __restrict__ luts,
-                                                  const cplx<float>* __restrict__ U,
-                                                  const cplx<float>* __restrict__ ph) {
+__global__ void __launch_bounds__(256, QPINN_HB_MINB)
+hb_sm_pass(int n, cplx<float>* __restrict__ X, const cplx<float>* __restrict__ XC,
+           const HbOp* __restrict__ ops, int nops, const int* __restrict__ luts,
+           const cplx<float>* __restrict__ U, const cplx<float>* __restrict__ ph,
+           double* __restrict__ part) {
   constexpr int TS = 1 << kHbT, PER = TS / 256;
-  __shared__ cplx<float> t[TS];
+  extern __shared__ __align__(16) unsigned char hb_smem[];
+  auto* t = (cplx<float>*)hb_smem;
+  auto* tx = t + TS;  // checkpoint tile (OUTER passes)
+  __shared__ double red[8 * 8];
   const int h = n - kHbT;
   const int64_t D = (int64_t)1 << n;
   const int64_t row = blockIdx.x >> h;
@@ -686,9 +867,16 @@ __global__ void __launch_bounds__(256, QPINN_HB_MINB) hb_sm_pass(int n, cplx<flo
     for (int j = 0; j < PER; ++j) r[j] = x[threadIdx.x + 256 * j];
 #pragma unroll
     for (int j = 0; j < PER; ++j) t[threadIdx.x + 256 * j] = r[j];
+    if (XC) {
+      const cplx<float>* xc = XC + row * D + ((int64_t)s << kHbT);
+#pragma unroll
+      for (int j = 0; j < PER; ++j) r[j] = xc[threadIdx.x + 256 * j];
+#pragma unroll
+      for (int j = 0; j < PER; ++j) tx[threadIdx.x + 256 * j] = r[j];
+    }
   }
   __syncthreads();
-  int o = 0;
+  int o = 0, slot = 0;
   while (o < nops) {
     const HbOp op = ops[o];
     if (op.type == HB_U1) {
@@ -717,11 +905,27 @@ __global__ void __launch_bounds__(256, QPINN_HB_MINB) hb_sm_pass(int n, cplx<flo
 #pragma unroll
       for (int r = 0; r < PER; ++r) t[threadIdx.x + r * 256] = v[r];
       o += op.b >> 8;
+    } else if (op.type == HB_OUTER) {  // M' = sum over pairs on bit a of conj(abar) x
+      float m[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+      for (int k = threadIdx.x; k < TS / 2; k += blockDim.x) {
+        const int i0 = hb_insert0(k, op.a), i1 = i0 | (1 << op.a);
+        const cplx<float> a0 = t[i0], a1 = t[i1], x0 = tx[i0], x1 = tx[i1];
+        cmac_c(m[0], m[1], a0, x0);
+        cmac_c(m[2], m[3], a0, x1);
+        cmac_c(m[4], m[5], a1, x0);
+        cmac_c(m[6], m[7], a1, x1);
+      }
+      hb_outer_commit(m, red, part + ((int64_t)slot * gridDim.x + blockIdx.x) * 8);
+      ++slot;
+      ++o;
     } else {
       const cplx<float>* ep = ph + (int64_t)op.idx * D + ((int64_t)s << kHbT);
       cplx<float> e[PER];
 #pragma unroll
-      for (int j = 0; j < PER; ++j) e[j] = ep[threadIdx.x + 256 * j];
+      for (int j = 0; j < PER; ++j) {
+        e[j] = ep[threadIdx.x + 256 * j];
+        if (op.b) e[j].im = -e[j].im;
+      }
 #pragma unroll
       for (int j = 0; j < PER; ++j) t[threadIdx.x + 256 * j] = cmul(t[threadIdx.x + 256 * j], e[j]);
       ++o;
@@ -747,24 +951,45 @@ __device__ __forceinline__ void hb_swap_bit(cplx<float> (&v)[1 << H], int rb, in
 }
 
 template <int H, int RB>
-__device__ __forceinline__ void hb_gate_bit(cplx<float> (&v)[1 << H], cplx<float> u00,
-                                            cplx<float> u01, cplx<float> u10, cplx<float> u11) {
+__device__ __forceinline__ void hb_gate_bit(cplx<float> (&v)[1 << H], const cplx<float> (&u)[4]) {
 #pragma unroll
   for (int j = 0; j < (1 << H); ++j) {
     if ((j >> RB) & 1) continue;
     const cplx<float> a = v[j], b = v[j | (1 << RB)];
-    v[j] = cmul2(u00, a, u01, b);
-    v[j | (1 << RB)] = cmul2(u10, a, u11, b);
+    v[j] = cmul2(u[0], a, u[1], b);
+    v[j | (1 << RB)] = cmul2(u[2], a, u[3], b);
   }
 }
 
-template <int H>
+template <int H, int RB>
+__device__ __forceinline__ void hb_outer_bit(const cplx<float> (&v)[1 << H],
+                                             const cplx<float> (&xv)[1 << H], float (&m)[8]) {
+#pragma unroll
+  for (int j = 0; j < (1 << H); ++j) {
+    if ((j >> RB) & 1) continue;
+    const int j1 = j | (1 << RB);
+    cmac_c(m[0], m[1], v[j], xv[j]);
+    cmac_c(m[2], m[3], v[j], xv[j1]);
+    cmac_c(m[4], m[5], v[j1], xv[j]);
+    cmac_c(m[6], m[7], v[j1], xv[j1]);
+  }
+}
+
+template <int H, bool XOUT>
 __global__ void __launch_bounds__(256) hb_cs_pass(int n, int64_t rows, cplx<float>* __restrict__ X,
+                                                  const cplx<float>* __restrict__ XC,
                                                   const HbOp* __restrict__ ops, int nops,
                                                   const cplx<float>* __restrict__ U,
-                                                  const cplx<float>* __restrict__ ph) {
+                                                  const cplx<float>* __restrict__ ph,
+                                                  double* __restrict__ part, int n_outer) {
   constexpr int V = 1 << H, TS = 1 << kHbT;
+  __shared__ double red[8 * 8];
   const int64_t D = (int64_t)1 << n;
+  float mo[XOUT ? 4 : 1][8];  // per-thread outer sums of this pass's OUTER ops (<= H of them)
+#pragma unroll
+  for (int i = 0; i < (XOUT ? 4 : 1); ++i)
+#pragma unroll
+    for (int k = 0; k < 8; ++k) mo[i][k] = 0.f;
   for (int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; gid < rows * TS;
        gid += (int64_t)gridDim.x * blockDim.x) {
     const int64_t row = gid >> kHbT;
@@ -773,18 +998,25 @@ __global__ void __launch_bounds__(256) hb_cs_pass(int n, int64_t rows, cplx<floa
     cplx<float> v[V];
 #pragma unroll
     for (int j = 0; j < V; ++j) v[j] = x[(int64_t)j << kHbT];
+    cplx<float> xv[XOUT ? V : 1];
+    if constexpr (XOUT) {
+      const cplx<float>* xc = XC + row * D + l;
+#pragma unroll
+      for (int j = 0; j < V; ++j) xv[j] = xc[(int64_t)j << kHbT];
+    }
+    int slot = 0;
     for (int o = 0; o < nops; ++o) {
       const HbOp op = ops[o];
       if (op.type == HB_U1) {
-        const cplx<float>* u = U + 4 * op.idx;
-        const cplx<float> u00 = u[0], u01 = u[1], u10 = u[2], u11 = u[3];
+        cplx<float> u[4];
+        hb_load_u(U, op, u);
         const int rb = op.a - kHbT;
-        if (rb == 0) hb_gate_bit<H, 0>(v, u00, u01, u10, u11);
-        if constexpr (H > 1) if (rb == 1) hb_gate_bit<H, 1>(v, u00, u01, u10, u11);
-        if constexpr (H > 2) if (rb == 2) hb_gate_bit<H, 2>(v, u00, u01, u10, u11);
-        if constexpr (H > 3) if (rb == 3) hb_gate_bit<H, 3>(v, u00, u01, u10, u11);
+        if (rb == 0) hb_gate_bit<H, 0>(v, u);
+        if constexpr (H > 1) if (rb == 1) hb_gate_bit<H, 1>(v, u);
+        if constexpr (H > 2) if (rb == 2) hb_gate_bit<H, 2>(v, u);
+        if constexpr (H > 3) if (rb == 3) hb_gate_bit<H, 3>(v, u);
       } else if (op.type == HB_CNOT) {
-        const int rb = op.b - kHbT;
+        const int rb = (op.b & 0xff) - kHbT;
         if (op.a < kHbT) {  // low control: fixed for this thread
           if ((l >> op.a) & 1) {
 #pragma unroll
@@ -799,15 +1031,95 @@ __global__ void __launch_bounds__(256) hb_cs_pass(int n, int64_t rows, cplx<floa
             for (int r = 0; r < H; ++r)
               if (q == rb && r == rc) hb_swap_bit<H>(v, q, r);
         }
+      } else if (op.type == HB_OUTER) {
+        if constexpr (XOUT) {
+          const int rb = op.a - kHbT;
+#pragma unroll
+          for (int sl = 0; sl < 4; ++sl) {
+            if (sl != slot) continue;
+            if (rb == 0) hb_outer_bit<H, 0>(v, xv, mo[sl]);
+            if constexpr (H > 1) if (rb == 1) hb_outer_bit<H, 1>(v, xv, mo[sl]);
+            if constexpr (H > 2) if (rb == 2) hb_outer_bit<H, 2>(v, xv, mo[sl]);
+            if constexpr (H > 3) if (rb == 3) hb_outer_bit<H, 3>(v, xv, mo[sl]);
+          }
+          ++slot;
+        }
       } else {
         const cplx<float>* e = ph + (int64_t)op.idx * D + l;
 #pragma unroll
-        for (int j = 0; j < V; ++j) v[j] = cmul(v[j], e[(int64_t)j << kHbT]);
+        for (int j = 0; j < V; ++j) {
+          cplx<float> ej = e[(int64_t)j << kHbT];
+          if (op.b) ej.im = -ej.im;
+          v[j] = cmul(v[j], ej);
+        }
       }
     }
 #pragma unroll
     for (int j = 0; j < V; ++j) x[(int64_t)j << kHbT] = v[j];
   }
+  if constexpr (XOUT) {
+    for (int sl = 0; sl < n_outer; ++sl) {
+      float m[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) m[k] = 0.f;
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        if (i == sl)
+#pragma unroll
+          for (int k = 0; k < 8; ++k) m[k] = mo[i][k];
+      hb_outer_commit(m, red, part + ((int64_t)sl * gridDim.x + blockIdx.x) * 8);
+    }
+  }
+}
+
+// phase-step gradient sums (as gb_phase_grad) parallel over row chunks too:
+// part[c][b] = sum over chunk c's rows of Im(conj(a) x e), then acc[b] += sum_c in order
+__global__ void hb_phase_grad_part(int n, int64_t rows, int64_t per, const cplx<float>* __restrict__ X,
+                                   const cplx<float>* __restrict__ A,
+                                   const cplx<float>* __restrict__ ph, double* __restrict__ part) {
+  const int64_t D = (int64_t)1 << n;
+  const int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= D) return;
+  const cplx<float> e = ph[b];
+  const int64_t r0 = blockIdx.y * per, r1 = r0 + per < rows ? r0 + per : rows;
+  double v = 0.0;
+  for (int64_t r = r0; r < r1; ++r) {
+    const cplx<float> xp = cmul(X[r * D + b], e), a = A[r * D + b];
+    v += (double)(a.im * xp.re - a.re * xp.im);
+  }
+  part[blockIdx.y * D + b] = v;
+}
+
+__global__ void hb_phase_grad_sum(int n, int chunks, const double* __restrict__ part,
+                                  double* __restrict__ acc) {
+  const int64_t D = (int64_t)1 << n;
+  for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < D;
+       b += (int64_t)gridDim.x * blockDim.x) {
+    double v = 0.0;
+    for (int c = 0; c < chunks; ++c) v += part[c * D + b];
+    acc[b] += v;
+  }
+}
+
+// acc[8 idx + k] += sum over the pass's CTAs of its partials, in CTA order per lane,
+// then a fixed shuffle tree (one CTA per OUTER op of the pass)
+__global__ void hb_outer_reduce(const HbOp* __restrict__ ops, int nops, int nctas,
+                                const double* __restrict__ part, double* __restrict__ acc) {
+  const int k = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  int slot = -1, idx = 0;
+  for (int o = 0, sl = 0; o < nops; ++o)
+    if (ops[o].type == HB_OUTER) {
+      if (sl == blockIdx.x) {
+        slot = sl;
+        idx = ops[o].idx;
+      }
+      ++sl;
+    }
+  if (slot < 0) return;
+  double v = 0.0;
+  for (int c = lane; c < nctas; c += 32) v += part[((int64_t)slot * nctas + c) * 8 + k];
+  for (int s = 16; s >= 1; s >>= 1) v += __shfl_xor_sync(0xffffffffu, v, s);
+  if (lane == 0) acc[8 * idx + k] += v;
 }
 
 struct HbLayout {
@@ -835,19 +1147,53 @@ HbLayout hb_layout(const qpinn_circuit* c, int64_t B, int nops, int nluts) {
   return g;
 }
 
-int hb_launch_cs(int h, int n, int64_t rows, cplx<float>* X, const HbOp* ops, int nops,
-                 const cplx<float>* U, const cplx<float>* ph, cudaStream_t st) {
+int hb_cs_grid(int64_t rows) {
   const int64_t threads = rows << kHbT;
-  const int grid = (int)((threads + 255) / 256 < (int64_t)num_sms() * 8 ? (threads + 255) / 256
-                                                                       : (int64_t)num_sms() * 8);
+  const int64_t b = (threads + 255) / 256, cap = (int64_t)num_sms() * 8;
+  return (int)(b < cap ? b : cap);
+}
+
+int hb_launch_cs(int h, int n, int64_t rows, cplx<float>* X, const cplx<float>* XC,
+                 const HbOp* ops, int nops, const cplx<float>* U, const cplx<float>* ph,
+                 double* part, int n_outer, cudaStream_t st) {
+  const int grid = hb_cs_grid(rows);
+#define QPINN_HB_CS(H)                                                                       \
+  (XC ? hb_cs_pass<H, true><<<grid, 256, 0, st>>>(n, rows, X, XC, ops, nops, U, ph, part,    \
+                                                  n_outer)                                  \
+      : hb_cs_pass<H, false><<<grid, 256, 0, st>>>(n, rows, X, XC, ops, nops, U, ph, part, 0))
   switch (h) {
-    case 1: hb_cs_pass<1><<<grid, 256, 0, st>>>(n, rows, X, ops, nops, U, ph); break;
-    case 2: hb_cs_pass<2><<<grid, 256, 0, st>>>(n, rows, X, ops, nops, U, ph); break;
-    case 3: hb_cs_pass<3><<<grid, 256, 0, st>>>(n, rows, X, ops, nops, U, ph); break;
-    case 4: hb_cs_pass<4><<<grid, 256, 0, st>>>(n, rows, X, ops, nops, U, ph); break;
+    case 1: QPINN_HB_CS(1); break;
+    case 2: QPINN_HB_CS(2); break;
+    case 3: QPINN_HB_CS(3); break;
+    case 4: QPINN_HB_CS(4); break;
     default: return fail(QPINN_ERR_CAPACITY, "multi-gate HBM pass: 13 <= n <= 16");
   }
+#undef QPINN_HB_CS
   QPINN_CUDA_CHECK(cudaGetLastError());
+  return QPINN_OK;
+}
+
+// one pass of a plan on the batch's states (SM or CS kind)
+int hb_run_pass(const HbPass& ps, int n, int64_t rows, cplx<float>* X, const cplx<float>* XC,
+                const HbOp* dops, const int* dluts, const cplx<float>* U, const cplx<float>* ph,
+                double* part, double* acc, cudaStream_t st) {
+  const int h = n - kHbT;
+  const HbOp* ops = dops + ps.op0;
+  int nctas;
+  if (ps.kind == HB_SM) {
+    nctas = (int)(rows << h);
+    const int smem = (XC ? 2 : 1) * (1 << kHbT) * (int)sizeof(cplx<float>);
+    hb_sm_pass<<<(unsigned)nctas, 256, smem, st>>>(n, X, XC, ops, ps.nops, dluts, U, ph, part);
+    QPINN_CUDA_CHECK(cudaGetLastError());
+  } else {
+    nctas = hb_cs_grid(rows);
+    if (int rc = hb_launch_cs(h, n, rows, X, XC, ops, ps.nops, U, ph, part, ps.n_outer, st))
+      return rc;
+  }
+  if (ps.n_outer) {
+    hb_outer_reduce<<<ps.n_outer, 256, 0, st>>>(ops, ps.nops, nctas, part, acc);
+    QPINN_CUDA_CHECK(cudaGetLastError());
+  }
   return QPINN_OK;
 }
 
@@ -856,13 +1202,15 @@ int hb_launch_cs(int h, int n, int64_t rows, cplx<float>* X, const HbOp* ops, in
 bool hbm_fwd_supported(const qpinn_circuit* c, int dtype) {
   if (!c || dtype != QPINN_F32 || c->n <= kHbT || c->n > kHbT + 4) return false;
   if (getenv("QPINN_PQC_HBM_MULTIGATE") && atoi(getenv("QPINN_PQC_HBM_MULTIGATE")) == 0) return false;
-  return true;
+  return layer_entangler(c) >= 0;
 }
+
+bool hbm_bwd_supported(const qpinn_circuit* c, int dtype) { return hbm_fwd_supported(c, dtype); }
 
 // forward with tangents (or value only), several gates per HBM pass (see hb_plan)
 int hbm_forward(const qpinn_circuit* c, const KArgs<float>* a, unsigned char* ws, size_t bytes) {
   const PlanDev& p = c->dev;
-  const int n = c->n, h = n - kHbT;
+  const int n = c->n;
   const int64_t D = (int64_t)1 << n;
   const HbPlan plan = hb_plan(c);
   const int nops = (int)plan.ops.size();
@@ -884,8 +1232,8 @@ int hbm_forward(const qpinn_circuit* c, const KArgs<float>* a, unsigned char* ws
   auto* PT = (float*)(ws + g.PT);
   auto* RP = (double*)(ws + g.RP);
   auto* dops = (HbOp*)(ws + g.ops);
-  auto* X = (cplx<float>*)(ws + g.X);
   auto* dluts = (int*)(dops + nops);
+  auto* X = (cplx<float>*)(ws + g.X);
   QPINN_CUDA_CHECK(cudaMemcpyAsync(dops, plan.ops.data(), sizeof(HbOp) * nops,
                                    cudaMemcpyHostToDevice, st));
   if (nluts)
@@ -904,15 +1252,9 @@ int hbm_forward(const qpinn_circuit* c, const KArgs<float>* a, unsigned char* ws
     gb_point<float><<<gb_blocks(Bc * n), kGbThreads, 0, st>>>(n, a->scale, a->R, p0, Bc, a->act,
                                                               a->tan, PT);
     gb_embed<float><<<gb_blocks(Bc * D), kGbThreads, 0, st>>>(n, Bc, ns, PT, X);
-    for (const HbPass& ps : plan.passes) {
-      if (ps.kind == HB_SM) {
-        hb_sm_pass<<<(unsigned)(rows << h), 256, 0, st>>>(n, X, dops + ps.op0, ps.nops, dluts, U,
-                                                          ph);
-        QPINN_CUDA_CHECK(cudaGetLastError());
-      } else if (int rc = hb_launch_cs(h, n, rows, X, dops + ps.op0, ps.nops, U, ph, st)) {
+    for (const HbPass& ps : plan.passes)
+      if (int rc = hb_run_pass(ps, n, rows, X, nullptr, dops, dluts, U, ph, nullptr, nullptr, st))
         return rc;
-      }
-    }
     gb_readout<float><<<dim3(kGbChunks, Bc), 128, ro_smem, st>>>(n, kGbChunks, ns, X, RP);
     gb_readout_final<float><<<gb_blocks(Bc * n), kGbThreads, 0, st>>>(n, Bc, kGbChunks, ns, p0,
                                                                       a->R, RP, a->z, a->dz);
@@ -924,6 +1266,140 @@ int hbm_forward(const qpinn_circuit* c, const KArgs<float>* a, unsigned char* ws
 // number of HBM passes per forward of the multi-gate path (diagnostics)
 int hbm_forward_passes(const qpinn_circuit* c) { return (int)hb_plan(c).passes.size(); }
 
+namespace {
+
+struct HbBwdLayout {
+  int B;
+  size_t acc, U, ph, PT, EG, ops, part, X, A, CK, total;
+};
+
+HbBwdLayout hb_bwd_layout(const qpinn_circuit* c, int64_t B, int nops, int nluts) {
+  const size_t D = (size_t)1 << c->n, es = sizeof(cplx<float>);
+  HbBwdLayout g{};
+  g.B = (int)B;
+  size_t o = 0;
+  auto take = [&](size_t bytes) {
+    const size_t at = o;
+    o += align_up(bytes, 256);
+    return at;
+  };
+  const int64_t rows = 4 * B;
+  const int64_t max_ctas = std::max<int64_t>(rows << (c->n - kHbT), (int64_t)num_sms() * 8);
+  g.acc = take(8 * (8 * (size_t)c->n_u1 + D * c->n_phase));
+  g.U = take(es * 4 * c->n_u1);
+  g.ph = take(es * D * c->n_phase);
+  g.PT = take(sizeof(float) * 8 * (size_t)B * c->n);
+  g.EG = take(8 * (size_t)B * kGbChunks * 4 * c->n);
+  g.ops = take(sizeof(HbOp) * (size_t)(nops > 0 ? nops : 1) + sizeof(int) * (size_t)nluts);
+  g.part = take(std::max<size_t>(8 * 8 * (size_t)c->n * max_ctas, 8 * 32 * D));
+  g.X = take(4 * D * (size_t)B * es);
+  g.A = take(4 * D * (size_t)B * es);
+  g.CK = take((size_t)c->L * 4 * D * (size_t)B * es);
+  g.total = o;
+  return g;
+}
+
+}  // namespace
+
+// adjoint backward, several gates per HBM pass (see hb_plan_bwd)
+int hbm_backward(const qpinn_circuit* c, const KArgs<float>* a, unsigned char* ws, size_t bytes) {
+  const PlanDev& p = c->dev;
+  const int n = c->n, L = c->L;
+  const int64_t D = (int64_t)1 << n;
+  const HbBwdPlan bp = hb_plan_bwd(c);
+  // one op / lut array: forward plan first, reverse plan after it
+  std::vector<HbOp> ops = bp.fwd.ops;
+  std::vector<int> luts = bp.fwd.luts;
+  const int rev_op0 = (int)ops.size(), rev_lut0 = (int)luts.size();
+  for (HbOp op : bp.rev.ops) {
+    if (op.type == HB_CNOT && (op.b >> 8)) op.idx += rev_lut0;  // run head: table offset
+    ops.push_back(op);
+  }
+  luts.insert(luts.end(), bp.rev.luts.begin(), bp.rev.luts.end());
+  const int nops = (int)ops.size(), nluts = (int)luts.size();
+  if (getenv("QPINN_VERBOSE"))
+    fprintf(stderr, "[qpinn] multi-gate HBM adjoint: n = %d, L = %d, %d forward + %d reverse passes\n",
+            n, L, (int)bp.fwd.passes.size(), (int)bp.rev.passes.size());
+  int64_t B = a->R < 256 ? a->R : 256;
+  while (B > 1 && hb_bwd_layout(c, B, nops, nluts).total > bytes) B = B * 3 / 4;
+  const HbBwdLayout g = hb_bwd_layout(c, B < 1 ? 1 : B, nops, nluts);
+  if (bytes < g.total) return fail(QPINN_ERR_CONFIG, "multi-gate HBM adjoint: workspace too small");
+  cudaStream_t st = a->stream;
+  auto* acc = (double*)(ws + g.acc);
+  auto* U = (cplx<float>*)(ws + g.U);
+  auto* ph = (cplx<float>*)(ws + g.ph);
+  auto* PT = (float*)(ws + g.PT);
+  auto* EG = (double*)(ws + g.EG);
+  auto* dops = (HbOp*)(ws + g.ops);
+  auto* dluts = (int*)(dops + nops);
+  auto* part = (double*)(ws + g.part);
+  auto* X = (cplx<float>*)(ws + g.X);
+  auto* A = (cplx<float>*)(ws + g.A);
+  auto* CK = (cplx<float>*)(ws + g.CK);
+  QPINN_CUDA_CHECK(cudaMemcpyAsync(dops, ops.data(), sizeof(HbOp) * nops, cudaMemcpyHostToDevice,
+                                   st));
+  if (nluts)
+    QPINN_CUDA_CHECK(cudaMemcpyAsync(dluts, luts.data(), sizeof(int) * nluts,
+                                     cudaMemcpyHostToDevice, st));
+  const int n_acc = 8 * p.n_u1 + (int)D * p.n_phase;
+  QPINN_CUDA_CHECK(cudaMemsetAsync(acc, 0, 8 * (size_t)n_acc, st));
+  const int eg_smem = 4 * n * 4 * (int)sizeof(double);  // [4 warps][4 n]
+  QPINN_CUDA_CHECK(cudaFuncSetAttribute(gb_embed_grad<float>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, eg_smem));
+  QPINN_CUDA_CHECK(cudaFuncSetAttribute(hb_sm_pass, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        2 * (1 << kHbT) * (int)sizeof(cplx<float>)));
+  gb_tables<float><<<64, 256, 0, st>>>(p, a->qp, U, ph);
+  for (int64_t p0 = 0; p0 < a->R; p0 += g.B) {
+    const int Bc = (int)(a->R - p0 < g.B ? a->R - p0 : g.B);
+    const int64_t rows = (int64_t)Bc * 4;
+    const size_t ckl = (size_t)rows * D;  // one layer's checkpoint
+    gb_point<float><<<gb_blocks(Bc * n), kGbThreads, 0, st>>>(n, a->scale, a->R, p0, Bc, a->act,
+                                                              a->tan, PT);
+    gb_embed<float><<<gb_blocks(Bc * D), kGbThreads, 0, st>>>(n, Bc, 4, PT, X);
+    for (const HbPass& ps : bp.fwd.passes) {  // forward, checkpointing every layer boundary
+      if (int rc = hb_run_pass(ps, n, rows, X, nullptr, dops, dluts, U, ph, nullptr, nullptr, st))
+        return rc;
+      if (ps.ck >= 0)
+        QPINN_CUDA_CHECK(cudaMemcpyAsync(CK + ps.ck * ckl, X, ckl * sizeof(cplx<float>),
+                                         cudaMemcpyDeviceToDevice, st));
+    }
+    gb_seed<float><<<gb_blocks(Bc * D), kGbThreads, 0, st>>>(n, Bc, p0, a->R, a->gz, a->gdz, X, A);
+    for (const HbPass& pr : bp.rev.passes) {
+      HbPass ps = pr;
+      ps.op0 += rev_op0;
+      if (ps.phase_grad >= 0) {  // Im<abar, i pmat x'> sums of this phase step, per basis state
+        const int l = ps.phase_grad;
+        const int chunks = (int)std::min<int64_t>(32, rows);
+        const int64_t per = (rows + chunks - 1) / chunks;
+        hb_phase_grad_part<<<dim3((unsigned)((D + 255) / 256), chunks), 256, 0, st>>>(
+            n, rows, per, CK + l * ckl, A, ph + (size_t)l * D, part);
+        hb_phase_grad_sum<<<gb_blocks(D), kGbThreads, 0, st>>>(n, chunks, part,
+                                                              acc + 8 * p.n_u1 + (size_t)l * D);
+      }
+      const cplx<float>* xc = ps.layer >= 0 ? CK + ps.layer * ckl : nullptr;
+      if (int rc = hb_run_pass(ps, n, rows, A, xc, dops, dluts, U, ph, part, acc, st)) return rc;
+    }
+    gb_embed<float><<<gb_blocks(Bc * D), kGbThreads, 0, st>>>(n, Bc, 1, PT, X);
+    gb_embed_grad<float><<<dim3(kGbChunks, Bc), 128, eg_smem, st>>>(n, kGbChunks, PT, X, A, EG);
+    gb_embed_final<float><<<gb_blocks(Bc * n), kGbThreads, 0, st>>>(n, Bc, kGbChunks, p0, a->R,
+                                                                    EG, PT, a->tan, a->g_act,
+                                                                    a->g_tan);
+    QPINN_CUDA_CHECK(cudaGetLastError());
+  }
+  return pqc_param_grads<float>(c, acc, n, a->qp, a->g_qp, st);
+}
+
+size_t hbm_bwd_workspace_bytes(const qpinn_circuit* c) {
+  const HbBwdPlan bp = hb_plan_bwd(c);
+  const int nops = (int)(bp.fwd.ops.size() + bp.rev.ops.size());
+  const int nluts = (int)(bp.fwd.luts.size() + bp.rev.luts.size());
+  // ~1 GB of batch state: X, A and L checkpoints per point
+  const int64_t per = (int64_t)(2 + c->L) * 4 * ((int64_t)8 << c->n);
+  int64_t B = ((int64_t)1 << 30) / per;
+  B = B < 1 ? 1 : B > 256 ? 256 : B;
+  return hb_bwd_layout(c, B, nops, nluts).total;
+}
+
 size_t global_adjoint_workspace_bytes(const qpinn_circuit* c, int dtype) {
   if (dtype == QPINN_F64) return gb_layout<double>(c).total;
   // the multi-gate forward reuses this region with batches of ~256 MB of state
@@ -932,7 +1408,9 @@ size_t global_adjoint_workspace_bytes(const qpinn_circuit* c, int dtype) {
   if (!hbm_fwd_supported(c, dtype)) return g;
   const int64_t B = ((int64_t)256 << 20) / (4 * ((int64_t)8 << c->n));
   const HbPlan plan = hb_plan(c);
-  const size_t h = hb_layout(c, B < 1 ? 1 : B, (int)plan.ops.size(), (int)plan.luts.size()).total;
+  size_t h = hb_layout(c, B < 1 ? 1 : B, (int)plan.ops.size(), (int)plan.luts.size()).total;
+  const size_t hb = hbm_bwd_workspace_bytes(c);
+  h = hb > h ? hb : h;
   return h > g ? h : g;
 }
 
@@ -957,7 +1435,7 @@ int global_backward(const qpinn_circuit* c, const KArgs<T>* a, unsigned char* ws
   cplx<T>* CK = (cplx<T>*)(ws + g.CK);
   double* EG = (double*)(ws + g.EG);
   const int n_acc = 8 * p.n_u1 + (int)D * p.n_phase;
-  const int eg_smem = 4 * n * 128 * (int)sizeof(double);
+  const int eg_smem = 4 * n * 4 * (int)sizeof(double);  // [4 warps][4 n]
   QPINN_CUDA_CHECK(cudaFuncSetAttribute(gb_embed_grad<T>,
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, eg_smem));
   QPINN_CUDA_CHECK(cudaMemsetAsync(acc, 0, 8 * (size_t)n_acc, st));

@@ -69,6 +69,9 @@ bool big_fwd_supported(const qpinn_circuit* c, int dtype);
 bool hbm_fwd_supported(const qpinn_circuit* c, int dtype);
 int hbm_forward(const qpinn_circuit* c, const KArgs<float>* a, unsigned char* ws, size_t bytes);
 int hbm_forward_passes(const qpinn_circuit* c);
+bool hbm_bwd_supported(const qpinn_circuit* c, int dtype);
+int hbm_backward(const qpinn_circuit* c, const KArgs<float>* a, unsigned char* ws, size_t bytes);
+size_t hbm_bwd_workspace_bytes(const qpinn_circuit* c);
 // transfer-matrix K1 / K2 on the tensor cores (pqc_transfer.cu)
 bool transfer_supported(const qpinn_circuit* c, int dtype);
 size_t transfer_workspace_bytes(const qpinn_circuit* c, int64_t R);
