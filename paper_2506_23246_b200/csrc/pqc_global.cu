@@ -94,26 +94,35 @@ __global__ void gb_embed(int n, int B, int nstates, const T* __restrict__ PT,
     const int pb = (int)(i / D);
     const int64_t b = i % D;
     const T* pt = PT + (int64_t)pb * n * 8;
-    T pre[17];
+    T pre[17];  // prefix products, statically indexed (registers, no local memory)
     pre[0] = T(1);
-    for (int q = 0; q < n; ++q) {
-      const int bit = (b >> (n - 1 - q)) & 1;
-      pre[q + 1] = pre[q] * (bit ? pt[q * 8 + 1] : pt[q * 8]);
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+      if (q < n) {
+        const int bit = (b >> (n - 1 - q)) & 1;
+        pre[q + 1] = pre[q] * (bit ? pt[q * 8 + 1] : pt[q * 8]);
+      } else {
+        pre[q + 1] = pre[q];
+      }
     }
     T tk[3] = {T(0), T(0), T(0)}, suf = T(1);
-    for (int q = n - 1; q >= 0; --q) {
-      const int bit = (b >> (n - 1 - q)) & 1;
-      const T df = bit ? T(0.5) * pt[q * 8] : T(-0.5) * pt[q * 8 + 1];
-      const T rest = pre[q] * suf;
-      for (int k = 0; k < 3; ++k) tk[k] += pt[q * 8 + 4 + k] * df * rest;
-      suf *= bit ? pt[q * 8 + 1] : pt[q * 8];
+#pragma unroll
+    for (int q = 15; q >= 0; --q) {
+      if (q < n) {
+        const int bit = (b >> (n - 1 - q)) & 1;
+        const T df = bit ? T(0.5) * pt[q * 8] : T(-0.5) * pt[q * 8 + 1];
+        const T rest = pre[q] * suf;
+#pragma unroll
+        for (int k = 0; k < 3; ++k) tk[k] += pt[q * 8 + 4 + k] * df * rest;
+        suf *= bit ? pt[q * 8 + 1] : pt[q * 8];
+      }
     }
     const int ph = __popcll(b) & 3;  // (-i)^popcount
     auto put = [&](int s, T m) {
       X[((int64_t)pb * 4 + s) * D + b] = {ph == 0 ? m : ph == 2 ? -m : T(0),
                                            ph == 1 ? -m : ph == 3 ? m : T(0)};
     };
-    put(0, pre[n]);
+    put(0, pre[16]);  // = the product over the n wires (pre is constant past n)
     if (nstates == 4)
       for (int k = 0; k < 3; ++k) put(k + 1, tk[k]);
   }
