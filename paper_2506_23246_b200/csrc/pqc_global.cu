@@ -512,6 +512,8 @@ GbLayout gb_layout(const qpinn_circuit* c) {
 // costs about two passes.  OUTER partials are reduced per CTA and then across CTAs
 // in a fixed order (deterministic).
 constexpr int kHbT = 12;  // low bits per SM tile: 2^12 complex = 32 KB of shared memory
+// the SM tile of an n-qubit state: the whole state (h = 0, SM passes only) for n <= 12
+inline int hb_tbits(int n) { return n < kHbT ? n : kHbT; }
 enum { HB_U1 = 0, HB_CNOT = 1, HB_PHASE = 2, HB_OUTER = 3 };
 enum { HB_SM = 0, HB_CS = 1, HB_ANY = 2 };
 struct HbOp {
@@ -591,7 +593,15 @@ void hb_schedule(const std::vector<HbSOp>& seq, HbPlan& plan) {
           pgrad.push_back(-1);
         }
       } else {
-        while (k < (int)members.size() && kinds[k] != seq[i].kind) ++k;
+        // an OUTER op reads its layer's checkpoint tile: one layer per pass (with
+        // h = 0 every op is of SM kind and consecutive layers would share a pass)
+        auto other_layer = [&](int kk) {
+          if (seq[i].op.type != HB_OUTER) return false;
+          for (int j : members[kk])
+            if (seq[j].op.type == HB_OUTER && seq[j].layer != seq[i].layer) return true;
+          return false;
+        };
+        while (k < (int)members.size() && (kinds[k] != seq[i].kind || other_layer(k))) ++k;
         if (k == (int)members.size()) {
           kinds.push_back(seq[i].kind);
           members.emplace_back();
@@ -661,7 +671,7 @@ struct HbLayerOps {
 };
 
 std::vector<HbLayerOps> hb_layers(const qpinn_circuit* c) {
-  const int n = c->n, h = n - kHbT;
+  const int n = c->n, h = n - hb_tbits(n);
   std::vector<HbLayerOps> layers(c->L);
   const int n_steps = (int)c->steps.size() / 3;
   int l = 0, in_layer = 0;
@@ -797,10 +807,10 @@ __device__ __forceinline__ void hb_outer_commit(float (&m)[8], double* __restric
 // Runs of up to QPINN_HB_G single-qubit gates on distinct bits are applied together
 // (one barrier per run), and a run of CNOTs is one gather through its tabulated index
 // map.  OUTER ops read the checkpoint tile xc (loaded into a second buffer).
-template <int G>
+template <int G, int T>
 __device__ __forceinline__ void hb_sm_u1_group(cplx<float>* t, const HbOp* op,
                                                const cplx<float>* __restrict__ U) {
-  constexpr int TS = 1 << kHbT, M = 1 << G;
+  constexpr int TS = 1 << T, M = 1 << G;
   int bits[G], sorted[G];
   cplx<float> u[G][4];
 #pragma unroll
@@ -855,21 +865,22 @@ __device__ __forceinline__ void hb_sm_u1_group(cplx<float>* t, const HbOp* op,
 #ifndef QPINN_HB_G
 #define QPINN_HB_G 2
 #endif
+template <int T>
 __global__ void __launch_bounds__(256, QPINN_HB_MINB)
 hb_sm_pass(int n, cplx<float>* __restrict__ X, const cplx<float>* __restrict__ XC,
            const HbOp* __restrict__ ops, int nops, const int* __restrict__ luts,
            const cplx<float>* __restrict__ U, const cplx<float>* __restrict__ ph,
            double* __restrict__ part) {
-  constexpr int TS = 1 << kHbT, PER = TS / 256;
+  constexpr int TS = 1 << T, PER = TS / 256;
   extern __shared__ __align__(16) unsigned char hb_smem[];
   auto* t = (cplx<float>*)hb_smem;
   auto* tx = t + TS;  // checkpoint tile (OUTER passes)
   __shared__ double red[8 * 8];
-  const int h = n - kHbT;
+  const int h = n - T;
   const int64_t D = (int64_t)1 << n;
   const int64_t row = blockIdx.x >> h;
   const int s = blockIdx.x & ((1 << h) - 1);
-  cplx<float>* x = X + row * D + ((int64_t)s << kHbT);
+  cplx<float>* x = X + row * D + ((int64_t)s << T);
   {  // all of the thread's loads in flight before any shared-memory store
     cplx<float> r[PER];
 #pragma unroll
@@ -877,7 +888,7 @@ hb_sm_pass(int n, cplx<float>* __restrict__ X, const cplx<float>* __restrict__ X
 #pragma unroll
     for (int j = 0; j < PER; ++j) t[threadIdx.x + 256 * j] = r[j];
     if (XC) {
-      const cplx<float>* xc = XC + row * D + ((int64_t)s << kHbT);
+      const cplx<float>* xc = XC + row * D + ((int64_t)s << T);
 #pragma unroll
       for (int j = 0; j < PER; ++j) r[j] = xc[threadIdx.x + 256 * j];
 #pragma unroll
@@ -896,9 +907,9 @@ hb_sm_pass(int n, cplx<float>* __restrict__ X, const cplx<float>* __restrict__ X
         if (!distinct) break;
         ++g;
       }
-      if (QPINN_HB_G >= 3 && g == 3) hb_sm_u1_group<3>(t, ops + o, U);
-      else if (QPINN_HB_G >= 2 && g == 2) hb_sm_u1_group<2>(t, ops + o, U);
-      else hb_sm_u1_group<1>(t, ops + o, U);
+      if (QPINN_HB_G >= 3 && g == 3) hb_sm_u1_group<3, T>(t, ops + o, U);
+      else if (QPINN_HB_G >= 2 && g == 2) hb_sm_u1_group<2, T>(t, ops + o, U);
+      else hb_sm_u1_group<1, T>(t, ops + o, U);
       o += g;
     } else if (op.type == HB_CNOT) {
       // a run of CNOTs: new[i] = old[f(i, s)] through the run's tabulated index map
@@ -928,7 +939,7 @@ hb_sm_pass(int n, cplx<float>* __restrict__ X, const cplx<float>* __restrict__ X
       ++slot;
       ++o;
     } else {
-      const cplx<float>* ep = ph + (int64_t)op.idx * D + ((int64_t)s << kHbT);
+      const cplx<float>* ep = ph + (int64_t)op.idx * D + ((int64_t)s << T);
       cplx<float> e[PER];
 #pragma unroll
       for (int j = 0; j < PER; ++j) {
@@ -1186,13 +1197,25 @@ int hb_launch_cs(int h, int n, int64_t rows, cplx<float>* X, const cplx<float>* 
 int hb_run_pass(const HbPass& ps, int n, int64_t rows, cplx<float>* X, const cplx<float>* XC,
                 const HbOp* dops, const int* dluts, const cplx<float>* U, const cplx<float>* ph,
                 double* part, double* acc, cudaStream_t st) {
-  const int h = n - kHbT;
+  const int tb = hb_tbits(n), h = n - tb;
   const HbOp* ops = dops + ps.op0;
   int nctas;
   if (ps.kind == HB_SM) {
     nctas = (int)(rows << h);
-    const int smem = (XC ? 2 : 1) * (1 << kHbT) * (int)sizeof(cplx<float>);
-    hb_sm_pass<<<(unsigned)nctas, 256, smem, st>>>(n, X, XC, ops, ps.nops, dluts, U, ph, part);
+    const int smem = (XC ? 2 : 1) * (1 << tb) * (int)sizeof(cplx<float>);
+    switch (tb) {
+#define QPINN_HB_SM(T)                                                                       \
+  case T:                                                                                    \
+    hb_sm_pass<T><<<(unsigned)nctas, 256, smem, st>>>(n, X, XC, ops, ps.nops, dluts, U, ph, \
+                                                      part);                                \
+    break;
+      QPINN_HB_SM(9)
+      QPINN_HB_SM(10)
+      QPINN_HB_SM(11)
+      QPINN_HB_SM(12)
+#undef QPINN_HB_SM
+      default: return fail(QPINN_ERR_CAPACITY, "multi-gate HBM pass: 9 <= n <= 16");
+    }
     QPINN_CUDA_CHECK(cudaGetLastError());
   } else {
     nctas = hb_cs_grid(rows);
@@ -1208,13 +1231,40 @@ int hb_run_pass(const HbPass& ps, int n, int64_t rows, cplx<float>* X, const cpl
 
 }  // namespace
 
-bool hbm_fwd_supported(const qpinn_circuit* c, int dtype) {
-  if (!c || dtype != QPINN_F32 || c->n <= kHbT || c->n > kHbT + 4) return false;
+namespace {
+// smallest n routed to the multi-gate passes; below it the CTA kernels of pqc_big.cu
+// are faster (n = 9..12 both ways: profiles/r02/config5_hbm_vs_cta.txt); QPINN_PQC_HBM_{FWD,BWD}_MIN
+// override it, QPINN_PQC_HBM_MULTIGATE=0 turns the path off
+bool hbm_supported(const qpinn_circuit* c, int dtype, const char* env, int min_n) {
+  if (!c || dtype != QPINN_F32 || c->n < 9 || c->n > kHbT + 4) return false;
   if (getenv("QPINN_PQC_HBM_MULTIGATE") && atoi(getenv("QPINN_PQC_HBM_MULTIGATE")) == 0) return false;
-  return layer_entangler(c) >= 0;
+  if (getenv(env)) min_n = atoi(getenv(env));
+  return c->n >= min_n && layer_entangler(c) >= 0;
+}
+}  // namespace
+
+// Whole-state tiles (n <= 12) against the CTA kernels of pqc_big.cu, config 5
+// (profiles/r02/config5_hbm_vs_cta.txt): the adjoint is 1.2-4x faster from n = 12 for
+// every entangler and at n = 11 with CNOT entanglers or L = 1 (phase and no-entangler
+// adjoints at L >= 4 stay 10-20% faster on the CTA kernels); the forward is 1.0-1.7x
+// faster from n = 12 with L >= 2 (the n = 12, L = 1 forward stays 1.1-1.4x faster on
+// the CTA kernels); n <= 10 stays on the CTA kernels both ways.
+bool hbm_fwd_supported(const qpinn_circuit* c, int dtype) {
+  return hbm_supported(c, dtype, "QPINN_PQC_HBM_FWD_MIN", c && c->L >= 2 ? 12 : 13);
 }
 
-bool hbm_bwd_supported(const qpinn_circuit* c, int dtype) { return hbm_fwd_supported(c, dtype); }
+bool hbm_bwd_supported(const qpinn_circuit* c, int dtype) {
+  return hbm_supported(c, dtype, "QPINN_PQC_HBM_BWD_MIN",
+                       c && (c->L == 1 || layer_entangler(c) == ENT_PERM) ? 11 : 12);
+}
+
+namespace {
+// points per batch: ~1 GB of adjoint state (X, A, L checkpoints), ~256 MB of forward state
+int64_t hb_bwd_bcap(int n) { return std::max<int64_t>(256, (int64_t)1 << (22 - n)); }
+// blocks per point of the readout / embedding gradient: >= 1024 amplitudes each
+int hb_chunks(int n) { return n <= 10 ? 1 : std::min(kGbChunks, 1 << (n - 10)); }
+int64_t hb_fwd_bcap(int n) { return std::max<int64_t>(1024, (int64_t)1 << (22 - n)); }
+}  // namespace
 
 // forward with tangents (or value only), several gates per HBM pass (see hb_plan)
 int hbm_forward(const qpinn_circuit* c, const KArgs<float>* a, unsigned char* ws, size_t bytes) {
@@ -1230,7 +1280,7 @@ int hbm_forward(const qpinn_circuit* c, const KArgs<float>* a, unsigned char* ws
     fprintf(stderr, "\n");
   }
   // largest batch of points that fits the workspace
-  int64_t B = a->R < 1024 ? a->R : 1024;
+  int64_t B = std::min<int64_t>(a->R, hb_fwd_bcap(n));
   const int nluts = (int)plan.luts.size();
   while (B > 1 && hb_layout(c, B, nops, nluts).total > bytes) B = B * 3 / 4;
   const HbLayout g = hb_layout(c, B < 1 ? 1 : B, nops, nluts);
@@ -1249,6 +1299,7 @@ int hbm_forward(const qpinn_circuit* c, const KArgs<float>* a, unsigned char* ws
     QPINN_CUDA_CHECK(cudaMemcpyAsync(dluts, plan.luts.data(), sizeof(int) * nluts,
                                      cudaMemcpyHostToDevice, st));
   const int ns = a->tan ? 4 : 1;
+  const int chunks = hb_chunks(n);
   const int ro_smem = 4 * n * 4 * (int)sizeof(double);  // [4 warps][4 n]
   QPINN_CUDA_CHECK(cudaFuncSetAttribute(gb_readout<float>,
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, ro_smem));
@@ -1264,8 +1315,8 @@ int hbm_forward(const qpinn_circuit* c, const KArgs<float>* a, unsigned char* ws
     for (const HbPass& ps : plan.passes)
       if (int rc = hb_run_pass(ps, n, rows, X, nullptr, dops, dluts, U, ph, nullptr, nullptr, st))
         return rc;
-    gb_readout<float><<<dim3(kGbChunks, Bc), 128, ro_smem, st>>>(n, kGbChunks, ns, X, RP);
-    gb_readout_final<float><<<gb_blocks(Bc * n), kGbThreads, 0, st>>>(n, Bc, kGbChunks, ns, p0,
+    gb_readout<float><<<dim3(chunks, Bc), 128, ro_smem, st>>>(n, chunks, ns, X, RP);
+    gb_readout_final<float><<<gb_blocks(Bc * n), kGbThreads, 0, st>>>(n, Bc, chunks, ns, p0,
                                                                       a->R, RP, a->z, a->dz);
     QPINN_CUDA_CHECK(cudaGetLastError());
   }
@@ -1293,7 +1344,7 @@ HbBwdLayout hb_bwd_layout(const qpinn_circuit* c, int64_t B, int nops, int nluts
     return at;
   };
   const int64_t rows = 4 * B;
-  const int64_t max_ctas = std::max<int64_t>(rows << (c->n - kHbT), (int64_t)num_sms() * 8);
+  const int64_t max_ctas = std::max<int64_t>(rows << (c->n - hb_tbits(c->n)), (int64_t)num_sms() * 8);
   g.acc = take(8 * (8 * (size_t)c->n_u1 + D * c->n_phase));
   g.U = take(es * 4 * c->n_u1);
   g.ph = take(es * D * c->n_phase);
@@ -1329,7 +1380,7 @@ int hbm_backward(const qpinn_circuit* c, const KArgs<float>* a, unsigned char* w
   if (getenv("QPINN_VERBOSE"))
     fprintf(stderr, "[qpinn] multi-gate HBM adjoint: n = %d, L = %d, %d forward + %d reverse passes\n",
             n, L, (int)bp.fwd.passes.size(), (int)bp.rev.passes.size());
-  int64_t B = a->R < 256 ? a->R : 256;
+  int64_t B = std::min<int64_t>(a->R, hb_bwd_bcap(n));
   while (B > 1 && hb_bwd_layout(c, B, nops, nluts).total > bytes) B = B * 3 / 4;
   const HbBwdLayout g = hb_bwd_layout(c, B < 1 ? 1 : B, nops, nluts);
   if (bytes < g.total) return fail(QPINN_ERR_CONFIG, "multi-gate HBM adjoint: workspace too small");
@@ -1353,9 +1404,11 @@ int hbm_backward(const qpinn_circuit* c, const KArgs<float>* a, unsigned char* w
   const int n_acc = 8 * p.n_u1 + (int)D * p.n_phase;
   QPINN_CUDA_CHECK(cudaMemsetAsync(acc, 0, 8 * (size_t)n_acc, st));
   const int eg_smem = 4 * n * 4 * (int)sizeof(double);  // [4 warps][4 n]
+  const int chunks = hb_chunks(n);
   QPINN_CUDA_CHECK(cudaFuncSetAttribute(gb_embed_grad<float>,
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, eg_smem));
-  QPINN_CUDA_CHECK(cudaFuncSetAttribute(hb_sm_pass, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  QPINN_CUDA_CHECK(cudaFuncSetAttribute(hb_sm_pass<kHbT>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         2 * (1 << kHbT) * (int)sizeof(cplx<float>)));
   gb_tables<float><<<64, 256, 0, st>>>(p, a->qp, U, ph);
   for (int64_t p0 = 0; p0 < a->R; p0 += g.B) {
@@ -1389,8 +1442,8 @@ int hbm_backward(const qpinn_circuit* c, const KArgs<float>* a, unsigned char* w
       if (int rc = hb_run_pass(ps, n, rows, A, xc, dops, dluts, U, ph, part, acc, st)) return rc;
     }
     gb_embed<float><<<gb_blocks(Bc * D), kGbThreads, 0, st>>>(n, Bc, 1, PT, X);
-    gb_embed_grad<float><<<dim3(kGbChunks, Bc), 128, eg_smem, st>>>(n, kGbChunks, PT, X, A, EG);
-    gb_embed_final<float><<<gb_blocks(Bc * n), kGbThreads, 0, st>>>(n, Bc, kGbChunks, p0, a->R,
+    gb_embed_grad<float><<<dim3(chunks, Bc), 128, eg_smem, st>>>(n, chunks, PT, X, A, EG);
+    gb_embed_final<float><<<gb_blocks(Bc * n), kGbThreads, 0, st>>>(n, Bc, chunks, p0, a->R,
                                                                     EG, PT, a->tan, a->g_act,
                                                                     a->g_tan);
     QPINN_CUDA_CHECK(cudaGetLastError());
@@ -1405,7 +1458,7 @@ size_t hbm_bwd_workspace_bytes(const qpinn_circuit* c) {
   // ~1 GB of batch state: X, A and L checkpoints per point
   const int64_t per = (int64_t)(2 + c->L) * 4 * ((int64_t)8 << c->n);
   int64_t B = ((int64_t)1 << 30) / per;
-  B = B < 1 ? 1 : B > 256 ? 256 : B;
+  B = B < 1 ? 1 : std::min<int64_t>(B, hb_bwd_bcap(c->n));
   return hb_bwd_layout(c, B, nops, nluts).total;
 }
 
@@ -1414,12 +1467,13 @@ size_t global_adjoint_workspace_bytes(const qpinn_circuit* c, int dtype) {
   // the multi-gate forward reuses this region with batches of ~256 MB of state
   // (1024 points at n = 13), so few launches carry the batch loop
   const size_t g = gb_layout<float>(c).total;
-  if (!hbm_fwd_supported(c, dtype)) return g;
-  const int64_t B = ((int64_t)256 << 20) / (4 * ((int64_t)8 << c->n));
-  const HbPlan plan = hb_plan(c);
-  size_t h = hb_layout(c, B < 1 ? 1 : B, (int)plan.ops.size(), (int)plan.luts.size()).total;
-  const size_t hb = hbm_bwd_workspace_bytes(c);
-  h = hb > h ? hb : h;
+  size_t h = 0;
+  if (hbm_fwd_supported(c, dtype)) {
+    const int64_t B = ((int64_t)256 << 20) / (4 * ((int64_t)8 << c->n));
+    const HbPlan plan = hb_plan(c);
+    h = hb_layout(c, B < 1 ? 1 : B, (int)plan.ops.size(), (int)plan.luts.size()).total;
+  }
+  if (hbm_bwd_supported(c, dtype)) h = std::max(h, hbm_bwd_workspace_bytes(c));
   return h > g ? h : g;
 }
 

@@ -219,6 +219,38 @@ def test_cluster_kernels_large_n_vs_oracle(n, L, kind, bwd):
         assert_close_budget(gq, wgq, dtype, fl[5], f"n={n} gq")
 
 
+@pytest.mark.parametrize("n,L,kind", [(9, 2, "strongly"), (10, 3, "cross_mesh"),
+                                      (11, 2, "no_entanglement"), (12, 3, "strongly"),
+                                      (12, 2, "cross_mesh_2rot"), (12, 2, "basic")])
+def test_hbm_multigate_whole_state_tiles_vs_oracle(n, L, kind, monkeypatch):
+    """The multi-gate HBM passes with one whole-state SM tile per row (n <= 12, no CS
+    passes; the default for the n = 12 adjoint and CNOT-entangler forward) forced on
+    from n = 9, K1 and K2 vs the oracle.  Every reverse pass holds the OUTER ops of
+    one layer only (they read that layer's checkpoint)."""
+    from paper_2506_23246_b200.ansatz import build_circuit, pqc_backward_raw, pqc_forward_raw
+    monkeypatch.setenv("QPINN_PQC_HBM_FWD_MIN", "9")
+    monkeypatch.setenv("QPINN_PQC_HBM_BWD_MIN", "9")
+    dtype = torch.float32
+    rng = np.random.default_rng(n * 17 + L)
+    c = build_circuit(kind, n, L)
+    R = 5
+    d = dict(a=rng.uniform(-0.9, 0.9, (R, n)), da=rng.normal(size=(3, R, n)),
+             qp=rng.uniform(0, 2 * np.pi, c.param_count), gz=rng.normal(size=(R, n)),
+             gdz=rng.normal(size=(3, R, n)))
+    a, da, qp = cuda(d["a"], dtype), cuda(d["da"], dtype), cuda(d["qp"], dtype)
+    z, dz = pqc_forward_raw(c, "acos", a, da, qp)
+    wz, wdz = O.pqc_forward(d["a"], d["da"], d["qp"], kind, "acos", L)
+    fl = _floors(d, kind, "acos", L)
+    assert_close_budget(z, wz, dtype, fl[0], f"n={n} z")
+    assert_close_budget(dz, wdz, dtype, fl[1], f"n={n} dz")
+    ga, gda, gq = pqc_backward_raw(c, "acos", a, da, qp, cuda(d["gz"], dtype),
+                                   cuda(d["gdz"], dtype))
+    wga, wgda, wgq = O.pqc_backward(d["a"], d["da"], d["qp"], kind, "acos", L, d["gz"], d["gdz"])
+    assert_close_budget(ga, wga, dtype, fl[3], f"n={n} ga")
+    assert_close_budget(gda, wgda, dtype, fl[4], f"n={n} gda")
+    assert_close_budget(gq, wgq, dtype, fl[5], f"n={n} gq")
+
+
 @pytest.mark.parametrize("n,L,kind", [(16, 1, "strongly"), (15, 1, "cross_mesh")])
 def test_hbm_regime_adjoint_float64(n, L, kind):
     """float64 adjoint beyond the cluster-resident range vs the oracle (1e-10)."""
