@@ -1121,22 +1121,42 @@ wgrad_kernel(const __grid_constant__ CUtensorMap mX, const __grid_constant__ CUt
 // 32 chunk groups per 32 entries (1024 threads): every thread has at most a few
 // partials to load, so the launch is not latency-bound on a serial load chain
 __global__ void __launch_bounds__(1024) wgrad_reduce(int n_kc, int64_t n,
-                                                     const float* __restrict__ partial,
-                                                     float* __restrict__ dW) {
-  __shared__ double red[32][33];
-  const int c = threadIdx.x & 31, grp = threadIdx.x >> 5;
-  const int64_t i = (int64_t)blockIdx.x * 32 + c;
-  double s = 0.0;
-  if (i < n)
-#pragma unroll 4
-    for (int k = grp; k < n_kc; k += 32) s += (double)partial[(int64_t)k * n + i];
-  red[grp][c] = s;
+                                                    const float* __restrict__ partial,
+                                                    float* __restrict__ dW) {
+  // block = 128 columns (a float4 per lane), warp w sums chunks k = w, w + 32, ... in
+  // float64, then the 32 warps are added in order (deterministic)
+  __shared__ double red[32][128];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t i = (int64_t)blockIdx.x * 128 + 4 * lane;
+  double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+  if ((n & 3) == 0 && i < n) {  // 16-byte rows
+#pragma unroll 2
+    for (int k = w; k < n_kc; k += 32) {
+      const float4 v = __ldg(reinterpret_cast<const float4*>(partial + (int64_t)k * n + i));
+      s0 += (double)v.x;
+      s1 += (double)v.y;
+      s2 += (double)v.z;
+      s3 += (double)v.w;
+    }
+  } else if (i < n) {
+    for (int k = w; k < n_kc; k += 32) {
+      const float* r = partial + (int64_t)k * n + i;
+      s0 += (double)r[0];
+      if (i + 1 < n) s1 += (double)r[1];
+      if (i + 2 < n) s2 += (double)r[2];
+      if (i + 3 < n) s3 += (double)r[3];
+    }
+  }
+  red[w][4 * lane] = s0;
+  red[w][4 * lane + 1] = s1;
+  red[w][4 * lane + 2] = s2;
+  red[w][4 * lane + 3] = s3;
   __syncthreads();
-  if (grp == 0 && i < n) {
+  if (threadIdx.x < 128 && (int64_t)blockIdx.x * 128 + threadIdx.x < n) {
     double v = 0.0;
 #pragma unroll
-    for (int g = 0; g < 32; ++g) v += red[g][c];
-    dW[i] = (float)v;
+    for (int g = 0; g < 32; ++g) v += red[g][threadIdx.x];
+    dW[(int64_t)blockIdx.x * 128 + threadIdx.x] = (float)v;
   }
 }
 
@@ -1402,7 +1422,7 @@ int wgrad(int64_t rows, int Kin, int Nout, const float* X, int64_t ldx, const fl
   wgrad_kernel<<<grid, kThreadsW, kWSmem, st>>>(mX, mG, a);
   QPINN_CUDA_CHECK(cudaGetLastError());
   const int64_t n = (int64_t)Kin * Nout;
-  wgrad_reduce<<<(int)((n + 31) / 32), 1024, 0, st>>>(a.n_kc, n, a.partial, dW);
+  wgrad_reduce<<<(int)((n + 127) / 128), 1024, 0, st>>>(a.n_kc, n, a.partial, dW);
   QPINN_CUDA_CHECK(cudaGetLastError());
   return QPINN_OK;
 }
