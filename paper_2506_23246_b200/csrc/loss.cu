@@ -226,22 +226,24 @@ loss_head_kernel(LossDev L, int64_t R, const T* __restrict__ Z, const T* __restr
 }
 
 // fixed-order grid reduction: sums[0..23) (double) and the head gradient (dtype);
-// 32 values x 8 interleaved block groups per CTA, groups combined in order
+// 32 values x 32 interleaved block groups per CTA, groups combined in order
 template <typename T>
-__global__ void loss_head_reduce(const double* __restrict__ partial, int blocks, int nv,
+__global__ void __launch_bounds__(1024) loss_head_reduce(const double* __restrict__ partial, int blocks, int nv,
                                  double* __restrict__ sums, T* __restrict__ g_wo,
                                  T* __restrict__ g_bo) {
-  __shared__ double red[8][32];
+  __shared__ double red[32][33];  // 32 row groups (blockDim 1024), added in order
   const int c = threadIdx.x & 31, grp = threadIdx.x >> 5;
   const int v = blockIdx.x * 32 + c;
   double x = 0.0;
-  if (v < nv)
-    for (int b = grp; b < blocks; b += 8) x += partial[(size_t)b * nv + v];
+  if (v < nv) {
+#pragma unroll 4
+    for (int b = grp; b < blocks; b += 32) x += __ldg(partial + (size_t)b * nv + v);
+  }
   red[grp][c] = x;
   __syncthreads();
   if (grp == 0 && v < nv) {
     double t = 0.0;
-    for (int g2 = 0; g2 < 8; ++g2) t += red[g2][c];
+    for (int g2 = 0; g2 < 32; ++g2) t += red[g2][c];
     if (v < kNS) sums[v] = t;
     else if (v < nv - 3) g_wo[v - kNS] = T(t);
     else g_bo[v - (nv - 3)] = T(t);
@@ -388,7 +390,7 @@ static int launch_head(const LossDev& L, int64_t R, const T* z, const T* wo, con
   const int grid = loss_grid(R);
   loss_head_kernel<T, W><<<grid, kLossThreads, 0, st>>>(L, R, z, wo, bo, weights, gz, partial);
   QPINN_CUDA_CHECK(cudaGetLastError());
-  loss_head_reduce<T><<<(kNS + 3 * W + 3 + 31) / 32, 256, 0, st>>>(partial, grid,
+  loss_head_reduce<T><<<(kNS + 3 * W + 3 + 31) / 32, 1024, 0, st>>>(partial, grid,
                                                                     kNS + 3 * W + 3, sums, g_wo,
                                                                     g_bo);
   QPINN_CUDA_CHECK(cudaGetLastError());

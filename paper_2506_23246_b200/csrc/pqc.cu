@@ -402,10 +402,15 @@ __global__ void pqc_reduce_partials(const double* __restrict__ partial, int bloc
 template <typename T>
 __global__ void pqc_u1_grads(PlanDev p, const T* __restrict__ qp, const double* __restrict__ tot,
                              T* __restrict__ g_qp) {
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < p.n_u1; i += gridDim.x * blockDim.x) {
+  // one thread per (gate, parameter slot): the double-precision trig of a gate's
+  // matrix and derivative runs in parallel over its slots
+  for (int it = blockIdx.x * blockDim.x + threadIdx.x; it < 3 * p.n_u1;
+       it += gridDim.x * blockDim.x) {
+    const int i = it / 3, jslot = it % 3;
     const int kind = p.u1[i * 4];
     double th[3] = {0, 0, 0};
     const int ns = u1_nslots(kind);
+    if (jslot >= ns) continue;
     for (int j = 0; j < ns; ++j) th[j] = (double)qp[p.u1[i * 4 + 1 + j]];
     double U[8];
     u1_matrix_d(kind, th, U);
@@ -424,7 +429,8 @@ __global__ void pqc_u1_grads(PlanDev p, const T* __restrict__ qp, const double* 
         M[(a * 2 + b) * 2] = re;
         M[(a * 2 + b) * 2 + 1] = im;
       }
-    for (int j = 0; j < ns; ++j) {
+    {
+      const int j = jslot;
       double dU[8];
       u1_dmatrix_d(kind, th, j, dU);
       double g = 0.0;  // Re sum_ij dU_ij M_ij
@@ -552,7 +558,7 @@ int pqc_finish_grads_ab(const qpinn_circuit* c, int grid, const KArgs<T>* a, int
     pqc_reduce_partials<<<(n_acc + 255) / 256, 256, 0, a->stream>>>(a->partial, grid, n_acc, a->tot);
     QPINN_CUDA_CHECK(cudaGetLastError());
   }
-  pqc_u1_grads<T><<<1, 256, 0, a->stream>>>(p, a->qp, a->tot, a->g_qp);
+  pqc_u1_grads<T><<<p.n_u1 > 0 ? (3 * p.n_u1 + 127) / 128 : 1, 128, 0, a->stream>>>(p, a->qp, a->tot, a->g_qp);
   QPINN_CUDA_CHECK(cudaGetLastError());
   if (p.n_phase) {
     pqc_phase_grads<T><<<1, 256, 0, a->stream>>>(p, ab, a->tot, a->g_qp);
@@ -563,7 +569,7 @@ int pqc_finish_grads_ab(const qpinn_circuit* c, int grid, const KArgs<T>* a, int
 template <typename T>
 int pqc_param_grads(const qpinn_circuit* c, const double* tot, int ab, const T* qp, T* g_qp,
                     cudaStream_t st) {
-  pqc_u1_grads<T><<<1, 256, 0, st>>>(c->dev, qp, tot, g_qp);
+  pqc_u1_grads<T><<<c->dev.n_u1 > 0 ? (3 * c->dev.n_u1 + 127) / 128 : 1, 128, 0, st>>>(c->dev, qp, tot, g_qp);
   QPINN_CUDA_CHECK(cudaGetLastError());
   if (c->dev.n_phase) {
     pqc_phase_grads<T><<<1, 256, 0, st>>>(c->dev, ab, tot, g_qp);

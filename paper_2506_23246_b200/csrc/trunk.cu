@@ -248,8 +248,9 @@ template <typename T, int NA>
 __global__ void __launch_bounds__(128) adapter_bwd(int64_t R, int Hd, int64_t rows_per, const T* __restrict__ g_act,
                             const T* __restrict__ act, const T* __restrict__ Hl,
                             const T* __restrict__ Wa, T* __restrict__ GU,
-                            double* __restrict__ part_wa, double* __restrict__ part_b,
-                            double* __restrict__ part_ba) {
+                            double* __restrict__ part) {
+  // partials: one row per block, [db (Hd) | dWa (Hd x n) | dba (n)] -- the order of
+  // h_last.b, adapter.W, adapter.b in the flat parameter vector (network.py layout)
   constexpr int n = NA;
   constexpr int NAP = (NA + 3) / 4 * 4;  // padded rows: vector shared-memory loads
   __shared__ __align__(16) T gua[32][4][NAP];
@@ -328,13 +329,13 @@ __global__ void __launch_bounds__(128) adapter_bwd(int64_t R, int Hd, int64_t ro
     }
     __syncthreads();
   }
+  double* row = part + (int64_t)blockIdx.x * (Hd + Hd * n + n);
   if (col) {
-    part_b[(int64_t)blockIdx.x * Hd + j] = acc_b;
+    row[j] = acc_b;
 #pragma unroll
-    for (int k = 0; k < NA; ++k)
-      part_wa[(int64_t)blockIdx.x * Hd * n + (int64_t)j * n + k] = (double)acc_w[k];
+    for (int k = 0; k < NA; ++k) row[Hd + (int64_t)j * n + k] = (double)acc_w[k];
   }
-  if (tid < n) part_ba[(int64_t)blockIdx.x * n + tid] = acc_ba;
+  if (tid < n) row[Hd + Hd * n + tid] = acc_ba;
 }
 
 // deterministic column sums of X [R, N]: block b sums rows [b*rows_per, ...)
@@ -354,15 +355,18 @@ __global__ void colsum_partial(int64_t R, int N, int64_t rows_per, const T* __re
 // group sums combined in fixed order (deterministic)
 template <typename T>
 __global__ void __launch_bounds__(1024) colsum_reduce(int nb, int N, const double* __restrict__ partial,
-                                                      T* __restrict__ out) {
+                                                      T* __restrict__ out, int64_t ld = 0) {
   // block = 32 columns x (blockDim / 32) row groups; group g sums rows g, g + G, ...,
-  // then the groups are added in order (deterministic)
+  // then the groups are added in order (deterministic); partial rows ld apart (0: N)
   __shared__ double red[32][33];
   const int c = threadIdx.x & 31, grp = threadIdx.x >> 5, G = blockDim.x >> 5;
   const int j = blockIdx.x * 32 + c;
+  const int64_t rs = ld ? ld : N;
   double acc = 0.0;
-  if (j < N)
-    for (int b = grp; b < nb; b += G) acc += partial[(int64_t)b * N + j];
+  if (j < N) {
+#pragma unroll 4
+    for (int b = grp; b < nb; b += G) acc += __ldg(partial + (int64_t)b * rs + j);
+  }
   red[grp][c] = acc;
   __syncthreads();
   if (grp == 0 && j < N) {
@@ -648,10 +652,8 @@ static int backward_impl(const qpinn_trunk_desc* d, int64_t R, const T* x, const
   const int Kl = d->n_hidden ? H : 2 * F;
   const bool fused = d->n_hidden > 0 && n <= kAdMaxN && H <= 128;
   if (fused) {  // adapter + last hidden layer's reverse dual tanh in one pass (g1 = its dL/dU)
-    double* pa = (double*)(ws + w.apart);
-    double* pwa = pa;
-    double* pb = pwa + (size_t)kAdBlocks * H * n;
-    double* pba = pb + (size_t)kAdBlocks * H;
+    double* pa = (double*)(ws + w.apart);  // [blocks][H + H n + n]
+    const int W = H + H * n + n;
     const int64_t rows_per = (R + kAdBlocks - 1) / kAdBlocks;
     const int nb = (int)((R + rows_per - 1) / rows_per);
     const int thr = (H + 31) / 32 * 32;
@@ -659,16 +661,23 @@ static int backward_impl(const qpinn_trunk_desc* d, int64_t R, const T* x, const
     switch (n) {
 #define QPINN_AD(NN)                                                                        \
   case NN:                                                                                  \
-    adapter_bwd<T, NN><<<nb, thr, 0, st>>>(R, H, rows_per, g_act, act, Hl, Wa, g1, pwa, pb, pba); \
+    adapter_bwd<T, NN><<<nb, thr, 0, st>>>(R, H, rows_per, g_act, act, Hl, Wa, g1, pa); \
     break;
       QPINN_AD(1) QPINN_AD(2) QPINN_AD(3) QPINN_AD(4) QPINN_AD(5) QPINN_AD(6) QPINN_AD(7)
       QPINN_AD(8) QPINN_AD(9) QPINN_AD(10) QPINN_AD(11) QPINN_AD(12) QPINN_AD(13)
       QPINN_AD(14) QPINN_AD(15) QPINN_AD(16)
 #undef QPINN_AD
     }
-    colsum_reduce<T><<<(H * n + 31) / 32, 1024, 0, st>>>(nb, H * n, pwa, grad + d->off_adapter_w);
-    colsum_reduce<T><<<(H + 31) / 32, 1024, 0, st>>>(nb, H, pb, grad + d->off_b[d->n_hidden - 1]);
-    colsum_reduce<T><<<(n + 31) / 32, 1024, 0, st>>>(nb, n, pba, grad + d->off_adapter_b);
+    const int ob = d->off_b[d->n_hidden - 1];
+    if (d->off_adapter_w == ob + H && d->off_adapter_b == ob + H + H * n) {  // contiguous
+      colsum_reduce<T><<<(W + 31) / 32, 1024, 0, st>>>(nb, W, pa, grad + ob);
+    } else {
+      colsum_reduce<T><<<(H + 31) / 32, 1024, 0, st>>>(nb, H, pa, grad + ob, W);
+      colsum_reduce<T><<<(H * n + 31) / 32, 1024, 0, st>>>(nb, H * n, pa + H,
+                                                          grad + d->off_adapter_w, W);
+      colsum_reduce<T><<<(n + 31) / 32, 1024, 0, st>>>(nb, n, pa + H + H * n,
+                                                      grad + d->off_adapter_b, W);
+    }
     QPINN_CUDA_CHECK(cudaGetLastError());
   } else {
     if (int rc = tanh_bwd_and_bias<T>(R, n, g_act, act, g1, part, grad + d->off_adapter_b, st))
