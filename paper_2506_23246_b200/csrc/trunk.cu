@@ -467,6 +467,167 @@ __global__ void __launch_bounds__(256) features_bwd(int64_t R, int F, const T* _
   }
 }
 
+// fp32, F = 128 NC: the same two passes with a warp per point and a lane per 4
+// consecutive features of each 128-feature chunk, so every H0 / G0 row moves as 16-byte
+// vectors (HBM-bound passes; the scalar versions above issue 4x the memory instructions).
+// The lane's omega rows stay in registers across points.
+template <int NC>
+__global__ void __launch_bounds__(256) features_fwd_v4(int64_t R, int F, const float* __restrict__ x,
+                                                       const float* __restrict__ y,
+                                                       const float* __restrict__ t,
+                                                       const float* __restrict__ omega,
+                                                       const float* __restrict__ params,
+                                                       int64_t off_tau, float t_dom,
+                                                       float* __restrict__ H0, int nch) {
+  __shared__ float trig[kFeatPB][6];
+  const float tau = tau_of(params, off_tau, t_dom);
+  const float w = float(2.0 * kPi) / tau;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t W = 2 * (int64_t)F;
+  float om[NC][4][6];
+#pragma unroll
+  for (int c = 0; c < NC; ++c)
+#pragma unroll
+    for (int e = 0; e < 4; ++e)
+#pragma unroll
+      for (int j = 0; j < 6; ++j) om[c][e][j] = __ldg(omega + 6 * (128 * c + 4 * lane + e) + j);
+  for (int64_t p0 = (int64_t)blockIdx.x * kFeatPB; p0 < R; p0 += (int64_t)gridDim.x * kFeatPB) {
+    if (threadIdx.x < kFeatPB && p0 + threadIdx.x < R) {
+      const int64_t p = p0 + threadIdx.x;
+      float* tr = trig[threadIdx.x];
+      sincospif(x[p], &tr[0], &tr[1]);
+      sincospif(y[p], &tr[2], &tr[3]);
+      sincosf((t[p] * float(2.0 * kPi)) / tau, &tr[4], &tr[5]);
+    }
+    __syncthreads();
+    for (int pl = warp; pl < kFeatPB && p0 + pl < R; pl += 8) {
+      const int64_t p = p0 + pl;
+      const float* tr = trig[pl];
+      const float sx = tr[0], cx = tr[1], sy = tr[2], cy = tr[3], st = tr[4], ct = tr[5];
+#pragma unroll
+      for (int c = 0; c < NC; ++c) {
+        float cp[4], sp[4], dps[3][4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float* o = om[c][e];
+          const float proj = sx * o[0] + cx * o[1] + sy * o[2] + cy * o[3] + st * o[4] + ct * o[5];
+          sincosf(proj, &sp[e], &cp[e]);
+          dps[0][e] = float(kPi) * cx * o[0] - float(kPi) * sx * o[1];
+          dps[1][e] = float(kPi) * cy * o[2] - float(kPi) * sy * o[3];
+          dps[2][e] = w * ct * o[4] - w * st * o[5];
+        }
+        const int64_t f0 = 128 * c + 4 * lane;
+        float* row = H0 + p * W;
+        *reinterpret_cast<float4*>(row + f0) = make_float4(cp[0], cp[1], cp[2], cp[3]);
+        *reinterpret_cast<float4*>(row + F + f0) = make_float4(sp[0], sp[1], sp[2], sp[3]);
+        if (nch == 1) continue;
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+          float* rk = H0 + (int64_t)(k + 1) * R * W + p * W;
+          *reinterpret_cast<float4*>(rk + f0) =
+              make_float4(-sp[0] * dps[k][0], -sp[1] * dps[k][1], -sp[2] * dps[k][2], -sp[3] * dps[k][3]);
+          *reinterpret_cast<float4*>(rk + F + f0) =
+              make_float4(cp[0] * dps[k][0], cp[1] * dps[k][1], cp[2] * dps[k][2], cp[3] * dps[k][3]);
+        }
+      }
+    }
+    __syncthreads();
+  }
+}
+
+template <int NC>
+__global__ void __launch_bounds__(256) features_bwd_v4(int64_t R, int F, const float* __restrict__ x,
+                                                       const float* __restrict__ y,
+                                                       const float* __restrict__ t,
+                                                       const float* __restrict__ omega,
+                                                       const float* __restrict__ params,
+                                                       int64_t off_tau, float t_dom,
+                                                       const float* __restrict__ G0,
+                                                       double* __restrict__ partial) {
+  __shared__ float trig[kFeatBPB][7];
+  const float tau = tau_of(params, off_tau, t_dom);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t W = 2 * (int64_t)F;
+  const float w = float(2.0 * kPi) / tau;
+  float om[NC][4][6];
+#pragma unroll
+  for (int c = 0; c < NC; ++c)
+#pragma unroll
+    for (int e = 0; e < 4; ++e)
+#pragma unroll
+      for (int j = 0; j < 6; ++j) om[c][e][j] = __ldg(omega + 6 * (128 * c + 4 * lane + e) + j);
+  double acc = 0.0;
+  for (int64_t p0 = (int64_t)blockIdx.x * kFeatBPB; p0 < R; p0 += (int64_t)gridDim.x * kFeatBPB) {
+    if (threadIdx.x < kFeatBPB && p0 + threadIdx.x < R) {
+      const int64_t p = p0 + threadIdx.x;
+      float* tr = trig[threadIdx.x];
+      sincospif(x[p], &tr[0], &tr[1]);
+      sincospif(y[p], &tr[2], &tr[3]);
+      const float at = (t[p] * float(2.0 * kPi)) / tau;
+      sincosf(at, &tr[4], &tr[5]);
+      tr[6] = at;
+    }
+    __syncthreads();
+#pragma unroll 2
+    for (int pl = warp; pl < kFeatBPB && p0 + pl < R; pl += 8) {
+      const int64_t p = p0 + pl;
+      const float* tr = trig[pl];
+      const float sx = tr[0], cx = tr[1], sy = tr[2], cy = tr[3], st = tr[4], ct = tr[5], at = tr[6];
+      float G4 = 0.f, G5 = 0.f, D4 = 0.f, D5 = 0.f;
+#pragma unroll
+      for (int c = 0; c < NC; ++c) {
+        const int64_t f0 = 128 * c + 4 * lane;
+        float4 gv[4][2];  // [channel][cos half, sin half]
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const float* rk = G0 + (int64_t)k * R * W + p * W;
+          gv[k][0] = __ldg(reinterpret_cast<const float4*>(rk + f0));
+          gv[k][1] = __ldg(reinterpret_cast<const float4*>(rk + F + f0));
+        }
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float* o = om[c][e];
+          const float dps[3] = {float(kPi) * cx * o[0] - float(kPi) * sx * o[1],
+                                float(kPi) * cy * o[2] - float(kPi) * sy * o[3],
+                                w * ct * o[4] - w * st * o[5]};
+          const float proj = sx * o[0] + cx * o[1] + sy * o[2] + cy * o[3] + st * o[4] + ct * o[5];
+          float sp, cp;
+          sincosf(proj, &sp, &cp);
+          const float* g0c = &gv[0][0].x;
+          const float* g0s = &gv[0][1].x;
+          float gproj = -sp * g0c[e] + cp * g0s[e], gdp2 = 0.f;
+#pragma unroll
+          for (int k = 0; k < 3; ++k) {
+            const float gdc = (&gv[k + 1][0].x)[e], gds = (&gv[k + 1][1].x)[e];
+            gproj += -cp * dps[k] * gdc - sp * dps[k] * gds;
+            if (k == 2) gdp2 = -sp * gdc + cp * gds;
+          }
+          G4 += gproj * o[4];
+          G5 += gproj * o[5];
+          D4 += gdp2 * o[4];
+          D5 += gdp2 * o[5];
+        }
+      }
+      const float dat = -at / tau;
+      const float w2 = float(2.0 * kPi) / (tau * tau);
+      const float gt = G4 * ct * dat + G5 * (-st) * dat + D4 * (-w2 * ct + w2 * at * st) +
+                       D5 * (w2 * st + w2 * at * ct);
+      acc += (double)gt;
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int m = 16; m >= 1; m >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, m);
+  __shared__ double red[8];
+  if (lane == 0) red[warp] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double v = 0.0;
+    for (int w3 = 0; w3 < 8; ++w3) v += red[w3];
+    partial[blockIdx.x] = v;
+  }
+}
+
 // one block: strided per-thread sums, then a fixed-order tree (deterministic)
 template <typename T>
 __global__ void tau_grad_reduce(int nb, const double* __restrict__ partial, const T* __restrict__ params,
@@ -572,6 +733,15 @@ static int bias_grad(int64_t R, int N, const T* GU0, double* part, T* out, cudaS
   return QPINN_OK;
 }
 
+// QPINN_FEAT_V4=0: the scalar feature passes (A/B experiments)
+static bool feat_v4_off() {
+  static const bool off = [] {
+    const char* e = getenv("QPINN_FEAT_V4");
+    return e && atoi(e) == 0;
+  }();
+  return off;
+}
+
 // QPINN_FUSE_ADAPTER=0: the adapter as its own tensor-core layer (A/B experiments)
 static bool adapter_fusion_off() {
   static const bool off = [] {
@@ -590,8 +760,15 @@ static int forward_impl(const qpinn_trunk_desc* d, int64_t R, const T* x, const 
   T* H0 = (T*)(ws + w.h0);
   const int fb = (int)((R + kFeatPB - 1) / kFeatPB < num_sms() * 8 ? (R + kFeatPB - 1) / kFeatPB
                                                                    : num_sms() * 8);
-  features_fwd<T><<<fb > 0 ? fb : 1, 256, 0, st>>>(R, F, x, y, t, (const T*)d->omega, params,
-                                                  d->off_tau_raw, (T)d->t_domain, H0, nch);
+  if (sizeof(T) == 4 && (F == 128 || F == 256) && !feat_v4_off()) {
+    auto kern = F == 128 ? features_fwd_v4<1> : features_fwd_v4<2>;
+    kern<<<fb > 0 ? fb : 1, 256, 0, st>>>(R, F, (const float*)x, (const float*)y, (const float*)t,
+                                          (const float*)d->omega, (const float*)params,
+                                          d->off_tau_raw, (float)d->t_domain, (float*)H0, nch);
+  } else {
+    features_fwd<T><<<fb > 0 ? fb : 1, 256, 0, st>>>(R, F, x, y, t, (const T*)d->omega, params,
+                                                    d->off_tau_raw, (T)d->t_domain, H0, nch);
+  }
   QPINN_CUDA_CHECK(cudaGetLastError());
   const T* in = H0;
   int K = 2 * F;
@@ -717,9 +894,16 @@ static int backward_impl(const qpinn_trunk_desc* d, int64_t R, const T* x, const
   }
   // tau_raw through the time features
   double* tp = (double*)(ws + w.tau_part);
-  features_bwd<T><<<kTauBlocks, 256, 0, st>>>(R, F, x, y, t, (const T*)d->omega, params,
-                                               d->off_tau_raw, (T)d->t_domain,
-                                               (const T*)(ws + w.h0), g0, tp);
+  if (sizeof(T) == 4 && (F == 128 || F == 256) && !feat_v4_off()) {
+    auto kern = F == 128 ? features_bwd_v4<1> : features_bwd_v4<2>;
+    kern<<<kTauBlocks, 256, 0, st>>>(R, F, (const float*)x, (const float*)y, (const float*)t,
+                                     (const float*)d->omega, (const float*)params,
+                                     d->off_tau_raw, (float)d->t_domain, (const float*)g0, tp);
+  } else {
+    features_bwd<T><<<kTauBlocks, 256, 0, st>>>(R, F, x, y, t, (const T*)d->omega, params,
+                                                 d->off_tau_raw, (T)d->t_domain,
+                                                 (const T*)(ws + w.h0), g0, tp);
+  }
   tau_grad_reduce<T><<<1, 256, 0, st>>>(kTauBlocks, tp, params, d->off_tau_raw, (T)d->t_domain, grad);
   QPINN_CUDA_CHECK(cudaGetLastError());
   return QPINN_OK;
