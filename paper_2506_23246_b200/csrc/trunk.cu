@@ -244,8 +244,14 @@ __device__ __forceinline__ void lds_vec(const T* src, T (&dst)[NV]) {
     }
   }
 }
+#ifndef QPINN_ADB_MINB
+#define QPINN_ADB_MINB 5  // 102 registers, 5 blocks per SM: 69 -> 60 us (4 and 6-8 measured worse)
+#endif
+#ifndef QPINN_ADB_PB
+#define QPINN_ADB_PB 8
+#endif
 template <typename T, int NA>
-__global__ void __launch_bounds__(128) adapter_bwd(int64_t R, int Hd, int64_t rows_per, const T* __restrict__ g_act,
+__global__ void __launch_bounds__(128, QPINN_ADB_MINB) adapter_bwd(int64_t R, int Hd, int64_t rows_per, const T* __restrict__ g_act,
                             const T* __restrict__ act, const T* __restrict__ Hl,
                             const T* __restrict__ Wa, T* __restrict__ GU,
                             double* __restrict__ part) {
@@ -289,16 +295,17 @@ __global__ void __launch_bounds__(128) adapter_bwd(int64_t R, int Hd, int64_t ro
     if (tid < n)
       for (int pt = 0; pt < np; ++pt) acc_ba += (double)gua[pt][0][tid];
     if (col) {
-      // 8 points at a time with their 32 loads issued up front (latency bound otherwise)
-      for (int pb = 0; pb < np; pb += 8) {
-        T hb[8][4];
+      // PB points at a time with their 4 PB loads issued up front (latency bound otherwise)
+      constexpr int PB = QPINN_ADB_PB;
+      for (int pb = 0; pb < np; pb += PB) {
+        T hb[PB][4];
 #pragma unroll
-        for (int u = 0; u < 8; ++u)
+        for (int u = 0; u < PB; ++u)
 #pragma unroll
           for (int c = 0; c < 4; ++c)
             hb[u][c] = pb + u < np ? Hl[c * nH + (p0 + pb + u) * Hd + j] : T(0);
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
+      for (int u = 0; u < PB; ++u) {
         const int pt = pb + u;
         if (pt >= np) break;
         const int64_t i = (p0 + pt) * Hd + j;
