@@ -542,8 +542,11 @@ __global__ void __launch_bounds__(256) features_fwd_v4(int64_t R, int F, const f
   }
 }
 
+#ifndef QPINN_FB4_MINB
+#define QPINN_FB4_MINB 3  // 85 registers: 65 -> 62 us (4: 66 us)
+#endif
 template <int NC>
-__global__ void __launch_bounds__(256) features_bwd_v4(int64_t R, int F, const float* __restrict__ x,
+__global__ void __launch_bounds__(256, QPINN_FB4_MINB) features_bwd_v4(int64_t R, int F, const float* __restrict__ x,
                                                        const float* __restrict__ y,
                                                        const float* __restrict__ t,
                                                        const float* __restrict__ omega,
