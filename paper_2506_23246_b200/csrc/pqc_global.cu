@@ -1246,11 +1246,13 @@ bool hbm_supported(const qpinn_circuit* c, int dtype, const char* env, int min_n
 // Whole-state tiles (n <= 12) against the CTA kernels of pqc_big.cu, config 5
 // (profiles/r02/config5_hbm_vs_cta.txt): the adjoint is 1.2-4x faster from n = 12 for
 // every entangler and at n = 11 with CNOT entanglers or L = 1 (phase and no-entangler
-// adjoints at L >= 4 stay 10-20% faster on the CTA kernels); the forward is 1.0-1.7x
-// faster from n = 12 with L >= 2 (the n = 12, L = 1 forward stays 1.1-1.4x faster on
-// the CTA kernels); n <= 10 stays on the CTA kernels both ways.
+// adjoints at L >= 4 stay 10-20% faster on the CTA kernels); the n = 12 forward is
+// 1.6-1.7x faster with CNOT entanglers and L >= 2 and 1.03-1.08x with any entangler at
+// L = 8 (phase / none at L = 4: 0.95-1.0x, L = 1: 0.7-0.9x, kept on the CTA kernels);
+// n <= 10 stays on the CTA kernels both ways.
 bool hbm_fwd_supported(const qpinn_circuit* c, int dtype) {
-  return hbm_supported(c, dtype, "QPINN_PQC_HBM_FWD_MIN", c && c->L >= 2 ? 12 : 13);
+  const bool n12 = c && ((c->L >= 2 && layer_entangler(c) == ENT_PERM) || c->L >= 8);
+  return hbm_supported(c, dtype, "QPINN_PQC_HBM_FWD_MIN", n12 ? 12 : 13);
 }
 
 bool hbm_bwd_supported(const qpinn_circuit* c, int dtype) {
