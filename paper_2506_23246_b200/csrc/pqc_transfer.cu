@@ -26,6 +26,7 @@
 #include <mutex>
 
 #include "pqc_layer.h"
+#include "tc_gemm.cuh"
 #include "tc_gemm.h"
 
 namespace qpinn {
@@ -221,6 +222,8 @@ __device__ __forceinline__ void embed_phase(int b, float& pr, float& pi) {
 //   dL/dW' = m^T Abar   (D x 2D),   dL/dW[b] = Re p_b dL/dW'[b], dL/dW[D+b] = Im p_b dL/dW'[b]
 // which halves all three transfer GEMMs and the embedded-state traffic.
 // Wt [2D][D] = W'^T (forward GEMM operand) and W [D][2D] = W' (backward operand).
+// W' and W'^T go straight out as the tf32 hi / lo pairs the map's GEMMs take (W: hi
+// [D][2D] then lo; Wt: hi [2D][D] then lo), so no GEMM splits them again
 __global__ void tr_wmat(int n, const cplx<float>* __restrict__ B, float* __restrict__ W,
                         float* __restrict__ Wt) {
   const int D = 1 << n, D2 = 2 * D;
@@ -232,8 +235,11 @@ __global__ void tr_wmat(int n, const cplx<float>* __restrict__ B, float* __restr
     float pr, pi;
     embed_phase(r, pr, pi);
     const float v = pr * top + pi * bot;
-    W[i] = v;
-    Wt[(size_t)c * D + r] = v;
+    const float hi = tc::rna_tf32(v), lo = tc::rna_tf32(v - hi);
+    W[i] = hi;
+    W[(size_t)D * D2 + i] = lo;
+    Wt[(size_t)c * D + r] = hi;
+    Wt[(size_t)D * D2 + (size_t)c * D + r] = lo;
   }
 }
 
@@ -622,9 +628,17 @@ struct TrCircuit {
   cplx<float>* U;
   cplx<float>* ph;
   cplx<float>* CK;
-  float* W;
-  float* Wt;
+  float* W;   // W' [D][2D] tf32 hi, then lo
+  float* Wt;  // W'^T [2D][D] tf32 hi, then lo
 };
+
+// the split operands of the map's GEMMs: B = W'^T [2D, D] (forward), B = W' [D, 2D]
+inline tc::Wsplit split_wt(const TrCircuit& cc, int D) {
+  return tc::Wsplit{cc.Wt, cc.Wt + (size_t)2 * D * D, D};
+}
+inline tc::Wsplit split_w(const TrCircuit& cc, int D) {
+  return tc::Wsplit{cc.W, cc.W + (size_t)2 * D * D, 2 * D};
+}
 
 // hand-off layout (after the forward with tangents): [Psi | Phi | W | CK | U | ph]
 struct TrHandoff {
@@ -642,7 +656,7 @@ TrHandoff tr_handoff(const qpinn_circuit* c, int64_t R) {
   };
   h.psi = take(4 * (size_t)R * D2 * 4);
   h.phi = take(4 * (size_t)R * D * 4);
-  h.W = take(4 * D * D2);
+  h.W = take(2 * 4 * D * D2);  // tf32 hi / lo
   h.CK = take(cs * D * D * c->L);
   h.U = take(cs * 4 * c->n_u1);
   h.ph = take(cs * D * c->n_phase);
@@ -727,11 +741,13 @@ int fwd_n(const qpinn_circuit* c, const KArgs<float>* a, unsigned char* ws, cons
   tr_embed<NQ><<<grid_points(a->R), 256, 0, st>>>(a->scale, a->R, a->act, a->tan, Phi, a->maxabs);
   QPINN_CUDA_CHECK(cudaGetLastError());
   if (NQ == 7 && ns == 4 && !fused_readout_off()) {  // map + readout in one tensor-core pass
+    const tc::Wsplit wt = split_wt(cc, D);
     return tc::gemm3_readout(a->R, Phi, cc.Wt, Psi, a->z, a->dz, ws + t.g3,
-                             tc::gemm3_workspace_bytes(D2, D2), st);
+                             tc::gemm3_workspace_bytes(D2, D2), st, &wt);
   }
+  const tc::Wsplit wt = split_wt(cc, D);
   if (int rc = tc::gemm3(ns * a->R, D2, D, Phi, D, cc.Wt, D, Psi, D2, ws + t.g3,
-                         tc::gemm3_workspace_bytes(D2, D2), st))
+                         tc::gemm3_workspace_bytes(D2, D2), st, &wt))
     return rc;
   tr_readout<NQ><<<grid_points(a->R), 256, 0, st>>>(a->R, ns, Psi, a->z, a->dz);
   QPINN_CUDA_CHECK(cudaGetLastError());
@@ -763,8 +779,9 @@ int bwd_n(const qpinn_circuit* c, const KArgs<float>* a, unsigned char* ws, cons
     if (int rc = build_transfer(c, a->qp, cc, (cplx<float>*)(ws + t.B), st)) return rc;
     tr_embed<NQ><<<gp, 256, 0, st>>>(a->scale, a->R, a->act, a->tan, Abar, nullptr);
     QPINN_CUDA_CHECK(cudaGetLastError());
+    const tc::Wsplit wt = split_wt(cc, D);
     if (int rc = tc::gemm3(4 * a->R, D2, D, Abar, D, cc.Wt, D, G, D2, ws + t.g3,
-                           tc::gemm3_workspace_bytes(D2, D2), st))
+                           tc::gemm3_workspace_bytes(D2, D2), st, &wt))
       return rc;
     Psi = G;
     Phi = nullptr;  // re-embedded after the embedding gradient
@@ -814,8 +831,9 @@ int bwd_n(const qpinn_circuit* c, const KArgs<float>* a, unsigned char* ws, cons
     join.st = st;
   }
   // dL/dm = Abar W'^T  (D per row)
+  const tc::Wsplit wsp = split_w(cc, D);
   if (int rc = tc::gemm3(4 * a->R, D, D2, Abar, D2, cc.W, D2, G, D, ws + t.g3,
-                         tc::gemm3_workspace_bytes(D2, D2), st))
+                         tc::gemm3_workspace_bytes(D2, D2), st, &wsp))
     return rc;
   if (side)
     if (int rc = weight_chain(side->s)) return rc;

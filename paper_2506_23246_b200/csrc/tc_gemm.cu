@@ -25,6 +25,7 @@
 #include <mutex>
 
 #include "tc_gemm.cuh"
+#include "tc_gemm.h"
 
 namespace qpinn {
 namespace tc {
@@ -1174,6 +1175,24 @@ __global__ void split_rows(const float* __restrict__ B, int N, int K, int64_t ld
   }
 }
 
+struct SplitJobs {
+  SplitJob j[kMaxSplitJobs];
+};
+
+// every weight split of a step in one launch (blockIdx.y = job)
+__global__ void split_batch(SplitJobs jobs) {
+  const SplitJob& b = jobs.j[blockIdx.y];
+  const int64_t n = (int64_t)b.N * b.ldk;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int r = (int)(i / b.ldk), c = (int)(i % b.ldk);
+    const float v = c < b.K ? (b.transpose ? b.src[(int64_t)c * b.ld + r] : b.src[r * b.ld + c]) : 0.f;
+    const float h = rna_tf32(v);
+    b.hi[i] = h;
+    b.lo[i] = rna_tf32(v - h);
+  }
+}
+
 // W [K,N] row-major (a layer's weights) -> (W^T)_hi, (W^T)_lo [N, ldk]
 __global__ void split_transpose(const float* __restrict__ W, int K, int N, int ldk,
                                 float* __restrict__ hi, float* __restrict__ lo) {
@@ -1223,6 +1242,16 @@ static int make_map(CUtensorMap* m, const float* base, uint64_t rows, uint64_t c
 }
 
 static inline int ldk_of(int K) { return (K + 3) & ~3; }
+
+int split_weights(const SplitJob* jobs, int njobs, cudaStream_t st) {
+  if (njobs < 0 || njobs > kMaxSplitJobs) return fail(QPINN_ERR_CONFIG, "split_weights: jobs");
+  if (njobs == 0) return QPINN_OK;
+  SplitJobs jj{};
+  for (int i = 0; i < njobs; ++i) jj.j[i] = jobs[i];
+  split_batch<<<dim3(16, (unsigned)njobs), 256, 0, st>>>(jj);
+  QPINN_CUDA_CHECK(cudaGetLastError());
+  return QPINN_OK;
+}
 
 size_t gemm3_workspace_bytes(int N, int K) { return 2 * (size_t)N * ldk_of(K) * 4 + 256; }
 
@@ -1348,15 +1377,25 @@ static int dispatch(const GemmArgs& g, const float* A, int64_t lda, const float*
 }
 
 int gemm3(int64_t M, int N, int K, const float* A, int64_t lda, const float* B, int64_t ldb,
-          float* C, int64_t ldc, void* ws, size_t ws_bytes, cudaStream_t st) {
+          float* C, int64_t ldc, void* ws, size_t ws_bytes, cudaStream_t st, const Wsplit* pre) {
   if (M < 0 || N < 1 || K < 1) return fail(QPINN_ERR_CONFIG, "gemm3: bad shape");
   if (ws_bytes < gemm3_workspace_bytes(N, K)) return fail(QPINN_ERR_CONFIG, "gemm3: workspace");
   if (M == 0) return QPINN_OK;
-  const int ldk = ldk_of(K);
-  float* hi = (float*)(((uintptr_t)ws + 255) & ~(uintptr_t)255);
-  float* lo = hi + (size_t)N * ldk;
-  split_rows<<<64, 256, 0, st>>>(B, N, K, ldb, ldk, hi, lo);
-  QPINN_CUDA_CHECK(cudaGetLastError());
+  int ldk = ldk_of(K);
+  const float* hi;
+  const float* lo;
+  if (pre) {  // split once per step by the caller (split_weights)
+    hi = pre->hi;
+    lo = pre->lo;
+    ldk = pre->ldk;
+  } else {
+    float* h = (float*)(((uintptr_t)ws + 255) & ~(uintptr_t)255);
+    float* l = h + (size_t)N * ldk;
+    split_rows<<<64, 256, 0, st>>>(B, N, K, ldb, ldk, h, l);
+    QPINN_CUDA_CHECK(cudaGetLastError());
+    hi = h;
+    lo = l;
+  }
   GemmArgs g{M, 0, N, K, C, ldc, nullptr, 0, nullptr, nullptr, nullptr, nullptr, nullptr, 0};
   return dispatch<EPI_STORE>(g, A, lda, hi, lo, ldk, st);
 }
@@ -1364,15 +1403,25 @@ int gemm3(int64_t M, int N, int K, const float* A, int64_t lda, const float* B, 
 // Psi [4R, 256] = Phi [4R, 128] Wt^T (Wt [256, 128]) with the fused Pauli-Z readout:
 // z [R, 7], dz [3, R, 7] (the n = 7 transfer-matrix forward with tangents)
 int gemm3_readout(int64_t R, const float* Phi, const float* Wt, float* Psi, float* z, float* dz,
-                  void* ws, size_t ws_bytes, cudaStream_t st) {
+                  void* ws, size_t ws_bytes, cudaStream_t st, const Wsplit* pre) {
   constexpr int N = 256, K = 128;
   if (ws_bytes < gemm3_workspace_bytes(N, K)) return fail(QPINN_ERR_CONFIG, "gemm3: workspace");
   if (R == 0) return QPINN_OK;
-  const int ldk = ldk_of(K);
-  float* hi = (float*)(((uintptr_t)ws + 255) & ~(uintptr_t)255);
-  float* lo = hi + (size_t)N * ldk;
-  split_rows<<<64, 256, 0, st>>>(Wt, N, K, K, ldk, hi, lo);
-  QPINN_CUDA_CHECK(cudaGetLastError());
+  int ldk = ldk_of(K);
+  const float* hi;
+  const float* lo;
+  if (pre) {  // split once per step by the caller (split_weights)
+    hi = pre->hi;
+    lo = pre->lo;
+    ldk = pre->ldk;
+  } else {
+    float* h = (float*)(((uintptr_t)ws + 255) & ~(uintptr_t)255);
+    float* l = h + (size_t)N * ldk;
+    split_rows<<<64, 256, 0, st>>>(Wt, N, K, K, ldk, h, l);
+    QPINN_CUDA_CHECK(cudaGetLastError());
+    hi = h;
+    lo = l;
+  }
   GemmArgs g{4 * R, R, N, K, Psi, N, nullptr, 0, z, dz, nullptr, nullptr, nullptr, 0};
   return launch_gemm3<128, EPI_READOUT>(g, Phi, K, hi, lo, ldk, st);
 }
@@ -1429,28 +1478,48 @@ int wgrad(int64_t rows, int Kin, int Nout, const float* X, int64_t ldx, const fl
 
 // H [R, N] = tanh(X [R, K] W [K, N] + b): the value-only dense layer (inference)
 int dense_tanh1(int64_t R, int N, int K, const float* X, const float* W, const float* bias,
-                float* H, void* ws, size_t ws_bytes, cudaStream_t st) {
+                float* H, void* ws, size_t ws_bytes, cudaStream_t st, const Wsplit* pre) {
   if (ws_bytes < gemm3_workspace_bytes(N, K)) return fail(QPINN_ERR_CONFIG, "dense: workspace");
   if (R == 0) return QPINN_OK;
-  const int ldk = ldk_of(K);
-  float* hi = (float*)(((uintptr_t)ws + 255) & ~(uintptr_t)255);
-  float* lo = hi + (size_t)N * ldk;
-  split_transpose<<<64, 256, 0, st>>>(W, K, N, ldk, hi, lo);
-  QPINN_CUDA_CHECK(cudaGetLastError());
+  int ldk = ldk_of(K);
+  const float* hi;
+  const float* lo;
+  if (pre) {  // split once per step by the caller (split_weights)
+    hi = pre->hi;
+    lo = pre->lo;
+    ldk = pre->ldk;
+  } else {
+    float* h = (float*)(((uintptr_t)ws + 255) & ~(uintptr_t)255);
+    float* l = h + (size_t)N * ldk;
+    split_transpose<<<64, 256, 0, st>>>(W, K, N, ldk, h, l);
+    QPINN_CUDA_CHECK(cudaGetLastError());
+    hi = h;
+    lo = l;
+  }
   GemmArgs g{R, R, N, K, H, N, bias, 0, nullptr, nullptr, nullptr, nullptr, nullptr, 0};
   return dispatch<EPI_TANH1>(g, X, K, hi, lo, ldk, st);
 }
 
 // H [4R, N] = dual tanh of X [4R, K] W [K, N] + b (channel blocks of R rows)
 int dense_tanh(int64_t R, int N, int K, const float* X, const float* W, const float* bias,
-               float* H, void* ws, size_t ws_bytes, cudaStream_t st) {
+               float* H, void* ws, size_t ws_bytes, cudaStream_t st, const Wsplit* pre) {
   if (ws_bytes < gemm3_workspace_bytes(N, K)) return fail(QPINN_ERR_CONFIG, "dense: workspace");
   if (R == 0) return QPINN_OK;
-  const int ldk = ldk_of(K);
-  float* hi = (float*)(((uintptr_t)ws + 255) & ~(uintptr_t)255);
-  float* lo = hi + (size_t)N * ldk;
-  split_transpose<<<64, 256, 0, st>>>(W, K, N, ldk, hi, lo);
-  QPINN_CUDA_CHECK(cudaGetLastError());
+  int ldk = ldk_of(K);
+  const float* hi;
+  const float* lo;
+  if (pre) {  // split once per step by the caller (split_weights)
+    hi = pre->hi;
+    lo = pre->lo;
+    ldk = pre->ldk;
+  } else {
+    float* h = (float*)(((uintptr_t)ws + 255) & ~(uintptr_t)255);
+    float* l = h + (size_t)N * ldk;
+    split_transpose<<<64, 256, 0, st>>>(W, K, N, ldk, h, l);
+    QPINN_CUDA_CHECK(cudaGetLastError());
+    hi = h;
+    lo = l;
+  }
   GemmArgs g{4 * R, R, N, K, H, N, bias, 0, nullptr, nullptr, nullptr, nullptr, nullptr, 0};
   return dispatch<EPI_TANH>(g, X, K, hi, lo, ldk, st);
 }
@@ -1459,15 +1528,25 @@ int dense_tanh(int64_t R, int N, int K, const float* X, const float* W, const fl
 // act [4R, n_ad] = dual tanh(H Wa + ba) (N <= 128, n_ad <= 8)
 int dense_tanh_adapter(int64_t R, int N, int K, const float* X, const float* W, const float* bias,
                        float* H, const float* Wa, const float* ba, int n_ad, float* act, void* ws,
-                       size_t ws_bytes, cudaStream_t st) {
+                       size_t ws_bytes, cudaStream_t st, const Wsplit* pre) {
   if (ws_bytes < gemm3_workspace_bytes(N, K)) return fail(QPINN_ERR_CONFIG, "dense: workspace");
   if (N > 128 || n_ad < 1 || n_ad > 8) return fail(QPINN_ERR_CONFIG, "fused adapter: shape");
   if (R == 0) return QPINN_OK;
-  const int ldk = ldk_of(K);
-  float* hi = (float*)(((uintptr_t)ws + 255) & ~(uintptr_t)255);
-  float* lo = hi + (size_t)N * ldk;
-  split_transpose<<<64, 256, 0, st>>>(W, K, N, ldk, hi, lo);
-  QPINN_CUDA_CHECK(cudaGetLastError());
+  int ldk = ldk_of(K);
+  const float* hi;
+  const float* lo;
+  if (pre) {  // split once per step by the caller (split_weights)
+    hi = pre->hi;
+    lo = pre->lo;
+    ldk = pre->ldk;
+  } else {
+    float* h = (float*)(((uintptr_t)ws + 255) & ~(uintptr_t)255);
+    float* l = h + (size_t)N * ldk;
+    split_transpose<<<64, 256, 0, st>>>(W, K, N, ldk, h, l);
+    QPINN_CUDA_CHECK(cudaGetLastError());
+    hi = h;
+    lo = l;
+  }
   GemmArgs g{4 * R, R, N, K, H, N, bias, 0, nullptr, nullptr, Wa, ba, act, n_ad};
   return launch_gemm3<128, EPI_TANH>(g, X, K, hi, lo, ldk, st);
 }

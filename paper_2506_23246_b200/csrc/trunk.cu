@@ -660,8 +660,55 @@ __global__ void tau_grad_reduce(int nb, const double* __restrict__ partial, cons
 
 // ---- workspace plan ----------------------------------------------------------------------------
 struct TrunkWS {
-  size_t h0, u, h[8], g0, g1, part, apart, tau_part, wsplit, total;
+  size_t h0, u, h[8], g0, g1, part, apart, tau_part, wcache, wsplit, total;
 };
+
+// float32: every dense layer's weights split into tf32 hi / lo once per forward (one
+// split_weights launch), in the two layouts the GEMMs take: forward B = W^T [H, K_in]
+// and input-gradient B = W [K_in, H]; the backward reuses the forward's splits (it
+// already requires the forward's activations in the same workspace)
+struct WCache {
+  tc::Wsplit fwd[8], bwd[8], ad;
+};
+
+static size_t wcache_bytes(const qpinn_trunk_desc* d) {
+  size_t b = 0;
+  const int H = d->hidden;
+  for (int i = 0; i < d->n_hidden; ++i) {
+    const int K = i == 0 ? 2 * d->rff : H;
+    b += 2 * ((size_t)H * tc::split_ldk(K) + (size_t)K * tc::split_ldk(H)) * 4;
+  }
+  const int Kl = d->n_hidden ? H : 2 * d->rff;
+  b += 2 * (size_t)d->n_out * tc::split_ldk(Kl) * 4;
+  return b + 256;
+}
+
+// carve the cache and, when jobs is given, list the splits that fill it
+static WCache wcache_of(const qpinn_trunk_desc* d, unsigned char* base, const float* params,
+                        tc::SplitJob* jobs, int* njobs) {
+  WCache c{};
+  float* o = (float*)(((uintptr_t)base + 255) & ~(uintptr_t)255);
+  const int H = d->hidden;
+  int nj = 0;
+  auto take = [&](int N, int K, const float* src, int transpose, int64_t ld) {
+    const int ldk = tc::split_ldk(K);
+    float* hi = o;
+    float* lo = o + (size_t)N * ldk;
+    o = lo + (size_t)N * ldk;
+    if (jobs) jobs[nj++] = tc::SplitJob{src, N, K, transpose, ldk, ld, hi, lo};
+    return tc::Wsplit{hi, lo, ldk};
+  };
+  for (int i = 0; i < d->n_hidden; ++i) {
+    const int K = i == 0 ? 2 * d->rff : H;
+    const float* W = params + d->off_w[i];  // [K, H] row-major
+    c.fwd[i] = take(H, K, W, 1, H);
+    c.bwd[i] = take(K, H, W, 0, H);
+  }
+  const int Kl = d->n_hidden ? H : 2 * d->rff;
+  c.ad = take(d->n_out, Kl, params + d->off_adapter_w, 1, d->n_out);
+  if (njobs) *njobs = nj;
+  return c;
+}
 
 constexpr int kColBlocks = 256;
 constexpr int kTanhBlocks = 592;  // 4 per SM for the fused reverse dual tanh
@@ -691,6 +738,8 @@ static TrunkWS trunk_ws(const qpinn_trunk_desc* d, size_t es, int64_t R) {
   o += ((size_t)kAdBlocks * (H * d->n_out + H + d->n_out) * 8 + 255) / 256 * 256;
   w.tau_part = o;
   o += (kTauBlocks * 8 + 255) / 256 * 256;
+  w.wcache = o;
+  if (es == 4) o += (wcache_bytes(d) + 255) / 256 * 256;
   // float32 tensor-core scratch, used by one GEMM at a time: the tf32 hi/lo
   // split of a weight matrix, or the split-K partials of a weight gradient
   w.wsplit = o;
@@ -785,14 +834,22 @@ static int forward_impl(const qpinn_trunk_desc* d, int64_t R, const T* x, const 
   cublasHandle_t h;
   if (int rc = blas_handle(st, &h)) return rc;
   T* U = (T*)(ws + w.u);
+  WCache wc{};
+  if constexpr (sizeof(T) == 4) {  // this forward's weight splits, one launch
+    tc::SplitJob jobs[tc::kMaxSplitJobs];
+    int nj = 0;
+    wc = wcache_of(d, ws + w.wcache, (const float*)params, jobs, &nj);
+    if (int rc = tc::split_weights(jobs, nj, st)) return rc;
+  }
   // one dense layer + dual tanh: tensor cores (float32, 16-byte aligned rows) or cuBLAS
-  auto dense = [&](int Kin, int N, const T* X, int64_t off_w, int64_t off_b, T* out) -> int {
+  auto dense = [&](int Kin, int N, const T* X, int64_t off_w, int64_t off_b, T* out,
+                   const tc::Wsplit* pre) -> int {
     if constexpr (sizeof(T) == 4) {
       if (Kin % 4 == 0)
         return nch == 4 ? tc::dense_tanh(R, N, Kin, X, params + off_w, params + off_b, out,
-                                         ws + w.wsplit, w.total - w.wsplit, st)
+                                         ws + w.wsplit, w.total - w.wsplit, st, pre)
                         : tc::dense_tanh1(R, N, Kin, X, params + off_w, params + off_b, out,
-                                          ws + w.wsplit, w.total - w.wsplit, st);
+                                          ws + w.wsplit, w.total - w.wsplit, st, pre);
     }
     if (int rc = gemm_rm<T>(h, false, false, nch * R, N, Kin, X, Kin, params + off_w, N, U, N,
                             T(0)))
@@ -814,13 +871,13 @@ static int forward_impl(const qpinn_trunk_desc* d, int64_t R, const T* x, const 
         return tc::dense_tanh_adapter(R, H, K, (const float*)in, params + d->off_w[i],
                                       params + d->off_b[i], Hn, params + d->off_adapter_w,
                                       params + d->off_adapter_b, n, act, ws + w.wsplit,
-                                      w.total - w.wsplit, st);
+                                      w.total - w.wsplit, st, &wc.fwd[i]);
     }
-    if (int rc = dense(K, H, in, d->off_w[i], d->off_b[i], Hn)) return rc;
+    if (int rc = dense(K, H, in, d->off_w[i], d->off_b[i], Hn, &wc.fwd[i])) return rc;
     in = Hn;
     K = H;
   }
-  return dense(K, n, in, d->off_adapter_w, d->off_adapter_b, act);
+  return dense(K, n, in, d->off_adapter_w, d->off_adapter_b, act, &wc.ad);
 }
 
 template <typename T>
@@ -894,8 +951,9 @@ static int backward_impl(const qpinn_trunk_desc* d, int64_t R, const T* x, const
       return rc;
     }
     if (sizeof(T) == 4 && H % 4 == 0) {  // dL/dH_in = GU W^T on the tensor cores
+      const WCache wc = wcache_of(d, ws + w.wcache, (const float*)params, nullptr, nullptr);
       if (int rc = tc::gemm3(4 * R, K, H, (const float*)g1, H, (const float*)(params + d->off_w[i]),
-                             H, (float*)g0, K, ws + w.wsplit, w.total - w.wsplit, st))
+                             H, (float*)g0, K, ws + w.wsplit, w.total - w.wsplit, st, &wc.bwd[i]))
         return rc;
     } else if (int rc = gemm_rm<T>(h, false, true, 4 * R, K, H, g1, H, params + d->off_w[i], H, g0,
                                    K, T(0))) {

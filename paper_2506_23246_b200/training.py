@@ -263,6 +263,29 @@ class TrainResult:
 
 # -- the step engine ---------------------------------------------------------------------
 
+def _graph_kernel_nodes(g) -> Optional[int]:
+    """Kernel nodes of a captured step graph (cuda-python on the raw cudaGraph_t; the
+    step's own kernels plus the few torch elementwise ops inside it); None when the
+    bindings are unavailable."""
+    try:
+        import cuda.bindings.runtime as rt
+        graph = rt.cudaGraph_t(init_value=int(g.raw_cuda_graph()))
+        err, _, n = rt.cudaGraphGetNodes(graph, 0)
+        if err != rt.cudaError_t.cudaSuccess:
+            return None
+        err, nodes, n = rt.cudaGraphGetNodes(graph, n)
+        if err != rt.cudaError_t.cudaSuccess:
+            return None
+        k = 0
+        for nd in nodes[:n]:
+            err, t = rt.cudaGraphNodeGetType(nd)
+            if err == rt.cudaError_t.cudaSuccess and t == rt.cudaGraphNodeType.cudaGraphNodeTypeKernel:
+                k += 1
+        return k
+    except Exception:  # noqa: BLE001 - instrumentation only
+        return None
+
+
 class Trainer:
     """Device-resident QPINN epoch step (training.py:359-407; probes run in ``train``)."""
 
@@ -439,12 +462,16 @@ class Trainer:
             key = (self.weights.data_ptr() if self.weights is not None else 0, par)
             entry = self._graphs.get(key)
             if entry is None:
-                g = torch.cuda.CUDAGraph()
+                g = torch.cuda.CUDAGraph(keep_graph=True)
                 l0 = N.LAUNCHES["count"]
                 with torch.cuda.graph(g):
                     self._local_sweep()
-                entry = (g, N.LAUNCHES["count"] - l0)
+                # launches per replay: the graph's kernel nodes when cuda-python can
+                # read them, else the count the wrappers declared while capturing
+                nodes = _graph_kernel_nodes(g)
+                entry = (g, nodes if nodes is not None else N.LAUNCHES["count"] - l0)
                 N.LAUNCHES["count"] = l0
+                g.instantiate()
                 self._graphs[key] = entry
             entry[0].replay()
             N.count_launches(entry[1])
