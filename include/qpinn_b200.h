@@ -98,7 +98,14 @@ int qpinn_pqc_max_qubits(int dtype);
 
 /* ---- PQC forward + tangents (K1) and adjoint backward (K2) -------------- */
 /* Device scratch needed by forward/backward for `rows` points (the
- * transfer-matrix kernels stage [4 rows, 2^(n+1)] float32 operands here). */
+ * transfer-matrix kernels stage [4 rows, 2^(n+1)] float32 operands here).
+ * Beyond qpinn_pqc_max_qubits the statevectors no longer fit registers: the
+ * CTA / cluster kernels hold a point's states in shared memory, and for
+ * float32 standard layer plans the multi-gate HBM passes take over (forward
+ * from n = 12 with CNOT entanglers and L >= 2, or L >= 8, else from n = 13;
+ * adjoint from n = 12, and n = 11 with CNOT entanglers or L = 1), streaming
+ * batches of points' states through this scratch: up to ~256 MB for the
+ * forward and ~1 GB (states, adjoints, layer checkpoints) for the adjoint. */
 size_t qpinn_pqc_workspace_bytes(const qpinn_circuit* c, int dtype, int64_t rows);
 
 /* Bytes of the optional state hand-off buffer that lets the backward skip
