@@ -734,12 +734,38 @@ int fwd_n(const qpinn_circuit* c, const KArgs<float>* a, unsigned char* ws, cons
     cc.CK = (cplx<float>*)(hs + h.CK);
     cc.W = (float*)(hs + h.W);
   }
-  if (int rc = build_transfer(c, a->qp, cc, (cplx<float>*)(ws + t.B), st)) return rc;
   auto* Psi = a->states ? (float*)(hs + h.psi) : (float*)(ws + t.BUF2);
   auto* Phi = handoff ? (float*)(hs + h.phi) : (float*)(ws + t.BUF1);
   const int ns = a->tan ? 4 : 1;
-  tr_embed<NQ><<<grid_points(a->R), 256, 0, st>>>(a->scale, a->R, a->act, a->tan, Phi, a->maxabs);
-  QPINN_CUDA_CHECK(cudaGetLastError());
+  {
+    // the circuit's transfer map depends on qparams only: it is built on the side
+    // stream while the points are embedded, and joined before the map's GEMM
+    SideStream* side = nullptr;
+    static const bool serial = getenv("QPINN_SERIAL_BWD") != nullptr;  // A/B switch
+    if (!serial)
+      if (int rc = side_stream(st, &side)) return rc;
+    struct Join {  // every return path joins a forked side stream back into `st`
+      SideStream* side = nullptr;
+      cudaStream_t st = nullptr;
+      ~Join() {
+        if (side) {
+          cudaEventRecord(side->join, side->s);
+          cudaStreamWaitEvent(st, side->join, 0);
+        }
+      }
+    } join;
+    if (side) {
+      QPINN_CUDA_CHECK(cudaEventRecord(side->fork, st));
+      QPINN_CUDA_CHECK(cudaStreamWaitEvent(side->s, side->fork, 0));
+      join.side = side;
+      join.st = st;
+    }
+    if (int rc = build_transfer(c, a->qp, cc, (cplx<float>*)(ws + t.B), side ? side->s : st))
+      return rc;
+    tr_embed<NQ><<<grid_points(a->R), 256, 0, st>>>(a->scale, a->R, a->act, a->tan, Phi,
+                                                    a->maxabs);
+    QPINN_CUDA_CHECK(cudaGetLastError());
+  }
   if (NQ == 7 && ns == 4 && !fused_readout_off()) {  // map + readout in one tensor-core pass
     const tc::Wsplit wt = split_wt(cc, D);
     return tc::gemm3_readout(a->R, Phi, cc.Wt, Psi, a->z, a->dz, ws + t.g3,
