@@ -682,7 +682,7 @@ size_t qpinn_pqc_workspace_bytes(const qpinn_circuit* c, int dtype, int64_t rows
   if (!c) return 0;
   if (c->n > qpinn_pqc_max_qubits(dtype))
     return align_up(big_workspace_bytes(c, dtype), 256) +
-           global_adjoint_workspace_bytes(c, dtype);
+           global_adjoint_workspace_bytes(c, dtype, rows);
   size_t b = small_ws_bytes(c);
   if (transfer_supported(c, dtype)) b += transfer_workspace_bytes(c, rows);
   return b;

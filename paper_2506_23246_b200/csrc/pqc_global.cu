@@ -1453,29 +1453,34 @@ int hbm_backward(const qpinn_circuit* c, const KArgs<float>* a, unsigned char* w
   return pqc_param_grads<float>(c, acc, n, a->qp, a->g_qp, st);
 }
 
-size_t hbm_bwd_workspace_bytes(const qpinn_circuit* c) {
+size_t hbm_bwd_workspace_bytes(const qpinn_circuit* c, int64_t rows) {
   const HbBwdPlan bp = hb_plan_bwd(c);
   const int nops = (int)(bp.fwd.ops.size() + bp.rev.ops.size());
   const int nluts = (int)(bp.fwd.luts.size() + bp.rev.luts.size());
-  // ~1 GB of batch state: X, A and L checkpoints per point
+  // ~1 GB of batch state: X, A and L checkpoints per point (no more points than rows)
   const int64_t per = (int64_t)(2 + c->L) * 4 * ((int64_t)8 << c->n);
   int64_t B = ((int64_t)1 << 30) / per;
-  B = B < 1 ? 1 : std::min<int64_t>(B, hb_bwd_bcap(c->n));
+  B = std::min<int64_t>(B, hb_bwd_bcap(c->n));
+  if (rows >= 0) B = std::min<int64_t>(B, rows);
+  B = B < 1 ? 1 : B;
   return hb_bwd_layout(c, B, nops, nluts).total;
 }
 
-size_t global_adjoint_workspace_bytes(const qpinn_circuit* c, int dtype) {
+size_t global_adjoint_workspace_bytes(const qpinn_circuit* c, int dtype, int64_t rows) {
   if (dtype == QPINN_F64) return gb_layout<double>(c).total;
   // the multi-gate forward reuses this region with batches of ~256 MB of state
-  // (1024 points at n = 13), so few launches carry the batch loop
+  // (1024 points at n = 13), so few launches carry the batch loop; both passes size
+  // their batch to the call's rows when that is smaller
   const size_t g = gb_layout<float>(c).total;
   size_t h = 0;
   if (hbm_fwd_supported(c, dtype)) {
-    const int64_t B = ((int64_t)256 << 20) / (4 * ((int64_t)8 << c->n));
+    int64_t B = ((int64_t)256 << 20) / (4 * ((int64_t)8 << c->n));
+    B = std::min<int64_t>(B, hb_fwd_bcap(c->n));
+    if (rows >= 0) B = std::min<int64_t>(B, rows);
     const HbPlan plan = hb_plan(c);
     h = hb_layout(c, B < 1 ? 1 : B, (int)plan.ops.size(), (int)plan.luts.size()).total;
   }
-  if (hbm_bwd_supported(c, dtype)) h = std::max(h, hbm_bwd_workspace_bytes(c));
+  if (hbm_bwd_supported(c, dtype)) h = std::max(h, hbm_bwd_workspace_bytes(c, rows));
   return h > g ? h : g;
 }
 

@@ -58,7 +58,7 @@ template <typename T>
 int pqc_param_grads(const qpinn_circuit* c, const double* tot, int ab, const T* qp, T* g_qp,
                     cudaStream_t st);
 // HBM-regime adjoint (pqc_global.cu)
-size_t global_adjoint_workspace_bytes(const qpinn_circuit* c, int dtype);
+size_t global_adjoint_workspace_bytes(const qpinn_circuit* c, int dtype, int64_t rows = -1);
 template <typename T>
 int global_backward(const qpinn_circuit* c, const KArgs<T>* a, unsigned char* ws, size_t bytes);
 template <typename T>
@@ -71,7 +71,7 @@ int hbm_forward(const qpinn_circuit* c, const KArgs<float>* a, unsigned char* ws
 int hbm_forward_passes(const qpinn_circuit* c);
 bool hbm_bwd_supported(const qpinn_circuit* c, int dtype);
 int hbm_backward(const qpinn_circuit* c, const KArgs<float>* a, unsigned char* ws, size_t bytes);
-size_t hbm_bwd_workspace_bytes(const qpinn_circuit* c);
+size_t hbm_bwd_workspace_bytes(const qpinn_circuit* c, int64_t rows = -1);
 // transfer-matrix K1 / K2 on the tensor cores (pqc_transfer.cu)
 bool transfer_supported(const qpinn_circuit* c, int dtype);
 size_t transfer_workspace_bytes(const qpinn_circuit* c, int64_t R);
