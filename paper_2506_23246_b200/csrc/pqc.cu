@@ -666,9 +666,10 @@ static size_t small_ws_bytes(const qpinn_circuit* c) {
 }
 
 // the transfer-matrix kernels (pqc_transfer.cu): variant 2, and the default for
-// float32 n = 5, 6, 7 (measured with the phase-folded map, 2^16 points, L = 4,
+// float32 n = 5..8 (measured with the phase-folded map, 2^16 points, L = 4,
 // K1 + K2: n = 7 0.69 ms vs 1.74 ms for the layer kernels, n = 6 0.41 vs 0.82,
-// n = 5 0.32 vs 0.37-0.39; profiles/r01/transfer_vs_layer_folded.txt)
+// n = 5 0.32 vs 0.37-0.39; profiles/r01/transfer_vs_layer_folded.txt; n = 8 at
+// 2^17 points: 3.7 vs 13.2 ms, profiles/r02/config5_n8_transfer_vs_layer.txt)
 static bool use_transfer(const qpinn_circuit* c, int dtype) {
   if (!transfer_supported(c, dtype)) return false;
   return c->variant == 2 || c->variant == 0;

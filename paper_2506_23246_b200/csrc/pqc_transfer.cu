@@ -20,8 +20,9 @@
 //   dL/dW' = m^T Abar (deterministic split-K)  -> adjoint of the rows of B
 //   the circuit's adjoint on the D basis rows (one CTA per row, checkpointed
 //   at the layer boundaries like K2) -> the gate-space sums -> dL/dqparams.
-// Float32 only (the GEMM is 3xTF32); chosen for 5 <= n <= 7, where the dense
-// map costs at most 2 D / (n L) times the gate-by-gate flops.
+// Float32 only (the GEMM is 3xTF32); chosen for 5 <= n <= 8: the folded map costs
+// 8 D^2 FLOP per point against ~5 n L D for the gate sweep, but at tensor-core rate
+// (n = 8: 1.4-7.5x faster than the layer kernels, profiles/r02).
 #include <cstdlib>
 #include <mutex>
 
@@ -33,8 +34,8 @@ namespace qpinn {
 
 namespace {
 
-constexpr int kTrThreads = 64;  // circuit kernels: one thread per amplitude pair (D <= 128)
-constexpr int kTrMaxN = 7;      // transfer-matrix path: n <= 7
+constexpr int kTrThreads = 64;  // circuit kernels: amplitude pairs strided over 64 threads
+constexpr int kTrMaxN = 8;      // transfer-matrix path: n <= 8
 
 // u1 matrices [n_u1][4] and phase diagonals [n_phase][D] (as gb_tables, pqc_global.cu)
 __global__ void tr_tables(PlanDev p, const float* __restrict__ qp, cplx<float>* __restrict__ U,
@@ -72,7 +73,7 @@ __device__ __forceinline__ void pair_index(int k, int pos, int& i0, int& i1) {
 __global__ void __launch_bounds__(kTrThreads) tr_circuit_fwd(
     int n, int L, int ent, const cplx<float>* __restrict__ U, const cplx<float>* __restrict__ ph,
     const uint16_t* __restrict__ perm, cplx<float>* __restrict__ B, cplx<float>* __restrict__ CK) {
-  __shared__ cplx<float> s[2][128];
+  __shared__ cplx<float> s[2][1 << kTrMaxN];
   const int D = 1 << n, j = blockIdx.x, t = threadIdx.x;
   int cur = 0;
   for (int b = t; b < D; b += kTrThreads) s[0][b] = {b == j ? 1.f : 0.f, 0.f};
@@ -124,7 +125,7 @@ __global__ void __launch_bounds__(kTrThreads) tr_circuit_bwd(
     const uint16_t* __restrict__ iperm, const cplx<float>* __restrict__ Abar,
     const cplx<float>* __restrict__ CK, double* __restrict__ part_u1,
     double* __restrict__ part_ph) {
-  __shared__ cplx<float> s[2][128];
+  __shared__ cplx<float> s[2][1 << kTrMaxN];
   __shared__ double red[2 * 8 * kTrMaxN];
   const int D = 1 << n, j = blockIdx.x, t = threadIdx.x, n_u1 = n * L;
   int cur = 0;
@@ -358,7 +359,7 @@ __device__ __forceinline__ void for_points(int64_t R, F&& body) {
 #define QPINN_TR_EMB_MINB 4
 #endif
 template <int NQ>
-__global__ void __launch_bounds__(256, QPINN_TR_EMB_MINB) tr_embed(int scale, int64_t R, const float* __restrict__ act,
+__global__ void __launch_bounds__(256, NQ >= 8 ? 2 : QPINN_TR_EMB_MINB) tr_embed(int scale, int64_t R, const float* __restrict__ act,
                                                 const float* __restrict__ tan,
                                                 float* __restrict__ Phi,
                                                 unsigned long long* __restrict__ maxabs) {
@@ -501,7 +502,7 @@ __device__ __forceinline__ float flip_get(const float (&v)[J], int j, int q) {
 #define QPINN_TR_EG_MINB 4  // 64 registers, no spills: 58 vs 63 us at 3 (real-arithmetic version)
 #endif
 template <int NQ>
-__global__ void __launch_bounds__(256, QPINN_TR_EG_MINB) tr_embed_grad(int scale, int64_t R,
+__global__ void __launch_bounds__(256, NQ >= 8 ? 2 : QPINN_TR_EG_MINB) tr_embed_grad(int scale, int64_t R,
                                                      const float* __restrict__ act,
                                                      const float* __restrict__ tan,
                                                      const float* __restrict__ gPhi,
@@ -876,7 +877,7 @@ int bwd_n(const qpinn_circuit* c, const KArgs<float>* a, unsigned char* ws, cons
 }  // namespace
 
 bool transfer_supported(const qpinn_circuit* c, int dtype) {
-  return c && dtype == QPINN_F32 && c->n >= 5 && c->n <= 7 && layer_entangler(c) >= 0;
+  return c && dtype == QPINN_F32 && c->n >= 5 && c->n <= kTrMaxN && layer_entangler(c) >= 0;
 }
 
 size_t transfer_state_bytes(const qpinn_circuit* c, int64_t R) {
@@ -895,7 +896,8 @@ int transfer_forward(const qpinn_circuit* c, const KArgs<float>* a, unsigned cha
     case 5: return fwd_n<5>(c, a, ws, t);
     case 6: return fwd_n<6>(c, a, ws, t);
     case 7: return fwd_n<7>(c, a, ws, t);
-    default: return fail(QPINN_ERR_CAPACITY, "transfer PQC covers 5 <= n <= 7");
+    case 8: return fwd_n<8>(c, a, ws, t);
+    default: return fail(QPINN_ERR_CAPACITY, "transfer PQC covers 5 <= n <= 8");
   }
 }
 
@@ -907,7 +909,8 @@ int transfer_backward(const qpinn_circuit* c, const KArgs<float>* a, unsigned ch
     case 5: return bwd_n<5>(c, a, ws, t);
     case 6: return bwd_n<6>(c, a, ws, t);
     case 7: return bwd_n<7>(c, a, ws, t);
-    default: return fail(QPINN_ERR_CAPACITY, "transfer PQC covers 5 <= n <= 7");
+    case 8: return bwd_n<8>(c, a, ws, t);
+    default: return fail(QPINN_ERR_CAPACITY, "transfer PQC covers 5 <= n <= 8");
   }
 }
 

@@ -6,7 +6,7 @@ diagonal, no_entanglement), acos scaling.
 Inputs: a ~ U(-0.9, 0.9) [R,n], tangents ~ N(0,1) [3,R,n], qparams ~ U(0, 2pi),
 seed 0.  R*2^n is capped (the statevector work per point grows as 2^n); the
 metric is points/s and algorithmic TFLOP/s (roofline.pqc_flops).
-Usage: python scripts/sweep_pqc.py [--quick]   -> one JSON line per cell
+Usage: python scripts/sweep_pqc.py [--quick] [--n=..] [--variant=..]   -> one JSON line per cell
 """
 import json
 import os
@@ -44,9 +44,12 @@ def main():
     quick = "--quick" in sys.argv
     rng = np.random.default_rng(0)
     ns = range(4, 17)
+    variant = None
     for arg in sys.argv[1:]:
         if arg.startswith("--n="):  # e.g. --n=15,16
             ns = [int(v) for v in arg[4:].split(",")]
+        if arg.startswith("--variant="):  # auto | transfer | layer | generic
+            variant = arg.split("=", 1)[1]
     Ls = (1, 4) if quick else (1, 4, 8)
     kinds = ("strongly", "cross_mesh", "no_entanglement")
     for n in ns:
@@ -61,6 +64,8 @@ def main():
                 if n <= 8:
                     R = min(R, (4 << 30) // (L * 4 * (1 << n) * 8))
                 c = build_circuit(kind, n, L)
+                if variant:
+                    c.set_kernel_variant(variant)
                 a = torch.as_tensor(rng.uniform(-0.9, 0.9, (R, n)), dtype=torch.float32, device="cuda")
                 da = torch.as_tensor(rng.normal(size=(3, R, n)), dtype=torch.float32, device="cuda")
                 qp = torch.as_tensor(rng.uniform(0, 2 * np.pi, c.param_count), dtype=torch.float32,
