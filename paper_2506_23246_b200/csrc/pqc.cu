@@ -671,8 +671,8 @@ static size_t small_ws_bytes(const qpinn_circuit* c) {
 // n = 5 0.32 vs 0.37-0.39; profiles/r01/transfer_vs_layer_folded.txt; n = 8 at
 // 2^17 points: 3.7 vs 13.2 ms, profiles/r02/config5_n8_transfer_vs_layer.txt)
 static bool use_transfer(const qpinn_circuit* c, int dtype) {
-  if (!transfer_supported(c, dtype)) return false;
-  return c->variant == 2 || c->variant == 0;
+  if (c->variant == 2) return transfer_supported(c, dtype);
+  return c->variant == 0 && transfer_default(c, dtype);
 }
 
 int qpinn_pqc_uses_transfer(const qpinn_circuit* c, int dtype) {
@@ -681,12 +681,15 @@ int qpinn_pqc_uses_transfer(const qpinn_circuit* c, int dtype) {
 
 size_t qpinn_pqc_workspace_bytes(const qpinn_circuit* c, int dtype, int64_t rows) {
   if (!c) return 0;
-  if (c->n > qpinn_pqc_max_qubits(dtype))
-    return align_up(big_workspace_bytes(c, dtype), 256) +
-           global_adjoint_workspace_bytes(c, dtype, rows);
-  size_t b = small_ws_bytes(c);
-  if (transfer_supported(c, dtype)) b += transfer_workspace_bytes(c, rows);
-  return b;
+  size_t t = 0;  // the transfer-matrix kernels (any variant may be selected later)
+  if (transfer_supported(c, dtype)) t = small_ws_bytes(c) + transfer_workspace_bytes(c, rows);
+  if (c->n > qpinn_pqc_max_qubits(dtype)) {
+    const size_t b = align_up(big_workspace_bytes(c, dtype), 256) +
+                     global_adjoint_workspace_bytes(c, dtype, rows);
+    return b > t ? b : t;
+  }
+  const size_t b = small_ws_bytes(c);
+  return b > t ? b : t;
 }
 
 size_t qpinn_pqc_state_bytes(const qpinn_circuit* c, int dtype, int64_t rows) {
@@ -726,7 +729,7 @@ int qpinn_pqc_forward(const qpinn_circuit* cc, int dtype, int scale, int64_t row
   if (rc) return rc;
   cudaStream_t st = (cudaStream_t)stream;
   auto* maxabs = (unsigned long long*)workspace;  // running max, reset by domain_check
-  if (n > qpinn_pqc_max_qubits(dtype)) {  // cluster kernels (pqc_big.cu)
+  if (n > qpinn_pqc_max_qubits(dtype) && !use_transfer(c, dtype)) {  // cluster kernels (pqc_big.cu)
     if (rows == 0) return QPINN_OK;
     double* partial;
     double* tot;
@@ -818,7 +821,7 @@ int qpinn_pqc_backward(const qpinn_circuit* cc, int dtype, int scale, int64_t ro
   rc = ensure_device_plan(c);
   if (rc) return rc;
   cudaStream_t st = (cudaStream_t)stream;
-  if (n > qpinn_pqc_max_qubits(dtype)) {  // cluster kernels (pqc_big.cu), forward replayed
+  if (n > qpinn_pqc_max_qubits(dtype) && !use_transfer(c, dtype)) {  // cluster kernels, forward replayed
     if (rows == 0) {
       QPINN_CUDA_CHECK(cudaMemsetAsync(g_qparams, 0,
                                        (dtype == QPINN_F64 ? 8 : 4) * (size_t)c->n_params, st));

@@ -74,6 +74,7 @@ int hbm_backward(const qpinn_circuit* c, const KArgs<float>* a, unsigned char* w
 size_t hbm_bwd_workspace_bytes(const qpinn_circuit* c, int64_t rows = -1);
 // transfer-matrix K1 / K2 on the tensor cores (pqc_transfer.cu)
 bool transfer_supported(const qpinn_circuit* c, int dtype);
+bool transfer_default(const qpinn_circuit* c, int dtype);
 size_t transfer_workspace_bytes(const qpinn_circuit* c, int64_t R);
 size_t transfer_state_bytes(const qpinn_circuit* c, int64_t R);
 int transfer_forward(const qpinn_circuit* c, const KArgs<float>* a, unsigned char* ws, size_t bytes);

@@ -35,7 +35,7 @@ namespace qpinn {
 namespace {
 
 constexpr int kTrThreads = 64;  // circuit kernels: amplitude pairs strided over 64 threads
-constexpr int kTrMaxN = 8;      // transfer-matrix path: n <= 8
+constexpr int kTrMaxN = 9;      // transfer-matrix path: n <= 9
 
 // u1 matrices [n_u1][4] and phase diagonals [n_phase][D] (as gb_tables, pqc_global.cu)
 __global__ void tr_tables(PlanDev p, const float* __restrict__ qp, cplx<float>* __restrict__ U,
@@ -168,13 +168,13 @@ __global__ void __launch_bounds__(kTrThreads) tr_circuit_bwd(
       }
     }
     block_sum<8 * kTrMaxN>(m, red);
-    if (t < 8 * n) {
-      // m is uniform after the sum: pick entry t without dynamic register indexing
+    for (int t2 = t; t2 < 8 * n; t2 += kTrThreads) {
+      // m is uniform after the sum: pick entry t2 without dynamic register indexing
       double v = 0.0;
 #pragma unroll
       for (int e = 0; e < 8 * kTrMaxN; ++e)
-        if (e == t) v = m[e];
-      part_u1[((size_t)j * n_u1 + l * n) * 8 + t] = v;
+        if (e == t2) v = m[e];
+      part_u1[((size_t)j * n_u1 + l * n) * 8 + t2] = v;
     }
     for (int q = 0; q < n; ++q) {
       const cplx<float>* u = U + 4 * (l * n + q);
@@ -333,7 +333,37 @@ __device__ __forceinline__ void embed_amp(const PointAngles<NQ>& pa, int b, bool
 }
 
 // lane l ends with the warp total of value index l (recursive halving, 31 shuffles)
-__device__ __forceinline__ void reduce_scatter32(float (&v)[32]) {
+__device__ __forceinline__ void reduce_scatter32(float* v);
+
+// NV <= 64 per-lane values -> warp totals: value e on lane e % 32 of half e / 32
+// (h[0] = values 0..31, h[1] = 32..63); total of value e for any lane via warp_value
+template <int NV>
+struct Scatter {
+  static constexpr int H = NV <= 32 ? 1 : 2;
+  float h[H];
+};
+template <int NV>
+__device__ __forceinline__ Scatter<NV> reduce_scatter(float* v) {
+  Scatter<NV> r;
+  reduce_scatter32(v);
+  r.h[0] = v[0];
+  if constexpr (NV > 32) {
+    reduce_scatter32(v + 32);
+    r.h[1] = v[32];
+  }
+  return r;
+}
+template <int NV>
+__device__ __forceinline__ float warp_value(const Scatter<NV>& r, int e) {
+  const float a = __shfl_sync(0xffffffffu, r.h[0], e & 31);
+  if constexpr (NV > 32) {
+    const float b = __shfl_sync(0xffffffffu, r.h[1], e & 31);
+    return e >= 32 ? b : a;
+  }
+  return a;
+}
+
+__device__ __forceinline__ void reduce_scatter32(float* v) {
   const int lane = threadIdx.x & 31;
 #pragma unroll
   for (int m = 16; m >= 1; m >>= 1) {
@@ -359,7 +389,7 @@ __device__ __forceinline__ void for_points(int64_t R, F&& body) {
 #define QPINN_TR_EMB_MINB 4
 #endif
 template <int NQ>
-__global__ void __launch_bounds__(256, NQ >= 8 ? 2 : QPINN_TR_EMB_MINB) tr_embed(int scale, int64_t R, const float* __restrict__ act,
+__global__ void __launch_bounds__(256, NQ >= 9 ? 1 : NQ >= 8 ? 2 : QPINN_TR_EMB_MINB) tr_embed(int scale, int64_t R, const float* __restrict__ act,
                                                 const float* __restrict__ tan,
                                                 float* __restrict__ Phi,
                                                 unsigned long long* __restrict__ maxabs) {
@@ -402,9 +432,10 @@ __global__ void __launch_bounds__(256, QPINN_TR_RD_MINB) tr_readout(int64_t R, i
   const int lane = threadIdx.x & 31;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   for (int64_t p = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; p < R; p += nw) {
-    float acc[32];
+    constexpr int NV = 4 * NQ, NA = NV <= 32 ? 32 : 64;
+    float acc[NA];
 #pragma unroll
-    for (int e = 0; e < 32; ++e) acc[e] = 0.f;
+    for (int e = 0; e < NA; ++e) acc[e] = 0.f;
 #pragma unroll
     for (int b = lane; b < D; b += 32) {
       const float pr = Psi[p * D2 + b], pi = Psi[p * D2 + D + b];
@@ -426,10 +457,14 @@ __global__ void __launch_bounds__(256, QPINN_TR_RD_MINB) tr_readout(int64_t R, i
         for (int k = 0; k < 4; ++k) acc[k * NQ + q] += neg ? -v[k] : v[k];
       }
     }
-    reduce_scatter32(acc);
-    const int k = lane / NQ, q = lane % NQ;
-    if (k == 0) z[p * NQ + q] = acc[0];
-    else if (k < ns) dz[((int64_t)(k - 1) * R + p) * NQ + q] = acc[0];
+    const Scatter<NV> sc = reduce_scatter<NV>(acc);
+#pragma unroll
+    for (int hh = 0; hh < Scatter<NV>::H; ++hh) {
+      const int e = lane + 32 * hh, k = e / NQ, q = e % NQ;
+      if (e >= NV) continue;
+      if (k == 0) z[p * NQ + q] = sc.h[hh];
+      else if (k < ns) dz[((int64_t)(k - 1) * R + p) * NQ + q] = sc.h[hh];
+    }
   }
 }
 
@@ -502,7 +537,7 @@ __device__ __forceinline__ float flip_get(const float (&v)[J], int j, int q) {
 #define QPINN_TR_EG_MINB 4  // 64 registers, no spills: 58 vs 63 us at 3 (real-arithmetic version)
 #endif
 template <int NQ>
-__global__ void __launch_bounds__(256, NQ >= 8 ? 2 : QPINN_TR_EG_MINB) tr_embed_grad(int scale, int64_t R,
+__global__ void __launch_bounds__(256, NQ >= 9 ? 1 : NQ >= 8 ? 2 : QPINN_TR_EG_MINB) tr_embed_grad(int scale, int64_t R,
                                                      const float* __restrict__ act,
                                                      const float* __restrict__ tan,
                                                      const float* __restrict__ gPhi,
@@ -551,9 +586,10 @@ __global__ void __launch_bounds__(256, NQ >= 8 ? 2 : QPINN_TR_EG_MINB) tr_embed_
           et[j] += ((lane + 32 * j) >> (NQ - 1 - q)) & 1 ? -f : f;
         }
       }
-      float acc[32];
+      constexpr int NV = 4 * NQ, NA = NV <= 32 ? 32 : 64;
+      float acc[NA];
 #pragma unroll
-      for (int e = 0; e < 32; ++e) acc[e] = 0.f;
+      for (int e = 0; e < NA; ++e) acc[e] = 0.f;
 #pragma unroll
       for (int q = 0; q < NQ; ++q) {
 #pragma unroll
@@ -565,15 +601,16 @@ __global__ void __launch_bounds__(256, NQ >= 8 ? 2 : QPINN_TR_EG_MINB) tr_embed_
           for (int k = 0; k < 3; ++k) acc[NQ + k * NQ + q] = fmaf(g[k + 1][j], y, acc[NQ + k * NQ + q]);
         }
       }
-      reduce_scatter32(acc);
-      // lane l holds value l: g_th[q] on lanes 0..NQ-1, g_dth[k][q] on NQ + k NQ + q
+      // value v on lane v % 32 of half v / 32: g_th[q] = value q, g_dth[k][q] = NQ + k NQ + q
+      const Scatter<NV> sc = reduce_scatter<NV>(acc);
       const int q = lane < NQ ? lane : 0;
       float gd[3];
 #pragma unroll
-      for (int k = 0; k < 3; ++k) gd[k] = 0.5f * __shfl_sync(0xffffffffu, acc[0], NQ + k * NQ + q);
+      for (int k = 0; k < 3; ++k) gd[k] = 0.5f * warp_value<NV>(sc, NQ + k * NQ + q);
+      const float gth = warp_value<NV>(sc, q);
       if (lane < NQ) {
         const float* a = pang + q * kAng;
-        float ga = acc[0] * a[2];
+        float ga = gth * a[2];
 #pragma unroll
         for (int k = 0; k < 3; ++k) {
           ga += gd[k] * a[6 + k];
@@ -880,6 +917,14 @@ bool transfer_supported(const qpinn_circuit* c, int dtype) {
   return c && dtype == QPINN_F32 && c->n >= 5 && c->n <= kTrMaxN && layer_entangler(c) >= 0;
 }
 
+// the default (variant 0) path: the transfer map up to n = 8, and at n = 9 from L = 4
+// (its cost does not grow with L: K1 1.9 ms, K2 6.6-6.9 ms at 2^16 points against the
+// CTA kernels' 2.3-2.7 / 11.5-13.1 ms at L = 4 and 4.0-4.8 / 19.6-23.1 ms at L = 8;
+// at L = 1 the CTA kernels win, 1.0 / 5.5-6.0 ms; profiles/r02/config5_n9_transfer_vs_cta.txt)
+bool transfer_default(const qpinn_circuit* c, int dtype) {
+  return transfer_supported(c, dtype) && (c->n <= 8 || c->L >= 4);
+}
+
 size_t transfer_state_bytes(const qpinn_circuit* c, int64_t R) {
   return R <= 0 ? 0 : tr_handoff(c, R).total;
 }
@@ -897,7 +942,8 @@ int transfer_forward(const qpinn_circuit* c, const KArgs<float>* a, unsigned cha
     case 6: return fwd_n<6>(c, a, ws, t);
     case 7: return fwd_n<7>(c, a, ws, t);
     case 8: return fwd_n<8>(c, a, ws, t);
-    default: return fail(QPINN_ERR_CAPACITY, "transfer PQC covers 5 <= n <= 8");
+    case 9: return fwd_n<9>(c, a, ws, t);
+    default: return fail(QPINN_ERR_CAPACITY, "transfer PQC covers 5 <= n <= 9");
   }
 }
 
@@ -910,7 +956,8 @@ int transfer_backward(const qpinn_circuit* c, const KArgs<float>* a, unsigned ch
     case 6: return bwd_n<6>(c, a, ws, t);
     case 7: return bwd_n<7>(c, a, ws, t);
     case 8: return bwd_n<8>(c, a, ws, t);
-    default: return fail(QPINN_ERR_CAPACITY, "transfer PQC covers 5 <= n <= 8");
+    case 9: return bwd_n<9>(c, a, ws, t);
+    default: return fail(QPINN_ERR_CAPACITY, "transfer PQC covers 5 <= n <= 9");
   }
 }
 

@@ -299,7 +299,7 @@ def test_global_memory_forward_vs_oracle(n, L, kind, dtype):
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("R", [1000, 1, 65])
-@pytest.mark.parametrize("n", [5, 6, 7, 8])
+@pytest.mark.parametrize("n", [5, 6, 7, 8, 9])
 @pytest.mark.parametrize("kind", O.KINDS)
 def test_transfer_matrix_kernels_vs_oracle(kind, n, R):
     """Transfer-matrix K1/K2 (variant "transfer": the circuit as one [2D, 2D]
