@@ -20,9 +20,10 @@
 //   dL/dW' = m^T Abar (deterministic split-K)  -> adjoint of the rows of B
 //   the circuit's adjoint on the D basis rows (one CTA per row, checkpointed
 //   at the layer boundaries like K2) -> the gate-space sums -> dL/dqparams.
-// Float32 only (the GEMM is 3xTF32); chosen for 5 <= n <= 8: the folded map costs
-// 8 D^2 FLOP per point against ~5 n L D for the gate sweep, but at tensor-core rate
-// (n = 8: 1.4-7.5x faster than the layer kernels, profiles/r02).
+// Float32 only (the GEMM is 3xTF32); chosen for 5 <= n <= 8 and n = 9 at L >= 4: the
+// folded map costs 8 D^2 FLOP per point against ~5 n L D for the gate sweep, but at
+// tensor-core rate (n = 8: 1.4-7.5x faster than the layer kernels; n = 9, L >= 4:
+// 1.2-3.3x faster than the CTA kernels; profiles/r02).
 #include <cstdlib>
 #include <mutex>
 
