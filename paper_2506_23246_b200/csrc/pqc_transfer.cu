@@ -71,10 +71,11 @@ __device__ __forceinline__ void pair_index(int k, int pos, int& i0, int& i1) {
 }
 
 // B[j] = circuit(e_j); CK[l][j] = the state after layer l's single-qubit gates
+template <int NQ>  // the circuit's qubit count: shared-memory rows of 2^NQ amplitudes
 __global__ void __launch_bounds__(kTrThreads) tr_circuit_fwd(
     int n, int L, int ent, const cplx<float>* __restrict__ U, const cplx<float>* __restrict__ ph,
     const uint16_t* __restrict__ perm, cplx<float>* __restrict__ B, cplx<float>* __restrict__ CK) {
-  __shared__ cplx<float> s[2][1 << kTrMaxN];
+  __shared__ cplx<float> s[2][1 << NQ];
   const int D = 1 << n, j = blockIdx.x, t = threadIdx.x;
   int cur = 0;
   for (int b = t; b < D; b += kTrThreads) s[0][b] = {b == j ? 1.f : 0.f, 0.f};
@@ -121,13 +122,14 @@ __device__ __forceinline__ void block_sum(double (&v)[NV], double* red /* [2][NV
 // post-gate outer product M'_ab = sum conj(abar_a) x_b (gates of one layer
 // commute, so each is the layer's last), per phase layer Im(conj(abar) x');
 // per-row partials, reduced over rows in fixed order by tr_reduce
+template <int NQ>  // the circuit's qubit count (register sums: 8 per qubit)
 __global__ void __launch_bounds__(kTrThreads) tr_circuit_bwd(
     int n, int L, int ent, const cplx<float>* __restrict__ U, const cplx<float>* __restrict__ ph,
     const uint16_t* __restrict__ iperm, const cplx<float>* __restrict__ Abar,
     const cplx<float>* __restrict__ CK, double* __restrict__ part_u1,
     double* __restrict__ part_ph) {
-  __shared__ cplx<float> s[2][1 << kTrMaxN];
-  __shared__ double red[2 * 8 * kTrMaxN];
+  __shared__ cplx<float> s[2][1 << NQ];
+  __shared__ double red[2 * 8 * NQ];
   const int D = 1 << n, j = blockIdx.x, t = threadIdx.x, n_u1 = n * L;
   int cur = 0;
   for (int b = t; b < D; b += kTrThreads) s[0][b] = Abar[(size_t)j * D + b];
@@ -148,11 +150,11 @@ __global__ void __launch_bounds__(kTrThreads) tr_circuit_bwd(
     }
     // all of the layer's outer products from the same (adjoint, checkpoint) pair,
     // then one block reduction for the layer (8 n sums)
-    double m[8 * kTrMaxN];
+    double m[8 * NQ];
 #pragma unroll
-    for (int e = 0; e < 8 * kTrMaxN; ++e) m[e] = 0.0;
+    for (int e = 0; e < 8 * NQ; ++e) m[e] = 0.0;
 #pragma unroll
-    for (int q = 0; q < kTrMaxN; ++q) {
+    for (int q = 0; q < NQ; ++q) {
       if (q < n) {
         for (int k = t; k < D / 2; k += kTrThreads) {
           int i0, i1;
@@ -168,12 +170,12 @@ __global__ void __launch_bounds__(kTrThreads) tr_circuit_bwd(
         }
       }
     }
-    block_sum<8 * kTrMaxN>(m, red);
+    block_sum<8 * NQ>(m, red);
     for (int t2 = t; t2 < 8 * n; t2 += kTrThreads) {
       // m is uniform after the sum: pick entry t2 without dynamic register indexing
       double v = 0.0;
 #pragma unroll
-      for (int e = 0; e < 8 * kTrMaxN; ++e)
+      for (int e = 0; e < 8 * NQ; ++e)
         if (e == t2) v = m[e];
       part_u1[((size_t)j * n_u1 + l * n) * 8 + t2] = v;
     }
@@ -710,7 +712,16 @@ int build_transfer(const qpinn_circuit* c, const float* qp, const TrCircuit& tc_
   const int n = c->n, D = 1 << n;
   const int ent = layer_entangler(c);
   tr_tables<<<32, 256, 0, st>>>(p, qp, tc_.U, tc_.ph);
-  tr_circuit_fwd<<<D, kTrThreads, 0, st>>>(n, c->L, ent, tc_.U, tc_.ph, p.perm, B, tc_.CK);
+  switch (n) {  // rows of 2^n amplitudes in shared memory
+#define QPINN_TR_CF(NN)                                                                  \
+  case NN:                                                                               \
+    tr_circuit_fwd<NN><<<D, kTrThreads, 0, st>>>(n, c->L, ent, tc_.U, tc_.ph, p.perm, B, \
+                                                 tc_.CK);                                \
+    break;
+    QPINN_TR_CF(5) QPINN_TR_CF(6) QPINN_TR_CF(7) QPINN_TR_CF(8) QPINN_TR_CF(9)
+#undef QPINN_TR_CF
+    default: return fail(QPINN_ERR_CAPACITY, "transfer PQC covers 5 <= n <= 9");
+  }
   tr_wmat<<<(2 * D * D + 255) / 256, 256, 0, st>>>(n, B, tc_.W, tc_.Wt);
   QPINN_CUDA_CHECK(cudaGetLastError());
   return QPINN_OK;
@@ -866,7 +877,7 @@ int bwd_n(const qpinn_circuit* c, const KArgs<float>* a, unsigned char* ws, cons
     auto* pu = (double*)(ws + t.pu);
     auto* pp = (double*)(ws + t.pp);
     auto* acc = (double*)(ws + t.acc);
-    tr_circuit_bwd<<<D, kTrThreads, 0, s2>>>(NQ, L, ent, cc.U, cc.ph, p.iperm, Ab, cc.CK, pu, pp);
+    tr_circuit_bwd<NQ><<<D, kTrThreads, 0, s2>>>(NQ, L, ent, cc.U, cc.ph, p.iperm, Ab, cc.CK, pu, pp);
     const int n_ph = D * c->n_phase, n_acc = 8 * n_u1 + n_ph;
     tr_reduce<<<(n_acc + 7) / 8, 256, 0, s2>>>(D, n_u1, n_ph, pu, pp, acc);
     QPINN_CUDA_CHECK(cudaGetLastError());
