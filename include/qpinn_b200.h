@@ -79,10 +79,10 @@ size_t qpinn_circuit_dump(const qpinn_circuit* c, char* buf, size_t len);
  * "phases <c:t:slot ...>". */
 size_t qpinn_circuit_plan_dump(const qpinn_circuit* c, char* buf, size_t len);
 /* Kernel choice for this circuit: 0 (default) uses the transfer-matrix K1/K2
- * for float32 n = 5..8 (and n = 9 from L = 4) and the layer-loop K1/K2 (wires unrolled at compile
+ * for float32 n = 5..8 (and n = 9, 10 from L = 4) and the layer-loop K1/K2 (wires unrolled at compile
  * time) otherwise, when the fused plan has the uniform layer shape every
  * build_circuit ansatz has; 1 forces the generic runtime-plan kernels; 2
- * forces the transfer-matrix kernels (float32, 5 <= n <= 9: the circuit as
+ * forces the transfer-matrix kernels (float32, 5 <= n <= 10: the circuit as
  * one [2^(n+1), 2^(n+1)] real map applied on the tensor cores, the
  * reference's via="matrix" formulation, ansatz.py:300-338); 3 forces the
  * layer-loop kernels wherever the plan allows them.  Set it before

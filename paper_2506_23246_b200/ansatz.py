@@ -177,9 +177,9 @@ class CircuitSpec:
         return bool(N.lib().qpinn_pqc_uses_transfer(self._h, N.dtype_code(dtype)))
 
     def set_kernel_variant(self, variant: str) -> None:
-        """"auto" (transfer-matrix kernels for float32 n = 5..8, and n = 9 from
+        """"auto" (transfer-matrix kernels for float32 n = 5..8, and n = 9, 10 from
         L = 4, else the layer-loop / CTA kernels), "generic", "transfer" (float32,
-        5 <= n <= 9: the transfer-matrix map on the tensor cores) or "layer"
+        5 <= n <= 10: the transfer-matrix map on the tensor cores) or "layer"
         (the layer-loop kernels wherever they apply)."""
         code = {"auto": 0, "generic": 1, "transfer": 2, "layer": 3}[variant]
         N.check(N.lib().qpinn_circuit_set_kernel_variant(self._h, code), "set_kernel_variant")

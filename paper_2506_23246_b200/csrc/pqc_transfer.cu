@@ -20,10 +20,10 @@
 //   dL/dW' = m^T Abar (deterministic split-K)  -> adjoint of the rows of B
 //   the circuit's adjoint on the D basis rows (one CTA per row, checkpointed
 //   at the layer boundaries like K2) -> the gate-space sums -> dL/dqparams.
-// Float32 only (the GEMM is 3xTF32); chosen for 5 <= n <= 8 and n = 9 at L >= 4: the
-// folded map costs 8 D^2 FLOP per point against ~5 n L D for the gate sweep, but at
-// tensor-core rate (n = 8: 1.4-7.5x faster than the layer kernels; n = 9, L >= 4:
-// 1.2-3.3x faster than the CTA kernels; profiles/r02).
+// Float32 only (the GEMM is 3xTF32); chosen for 5 <= n <= 8 and n = 9, 10 at L >= 4:
+// the folded map costs 8 D^2 FLOP per point against ~5 n L D for the gate sweep, but at
+// tensor-core rate (n = 8: 1.4-7.5x faster than the layer kernels; n = 9, 10 at
+// L >= 4: 1.2-3.3x faster than the CTA kernels for K1 + K2; profiles/r02).
 #include <cstdlib>
 #include <mutex>
 
@@ -36,7 +36,7 @@ namespace qpinn {
 namespace {
 
 constexpr int kTrThreads = 64;  // circuit kernels: amplitude pairs strided over 64 threads
-constexpr int kTrMaxN = 9;      // transfer-matrix path: n <= 9
+constexpr int kTrMaxN = 10;     // transfer-matrix path: n <= 10
 
 // u1 matrices [n_u1][4] and phase diagonals [n_phase][D] (as gb_tables, pqc_global.cu)
 __global__ void tr_tables(PlanDev p, const float* __restrict__ qp, cplx<float>* __restrict__ U,
@@ -407,7 +407,7 @@ __global__ void __launch_bounds__(256, NQ >= 9 ? 1 : NQ >= 8 ? 2 : QPINN_TR_EMB_
       const int64_t p = p0 + pl;
       PointAngles<NQ> pa;
       read_angles<NQ>(ang + pl * NQ * kAng, pa);
-#pragma unroll
+#pragma unroll(NQ >= 10 ? 4 : D / 32)
       for (int b = lane; b < D; b += 32) {
         float m0, mk[3];
         embed_amp<NQ>(pa, b, tan != nullptr, m0, mk);
@@ -566,6 +566,64 @@ __global__ void __launch_bounds__(256, NQ >= 9 ? 1 : NQ >= 8 ? 2 : QPINN_TR_EG_M
       //   nu_q(b)  = sum_k dth_kq g_k(b)                      (g_k = dL/dm of tangent row k)
       //   eta(b)   = g_0(b) / 2 - 1/4 sum_q sigma_q(b) nu_q(b ^ q)
       //   g_th[q]  = sum_b sigma_q(b) eta(b) m(b ^ q),  g_dth[k][q] = 1/2 sum_b sigma_q(b) g_k(b) m(b ^ q)
+      constexpr int NV = 4 * NQ, NA = NV <= 32 ? 32 : 64;
+      float acc[NA];
+#pragma unroll
+      for (int e = 0; e < NA; ++e) acc[e] = 0.f;
+      if constexpr (J >= 32) {
+        // 32 amplitudes per lane: only the adjoint rows one at a time stay in registers
+        // (flips are linear, so nu's flip is the sum of the rows' flips; the rows are
+        // re-read from L1/L2 for the outer products)
+        const float* grow = gPhi + p * D + lane;
+        const int64_t rs = R * D;
+        float m[J], et[J];
+#pragma unroll
+        for (int j = 0; j < J; ++j) {
+          float mk[3];
+          embed_amp<NQ>(pa, lane + 32 * j, false, m[j], mk);
+          et[j] = 0.5f * grow[32 * j];
+        }
+        for (int k = 0; k < 3; ++k) {
+          float gk[J];
+#pragma unroll
+          for (int j = 0; j < J; ++j) gk[j] = grow[(k + 1) * rs + 32 * j];
+#pragma unroll
+          for (int q = 0; q < NQ; ++q) {
+            const float dq = 0.25f * pang[q * kAng + 3 + k];  // pa.d[k][q] (k not unrolled)
+#pragma unroll
+            for (int j = 0; j < J; ++j) {
+              const float f = dq * flip_get<NQ, J>(gk, j, q);
+              et[j] += ((lane + 32 * j) >> (NQ - 1 - q)) & 1 ? -f : f;
+            }
+          }
+        }
+#pragma unroll
+        for (int q = 0; q < NQ; ++q)
+#pragma unroll
+          for (int j = 0; j < J; ++j) {
+            const float mf = flip_get<NQ, J>(m, j, q);
+            const float y = ((lane + 32 * j) >> (NQ - 1 - q)) & 1 ? mf : -mf;
+            acc[q] = fmaf(et[j], y, acc[q]);
+          }
+        for (int k = 0; k < 3; ++k) {
+          float gk[J];
+#pragma unroll
+          for (int j = 0; j < J; ++j) gk[j] = grow[(k + 1) * rs + 32 * j];
+#pragma unroll
+          for (int q = 0; q < NQ; ++q) {
+            float a = 0.f;
+#pragma unroll
+            for (int j = 0; j < J; ++j) {
+              const float mf = flip_get<NQ, J>(m, j, q);
+              a = fmaf(gk[j], ((lane + 32 * j) >> (NQ - 1 - q)) & 1 ? mf : -mf, a);
+            }
+            // acc index NQ + k NQ + q with k a loop variable: select without local memory
+#pragma unroll
+            for (int kk = 0; kk < 3; ++kk)
+              if (kk == k) acc[NQ + kk * NQ + q] += a;
+          }
+        }
+      } else {
       float m[J], et[J], g[4][J];
 #pragma unroll
       for (int r = 0; r < 4; ++r)  // all the point's loads in flight before any use
@@ -589,10 +647,6 @@ __global__ void __launch_bounds__(256, NQ >= 9 ? 1 : NQ >= 8 ? 2 : QPINN_TR_EG_M
           et[j] += ((lane + 32 * j) >> (NQ - 1 - q)) & 1 ? -f : f;
         }
       }
-      constexpr int NV = 4 * NQ, NA = NV <= 32 ? 32 : 64;
-      float acc[NA];
-#pragma unroll
-      for (int e = 0; e < NA; ++e) acc[e] = 0.f;
 #pragma unroll
       for (int q = 0; q < NQ; ++q) {
 #pragma unroll
@@ -603,6 +657,7 @@ __global__ void __launch_bounds__(256, NQ >= 9 ? 1 : NQ >= 8 ? 2 : QPINN_TR_EG_M
 #pragma unroll
           for (int k = 0; k < 3; ++k) acc[NQ + k * NQ + q] = fmaf(g[k + 1][j], y, acc[NQ + k * NQ + q]);
         }
+      }
       }
       // value v on lane v % 32 of half v / 32: g_th[q] = value q, g_dth[k][q] = NQ + k NQ + q
       const Scatter<NV> sc = reduce_scatter<NV>(acc);
@@ -718,9 +773,9 @@ int build_transfer(const qpinn_circuit* c, const float* qp, const TrCircuit& tc_
     tr_circuit_fwd<NN><<<D, kTrThreads, 0, st>>>(n, c->L, ent, tc_.U, tc_.ph, p.perm, B, \
                                                  tc_.CK);                                \
     break;
-    QPINN_TR_CF(5) QPINN_TR_CF(6) QPINN_TR_CF(7) QPINN_TR_CF(8) QPINN_TR_CF(9)
+    QPINN_TR_CF(5) QPINN_TR_CF(6) QPINN_TR_CF(7) QPINN_TR_CF(8) QPINN_TR_CF(9) QPINN_TR_CF(10)
 #undef QPINN_TR_CF
-    default: return fail(QPINN_ERR_CAPACITY, "transfer PQC covers 5 <= n <= 9");
+    default: return fail(QPINN_ERR_CAPACITY, "transfer PQC covers 5 <= n <= 10");
   }
   tr_wmat<<<(2 * D * D + 255) / 256, 256, 0, st>>>(n, B, tc_.W, tc_.Wt);
   QPINN_CUDA_CHECK(cudaGetLastError());
@@ -929,10 +984,11 @@ bool transfer_supported(const qpinn_circuit* c, int dtype) {
   return c && dtype == QPINN_F32 && c->n >= 5 && c->n <= kTrMaxN && layer_entangler(c) >= 0;
 }
 
-// the default (variant 0) path: the transfer map up to n = 8, and at n = 9 from L = 4
-// (its cost does not grow with L: K1 1.9 ms, K2 6.6-6.9 ms at 2^16 points against the
-// CTA kernels' 2.3-2.7 / 11.5-13.1 ms at L = 4 and 4.0-4.8 / 19.6-23.1 ms at L = 8;
-// at L = 1 the CTA kernels win, 1.0 / 5.5-6.0 ms; profiles/r02/config5_n9_transfer_vs_cta.txt)
+// the default (variant 0) path: the transfer map up to n = 8, and at n = 9, 10 from
+// L = 4 (its cost does not grow with L; at 2^16 points K1 + K2 take 8.6 ms at n = 9 and
+// 30 ms at n = 10 against the CTA kernels' 14-16 / 33-38 ms at L = 4 and 24-28 / 56-64
+// ms at L = 8; at L = 1 the CTA kernels win, 6.5-7.1 / 16-18 ms;
+// profiles/r02/config5_n9_transfer_vs_cta.txt, config5_n10_transfer_vs_cta.txt)
 bool transfer_default(const qpinn_circuit* c, int dtype) {
   return transfer_supported(c, dtype) && (c->n <= 8 || c->L >= 4);
 }
@@ -955,7 +1011,8 @@ int transfer_forward(const qpinn_circuit* c, const KArgs<float>* a, unsigned cha
     case 7: return fwd_n<7>(c, a, ws, t);
     case 8: return fwd_n<8>(c, a, ws, t);
     case 9: return fwd_n<9>(c, a, ws, t);
-    default: return fail(QPINN_ERR_CAPACITY, "transfer PQC covers 5 <= n <= 9");
+    case 10: return fwd_n<10>(c, a, ws, t);
+    default: return fail(QPINN_ERR_CAPACITY, "transfer PQC covers 5 <= n <= 10");
   }
 }
 
@@ -969,7 +1026,8 @@ int transfer_backward(const qpinn_circuit* c, const KArgs<float>* a, unsigned ch
     case 7: return bwd_n<7>(c, a, ws, t);
     case 8: return bwd_n<8>(c, a, ws, t);
     case 9: return bwd_n<9>(c, a, ws, t);
-    default: return fail(QPINN_ERR_CAPACITY, "transfer PQC covers 5 <= n <= 9");
+    case 10: return bwd_n<10>(c, a, ws, t);
+    default: return fail(QPINN_ERR_CAPACITY, "transfer PQC covers 5 <= n <= 10");
   }
 }
 
