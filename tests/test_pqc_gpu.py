@@ -185,6 +185,7 @@ def test_specialized_kernels_match_generic_and_oracle(kind, dtype):
 
 
 BIG_CASES = [(9, 2, "strongly", True), (10, 1, "cross_mesh_2rot", True), (11, 2, "cross_mesh", True),
+             (9, 4, "cross_mesh", True), (10, 4, "strongly", True),
              (11, 2, "strongly", True), (12, 3, "cross_mesh", True),
              (12, 2, "strongly", True), (13, 1, "basic", True), (14, 1, "cross_mesh_cnot", True),
              (15, 1, "strongly", True), (16, 1, "no_entanglement", True),
@@ -193,10 +194,10 @@ BIG_CASES = [(9, 2, "strongly", True), (10, 1, "cross_mesh_2rot", True), (11, 2,
 
 @pytest.mark.parametrize("n,L,kind,bwd", BIG_CASES)
 def test_cluster_kernels_large_n_vs_oracle(n, L, kind, bwd):
-    """n = 9..16 on the default dispatch vs the oracle: CTA / cluster kernels, and the
-    multi-gate HBM passes (pqc_global.cu) where they take over -- including the mixed
-    cases (n = 11 strongly, n = 12 cross_mesh: forward on the CTA kernels, adjoint on
-    the HBM passes)."""
+    """n = 9..16 on the default dispatch vs the oracle: CTA / cluster kernels, the
+    transfer map (n = 9, 10 from L = 4), and the multi-gate HBM passes (pqc_global.cu)
+    where they take over -- including the mixed cases (n = 11 strongly, n = 12
+    cross_mesh: forward on the CTA kernels, adjoint on the HBM passes)."""
     from paper_2506_23246_b200.ansatz import build_circuit, pqc_backward_raw, pqc_forward_raw
     dtype = torch.float32
     rng = np.random.default_rng(n * 7 + L)
