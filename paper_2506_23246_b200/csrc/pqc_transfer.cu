@@ -811,6 +811,33 @@ int side_stream(cudaStream_t st, SideStream** out) {
   return QPINN_OK;
 }
 
+// A fork of `st` onto the side stream that every return path joins back (errors
+// included): a graph capture never ends with an unjoined fork, and an eager caller
+// never gets control back while side work still runs.  fork() returns the side
+// stream, or `st` itself when there is none (serial fallback).
+struct ForkJoin {
+  SideStream* side = nullptr;
+  cudaStream_t st = nullptr;
+  int fork(cudaStream_t main, cudaStream_t* out) {
+    st = main;
+    *out = main;
+    static const bool serial = getenv("QPINN_SERIAL_BWD") != nullptr;  // A/B switch
+    if (serial) return QPINN_OK;
+    if (int rc = side_stream(main, &side)) return rc;
+    if (!side) return QPINN_OK;
+    QPINN_CUDA_CHECK(cudaEventRecord(side->fork, main));
+    QPINN_CUDA_CHECK(cudaStreamWaitEvent(side->s, side->fork, 0));
+    *out = side->s;
+    return QPINN_OK;
+  }
+  ~ForkJoin() {
+    if (side) {
+      cudaEventRecord(side->join, side->s);
+      cudaStreamWaitEvent(st, side->join, 0);
+    }
+  }
+};
+
 // QPINN_TR_FUSED_READOUT=0: the separate tr_readout pass (A/B experiments)
 bool fused_readout_off() {
   static const bool off = [] {
@@ -845,28 +872,10 @@ int fwd_n(const qpinn_circuit* c, const KArgs<float>* a, unsigned char* ws, cons
   {
     // the circuit's transfer map depends on qparams only: it is built on the side
     // stream while the points are embedded, and joined before the map's GEMM
-    SideStream* side = nullptr;
-    static const bool serial = getenv("QPINN_SERIAL_BWD") != nullptr;  // A/B switch
-    if (!serial)
-      if (int rc = side_stream(st, &side)) return rc;
-    struct Join {  // every return path joins a forked side stream back into `st`
-      SideStream* side = nullptr;
-      cudaStream_t st = nullptr;
-      ~Join() {
-        if (side) {
-          cudaEventRecord(side->join, side->s);
-          cudaStreamWaitEvent(st, side->join, 0);
-        }
-      }
-    } join;
-    if (side) {
-      QPINN_CUDA_CHECK(cudaEventRecord(side->fork, st));
-      QPINN_CUDA_CHECK(cudaStreamWaitEvent(side->s, side->fork, 0));
-      join.side = side;
-      join.st = st;
-    }
-    if (int rc = build_transfer(c, a->qp, cc, (cplx<float>*)(ws + t.B), side ? side->s : st))
-      return rc;
+    ForkJoin fj;
+    cudaStream_t s2;
+    if (int rc = fj.fork(st, &s2)) return rc;
+    if (int rc = build_transfer(c, a->qp, cc, (cplx<float>*)(ws + t.B), s2)) return rc;
     tr_embed<NQ><<<grid_points(a->R), 256, 0, st>>>(a->scale, a->R, a->act, a->tan, Phi,
                                                     a->maxabs);
     QPINN_CUDA_CHECK(cudaGetLastError());
@@ -938,39 +947,23 @@ int bwd_n(const qpinn_circuit* c, const KArgs<float>* a, unsigned char* ws, cons
     QPINN_CUDA_CHECK(cudaGetLastError());
     return pqc_param_grads<float>(c, acc, NQ, a->qp, a->g_qp, s2);
   };
-  SideStream* side = nullptr;
-  static const bool serial = getenv("QPINN_SERIAL_BWD") != nullptr;  // A/B switch
-  if (Phi && !serial)
-    if (int rc = side_stream(st, &side)) return rc;
-  // once forked, every return path (errors included) joins the side stream back
-  // into `st`, so a graph capture never ends with an unjoined fork and an eager
-  // caller never gets control back while side work still writes g_qp
-  struct Join {
-    SideStream* side = nullptr;
-    cudaStream_t st = nullptr;
-    ~Join() {
-      if (side) {
-        cudaEventRecord(side->join, side->s);
-        cudaStreamWaitEvent(st, side->join, 0);
-      }
-    }
-  } join;
-  if (side) {
-    QPINN_CUDA_CHECK(cudaEventRecord(side->fork, st));
-    QPINN_CUDA_CHECK(cudaStreamWaitEvent(side->s, side->fork, 0));
-    join.side = side;
-    join.st = st;
-  }
+  // with the hand-off the weight chain forks onto the side stream (joined on every
+  // return path, errors included: it writes g_qp)
+  ForkJoin fj;
+  cudaStream_t s2 = st;
+  if (Phi)
+    if (int rc = fj.fork(st, &s2)) return rc;
+  const bool side = s2 != st;
   // dL/dm = Abar W'^T  (D per row)
   const tc::Wsplit wsp = split_w(cc, D);
   if (int rc = tc::gemm3(4 * a->R, D, D2, Abar, D2, cc.W, D2, G, D, ws + t.g3,
                          tc::gemm3_workspace_bytes(D2, D2), st, &wsp))
     return rc;
   if (side)
-    if (int rc = weight_chain(side->s)) return rc;
+    if (int rc = weight_chain(s2)) return rc;
   tr_embed_grad<NQ><<<gp, 256, 0, st>>>(a->scale, a->R, a->act, a->tan, G, a->g_act, a->g_tan);
   QPINN_CUDA_CHECK(cudaGetLastError());
-  if (side) return QPINN_OK;  // joined by `join`
+  if (side) return QPINN_OK;  // joined by `fj`
   // replay path: re-embed m into G once the embedding gradient has read it
   tr_embed<NQ><<<gp, 256, 0, st>>>(a->scale, a->R, a->act, a->tan, G, nullptr);
   Phi = G;
