@@ -8,4 +8,4 @@ for v in 1 0 1 0; do
   env $1=$v timeout 600 python bench.py --steps 30 --warmup 5 --no-cpu-baseline > gpurun_out/b_ab.json 2>/dev/null
   python -c "import json; d=json.load(open('gpurun_out/b_ab.json')); print('$1=$v', d['ms_per_step'], d['value'], d['e2e']['value'])"
 done
-timeout 300 python scripts/profile_step.py > gpurun_out/step_kernels_ab.txt 2>&1; head -30 gpurun_out/step_kernels_ab.txt | grep -E "GPU kernel|features|adapter"
+timeout 300 python scripts/profile_step.py > gpurun_out/step_kernels_ab.txt 2>&1; grep -E "GPU kernel|tanh" gpurun_out/step_kernels_ab.txt
