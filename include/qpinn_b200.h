@@ -93,6 +93,11 @@ int qpinn_circuit_set_kernel_variant(qpinn_circuit* c, int variant);
 int qpinn_circuit_specialized(const qpinn_circuit* c);
 /* 1 if forward/backward run the transfer-matrix kernels for `dtype`. */
 int qpinn_pqc_uses_transfer(const qpinn_circuit* c, int dtype);
+/* Which kernels a forward (backward = 0, with tangents) or adjoint (backward = 1)
+ * of this circuit runs for `dtype` (diagnostics): 0 layer-loop register kernels,
+ * 1 generic register kernels, 2 transfer-matrix map, 3 shared-memory / cluster
+ * kernels, 4 multi-gate HBM passes, 5 one-pass-per-gate global-memory kernels. */
+int qpinn_pqc_regime(const qpinn_circuit* c, int dtype, int backward);
 /* Largest n_qubits the register-resident kernels accept for `dtype`. */
 int qpinn_pqc_max_qubits(int dtype);
 

@@ -65,6 +65,7 @@ SIGNATURES = [
     ("qpinn_circuit_set_kernel_variant", _I, [_VP, _I]),
     ("qpinn_circuit_specialized", _I, [_VP]),
     ("qpinn_pqc_uses_transfer", _I, [_VP, _I]),
+    ("qpinn_pqc_regime", _I, [_VP, _I, _I]),
     ("qpinn_pqc_max_qubits", _I, [_I]),
     ("qpinn_pqc_workspace_bytes", _SZ, [_VP, _I, _I64]),
     ("qpinn_pqc_state_bytes", _SZ, [_VP, _I, _I64]),

@@ -176,6 +176,13 @@ class CircuitSpec:
         """K1/K2 run as the transfer-matrix map on the tensor cores for ``dtype``."""
         return bool(N.lib().qpinn_pqc_uses_transfer(self._h, N.dtype_code(dtype)))
 
+    REGIMES = ("layer", "generic", "transfer", "cta/cluster", "multi-gate HBM", "global")
+
+    def regime(self, dtype, backward: bool = False) -> str:
+        """The kernels K1 (or, with backward, K2) runs for this circuit and dtype."""
+        r = N.lib().qpinn_pqc_regime(self._h, N.dtype_code(dtype), int(backward))
+        return self.REGIMES[r] if 0 <= r < len(self.REGIMES) else "unknown"
+
     def set_kernel_variant(self, variant: str) -> None:
         """"auto" (transfer-matrix kernels for float32 n = 5..8, and n = 9, 10 from
         L = 4, else the layer-loop / CTA kernels), "generic", "transfer" (float32,

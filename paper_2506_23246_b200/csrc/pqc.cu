@@ -675,6 +675,19 @@ static bool use_transfer(const qpinn_circuit* c, int dtype) {
   return c->variant == 0 && transfer_default(c, dtype);
 }
 
+int qpinn_pqc_regime(const qpinn_circuit* c, int dtype, int backward) {
+  if (!c) return -1;
+  if (use_transfer(c, dtype)) return 2;
+  if (c->n <= qpinn_pqc_max_qubits(dtype))
+    return (c->variant == 0 || c->variant == 3) && layer_entangler(c) >= 0 ? 0 : 1;
+  if (backward) {
+    if (hbm_bwd_supported(c, dtype)) return 4;
+    return big_bwd_supported(c, dtype) ? 3 : 5;
+  }
+  if (hbm_fwd_supported(c, dtype)) return 4;
+  return big_fwd_supported(c, dtype) ? 3 : 5;
+}
+
 int qpinn_pqc_uses_transfer(const qpinn_circuit* c, int dtype) {
   return c && use_transfer(c, dtype) ? 1 : 0;
 }

@@ -6,7 +6,7 @@ diagonal, no_entanglement), acos scaling.
 Inputs: a ~ U(-0.9, 0.9) [R,n], tangents ~ N(0,1) [3,R,n], qparams ~ U(0, 2pi),
 seed 0.  R*2^n is capped (the statevector work per point grows as 2^n); the
 metric is points/s and algorithmic TFLOP/s (roofline.pqc_flops).
-Usage: python scripts/sweep_pqc.py [--quick] [--n=..] [--variant=..]   -> one JSON line per cell
+Usage: python scripts/sweep_pqc.py [--quick] [--n=..] [--variant=..] [--all-ansatze]   -> one JSON line per cell
 """
 import json
 import os
@@ -52,6 +52,9 @@ def main():
             variant = arg.split("=", 1)[1]
     Ls = (1, 4) if quick else (1, 4, 8)
     kinds = ("strongly", "cross_mesh", "no_entanglement")
+    if "--all-ansatze" in sys.argv:  # all six ansatze
+        kinds = ("basic", "strongly", "cross_mesh", "cross_mesh_2rot", "cross_mesh_cnot",
+                 "no_entanglement")
     for n in ns:
         for L in Ls:
             for kind in kinds:
@@ -86,10 +89,8 @@ def main():
                     row["k2_tflops"] = round(fa * R / ms_b / 1e9, 2)
                 except CapacityError as e:
                     row["k2"] = f"unsupported: {e}"
-                row["regime"] = ("transfer (tcgen05 GEMMs)" if c.uses_transfer(torch.float32) else
-                                 "warp" if n <= 8 else ("cta" if n <= 12 else "cluster"))
-                if n >= 15:
-                    row["k2_regime"] = "hbm (global-memory checkpoints)"
+                row["regime"] = c.regime(torch.float32)  # K1's kernels (qpinn_pqc_regime)
+                row["k2_regime"] = c.regime(torch.float32, backward=True)
                 print(json.dumps(row), flush=True)
                 del a, da, g, gd, st
                 torch.cuda.empty_cache()

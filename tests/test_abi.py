@@ -83,3 +83,28 @@ def test_quantum_layer_rejects_cpu_tensors():
     with pytest.raises(ConfigError):
         quantum_layer_forward(torch.zeros(4, 3, dtype=torch.float64), np.zeros(12), "strongly",
                               "acos")
+
+
+@pytest.mark.parametrize("n,L,kind,fwd,bwd", [
+    (4, 2, "strongly", "layer", "layer"),
+    (7, 4, "strongly", "transfer", "transfer"),
+    (8, 4, "cross_mesh", "transfer", "transfer"),
+    (9, 1, "strongly", "cta/cluster", "cta/cluster"),
+    (9, 4, "strongly", "transfer", "transfer"),
+    (10, 8, "no_entanglement", "transfer", "transfer"),
+    (11, 4, "strongly", "cta/cluster", "multi-gate HBM"),
+    (11, 4, "cross_mesh", "cta/cluster", "cta/cluster"),
+    (12, 1, "strongly", "cta/cluster", "multi-gate HBM"),
+    (12, 4, "strongly", "multi-gate HBM", "multi-gate HBM"),
+    (12, 4, "cross_mesh", "cta/cluster", "multi-gate HBM"),
+    (13, 4, "cross_mesh", "multi-gate HBM", "multi-gate HBM"),
+    (16, 8, "strongly", "multi-gate HBM", "multi-gate HBM"),
+])
+def test_float32_dispatch_table(n, L, kind, fwd, bwd):
+    """The float32 K1 / K2 kernel choice (qpinn_pqc_regime) follows the measured
+    dispatch table of DESIGN 3.1a / 3.3 (host-side logic, no GPU needed)."""
+    import torch
+    from paper_2506_23246_b200.ansatz import build_circuit
+    c = build_circuit(kind, n, L)
+    assert c.regime(torch.float32) == fwd
+    assert c.regime(torch.float32, backward=True) == bwd
