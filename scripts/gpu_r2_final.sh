@@ -13,7 +13,7 @@ timeout 900 python bench.py --workload config3 --steps 10 --warmup 3 --no-cpu-ba
 QPINN_BENCH_FUNCTIONAL_DP=1 timeout 600 python bench.py --gpus 2 --steps 3 --warmup 3 --no-cpu-baseline > $O/bench_dp2_functional_gloo.log 2>&1
 timeout 300 python scripts/profile_step.py > $O/step_kernels.txt 2>&1
 timeout 1200 python scripts/sweep_ablation.py 5 > $O/config4_ablation_dielectric.jsonl 2> $O/config4.err
-timeout 2400 python scripts/sweep_pqc.py > $O/config5_sweep.jsonl 2> $O/config5.err
+timeout 2400 python scripts/sweep_pqc.py --all-ansatze > $O/config5_sweep.jsonl 2> $O/config5.err
 timeout 600 python scripts/fp32_error_budget.py > $O/fp32_error_budget.json 2> $O/fp32_error_budget.err
 timeout 300 python bench.py --steps 2 --warmup 3 --no-cpu-baseline > $O/bench_small.json 2>&1 && \
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/ncu_launches.csv \
