@@ -649,9 +649,9 @@ static BigTables big_tables(const qpinn_circuit* c, unsigned char* base) {
   return t;
 }
 
-template <typename K>
+template <typename K, typename... Args>
 static int launch_cluster(K kern, int grid, int threads, size_t smem, int C, cudaStream_t st,
-                          auto... args) {
+                          Args... args) {
   QPINN_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
