@@ -110,7 +110,9 @@ int qpinn_pqc_max_qubits(int dtype);
  * from n = 12 with CNOT entanglers and L >= 2, or L >= 8, else from n = 13;
  * adjoint from n = 12, and n = 11 with CNOT entanglers or L = 1), streaming
  * batches of points' states through this scratch: up to ~256 MB for the
- * forward and ~1 GB (states, adjoints, layer checkpoints) for the adjoint. */
+ * forward and ~1 GB (states, adjoints, layer checkpoints) for the adjoint.
+ * The size depends on the kernel variant: query it (and qpinn_pqc_state_bytes)
+ * after qpinn_circuit_set_kernel_variant. */
 size_t qpinn_pqc_workspace_bytes(const qpinn_circuit* c, int dtype, int64_t rows);
 
 /* Bytes of the optional state hand-off buffer that lets the backward skip

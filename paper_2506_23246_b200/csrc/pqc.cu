@@ -694,8 +694,12 @@ int qpinn_pqc_uses_transfer(const qpinn_circuit* c, int dtype) {
 
 size_t qpinn_pqc_workspace_bytes(const qpinn_circuit* c, int dtype, int64_t rows) {
   if (!c) return 0;
-  size_t t = 0;  // the transfer-matrix kernels (any variant may be selected later)
-  if (transfer_supported(c, dtype)) t = small_ws_bytes(c) + transfer_workspace_bytes(c, rows);
+  // the transfer-matrix kernels: up to n = 8 whatever the variant, beyond that (where
+  // their staging is GBs at large batches) only when the current variant selects them
+  // -- query the size after qpinn_circuit_set_kernel_variant
+  size_t t = 0;
+  if (c->n <= qpinn_pqc_max_qubits(dtype) ? transfer_supported(c, dtype) : use_transfer(c, dtype))
+    t = small_ws_bytes(c) + transfer_workspace_bytes(c, rows);
   if (c->n > qpinn_pqc_max_qubits(dtype)) {
     const size_t b = align_up(big_workspace_bytes(c, dtype), 256) +
                      global_adjoint_workspace_bytes(c, dtype, rows);
@@ -712,8 +716,12 @@ size_t qpinn_pqc_state_bytes(const qpinn_circuit* c, int dtype, int64_t rows) {
   const size_t per = 4 * ((size_t)1 << c->n) * 2 * (dtype == QPINN_F64 ? 8 : 4);
   const bool layer = c->n <= qpinn_pqc_max_qubits(dtype) && layer_entangler(c) >= 0;
   const size_t b = (size_t)rows * per * (layer && c->L > 1 ? (size_t)c->L : 1);
-  if (!transfer_supported(c, dtype)) return b;
-  const size_t t = transfer_state_bytes(c, rows);  // Psi, Phi, W, checkpoints, tables
+  // the transfer-matrix hand-off (Psi, Phi, W, checkpoints, tables): up to n = 8 for
+  // any variant, beyond that only when the current variant selects the transfer map
+  const bool tr = c->n <= qpinn_pqc_max_qubits(dtype) ? transfer_supported(c, dtype)
+                                                       : use_transfer(c, dtype);
+  if (!tr) return b;
+  const size_t t = transfer_state_bytes(c, rows);
   return t > b ? t : b;
 }
 
