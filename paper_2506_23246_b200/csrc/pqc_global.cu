@@ -483,10 +483,11 @@ GbLayout gb_layout(const qpinn_circuit* c) {
   return g;
 }
 
-// ---- several gates per HBM pass (fp32, 13 <= n <= 16) --------------------------------
+// ---- several gates per HBM pass (fp32, 9 <= n <= 16; the default from n = 11-13) -------
 // The one-pass-per-gate kernels above stream the [B][4][D] states through HBM once per
 // gate.  Here the basis index is split as b = (s, l): the top h = n - kHbT bits s
-// (wires 0 .. h-1) and the low kHbT bits l.  Two pass kinds each apply a run of ops in
+// (wires 0 .. h-1) and the low kHbT bits l (for n <= kHbT: h = 0, the tile is the
+// whole state and every pass is an SM pass).  Two pass kinds each apply a run of ops in
 // one read + write of the state:
 //   SM pass: one CTA per (row, s) holds the 2^kHbT amplitudes of that slice in
 //            shared memory -- gates on low wires, CNOTs whose target is a low wire

@@ -65,7 +65,8 @@ template <typename T>
 int global_forward(const qpinn_circuit* c, const KArgs<T>* a, unsigned char* ws, size_t bytes);
 // whether a cluster forward kernel with tangents exists for this circuit
 bool big_fwd_supported(const qpinn_circuit* c, int dtype);
-// forward with several gates per HBM pass (pqc_global.cu): fp32, 13 <= n <= 16
+// forward with several gates per HBM pass (pqc_global.cu): fp32, 9 <= n <= 16 (the default
+// from n = 11-13, see hbm_fwd_supported / hbm_bwd_supported)
 bool hbm_fwd_supported(const qpinn_circuit* c, int dtype);
 int hbm_forward(const qpinn_circuit* c, const KArgs<float>* a, unsigned char* ws, size_t bytes);
 int hbm_forward_passes(const qpinn_circuit* c);
