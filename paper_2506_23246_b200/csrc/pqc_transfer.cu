@@ -335,6 +335,46 @@ __device__ __forceinline__ void embed_amp(const PointAngles<NQ>& pa, int b, bool
   }
 }
 
+// embed_amp for the 4 amplitudes b0 .. b0 + 3 (b0 % 4 == 0: only the last two wires
+// differ): the first NQ - 2 factors, and their tangent terms, are shared
+template <int NQ>
+__device__ __forceinline__ void embed_amp4(const PointAngles<NQ>& pa, int b0, bool tangents,
+                                           float (&m0)[4], float (&mk)[4][3]) {
+  constexpr int H = NQ - 2;
+  float pre[H + 1];
+  pre[0] = 1.f;
+#pragma unroll
+  for (int q = 0; q < H; ++q) pre[q + 1] = pre[q] * (((b0 >> (NQ - 1 - q)) & 1) ? pa.s[q] : pa.c[q]);
+  const float P = pre[H];
+  // the last two wires: factor f(bit) and derivative factor df(bit) (as embed_amp)
+  const float fa[2] = {pa.c[H], pa.s[H]}, fb[2] = {pa.c[H + 1], pa.s[H + 1]};
+  const float da[2] = {-0.5f * pa.s[H], 0.5f * pa.c[H]}, db[2] = {-0.5f * pa.s[H + 1], 0.5f * pa.c[H + 1]};
+#pragma unroll
+  for (int e = 0; e < 4; ++e) m0[e] = P * fa[e >> 1] * fb[e & 1];
+#pragma unroll
+  for (int e = 0; e < 4; ++e) mk[e][0] = mk[e][1] = mk[e][2] = 0.f;
+  if (!tangents) return;
+  float T[3] = {0.f, 0.f, 0.f};  // sum over the shared wires of d_kq df_q prod_{q' != q} f_q'
+  float suf = 1.f;
+#pragma unroll
+  for (int q = H - 1; q >= 0; --q) {
+    const bool bit = (b0 >> (NQ - 1 - q)) & 1;
+    const float df = bit ? 0.5f * pa.c[q] : -0.5f * pa.s[q];
+    const float rest = pre[q] * suf;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) T[k] += pa.d[k][q] * df * rest;
+    suf *= bit ? pa.s[q] : pa.c[q];
+  }
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    const int ia = e >> 1, ib = e & 1;
+#pragma unroll
+    for (int k = 0; k < 3; ++k)
+      mk[e][k] = T[k] * fa[ia] * fb[ib] + pa.d[k][H] * da[ia] * P * fb[ib] +
+                 pa.d[k][H + 1] * db[ib] * P * fa[ia];
+  }
+}
+
 // lane l ends with the warp total of value index l (recursive halving, 31 shuffles)
 __device__ __forceinline__ void reduce_scatter32(float* v);
 
@@ -407,13 +447,28 @@ __global__ void __launch_bounds__(256, NQ >= 9 ? 1 : NQ >= 8 ? 2 : QPINN_TR_EMB_
       const int64_t p = p0 + pl;
       PointAngles<NQ> pa;
       read_angles<NQ>(ang + pl * NQ * kAng, pa);
-#pragma unroll(NQ >= 10 ? 4 : D / 32)
-      for (int b = lane; b < D; b += 32) {
-        float m0, mk[3];
-        embed_amp<NQ>(pa, b, tan != nullptr, m0, mk);
-        Phi[p * D + b] = m0;  // magnitudes: the phase (-i)^popcount(b) lives in W' (tr_wmat)
-        if (tan)
-          for (int k = 0; k < 3; ++k) Phi[((int64_t)(k + 1) * R + p) * D + b] = mk[k];
+      if constexpr (D >= 128) {  // 4 consecutive amplitudes per lane: 16-byte stores
+#pragma unroll(NQ >= 10 ? 2 : D / 128)
+        for (int b0 = 4 * lane; b0 < D; b0 += 128) {
+          float m0[4], mk[4][3];
+          embed_amp4<NQ>(pa, b0, tan != nullptr, m0, mk);
+          // magnitudes: the phase (-i)^popcount(b) lives in W' (tr_wmat)
+          *reinterpret_cast<float4*>(Phi + p * D + b0) = make_float4(m0[0], m0[1], m0[2], m0[3]);
+          if (tan)
+#pragma unroll
+            for (int k = 0; k < 3; ++k)
+              *reinterpret_cast<float4*>(Phi + ((int64_t)(k + 1) * R + p) * D + b0) =
+                  make_float4(mk[0][k], mk[1][k], mk[2][k], mk[3][k]);
+        }
+      } else {
+#pragma unroll
+        for (int b = lane; b < D; b += 32) {
+          float m0, mk[3];
+          embed_amp<NQ>(pa, b, tan != nullptr, m0, mk);
+          Phi[p * D + b] = m0;
+          if (tan)
+            for (int k = 0; k < 3; ++k) Phi[((int64_t)(k + 1) * R + p) * D + b] = mk[k];
+        }
       }
     }
     __syncthreads();
