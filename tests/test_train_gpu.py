@@ -52,7 +52,9 @@ def _check_fields(got, want, dtype, what):
 EVALS = ["eval_micro_vacuum.npz", "eval_micro_diel.npz", "eval_micro_asym.npz", "eval_desk.npz",
          "eval_vacuum7.npz", "eval_diel7.npz",
          # 6 qubits: the transfer-matrix PQC kernels (permutation and phase entanglers)
-         "eval_n6_strongly.npz", "eval_n6_crossmesh.npz"]
+         "eval_n6_strongly.npz", "eval_n6_crossmesh.npz",
+         # 8 and 9 qubits: the transfer map where it became the default in round 2
+         "eval_n8_strongly.npz", "eval_n9_crossmesh.npz"]
 
 
 @pytest.mark.parametrize("dtype", [torch.float64, torch.float32])
