@@ -1,6 +1,7 @@
-"""Golden LossEvaluator.evaluate(tape=True) vectors for 8- and 9-qubit hybrid models,
-which run the transfer-matrix PQC kernels by default since round 2 (n = 8 at any depth,
-n = 9 from L = 4; one permutation and one phase ansatz).
+"""Golden LossEvaluator.evaluate(tape=True) vectors for 8-, 9- and 12-qubit hybrid
+models: n = 8, 9 run the transfer-matrix PQC kernels by default since round 2 (n = 8 at
+any depth, n = 9 from L = 4; one permutation and one phase ansatz); n = 12 (strongly,
+L = 2) runs the multi-gate HBM passes for both K1 and K2.
 
     PYTHONDONTWRITEBYTECODE=1 python tests/golden/make_golden_n8.py
 
@@ -22,3 +23,6 @@ eval_case("eval_n8_strongly.npz",
 eval_case("eval_n9_crossmesh.npz",
           ModelConfig(**base, n_qubits=9, n_layers_pqc=4, ansatz="cross_mesh", scale="asin"),
           (4, 4, 4), "dielectric", t_end=0.7, chunk_slices=2, weights=None, energy=False)
+eval_case("eval_n12_strongly.npz",
+          ModelConfig(**base, n_qubits=12, n_layers_pqc=2, ansatz="strongly", scale="acos"),
+          (3, 3, 3), "vacuum", chunk_slices=3, weights=w)
