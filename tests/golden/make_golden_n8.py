@@ -1,7 +1,7 @@
-"""Golden LossEvaluator.evaluate(tape=True) vectors for 8-, 9- and 12-qubit hybrid
-models: n = 8, 9 run the transfer-matrix PQC kernels by default since round 2 (n = 8 at
-any depth, n = 9 from L = 4; one permutation and one phase ansatz); n = 12 (strongly,
-L = 2) runs the multi-gate HBM passes for both K1 and K2.
+"""Golden LossEvaluator.evaluate(tape=True) vectors for 8-, 9-, 10- and 12-qubit hybrid
+models: n = 8, 9, 10 run the transfer-matrix PQC kernels by default since round 2 (n = 8
+at any depth, n = 9, 10 from L = 4; permutation, phase and two-rotation phase ansaetze);
+n = 12 (strongly, L = 2) runs the multi-gate HBM passes for both K1 and K2.
 
     PYTHONDONTWRITEBYTECODE=1 python tests/golden/make_golden_n8.py
 
@@ -26,3 +26,6 @@ eval_case("eval_n9_crossmesh.npz",
 eval_case("eval_n12_strongly.npz",
           ModelConfig(**base, n_qubits=12, n_layers_pqc=2, ansatz="strongly", scale="acos"),
           (3, 3, 3), "vacuum", chunk_slices=3, weights=w)
+eval_case("eval_n10_2rot.npz",
+          ModelConfig(**base, n_qubits=10, n_layers_pqc=4, ansatz="cross_mesh_2rot", scale="pi"),
+          (4, 4, 3), "asymmetric", chunk_slices=2, weights=None)

@@ -49,7 +49,7 @@ def test_oracle_circuit_dump_matches_reference():
                                   "eval_vacuum7.npz", "eval_diel7.npz",
                                   "eval_n6_strongly.npz", "eval_n6_crossmesh.npz",
                                   "eval_n8_strongly.npz", "eval_n9_crossmesh.npz",
-                                  "eval_n12_strongly.npz"])
+                                  "eval_n10_2rot.npz", "eval_n12_strongly.npz"])
 def test_oracle_evaluate_matches_reference(name):
     g = load_golden(name)
     h, F, n, L, seed = (int(v) for v in g["config"])

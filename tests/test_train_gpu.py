@@ -54,7 +54,7 @@ EVALS = ["eval_micro_vacuum.npz", "eval_micro_diel.npz", "eval_micro_asym.npz", 
          # 6 qubits: the transfer-matrix PQC kernels (permutation and phase entanglers)
          "eval_n6_strongly.npz", "eval_n6_crossmesh.npz",
          # 8 and 9 qubits: the transfer map where it became the default in round 2
-         "eval_n8_strongly.npz", "eval_n9_crossmesh.npz",
+         "eval_n8_strongly.npz", "eval_n9_crossmesh.npz", "eval_n10_2rot.npz",
          # 12 qubits: the multi-gate HBM passes (K1 and K2)
          "eval_n12_strongly.npz"]
 
