@@ -513,6 +513,9 @@ GbLayout gb_layout(const qpinn_circuit* c) {
 // costs about two passes.  OUTER partials are reduced per CTA and then across CTAs
 // in a fixed order (deterministic).
 constexpr int kHbT = 12;  // low bits per SM tile: 2^12 complex = 32 KB of shared memory
+// the forward (no checkpoint tile) may use 2^13-amplitude tiles (64 KB): at n = 13 the
+// whole circuit runs in SM passes, and from n = 14 one wire fewer goes to CS passes
+constexpr int kHbTmax = 13;
 // the SM tile of an n-qubit state: the whole state (h = 0, SM passes only) for n <= 12
 inline int hb_tbits(int n) { return n < kHbT ? n : kHbT; }
 enum { HB_U1 = 0, HB_CNOT = 1, HB_PHASE = 2, HB_OUTER = 3 };
@@ -533,9 +536,10 @@ struct HbPass {
 struct HbPlan {
   std::vector<HbOp> ops;
   std::vector<HbPass> passes;
-  std::vector<int> luts;  // per CNOT run of an SM pass: [64 low | 64 high | 16 slice] index maps
+  std::vector<int> luts;  // per CNOT run of an SM pass: [64 low | 128 high | 16 slice] index maps
+  int T = kHbT;           // low (tile) bits of this plan's SM passes
 };
-constexpr int kHbLut = 64 + 64 + 16;
+constexpr int kHbLut = 64 + 128 + 16;
 
 struct HbSOp {  // an op being scheduled
   HbOp op;
@@ -629,6 +633,7 @@ void hb_schedule(const std::vector<HbSOp>& seq, HbPlan& plan) {
 // the slice bits as fixed controls): new[i] = old[f(i, s)] with f = g_first o ... o
 // g_last, g(j) = j ^ (bit_c(j) << t), tabulated as f(i, s) = lo[i & 63] ^ hi[i >> 6] ^ sl[s]
 void hb_tabulate(HbPlan& plan) {
+  const int T = plan.T;
   for (const HbPass& ps : plan.passes) {
     if (ps.kind != HB_SM) continue;
     int o = ps.op0;
@@ -644,7 +649,7 @@ void hb_tabulate(HbPlan& plan) {
         int j = i;
         for (int q = e - 1; q >= o; --q) {
           const HbOp& c = plan.ops[q];
-          const int on = c.a >= kHbT ? (sl >> (c.a - kHbT)) & 1 : (j >> c.a) & 1;
+          const int on = c.a >= T ? (sl >> (c.a - T)) & 1 : (j >> c.a) & 1;
           j ^= on << (c.b & 0xff);
         }
         return j;
@@ -653,11 +658,9 @@ void hb_tabulate(HbPlan& plan) {
       plan.luts.resize(off + kHbLut, 0);
       int* lo = plan.luts.data() + off;
       int* hi = lo + 64;
-      int* sl = hi + 64;
-      for (int v = 0; v < 64; ++v) {
-        lo[v] = f(v, 0);
-        hi[v] = f(v << 6, 0);
-      }
+      int* sl = hi + 128;
+      for (int v = 0; v < 64; ++v) lo[v] = f(v, 0);
+      for (int v = 0; v < 128; ++v) hi[v] = f(v << 6, 0);
       for (int v = 0; v < 16; ++v) sl[v] = f(0, v);
       plan.ops[o].idx = off;
       plan.ops[o].b = (plan.ops[o].b & 0xff) | ((e - o) << 8);
@@ -671,8 +674,8 @@ struct HbLayerOps {
   std::vector<HbSOp> u1, ent;
 };
 
-std::vector<HbLayerOps> hb_layers(const qpinn_circuit* c) {
-  const int n = c->n, h = n - hb_tbits(n);
+std::vector<HbLayerOps> hb_layers(const qpinn_circuit* c, int T) {
+  const int n = c->n, h = n - T;
   std::vector<HbLayerOps> layers(c->L);
   const int n_steps = (int)c->steps.size() / 3;
   int l = 0, in_layer = 0;
@@ -709,13 +712,28 @@ std::vector<HbLayerOps> hb_layers(const qpinn_circuit* c) {
 }
 
 // forward (no checkpoints): the whole circuit as one schedule
-HbPlan hb_plan(const qpinn_circuit* c) {
+// the forward's tile bits: at n = 13 one 2^13-amplitude tile holds the whole state, so
+// every op runs in SM passes (strongly L = 4: 18.3 -> 12.5 ms, cross_mesh 15.2 -> 12.5 ms
+// at 8192 points); from n = 14 the 12-bit tiles are as fast or faster (n = 16 strongly:
+// 18.4 vs 19.1 ms at L = 4; profiles/r02/hb_forward_tile_bits.txt).  QPINN_HB_FWD_T
+// overrides the tile bits (9..13).
+int hb_fwd_tbits(int n) {
+  static const int env = [] {
+    const char* e = getenv("QPINN_HB_FWD_T");
+    return e ? atoi(e) : 0;
+  }();
+  const int t = env >= 9 && env <= kHbTmax ? env : (n == kHbTmax ? kHbTmax : kHbT);
+  return n < t ? n : t;
+}
+
+HbPlan hb_plan(const qpinn_circuit* c, int T) {
   std::vector<HbSOp> seq;
-  for (const HbLayerOps& lo : hb_layers(c)) {
+  for (const HbLayerOps& lo : hb_layers(c, T)) {
     seq.insert(seq.end(), lo.u1.begin(), lo.u1.end());
     seq.insert(seq.end(), lo.ent.begin(), lo.ent.end());
   }
   HbPlan plan;
+  plan.T = T;
   hb_schedule(seq, plan);
   hb_tabulate(plan);
   return plan;
@@ -727,9 +745,10 @@ struct HbBwdPlan {
 };
 
 HbBwdPlan hb_plan_bwd(const qpinn_circuit* c) {
-  const std::vector<HbLayerOps> layers = hb_layers(c);
+  const std::vector<HbLayerOps> layers = hb_layers(c, hb_tbits(c->n));
   const int L = (int)layers.size();
   HbBwdPlan bp;
+  bp.fwd.T = bp.rev.T = hb_tbits(c->n);
   for (int l = 0; l <= L; ++l) {  // segment l: entangler(l-1), u1(l); checkpoint l after it
     std::vector<HbSOp> seq;
     if (l > 0) seq.insert(seq.end(), layers[l - 1].ent.begin(), layers[l - 1].ent.end());
@@ -867,7 +886,7 @@ __device__ __forceinline__ void hb_sm_u1_group(cplx<float>* t, const HbOp* op,
 #define QPINN_HB_G 2
 #endif
 template <int T>
-__global__ void __launch_bounds__(256, QPINN_HB_MINB)
+__global__ void __launch_bounds__(256, T >= 13 ? 3 : QPINN_HB_MINB)
 hb_sm_pass(int n, cplx<float>* __restrict__ X, const cplx<float>* __restrict__ XC,
            const HbOp* __restrict__ ops, int nops, const int* __restrict__ luts,
            const cplx<float>* __restrict__ U, const cplx<float>* __restrict__ ph,
@@ -882,18 +901,26 @@ hb_sm_pass(int n, cplx<float>* __restrict__ X, const cplx<float>* __restrict__ X
   const int64_t row = blockIdx.x >> h;
   const int s = blockIdx.x & ((1 << h) - 1);
   cplx<float>* x = X + row * D + ((int64_t)s << T);
-  {  // all of the thread's loads in flight before any shared-memory store
-    cplx<float> r[PER];
+  // all of a chunk's loads in flight before its shared-memory stores (chunks of up
+  // to 16 amplitudes per thread keep the registers bounded for 2^13 tiles)
+  constexpr int CH = PER < 16 ? PER : 16;
 #pragma unroll
-    for (int j = 0; j < PER; ++j) r[j] = x[threadIdx.x + 256 * j];
+  for (int j0 = 0; j0 < PER; j0 += CH) {
+    cplx<float> r[CH];
 #pragma unroll
-    for (int j = 0; j < PER; ++j) t[threadIdx.x + 256 * j] = r[j];
-    if (XC) {
-      const cplx<float>* xc = XC + row * D + ((int64_t)s << T);
+    for (int j = 0; j < CH; ++j) r[j] = x[threadIdx.x + 256 * (j0 + j)];
 #pragma unroll
-      for (int j = 0; j < PER; ++j) r[j] = xc[threadIdx.x + 256 * j];
+    for (int j = 0; j < CH; ++j) t[threadIdx.x + 256 * (j0 + j)] = r[j];
+  }
+  if (XC) {
+    const cplx<float>* xc = XC + row * D + ((int64_t)s << T);
 #pragma unroll
-      for (int j = 0; j < PER; ++j) tx[threadIdx.x + 256 * j] = r[j];
+    for (int j0 = 0; j0 < PER; j0 += CH) {
+      cplx<float> r[CH];
+#pragma unroll
+      for (int j = 0; j < CH; ++j) r[j] = xc[threadIdx.x + 256 * (j0 + j)];
+#pragma unroll
+      for (int j = 0; j < CH; ++j) tx[threadIdx.x + 256 * (j0 + j)] = r[j];
     }
   }
   __syncthreads();
@@ -915,7 +942,7 @@ hb_sm_pass(int n, cplx<float>* __restrict__ X, const cplx<float>* __restrict__ X
     } else if (op.type == HB_CNOT) {
       // a run of CNOTs: new[i] = old[f(i, s)] through the run's tabulated index map
       const int* lut = luts + op.idx;
-      const int fs = lut[128 + s];
+      const int fs = lut[192 + s];  // [64 low | 128 high | 16 slice]
       cplx<float> v[PER];
 #pragma unroll
       for (int r = 0; r < PER; ++r) {
@@ -941,14 +968,20 @@ hb_sm_pass(int n, cplx<float>* __restrict__ X, const cplx<float>* __restrict__ X
       ++o;
     } else {
       const cplx<float>* ep = ph + (int64_t)op.idx * D + ((int64_t)s << T);
-      cplx<float> e[PER];
 #pragma unroll
-      for (int j = 0; j < PER; ++j) {
-        e[j] = ep[threadIdx.x + 256 * j];
-        if (op.b) e[j].im = -e[j].im;
+      for (int j0 = 0; j0 < PER; j0 += CH) {
+        cplx<float> e[CH];
+#pragma unroll
+        for (int j = 0; j < CH; ++j) {
+          e[j] = ep[threadIdx.x + 256 * (j0 + j)];
+          if (op.b) e[j].im = -e[j].im;
+        }
+#pragma unroll
+        for (int j = 0; j < CH; ++j) {
+          const int ii = threadIdx.x + 256 * (j0 + j);
+          t[ii] = cmul(t[ii], e[j]);
+        }
       }
-#pragma unroll
-      for (int j = 0; j < PER; ++j) t[threadIdx.x + 256 * j] = cmul(t[threadIdx.x + 256 * j], e[j]);
       ++o;
     }
     __syncthreads();
@@ -996,14 +1029,14 @@ __device__ __forceinline__ void hb_outer_bit(const cplx<float> (&v)[1 << H],
   }
 }
 
-template <int H, bool XOUT>
+template <int H, bool XOUT, int T>
 __global__ void __launch_bounds__(256) hb_cs_pass(int n, int64_t rows, cplx<float>* __restrict__ X,
                                                   const cplx<float>* __restrict__ XC,
                                                   const HbOp* __restrict__ ops, int nops,
                                                   const cplx<float>* __restrict__ U,
                                                   const cplx<float>* __restrict__ ph,
                                                   double* __restrict__ part, int n_outer) {
-  constexpr int V = 1 << H, TS = 1 << kHbT;
+  constexpr int V = 1 << H, TS = 1 << T;
   __shared__ double red[8 * 8];
   const int64_t D = (int64_t)1 << n;
   float mo[XOUT ? 4 : 1][8];  // per-thread outer sums of this pass's OUTER ops (<= H of them)
@@ -1013,17 +1046,17 @@ __global__ void __launch_bounds__(256) hb_cs_pass(int n, int64_t rows, cplx<floa
     for (int k = 0; k < 8; ++k) mo[i][k] = 0.f;
   for (int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; gid < rows * TS;
        gid += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t row = gid >> kHbT;
+    const int64_t row = gid >> T;
     const int l = (int)(gid & (TS - 1));
     cplx<float>* x = X + row * D + l;
     cplx<float> v[V];
 #pragma unroll
-    for (int j = 0; j < V; ++j) v[j] = x[(int64_t)j << kHbT];
+    for (int j = 0; j < V; ++j) v[j] = x[(int64_t)j << T];
     cplx<float> xv[XOUT ? V : 1];
     if constexpr (XOUT) {
       const cplx<float>* xc = XC + row * D + l;
 #pragma unroll
-      for (int j = 0; j < V; ++j) xv[j] = xc[(int64_t)j << kHbT];
+      for (int j = 0; j < V; ++j) xv[j] = xc[(int64_t)j << T];
     }
     int slot = 0;
     for (int o = 0; o < nops; ++o) {
@@ -1031,21 +1064,21 @@ __global__ void __launch_bounds__(256) hb_cs_pass(int n, int64_t rows, cplx<floa
       if (op.type == HB_U1) {
         cplx<float> u[4];
         hb_load_u(U, op, u);
-        const int rb = op.a - kHbT;
+        const int rb = op.a - T;
         if (rb == 0) hb_gate_bit<H, 0>(v, u);
         if constexpr (H > 1) if (rb == 1) hb_gate_bit<H, 1>(v, u);
         if constexpr (H > 2) if (rb == 2) hb_gate_bit<H, 2>(v, u);
         if constexpr (H > 3) if (rb == 3) hb_gate_bit<H, 3>(v, u);
       } else if (op.type == HB_CNOT) {
-        const int rb = (op.b & 0xff) - kHbT;
-        if (op.a < kHbT) {  // low control: fixed for this thread
+        const int rb = (op.b & 0xff) - T;
+        if (op.a < T) {  // low control: fixed for this thread
           if ((l >> op.a) & 1) {
 #pragma unroll
             for (int q = 0; q < H; ++q)
               if (q == rb) hb_swap_bit<H>(v, q, -1);
           }
         } else {
-          const int rc = op.a - kHbT;
+          const int rc = op.a - T;
 #pragma unroll
           for (int q = 0; q < H; ++q)
 #pragma unroll
@@ -1054,7 +1087,7 @@ __global__ void __launch_bounds__(256) hb_cs_pass(int n, int64_t rows, cplx<floa
         }
       } else if (op.type == HB_OUTER) {
         if constexpr (XOUT) {
-          const int rb = op.a - kHbT;
+          const int rb = op.a - T;
 #pragma unroll
           for (int sl = 0; sl < 4; ++sl) {
             if (sl != slot) continue;
@@ -1069,14 +1102,14 @@ __global__ void __launch_bounds__(256) hb_cs_pass(int n, int64_t rows, cplx<floa
         const cplx<float>* e = ph + (int64_t)op.idx * D + l;
 #pragma unroll
         for (int j = 0; j < V; ++j) {
-          cplx<float> ej = e[(int64_t)j << kHbT];
+          cplx<float> ej = e[(int64_t)j << T];
           if (op.b) ej.im = -ej.im;
           v[j] = cmul(v[j], ej);
         }
       }
     }
 #pragma unroll
-    for (int j = 0; j < V; ++j) x[(int64_t)j << kHbT] = v[j];
+    for (int j = 0; j < V; ++j) x[(int64_t)j << T] = v[j];
   }
   if constexpr (XOUT) {
     for (int sl = 0; sl < n_outer; ++sl) {
@@ -1168,26 +1201,38 @@ HbLayout hb_layout(const qpinn_circuit* c, int64_t B, int nops, int nluts) {
   return g;
 }
 
-int hb_cs_grid(int64_t rows) {
-  const int64_t threads = rows << kHbT;
+int hb_cs_grid(int64_t rows, int T) {
+  const int64_t threads = rows << T;
   const int64_t b = (threads + 255) / 256, cap = (int64_t)num_sms() * 8;
   return (int)(b < cap ? b : cap);
 }
 
-int hb_launch_cs(int h, int n, int64_t rows, cplx<float>* X, const cplx<float>* XC,
+int hb_launch_cs(int h, int T, int n, int64_t rows, cplx<float>* X, const cplx<float>* XC,
                  const HbOp* ops, int nops, const cplx<float>* U, const cplx<float>* ph,
                  double* part, int n_outer, cudaStream_t st) {
-  const int grid = hb_cs_grid(rows);
-#define QPINN_HB_CS(H)                                                                       \
-  (XC ? hb_cs_pass<H, true><<<grid, 256, 0, st>>>(n, rows, X, XC, ops, nops, U, ph, part,    \
-                                                  n_outer)                                  \
-      : hb_cs_pass<H, false><<<grid, 256, 0, st>>>(n, rows, X, XC, ops, nops, U, ph, part, 0))
-  switch (h) {
-    case 1: QPINN_HB_CS(1); break;
-    case 2: QPINN_HB_CS(2); break;
-    case 3: QPINN_HB_CS(3); break;
-    case 4: QPINN_HB_CS(4); break;
-    default: return fail(QPINN_ERR_CAPACITY, "multi-gate HBM pass: 13 <= n <= 16");
+  const int grid = hb_cs_grid(rows, T);
+#define QPINN_HB_CS(H, TT)                                                                   \
+  (XC ? hb_cs_pass<H, true, TT><<<grid, 256, 0, st>>>(n, rows, X, XC, ops, nops, U, ph,      \
+                                                      part, n_outer)                        \
+      : hb_cs_pass<H, false, TT><<<grid, 256, 0, st>>>(n, rows, X, XC, ops, nops, U, ph,     \
+                                                       part, 0))
+  if (T == kHbT) {
+    switch (h) {
+      case 1: QPINN_HB_CS(1, kHbT); break;
+      case 2: QPINN_HB_CS(2, kHbT); break;
+      case 3: QPINN_HB_CS(3, kHbT); break;
+      case 4: QPINN_HB_CS(4, kHbT); break;
+      default: return fail(QPINN_ERR_CAPACITY, "multi-gate HBM pass: 13 <= n <= 16");
+    }
+  } else if (T == kHbTmax && !XC) {  // the forward's larger tiles
+    switch (h) {
+      case 1: hb_cs_pass<1, false, kHbTmax><<<grid, 256, 0, st>>>(n, rows, X, XC, ops, nops, U, ph, part, 0); break;
+      case 2: hb_cs_pass<2, false, kHbTmax><<<grid, 256, 0, st>>>(n, rows, X, XC, ops, nops, U, ph, part, 0); break;
+      case 3: hb_cs_pass<3, false, kHbTmax><<<grid, 256, 0, st>>>(n, rows, X, XC, ops, nops, U, ph, part, 0); break;
+      default: return fail(QPINN_ERR_CAPACITY, "multi-gate HBM pass: 14 <= n <= 16 at 13-bit tiles");
+    }
+  } else {
+    return fail(QPINN_ERR_CAPACITY, "multi-gate HBM pass: tile bits");
   }
 #undef QPINN_HB_CS
   QPINN_CUDA_CHECK(cudaGetLastError());
@@ -1195,10 +1240,10 @@ int hb_launch_cs(int h, int n, int64_t rows, cplx<float>* X, const cplx<float>* 
 }
 
 // one pass of a plan on the batch's states (SM or CS kind)
-int hb_run_pass(const HbPass& ps, int n, int64_t rows, cplx<float>* X, const cplx<float>* XC,
-                const HbOp* dops, const int* dluts, const cplx<float>* U, const cplx<float>* ph,
-                double* part, double* acc, cudaStream_t st) {
-  const int tb = hb_tbits(n), h = n - tb;
+int hb_run_pass(const HbPass& ps, int n, int tb, int64_t rows, cplx<float>* X,
+                const cplx<float>* XC, const HbOp* dops, const int* dluts, const cplx<float>* U,
+                const cplx<float>* ph, double* part, double* acc, cudaStream_t st) {
+  const int h = n - tb;
   const HbOp* ops = dops + ps.op0;
   int nctas;
   if (ps.kind == HB_SM) {
@@ -1214,13 +1259,14 @@ int hb_run_pass(const HbPass& ps, int n, int64_t rows, cplx<float>* X, const cpl
       QPINN_HB_SM(10)
       QPINN_HB_SM(11)
       QPINN_HB_SM(12)
+      QPINN_HB_SM(13)
 #undef QPINN_HB_SM
       default: return fail(QPINN_ERR_CAPACITY, "multi-gate HBM pass: 9 <= n <= 16");
     }
     QPINN_CUDA_CHECK(cudaGetLastError());
   } else {
-    nctas = hb_cs_grid(rows);
-    if (int rc = hb_launch_cs(h, n, rows, X, XC, ops, ps.nops, U, ph, part, ps.n_outer, st))
+    nctas = hb_cs_grid(rows, tb);
+    if (int rc = hb_launch_cs(h, tb, n, rows, X, XC, ops, ps.nops, U, ph, part, ps.n_outer, st))
       return rc;
   }
   if (ps.n_outer) {
@@ -1274,7 +1320,7 @@ int hbm_forward(const qpinn_circuit* c, const KArgs<float>* a, unsigned char* ws
   const PlanDev& p = c->dev;
   const int n = c->n;
   const int64_t D = (int64_t)1 << n;
-  const HbPlan plan = hb_plan(c);
+  const HbPlan plan = hb_plan(c, hb_fwd_tbits(n));
   const int nops = (int)plan.ops.size();
   if (getenv("QPINN_VERBOSE")) {
     fprintf(stderr, "[qpinn] multi-gate HBM forward: n = %d, L = %d, %d ops in %d passes:", n,
@@ -1304,6 +1350,10 @@ int hbm_forward(const qpinn_circuit* c, const KArgs<float>* a, unsigned char* ws
   const int ns = a->tan ? 4 : 1;
   const int chunks = hb_chunks(n);
   const int ro_smem = 4 * n * 4 * (int)sizeof(double);  // [4 warps][4 n]
+  if (plan.T == kHbTmax)  // one 2^13-amplitude tile: 64 KB of dynamic shared memory
+    QPINN_CUDA_CHECK(cudaFuncSetAttribute(hb_sm_pass<kHbTmax>,
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (1 << kHbTmax) * (int)sizeof(cplx<float>)));
   QPINN_CUDA_CHECK(cudaFuncSetAttribute(gb_readout<float>,
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, ro_smem));
   gb_tables<float><<<64, 256, 0, st>>>(p, a->qp, U, ph);
@@ -1316,7 +1366,8 @@ int hbm_forward(const qpinn_circuit* c, const KArgs<float>* a, unsigned char* ws
                                                               a->tan, PT);
     gb_embed<float><<<gb_blocks(Bc * D), kGbThreads, 0, st>>>(n, Bc, ns, PT, X);
     for (const HbPass& ps : plan.passes)
-      if (int rc = hb_run_pass(ps, n, rows, X, nullptr, dops, dluts, U, ph, nullptr, nullptr, st))
+      if (int rc = hb_run_pass(ps, n, plan.T, rows, X, nullptr, dops, dluts, U, ph, nullptr,
+                               nullptr, st))
         return rc;
     gb_readout<float><<<dim3(chunks, Bc), 128, ro_smem, st>>>(n, chunks, ns, X, RP);
     gb_readout_final<float><<<gb_blocks(Bc * n), kGbThreads, 0, st>>>(n, Bc, chunks, ns, p0,
@@ -1327,7 +1378,9 @@ int hbm_forward(const qpinn_circuit* c, const KArgs<float>* a, unsigned char* ws
 }
 
 // number of HBM passes per forward of the multi-gate path (diagnostics)
-int hbm_forward_passes(const qpinn_circuit* c) { return (int)hb_plan(c).passes.size(); }
+int hbm_forward_passes(const qpinn_circuit* c) {
+  return (int)hb_plan(c, hb_fwd_tbits(c->n)).passes.size();
+}
 
 namespace {
 
@@ -1422,7 +1475,8 @@ int hbm_backward(const qpinn_circuit* c, const KArgs<float>* a, unsigned char* w
                                                               a->tan, PT);
     gb_embed<float><<<gb_blocks(Bc * D), kGbThreads, 0, st>>>(n, Bc, 4, PT, X);
     for (const HbPass& ps : bp.fwd.passes) {  // forward, checkpointing every layer boundary
-      if (int rc = hb_run_pass(ps, n, rows, X, nullptr, dops, dluts, U, ph, nullptr, nullptr, st))
+      if (int rc = hb_run_pass(ps, n, bp.fwd.T, rows, X, nullptr, dops, dluts, U, ph, nullptr,
+                               nullptr, st))
         return rc;
       if (ps.ck >= 0)
         QPINN_CUDA_CHECK(cudaMemcpyAsync(CK + ps.ck * ckl, X, ckl * sizeof(cplx<float>),
@@ -1442,7 +1496,8 @@ int hbm_backward(const qpinn_circuit* c, const KArgs<float>* a, unsigned char* w
                                                               acc + 8 * p.n_u1 + (size_t)l * D);
       }
       const cplx<float>* xc = ps.layer >= 0 ? CK + ps.layer * ckl : nullptr;
-      if (int rc = hb_run_pass(ps, n, rows, A, xc, dops, dluts, U, ph, part, acc, st)) return rc;
+      if (int rc = hb_run_pass(ps, n, bp.rev.T, rows, A, xc, dops, dluts, U, ph, part, acc, st))
+        return rc;
     }
     gb_embed<float><<<gb_blocks(Bc * D), kGbThreads, 0, st>>>(n, Bc, 1, PT, X);
     gb_embed_grad<float><<<dim3(chunks, Bc), 128, eg_smem, st>>>(n, chunks, PT, X, A, EG);
@@ -1478,7 +1533,7 @@ size_t global_adjoint_workspace_bytes(const qpinn_circuit* c, int dtype, int64_t
     int64_t B = ((int64_t)256 << 20) / (4 * ((int64_t)8 << c->n));
     B = std::min<int64_t>(B, hb_fwd_bcap(c->n));
     if (rows >= 0) B = std::min<int64_t>(B, rows);
-    const HbPlan plan = hb_plan(c);
+    const HbPlan plan = hb_plan(c, hb_fwd_tbits(c->n));
     h = hb_layout(c, B < 1 ? 1 : B, (int)plan.ops.size(), (int)plan.luts.size()).total;
   }
   if (hbm_bwd_supported(c, dtype)) h = std::max(h, hbm_bwd_workspace_bytes(c, rows));
