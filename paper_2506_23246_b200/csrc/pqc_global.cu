@@ -744,11 +744,26 @@ struct HbBwdPlan {
   HbPlan fwd, rev;
 };
 
+// the adjoint's tile bits: at n = 13 the whole state per tile too (state + checkpoint
+// tiles: 128 KB, one CTA per SM): strongly L = 4 71.7 -> 59.6 ms, cross_mesh 70.6 ->
+// 65.7 ms at 8192 points (profiles/r02/hb_forward_tile_bits.txt).  QPINN_HB_BWD_T
+// overrides (9..13; 13-bit adjoint tiles only where they hold the whole state)
+int hb_bwd_tbits(int n) {
+  static const int env = [] {
+    const char* e = getenv("QPINN_HB_BWD_T");
+    return e ? atoi(e) : 0;
+  }();
+  const int def = n == kHbTmax ? kHbTmax : kHbT;
+  const int t = env >= 9 && env <= kHbTmax && (env <= kHbT || n <= kHbTmax) ? env : def;
+  return n < t ? n : t;
+}
+
 HbBwdPlan hb_plan_bwd(const qpinn_circuit* c) {
-  const std::vector<HbLayerOps> layers = hb_layers(c, hb_tbits(c->n));
+  const int T = hb_bwd_tbits(c->n);
+  const std::vector<HbLayerOps> layers = hb_layers(c, T);
   const int L = (int)layers.size();
   HbBwdPlan bp;
-  bp.fwd.T = bp.rev.T = hb_tbits(c->n);
+  bp.fwd.T = bp.rev.T = T;
   for (int l = 0; l <= L; ++l) {  // segment l: entangler(l-1), u1(l); checkpoint l after it
     std::vector<HbSOp> seq;
     if (l > 0) seq.insert(seq.end(), layers[l - 1].ent.begin(), layers[l - 1].ent.end());
@@ -1400,7 +1415,8 @@ HbBwdLayout hb_bwd_layout(const qpinn_circuit* c, int64_t B, int nops, int nluts
     return at;
   };
   const int64_t rows = 4 * B;
-  const int64_t max_ctas = std::max<int64_t>(rows << (c->n - hb_tbits(c->n)), (int64_t)num_sms() * 8);
+  const int64_t max_ctas =
+      std::max<int64_t>(rows << (c->n - hb_bwd_tbits(c->n)), (int64_t)num_sms() * 8);
   g.acc = take(8 * (8 * (size_t)c->n_u1 + D * c->n_phase));
   g.U = take(es * 4 * c->n_u1);
   g.ph = take(es * D * c->n_phase);
@@ -1466,6 +1482,10 @@ int hbm_backward(const qpinn_circuit* c, const KArgs<float>* a, unsigned char* w
   QPINN_CUDA_CHECK(cudaFuncSetAttribute(hb_sm_pass<kHbT>,
                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         2 * (1 << kHbT) * (int)sizeof(cplx<float>)));
+  if (bp.rev.T == kHbTmax)  // state + checkpoint tiles of 2^13 amplitudes: 128 KB
+    QPINN_CUDA_CHECK(cudaFuncSetAttribute(hb_sm_pass<kHbTmax>,
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          2 * (1 << kHbTmax) * (int)sizeof(cplx<float>)));
   gb_tables<float><<<64, 256, 0, st>>>(p, a->qp, U, ph);
   for (int64_t p0 = 0; p0 < a->R; p0 += g.B) {
     const int Bc = (int)(a->R - p0 < g.B ? a->R - p0 : g.B);
