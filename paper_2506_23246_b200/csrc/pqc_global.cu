@@ -536,10 +536,10 @@ struct HbPass {
 struct HbPlan {
   std::vector<HbOp> ops;
   std::vector<HbPass> passes;
-  std::vector<int> luts;  // per CNOT run of an SM pass: [64 low | 128 high | 16 slice] index maps
+  std::vector<int> luts;  // per CNOT run of an SM pass: [64 low | 256 high | 16 slice] index maps
   int T = kHbT;           // low (tile) bits of this plan's SM passes
 };
-constexpr int kHbLut = 64 + 128 + 16;
+constexpr int kHbLut = 64 + 256 + 16;
 
 struct HbSOp {  // an op being scheduled
   HbOp op;
@@ -658,9 +658,9 @@ void hb_tabulate(HbPlan& plan) {
       plan.luts.resize(off + kHbLut, 0);
       int* lo = plan.luts.data() + off;
       int* hi = lo + 64;
-      int* sl = hi + 128;
+      int* sl = hi + 256;
       for (int v = 0; v < 64; ++v) lo[v] = f(v, 0);
-      for (int v = 0; v < 128; ++v) hi[v] = f(v << 6, 0);
+      for (int v = 0; v < 256; ++v) hi[v] = f(v << 6, 0);
       for (int v = 0; v < 16; ++v) sl[v] = f(0, v);
       plan.ops[o].idx = off;
       plan.ops[o].b = (plan.ops[o].b & 0xff) | ((e - o) << 8);
@@ -712,17 +712,23 @@ std::vector<HbLayerOps> hb_layers(const qpinn_circuit* c, int T) {
 }
 
 // forward (no checkpoints): the whole circuit as one schedule
-// the forward's tile bits: at n = 13 one 2^13-amplitude tile holds the whole state, so
-// every op runs in SM passes (strongly L = 4: 18.3 -> 12.5 ms, cross_mesh 15.2 -> 12.5 ms
-// at 8192 points); from n = 14 the 12-bit tiles are as fast or faster (n = 16 strongly:
-// 18.4 vs 19.1 ms at L = 4; profiles/r02/hb_forward_tile_bits.txt).  QPINN_HB_FWD_T
-// overrides the tile bits (9..13).
-int hb_fwd_tbits(int n) {
+// the forward's tile bits (profiles/r02/hb_forward_tile_bits.txt): at n = 13 one
+// 2^13-amplitude tile (64 KB, 3 CTAs/SM) holds the whole state, so every op runs in SM
+// passes (strongly L = 4: 18.3 -> 12.5 ms, cross_mesh 15.2 -> 12.5 ms at 8192 points);
+// at n = 14 a whole-state 2^14 tile (128 KB, one CTA/SM) pays for CNOT entanglers
+// (strongly L = 8: 34.7 -> 28.3 ms, CNOT mesh 33.8 -> 20.9 ms at 4096 points) but not for
+// the phase / no entangler (13-bit tiles, within 5 %); from n = 15 the 12-bit tiles (with
+// CS passes at 4 CTAs/SM) are as fast or faster.  QPINN_HB_FWD_T overrides (9..14).
+int hb_fwd_tbits(const qpinn_circuit* c) {
   static const int env = [] {
     const char* e = getenv("QPINN_HB_FWD_T");
     return e ? atoi(e) : 0;
   }();
-  const int t = env >= 9 && env <= kHbTmax ? env : (n == kHbTmax ? kHbTmax : kHbT);
+  const int n = c->n;
+  int def = kHbT;
+  if (n == 13) def = 13;
+  if (n == 14) def = layer_entangler(c) == ENT_PERM ? 14 : 13;
+  const int t = env >= 9 && env <= 14 ? env : def;
   return n < t ? n : t;
 }
 
@@ -901,7 +907,7 @@ __device__ __forceinline__ void hb_sm_u1_group(cplx<float>* t, const HbOp* op,
 #define QPINN_HB_G 2
 #endif
 template <int T>
-__global__ void __launch_bounds__(256, T >= 13 ? 3 : QPINN_HB_MINB)
+__global__ void __launch_bounds__(256, T >= 14 ? 1 : T >= 13 ? 3 : QPINN_HB_MINB)
 hb_sm_pass(int n, cplx<float>* __restrict__ X, const cplx<float>* __restrict__ XC,
            const HbOp* __restrict__ ops, int nops, const int* __restrict__ luts,
            const cplx<float>* __restrict__ U, const cplx<float>* __restrict__ ph,
@@ -957,7 +963,7 @@ hb_sm_pass(int n, cplx<float>* __restrict__ X, const cplx<float>* __restrict__ X
     } else if (op.type == HB_CNOT) {
       // a run of CNOTs: new[i] = old[f(i, s)] through the run's tabulated index map
       const int* lut = luts + op.idx;
-      const int fs = lut[192 + s];  // [64 low | 128 high | 16 slice]
+      const int fs = lut[320 + s];  // [64 low | 256 high | 16 slice]
       cplx<float> v[PER];
 #pragma unroll
       for (int r = 0; r < PER; ++r) {
@@ -1246,6 +1252,12 @@ int hb_launch_cs(int h, int T, int n, int64_t rows, cplx<float>* X, const cplx<f
       case 3: hb_cs_pass<3, false, kHbTmax><<<grid, 256, 0, st>>>(n, rows, X, XC, ops, nops, U, ph, part, 0); break;
       default: return fail(QPINN_ERR_CAPACITY, "multi-gate HBM pass: 14 <= n <= 16 at 13-bit tiles");
     }
+  } else if (T == 14 && !XC) {  // 2^14-amplitude forward tiles
+    switch (h) {
+      case 1: hb_cs_pass<1, false, 14><<<grid, 256, 0, st>>>(n, rows, X, XC, ops, nops, U, ph, part, 0); break;
+      case 2: hb_cs_pass<2, false, 14><<<grid, 256, 0, st>>>(n, rows, X, XC, ops, nops, U, ph, part, 0); break;
+      default: return fail(QPINN_ERR_CAPACITY, "multi-gate HBM pass: 15 <= n <= 16 at 14-bit tiles");
+    }
   } else {
     return fail(QPINN_ERR_CAPACITY, "multi-gate HBM pass: tile bits");
   }
@@ -1275,6 +1287,7 @@ int hb_run_pass(const HbPass& ps, int n, int tb, int64_t rows, cplx<float>* X,
       QPINN_HB_SM(11)
       QPINN_HB_SM(12)
       QPINN_HB_SM(13)
+      QPINN_HB_SM(14)
 #undef QPINN_HB_SM
       default: return fail(QPINN_ERR_CAPACITY, "multi-gate HBM pass: 9 <= n <= 16");
     }
@@ -1335,7 +1348,7 @@ int hbm_forward(const qpinn_circuit* c, const KArgs<float>* a, unsigned char* ws
   const PlanDev& p = c->dev;
   const int n = c->n;
   const int64_t D = (int64_t)1 << n;
-  const HbPlan plan = hb_plan(c, hb_fwd_tbits(n));
+  const HbPlan plan = hb_plan(c, hb_fwd_tbits(c));
   const int nops = (int)plan.ops.size();
   if (getenv("QPINN_VERBOSE")) {
     fprintf(stderr, "[qpinn] multi-gate HBM forward: n = %d, L = %d, %d ops in %d passes:", n,
@@ -1369,6 +1382,10 @@ int hbm_forward(const qpinn_circuit* c, const KArgs<float>* a, unsigned char* ws
     QPINN_CUDA_CHECK(cudaFuncSetAttribute(hb_sm_pass<kHbTmax>,
                                           cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           (1 << kHbTmax) * (int)sizeof(cplx<float>)));
+  if (plan.T == 14)  // one 2^14-amplitude tile: 128 KB (experiment, QPINN_HB_FWD_T=14)
+    QPINN_CUDA_CHECK(cudaFuncSetAttribute(hb_sm_pass<14>,
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (1 << 14) * (int)sizeof(cplx<float>)));
   QPINN_CUDA_CHECK(cudaFuncSetAttribute(gb_readout<float>,
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, ro_smem));
   gb_tables<float><<<64, 256, 0, st>>>(p, a->qp, U, ph);
@@ -1394,7 +1411,7 @@ int hbm_forward(const qpinn_circuit* c, const KArgs<float>* a, unsigned char* ws
 
 // number of HBM passes per forward of the multi-gate path (diagnostics)
 int hbm_forward_passes(const qpinn_circuit* c) {
-  return (int)hb_plan(c, hb_fwd_tbits(c->n)).passes.size();
+  return (int)hb_plan(c, hb_fwd_tbits(c)).passes.size();
 }
 
 namespace {
@@ -1553,7 +1570,7 @@ size_t global_adjoint_workspace_bytes(const qpinn_circuit* c, int dtype, int64_t
     int64_t B = ((int64_t)256 << 20) / (4 * ((int64_t)8 << c->n));
     B = std::min<int64_t>(B, hb_fwd_bcap(c->n));
     if (rows >= 0) B = std::min<int64_t>(B, rows);
-    const HbPlan plan = hb_plan(c, hb_fwd_tbits(c->n));
+    const HbPlan plan = hb_plan(c, hb_fwd_tbits(c));
     h = hb_layout(c, B < 1 ? 1 : B, (int)plan.ops.size(), (int)plan.luts.size()).total;
   }
   if (hbm_bwd_supported(c, dtype)) h = std::max(h, hbm_bwd_workspace_bytes(c, rows));
