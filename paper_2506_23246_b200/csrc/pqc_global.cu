@@ -765,15 +765,18 @@ int hb_bwd_tbits(int n) {
 }
 
 HbBwdPlan hb_plan_bwd(const qpinn_circuit* c) {
-  const int T = hb_bwd_tbits(c->n);
+  // the forward segments carry no checkpoint tile: they take the forward's tile bits
+  const int Tf = hb_fwd_tbits(c), T = hb_bwd_tbits(c->n);
+  const std::vector<HbLayerOps> flayers = hb_layers(c, Tf);
   const std::vector<HbLayerOps> layers = hb_layers(c, T);
   const int L = (int)layers.size();
   HbBwdPlan bp;
-  bp.fwd.T = bp.rev.T = T;
+  bp.fwd.T = Tf;
+  bp.rev.T = T;
   for (int l = 0; l <= L; ++l) {  // segment l: entangler(l-1), u1(l); checkpoint l after it
     std::vector<HbSOp> seq;
-    if (l > 0) seq.insert(seq.end(), layers[l - 1].ent.begin(), layers[l - 1].ent.end());
-    if (l < L) seq.insert(seq.end(), layers[l].u1.begin(), layers[l].u1.end());
+    if (l > 0) seq.insert(seq.end(), flayers[l - 1].ent.begin(), flayers[l - 1].ent.end());
+    if (l < L) seq.insert(seq.end(), flayers[l].u1.begin(), flayers[l].u1.end());
     if (seq.empty()) continue;
     hb_schedule(seq, bp.fwd);
     if (l < L) bp.fwd.passes.back().ck = l;
@@ -1343,6 +1346,19 @@ int hb_chunks(int n) { return n <= 10 ? 1 : std::min(kGbChunks, 1 << (n - 10)); 
 int64_t hb_fwd_bcap(int n) { return std::max<int64_t>(1024, (int64_t)1 << (22 - n)); }
 }  // namespace
 
+// dynamic shared memory limits of the SM-pass instances (state tile, plus the
+// checkpoint tile where it is used: 12- and 13-bit adjoint tiles)
+int hb_set_smem_limits() {
+  const int es = (int)sizeof(cplx<float>);
+  QPINN_CUDA_CHECK(cudaFuncSetAttribute(hb_sm_pass<12>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * es << 12));
+  QPINN_CUDA_CHECK(cudaFuncSetAttribute(hb_sm_pass<13>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * es << 13));
+  QPINN_CUDA_CHECK(cudaFuncSetAttribute(hb_sm_pass<14>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, es << 14));
+  return QPINN_OK;
+}
+
 // forward with tangents (or value only), several gates per HBM pass (see hb_plan)
 int hbm_forward(const qpinn_circuit* c, const KArgs<float>* a, unsigned char* ws, size_t bytes) {
   const PlanDev& p = c->dev;
@@ -1378,14 +1394,7 @@ int hbm_forward(const qpinn_circuit* c, const KArgs<float>* a, unsigned char* ws
   const int ns = a->tan ? 4 : 1;
   const int chunks = hb_chunks(n);
   const int ro_smem = 4 * n * 4 * (int)sizeof(double);  // [4 warps][4 n]
-  if (plan.T == kHbTmax)  // one 2^13-amplitude tile: 64 KB of dynamic shared memory
-    QPINN_CUDA_CHECK(cudaFuncSetAttribute(hb_sm_pass<kHbTmax>,
-                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          (1 << kHbTmax) * (int)sizeof(cplx<float>)));
-  if (plan.T == 14)  // one 2^14-amplitude tile: 128 KB (experiment, QPINN_HB_FWD_T=14)
-    QPINN_CUDA_CHECK(cudaFuncSetAttribute(hb_sm_pass<14>,
-                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          (1 << 14) * (int)sizeof(cplx<float>)));
+  if (int rc = hb_set_smem_limits()) return rc;
   QPINN_CUDA_CHECK(cudaFuncSetAttribute(gb_readout<float>,
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, ro_smem));
   gb_tables<float><<<64, 256, 0, st>>>(p, a->qp, U, ph);
@@ -1496,13 +1505,7 @@ int hbm_backward(const qpinn_circuit* c, const KArgs<float>* a, unsigned char* w
   const int chunks = hb_chunks(n);
   QPINN_CUDA_CHECK(cudaFuncSetAttribute(gb_embed_grad<float>,
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, eg_smem));
-  QPINN_CUDA_CHECK(cudaFuncSetAttribute(hb_sm_pass<kHbT>,
-                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        2 * (1 << kHbT) * (int)sizeof(cplx<float>)));
-  if (bp.rev.T == kHbTmax)  // state + checkpoint tiles of 2^13 amplitudes: 128 KB
-    QPINN_CUDA_CHECK(cudaFuncSetAttribute(hb_sm_pass<kHbTmax>,
-                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          2 * (1 << kHbTmax) * (int)sizeof(cplx<float>)));
+  if (int rc = hb_set_smem_limits()) return rc;
   gb_tables<float><<<64, 256, 0, st>>>(p, a->qp, U, ph);
   for (int64_t p0 = 0; p0 < a->R; p0 += g.B) {
     const int Bc = (int)(a->R - p0 < g.B ? a->R - p0 : g.B);
