@@ -516,6 +516,10 @@ constexpr int kHbT = 12;  // low bits per SM tile: 2^12 complex = 32 KB of share
 // the forward (no checkpoint tile) may use 2^13-amplitude tiles (64 KB): at n = 13 the
 // whole circuit runs in SM passes, and from n = 14 one wire fewer goes to CS passes
 constexpr int kHbTmax = 13;
+#ifndef QPINN_HB_OUTER2
+#define QPINN_HB_OUTER2 1
+#endif
+constexpr bool kHbOuter2 = QPINN_HB_OUTER2;  // OUTER ops two per sweep in SM passes
 // the SM tile of an n-qubit state: the whole state (h = 0, SM passes only) for n <= 12
 inline int hb_tbits(int n) { return n < kHbT ? n : kHbT; }
 enum { HB_U1 = 0, HB_CNOT = 1, HB_PHASE = 2, HB_OUTER = 3 };
@@ -978,18 +982,55 @@ hb_sm_pass(int n, cplx<float>* __restrict__ X, const cplx<float>* __restrict__ X
       for (int r = 0; r < PER; ++r) t[threadIdx.x + r * 256] = v[r];
       o += op.b >> 8;
     } else if (op.type == HB_OUTER) {  // M' = sum over pairs on bit a of conj(abar) x
+      // two OUTER ops on distinct bits share one sweep over both tiles (QPINN_HB_OUTER2)
+      const bool two = kHbOuter2 && o + 1 < nops && ops[o + 1].type == HB_OUTER &&
+                       ops[o + 1].a != op.a;
       float m[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-      for (int k = threadIdx.x; k < TS / 2; k += blockDim.x) {
-        const int i0 = hb_insert0(k, op.a), i1 = i0 | (1 << op.a);
-        const cplx<float> a0 = t[i0], a1 = t[i1], x0 = tx[i0], x1 = tx[i1];
-        cmac_c(m[0], m[1], a0, x0);
-        cmac_c(m[2], m[3], a0, x1);
-        cmac_c(m[4], m[5], a1, x0);
-        cmac_c(m[6], m[7], a1, x1);
+      float m2[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+      if (two) {
+        const int b0 = op.a, b1 = ops[o + 1].a;
+        const int lo = b0 < b1 ? b0 : b1, hi = b0 < b1 ? b1 : b0;
+        for (int k = threadIdx.x; k < TS / 4; k += blockDim.x) {
+          const int i00 = hb_insert0(hb_insert0(k, lo), hi);
+          const int i10 = i00 | (1 << b0), i01 = i00 | (1 << b1), i11 = i10 | (1 << b1);
+          const cplx<float> a00 = t[i00], a10 = t[i10], a01 = t[i01], a11 = t[i11];
+          const cplx<float> x00 = tx[i00], x10 = tx[i10], x01 = tx[i01], x11 = tx[i11];
+          // bit b0: pairs (00, 10) and (01, 11)
+          cmac_c(m[0], m[1], a00, x00);
+          cmac_c(m[2], m[3], a00, x10);
+          cmac_c(m[4], m[5], a10, x00);
+          cmac_c(m[6], m[7], a10, x10);
+          cmac_c(m[0], m[1], a01, x01);
+          cmac_c(m[2], m[3], a01, x11);
+          cmac_c(m[4], m[5], a11, x01);
+          cmac_c(m[6], m[7], a11, x11);
+          // bit b1: pairs (00, 01) and (10, 11)
+          cmac_c(m2[0], m2[1], a00, x00);
+          cmac_c(m2[2], m2[3], a00, x01);
+          cmac_c(m2[4], m2[5], a01, x00);
+          cmac_c(m2[6], m2[7], a01, x01);
+          cmac_c(m2[0], m2[1], a10, x10);
+          cmac_c(m2[2], m2[3], a10, x11);
+          cmac_c(m2[4], m2[5], a11, x10);
+          cmac_c(m2[6], m2[7], a11, x11);
+        }
+      } else {
+        for (int k = threadIdx.x; k < TS / 2; k += blockDim.x) {
+          const int i0 = hb_insert0(k, op.a), i1 = i0 | (1 << op.a);
+          const cplx<float> a0 = t[i0], a1 = t[i1], x0 = tx[i0], x1 = tx[i1];
+          cmac_c(m[0], m[1], a0, x0);
+          cmac_c(m[2], m[3], a0, x1);
+          cmac_c(m[4], m[5], a1, x0);
+          cmac_c(m[6], m[7], a1, x1);
+        }
       }
       hb_outer_commit(m, red, part + ((int64_t)slot * gridDim.x + blockIdx.x) * 8);
       ++slot;
-      ++o;
+      if (two) {
+        hb_outer_commit(m2, red, part + ((int64_t)slot * gridDim.x + blockIdx.x) * 8);
+        ++slot;
+      }
+      o += two ? 2 : 1;
     } else {
       const cplx<float>* ep = ph + (int64_t)op.idx * D + ((int64_t)s << T);
 #pragma unroll
