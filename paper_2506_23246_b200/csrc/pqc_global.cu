@@ -84,32 +84,36 @@ __global__ void gb_point(int n, int scale, int64_t R, int64_t p0, int B,
   }
 }
 
-// embedded state and its tangents (ansatz.py:233-243, :380-390); wire q is bit n-1-q
+// embedded state and its tangents (ansatz.py:233-243, :380-390); wire q is bit n-1-q.
+// 4 consecutive amplitudes per thread (b0 .. b0 + 3: only the last two wires differ):
+// the first n - 2 factors and their tangent terms are shared (n >= 2)
 template <typename T>
-__global__ void gb_embed(int n, int B, int nstates, const T* __restrict__ PT,
-                         cplx<T>* __restrict__ X) {
-  const int64_t D = (int64_t)1 << n;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < B * D;
+__global__ void gb_embed4(int n, int B, int nstates, const T* __restrict__ PT,
+                          cplx<T>* __restrict__ X) {
+  const int64_t D = (int64_t)1 << n, Q = D / 4;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < B * Q;
        i += (int64_t)gridDim.x * blockDim.x) {
-    const int pb = (int)(i / D);
-    const int64_t b = i % D;
+    const int pb = (int)(i / Q);
+    const int64_t b0 = (i % Q) * 4;
     const T* pt = PT + (int64_t)pb * n * 8;
-    T pre[17];  // prefix products, statically indexed (registers, no local memory)
+    const int H = n - 2;
+    T pre[15];  // prefix products over the shared wires (statically indexed)
     pre[0] = T(1);
 #pragma unroll
-    for (int q = 0; q < 16; ++q) {
-      if (q < n) {
-        const int bit = (b >> (n - 1 - q)) & 1;
+    for (int q = 0; q < 14; ++q) {
+      if (q < H) {
+        const int bit = (b0 >> (n - 1 - q)) & 1;
         pre[q + 1] = pre[q] * (bit ? pt[q * 8 + 1] : pt[q * 8]);
       } else {
         pre[q + 1] = pre[q];
       }
     }
+    const T P = pre[14];
     T tk[3] = {T(0), T(0), T(0)}, suf = T(1);
 #pragma unroll
-    for (int q = 15; q >= 0; --q) {
-      if (q < n) {
-        const int bit = (b >> (n - 1 - q)) & 1;
+    for (int q = 13; q >= 0; --q) {
+      if (q < H) {
+        const int bit = (b0 >> (n - 1 - q)) & 1;
         const T df = bit ? T(0.5) * pt[q * 8] : T(-0.5) * pt[q * 8 + 1];
         const T rest = pre[q] * suf;
 #pragma unroll
@@ -117,14 +121,34 @@ __global__ void gb_embed(int n, int B, int nstates, const T* __restrict__ PT,
         suf *= bit ? pt[q * 8 + 1] : pt[q * 8];
       }
     }
-    const int ph = __popcll(b) & 3;  // (-i)^popcount
-    auto put = [&](int s, T m) {
-      X[((int64_t)pb * 4 + s) * D + b] = {ph == 0 ? m : ph == 2 ? -m : T(0),
-                                           ph == 1 ? -m : ph == 3 ? m : T(0)};
-    };
-    put(0, pre[16]);  // = the product over the n wires (pre is constant past n)
-    if (nstates == 4)
-      for (int k = 0; k < 3; ++k) put(k + 1, tk[k]);
+    // the last two wires a = H (bit 1 of b - b0), c = H + 1 (bit 0)
+    const T* pa = pt + H * 8;
+    const T* pc = pa + 8;
+    const T fa[2] = {pa[0], pa[1]}, fc[2] = {pc[0], pc[1]};
+    const T da[2] = {T(-0.5) * pa[1], T(0.5) * pa[0]}, dc[2] = {T(-0.5) * pc[1], T(0.5) * pc[0]};
+    T m[4][4];  // [state][amplitude]
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int ia = e >> 1, ic = e & 1;
+      m[0][e] = P * fa[ia] * fc[ic];
+#pragma unroll
+      for (int k = 0; k < 3; ++k)
+        m[k + 1][e] = tk[k] * fa[ia] * fc[ic] + pa[4 + k] * da[ia] * P * fc[ic] +
+                      pc[4 + k] * dc[ic] * P * fa[ia];
+    }
+    const int pop = __popcll(b0);
+    for (int s = 0; s < nstates; ++s) {
+      cplx<T> o[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int ph = (pop + __popc(e)) & 3;  // (-i)^popcount(b0 + e)
+        const T v = m[s][e];
+        o[e] = {ph == 0 ? v : ph == 2 ? -v : T(0), ph == 1 ? -v : ph == 3 ? v : T(0)};
+      }
+      cplx<T>* dst = X + ((int64_t)pb * 4 + s) * D + b0;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) dst[e] = o[e];
+    }
   }
 }
 
@@ -520,8 +544,6 @@ constexpr int kHbTmax = 13;
 #define QPINN_HB_OUTER2 1
 #endif
 constexpr bool kHbOuter2 = QPINN_HB_OUTER2;  // OUTER ops two per sweep in SM passes
-// the SM tile of an n-qubit state: the whole state (h = 0, SM passes only) for n <= 12
-inline int hb_tbits(int n) { return n < kHbT ? n : kHbT; }
 enum { HB_U1 = 0, HB_CNOT = 1, HB_PHASE = 2, HB_OUTER = 3 };
 enum { HB_SM = 0, HB_CS = 1, HB_ANY = 2 };
 struct HbOp {
@@ -1446,7 +1468,7 @@ int hbm_forward(const qpinn_circuit* c, const KArgs<float>* a, unsigned char* ws
     const int64_t rows = (int64_t)Bc * 4;
     gb_point<float><<<gb_blocks(Bc * n), kGbThreads, 0, st>>>(n, a->scale, a->R, p0, Bc, a->act,
                                                               a->tan, PT);
-    gb_embed<float><<<gb_blocks(Bc * D), kGbThreads, 0, st>>>(n, Bc, ns, PT, X);
+    gb_embed4<float><<<gb_blocks(Bc * D / 4), kGbThreads, 0, st>>>(n, Bc, ns, PT, X);
     for (const HbPass& ps : plan.passes)
       if (int rc = hb_run_pass(ps, n, plan.T, rows, X, nullptr, dops, dluts, U, ph, nullptr,
                                nullptr, st))
@@ -1554,7 +1576,7 @@ int hbm_backward(const qpinn_circuit* c, const KArgs<float>* a, unsigned char* w
     const size_t ckl = (size_t)rows * D;  // one layer's checkpoint
     gb_point<float><<<gb_blocks(Bc * n), kGbThreads, 0, st>>>(n, a->scale, a->R, p0, Bc, a->act,
                                                               a->tan, PT);
-    gb_embed<float><<<gb_blocks(Bc * D), kGbThreads, 0, st>>>(n, Bc, 4, PT, X);
+    gb_embed4<float><<<gb_blocks(Bc * D / 4), kGbThreads, 0, st>>>(n, Bc, 4, PT, X);
     for (const HbPass& ps : bp.fwd.passes) {  // forward, checkpointing every layer boundary
       if (int rc = hb_run_pass(ps, n, bp.fwd.T, rows, X, nullptr, dops, dluts, U, ph, nullptr,
                                nullptr, st))
@@ -1580,7 +1602,7 @@ int hbm_backward(const qpinn_circuit* c, const KArgs<float>* a, unsigned char* w
       if (int rc = hb_run_pass(ps, n, bp.rev.T, rows, A, xc, dops, dluts, U, ph, part, acc, st))
         return rc;
     }
-    gb_embed<float><<<gb_blocks(Bc * D), kGbThreads, 0, st>>>(n, Bc, 1, PT, X);
+    gb_embed4<float><<<gb_blocks(Bc * D / 4), kGbThreads, 0, st>>>(n, Bc, 1, PT, X);
     gb_embed_grad<float><<<dim3(chunks, Bc), 128, eg_smem, st>>>(n, chunks, PT, X, A, EG);
     gb_embed_final<float><<<gb_blocks(Bc * n), kGbThreads, 0, st>>>(n, Bc, chunks, p0, a->R,
                                                                     EG, PT, a->tan, a->g_act,
@@ -1653,7 +1675,7 @@ int global_backward(const qpinn_circuit* c, const KArgs<T>* a, unsigned char* ws
   for (int64_t p0 = 0; p0 < a->R; p0 += B) {
     gb_point<T><<<gb_blocks(B * n), kGbThreads, 0, st>>>(n, a->scale, a->R, p0, B, a->act, a->tan,
                                                          PT);
-    gb_embed<T><<<gb_blocks(B * D), kGbThreads, 0, st>>>(n, B, 4, PT, X);
+    gb_embed4<T><<<gb_blocks(B * D / 4), kGbThreads, 0, st>>>(n, B, 4, PT, X);
     // forward with layer-boundary checkpoints
     for (int l = 0; l < L; ++l) {
       for (int q = 0; q < n; ++q)
@@ -1687,7 +1709,7 @@ int global_backward(const qpinn_circuit* c, const KArgs<T>* a, unsigned char* ws
         gb_u1<T><<<ob, kGbThreads, 0, st>>>(n, rows, A, q, U + 4 * (l * n + q), 1);
     }
     // embedding gradient against the re-embedded state
-    gb_embed<T><<<gb_blocks(B * D), kGbThreads, 0, st>>>(n, B, 1, PT, X);
+    gb_embed4<T><<<gb_blocks(B * D / 4), kGbThreads, 0, st>>>(n, B, 1, PT, X);
     gb_embed_grad<T><<<dim3(kGbChunks, B), 128, eg_smem, st>>>(
         n, kGbChunks, PT, X, A, EG);
     gb_embed_final<T><<<gb_blocks(B * n), kGbThreads, 0, st>>>(n, B, kGbChunks, p0, a->R, EG, PT,
@@ -1728,7 +1750,7 @@ int global_forward(const qpinn_circuit* c, const KArgs<T>* a, unsigned char* ws,
   for (int64_t p0 = 0; p0 < a->R; p0 += B) {
     gb_point<T><<<gb_blocks(B * n), kGbThreads, 0, st>>>(n, a->scale, a->R, p0, B, a->act,
                                                          a->tan, PT);
-    gb_embed<T><<<gb_blocks(B * D), kGbThreads, 0, st>>>(n, B, ns, PT, X);
+    gb_embed4<T><<<gb_blocks(B * D / 4), kGbThreads, 0, st>>>(n, B, ns, PT, X);
     for (int l = 0; l < L; ++l) {
       for (int q = 0; q < n; ++q)
         gb_u1<T><<<ob, kGbThreads, 0, st>>>(n, rows, X, q, U + 4 * (l * n + q), 0);
