@@ -402,6 +402,8 @@ __global__ void gb_readout(int n, int chunks, int nstates, const cplx<T>* __rest
   for (int j = 0; j < 4 * 16; ++j) acc[j] = T(0);
   const int64_t per = (D + chunks - 1) / chunks;
   const int64_t b0 = blockIdx.x * per, b1 = b0 + per < D ? b0 + per : D;
+  T plain[4] = {T(0), T(0), T(0), T(0)};
+  const int lowb = (int)((b0 + threadIdx.x) & 127);  // b's low 7 bits (blockDim = 128)
   for (int64_t b = b0 + threadIdx.x; b < b1; b += blockDim.x) {
     const cplx<T> psi = x[b];
     T v[4];
@@ -415,13 +417,25 @@ __global__ void gb_readout(int n, int chunks, int nstates, const cplx<T>* __rest
         v[k] = T(0);
       }
     }
+    // the wires on the 7 low bits of b are fixed per thread (b advances by 128): their
+    // sums are the thread's plain sums, signed once after the loop
+#pragma unroll
+    for (int k = 0; k < 4; ++k) plain[k] += v[k];
 #pragma unroll
     for (int q = 0; q < 16; ++q) {
-      if (q < n) {
+      if (q < n - 7) {
         const bool neg = (b >> (n - 1 - q)) & 1;
 #pragma unroll
         for (int k = 0; k < 4; ++k) acc[k * 16 + q] += neg ? -v[k] : v[k];
       }
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < 16; ++q) {
+    if (q >= n - 7 && q < n) {
+      const bool neg = (lowb >> (n - 1 - q)) & 1;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) acc[k * 16 + q] = neg ? -plain[k] : plain[k];
     }
   }
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
