@@ -14,6 +14,8 @@ col = {h: i for i, h in enumerate(hdr)}
 want = [("time_us", "gpu__time_duration.sum", 1),
         ("dram_rd_MB", "dram__bytes_read.sum", None), ("dram_wr_MB", "dram__bytes_write.sum", None),
         ("issue_%", "sm__inst_issued.avg.pct_of_peak_sustained_active", 1),
+        ("tc_pipe_%", "TPC.TriageCompute.sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed", 1),
+        ("tmem_%", "sm__mem_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed", 1),
         ("regs", "launch__registers_per_thread", 1), ("grid", "launch__grid_size", 1)]
 scale_mb = {"byte": 1e-6, "Kbyte": 1e-3, "Mbyte": 1.0, "Gbyte": 1e3}
 print(f"{'kernel':60s}" + "".join(f"{w[0]:>12s}" for w in want))
