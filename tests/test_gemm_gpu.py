@@ -50,3 +50,34 @@ def test_gemm_rejects_unaligned_rows():
     B = torch.randn(16, 10, device="cuda")
     with pytest.raises(Exception):
         _gemm(A, B)
+
+
+def _gemm_atb(X, G):
+    lib = N.lib()
+    rows, m = X.shape
+    n = G.shape[1]
+    C = torch.full((m, n), float("nan"), dtype=torch.float32, device="cuda")
+    ws = torch.empty(max(1, lib.qpinn_gemm_f32_atb_workspace_bytes(rows, m, n)), dtype=torch.uint8,
+                     device="cuda")
+    N.check(lib.qpinn_gemm_f32_atb(rows, m, n, X.data_ptr(), X.stride(0), G.data_ptr(), G.stride(0),
+                                   C.data_ptr(), ws.data_ptr(), ws.numel(), N.stream_ptr()),
+            "qpinn_gemm_f32_atb")
+    return C
+
+
+@pytest.mark.parametrize("rows,m,n", [(32, 128, 128), (1000, 128, 128), (4097, 256, 128),
+                                      (300, 7, 128), (262144, 256, 128), (70001, 128, 36),
+                                      (262144, 128, 7)])
+def test_gemm_f32_atb_matches_f64(rows, m, n):
+    """The weight-gradient kernel (X^T G, reduction over rows; A = X^T split into
+    TMEM, B = G split in shared memory) against float64, ragged rows and columns."""
+    g = torch.Generator(device="cuda").manual_seed(rows + 5 * m + n)
+    pad = lambda k: (k + 3) // 4 * 4  # noqa: E731  (row strides are multiples of 4)
+    X = torch.randn(rows, pad(m), device="cuda", generator=g)[:, :m]
+    G = (torch.randn(rows, pad(n), device="cuda", generator=g) / rows ** 0.5)[:, :n]
+    C = _gemm_atb(X, G)
+    ref = X.double().T @ G.double()
+    assert torch.isfinite(C).all()
+    err = (C.double() - ref).abs().max().item()
+    assert err <= 3e-6 * ref.abs().max().item(), err
+    assert torch.equal(C, _gemm_atb(X, G))  # fixed-order chunk sum
