@@ -1,9 +1,11 @@
 // tcgen05 / TMA building blocks for the trunk GEMMs (sm_100a).
 //
 // FP32-accurate GEMM on the TF32 tensor cores ("3xTF32"): every fp32 operand
-// x is split into x_hi = rna_tf32(x) and x_lo = rna_tf32(x - x_hi), and
-// A B ~= A_lo B_hi + A_hi B_lo + A_hi B_hi accumulates in fp32 in TMEM (the
-// dropped A_lo B_lo term is ~2^-22 relative).  Operand tiles arrive by TMA
+// x is split into x_hi = rna_tf32(x) and x_lo = x - x_hi (weights: x_lo =
+// rna_tf32(x - x_hi); activations are split on chip and hand x_lo to the MMA
+// unrounded, which truncates it to tf32), and A B ~= A_lo B_hi + A_hi B_lo +
+// A_hi B_hi accumulates in fp32 in TMEM (the dropped A_lo B_lo term is ~2^-22
+// relative).  Operand tiles arrive by TMA
 // with the 128-byte swizzle the UMMA shared-memory descriptors expect.
 #pragma once
 #include <cuda.h>
@@ -266,18 +268,38 @@ __device__ __forceinline__ void sts128(uint32_t addr, float4 v) {
                : "memory");
 }
 
-// x = hi + lo with hi, lo tf32 (round-to-nearest on the magnitude, ties away:
-// add half an ulp of the 10-bit mantissa and clear the 13 low bits; finite x)
-__device__ __forceinline__ void split_tf32(float x, float& hi, float& lo) {
-  hi = __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xFFFFE000u);
-  const float r = x - hi;
-  lo = __uint_as_float((__float_as_uint(r) + 0x1000u) & 0xFFFFE000u);
-}
-
 __device__ __forceinline__ float rna_tf32(float x) {
   uint32_t r;
   asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
   return __uint_as_float(r);
+}
+
+// on-chip split of an activation, x = hi + lo: hi is x rounded to tf32 (add half an
+// ulp of the 10-bit mantissa and clear the 13 low bits; finite x).  The split warps
+// issue this for every operand element, and they pace the GEMMs, so its ALU op count
+// shows in the step time (QPINN_SPLIT_MODE, measured on the bench step):
+//   0: lo rounded to tf32 as well, 5 ops: 1.718-1.720 ms;
+//   1: lo = x - hi unrounded, 3 ops: 1.690-1.703 ms, all GPU tests pass, GEMM errors
+//      within +-10 % of mode 0 (the MMA truncates lo to tf32; scripts/gemm_check.py);
+//   2: hi by cvt.rna.tf32 (slow conversion pipe), 2 instructions: 1.712-1.716 ms;
+//   3: hi = x (the MMA truncates it), lo = x - trunc(x), 2 ops: 1.674-1.684 ms, but
+//      |lo| up to 2^-10 |x| doubles its truncation error; one mid-size PQC dz entry
+//      fails its tolerance (tests/test_pqc_gpu.py::test_pqc_mid_sizes).
+#ifndef QPINN_SPLIT_MODE
+#define QPINN_SPLIT_MODE 1
+#endif
+__device__ __forceinline__ void split_tf32(float x, float& hi, float& lo) {
+  if constexpr (QPINN_SPLIT_MODE == 3) {
+    hi = x;
+    lo = x - __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
+  } else if constexpr (QPINN_SPLIT_MODE == 2) {
+    hi = rna_tf32(x);
+    lo = x - hi;
+  } else {
+    hi = __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xFFFFE000u);
+    const float r = x - hi;
+    lo = QPINN_SPLIT_MODE == 1 ? r : __uint_as_float((__float_as_uint(r) + 0x1000u) & 0xFFFFE000u);
+  }
 }
 
 }  // namespace tc
