@@ -373,6 +373,7 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUt
         if (warp == 0) GPROF(6, mbar_wait(raw_full + r, (uint32_t)((j / RS) & 1)));
         else mbar_wait(raw_full + r, (uint32_t)((j / RS) & 1));
         if constexpr (QPINN_ABL_NOSPLIT) {
+          fence_proxy_async_smem();  // generic reads of the raw stage before its TMA refill
           __syncwarp();
           if (lane == 0) mbar_arrive(raw_empty + r);
         } else {
@@ -388,6 +389,10 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUt
           split_tf32(v[c].z, hi[4 * c + 2], lo[4 * c + 2]);
           split_tf32(v[c].w, hi[4 * c + 3], lo[4 * c + 3]);
         }
+        // the raw stage is refilled by TMA (async proxy) once raw_empty completes: order
+        // this thread's generic-proxy reads of it before that write (without the fence
+        // one row in ~10^4 tiles read the next k-block's data: scripts/race_gemm.py)
+        fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) mbar_arrive(raw_empty + r);
         const uint32_t a = tmem + lane_base + Cfg::kACol + o * 2 * kBK;
@@ -571,13 +576,16 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUt
             if (n0 + c_off + c < g.N) dst[c] = acc[c];
         }
         if (g.ad_w) {  // fused adapter: u = y Wa per row (fp32 FMA, two column halves)
+          // weight rows by explicit shared-memory loads (broadcast); with generic
+          // pointers they compiled to generic LDs: 291 -> 273 us for the step's three
+          // EPI_TANH launches together with the static-index store below
           float u[8];
 #pragma unroll
           for (int jj = 0; jj < 8; ++jj) u[jj] = 0.f;
+          const uint32_t wa0 = smem_u32(s_wa + c_off * 8);
 #pragma unroll
           for (int c = 0; c < CW; ++c) {
-            const float4 w0 = *reinterpret_cast<const float4*>(s_wa + (c_off + c) * 8);
-            const float4 w1 = *reinterpret_cast<const float4*>(s_wa + (c_off + c) * 8 + 4);
+            const float4 w0 = lds128(wa0 + c * 32), w1 = lds128(wa0 + c * 32 + 16);
             u[0] = fmaf(acc[c], w0.x, u[0]);
             u[1] = fmaf(acc[c], w0.y, u[1]);
             u[2] = fmaf(acc[c], w0.z, u[2]);
@@ -604,9 +612,12 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUt
           asm volatile("bar.sync 1, 256;" ::: "memory");
           if (h == 0 && p < g.R) {  // a = tanh(u0 + ba); da_k = (1 - a^2) u_k
             float* dst = g.act + ((int64_t)q * g.R + p) * g.n_ad;
-            for (int jj = 0; jj < g.n_ad; ++jj) {
-              const float a = s_a[lane * 8 + jj];
-              dst[jj] = q == 0 ? a : (1.f - a * a) * u[jj];
+#pragma unroll
+            for (int jj = 0; jj < 8; ++jj) {  // static indices: u stays in registers
+              if (jj < g.n_ad) {
+                const float a = s_a[lane * 8 + jj];
+                dst[jj] = q == 0 ? a : (1.f - a * a) * u[jj];
+              }
             }
           }
         }
@@ -809,6 +820,7 @@ gemm3_pair_kernel(const __grid_constant__ CUtensorMap mA, const __grid_constant_
           split_tf32(v[c].z, hi[4 * c + 2], lo[4 * c + 2]);
           split_tf32(v[c].w, hi[4 * c + 3], lo[4 * c + 3]);
         }
+        fence_proxy_async_smem();  // generic reads of the raw stage before its TMA refill
         __syncwarp();
         if (lane == 0) mbar_arrive(raw_empty + r);
         const uint32_t a = tmem + lane_base + Cfg::kACol + o * 2 * kBK;

@@ -364,3 +364,22 @@ def test_torch_ops_boundary_default_7q_4l(dtype):
                           (tok, scale, a, da, qp, True),
                           test_utils=("test_schema", "test_faketensor",
                                       "test_autograd_registration"))
+
+
+def test_transfer_forward_repeatable_under_load():
+    """The transfer-path forward (tensor-core map + fused readout, and the
+    value-only map + readout pass) is bitwise repeatable over many launches."""
+    from paper_2506_23246_b200.ansatz import build_circuit, pqc_forward_raw
+    rng = np.random.default_rng(11)
+    R, n = 1 << 16, 7
+    c = build_circuit("strongly", n, 4)
+    a = cuda(rng.uniform(-0.95, 0.95, (R, n)), torch.float32)
+    da = cuda(rng.normal(size=(3, R, n)), torch.float32)
+    qp = cuda(rng.uniform(0, 2 * np.pi, c.param_count), torch.float32)
+    for tan in (da, None):
+        z0, dz0 = pqc_forward_raw(c, "acos", a, tan, qp)
+        for _ in range(60):
+            z, dz = pqc_forward_raw(c, "acos", a, tan, qp)
+            assert torch.equal(z, z0)
+            if tan is not None:
+                assert torch.equal(dz, dz0)
