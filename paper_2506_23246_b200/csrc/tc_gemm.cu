@@ -199,7 +199,9 @@ gemm3_kernel(const __grid_constant__ CUtensorMap mA, const __grid_constant__ CUt
     return (jj / nkk) * ngrp_t + (jj % nkk) / kPromote;
   };
   extern __shared__ unsigned char smem_raw[];
-  unsigned char* smem = (unsigned char*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  // 1024-byte aligned by offsetting the shared array itself, so pointers derived
+  // from it keep the shared address space (LDS/STS rather than generic LD/ST)
+  unsigned char* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   unsigned char* raw = smem;                        // [RS][16 KB] fp32 A tiles
   unsigned char* ops = smem + RS * kABytes;         // [OS][A_hi | A_lo]
   unsigned char* bst = ops + OS * Cfg::kOpBytes;    // [BS][B_hi | B_lo]
@@ -676,7 +678,9 @@ gemm3_pair_kernel(const __grid_constant__ CUtensorMap mA, const __grid_constant_
   using Cfg = PairCfg<BN>;
   constexpr int RS = Cfg::RS, OS = Cfg::OS, NB = Cfg::NB, HB = Cfg::HB;
   extern __shared__ unsigned char smem_raw[];
-  unsigned char* smem = (unsigned char*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  // 1024-byte aligned by offsetting the shared array itself, so pointers derived
+  // from it keep the shared address space (LDS/STS rather than generic LD/ST)
+  unsigned char* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   const int nk = (g.K + kBK - 1) / kBK;
   unsigned char* raw = smem;                                  // [RS][16 KB] fp32 A tiles
   unsigned char* bres = raw + RS * kABytes;                   // [hi: nk slabs][lo: nk slabs]
@@ -941,7 +945,9 @@ wgrad_kernel(const __grid_constant__ CUtensorMap mX, const __grid_constant__ CUt
              const WgradArgs g) {
   constexpr int RS = kWRaw, OS = kWOps, NB = kWNB, P = kWPromote;
   extern __shared__ unsigned char smem_raw[];
-  unsigned char* smem = (unsigned char*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  // 1024-byte aligned by offsetting the shared array itself, so pointers derived
+  // from it keep the shared address space (LDS/STS rather than generic LD/ST)
+  unsigned char* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   unsigned char* raw = smem;
   unsigned char* ops = smem + RS * kWRawBytes;
   uint64_t* raw_full = (uint64_t*)(ops + OS * kWOpBytes);
