@@ -258,3 +258,15 @@ def test_model_forward_runs_our_kernels_only():
     assert not lib, f"library GEMM kernels in Model.forward: {lib}"
     ours = [k for k in names if re.search(r"gemm3_kernel|pqc|tr_|features|head", k)]
     assert any("gemm3_kernel" in k for k in ours), names
+
+
+def test_bench_steps_bitwise_repeatable():
+    """Two bench trainers from the same initial state stay bit-identical over 15
+    steps (graph replays included): no data race anywhere in the step
+    (scripts/race_step.py runs the longer version)."""
+    _, a = bench_trainer(torch.float32, (64, 64, 16))
+    _, b = bench_trainer(torch.float32, (64, 64, 16))
+    for _ in range(15):
+        ra, rb = a.step(), b.step()
+        assert ra.total == rb.total
+        assert torch.equal(a.flat, b.flat)
