@@ -416,20 +416,23 @@ __global__ void colsum_partial(int64_t R, int N, int64_t rows_per, const T* __re
   }
 }
 
-// out[j] = sum_b partial[b][j]: 32 columns x 8 interleaved block groups per CTA,
-// group sums combined in fixed order (deterministic)
+// out[j] = sum_b partial[b][j]: a CTA owns kCsCols columns and splits the partial rows
+// into blockDim / kCsCols interleaved groups (group g sums rows g, g + G, ...); the
+// group sums are combined in fixed order (deterministic).  8 columns x 128 groups:
+// ~5 rows per thread, all loads in flight at once, and N / 8 CTAs (with 32 columns x
+// 32 groups the 592-row partials took ~8.7 us per launch, a chain of dependent loads
+// on N / 32 CTAs)
+constexpr int kCsCols = 8;
 template <typename T>
 __global__ void __launch_bounds__(1024) colsum_reduce(int nb, int N, const double* __restrict__ partial,
                                                       T* __restrict__ out, int64_t ld = 0) {
-  // block = 32 columns x (blockDim / 32) row groups; group g sums rows g, g + G, ...,
-  // then the groups are added in order (deterministic); partial rows ld apart (0: N)
-  __shared__ double red[32][33];
-  const int c = threadIdx.x & 31, grp = threadIdx.x >> 5, G = blockDim.x >> 5;
-  const int j = blockIdx.x * 32 + c;
-  const int64_t rs = ld ? ld : N;
+  __shared__ double red[1024 / kCsCols][kCsCols + 1];
+  const int c = threadIdx.x % kCsCols, grp = threadIdx.x / kCsCols, G = blockDim.x / kCsCols;
+  const int j = blockIdx.x * kCsCols + c;
+  const int64_t rs = ld ? ld : N;  // partial rows ld apart (0: N)
   double acc = 0.0;
   if (j < N) {
-#pragma unroll 4
+#pragma unroll 8
     for (int b = grp; b < nb; b += G) acc += __ldg(partial + (int64_t)b * rs + j);
   }
   red[grp][c] = acc;
@@ -440,6 +443,7 @@ __global__ void __launch_bounds__(1024) colsum_reduce(int nb, int N, const doubl
     out[j] = T(v);
   }
 }
+constexpr int colsum_grid(int N) { return (N + kCsCols - 1) / kCsCols; }
 
 // dL/dtau_raw through at = 2 pi t / tau and the t-tangent features (one warp per point;
 // the per-point trig of a block's kFeatBPB points is computed once into shared memory)
@@ -850,7 +854,7 @@ static int tanh_bwd_and_bias(int64_t R, int N, const T* GY, const T* Y, T* GU, d
     tanh_bwd_bias<T><<<nb, threads, threads * sizeof(double), st>>>(R, N, rows_per, GY, Y, GU,
                                                                     part);
   }
-  colsum_reduce<T><<<(N + 31) / 32, 1024, 0, st>>>(nb, N, part, out);
+  colsum_reduce<T><<<colsum_grid(N), 1024, 0, st>>>(nb, N, part, out);
   QPINN_CUDA_CHECK(cudaGetLastError());
   return QPINN_OK;
 }
@@ -860,7 +864,7 @@ static int bias_grad(int64_t R, int N, const T* GU0, double* part, T* out, cudaS
   const int64_t rows_per = (R + kColBlocks - 1) / kColBlocks;
   const int nb = (int)((R + rows_per - 1) / rows_per);
   colsum_partial<T><<<nb, N < 128 ? 32 * ((N + 31) / 32) : 128, 0, st>>>(R, N, rows_per, GU0, part);
-  colsum_reduce<T><<<(N + 31) / 32, 1024, 0, st>>>(nb, N, part, out);
+  colsum_reduce<T><<<colsum_grid(N), 1024, 0, st>>>(nb, N, part, out);
   QPINN_CUDA_CHECK(cudaGetLastError());
   return QPINN_OK;
 }
@@ -987,12 +991,12 @@ static int backward_impl(const qpinn_trunk_desc* d, int64_t R, const T* x, const
     }
     const int ob = d->off_b[d->n_hidden - 1];
     if (d->off_adapter_w == ob + H && d->off_adapter_b == ob + H + H * n) {  // contiguous
-      colsum_reduce<T><<<(W + 31) / 32, 1024, 0, st>>>(nb, W, pa, grad + ob);
+      colsum_reduce<T><<<colsum_grid(W), 1024, 0, st>>>(nb, W, pa, grad + ob);
     } else {
-      colsum_reduce<T><<<(H + 31) / 32, 1024, 0, st>>>(nb, H, pa, grad + ob, W);
-      colsum_reduce<T><<<(H * n + 31) / 32, 1024, 0, st>>>(nb, H * n, pa + H,
+      colsum_reduce<T><<<colsum_grid(H), 1024, 0, st>>>(nb, H, pa, grad + ob, W);
+      colsum_reduce<T><<<colsum_grid(H * n), 1024, 0, st>>>(nb, H * n, pa + H,
                                                           grad + d->off_adapter_w, W);
-      colsum_reduce<T><<<(n + 31) / 32, 1024, 0, st>>>(nb, n, pa + H + H * n,
+      colsum_reduce<T><<<colsum_grid(n), 1024, 0, st>>>(nb, n, pa + H + H * n,
                                                       grad + d->off_adapter_b, W);
     }
     QPINN_CUDA_CHECK(cudaGetLastError());
