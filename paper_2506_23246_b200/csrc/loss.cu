@@ -55,7 +55,10 @@ __device__ __forceinline__ void point_loss(const LossDev& L, const double* __res
 #pragma unroll
   for (int mm = 0; mm < 5; ++mm) {
     if (mm != m) continue;
-    acc[4 * mm + k1] += (double)(res1 * res1);
+    // static indices only (a runtime one would put acc in local memory)
+    const double r1 = (double)(res1 * res1);
+    if (k1) acc[4 * mm + 1] += r1;
+    else acc[4 * mm] += r1;
     acc[4 * mm + 2] += (double)(res2 * res2);
     acc[4 * mm + 3] += (double)(res3 * res3);
   }
