@@ -250,13 +250,16 @@ class NativeEngine:
     def sweep(self, flat: torch.Tensor, grad: Optional[torch.Tensor], weights_dev,
               sums_out: torch.Tensor, tape: bool = True) -> None:
         """Forward (+ full gradient into ``grad`` when tape) over every chunk;
-        raw loss sums accumulate into ``sums_out`` (float64 [23])."""
+        raw loss sums accumulate into ``sums_out`` (float64 [23]; with one chunk they
+        overwrite it)."""
         lib = N.lib()
         st = N.stream_ptr()
         fp = flat.data_ptr()
         dc, n = self.dcode, self.n
         es = flat.element_size()
         wptr = N.ptr(weights_dev)
+        # one chunk: the loss reduction writes (not adds) the sums straight into sums_out
+        direct = len(self.chunks) == 1 and sums_out.is_contiguous()
         for i, (ch, b) in enumerate(zip(self.chunks, self.bufs)):
             R = b.R
             g = grad if (self.grad_chunk is None or grad is None) else self.grad_chunk
@@ -282,7 +285,8 @@ class NativeEngine:
                     fp + self.off_out_b * es, wptr, b.gz.data_ptr(),
                     (gp + self.off_out_w * es) if g is not None else scratch_w.data_ptr(),
                     (gp + self.off_out_b * es) if g is not None else scratch_w.data_ptr() + 64 * es,
-                    b.sums.data_ptr(), self.loss_ws.data_ptr(), self.loss_ws.numel(), st),
+                    (sums_out if direct else b.sums).data_ptr(), self.loss_ws.data_ptr(),
+                    self.loss_ws.numel(), st),
                     "qpinn_loss_head_forward_backward")
             if tape:
                 gz0 = b.gz.data_ptr()
@@ -304,7 +308,8 @@ class NativeEngine:
                         grad.copy_(g)
                     else:
                         grad.add_(g)
-            sums_out += b.sums
+            if not direct:
+                sums_out += b.sums
             N.count_launches(self._launches(tape))
 
     def _launches(self, tape: bool) -> int:

@@ -419,7 +419,9 @@ class Trainer:
 
     def _local_sweep(self):
         """The sweep (forward + backward) over this rank's chunks."""
-        self.sums.zero_()
+        eng = self.evaluator.engine
+        if eng is None or len(eng.chunks) > 1:  # one native chunk overwrites the sums
+            self.sums.zero_()
         return self._sweep(self.grad, self.weights, True, self.sums)
 
     def _pqc_workspace(self):
