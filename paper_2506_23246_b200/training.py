@@ -325,6 +325,7 @@ class Trainer:
         self._packed = None
         self.log_grad = log_grad
         self._host = torch.zeros(20, dtype=torch.float64, pin_memory=True)
+        self._host_flag = torch.zeros(1, dtype=torch.int32, pin_memory=True)  # same dtype: a plain D2H
         if config.adaptive_weighting:
             # untaped initial pass (training.py:336-339)
             bins = self._evaluate_untaped()
@@ -393,7 +394,7 @@ class Trainer:
         return sum(v.numel() * v.element_size() for v in self._host_inputs)
 
     def readback_bytes(self) -> int:
-        return 10 * 8 + 8 + 3 * 8 + (32 if self.log_grad else 0)  # loss record, flag, domain
+        return 10 * 8 + 4 + 3 * 8 + (32 if self.log_grad else 0)  # loss record, flag, domain
 
     def _evaluate_untaped(self):
         sums = torch.zeros(N.LOSS_NSUMS, dtype=torch.float64, device=self.device)
@@ -493,7 +494,7 @@ class Trainer:
                   sync=False, veto=self.dom[0:1] if self.model.circuit is not None else None)
         host = self._host
         host[:10].copy_(self.bd, non_blocking=True)
-        host[10:11].copy_(self.flag, non_blocking=True)
+        self._host_flag.copy_(self.flag, non_blocking=True)
         if self.log_grad:
             g = grad.double()
             host[11] = 0.0
@@ -508,7 +509,7 @@ class Trainer:
         v = host.numpy()
         # the forward's DomainError comes first, as in the reference (Adam was vetoed)
         raise_domain(v[15], v[16], v[17])
-        f = int(v[10])
+        f = int(self._host_flag[0])
         if f:
             raise RunAborted(("non-finite loss" if f & 2 else "non-finite gradient")
                              + f" at epoch {epoch}; last good parameters preserved")
