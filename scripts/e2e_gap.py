@@ -28,7 +28,8 @@ def timed(k):
     return e0.elapsed_time(e1) / k, (time.perf_counter() - t0) * 1e3 / k
 
 
-for mode in ("device", "host", "device", "host"):
+order = sys.argv[1].split(",") if len(sys.argv) > 1 else ["device", "host", "device", "host"]
+for mode in order:
     tr.set_host_inputs(mode == "host")
     for _ in range(3):
         tr.step()
