@@ -383,3 +383,27 @@ def test_transfer_forward_repeatable_under_load():
             assert torch.equal(z, z0)
             if tan is not None:
                 assert torch.equal(dz, dz0)
+
+
+@pytest.mark.parametrize("n", [4, 7])
+def test_parameter_shift_matches_adjoint_f64(n):
+    """The reference suite's shift-rule check (test_qsim.py:139-166) on our kernels:
+    d(sum z)/d(theta) from two shifted K1 launches per slot equals K2's adjoint
+    gradient to 1e-10 in fp64 (strongly: every slot in a single-axis rotation)."""
+    from paper_2506_23246_b200.ansatz import build_circuit, pqc_backward_raw, pqc_forward_raw
+    rng = np.random.default_rng(21)
+    L, R = 2, 16
+    c = build_circuit("strongly", n, L)
+    a = cuda(rng.uniform(-0.9, 0.9, (R, n)), torch.float64)
+    da = cuda(np.zeros((3, R, n)), torch.float64)
+    qp0 = rng.uniform(0, 2 * np.pi, c.param_count)
+    gz = cuda(np.ones((R, n)), torch.float64)
+    _, _, gq = pqc_backward_raw(c, "acos", a, da, cuda(qp0, torch.float64), gz,
+                                cuda(np.zeros((3, R, n)), torch.float64))
+
+    def f(q):
+        return pqc_forward_raw(c, "acos", a, da, cuda(q, torch.float64))[0].sum().item()
+
+    shift = np.array([(f(qp0 + np.pi / 2 * e) - f(qp0 - np.pi / 2 * e)) / 2.0
+                      for e in np.eye(qp0.size)])
+    assert np.max(np.abs(shift - gq.cpu().numpy())) <= 1e-10
