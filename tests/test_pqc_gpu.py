@@ -407,3 +407,23 @@ def test_parameter_shift_matches_adjoint_f64(n):
     shift = np.array([(f(qp0 + np.pi / 2 * e) - f(qp0 - np.pi / 2 * e)) / 2.0
                       for e in np.eye(qp0.size)])
     assert np.max(np.abs(shift - gq.cpu().numpy())) <= 1e-10
+
+
+@pytest.mark.parametrize("kind,n", [("cross_mesh", 5), ("strongly", 7), ("basic", 10)])
+def test_tangents_match_central_differences_f64(kind, n):
+    """K1's forward-mode tangents against central differences of its own values
+    (test_autodiff.py:129-150 on our kernels), fp64."""
+    from paper_2506_23246_b200.ansatz import build_circuit, pqc_forward_raw
+    rng = np.random.default_rng(22)
+    L, R = 3, 12
+    c = build_circuit(kind, n, L)
+    a = rng.uniform(-0.8, 0.8, (R, n))
+    da = rng.normal(size=(3, R, n))
+    qp = cuda(rng.uniform(0, 2 * np.pi, c.param_count), torch.float64)
+    _, dz = pqc_forward_raw(c, "asin", cuda(a, torch.float64), cuda(da, torch.float64), qp)
+    h = 1e-6
+    for k in range(3):
+        zp = pqc_forward_raw(c, "asin", cuda(a + h * da[k], torch.float64), None, qp)[0]
+        zm = pqc_forward_raw(c, "asin", cuda(a - h * da[k], torch.float64), None, qp)[0]
+        fd = ((zp - zm) / (2 * h)).cpu().numpy()
+        assert np.max(np.abs(fd - dz[k].cpu().numpy())) <= 1e-7
